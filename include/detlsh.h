@@ -1,0 +1,183 @@
+/*
+ * detlsh.h -- C ABI of the B200-native DET-LSH hot path (arxiv 2603.24920).
+ *
+ * The library builds L DE-Trees over n points (Alg. 1 dynamic encoding + Alg. 2
+ * index creation) and answers batched c^2-k-ANN queries
+ * (Alg. 5) entirely in sm_100a CUDA kernels.  Citations "P:n" are
+ * lines of the paper's LaTeX; "AMB-n" are the readings listed in DESIGN.md.
+ *
+ * Conventions for every entry point
+ *  - Pointers may be host or device memory (detected with cudaPointerGetAttributes);
+ *    host buffers are copied in/out inside the call.  Arrays are row-major, dense.
+ *  - The caller owns every input and output buffer.  An index owns its device
+ *    memory (including its own copy of the data unless opts.borrow_data is set).
+ *  - Functions return a detlsh_status and never abort.  On error no output is
+ *    written (no partial results) and detlsh_last_error() describes the failure.
+ *  - All work runs on opts->stream (a cudaStream_t cast to uint64; 0 = legacy
+ *    default stream).  Calls return after the stream work has completed unless a
+ *    function says otherwise.
+ *  - An index is read-only after build: concurrent queries on different streams
+ *    are allowed.
+ */
+#ifndef DETLSH_H
+#define DETLSH_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct detlsh_index detlsh_index; /* opaque; owns device memory */
+
+typedef enum {
+    DETLSH_OK = 0,
+    DETLSH_EINVAL = 1,    /* bad argument (see each function) */
+    DETLSH_ENOMEM = 2,    /* device or host allocation failed */
+    DETLSH_ECUDA = 3,     /* a CUDA runtime/kernel error; also "no CUDA device" */
+    DETLSH_ENCCL = 4,     /* reserved for collective glue */
+    DETLSH_EINTERNAL = 5  /* an internal invariant failed */
+} detlsh_status;
+
+/* Range-query predicate inside partially covered leaves (AMB-12). */
+enum { DETLSH_MODE_CELL = 0,     /* point's own region lower bound <= eps r (hot path) */
+       DETLSH_MODE_RELAXED = 1   /* Sec. 6.2.2(1): whole leaf when leaf LB <= eps r */ };
+
+typedef struct {
+    int32_t  max_size;     /* leaf capacity of Alg. 2 (AMB-8), default 128 */
+    double   sample_frac;  /* n_s = min(n, max(ceil(f n), 32 N_r)) (AMB-3), default 0.01 */
+    int32_t  mode;         /* DETLSH_MODE_*, default CELL */
+    int32_t  query_batch;  /* queries per device batch, 0 = sized from free memory */
+    uint64_t stream;       /* cudaStream_t, 0 = legacy default stream */
+    int32_t  borrow_data;  /* 1: keep the caller's device pointer (d % 8 == 0) instead of copying */
+    int32_t  proj_impl;    /* projection kernel: 0 = tcgen05 tensor cores, 1 = SIMT fp32 */
+    int64_t  mem_budget;   /* bytes of device scratch for query batches, 0 = auto */
+} detlsh_opts;
+
+/* Per-query statistics (Alg. 5 bookkeeping). */
+typedef struct {
+    int32_t rounds;      /* radius rounds started (r = r_min c^(rounds-1) at the end) */
+    int32_t trees_last;  /* trees processed in the last round */
+    int32_t reason;      /* 0 = budget |S| >= beta n + k (line 7), 1 = radius (line 9), 2 = 64-round cap */
+    int32_t pad;
+    int64_t n_cand;      /* |S| at termination */
+    double  r_final;     /* r of the last round */
+} detlsh_query_stats;
+
+void detlsh_default_opts(detlsh_opts* opts);
+
+/*
+ * Build an index over data[n][d] (fp32).  Steps:
+ *  hash family A[L*K][d], a ~ N(0,1) from `seed` (Eq. 1; AMB-1);
+ *  sample n_s ids (AMB-3/4); project; breakpoints
+ *  B[L*K][N_r+1] from the sorted sample (AMB-5); encode every
+ *  coordinate to an 8-bit symbol (Alg. 1; AMB-6/7); per tree sort by the
+ *  first-layer key and split segments into leaves (Alg. 2 + SplitNode).
+ * Errors (EINVAL): data NULL; n < 1 or n >= 2^31; d < 1; L < 1; K < 1 or K > 32;
+ *  N_r not a power of two in [2,256]; max_size < 1; sample_frac not in (0,1];
+ *  any non-finite value in data.
+ */
+detlsh_status detlsh_build(const float* data, int64_t n, int32_t d, int32_t L, int32_t K,
+                           int32_t N_r, uint64_t seed, detlsh_index** out);
+
+/*
+ * As detlsh_build, for one shard of a larger point-sharded dataset:
+ *  id_offset   global id of data row 0 (query outputs report global ids);
+ *  n_global    rows of the whole dataset (the sample rule and candidate budget of
+ *              each shard use this shard's n; n_global only labels ids);
+ *  breakpoints nullable [L*K][N_r+1] fp32 (host or device): use these instead of
+ *              this shard's own sample (C1: every shard gets the same breakpoints).
+ */
+detlsh_status detlsh_build_ex(const float* data, int64_t n, int32_t d, int32_t L, int32_t K,
+                              int32_t N_r, uint64_t seed, const detlsh_opts* opts,
+                              int64_t id_offset, int64_t n_global, const float* breakpoints,
+                              detlsh_index** out);
+
+/*
+ * c^2-k-ANN for queries[nq][d] (Alg. 5): rounds r = r_min c^m; each round
+ * runs the L range queries at radius eps*r (eps from Eq. 2 for (K, L); AMB-23),
+ * unions and de-duplicates candidates in a per-query bitmap, stops after a tree once
+ * |S| >= ceil(beta n) + k (AMB-17), else after the round once the k-th smallest exact
+ * distance <= c r; at most 64 rounds (AMB-20).  Outputs out_ids[nq][k] (global ids,
+ * int64) and out_dists[nq][k] (Euclidean, fp32), ascending by (dist, id) (AMB-21);
+ * unfilled slots (fewer than k candidates at the cap) are (-1, +inf).
+ * Errors (EINVAL): idx NULL; nq < 0; k < 1 or k > n or k > 4096; c <= 1; beta <= 0;
+ *  r_min <= 0 or non-finite; NaN/Inf in queries.  nq == 0 is a no-op.
+ */
+detlsh_status detlsh_query(const detlsh_index* idx, const float* queries, int64_t nq, int32_t k,
+                           double c, double r_min, double beta, int64_t* out_ids, float* out_dists);
+
+/* As detlsh_query with options and optional per-query statistics (host or device, [nq]). */
+detlsh_status detlsh_query_ex(const detlsh_index* idx, const float* queries, int64_t nq, int32_t k,
+                              double c, double r_min, double beta, const detlsh_opts* opts,
+                              int64_t* out_ids, float* out_dists, detlsh_query_stats* stats);
+
+void detlsh_free(detlsh_index* idx);
+
+/* Thread-local description of the last failure; valid until the next call on this thread. */
+const char* detlsh_last_error(void);
+
+/* ---------------------------------------------------------------- helpers */
+
+/* eps = sqrt(chi2_{alpha1}(K)), alpha1 = e^{-1/L}; alpha2 = Pr[chi2(K) > eps^2/c^2];
+   beta_theory = 2 - 2 alpha2^L (Lemma 3 / Eq. 2).  Host only.  Any out may be NULL. */
+detlsh_status detlsh_params(int32_t K, int32_t L, double c, double* eps, double* alpha2,
+                            double* beta_theory);
+
+/* n_s = min(n, max(ceil(f n), 32 N_r)) (AMB-3).  Host only. */
+int64_t detlsh_sample_size(int64_t n, int32_t N_r, double sample_frac);
+
+/*
+ * C1 helper for point-sharded builds: projections of this shard's rows that belong to
+ * the global sample (the n_s smallest keyed hashes over [0, n_global), AMB-4).
+ * data = this shard's rows [n][d]; rows are global ids id_offset..id_offset+n-1.
+ * out = device or host [cap][L*K] fp32; *n_out = rows written.  EINVAL if cap is too small.
+ */
+detlsh_status detlsh_sample_projections(const float* data, int64_t n, int32_t d, int32_t L,
+                                        int32_t K, int32_t N_r, uint64_t seed, double sample_frac,
+                                        int64_t id_offset, int64_t n_global, const detlsh_opts* opts,
+                                        float* out, int64_t cap, int64_t* n_out);
+
+/* Breakpoints [L*K][N_r+1] from m sample projections [m][L*K] (AMB-5),
+   by device radix sort.  Pointers host or device. */
+detlsh_status detlsh_breakpoints_from_samples(const float* samples, int64_t m, int32_t LK,
+                                              int32_t N_r, const detlsh_opts* opts, float* out);
+
+/*
+ * C2 merge: G per-shard top-k lists ids[G][nq][k], dists[G][nq][k] ->
+ * the k best by (dist, id); ids < 0 are empty slots.  Host memory only (plain C++).
+ */
+detlsh_status detlsh_merge_topk(const int64_t* ids, const float* dists, int32_t G, int64_t nq,
+                                int32_t k, int64_t* out_ids, float* out_dists);
+
+/* Projection P = X A^T of m rows with the index's hash family, [m][L*K] fp32. */
+detlsh_status detlsh_project(const detlsh_index* idx, const float* X, int64_t m, float* out);
+/* As detlsh_project with an explicit kernel: proj_impl 0 = tcgen05, 1 = SIMT fp32. */
+detlsh_status detlsh_project_ex(const detlsh_index* idx, const float* X, int64_t m, int32_t proj_impl,
+                                float* out);
+
+/*
+ * Test/debug export of index contents.  what:
+ *  0 A [L*K][d] f32          1 breakpoints [L*K][N_r+1] f32    2 codes [n][L*K] u8 (data order)
+ *  3 sample ids [n_s] i64    4 tree perm [n] i64 (leaf order)   5 tree leaf_off [nl+1] i64
+ *  6 tree leaf lo [nl][K] u8 7 tree leaf hi [nl][K] u8         8 tree leaf bits [nl][K] u8
+ *  9 scalars i64[4] = {n, n_s, nl(tree), d}
+ * `tree` selects the tree for 4-9.  dst is host memory of `bytes`; *needed gets the size.
+ * EINVAL if bytes < needed (nothing written).
+ */
+detlsh_status detlsh_debug_export(const detlsh_index* idx, int32_t what, int32_t tree, void* dst,
+                                  size_t bytes, size_t* needed);
+
+/* Test hook: build only the L trees from given codes[n][L*K] (host or device), so the GPU
+   tree builder can be cross-fed the oracle's codes (SURVEY §8(c) acceptance 3). */
+detlsh_status detlsh_build_from_codes(const uint8_t* codes, int64_t n, int32_t L, int32_t K,
+                                      int32_t N_r, const detlsh_opts* opts, detlsh_index** out);
+
+/* Number of kernels this library has launched in this process (evidence counter). */
+int64_t detlsh_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DETLSH_H */

@@ -1,0 +1,800 @@
+// build.cu -- index construction on sm_100a.
+//
+//  B0 hash family A (Eq. 1; AMB-1)      k_hash_family
+//  B1 sample: n_s smallest keyed hashes (AMB-3/4)  k_sel_hist / k_sel_pick / k_sel_collect
+//  B2 projection P = X A^T                  project_rows (tcgen05 or SIMT, project*.cu)
+//  B3 breakpoints from the sorted sample (AMB-5)  radix sort + k_bp_gather
+//  B4 encode, Alg. 1 lines 3-8 (AMB-6/7) k_encode
+//  B5 first layer, Alg. 2 line 2    k_first_key + batched radix sort
+//  B6 splits, Alg. 2 lines 7-10 + SplitNode, bulk rule:
+//     a node with more than max_size points splits on the dimension whose next bit most
+//     evenly divides its first max_size points (ascending id); children are the stable
+//     partition.  Level-synchronous over all L trees at once.
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "index.cuh"
+
+namespace detlsh {
+
+namespace {
+
+// ------------------------------------------------------------------ B0
+__global__ void k_hash_family(uint64_t seed, int LK, int d, int ld, float* __restrict__ A) {
+    const int64_t total = (int64_t)LK * ld;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int r = (int)(i / ld), t = (int)(i % ld);
+        float out = 0.f;
+        if (t < d) {
+            const uint64_t e = (uint64_t)r * d + t;             // entry index of A[r][t]
+            double u1 = (double)(keyed(seed, 2 * e) >> 11) * (1.0 / 9007199254740992.0);
+            double u2 = (double)(keyed(seed, 2 * e + 1) >> 11) * (1.0 / 9007199254740992.0);
+            double g = sqrt(-2.0 * log(1.0 - u1)) * cos(6.283185307179586476925286766559 * u2);
+            uint32_t u = __float_as_uint(__double2float_rn(g));
+            u += 0xFFFu + ((u >> 13) & 1u);                     // round to TF32 (nearest even)
+            u &= ~0x1FFFu;
+            out = __uint_as_float(u);
+        }
+        A[i] = out;                                             // padded row stride ld, zeros beyond d
+    }
+}
+
+// ------------------------------------------------------------------ B1 radix select over keyed hashes
+struct SelState {
+    unsigned long long prefix, mask, remaining, eq_count;
+};
+
+__global__ void k_sel_init(SelState* s, int64_t n_s) {
+    s->prefix = 0; s->mask = 0; s->remaining = (unsigned long long)n_s; s->eq_count = 0;
+}
+
+__global__ void __launch_bounds__(256) k_sel_hist(uint64_t salt, int64_t n_global, int shift,
+                                                  const SelState* __restrict__ st,
+                                                  uint32_t* __restrict__ hist) {
+    __shared__ uint32_t h[256];
+    h[threadIdx.x] = 0;
+    __syncthreads();
+    const uint64_t prefix = st->prefix, mask = st->mask;
+    for (int64_t id = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; id < n_global;
+         id += (int64_t)gridDim.x * blockDim.x) {
+        uint64_t key = keyed(salt, (uint64_t)id);
+        if ((key & mask) == prefix) atomicAdd(&h[(key >> shift) & 255u], 1u);
+    }
+    __syncthreads();
+    if (h[threadIdx.x]) atomicAdd(&hist[threadIdx.x], h[threadIdx.x]);
+}
+
+__global__ void __launch_bounds__(256) k_sel_pick(int shift, SelState* st, uint32_t* hist) {
+    __shared__ unsigned long long s_incl[256];
+    const unsigned long long v = hist[threadIdx.x];
+    s_incl[threadIdx.x] = v;
+    __syncthreads();
+    for (int o = 1; o < 256; o <<= 1) {
+        unsigned long long add = threadIdx.x >= o ? s_incl[threadIdx.x - o] : 0ull;
+        __syncthreads();
+        s_incl[threadIdx.x] += add;
+        __syncthreads();
+    }
+    const unsigned long long incl = s_incl[threadIdx.x], excl = incl - v;
+    const unsigned long long rem = st->remaining;
+    __syncthreads();
+    if (v > 0 && excl < rem && rem <= incl) {
+        st->prefix |= (unsigned long long)threadIdx.x << shift;
+        st->mask |= 0xFFull << shift;
+        st->remaining = rem - excl;
+        st->eq_count = v;
+    }
+    hist[threadIdx.x] = 0;
+}
+
+__global__ void __launch_bounds__(256) k_sel_collect(uint64_t salt, int64_t id_lo, int64_t n_range,
+                                                     const SelState* __restrict__ st,
+                                                     uint32_t* __restrict__ out,
+                                                     unsigned long long* __restrict__ counter) {
+    const uint64_t T = st->prefix;
+    const bool take_eq = st->eq_count == st->remaining;         // all ties needed (the usual case)
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_range;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        uint64_t key = keyed(salt, (uint64_t)(id_lo + i));
+        if (key < T || (take_eq && key == T)) out[atomicAdd(counter, 1ull)] = (uint32_t)i;
+    }
+}
+
+// Ties at the threshold beyond what is needed: take the lowest ids (AMB-4), serially.
+// Only reachable when two 64-bit keys collide exactly at the n_s-th position.
+__global__ void k_sel_ties(uint64_t salt, int64_t id_lo, int64_t n_range, int64_t n_global,
+                           const SelState* __restrict__ st, uint32_t* __restrict__ out,
+                           unsigned long long* __restrict__ counter) {
+    if (st->eq_count == st->remaining) return;
+    const uint64_t T = st->prefix;
+    unsigned long long need = st->remaining;
+    for (int64_t id = 0; id < n_global && need; ++id) {
+        if (keyed(salt, (uint64_t)id) == T) {
+            --need;
+            if (id >= id_lo && id < id_lo + n_range) out[atomicAdd(counter, 1ull)] = (uint32_t)(id - id_lo);
+        }
+    }
+}
+
+__global__ void k_gather_rows(const float* __restrict__ X, int64_t ld, const uint32_t* __restrict__ ids,
+                              int64_t m, float* __restrict__ out) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t r = warp; r < m; r += nwarps) {
+        const float4* src = reinterpret_cast<const float4*>(X + (int64_t)ids[r] * ld);
+        float4* dst = reinterpret_cast<float4*>(out + r * ld);
+        for (int64_t f = lane; f < ld / 4; f += 32) dst[f] = src[f];
+    }
+}
+
+// ------------------------------------------------------------------ B3
+__global__ void k_transpose_keys(const float* __restrict__ Ps, int64_t m, int LK, uint32_t* __restrict__ keys) {
+    const int64_t total = m * LK;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t s = i / LK;
+        const int r = (int)(i % LK);
+        keys[(int64_t)r * m + s] = f2key(Ps[i]);
+    }
+}
+
+// B(1) = C^(1), B(z) = C^(floor(m/N_r)(z-1)) (1-based, z=2..N_r), B(N_r+1) = C^(m)  (AMB-5)
+__global__ void k_bp_gather(const uint32_t* __restrict__ sorted, int64_t m, int LK, int N_r, float* __restrict__ B) {
+    const int64_t total = (int64_t)LK * (N_r + 1);
+    const int64_t stride = m / N_r > 0 ? m / N_r : 1;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int r = (int)(i / (N_r + 1)), t = (int)(i % (N_r + 1));
+        int64_t pos;
+        if (t == 0) pos = 0;
+        else if (t == N_r) pos = m - 1;
+        else pos = min((int64_t)t * stride, m) - 1;
+        B[i] = key2f(sorted[(int64_t)r * m + pos]);
+    }
+}
+
+// ------------------------------------------------------------------ B4 encode (Alg. 1)
+// code = #{t in 1..N_r-1 : b_t < x}: branch-free lower_bound over the interior breakpoints
+// with a +inf sentinel (AMB-6: ties go to the lower region; AMB-7: clamp to 0 / N_r-1).
+__global__ void __launch_bounds__(256) k_encode(const float* __restrict__ P, int64_t m, int LK, int N_r,
+                                                const float* __restrict__ B, uint8_t* __restrict__ EP) {
+    extern __shared__ float tab[];  // [LK][N_r]
+    for (int i = threadIdx.x; i < LK * N_r; i += blockDim.x) {
+        const int r = i / N_r, t = i % N_r;
+        tab[i] = (t < N_r - 1) ? B[(int64_t)r * (N_r + 1) + t + 1] : __int_as_float(0x7f800000);
+    }
+    __syncthreads();
+    if (LK & 3) {  // generic path
+        for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m * LK;
+             i += (int64_t)gridDim.x * blockDim.x) {
+            const float* t = tab + (int)(i % LK) * N_r;
+            const float x = P[i];
+            int pos = 0;
+            for (int s = N_r >> 1; s > 0; s >>= 1) pos += (t[pos + s - 1] < x) ? s : 0;
+            EP[i] = (uint8_t)pos;
+        }
+        return;
+    }
+    const int64_t total4 = m * LK / 4;
+    const float4* P4 = reinterpret_cast<const float4*>(P);
+    uchar4* E4 = reinterpret_cast<uchar4*>(EP);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total4;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const float4 v = P4[i];
+        const int r0 = (int)((i * 4) % LK);
+        const float xs[4] = {v.x, v.y, v.z, v.w};
+        uint8_t c[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const float* t = tab + (r0 + q) * N_r;
+            int pos = 0;
+            for (int s = N_r >> 1; s > 0; s >>= 1) pos += (t[pos + s - 1] < xs[q]) ? s : 0;
+            c[q] = (uint8_t)pos;
+        }
+        E4[i] = make_uchar4(c[0], c[1], c[2], c[3]);
+    }
+}
+
+// ------------------------------------------------------------------ B5/B6 trees
+struct __align__(16) Node {
+    uint4 bits;       // 4-bit symbol-prefix length per dimension (32 dims)
+    uint32_t start;   // global position in the [L*n] perm array (tree = start / n)
+    uint32_t len;
+    uint32_t pad0, pad1;
+};
+
+__device__ inline int nib(const uint4& b, int j) {
+    const uint32_t w = j < 8 ? b.x : j < 16 ? b.y : j < 24 ? b.z : b.w;
+    return (int)((w >> ((j & 7) * 4)) & 15u);
+}
+__device__ inline void nib_inc(uint4& b, int j) {
+    const uint32_t add = 1u << ((j & 7) * 4);
+    if (j < 8) b.x += add; else if (j < 16) b.y += add; else if (j < 24) b.z += add; else b.w += add;
+}
+__device__ inline bool splittable(const uint4& b, int K, int nb) {
+    for (int j = 0; j < K; ++j)
+        if (nib(b, j) < nb) return true;
+    return false;
+}
+
+// First-layer key of point id in tree t: MSB of each of the K symbols, dim 0 most significant (AMB-11).
+__global__ void k_first_key(const uint8_t* __restrict__ EP, int64_t n, int L, int K, int nb,
+                            uint32_t* __restrict__ keys, uint32_t* __restrict__ vals) {
+    const int LK = L * K;
+    const int64_t total = n * L;
+    for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total;
+         g += (int64_t)gridDim.x * blockDim.x) {
+        const int t = (int)(g / n);
+        const int64_t id = g - (int64_t)t * n;
+        const uint8_t* c = EP + id * LK + t * K;
+        uint32_t key = 0;
+        for (int j = 0; j < K; ++j) key = (key << 1) | ((c[j] >> (nb - 1)) & 1u);
+        keys[g] = key;
+        vals[g] = (uint32_t)id;
+    }
+}
+
+__global__ void k_seg_flags(const uint32_t* __restrict__ keys, int64_t n, int64_t total, uint32_t* __restrict__ flags) {
+    for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total;
+         g += (int64_t)gridDim.x * blockDim.x)
+        flags[g] = (g % n == 0 || keys[g] != keys[g - 1]) ? 1u : 0u;
+}
+
+__global__ void k_seg_write(const uint32_t* __restrict__ flags, const uint32_t* __restrict__ idx, int64_t total,
+                            uint32_t* __restrict__ starts) {
+    for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total;
+         g += (int64_t)gridDim.x * blockDim.x)
+        if (flags[g]) starts[idx[g]] = (uint32_t)g;
+}
+
+// Append with a capacity guard: the count keeps growing past cap so the host can detect
+// overflow and retry with more room.
+__device__ inline void push_node(Node* arr, uint32_t* cnt, uint32_t cap, const Node& nd) {
+    const uint32_t i = atomicAdd(cnt, 1u);
+    if (i < cap) arr[i] = nd;
+}
+
+__global__ void k_init_nodes(const uint32_t* __restrict__ starts, const uint32_t* __restrict__ nseg_p,
+                             int64_t total, int K, int nb, int max_size, Node* __restrict__ active,
+                             uint32_t* __restrict__ n_active, uint32_t cap_active, Node* __restrict__ leaves,
+                             uint32_t* __restrict__ n_leaves, uint32_t cap_leaves) {
+    const uint32_t nseg = *nseg_p;
+    for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < nseg;
+         s += (int64_t)gridDim.x * blockDim.x) {
+        Node nd;
+        uint32_t w[4];
+        for (int q = 0; q < 4; ++q) {
+            uint32_t x = 0;
+            for (int e = 0; e < 8; ++e) x |= (uint32_t)((q * 8 + e) < K ? 1 : nb) << (4 * e);
+            w[q] = x;
+        }
+        nd.bits = make_uint4(w[0], w[1], w[2], w[3]);
+        nd.start = starts[s];
+        nd.len = (uint32_t)((s + 1 < nseg ? (int64_t)starts[s + 1] : total) - nd.start);
+        nd.pad0 = nd.pad1 = 0;
+        if ((int64_t)nd.len <= max_size || !splittable(nd.bits, K, nb)) push_node(leaves, n_leaves, cap_leaves, nd);
+        else push_node(active, n_active, cap_active, nd);
+    }
+}
+
+// SplitNode's dimension (AMB-9): over the node's first max_size points, the dim with bits
+// left whose next bit minimises |n0 - n1|; ties to the lowest dim.  One warp per node.
+__global__ void k_choose_split(const Node* __restrict__ nodes, const uint32_t* __restrict__ n_nodes_p,
+                               const uint32_t* __restrict__ perm, const uint8_t* __restrict__ EP,
+                               int64_t n, int LK, int K, int nb, int max_size, int chunk,
+                               int* __restrict__ split, uint32_t* __restrict__ nch) {
+    const uint32_t n_nodes = *n_nodes_p;
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t a = warp; a < n_nodes; a += nwarps) {
+        const Node nd = nodes[a];
+        const int t = (int)(nd.start / n);
+        int ones[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) ones[j] = 0;
+        for (int e = lane; e < max_size; e += 32) {
+            const uint8_t* c = EP + (int64_t)perm[nd.start + e] * LK + t * K;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+                if (j < K) {
+                    const int b = nib(nd.bits, j);
+                    if (b < nb) ones[j] += (c[j] >> (nb - 1 - b)) & 1;
+                }
+            }
+        }
+        int best = -1, best_imb = 0x7fffffff;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+            int v = ones[j];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            if (j < K && nib(nd.bits, j) < nb) {
+                int imb = abs(max_size - 2 * v);
+                if (imb < best_imb) { best_imb = imb; best = j; }
+            }
+        }
+        if (lane == 0) {
+            split[a] = best;
+            nch[a] = best >= 0 ? (uint32_t)ceil_div(nd.len, chunk) : 0u;
+        }
+    }
+}
+
+__device__ inline int64_t chunk_owner(const uint32_t* __restrict__ choff, int64_t n_nodes, uint32_t c) {
+    int64_t lo = 0, hi = n_nodes - 1;   // last a with choff[a] <= c
+    while (lo < hi) {
+        int64_t mid = (lo + hi + 1) >> 1;
+        if (choff[mid] <= c) lo = mid; else hi = mid - 1;
+    }
+    return lo;
+}
+
+constexpr int PART_THREADS = 256;
+constexpr int PART_IPT = 8;
+constexpr int PART_CHUNK = PART_THREADS * PART_IPT;
+
+__device__ inline int next_bit_of(const uint8_t* __restrict__ EP, uint32_t id, int64_t LK, int off, int shift) {
+    return (EP[(int64_t)id * LK + off] >> shift) & 1;
+}
+
+__global__ void __launch_bounds__(PART_THREADS) k_part_count(const Node* __restrict__ nodes, const int* __restrict__ split,
+                                                             const uint32_t* __restrict__ choff, const uint32_t* __restrict__ n_nodes_p,
+                                                             const uint32_t* __restrict__ total_ch_p,
+                                                             const uint32_t* __restrict__ perm, const uint8_t* __restrict__ EP,
+                                                             int64_t n, int LK, int K, int nb, uint32_t* __restrict__ zc) {
+    __shared__ uint32_t s_cnt;
+    const uint32_t c = blockIdx.x;
+    if (c >= *total_ch_p) return;
+    const int64_t a = chunk_owner(choff, *n_nodes_p, c);
+    const Node nd = nodes[a];
+    const int j = split[a];
+    const int t = (int)(nd.start / n);
+    const int shift = nb - 1 - nib(nd.bits, j);
+    const int64_t base = (int64_t)(c - choff[a]) * PART_CHUNK;
+    if (threadIdx.x == 0) s_cnt = 0;
+    __syncthreads();
+    uint32_t z = 0;
+    for (int q = 0; q < PART_IPT; ++q) {
+        const int64_t e = base + q * PART_THREADS + threadIdx.x;
+        if (e < nd.len) z += 1 - next_bit_of(EP, perm[nd.start + e], LK, t * K + j, shift);
+    }
+    for (int o = 16; o > 0; o >>= 1) z += __shfl_xor_sync(0xffffffffu, z, o);
+    if ((threadIdx.x & 31) == 0) atomicAdd(&s_cnt, z);
+    __syncthreads();
+    if (threadIdx.x == 0) zc[c] = s_cnt;
+}
+
+__global__ void k_part_offsets(const uint32_t* __restrict__ choff, const uint32_t* __restrict__ nch,
+                               const uint32_t* __restrict__ n_nodes_p, uint32_t* __restrict__ zc,
+                               uint32_t* __restrict__ zeros) {
+    const uint32_t n_nodes = *n_nodes_p;
+    for (int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a < n_nodes;
+         a += (int64_t)gridDim.x * blockDim.x) {
+        uint32_t run = 0;
+        for (uint32_t c = choff[a]; c < choff[a] + nch[a]; ++c) {
+            uint32_t v = zc[c];
+            zc[c] = run;
+            run += v;
+        }
+        zeros[a] = run;
+    }
+}
+
+__global__ void __launch_bounds__(PART_THREADS) k_part_scatter(const Node* __restrict__ nodes, const int* __restrict__ split,
+                                                               const uint32_t* __restrict__ choff, const uint32_t* __restrict__ n_nodes_p,
+                                                               const uint32_t* __restrict__ total_ch_p,
+                                                               const uint32_t* __restrict__ zoff, const uint32_t* __restrict__ zeros,
+                                                               const uint32_t* __restrict__ perm, const uint8_t* __restrict__ EP,
+                                                               int64_t n, int LK, int K, int nb, uint32_t* __restrict__ perm_out) {
+    __shared__ uint32_t s_warp[PART_THREADS / 32];
+    const uint32_t c = blockIdx.x;
+    if (c >= *total_ch_p) return;
+    const int64_t a = chunk_owner(choff, *n_nodes_p, c);
+    const Node nd = nodes[a];
+    const int j = split[a];
+    const int t = (int)(nd.start / n);
+    const int shift = nb - 1 - nib(nd.bits, j);
+    const int64_t base = (int64_t)(c - choff[a]) * PART_CHUNK;
+    const uint32_t Z = zeros[a], z0 = zoff[c];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    uint32_t run0 = 0;  // zeros before this round inside the chunk
+    for (int q = 0; q < PART_IPT; ++q) {
+        const int64_t e = base + q * PART_THREADS + threadIdx.x;
+        const bool ok = e < nd.len;
+        uint32_t id = 0;
+        int bit = 1;
+        if (ok) {
+            id = perm[nd.start + e];
+            bit = next_bit_of(EP, id, LK, t * K + j, shift);
+        }
+        const uint32_t is0 = ok && bit == 0;
+        const uint32_t bal = __ballot_sync(0xffffffffu, is0);
+        if (lane == 0) s_warp[w] = __popc(bal);
+        __syncthreads();
+        uint32_t before = run0, tot = 0;
+        for (int ww = 0; ww < PART_THREADS / 32; ++ww) {
+            if (ww < w) before += s_warp[ww];
+            tot += s_warp[ww];
+        }
+        before += __popc(bal & lanemask_lt());
+        if (ok) {
+            const int64_t pos_in_chunk = q * PART_THREADS + threadIdx.x;
+            const uint32_t r0 = before;                                   // zeros before me in chunk
+            const uint32_t r1 = (uint32_t)(pos_in_chunk) - (r0 - 0);       // ones before me in chunk
+            uint32_t dst;
+            if (is0) dst = nd.start + z0 + r0;
+            else dst = nd.start + Z + ((uint32_t)base - z0) + r1;
+            perm_out[dst] = id;
+        }
+        run0 += tot;
+        __syncthreads();
+    }
+}
+
+__global__ void __launch_bounds__(PART_THREADS) k_part_copy(const Node* __restrict__ nodes,
+                                                            const uint32_t* __restrict__ choff,
+                                                            const uint32_t* __restrict__ n_nodes_p,
+                                                            const uint32_t* __restrict__ total_ch_p,
+                                                            const uint32_t* __restrict__ src, uint32_t* __restrict__ dst) {
+    const uint32_t c = blockIdx.x;
+    if (c >= *total_ch_p) return;
+    const int64_t a = chunk_owner(choff, *n_nodes_p, c);
+    const Node nd = nodes[a];
+    const int64_t base = (int64_t)(c - choff[a]) * PART_CHUNK;
+    for (int q = 0; q < PART_IPT; ++q) {
+        const int64_t e = base + q * PART_THREADS + threadIdx.x;
+        if (e < nd.len) dst[nd.start + e] = src[nd.start + e];
+    }
+}
+
+__global__ void k_make_children(const Node* __restrict__ nodes, const uint32_t* __restrict__ n_nodes_p,
+                                const int* __restrict__ split, const uint32_t* __restrict__ zeros,
+                                int K, int nb, int max_size, Node* __restrict__ next,
+                                uint32_t* __restrict__ n_next, uint32_t cap_next, Node* __restrict__ leaves,
+                                uint32_t* __restrict__ n_leaves, uint32_t cap_leaves) {
+    const uint32_t n_nodes = *n_nodes_p;
+    for (int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a < n_nodes;
+         a += (int64_t)gridDim.x * blockDim.x) {
+        const Node nd = nodes[a];
+        const int j = split[a];
+        if (j < 0) {                          // unsplittable: an oversized leaf (AMB-9)
+            push_node(leaves, n_leaves, cap_leaves, nd);
+            continue;
+        }
+        const uint32_t Z = zeros[a];
+        for (int b = 0; b < 2; ++b) {
+            Node ch = nd;
+            nib_inc(ch.bits, j);
+            ch.start = b ? nd.start + Z : nd.start;
+            ch.len = b ? nd.len - Z : Z;
+            if (ch.len == 0) continue;        // empty children are dropped (AMB-11)
+            if ((int64_t)ch.len <= max_size || !splittable(ch.bits, K, nb)) push_node(leaves, n_leaves, cap_leaves, ch);
+            else push_node(next, n_next, cap_next, ch);
+        }
+    }
+}
+
+__global__ void k_leaf_keys(const Node* __restrict__ leaves, const uint32_t* __restrict__ nl_p,
+                            uint32_t* __restrict__ keys, uint32_t* __restrict__ vals) {
+    const uint32_t nl = *nl_p;
+    for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < nl;
+         l += (int64_t)gridDim.x * blockDim.x) {
+        keys[l] = leaves[l].start;
+        vals[l] = (uint32_t)l;
+    }
+}
+
+__global__ void k_leaf_finalize(const Node* __restrict__ leaves, const uint32_t* __restrict__ order, int64_t nl,
+                                const uint32_t* __restrict__ perm, const uint8_t* __restrict__ EP, int64_t n,
+                                int LK, int K, int nb, uint32_t* __restrict__ leaf_off, uint8_t* __restrict__ lo,
+                                uint8_t* __restrict__ hi, uint8_t* __restrict__ bits, int64_t total) {
+    for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < nl;
+         l += (int64_t)gridDim.x * blockDim.x) {
+        const Node nd = leaves[order[l]];
+        leaf_off[l] = nd.start;
+        const int t = (int)(nd.start / n);
+        const uint8_t* c = EP + (int64_t)perm[nd.start] * LK + t * K;
+        for (int j = 0; j < K; ++j) {
+            const int b = nib(nd.bits, j), fr = nb - b;
+            const int l0 = (c[j] >> fr) << fr;
+            lo[l * K + j] = (uint8_t)l0;
+            hi[l * K + j] = (uint8_t)(l0 + (1 << fr) - 1);
+            bits[l * K + j] = (uint8_t)b;
+        }
+        if (l == nl - 1) leaf_off[nl] = (uint32_t)total;
+    }
+}
+
+__global__ void k_tree_begin(const uint32_t* __restrict__ leaf_off, int64_t nl, int64_t n, int L,
+                             unsigned long long* __restrict__ begin) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t > L) return;
+    const uint64_t target = (uint64_t)t * n;   // first leaf with start >= t*n
+    int64_t lo = 0, hi = nl;
+    while (lo < hi) {
+        int64_t mid = (lo + hi) >> 1;
+        if (leaf_off[mid] < target) lo = mid + 1; else hi = mid;
+    }
+    begin[t] = (unsigned long long)lo;
+}
+
+__global__ void k_gather_tcodes(const uint32_t* __restrict__ perm, const uint8_t* __restrict__ EP, int64_t n,
+                                int L, int K, uint8_t* __restrict__ tcodes) {
+    const int LK = L * K;
+    const int64_t total = n * L;
+    for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total;
+         g += (int64_t)gridDim.x * blockDim.x) {
+        const int t = (int)(g / n);
+        const uint8_t* src = EP + (int64_t)perm[g] * LK + t * K;
+        uint8_t* dst = tcodes + g * K;
+        if ((K & 15) == 0) {
+            for (int j = 0; j < K; j += 16)
+                *reinterpret_cast<uint4*>(dst + j) = *reinterpret_cast<const uint4*>(src + j);
+        } else {
+            for (int j = 0; j < K; ++j) dst[j] = src[j];
+        }
+    }
+}
+
+__global__ void k_gather_rows_strided(const float* __restrict__ src, int64_t src_ld, int d,
+                                      const uint32_t* __restrict__ ids, int64_t m, float* __restrict__ dst,
+                                      int64_t dst_ld) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t r = warp; r < m; r += nwarps) {
+        const float* s = src + (int64_t)ids[r] * src_ld;
+        float* o = dst + r * dst_ld;
+        for (int64_t f = lane; f < dst_ld; f += 32) o[f] = f < d ? s[f] : 0.f;
+    }
+}
+
+int grid_for(int64_t work, int threads, int cap = 148 * 16) {
+    int64_t g = ceil_div(std::max<int64_t>(work, 1), threads);
+    return (int)std::min<int64_t>(g, cap);
+}
+
+template <class T> T d2h(const T* d, cudaStream_t st) {
+    T h;
+    DL_CUDA(cudaMemcpyAsync(&h, d, sizeof(T), cudaMemcpyDeviceToHost, st));
+    DL_CUDA(cudaStreamSynchronize(st));
+    return h;
+}
+
+}  // namespace
+
+// ====================================================================== host drivers
+
+// B1: ids in [id_lo, id_lo+n_range) among the n_s smallest keyed hashes of [0, n_global).
+void sample_ids_device(uint64_t seed, int64_t id_lo, int64_t n_range, int64_t n_global, int64_t n_s,
+                       uint32_t* d_out_local, int64_t* n_out_host, cudaStream_t st) {
+    const uint64_t salt = seed ^ kSampleSalt;
+    Scratch s_state(st, sizeof(SelState) + 256 * sizeof(uint32_t) + 16);
+    SelState* state = s_state.as<SelState>();
+    uint32_t* hist = reinterpret_cast<uint32_t*>(state + 1);
+    DL_CUDA(cudaMemsetAsync(hist, 0, 256 * sizeof(uint32_t), st));
+    DL_LAUNCH(k_sel_init, 1, 1, 0, st, state, n_s);
+    const int g = grid_for(n_global, 256, 148 * 8);
+    for (int pass = 0; pass < 8; ++pass) {
+        const int shift = 56 - 8 * pass;
+        DL_LAUNCH(k_sel_hist, g, 256, 0, st, salt, n_global, shift, state, hist);
+        DL_LAUNCH(k_sel_pick, 1, 256, 0, st, shift, state, hist);
+    }
+    Scratch s_cnt(st, sizeof(unsigned long long));
+    DL_CUDA(cudaMemsetAsync(s_cnt.p, 0, sizeof(unsigned long long), st));
+    DL_LAUNCH(k_sel_collect, grid_for(n_range, 256, 148 * 8), 256, 0, st, salt, id_lo, n_range, state, d_out_local,
+              s_cnt.as<unsigned long long>());
+    DL_LAUNCH(k_sel_ties, 1, 1, 0, st, salt, id_lo, n_range, n_global, state, d_out_local,
+              s_cnt.as<unsigned long long>());
+    *n_out_host = (int64_t)d2h(s_cnt.as<unsigned long long>(), st);
+}
+
+void breakpoints_from_projections(const float* d_Ps, int64_t m, int LK, int N_r, float* d_B, cudaStream_t st) {
+    Scratch keys(st, sizeof(uint32_t) * (size_t)(2 * m * LK));
+    uint32_t* k0 = keys.as<uint32_t>();
+    uint32_t* k1 = k0 + m * LK;
+    DL_LAUNCH(k_transpose_keys, grid_for(m * LK, 256), 256, 0, st, d_Ps, m, LK, k0);
+    bool flip = radix_sort_batched(k0, nullptr, k1, nullptr, m, LK, 32, st);
+    DL_LAUNCH(k_bp_gather, grid_for((int64_t)LK * (N_r + 1), 256), 256, 0, st, flip ? k1 : k0, m, LK, N_r, d_B);
+}
+
+static void encode_all(const Index& ix, const float* d_P, int64_t m, uint8_t* d_EP, cudaStream_t st) {
+    const size_t smem = sizeof(float) * (size_t)ix.LK * ix.N_r;
+    DL_CUDA(cudaFuncSetAttribute(k_encode, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    DL_LAUNCH(k_encode, grid_for(m * ix.LK / 4, 256, 148 * 4), 256, smem, st, d_P, m, ix.LK, ix.N_r,
+              ix.B.as<float>(), d_EP);
+}
+
+// B5 + B6 for all L trees at once, from codes EP[n][LK] (data order).  Returns false if the
+// leaf list overflowed its capacity (the caller retries with a larger factor).
+static bool build_trees_try(Index& ix, const uint8_t* d_EP, int64_t leaf_factor, cudaStream_t st) {
+    const int64_t n = ix.n, L = ix.L, total = n * L;
+    const int K = ix.K, nb = ix.nb, LK = ix.LK, max_size = ix.max_size;
+    DL_REQUIRE(total < (int64_t)0xFFFFFFFF, "L*n must be < 2^32");
+
+    ix.perm.alloc(sizeof(uint32_t) * (size_t)total);
+    Scratch s_sort(st, sizeof(uint32_t) * (size_t)(3 * total));
+    uint32_t* keys0 = s_sort.as<uint32_t>();
+    uint32_t* keys1 = keys0 + total;
+    uint32_t* vals1 = keys1 + total;
+    uint32_t* perm = ix.perm.as<uint32_t>();
+
+    // B5: first-layer keys, stable (key, id) sort per tree
+    DL_LAUNCH(k_first_key, grid_for(total, 256), 256, 0, st, d_EP, n, (int)L, K, nb, keys0, perm);
+    bool flip = radix_sort_batched(keys0, perm, keys1, vals1, n, L, K, st);
+    const uint32_t* skeys = flip ? keys1 : keys0;
+    if (flip) DL_CUDA(cudaMemcpyAsync(perm, vals1, sizeof(uint32_t) * total, cudaMemcpyDeviceToDevice, st));
+
+    // first-layer segments
+    Scratch s_seg(st, sizeof(uint32_t) * (size_t)(2 * total + 8));
+    uint32_t* flags = s_seg.as<uint32_t>();
+    uint32_t* idx = flags + total;
+    uint32_t* counters = idx + total;  // [0]=nseg [1]=n_active [2]=n_next [3]=n_leaves [4]=total_chunks
+    DL_CUDA(cudaMemsetAsync(counters, 0, 8 * sizeof(uint32_t), st));
+    DL_LAUNCH(k_seg_flags, grid_for(total, 256), 256, 0, st, skeys, n, total, flags);
+    exclusive_scan_u32(flags, idx, total, counters + 0, st);
+    const int64_t nseg = d2h(counters + 0, st);
+    Scratch s_starts(st, sizeof(uint32_t) * (size_t)nseg);
+    DL_LAUNCH(k_seg_write, grid_for(total, 256), 256, 0, st, flags, idx, total, s_starts.as<uint32_t>());
+
+    // node storage: active nodes of one level are disjoint and hold > max_size points each;
+    // leaves are disjoint and non-empty (<= total); start from a typical size and grow on overflow
+    const int64_t cap_active = total / std::max(1, max_size) + 1;
+    const int64_t cap_leaves = std::min<int64_t>(total, nseg + leaf_factor * (total / std::max(1, max_size)) + 1024);
+    Scratch s_nodes(st, sizeof(Node) * (size_t)(2 * cap_active + cap_leaves));
+    Node* act = s_nodes.as<Node>();
+    Node* nxt = act + cap_active;
+    Node* leaves = nxt + cap_active;
+    uint32_t* n_act = counters + 1;
+    uint32_t* n_nxt = counters + 2;
+    uint32_t* n_leaves = counters + 3;
+    uint32_t* total_ch = counters + 4;
+    DL_LAUNCH(k_init_nodes, grid_for(nseg, 256), 256, 0, st, s_starts.as<uint32_t>(), counters + 0, total, K, nb,
+              max_size, act, n_act, (uint32_t)cap_active, leaves, n_leaves, (uint32_t)cap_leaves);
+    s_starts.free_();
+
+    // B6: level loop
+    Scratch s_level(st, sizeof(uint32_t) * (size_t)(4 * cap_active + 4));
+    int* split = s_level.as<int>();
+    uint32_t* nch = reinterpret_cast<uint32_t*>(split + cap_active);
+    uint32_t* choff = nch + cap_active;
+    uint32_t* zeros = choff + cap_active;
+    Scratch s_tmp(st, sizeof(uint32_t) * (size_t)total);
+    Scratch s_zc(st);
+    int64_t zc_cap = 0;
+    int64_t na = d2h(n_act, st);
+    int level = 0;
+    while (na > 0) {
+        DL_REQUIRE(++level < 4096, "tree build: too many split levels");
+        DL_LAUNCH(k_choose_split, grid_for(na * 32, 256), 256, 0, st, act, n_act, perm, d_EP, n, LK, K, nb,
+                  max_size, PART_CHUNK, split, nch);
+        exclusive_scan_u32(nch, choff, na, total_ch, st);
+        const int64_t nc = d2h(total_ch, st);
+        if (nc > zc_cap) {
+            zc_cap = nc * 2;
+            s_zc.alloc(sizeof(uint32_t) * (size_t)zc_cap);
+        }
+        if (nc > 0) {
+            DL_LAUNCH(k_part_count, (unsigned)nc, PART_THREADS, 0, st, act, split, choff, n_act, total_ch, perm, d_EP,
+                      n, LK, K, nb, s_zc.as<uint32_t>());
+            DL_LAUNCH(k_part_offsets, grid_for(na, 256), 256, 0, st, choff, nch, n_act, s_zc.as<uint32_t>(), zeros);
+            DL_LAUNCH(k_part_scatter, (unsigned)nc, PART_THREADS, 0, st, act, split, choff, n_act, total_ch,
+                      s_zc.as<uint32_t>(), zeros, perm, d_EP, n, LK, K, nb, s_tmp.as<uint32_t>());
+            DL_LAUNCH(k_part_copy, (unsigned)nc, PART_THREADS, 0, st, act, choff, n_act, total_ch, s_tmp.as<uint32_t>(),
+                      perm);
+        }
+        DL_CUDA(cudaMemsetAsync(n_nxt, 0, sizeof(uint32_t), st));
+        DL_LAUNCH(k_make_children, grid_for(na, 256), 256, 0, st, act, n_act, split, zeros, K, nb, max_size, nxt,
+                  n_nxt, (uint32_t)cap_active, leaves, n_leaves, (uint32_t)cap_leaves);
+        std::swap(act, nxt);
+        std::swap(n_act, n_nxt);
+        na = d2h(n_act, st);
+        DL_REQUIRE(na <= cap_active, "tree build: active-node capacity exceeded");
+    }
+    s_tmp.free_();
+    s_zc.free_();
+    s_level.free_();
+
+    // leaves in canonical order = ascending start position (DFS, 0-child first, keys ascending)
+    const int64_t nl = d2h(n_leaves, st);
+    if (nl > cap_leaves) return false;
+    Scratch s_lsort(st, sizeof(uint32_t) * (size_t)(4 * nl));
+    uint32_t* lk0 = s_lsort.as<uint32_t>();
+    uint32_t* lv0 = lk0 + nl;
+    uint32_t* lk1 = lv0 + nl;
+    uint32_t* lv1 = lk1 + nl;
+    DL_LAUNCH(k_leaf_keys, grid_for(nl, 256), 256, 0, st, leaves, n_leaves, lk0, lv0);
+    int bits = 1;
+    while (bits < 32 && ((int64_t)1 << bits) < total) ++bits;
+    bits = (int)round_up(bits, 8);
+    bool lf = radix_sort_batched(lk0, lv0, lk1, lv1, nl, 1, bits, st);
+    ix.leaf_off.alloc(sizeof(uint32_t) * (size_t)(nl + 1));
+    ix.leaf_lo.alloc((size_t)nl * K);
+    ix.leaf_hi.alloc((size_t)nl * K);
+    ix.leaf_bits.alloc((size_t)nl * K);
+    DL_LAUNCH(k_leaf_finalize, grid_for(nl, 256), 256, 0, st, leaves, lf ? lv1 : lv0, nl, perm, d_EP, n, LK, K, nb,
+              ix.leaf_off.as<uint32_t>(), ix.leaf_lo.as<uint8_t>(), ix.leaf_hi.as<uint8_t>(),
+              ix.leaf_bits.as<uint8_t>(), total);
+    Scratch s_begin(st, sizeof(unsigned long long) * (size_t)(L + 1));
+    DL_LAUNCH(k_tree_begin, 1, 64, 0, st, ix.leaf_off.as<uint32_t>(), nl, n, (int)L, s_begin.as<unsigned long long>());
+    std::vector<unsigned long long> begin(L + 1);
+    DL_CUDA(cudaMemcpyAsync(begin.data(), s_begin.p, sizeof(unsigned long long) * (L + 1), cudaMemcpyDeviceToHost, st));
+    ix.tcodes.alloc((size_t)total * K);
+    DL_LAUNCH(k_gather_tcodes, grid_for(total, 256), 256, 0, st, perm, d_EP, n, (int)L, K, ix.tcodes.as<uint8_t>());
+    DL_CUDA(cudaStreamSynchronize(st));
+    ix.tree_leaf_begin.assign(begin.begin(), begin.end());
+    ix.tree_leaf_begin[L] = nl;
+    return true;
+}
+
+static void build_trees(Index& ix, const uint8_t* d_EP, cudaStream_t st) {
+    for (int64_t f = 4;; f *= 4) {
+        if (build_trees_try(ix, d_EP, f, st)) return;
+        DL_REQUIRE(f < (int64_t)1 << 40, "tree build: leaf list overflow");
+    }
+}
+
+void build_index(Index& ix, const float* d_data, int64_t data_ld, const float* bp_given, double sample_frac,
+                 int proj_impl, cudaStream_t st) {
+    const int64_t n = ix.n;
+    // B0: hash family
+    ix.A.alloc(sizeof(float) * (size_t)ix.LK * ix.ld);
+    DL_LAUNCH(k_hash_family, grid_for((int64_t)ix.LK * ix.ld, 256), 256, 0, st, ix.seed, ix.LK, ix.d, ix.ld,
+              ix.A.as<float>());
+    Scratch s_flag(st, sizeof(int));
+    DL_CUDA(cudaMemsetAsync(s_flag.p, 0, sizeof(int), st));
+    // B1-B3: breakpoints
+    ix.B.alloc(sizeof(float) * (size_t)ix.LK * (ix.N_r + 1));
+    if (bp_given) {
+        DL_CUDA(cudaMemcpyAsync(ix.B.p, bp_given, ix.B.bytes, cudaMemcpyDefault, st));
+        ix.n_s = 0;
+    } else {
+        const int64_t n_s = detlsh_sample_size(n, ix.N_r, sample_frac);
+        ix.sample.alloc(sizeof(uint32_t) * (size_t)n_s);
+        int64_t got = 0;
+        sample_ids_device(ix.seed, 0, n, n, n_s, ix.sample.as<uint32_t>(), &got, st);
+        DL_REQUIRE(got == n_s, "sample selection returned the wrong count");
+        ix.n_s = n_s;
+        Scratch s_xs(st, sizeof(float) * (size_t)(n_s * data_ld));
+        Scratch s_ps(st, sizeof(float) * (size_t)(n_s * ix.LK));
+        DL_LAUNCH(k_gather_rows, grid_for(n_s * 32, 256), 256, 0, st, d_data, data_ld, ix.sample.as<uint32_t>(), n_s,
+                  s_xs.as<float>());
+        project_rows(ix, s_xs.as<float>(), data_ld, n_s, s_ps.as<float>(), proj_impl, s_flag.as<int>(), st);
+        breakpoints_from_projections(s_ps.as<float>(), n_s, ix.LK, ix.N_r, ix.B.as<float>(), st);
+    }
+    // B2 + B4: project every row and encode (chunked so P stays bounded)
+    Scratch s_ep(st, (size_t)n * ix.LK);
+    {
+        const int64_t chunk = std::min<int64_t>(n, std::max<int64_t>(1 << 16, (int64_t)(1ll << 30) / (4 * ix.LK)));
+        Scratch s_p(st, sizeof(float) * (size_t)(chunk * ix.LK));
+        for (int64_t r0 = 0; r0 < n; r0 += chunk) {
+            const int64_t m = std::min(chunk, n - r0);
+            project_rows(ix, d_data + r0 * data_ld, data_ld, m, s_p.as<float>(), proj_impl, s_flag.as<int>(), st);
+            encode_all(ix, s_p.as<float>(), m, s_ep.as<uint8_t>() + r0 * ix.LK, st);
+        }
+    }
+    const int nonfinite = d2h(s_flag.as<int>(), st);
+    DL_REQUIRE(!nonfinite, "data contains NaN or Inf");
+    // B5 + B6
+    build_trees(ix, s_ep.as<uint8_t>(), st);
+}
+
+void build_trees_from_codes(Index& ix, const uint8_t* d_codes, cudaStream_t st) { build_trees(ix, d_codes, st); }
+
+void build_index_hash_only(Index& ix, cudaStream_t st) {
+    ix.A.alloc(sizeof(float) * (size_t)ix.LK * ix.ld);
+    DL_LAUNCH(k_hash_family, grid_for((int64_t)ix.LK * ix.ld, 256), 256, 0, st, ix.seed, ix.LK, ix.d, ix.ld,
+              ix.A.as<float>());
+}
+
+void gather_rows_strided(const float* d_src, int64_t src_ld, int d, const uint32_t* d_ids, int64_t m, float* d_dst,
+                         int64_t dst_ld, cudaStream_t st) {
+    if (m <= 0) return;
+    DL_LAUNCH(k_gather_rows_strided, grid_for(m * 32, 256), 256, 0, st, d_src, src_ld, d, d_ids, m, d_dst, dst_ld);
+}
+
+}  // namespace detlsh

@@ -1,0 +1,114 @@
+// common.cuh -- shared helpers of the DET-LSH sm_100a library (product code).
+// Nothing here is shared with oracle/ (the test oracle has its own C code).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <atomic>
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+
+#include "../../include/detlsh.h"
+
+namespace detlsh {
+
+// ------------------------------------------------------------------ errors
+struct Error : std::runtime_error {
+    detlsh_status code;
+    Error(detlsh_status c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define DL_CUDA(expr)                                                                          \
+    do {                                                                                       \
+        cudaError_t _e = (expr);                                                               \
+        if (_e != cudaSuccess) {                                                               \
+            throw ::detlsh::Error(_e == cudaErrorMemoryAllocation ? DETLSH_ENOMEM : DETLSH_ECUDA, \
+                                  std::string(#expr) + ": " + cudaGetErrorString(_e) + " (" +    \
+                                      __FILE__ + ":" + std::to_string(__LINE__) + ")");         \
+        }                                                                                      \
+    } while (0)
+
+#define DL_REQUIRE(cond, msg)                                                                  \
+    do {                                                                                       \
+        if (!(cond)) throw ::detlsh::Error(DETLSH_EINVAL, msg);                                \
+    } while (0)
+
+extern std::atomic<int64_t> g_launches;
+
+// Every kernel launch goes through this macro: counts launches (the evidence counter
+// behind detlsh_launch_count) and checks the launch error.
+#define DL_LAUNCH(kernel, grid, block, smem, stream, ...)                                       \
+    do {                                                                                       \
+        kernel<<<(grid), (block), (smem), (stream)>>>(__VA_ARGS__);                            \
+        ::detlsh::g_launches.fetch_add(1, std::memory_order_relaxed);                          \
+        DL_CUDA(cudaGetLastError());                                                           \
+    } while (0)
+
+// ------------------------------------------------------------------ math helpers
+__host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+__host__ __device__ inline int64_t round_up(int64_t a, int64_t b) { return ceil_div(a, b) * b; }
+
+// splitmix64 output for state x, and the keyed hash key(s, c) = splitmix64(s ^ splitmix64(c))
+// that AMB-1 (hash family) and AMB-4 (sample) are defined with.
+__host__ __device__ inline uint64_t mix64(uint64_t x) {
+    uint64_t z = x + 0x9E3779B97F4A7C15ULL;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+}
+__host__ __device__ inline uint64_t keyed(uint64_t s, uint64_t c) { return mix64(s ^ mix64(c)); }
+
+constexpr uint64_t kSampleSalt = 0x53414D504C45ULL;  // AMB-4
+
+#if defined(__CUDACC__)
+// Order-preserving fp32 <-> u32 maps (radix sorting floats).
+__device__ inline uint32_t f2key(float f) {
+    uint32_t u = __float_as_uint(f);
+    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ inline float key2f(uint32_t k) {
+    uint32_t u = (k & 0x80000000u) ? (k & 0x7FFFFFFFu) : ~k;
+    return __uint_as_float(u);
+}
+
+__device__ inline uint32_t lanemask_lt() {
+    uint32_t m;
+    asm volatile("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+#endif
+
+// ------------------------------------------------------------------ primitives (radix.cu)
+// Stable batched LSD radix sort: nseg independent segments of m u32 keys (segment s at
+// keys + s*m), optional u32 values; sorts on key bits [0, bits).  Ping-pongs between
+// (k0,v0) and (k1,v1); returns true if the result ended in (k1,v1).
+bool radix_sort_batched(uint32_t* k0, uint32_t* v0, uint32_t* k1, uint32_t* v1, int64_t m,
+                        int64_t nseg, int bits, cudaStream_t st);
+// Exclusive scan of n u32 values; writes the total to *d_total (device) if non-null.
+void exclusive_scan_u32(const uint32_t* in, uint32_t* out, int64_t n, uint32_t* d_total,
+                        cudaStream_t st);
+
+// ------------------------------------------------------------------ scratch allocation
+// Stream-ordered device scratch (cudaMallocAsync from the device pool).
+struct Scratch {
+    cudaStream_t st;
+    void* p = nullptr;
+    explicit Scratch(cudaStream_t s) : st(s) {}
+    Scratch(cudaStream_t s, size_t bytes) : st(s) { alloc(bytes); }
+    void alloc(size_t bytes) {
+        free_();
+        if (bytes) DL_CUDA(cudaMallocAsync(&p, bytes, st));
+    }
+    void free_() {
+        if (p) cudaFreeAsync(p, st);
+        p = nullptr;
+    }
+    ~Scratch() { free_(); }
+    template <class T> T* as() const { return static_cast<T*>(p); }
+    Scratch(const Scratch&) = delete;
+    Scratch& operator=(const Scratch&) = delete;
+};
+
+}  // namespace detlsh

@@ -1,0 +1,90 @@
+// index.cuh -- device layout of a DET-LSH index.
+#pragma once
+
+#include <vector>
+
+#include "common.cuh"
+
+namespace detlsh {
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf() { reset(); }
+    void alloc(size_t b) {
+        reset();
+        if (b) DL_CUDA(cudaMalloc(&p, b));
+        bytes = b;
+    }
+    void reset() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+    }
+    template <class T> T* as() const { return static_cast<T*>(p); }
+};
+
+struct Index {
+    // shape / parameters
+    int64_t n = 0;          // points in this index (shard)
+    int64_t n_global = 0;
+    int64_t id_offset = 0;
+    int32_t d = 0, ld = 0;  // dimension, padded row stride (floats, multiple of 8)
+    int32_t L = 0, K = 0, LK = 0, N_r = 0, nb = 0;
+    int32_t max_size = 128;
+    uint64_t seed = 0;
+    double eps = 0;         // sqrt(chi2_{e^{-1/L}}(K)) (Eq. 2)
+    int64_t n_s = 0;        // sample size used for the breakpoints (0 if given)
+    bool codes_only = false;
+
+    // device arrays
+    DevBuf X;               // [n][ld] fp32 (owned copy) -- unless borrowed
+    const float* Xp = nullptr;  // points to X or the borrowed buffer
+    DevBuf A;               // [LK][d] fp32 hash family (TF32-exact values, AMB-1)
+    DevBuf B;               // [LK][N_r+1] fp32 breakpoints
+    DevBuf sample;          // [n_s] u32 sample ids (local), unordered
+    DevBuf perm;            // [L*n] u32: tree t's point ids in leaf order at [t*n, (t+1)*n)
+    DevBuf tcodes;          // [L*n][K] u8: codes of perm in leaf order (per tree)
+    DevBuf leaf_off;        // [nl_total+1] u32 global positions into perm (tree-major)
+    DevBuf leaf_lo, leaf_hi;// [nl_total][K] u8 symbol range of each leaf box
+    DevBuf leaf_bits;       // [nl_total][K] u8 bits per dim of each leaf
+    std::vector<int64_t> tree_leaf_begin;  // [L+1] leaf index range of each tree (host copy)
+
+    int64_t nl_total() const { return tree_leaf_begin.empty() ? 0 : tree_leaf_begin.back(); }
+};
+
+// build.cu
+void build_index(Index& ix, const float* d_data, int64_t data_ld, const float* bp_given,
+                 double sample_frac, int proj_impl, cudaStream_t st);
+void build_trees_from_codes(Index& ix, const uint8_t* d_codes, cudaStream_t st);
+void build_index_hash_only(Index& ix, cudaStream_t st);
+void gather_rows_strided(const float* d_src, int64_t src_ld, int d, const uint32_t* d_ids, int64_t m, float* d_dst,
+                         int64_t dst_ld, cudaStream_t st);
+void project_rows(const Index& ix, const float* d_X, int64_t ld, int64_t m, float* d_P, int proj_impl,
+                  int* d_nonfinite, cudaStream_t st);
+void sample_ids_device(uint64_t seed, int64_t id_lo, int64_t n_range, int64_t n_global, int64_t n_s,
+                       uint32_t* d_out_local, int64_t* n_out_host, cudaStream_t st);
+void breakpoints_from_projections(const float* d_Ps, int64_t m, int LK, int N_r, float* d_B,
+                                  cudaStream_t st);
+
+// query.cu
+struct QueryArgs {
+    int64_t nq;
+    int k;
+    double c, r_min, beta;
+    int mode;
+    int query_batch;
+    int64_t mem_budget;
+    int proj_impl;
+};
+void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArgs& a, int64_t* d_ids,
+                 float* d_dists, detlsh_query_stats* d_stats, cudaStream_t st);
+
+// host_math.cpp
+double chi2_upper_quantile(double alpha, int K);
+double chi2_survival(double y, int K);
+
+}  // namespace detlsh

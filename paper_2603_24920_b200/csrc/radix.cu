@@ -1,0 +1,236 @@
+// radix.cu -- hand-written stable LSD radix sort (batched segments) and exclusive scan.
+//
+// Used by the build for (a) sorting the breakpoint sample per projected coordinate
+// and (b) the per-tree first-layer sort of (key, id) pairs (Alg. 2 line 2,
+// P:312; B5), and by the leaf finaliser.  No library sort is dispatched.
+//
+// One pass (8-bit digit): hist (per tile digit counts) -> scan (digit-major, per segment)
+// -> scatter (stable rank inside a tile via warp match + per-warp digit counts).
+#include "common.cuh"
+
+namespace detlsh {
+
+namespace {
+
+constexpr int RS_THREADS = 256;
+constexpr int RS_IPT = 16;                          // items per thread
+constexpr int RS_TILE = RS_THREADS * RS_IPT;        // 4096 keys per tile
+constexpr int RS_WARPS = RS_THREADS / 32;
+
+__global__ void __launch_bounds__(RS_THREADS) k_rs_hist(const uint32_t* __restrict__ keys, int64_t m,
+                                                        int shift, int tiles, uint32_t* __restrict__ hist) {
+    __shared__ uint32_t h[256];
+    const int seg = blockIdx.y, tile = blockIdx.x;
+    h[threadIdx.x] = 0;
+    __syncthreads();
+    const uint32_t* k = keys + (int64_t)seg * m;
+    int64_t base = (int64_t)tile * RS_TILE;
+#pragma unroll 4
+    for (int j = 0; j < RS_IPT; ++j) {
+        int64_t e = base + (int64_t)j * RS_THREADS + threadIdx.x;
+        if (e < m) atomicAdd(&h[(k[e] >> shift) & 255u], 1u);
+    }
+    __syncthreads();
+    hist[((int64_t)seg * 256 + threadIdx.x) * tiles + tile] = h[threadIdx.x];
+}
+
+// Block-wide exclusive scan of one value per thread (1024 threads max); returns the block total.
+template <int NT>
+__device__ inline uint32_t block_exclusive_scan(uint32_t v, uint32_t* s_warp, uint32_t& excl) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    uint32_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) s_warp[w] = x;
+    __syncthreads();
+    if (w == 0) {
+        uint32_t t = lane < NT / 32 ? s_warp[lane] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            uint32_t y = __shfl_up_sync(0xffffffffu, t, o);
+            if (lane >= o) t += y;
+        }
+        if (lane < NT / 32) s_warp[lane] = t;  // inclusive warp totals
+    }
+    __syncthreads();
+    uint32_t total = s_warp[NT / 32 - 1];
+    excl = x - v + (w ? s_warp[w - 1] : 0);
+    __syncthreads();
+    return total;
+}
+
+// Exclusive scan, in place, of each segment's 256*tiles digit-major counts (one block per segment).
+__global__ void __launch_bounds__(1024) k_rs_scan(uint32_t* __restrict__ hist, int64_t len) {
+    __shared__ uint32_t s_warp[32];
+    uint32_t* h = hist + (int64_t)blockIdx.x * len;
+    uint32_t carry = 0;
+    for (int64_t base = 0; base < len; base += 1024 * 4) {
+        uint32_t v[4], s = 0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            int64_t e = base + (int64_t)threadIdx.x * 4 + j;
+            v[j] = e < len ? h[e] : 0;
+            s += v[j];
+        }
+        uint32_t excl;
+        uint32_t tot = block_exclusive_scan<1024>(s, s_warp, excl);
+        uint32_t run = carry + excl;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            int64_t e = base + (int64_t)threadIdx.x * 4 + j;
+            if (e < len) h[e] = run;
+            run += v[j];
+        }
+        carry += tot;
+    }
+}
+
+template <bool HAS_VALS>
+__global__ void __launch_bounds__(RS_THREADS) k_rs_scatter(const uint32_t* __restrict__ kin,
+                                                           const uint32_t* __restrict__ vin,
+                                                           uint32_t* __restrict__ kout,
+                                                           uint32_t* __restrict__ vout, int64_t m,
+                                                           int shift, int tiles,
+                                                           const uint32_t* __restrict__ offs) {
+    __shared__ uint32_t s_base[256];
+    __shared__ uint32_t s_wcnt[RS_WARPS][256];
+    const int seg = blockIdx.y, tile = blockIdx.x;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    s_base[threadIdx.x] = offs[((int64_t)seg * 256 + threadIdx.x) * tiles + tile];
+    const uint32_t* k = kin + (int64_t)seg * m;
+    const uint32_t* v = HAS_VALS ? vin + (int64_t)seg * m : nullptr;
+    uint32_t* ko = kout + (int64_t)seg * m;
+    uint32_t* vo = HAS_VALS ? vout + (int64_t)seg * m : nullptr;
+    const int64_t base = (int64_t)tile * RS_TILE;
+    const uint32_t lt = lanemask_lt();
+    for (int j = 0; j < RS_IPT; ++j) {
+#pragma unroll
+        for (int ww = 0; ww < RS_WARPS; ++ww) s_wcnt[ww][threadIdx.x] = 0;
+        __syncthreads();
+        int64_t e = base + (int64_t)j * RS_THREADS + threadIdx.x;
+        bool ok = e < m;
+        uint32_t key = ok ? k[e] : 0u;
+        uint32_t val = (HAS_VALS && ok) ? v[e] : 0u;
+        uint32_t dig = ok ? ((key >> shift) & 255u) : 256u;
+        uint32_t peers = __match_any_sync(0xffffffffu, dig);
+        uint32_t rank = __popc(peers & lt);
+        if (ok && rank == 0) s_wcnt[w][dig] = __popc(peers);
+        __syncthreads();
+        if (ok) {
+            uint32_t pos = s_base[dig] + rank;
+            for (int ww = 0; ww < w; ++ww) pos += s_wcnt[ww][dig];
+            ko[pos] = key;
+            if (HAS_VALS) vo[pos] = val;
+        }
+        __syncthreads();
+        uint32_t add = 0;
+#pragma unroll
+        for (int ww = 0; ww < RS_WARPS; ++ww) add += s_wcnt[ww][threadIdx.x];
+        s_base[threadIdx.x] += add;
+        // the next iteration's zeroing is ordered after this read by the barrier below
+        __syncthreads();
+    }
+}
+
+constexpr int SC_THREADS = 1024;
+constexpr int SC_IPT = 8;
+constexpr int SC_TILE = SC_THREADS * SC_IPT;
+
+__global__ void __launch_bounds__(SC_THREADS) k_scan_tiles(const uint32_t* __restrict__ in, int64_t n,
+                                                           uint32_t* __restrict__ tile_sums) {
+    __shared__ uint32_t s_warp[32];
+    int64_t base = (int64_t)blockIdx.x * SC_TILE;
+    uint32_t s = 0;
+#pragma unroll
+    for (int j = 0; j < SC_IPT; ++j) {
+        int64_t e = base + (int64_t)threadIdx.x * SC_IPT + j;
+        if (e < n) s += in[e];
+    }
+    uint32_t excl;
+    uint32_t tot = block_exclusive_scan<SC_THREADS>(s, s_warp, excl);
+    if (threadIdx.x == 0) tile_sums[blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(SC_THREADS) k_scan_sums(uint32_t* __restrict__ sums, int64_t nt,
+                                                          uint32_t* __restrict__ d_total) {
+    __shared__ uint32_t s_warp[32];
+    uint32_t carry = 0;
+    for (int64_t base = 0; base < nt; base += SC_THREADS) {
+        int64_t e = base + threadIdx.x;
+        uint32_t v = e < nt ? sums[e] : 0;
+        uint32_t excl;
+        uint32_t tot = block_exclusive_scan<SC_THREADS>(v, s_warp, excl);
+        if (e < nt) sums[e] = carry + excl;
+        carry += tot;
+    }
+    if (threadIdx.x == 0 && d_total) *d_total = carry;
+}
+
+__global__ void __launch_bounds__(SC_THREADS) k_scan_apply(const uint32_t* __restrict__ in, int64_t n,
+                                                           const uint32_t* __restrict__ tile_offs,
+                                                           uint32_t* __restrict__ out) {
+    __shared__ uint32_t s_warp[32];
+    int64_t base = (int64_t)blockIdx.x * SC_TILE;
+    uint32_t v[SC_IPT], s = 0;
+#pragma unroll
+    for (int j = 0; j < SC_IPT; ++j) {
+        int64_t e = base + (int64_t)threadIdx.x * SC_IPT + j;
+        v[j] = e < n ? in[e] : 0;
+        s += v[j];
+    }
+    uint32_t excl;
+    block_exclusive_scan<SC_THREADS>(s, s_warp, excl);
+    uint32_t run = tile_offs[blockIdx.x] + excl;
+#pragma unroll
+    for (int j = 0; j < SC_IPT; ++j) {
+        int64_t e = base + (int64_t)threadIdx.x * SC_IPT + j;
+        if (e < n) out[e] = run;
+        run += v[j];
+    }
+}
+
+}  // namespace
+
+bool radix_sort_batched(uint32_t* k0, uint32_t* v0, uint32_t* k1, uint32_t* v1, int64_t m,
+                        int64_t nseg, int bits, cudaStream_t st) {
+    if (m <= 0 || nseg <= 0 || bits <= 0) return false;
+    const int tiles = (int)ceil_div(m, RS_TILE);
+    const int64_t len = (int64_t)256 * tiles;
+    Scratch hist(st, sizeof(uint32_t) * (size_t)(len * nseg));
+    bool flip = false;
+    for (int shift = 0; shift < bits; shift += 8) {
+        uint32_t* ki = flip ? k1 : k0;
+        uint32_t* vi = flip ? v1 : v0;
+        uint32_t* ko = flip ? k0 : k1;
+        uint32_t* vo = flip ? v0 : v1;
+        dim3 grid(tiles, (unsigned)nseg);
+        DL_LAUNCH(k_rs_hist, grid, RS_THREADS, 0, st, ki, m, shift, tiles, hist.as<uint32_t>());
+        DL_LAUNCH(k_rs_scan, (unsigned)nseg, 1024, 0, st, hist.as<uint32_t>(), len);
+        if (v0) {
+            DL_LAUNCH(k_rs_scatter<true>, grid, RS_THREADS, 0, st, ki, vi, ko, vo, m, shift, tiles,
+                      hist.as<uint32_t>());
+        } else {
+            DL_LAUNCH(k_rs_scatter<false>, grid, RS_THREADS, 0, st, ki, (const uint32_t*)nullptr, ko,
+                      (uint32_t*)nullptr, m, shift, tiles, hist.as<uint32_t>());
+        }
+        flip = !flip;
+    }
+    return flip;
+}
+
+void exclusive_scan_u32(const uint32_t* in, uint32_t* out, int64_t n, uint32_t* d_total, cudaStream_t st) {
+    if (n <= 0) {
+        if (d_total) DL_CUDA(cudaMemsetAsync(d_total, 0, sizeof(uint32_t), st));
+        return;
+    }
+    const int64_t nt = ceil_div(n, SC_TILE);
+    Scratch sums(st, sizeof(uint32_t) * (size_t)nt);
+    DL_LAUNCH(k_scan_tiles, (unsigned)nt, SC_THREADS, 0, st, in, n, sums.as<uint32_t>());
+    DL_LAUNCH(k_scan_sums, 1, SC_THREADS, 0, st, sums.as<uint32_t>(), nt, d_total);
+    DL_LAUNCH(k_scan_apply, (unsigned)nt, SC_THREADS, 0, st, in, n, sums.as<uint32_t>(), out);
+}
+
+}  // namespace detlsh

@@ -1,0 +1,258 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle, element by element.
+
+Tolerances (north_star):
+  hash family, sample ids, breakpoints-from-identical-samples, trees-from-identical-codes: bit-exact
+  projections: |dP| <= 1e-4 max(|p|, ||x||_2)
+  codes: bit-exact except coordinates within 1e-5 max(|x|, ||x||_2) of a separating breakpoint
+  top-k ids: recall vs oracle ids >= 0.99; matched distances within 1e-4 relative
+"""
+import math
+
+import numpy as np
+import pytest
+
+import datagen
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+P = pytest.importorskip("paper_2603_24920_b200")
+
+
+def _impls():
+    return [1]   # 0 (tcgen05) added with project_tc.cu
+
+
+@pytest.fixture(scope="module")
+def gpu_tiny(tiny):
+    c = tiny["cfg"]
+    return P.detlsh_build(tiny["X"], c.L, c.K, c.N_r, c.index_seed)
+
+
+@pytest.fixture(scope="module")
+def tiny_rmin(tiny, tiny_oracle):
+    c = tiny["cfg"]
+    return tiny_oracle.estimate_rmin(tiny["Qs"], c.k, c.c, c.beta)
+
+
+# ------------------------------------------------------------------ B0-B4
+def test_hash_family_bit_exact(gpu_tiny, tiny_oracle):
+    assert np.array_equal(gpu_tiny.A(), tiny_oracle.A())
+
+
+def test_sample_ids_exact(gpu_tiny, tiny_oracle):
+    assert np.array_equal(gpu_tiny.sample(), tiny_oracle.sample())
+
+
+@pytest.mark.parametrize("impl", _impls())
+def test_projection_tolerance(gpu_tiny, tiny_oracle, tiny, impl):
+    X = tiny["X"]
+    Pg = gpu_tiny.project(X, proj_impl=impl)
+    Po = tiny_oracle.P()
+    scale = np.maximum(np.abs(Po), np.linalg.norm(X.astype(np.float64), axis=1, keepdims=True))
+    rel = np.abs(Pg.astype(np.float64) - Po) / scale
+    print(f"impl {impl}: max rel {rel.max():.3e}  p99.9 {np.quantile(rel, 0.999):.3e}")
+    assert rel.max() <= 1e-4
+
+
+def test_breakpoints_from_oracle_samples_bit_exact(tiny_oracle):
+    """The device sort + AMB-5 gather on the oracle's own sample projections reproduces the
+    oracle's breakpoints exactly (integer-like work)."""
+    Ps = tiny_oracle.P()[tiny_oracle.sample()]
+    B = P.detlsh_breakpoints_from_samples(Ps, 256)
+    assert np.array_equal(B, tiny_oracle.breakpoints())
+
+
+def test_breakpoints_tolerance(gpu_tiny, tiny_oracle, tiny):
+    Bg, Bo = gpu_tiny.breakpoints(), tiny_oracle.breakpoints()
+    scale = np.median(np.linalg.norm(tiny["X"], axis=1))
+    assert np.abs(Bg.astype(np.float64) - Bo).max() <= 1e-4 * scale
+
+
+def _code_mismatch_ok(x, cg, co, b, tol):
+    lo, hi = min(cg, co), max(cg, co)
+    seps = b[lo + 1:hi + 1]           # breakpoints separating the two regions
+    return np.min(np.abs(seps.astype(np.float64) - x)) <= tol
+
+
+def test_codes_parity(gpu_tiny, tiny_oracle, tiny):
+    Cg, Co = gpu_tiny.codes(), tiny_oracle.codes()
+    Po, Bo = tiny_oracle.P(), tiny_oracle.breakpoints()
+    norms = np.linalg.norm(tiny["X"].astype(np.float64), axis=1)
+    bad = np.argwhere(Cg != Co)
+    for p, r in bad:
+        tol = 1e-5 * max(abs(float(Po[p, r])), norms[p])
+        assert _code_mismatch_ok(float(Po[p, r]), int(Cg[p, r]), int(Co[p, r]), Bo[r], tol), (p, r)
+    print(f"near-breakpoint code mismatches: {len(bad)} of {Cg.size}")
+    assert len(bad) <= 1e-3 * Cg.size
+
+
+# ------------------------------------------------------------------ B5/B6
+@pytest.mark.parametrize("max_size", [128, 7])
+def test_trees_from_oracle_codes_bit_exact(tiny_oracle, max_size):
+    codes = tiny_oracle.codes()
+    g = P.detlsh_build_from_codes(codes, 4, 16, 256, max_size=max_size)
+    for i in range(4):
+        o = O.Tree(codes[:, i * 16:(i + 1) * 16], 16, 256, max_size, builder=1).export()
+        t = g.tree(i)
+        for key in ("leaf_off", "perm", "lo", "hi", "bits"):
+            assert np.array_equal(t[key], o[key]), (i, key)
+
+
+def test_trees_duplicate_heavy_codes():
+    """Unsplittable (identical codes) and one-sided splits; small alphabets; K=4, N_r=16."""
+    rng = np.random.default_rng(11)
+    for alphabet, ms in [(2, 3), (4, 5), (16, 1)]:
+        codes = (rng.integers(0, alphabet, (3000, 8)) * (16 // alphabet)).astype(np.uint8)
+        g = P.detlsh_build_from_codes(codes, 2, 4, 16, max_size=ms)
+        for i in range(2):
+            o = O.Tree(codes[:, i * 4:(i + 1) * 4], 4, 16, ms, builder=1).export()
+            t = g.tree(i)
+            for key in ("leaf_off", "perm", "lo", "hi", "bits"):
+                assert np.array_equal(t[key], o[key]), (alphabet, i, key)
+
+
+def test_end_to_end_leaves(gpu_tiny, tiny_oracle):
+    """Points whose leaf differs between GPU and oracle trees (0 when codes agree)."""
+    Cg, Co = gpu_tiny.codes(), tiny_oracle.codes()
+    for i in range(4):
+        if not np.array_equal(Cg[:, i * 16:(i + 1) * 16], Co[:, i * 16:(i + 1) * 16]):
+            continue
+        t, o = gpu_tiny.tree(i), tiny_oracle.tree(i)
+        for key in ("leaf_off", "perm", "lo", "hi"):
+            assert np.array_equal(t[key], o[key])
+
+
+# ------------------------------------------------------------------ Q0-Q8
+def _recall(a, b):
+    return np.mean([len(set(a[q]) & set(b[q])) / a.shape[1] for q in range(a.shape[0])])
+
+
+def _dist_match(ig, dg, io, do):
+    for q in range(ig.shape[0]):
+        m = {i: d for i, d in zip(io[q], do[q])}
+        for i, d in zip(ig[q], dg[q]):
+            if i in m and np.isfinite(d):
+                assert abs(d - m[i]) <= 1e-4 * max(1e-30, m[i]) + 1e-30
+
+
+@pytest.mark.parametrize("mode", [P.MODE_CELL, P.MODE_RELAXED])
+def test_query_parity_tiny(gpu_tiny, tiny_oracle, tiny, tiny_rmin, mode):
+    c = tiny["cfg"]
+    ig, dg, sg = gpu_tiny.query(tiny["Q"], c.k, c.c, tiny_rmin, c.beta, opts=P.default_opts(mode=mode), stats=True)
+    io, do, so = tiny_oracle.query(tiny["Q"], c.k, c.c, tiny_rmin, c.beta, mode=mode)
+    rec = _recall(ig, io)
+    print(f"mode {mode}: recall vs oracle {rec:.4f}; reasons gpu {np.bincount(sg['reason'], minlength=3)} "
+          f"oracle {np.bincount(so['reason'], minlength=3)}; |S| gpu {sg['n_cand'].mean():.0f} oracle {so['n_cand'].mean():.0f}")
+    assert rec >= 0.99
+    _dist_match(ig, dg, io, do)
+    for q in range(len(ig)):   # ascending (dist, id)
+        assert all((dg[q, e], ig[q, e]) < (dg[q, e + 1], ig[q, e + 1]) for e in range(c.k - 1))
+    assert np.mean(sg["n_cand"] == so["n_cand"]) >= 0.9
+
+
+def test_query_exact_knn_special_case(tiny):
+    """beta >= 1 and a radius past every bound: S = D, exact kNN (numpy brute force)."""
+    X, Q = tiny["X"][:3000], tiny["Q"][:20]
+    g = P.detlsh_build(X, 4, 16, 256, 42)
+    ig, dg, st = g.query(Q, 10, 1.5, 1e9, 2.0, stats=True)
+    d2 = ((Q[:, None, :].astype(np.float64) - X[None]) ** 2).sum(-1)
+    ref = np.array([np.lexsort((np.arange(len(X)), row))[:10] for row in d2])
+    assert np.array_equal(ig, ref)
+    assert np.allclose(dg, np.sqrt(np.take_along_axis(d2, ref, 1)), rtol=1e-5)
+    assert np.all(st["reason"] == 1) and np.all(st["n_cand"] == 3000)
+
+
+def test_query_k_equals_n_and_self(tiny):
+    X = tiny["X"][:300]
+    g = P.detlsh_build(X, 4, 16, 256, 42, opts=P.default_opts(max_size=16))
+    ig, dg = g.query(X[[5, 77]], 300, 1.5, 1.0, 0.1)
+    d2 = ((X[[5, 77]][:, None, :].astype(np.float64) - X[None]) ** 2).sum(-1)
+    ref = np.array([np.lexsort((np.arange(300), row)) for row in d2])
+    assert np.array_equal(ig, ref)
+    ig, dg = g.query(X[[5, 77, 123]], 3, 1.5, 1e-3, 0.1)
+    assert ig[:, 0].tolist() == [5, 77, 123] and np.all(dg[:, 0] == 0)
+
+
+def test_query_round_cap(tiny):
+    g = P.detlsh_build(tiny["X"][:500], 4, 16, 256, 42)
+    ig, dg, st = g.query(tiny["Q"][:2], 5, 1.5, 1e-30, 0.1, stats=True)
+    assert np.all(st["reason"] == 2) and np.all(st["rounds"] == 64)
+    assert np.all(ig == -1) and np.all(np.isinf(dg))
+
+
+@pytest.mark.parametrize("n,d,L,K,N_r,ms", [(4097, 37, 2, 8, 16, 5), (1000, 100, 3, 12, 64, 32),
+                                             (5000, 128, 1, 32, 256, 128), (777, 24, 4, 4, 2, 9)])
+def test_ragged_shapes_parity(n, d, L, K, N_r, ms):
+    D = datagen.generate(1, n=n, nq=12)
+    X = np.ascontiguousarray(D["X"][:, :d])
+    Q = np.ascontiguousarray(D["Q"][:, :d])
+    g = P.detlsh_build(X, L, K, N_r, 7, opts=P.default_opts(max_size=ms, sample_frac=0.1))
+    o = O.Index(X, L, K, N_r, 7, max_size=ms, sample_frac=0.1)
+    assert np.array_equal(g.A(), o.A())
+    assert np.array_equal(g.sample(), o.sample())
+    Cg, Co = g.codes(), o.codes()
+    assert np.mean(Cg != Co) <= 1e-3
+    rmin = max(o.estimate_rmin(Q[:6], 5, 1.5, 0.1), 1e-3)   # r* can be 0 with N_r = 2
+    ig, dg = g.query(Q, 5, 1.5, rmin, 0.1)
+    io, do, _ = o.query(Q, 5, 1.5, rmin, 0.1)
+    assert _recall(ig, io) >= 0.95
+    if np.array_equal(Cg, Co):
+        for i in range(L):
+            t, ot = g.tree(i), o.tree(i)
+            for key in ("leaf_off", "perm", "lo", "hi", "bits"):
+                assert np.array_equal(t[key], ot[key])
+
+
+def test_device_buffers_and_determinism(tiny, gpu_tiny, tiny_rmin):
+    import torch
+    c = tiny["cfg"]
+    Qd = torch.from_numpy(tiny["Q"]).cuda()
+    ig, dg = gpu_tiny.query(Qd, c.k, c.c, tiny_rmin, c.beta)
+    ih, dh = gpu_tiny.query(tiny["Q"], c.k, c.c, tiny_rmin, c.beta)
+    assert np.array_equal(ig.cpu().numpy(), ih) and np.array_equal(dg.cpu().numpy(), dh)
+    Xd = torch.from_numpy(tiny["X"]).cuda()
+    g2 = P.detlsh_build(Xd, c.L, c.K, c.N_r, c.index_seed, opts=P.default_opts(borrow_data=1))
+    i2, d2 = g2.query(tiny["Q"], c.k, c.c, tiny_rmin, c.beta)
+    assert np.array_equal(i2, ih) and np.array_equal(d2, dh)
+    for _ in range(2):
+        i3, d3 = gpu_tiny.query(tiny["Q"], c.k, c.c, tiny_rmin, c.beta, opts=P.default_opts(query_batch=7))
+        assert np.array_equal(i3, ih) and np.array_equal(d3, dh)
+
+
+def test_errors_on_gpu(gpu_tiny, tiny):
+    with pytest.raises(P.DetlshError):
+        gpu_tiny.query(tiny["Q"], 0, 1.5, 1.0, 0.1)
+    with pytest.raises(P.DetlshError):
+        gpu_tiny.query(tiny["Q"], 5, 1.0, 1.0, 0.1)
+    bad = tiny["Q"][:3].copy()
+    bad[1, 3] = np.nan
+    with pytest.raises(P.DetlshError):
+        gpu_tiny.query(bad, 5, 1.5, 1.0, 0.1)
+    X = tiny["X"][:100].copy()
+    X[5, 5] = np.inf
+    with pytest.raises(P.DetlshError):
+        P.detlsh_build(X, 4, 16, 256, 1)
+    ig, dg = gpu_tiny.query(tiny["Q"][:0], 5, 1.5, 1.0, 0.1)
+    assert ig.shape == (0, 5)
+
+
+@pytest.mark.slow
+def test_config2_full_size_sampled_queries():
+    """configs[1] at full size (n = 1M, d = 256) in the bench launch configuration, checked
+    on 24 sampled queries the oracle answers one by one."""
+    D = datagen.generate(2, with_sample_queries=20)
+    c = D["cfg"]
+    o = O.Index(D["X"], c.L, c.K, c.N_r, c.index_seed)
+    rmin = o.estimate_rmin(D["Qs"], c.k, c.c, c.beta)
+    g = P.detlsh_build(D["X"], c.L, c.K, c.N_r, c.index_seed)
+    Cg, Co = g.codes(), o.codes()
+    print(f"cfg2 code mismatch fraction {np.mean(Cg != Co):.2e}")
+    assert np.mean(Cg != Co) <= 1e-4
+    sel = np.random.default_rng(5).choice(c.nq, 24, replace=False)
+    ig, dg = g.query(D["Q"], c.k, c.c, rmin, c.beta)       # full batch, as bench.py runs it
+    io, do, _ = o.query(D["Q"][sel], c.k, c.c, rmin, c.beta)
+    rec = _recall(ig[sel], io)
+    print(f"cfg2 recall vs oracle on 24 sampled queries: {rec:.4f}")
+    assert rec >= 0.99
+    _dist_match(ig[sel], dg[sel], io, do)

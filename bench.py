@@ -1,0 +1,354 @@
+#!/usr/bin/env python
+"""Benchmark of the DET-LSH hot path on B200 (contract: see DESIGN.md "Measurement").
+
+A step = one pass of the whole hot path over one batch of synthetic input:
+detlsh_build over the configuration's n points (B0-B6) + detlsh_query of its nq queries
+(Q0-Q8).  Inputs are device-resident before the timed region (X = 1.02 GB > L2, so no
+L2 flush is needed); timing uses CUDA events on the library's stream, max over ranks.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--impl reference]
+
+N > 1 runs under torchrun: points are sharded (strong scaling of the fixed config),
+breakpoints are global (C1 all-gather), every rank answers every query with its
+per-shard budget and the local top-k lists are all-gathered and merged (C2).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import datagen  # noqa: E402
+
+METRIC = "queries/s at recall@k>=0.9"
+
+
+def load_rmin(cid: int) -> float:
+    path = os.path.join(ROOT, "bench_configs.json")
+    data = json.load(open(path))
+    return float(data[str(cid)]["r_min"])
+
+
+def workload_desc(c) -> str:
+    return (f"configs[{c_index(c)}] {c.name}: n={c.n:,} d={c.d} fp32, nq={c.nq}, k={c.k}, L={c.L}, K={c.K}, "
+            f"N_r={c.N_r}, c={c.c}, beta={c.beta}")
+
+
+def c_index(c) -> int:
+    for i, v in datagen.CONFIGS.items():
+        if v == c:
+            return i - 1
+    return -1
+
+
+# ---------------------------------------------------------------- ground truth (harness)
+def exact_knn_sample(X: np.ndarray, Q: np.ndarray, k: int, sel: np.ndarray) -> np.ndarray:
+    """Exact kNN ids for Q[sel]: fp32 BLAS screening, fp64 re-rank, ties by id."""
+    norms = np.einsum("ij,ij->i", X, X, dtype=np.float64)
+    out = np.empty((len(sel), k), np.int64)
+    extra = k + 64
+    for s in range(0, len(sel), 50):
+        qs = Q[sel[s:s + 50]]
+        approx = norms[None, :] - 2.0 * (qs @ X.T).astype(np.float64)
+        cand = np.argpartition(approx, extra, axis=1)[:, :extra]
+        for r in range(len(qs)):
+            cid = cand[r]
+            d2 = ((X[cid].astype(np.float64) - qs[r].astype(np.float64)) ** 2).sum(1)
+            order = np.lexsort((cid, d2))[:k]
+            out[s + r] = cid[order]
+    return out
+
+
+def recall(ids: np.ndarray, gt: np.ndarray) -> float:
+    k = gt.shape[1]
+    return float(np.mean([len(set(ids[i].tolist()) & set(gt[i].tolist())) / k for i in range(len(gt))]))
+
+
+# ---------------------------------------------------------------- clocks sampler
+class Clocks:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                       "-lms", "100"], stdout=self.f, stderr=subprocess.DEVNULL)
+        except FileNotFoundError:
+            self.p = None
+
+    def stop(self) -> dict:
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.p.terminate()
+        self.p.wait()
+        self.f.flush()
+        rows = [r.split(",") for r in open(self.f.name).read().strip().splitlines() if r.strip()]
+        os.unlink(self.f.name)
+        sm = [float(r[1]) for r in rows if len(r) >= 9 and r[1].strip().replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if len(r) >= 9 and r[2].strip().replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows if len(r) >= 9 for i in range(4) if r[5 + i].strip() == "Active"})
+        load = [s for s in sm if s > 300] or sm
+        return {"sm_mhz": float(np.median(load)) if load else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ---------------------------------------------------------------- roofline models
+def peaks():
+    p = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else None
+    if p:
+        return p["hbm_gbs"], p["bf16_tflops"], p.get("bf16_tflops_sustained"), "measured (MEASURED_PEAKS.json)"
+    return 6650.0, 1590.0, 1400.0, "fallback (B200_PROFILING.md)"
+
+
+def kernel_bytes(name: str, c, steps: int, st, n_local: int, nq: int) -> float | None:
+    """Algorithmic bytes of all launches of `name` in the timed region.
+    `st` = per-query stats of one step (identical every step: the computation is deterministic)."""
+    d, LK, K = c.d, c.L * c.K, c.K
+    if name.startswith("k_verify"):
+        return float(steps) * float(st["n_cand"].sum()) * (4 * d + 4 + 4)   # row gather + id read + d2 write
+    if name.startswith("k_filter_mark"):
+        per = (st["leaves_tested"] * 2 * K + st["leaves_passed"] * 8 + st["points_tested"] * K
+               + st["points_passed"] * 12 + st["n_cand"] * 4)
+        return float(steps) * float(per.sum())
+    if name.startswith("k_project"):
+        return float(steps) * ((n_local + datagen_ns(c, n_local) + nq) * (4 * d + 4 * LK))
+    if name.startswith("k_encode"):
+        return float(steps) * n_local * LK * 5
+    return None
+
+
+def datagen_ns(c, n):
+    return min(n, max(int(np.ceil(c.sample_frac * n)), 32 * c.N_r))
+
+
+# ---------------------------------------------------------------- reference arm (the oracle)
+def run_reference(args, cfg):
+    from oracle import oracle as O
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    r_min = load_rmin(args.config)
+    D = datagen.generate(cfg)
+    X, Q = D["X"], D["Q"]
+    t0 = time.perf_counter()
+    ix = O.Index(X, cfg.L, cfg.K, cfg.N_r, cfg.index_seed, cfg.max_size, cfg.sample_frac)
+    build_s = time.perf_counter() - t0
+    per_step = args.ref_queries
+    rng = np.random.default_rng(0)
+    times = []
+    for s in range(args.warmup + args.steps):
+        sel = rng.choice(cfg.nq, per_step, replace=False)
+        t = time.perf_counter()
+        ix.query(Q[sel], cfg.k, cfg.c, r_min, cfg.beta)
+        if s >= args.warmup:
+            times.append(time.perf_counter() - t)
+    qps = per_step * len(times) / sum(times)
+    line = {"impl": "reference", "metric": METRIC, "value": qps, "unit": "queries/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * sum(times) / len(times),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": workload_desc(cfg), "r_min": r_min},
+            "cpu_baseline": {"value": qps, "unit": "queries/s", "cores": 1, "kind": "oracle",
+                             "sample": f"{per_step} random queries of the {cfg.nq} per step, index built once "
+                                       f"(oracle build {cfg.n / build_s:.0f} points/s, 1 core)"},
+            "e2e": {"value": qps, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline(cfg, X, Q, r_min, nqs: int) -> dict:
+    from oracle import oracle as O
+    t0 = time.perf_counter()
+    ix = O.Index(X, cfg.L, cfg.K, cfg.N_r, cfg.index_seed, cfg.max_size, cfg.sample_frac)
+    tb = time.perf_counter() - t0
+    sel = np.random.default_rng(1).choice(cfg.nq, nqs, replace=False)
+    t0 = time.perf_counter()
+    ix.query(Q[sel], cfg.k, cfg.c, r_min, cfg.beta)
+    tq = time.perf_counter() - t0
+    return {"value": nqs / tq, "unit": "queries/s", "cores": 1, "kind": "oracle",
+            "sample": f"oracle (single-thread fp64 C) full index build of all {cfg.n:,} points + {nqs} of the "
+                      f"{cfg.nq} queries", "build_points_per_s": cfg.n / tb, "seconds": tb + tq}
+
+
+# ---------------------------------------------------------------- our arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--ref-queries", type=int, default=4)
+    ap.add_argument("--cpu-queries", type=int, default=16)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--proj-impl", type=int, default=None)
+    ap.add_argument("--recall-queries", type=int, default=200)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+    cfg = datagen.CONFIGS[args.config]
+    if args.impl == "reference":
+        return run_reference(args, cfg)
+
+    import torch
+    import torch.distributed as dist
+    import paper_2603_24920_b200 as P
+    from paper_2603_24920_b200 import dist as PD
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    r_min = load_rmin(args.config)
+    Dd = datagen.generate(cfg)
+    X, Q = Dd["X"], Dd["Q"]
+    lo, hi = PD.shard_range(cfg.n, world, rank)
+    Xd = torch.from_numpy(X[lo:hi]).cuda()
+    Qd = torch.from_numpy(Q).cuda()
+    stream = torch.cuda.current_stream()
+    opts = P.default_opts(stream=stream.cuda_stream, borrow_data=1)
+    if args.proj_impl is not None:
+        opts.proj_impl = args.proj_impl
+    n_local = hi - lo
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def build():
+        if world > 1:
+            return PD.sharded_build(Xd, lo, cfg.n, cfg.L, cfg.K, cfg.N_r, cfg.index_seed, opts)
+        return P.detlsh_build(Xd, cfg.L, cfg.K, cfg.N_r, cfg.index_seed, opts=opts)
+
+    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+    results = {}
+
+    def step(timed: bool):
+        e0, e1, e2 = ev(), ev(), ev()
+        e0.record(stream)
+        idx = build()
+        e1.record(stream)
+        ids, dists, st = idx.query(Qd, cfg.k, cfg.c, r_min, cfg.beta, opts=opts, stats=True)
+        if world > 1:
+            ids, dists = PD.merge_shard_topk(ids, dists, cfg.k)
+        e2.record(stream)
+        results["ids"], results["stats"] = ids, st
+        idx.free()
+        return e0, e1, e2
+
+    for _ in range(args.warmup):
+        step(False)
+    torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    clk = Clocks(local)
+    clk.start()
+    time.sleep(0.3)
+    P.profile_reset()
+    P.profile_enable(True)
+    l0 = P.launch_count()
+    evs = [step(True) for _ in range(args.steps)]
+    torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    launches = P.launch_count() - l0
+    P.profile_enable(False)
+    prof = P.profile_read()
+    clocks = clk.stop()
+    build_ms = sum(a.elapsed_time(b) for a, b, _ in evs)
+    query_ms = sum(b.elapsed_time(c) for _, b, c in evs)
+    step_ms = sum(a.elapsed_time(c) for a, _, c in evs)
+    t = torch.tensor([build_ms, query_ms, step_ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    build_ms, query_ms, step_ms = t.tolist()
+
+    st = results["stats"]
+
+    # e2e through the public API with host (pinned) buffers: H2D of the queries and D2H of the results inside
+    Qh = torch.from_numpy(Q).pin_memory()
+    idh = torch.empty((cfg.nq, cfg.k), dtype=torch.int64).pin_memory()
+    dh = torch.empty((cfg.nq, cfg.k), dtype=torch.float32).pin_memory()
+    idx = build()
+    e2e_ms = []
+    for s in range(args.warmup + args.steps):
+        a, b = ev(), ev()
+        a.record(stream)
+        idx.query(Qh.numpy(), cfg.k, cfg.c, r_min, cfg.beta, opts=opts, out_ids=idh.numpy(), out_dists=dh.numpy())
+        b.record(stream)
+        b.synchronize()
+        if s >= args.warmup:
+            e2e_ms.append(a.elapsed_time(b))
+    idx.free()
+    te = torch.tensor([float(np.mean(e2e_ms))], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+
+    if rank == 0:
+        ids = results["ids"]
+        ids = ids.cpu().numpy() if torch.is_tensor(ids) else ids
+        sel = np.random.default_rng(2).choice(cfg.nq, min(args.recall_queries, cfg.nq), replace=False)
+        gt = exact_knn_sample(X, Q, cfg.k, sel)
+        rec = recall(ids[sel], gt)
+        hbm, bf16, bf16s, peak_src = peaks()
+        kern = {k: {"launches": v[0], "ms": round(v[1], 4)} for k, v in sorted(prof.items(), key=lambda kv: -kv[1][1])}
+        dom = max(prof.items(), key=lambda kv: kv[1][1])[0] if prof else None
+        roof = None
+        if dom is not None:
+            byts = kernel_bytes(dom, cfg, args.steps, st, n_local, cfg.nq)
+            ms = prof[dom][1]
+            if byts is not None:
+                ach = byts / (ms / 1e3) / 1e9
+                roof = {"kernel": dom, "bound": "hbm", "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s",
+                        "frac": round(ach / hbm, 4), "traffic": None, "peak_source": peak_src,
+                        "share_of_step": round(ms / step_ms, 4),
+                        "unit_of_work": "candidate (4d+8 B)" if dom.startswith("k_verify") else
+                        "per query: leaves x 2K + passed leaves x 8 + tested points x K + passing x 12 + new x 4 B"}
+        line = {
+            "metric": METRIC, "value": cfg.nq * args.steps / (query_ms / 1e3), "unit": "queries/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic",
+            "config": {"workload": workload_desc(cfg), "n": cfg.n, "d": cfg.d, "nq": cfg.nq, "k": cfg.k,
+                       "r_min": r_min, "parallelism": f"point-sharded x{world}",
+                       "l2": "no flush: X (1.02 GB at configs[1]) and the rebuilt index exceed L2 (126 MB)",
+                       "proj_impl": int(opts.proj_impl)},
+            "recall_at_k": rec, "recall_queries": int(len(sel)),
+            "query_ms_per_step": query_ms / args.steps,
+            "build": {"points_per_s": cfg.n * args.steps / (build_ms / 1e3), "ms_per_step": build_ms / args.steps},
+            "candidates_per_query": float(st["n_cand"].mean()),
+            "stop_reasons": np.bincount(st["reason"], minlength=3).tolist(),
+            "filter_counts_per_query": {k_: float(st[k_].mean()) for k_ in
+                                        ("leaves_tested", "leaves_passed", "points_tested", "points_passed")},
+            "roofline": roof,
+            "e2e": {"value": cfg.nq / (float(te.item()) / 1e3), "unit": "queries/s",
+                    "h2d_bytes_per_step": int(Q.nbytes), "d2h_bytes_per_step": int(cfg.nq * cfg.k * 12),
+                    "how": "detlsh_query with pinned host query/output buffers (copies inside the timed call)"},
+            "gpu_launches": int(launches), "clocks": clocks, "kernels": kern,
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_baseline(cfg, X, Q, r_min, args.cpu_queries)
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -63,6 +63,10 @@ typedef struct {
     int32_t pad;
     int64_t n_cand;      /* |S| at termination */
     double  r_final;     /* r of the last round */
+    int64_t leaves_tested;   /* leaf lower bounds evaluated (all rounds, all trees) */
+    int64_t leaves_passed;   /* leaves with LB <= eps r */
+    int64_t points_tested;   /* points of qualifying leaves examined */
+    int64_t points_passed;   /* points with cell LB <= eps r (before de-duplication) */
 } detlsh_query_stats;
 
 void detlsh_default_opts(detlsh_opts* opts);
@@ -176,6 +180,18 @@ detlsh_status detlsh_build_from_codes(const uint8_t* codes, int64_t n, int32_t L
 
 /* Number of kernels this library has launched in this process (evidence counter). */
 int64_t detlsh_launch_count(void);
+
+/* Per-kernel device time, measured with CUDA events recorded on each launch's stream while
+   enabled (used by bench.py for the live roofline).  read returns the number of kernels and
+   fills up to cap records (aggregated since the last reset). */
+typedef struct {
+    char    name[64];
+    int64_t launches;
+    double  total_ms;
+} detlsh_kernel_time;
+void    detlsh_profile_enable(int32_t on);
+void    detlsh_profile_reset(void);
+int32_t detlsh_profile_read(detlsh_kernel_time* out, int32_t cap);
 
 #ifdef __cplusplus
 }

@@ -69,6 +69,17 @@ void require_device() {
         cudaGetLastError();
         throw Error(DETLSH_ECUDA, "no CUDA device available");
     }
+    // Keep freed stream-ordered scratch in the device pool (no unmap/remap between calls).
+    int dev = 0;
+    DL_CUDA(cudaGetDevice(&dev));
+    static thread_local int configured = -1;
+    if (configured != dev) {
+        cudaMemPool_t pool;
+        DL_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+        uint64_t thr = UINT64_MAX;
+        DL_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+        configured = dev;
+    }
 }
 
 cudaStream_t stream_of(const detlsh_opts* o) { return o ? reinterpret_cast<cudaStream_t>(o->stream) : (cudaStream_t)0; }

@@ -36,13 +36,22 @@ struct Error : std::runtime_error {
     } while (0)
 
 extern std::atomic<int64_t> g_launches;
+extern std::atomic<int> g_profile;
+// Kernel timing (bench.py's live roofline): CUDA events recorded on the launch stream
+// around each launch while profiling is enabled (detlsh_profile_enable).
+void profile_begin(cudaStream_t st, const char* name, int* slot);
+void profile_end(cudaStream_t st, int slot);
 
 // Every kernel launch goes through this macro: counts launches (the evidence counter
-// behind detlsh_launch_count) and checks the launch error.
+// behind detlsh_launch_count), optionally times it, and checks the launch error.
 #define DL_LAUNCH(kernel, grid, block, smem, stream, ...)                                       \
     do {                                                                                       \
+        int _slot = -1;                                                                        \
+        if (::detlsh::g_profile.load(std::memory_order_relaxed))                               \
+            ::detlsh::profile_begin((stream), #kernel, &_slot);                                \
         kernel<<<(grid), (block), (smem), (stream)>>>(__VA_ARGS__);                            \
         ::detlsh::g_launches.fetch_add(1, std::memory_order_relaxed);                          \
+        if (_slot >= 0) ::detlsh::profile_end((stream), _slot);                                \
         DL_CUDA(cudaGetLastError());                                                           \
     } while (0)
 

@@ -37,6 +37,7 @@ struct QState {  // per query of a batch
     int32_t rounds;
     int32_t overflow;
     int32_t pad;
+    unsigned long long leaves_tested, leaves_passed, points_tested, points_passed;
 };
 
 struct TreeView {
@@ -66,6 +67,7 @@ __global__ void __launch_bounds__(FM_THREADS) k_filter_mark(TreeView tv, const f
     __shared__ int s_leaves[FM_CHUNK];
     __shared__ int s_nq;
     __shared__ unsigned long long s_new;
+    __shared__ unsigned long long s_ctr[4];   // leaves tested / passed, points tested / passed
     const int K = KT ? KT : tv.K;
     const int N_r = tv.N_r, LK = tv.L * K;
     const int q = act[blockIdx.x];
@@ -76,6 +78,8 @@ __global__ void __launch_bounds__(FM_THREADS) k_filter_mark(TreeView tv, const f
     int64_t cnt = qs[q].cnt;
     int status = ST_ACTIVE, trees = 0;
     const uint32_t lt = lanemask_lt();
+    if (threadIdx.x < 4) s_ctr[threadIdx.x] = 0;
+    uint32_t c_pt = 0, c_pp = 0;   // per-thread point counters
     for (int t = 0; t < tv.L; ++t) {
         // ---- LUT of tree t: D[j][s] = max(0, l_s - x, x - u_s)^2, cell s = (b_s, b_{s+1}]
         for (int i = threadIdx.x; i < K * N_r; i += FM_THREADS) {
@@ -126,6 +130,10 @@ __global__ void __launch_bounds__(FM_THREADS) k_filter_mark(TreeView tv, const f
             __syncthreads();
             // ---- point filter + mark, one warp per qualifying leaf
             const int nq = s_nq;
+            if (threadIdx.x == 0) {
+                s_ctr[0] += (unsigned long long)((le - base) < FM_CHUNK ? (le - base) : FM_CHUNK);
+                s_ctr[1] += (unsigned long long)nq;
+            }
             for (int qi = warp; qi < nq; qi += nwarps) {
                 const int l = s_leaves[qi];
                 const int64_t p0 = tv.leaf_off[l], p1 = tv.leaf_off[l + 1];
@@ -134,6 +142,7 @@ __global__ void __launch_bounds__(FM_THREADS) k_filter_mark(TreeView tv, const f
                     bool isnew = false;
                     uint32_t id = 0;
                     if (pos < p1) {
+                        ++c_pt;
                         bool pass = true;
                         if (mode == DETLSH_MODE_CELL) {
                             float acc = 0.f;
@@ -148,6 +157,7 @@ __global__ void __launch_bounds__(FM_THREADS) k_filter_mark(TreeView tv, const f
                             pass = acc <= rho2;
                         }
                         if (pass) {
+                            ++c_pp;
                             id = tv.perm[pos];
                             const uint32_t bit = 1u << (id & 31);
                             const uint32_t old = atomicOr(bm + (id >> 5), bit);
@@ -175,7 +185,20 @@ __global__ void __launch_bounds__(FM_THREADS) k_filter_mark(TreeView tv, const f
         __syncthreads();
         if (cnt >= budget) { status = ST_BUDGET; break; }   // Alg. 5 line 7
     }
+    for (int o = 16; o > 0; o >>= 1) {
+        c_pt += __shfl_xor_sync(0xffffffffu, c_pt, o);
+        c_pp += __shfl_xor_sync(0xffffffffu, c_pp, o);
+    }
+    if (lane == 0) {
+        atomicAdd(&s_ctr[2], (unsigned long long)c_pt);
+        atomicAdd(&s_ctr[3], (unsigned long long)c_pp);
+    }
+    __syncthreads();
     if (threadIdx.x == 0) {
+        qs[q].leaves_tested += s_ctr[0];
+        qs[q].leaves_passed += s_ctr[1];
+        qs[q].points_tested += s_ctr[2];
+        qs[q].points_passed += s_ctr[3];
         qs[q].cnt = cnt;
         qs[q].trees_last = trees;
         qs[q].rounds = round + 1;
@@ -493,6 +516,10 @@ __global__ void k_finalize(const QState* __restrict__ qs, const unsigned long lo
             o.pad = 0;
             o.n_cand = s.cnt;
             o.r_final = radii[max(0, s.rounds - 1)];
+            o.leaves_tested = (int64_t)s.leaves_tested;
+            o.leaves_passed = (int64_t)s.leaves_passed;
+            o.points_tested = (int64_t)s.points_tested;
+            o.points_passed = (int64_t)s.points_passed;
             stats[q] = o;
         }
     }
@@ -503,6 +530,7 @@ __global__ void k_init_batch(QState* __restrict__ qs, int* __restrict__ act, int
         QState s;
         s.cnt = 0; s.nver = 0; s.status = ST_ACTIVE; s.tk = 0; s.trees_last = 0; s.rounds = 0;
         s.overflow = 0; s.pad = 0;
+        s.leaves_tested = s.leaves_passed = s.points_tested = s.points_passed = 0;
         qs[q] = s;
         act[q] = q;
     }
@@ -584,8 +612,8 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
     tv.N_r = ix.N_r;
 
     const size_t lut_smem = sizeof(float) * (size_t)ix.K * ix.N_r;
-    auto fm = ix.K == 16 ? k_filter_mark<16> : k_filter_mark<0>;
-    DL_CUDA(cudaFuncSetAttribute(fm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lut_smem));
+    auto k_filter_mark_sel = ix.K == 16 ? k_filter_mark<16> : k_filter_mark<0>;
+    DL_CUDA(cudaFuncSetAttribute(k_filter_mark_sel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lut_smem));
     const int nv = (int)ceil_div(ix.ld / 4, 32);
     int vgrid = 148 * 8;
 
@@ -602,7 +630,7 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
             const double r = radii[m];
             const float rho2 = (float)((eps * r) * (eps * r));
             const float cr2 = (float)((a.c * r) * (a.c * r));
-            DL_LAUNCH(fm, (unsigned)na, FM_THREADS, lut_smem, st, tv, Qpb, cur, rho2, budget, a.mode, s_bm.as<uint32_t>(),
+            DL_LAUNCH(k_filter_mark_sel, (unsigned)na, FM_THREADS, lut_smem, st, tv, Qpb, cur, rho2, budget, a.mode, s_bm.as<uint32_t>(),
                       nwords, s_cand.as<uint32_t>(), cap, s_qs.as<QState>(), m);
             DL_LAUNCH(k_verify_prep, 1, 1024, 0, st, cur, na, s_qs.as<QState>(), choff, work);
             switch (nv) {

@@ -34,13 +34,21 @@ class detlsh_opts(C.Structure):
                 ("proj_impl", C.c_int32), ("mem_budget", C.c_int64)]
 
 
+class detlsh_kernel_time(C.Structure):
+    _fields_ = [("name", C.c_char * 64), ("launches", C.c_int64), ("total_ms", C.c_double)]
+
+
 class detlsh_query_stats(C.Structure):
     _fields_ = [("rounds", C.c_int32), ("trees_last", C.c_int32), ("reason", C.c_int32),
-                ("pad", C.c_int32), ("n_cand", C.c_int64), ("r_final", C.c_double)]
+                ("pad", C.c_int32), ("n_cand", C.c_int64), ("r_final", C.c_double),
+                ("leaves_tested", C.c_int64), ("leaves_passed", C.c_int64), ("points_tested", C.c_int64),
+                ("points_passed", C.c_int64)]
 
 
 STATS_DTYPE = np.dtype([("rounds", np.int32), ("trees_last", np.int32), ("reason", np.int32),
-                        ("pad", np.int32), ("n_cand", np.int64), ("r_final", np.float64)])
+                        ("pad", np.int32), ("n_cand", np.int64), ("r_final", np.float64),
+                        ("leaves_tested", np.int64), ("leaves_passed", np.int64), ("points_tested", np.int64),
+                        ("points_passed", np.int64)])
 
 _lib = None
 
@@ -80,6 +88,9 @@ def lib():
         "detlsh_debug_export": (i32, [P, i32, i32, P, sz, C.POINTER(sz)]),
         "detlsh_build_from_codes": (i32, [P, i64, i32, i32, i32, O, P]),
         "detlsh_launch_count": (i64, []),
+        "detlsh_profile_enable": (None, [i32]),
+        "detlsh_profile_reset": (None, []),
+        "detlsh_profile_read": (i32, [P, i32]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -132,6 +143,22 @@ def default_opts(**kw) -> detlsh_opts:
 
 def launch_count() -> int:
     return int(lib().detlsh_launch_count())
+
+
+def profile_enable(on: bool = True):
+    lib().detlsh_profile_enable(1 if on else 0)
+
+
+def profile_reset():
+    lib().detlsh_profile_reset()
+
+
+def profile_read() -> dict:
+    """{kernel name: (launches, total_ms)} since the last reset."""
+    n = lib().detlsh_profile_read(None, 0)
+    arr = (detlsh_kernel_time * max(n, 1))()
+    n = lib().detlsh_profile_read(C.cast(arr, C.c_void_p), n)
+    return {arr[i].name.decode(): (int(arr[i].launches), float(arr[i].total_ms)) for i in range(n)}
 
 
 def detlsh_params(K: int, L: int, c: float):

@@ -124,7 +124,7 @@ def kernel_bytes(name: str, c, steps: int, st, n_local: int, nq: int) -> float |
     d, LK, K = c.d, c.L * c.K, c.K
     if name.startswith("k_verify"):
         return float(steps) * float(st["n_cand"].sum()) * (4 * d + 4 + 4)   # row gather + id read + d2 write
-    if name.startswith("k_filter_mark"):
+    if name.startswith("k_range_filter"):
         per = (st["leaves_tested"] * 2 * K + st["leaves_passed"] * 8 + st["points_tested"] * K
                + st["points_passed"] * 12 + st["n_cand"] * 4)
         return float(steps) * float(per.sum())

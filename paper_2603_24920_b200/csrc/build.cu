@@ -553,6 +553,49 @@ __global__ void k_gather_rows_strided(const float* __restrict__ src, int64_t src
     }
 }
 
+// Query tiles: runs of consecutive leaves of one tree whose
+// first points fall in the same window of kTilePoints positions.  A tile holds at most
+// kTilePoints leaves, and every leaf but its last starts inside the window.
+__global__ void k_tile_flags(const uint32_t* __restrict__ leaf_off, int64_t nl, int64_t n, int tp,
+                             uint32_t* __restrict__ flags) {
+    for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < nl;
+         l += (int64_t)gridDim.x * blockDim.x) {
+        if (l == 0) { flags[l] = 1; continue; }
+        const uint32_t a = leaf_off[l - 1], b = leaf_off[l];
+        flags[l] = (a / n != b / n || (a % n) / tp != (b % n) / tp) ? 1u : 0u;
+    }
+}
+
+__global__ void k_tile_write(const uint32_t* __restrict__ flags, const uint32_t* __restrict__ idx, int64_t nl,
+                             uint32_t* __restrict__ tile_leaf) {
+    for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < nl;
+         l += (int64_t)gridDim.x * blockDim.x)
+        if (flags[l]) tile_leaf[idx[l]] = (uint32_t)l;
+}
+
+// Per point (tree order): index of its leaf within its query tile (u16; a tile holds at most
+// kTilePoints leaves).
+__global__ void k_point_tile_leaf(const uint32_t* __restrict__ leaf_off, const uint32_t* __restrict__ tile_leaf,
+                                  int64_t ntiles, int64_t nl, uint16_t* __restrict__ ptl) {
+    for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < nl;
+         l += (int64_t)gridDim.x * blockDim.x) {
+        int64_t lo = 0, hi = ntiles - 1;    // last tile with tile_leaf <= l
+        while (lo < hi) {
+            const int64_t mid = (lo + hi + 1) >> 1;
+            if (tile_leaf[mid] <= (uint32_t)l) lo = mid; else hi = mid - 1;
+        }
+        const uint16_t v = (uint16_t)(l - tile_leaf[lo]);
+        for (uint32_t p = leaf_off[l]; p < leaf_off[l + 1]; ++p) ptl[p] = v;
+    }
+}
+
+__global__ void k_tree_tiles(const uint32_t* __restrict__ idx, const unsigned long long* __restrict__ leaf_begin,
+                             int L, uint32_t ntiles, unsigned long long* __restrict__ tile_begin) {
+    const int t = threadIdx.x;
+    if (t < L) tile_begin[t] = idx[leaf_begin[t]];
+    if (t == L) tile_begin[t] = ntiles;
+}
+
 int grid_for(int64_t work, int threads, int cap = 148 * 16) {
     int64_t g = ceil_div(std::max<int64_t>(work, 1), threads);
     return (int)std::min<int64_t>(g, cap);
@@ -728,6 +771,31 @@ static bool build_trees_try(Index& ix, const uint8_t* d_EP, int64_t leaf_factor,
     DL_CUDA(cudaStreamSynchronize(st));
     ix.tree_leaf_begin.assign(begin.begin(), begin.end());
     ix.tree_leaf_begin[L] = nl;
+    // query tiles
+    {
+        Scratch s_tf(st, sizeof(uint32_t) * (size_t)(2 * nl + 2));
+        uint32_t* tf = s_tf.as<uint32_t>();
+        uint32_t* tidx = tf + nl;
+        uint32_t* ntiles_d = tidx + nl;
+        DL_LAUNCH(k_tile_flags, grid_for(nl, 256), 256, 0, st, ix.leaf_off.as<uint32_t>(), nl, n, kTilePoints, tf);
+        exclusive_scan_u32(tf, tidx, nl, ntiles_d, st);
+        const int64_t ntiles = d2h(ntiles_d, st);
+        ix.tile_leaf.alloc(sizeof(uint32_t) * (size_t)(ntiles + 1));
+        DL_LAUNCH(k_tile_write, grid_for(nl, 256), 256, 0, st, tf, tidx, nl, ix.tile_leaf.as<uint32_t>());
+        const uint32_t last = (uint32_t)nl;
+        DL_CUDA(cudaMemcpyAsync(ix.tile_leaf.as<uint32_t>() + ntiles, &last, sizeof(uint32_t), cudaMemcpyHostToDevice, st));
+        DL_CUDA(cudaMemcpyAsync(s_begin.p, begin.data(), sizeof(unsigned long long) * (L + 1), cudaMemcpyHostToDevice, st));
+        Scratch s_tb(st, sizeof(unsigned long long) * (size_t)(L + 1));
+        DL_LAUNCH(k_tree_tiles, 1, 64, 0, st, tidx, s_begin.as<unsigned long long>(), (int)L, (uint32_t)ntiles,
+                  s_tb.as<unsigned long long>());
+        ix.point_tile_leaf.alloc(sizeof(uint16_t) * (size_t)total);
+        DL_LAUNCH(k_point_tile_leaf, grid_for(nl, 256), 256, 0, st, ix.leaf_off.as<uint32_t>(), ix.tile_leaf.as<uint32_t>(),
+                  ntiles, nl, ix.point_tile_leaf.as<uint16_t>());
+        std::vector<unsigned long long> tb(L + 1);
+        DL_CUDA(cudaMemcpyAsync(tb.data(), s_tb.p, sizeof(unsigned long long) * (L + 1), cudaMemcpyDeviceToHost, st));
+        DL_CUDA(cudaStreamSynchronize(st));
+        ix.tree_tile_begin.assign(tb.begin(), tb.end());
+    }
     return true;
 }
 

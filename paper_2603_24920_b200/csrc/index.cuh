@@ -27,6 +27,8 @@ struct DevBuf {
     template <class T> T* as() const { return static_cast<T*>(p); }
 };
 
+constexpr int kTilePoints = 1024;   // query-tile window (points)
+
 struct Index {
     // shape / parameters
     int64_t n = 0;          // points in this index (shard)
@@ -52,6 +54,9 @@ struct Index {
     DevBuf leaf_lo, leaf_hi;// [nl_total][K] u8 symbol range of each leaf box
     DevBuf leaf_bits;       // [nl_total][K] u8 bits per dim of each leaf
     std::vector<int64_t> tree_leaf_begin;  // [L+1] leaf index range of each tree (host copy)
+    DevBuf tile_leaf;       // [ntiles+1] first leaf of each query tile (tree-major; see build.cu)
+    std::vector<int64_t> tree_tile_begin;  // [L+1] tile index range of each tree (host copy)
+    DevBuf point_tile_leaf; // [L*n] u16: leaf of each point (tree order) relative to its tile
 
     int64_t nl_total() const { return tree_leaf_begin.empty() ? 0 : tree_leaf_begin.back(); }
 };

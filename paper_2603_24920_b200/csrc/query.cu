@@ -1,13 +1,14 @@
 // query.cu -- batched c^2-k-ANN (Alg. 5) on sm_100a.
 //
 // Per round r = r_min c^m (host loop; one D2H of the active count per round):
-//  k_filter_mark  one CTA per active query walks the L trees in order (Alg. 5 lines 3-8):
-//                 per tree a 16x256 LUT of squared region distances (Fig. dist, P:581-584;
-//                 AMB-7) in shared memory; warps test leaf boxes (leaf LB = sum_j D_j[clamp(
-//                 s_x, lo_j, hi_j)]), then the points of qualifying leaves (cell LB = sum_j
+//  k_build_lut    once per query batch: per (query, tree, dim) the 256-entry table of squared
+//                 region distances (Fig. dist; AMB-7) and the query's symbol.
+//  k_range_filter per tree t (trees in order, Alg. 5 lines 3-8): CTAs = groups of 4 queries x
+//                 stripes of tiles; warps test leaf boxes (leaf LB = sum_j D_j[clamp(s_x,
+//                 lo_j, hi_j)]) then the points of qualifying leaves (cell LB = sum_j
 //                 D_j[code_j], AMB-12), OR them into the query's bitmap (de-duplicated union
-//                 S <- S u S_i, line 6) and append first-time ids; after each tree the budget
-//                 test |S| >= ceil(beta n)+k (line 7, AMB-15/17).
+//                 S <- S u S_i, line 6) and append first-time ids.
+//  k_tree_end     after tree t: budget test |S| >= ceil(beta n)+k (line 7, AMB-15/17).
 //  k_verify       exact squared L2 of the new candidates: one warp per row, float4 gathers,
 //                 warp-shuffle reduction (lines 8/10).
 //  k_topk         per query: radix-select the k smallest (d2, id) keys of old top-k u new,
@@ -37,7 +38,6 @@ struct QState {  // per query of a batch
     int32_t rounds;
     int32_t overflow;
     int32_t pad;
-    unsigned long long leaves_tested, leaves_passed, points_tested, points_passed;
 };
 
 struct TreeView {
@@ -52,158 +52,291 @@ struct TreeView {
     int L, K, N_r;
 };
 
-constexpr int FM_THREADS = 512;
-constexpr int FM_LEAVES_PER_THREAD = 4;
-constexpr int FM_CHUNK = FM_THREADS * FM_LEAVES_PER_THREAD;
-
-template <int KT>
-__global__ void __launch_bounds__(FM_THREADS) k_filter_mark(TreeView tv, const float* __restrict__ Qp,
-                                                            const int* __restrict__ act, float rho2,
-                                                            int64_t budget, int mode, uint32_t* __restrict__ bitmap,
-                                                            int64_t nwords, uint32_t* __restrict__ cand, int64_t cap,
-                                                            QState* __restrict__ qs, int round) {
-    extern __shared__ float D[];                // [K][N_r] squared region distances
-    __shared__ int s_sx[32];
-    __shared__ int s_leaves[FM_CHUNK];
-    __shared__ int s_nq;
-    __shared__ unsigned long long s_new;
-    __shared__ unsigned long long s_ctr[4];   // leaves tested / passed, points tested / passed
-    const int K = KT ? KT : tv.K;
-    const int N_r = tv.N_r, LK = tv.L * K;
-    const int q = act[blockIdx.x];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = FM_THREADS / 32;
-    const float* qp = Qp + (int64_t)q * LK;
-    uint32_t* bm = bitmap + (int64_t)q * nwords;
-    uint32_t* cl = cand + (int64_t)q * cap;
-    int64_t cnt = qs[q].cnt;
-    int status = ST_ACTIVE, trees = 0;
-    const uint32_t lt = lanemask_lt();
-    if (threadIdx.x < 4) s_ctr[threadIdx.x] = 0;
-    uint32_t c_pt = 0, c_pp = 0;   // per-thread point counters
-    for (int t = 0; t < tv.L; ++t) {
-        // ---- LUT of tree t: D[j][s] = max(0, l_s - x, x - u_s)^2, cell s = (b_s, b_{s+1}]
-        for (int i = threadIdx.x; i < K * N_r; i += FM_THREADS) {
-            const int j = i / N_r, s = i - j * N_r;
-            const float* b = tv.B + (int64_t)(t * K + j) * (N_r + 1);
-            const float x = qp[t * K + j];
-            const float l = s >= 1 ? b[s] : -INFINITY;
-            const float u = s <= N_r - 2 ? b[s + 1] : INFINITY;
-            const float v = fmaxf(0.f, fmaxf(l - x, x - u));
-            D[i] = v * v;
-        }
-        if (threadIdx.x < K) {     // the query's own symbol s_x (AMB-6)
-            const float* b = tv.B + (int64_t)(t * K + threadIdx.x) * (N_r + 1);
-            const float x = qp[t * K + threadIdx.x];
+// ---- per-batch LUTs: D[q][t][j][s] = max(0, l_s - x, x - u_s)^2 for cell s = (b_s, b_{s+1}],
+//      l_0 = -inf, u_{N_r-1} = +inf (Fig. dist; AMB-7), and the query's own symbol
+//      s_x (AMB-6).  The LUT depends only on the projected query, not on the radius.
+__global__ void k_build_lut(const float* __restrict__ Qp, int nqb, int LK, int N_r, const float* __restrict__ B,
+                            float* __restrict__ lut, uint8_t* __restrict__ sx) {
+    const int64_t total = (int64_t)nqb * LK * N_r;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int s = (int)(i % N_r);
+        const int64_t qr = i / N_r;                 // q * LK + r
+        const int r = (int)(qr % LK);
+        const float* b = B + (int64_t)r * (N_r + 1);
+        const float x = Qp[qr];
+        const float l = s >= 1 ? b[s] : -INFINITY;
+        const float u = s <= N_r - 2 ? b[s + 1] : INFINITY;
+        const float v = fmaxf(0.f, fmaxf(l - x, x - u));
+        lut[i] = v * v;
+        if (s == 0) {
             int pos = 0;
-            for (int s = N_r >> 1; s > 0; s >>= 1) {
-                const int idx = pos + s;               // breakpoint b_idx, idx in 1..N_r
-                pos += (idx <= N_r - 1 && b[idx] < x) ? s : 0;
+            for (int st = N_r >> 1; st > 0; st >>= 1) {
+                const int idx = pos + st;
+                pos += (idx <= N_r - 1 && b[idx] < x) ? st : 0;
             }
-            s_sx[threadIdx.x] = pos;
+            sx[qr] = (uint8_t)pos;
         }
-        if (threadIdx.x == 0) { s_nq = 0; s_new = 0; }
-        __syncthreads();
-        const int64_t lb = (int64_t)tv.tree_begin[t], le = (int64_t)tv.tree_begin[t + 1];
-        for (int64_t base = lb; base < le; base += FM_CHUNK) {
-            // ---- leaf filter: leaf LB^2 = sum_j D_j[clamp(s_x, lo_j, hi_j)] <= rho^2
-#pragma unroll
-            for (int i = 0; i < FM_LEAVES_PER_THREAD; ++i) {
-                const int64_t l = base + i * FM_THREADS + threadIdx.x;
-                if (l < le) {
-                    float acc = 0.f;
-                    if (KT == 16) {
-                        const uint4 lo4 = *reinterpret_cast<const uint4*>(tv.lo + l * 16);
-                        const uint4 hi4 = *reinterpret_cast<const uint4*>(tv.hi + l * 16);
-                        const uint32_t lw[4] = {lo4.x, lo4.y, lo4.z, lo4.w}, hw[4] = {hi4.x, hi4.y, hi4.z, hi4.w};
-#pragma unroll
-                        for (int j = 0; j < 16; ++j) {
-                            const int lo = (lw[j >> 2] >> ((j & 3) * 8)) & 255, hi = (hw[j >> 2] >> ((j & 3) * 8)) & 255;
-                            acc += D[j * N_r + min(max(s_sx[j], lo), hi)];
-                        }
-                    } else {
-                        for (int j = 0; j < K; ++j)
-                            acc += D[j * N_r + min(max(s_sx[j], (int)tv.lo[l * K + j]), (int)tv.hi[l * K + j])];
-                    }
-                    if (acc <= rho2) s_leaves[atomicAdd(&s_nq, 1)] = (int)l;
-                }
-            }
-            __syncthreads();
-            // ---- point filter + mark, one warp per qualifying leaf
-            const int nq = s_nq;
-            if (threadIdx.x == 0) {
-                s_ctr[0] += (unsigned long long)((le - base) < FM_CHUNK ? (le - base) : FM_CHUNK);
-                s_ctr[1] += (unsigned long long)nq;
-            }
-            for (int qi = warp; qi < nq; qi += nwarps) {
-                const int l = s_leaves[qi];
-                const int64_t p0 = tv.leaf_off[l], p1 = tv.leaf_off[l + 1];
-                for (int64_t pb = p0; pb < p1; pb += 32) {
-                    const int64_t pos = pb + lane;
-                    bool isnew = false;
-                    uint32_t id = 0;
-                    if (pos < p1) {
-                        ++c_pt;
-                        bool pass = true;
-                        if (mode == DETLSH_MODE_CELL) {
-                            float acc = 0.f;
-                            if (KT == 16) {
-                                const uint4 c4 = *reinterpret_cast<const uint4*>(tv.tcodes + pos * 16);
-                                const uint32_t cw[4] = {c4.x, c4.y, c4.z, c4.w};
-#pragma unroll
-                                for (int j = 0; j < 16; ++j) acc += D[j * N_r + ((cw[j >> 2] >> ((j & 3) * 8)) & 255)];
-                            } else {
-                                for (int j = 0; j < K; ++j) acc += D[j * N_r + tv.tcodes[pos * K + j]];
-                            }
-                            pass = acc <= rho2;
-                        }
-                        if (pass) {
-                            ++c_pp;
-                            id = tv.perm[pos];
-                            const uint32_t bit = 1u << (id & 31);
-                            const uint32_t old = atomicOr(bm + (id >> 5), bit);
-                            isnew = !(old & bit);
-                        }
-                    }
-                    const uint32_t nb = __ballot_sync(0xffffffffu, isnew);
-                    if (nb) {
-                        unsigned long long slot0 = 0;
-                        if (lane == 0) slot0 = atomicAdd(&s_new, (unsigned long long)__popc(nb));
-                        slot0 = __shfl_sync(0xffffffffu, slot0, 0);
-                        if (isnew) {
-                            const int64_t at = cnt + (int64_t)slot0 + __popc(nb & lt);
-                            if (at < cap) cl[at] = id;
-                        }
-                    }
-                }
-            }
-            __syncthreads();
-            if (threadIdx.x == 0) s_nq = 0;
-            __syncthreads();
+    }
+}
+
+// ---- range filter of one tree (Alg. 3 at radius eps*r, Alg. 5 lines 5-6), batched:
+//      CTA (group of G active queries) x (stripe of tiles).  Per tile: leaf lower bounds of
+//      every (leaf, query) -- sum_j D_j[clamp(s_x, lo_j, hi_j)] <= rho^2 -- then the cell
+//      bound of every point of a qualifying leaf (AMB-12; a point of a pruned leaf cannot
+//      pass since leaf LB <= cell LB), OR-marking the per-query bitmap and appending first-
+//      time ids.  Codes of a tile are read once for all G queries.
+constexpr int RF_THREADS = 256;
+constexpr int RF_G = 4;          // queries per CTA: one float4 LUT entry holds the G values
+
+struct RFArgs {
+    const uint8_t* tcodes;      // tree t: [n][K]
+    const uint16_t* ptl;        // tree t: [n] leaf within tile
+    const uint32_t* perm;       // tree t: [n]
+    const uint32_t* leaf_off;   // global positions
+    const uint8_t* lo;          // [nl_total][K]
+    const uint8_t* hi;
+    const uint32_t* tile_leaf;  // [ntiles+1]
+    int64_t tile_begin, tile_end;
+    int64_t pos_base;           // t * n
+    const float* lut;           // [Qb][L][K][N_r]
+    const uint8_t* sx;          // [Qb][L][K]
+    const int* act;
+    int na;
+    const QState* qs;
+    uint32_t* bitmap;           // [Qb][nwords] current union S (OR-marked, no return)
+    int64_t nwords;
+    float rho2;
+    int t, L, K, N_r, mode;
+    unsigned long long* ctr;    // [Qb][4] filter counters
+};
+
+template <int KT, int NRT>
+__global__ void __launch_bounds__(RF_THREADS, 3) k_range_filter(RFArgs a) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int K = KT ? KT : a.K;
+    const int N_r = NRT ? NRT : a.N_r;
+    float4* s_lut = reinterpret_cast<float4*>(smem);                                   // [K][N_r] x G
+    uint32_t* s_loff = reinterpret_cast<uint32_t*>(s_lut + K * N_r);                   // [kTilePoints+2]
+    uint32_t* s_lq = s_loff + kTilePoints + 2;                                         // [kTilePoints+1] G bytes
+    __shared__ int s_q[RF_G];
+    __shared__ uint8_t s_sx[RF_G][32];
+    __shared__ unsigned int s_ctr[RF_G][4];
+    __shared__ int s_active_mask;
+
+    const int lane = threadIdx.x & 31;
+    // ---- the query group and its LUTs, interleaved so one 16-byte load serves all G queries
+    if (threadIdx.x < RF_G) {
+        const int gi = blockIdx.x * RF_G + threadIdx.x;
+        int q = -1;
+        if (gi < a.na) {
+            q = a.act[gi];
+            if (a.qs[q].status != ST_ACTIVE) q = -1;       // stopped at an earlier tree (line 7)
         }
-        cnt += (int64_t)s_new;
-        trees = t + 1;
-        __syncthreads();
-        if (cnt >= budget) { status = ST_BUDGET; break; }   // Alg. 5 line 7
-    }
-    for (int o = 16; o > 0; o >>= 1) {
-        c_pt += __shfl_xor_sync(0xffffffffu, c_pt, o);
-        c_pp += __shfl_xor_sync(0xffffffffu, c_pp, o);
-    }
-    if (lane == 0) {
-        atomicAdd(&s_ctr[2], (unsigned long long)c_pt);
-        atomicAdd(&s_ctr[3], (unsigned long long)c_pp);
+        s_q[threadIdx.x] = q;
+        for (int c = 0; c < 4; ++c) s_ctr[threadIdx.x][c] = 0;
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-        qs[q].leaves_tested += s_ctr[0];
-        qs[q].leaves_passed += s_ctr[1];
-        qs[q].points_tested += s_ctr[2];
-        qs[q].points_passed += s_ctr[3];
-        qs[q].cnt = cnt;
-        qs[q].trees_last = trees;
-        qs[q].rounds = round + 1;
-        if (cnt > cap) qs[q].overflow = 1;
-        if (status != ST_ACTIVE) qs[q].status = status;
+        int m = 0;
+        for (int g = 0; g < RF_G; ++g) m |= (s_q[g] >= 0) << g;
+        s_active_mask = m;
+    }
+    __syncthreads();
+    const int amask = s_active_mask;
+    if (amask == 0) return;
+    {
+        const float* src[RF_G];
+#pragma unroll
+        for (int g = 0; g < RF_G; ++g)
+            src[g] = s_q[g] >= 0 ? a.lut + ((int64_t)s_q[g] * a.L + a.t) * K * N_r : nullptr;
+        for (int i = threadIdx.x; i < K * N_r; i += RF_THREADS) {
+            float v[RF_G];
+#pragma unroll
+            for (int g = 0; g < RF_G; ++g) v[g] = src[g] ? src[g][i] : INFINITY;   // inactive: never passes
+            s_lut[i] = make_float4(v[0], v[1], v[2], v[3]);
+        }
+        if (threadIdx.x < K) {
+#pragma unroll
+            for (int g = 0; g < RF_G; ++g)
+                s_sx[g][threadIdx.x] = s_q[g] >= 0 ? a.sx[((int64_t)s_q[g] * a.L + a.t) * K + threadIdx.x] : 0;
+        }
+    }
+    __syncthreads();
+    const float rho2 = a.rho2;
+    const float* s_lutf = reinterpret_cast<const float*>(s_lut);
+    uint32_t c_lt = 0, c_lp = 0, c_pt[RF_G], c_pp[RF_G];   // leaf counters summed over the group
+#pragma unroll
+    for (int g = 0; g < RF_G; ++g) c_pt[g] = c_pp[g] = 0;
+
+    for (int64_t tile = a.tile_begin + blockIdx.y; tile < a.tile_end; tile += gridDim.y) {
+        const uint32_t lb = a.tile_leaf[tile], le = a.tile_leaf[tile + 1];
+        const int nlt = (int)(le - lb);
+        const uint32_t P0 = a.leaf_off[lb], P1 = a.leaf_off[le];
+        for (int i = threadIdx.x; i <= nlt; i += RF_THREADS) s_loff[i] = a.leaf_off[lb + i] - P0;
+        __syncthreads();
+        // ---- leaf lower bounds (Alg. 3 pruning, Fig. dist): one thread per (leaf, query)
+        uint8_t* s_lqb = reinterpret_cast<uint8_t*>(s_lq);
+        for (int i = threadIdx.x; i < nlt * RF_G; i += RF_THREADS) {
+            const int li = i / RF_G, g = i - li * RF_G;
+            const int64_t l = (int64_t)lb + li;
+            float lacc = 0.f;
+            if (KT == 16) {
+                const uint4 lo4 = *reinterpret_cast<const uint4*>(a.lo + l * 16);
+                const uint4 hi4 = *reinterpret_cast<const uint4*>(a.hi + l * 16);
+#pragma unroll
+                for (int w = 0; w < 4; ++w) {
+                    const uint32_t lw = w == 0 ? lo4.x : w == 1 ? lo4.y : w == 2 ? lo4.z : lo4.w;
+                    const uint32_t hw = w == 0 ? hi4.x : w == 1 ? hi4.y : w == 2 ? hi4.z : hi4.w;
+#pragma unroll
+                    for (int b = 0; b < 4; ++b) {
+                        const int j = w * 4 + b;
+                        const int lo_ = (lw >> (8 * b)) & 255, hi_ = (hw >> (8 * b)) & 255;
+                        lacc += s_lutf[(j * N_r + min(max((int)s_sx[g][j], lo_), hi_)) * RF_G + g];
+                    }
+                }
+            } else {
+                for (int j = 0; j < K; ++j) {
+                    const int lo_ = a.lo[l * K + j], hi_ = a.hi[l * K + j];
+                    lacc += s_lutf[(j * N_r + min(max((int)s_sx[g][j], lo_), hi_)) * RF_G + g];
+                }
+            }
+            const bool ok = lacc <= rho2 && ((amask >> g) & 1);
+            s_lqb[i] = ok ? 1 : 0;
+            c_lt += (amask >> g) & 1;
+            c_lp += ok;
+        }
+        __syncthreads();
+        // ---- points of the tile: cell lower bounds (AMB-12), OR-marking the query bitmaps
+        const uint32_t np = P1 - P0;
+        for (uint32_t pb = 0; pb < np; pb += RF_THREADS) {
+            const uint32_t pl = pb + threadIdx.x;
+            uint32_t m = 0;
+            if (pl < np) {
+                const uint32_t x = s_lq[a.ptl[(int64_t)P0 + pl - a.pos_base]];   // G flag bytes -> G bits
+                m = (x & 1u) | ((x >> 7) & 2u) | ((x >> 14) & 4u) | ((x >> 21) & 8u);
+            }
+            if (__ballot_sync(0xffffffffu, m != 0) == 0) continue;    // whole warp pruned by leaf LBs
+            const int64_t pos = (int64_t)P0 + pl - a.pos_base;
+            float acc[RF_G];
+#pragma unroll
+            for (int g = 0; g < RF_G; ++g) acc[g] = 0.f;
+            if (m && a.mode == DETLSH_MODE_CELL) {
+                // terms summed in j order, as in the leaf bound, so leaf LB <= cell LB in fp32
+                if (KT == 16) {
+                    const uint4 c4 = *reinterpret_cast<const uint4*>(a.tcodes + pos * 16);
+#pragma unroll 1
+                    for (int w = 0; w < 4; ++w) {      // 4 codes per 32-bit word, j = 4w + b
+                        const uint32_t word = w == 0 ? c4.x : w == 1 ? c4.y : w == 2 ? c4.z : c4.w;
+                        const float4* row = s_lut + (w * 4) * N_r;
+#pragma unroll
+                        for (int b = 0; b < 4; ++b) {
+                            const float4 v = row[b * N_r + ((word >> (8 * b)) & 255u)];
+                            acc[0] += v.x; acc[1] += v.y; acc[2] += v.z; acc[3] += v.w;
+                        }
+                    }
+                } else {
+                    for (int j = 0; j < K; ++j) {
+                        const float4 v = s_lut[j * N_r + a.tcodes[pos * K + j]];
+                        acc[0] += v.x; acc[1] += v.y; acc[2] += v.z; acc[3] += v.w;
+                    }
+                }
+            }
+            uint32_t id = 0;
+            bool have_id = false;
+#pragma unroll
+            for (int g = 0; g < RF_G; ++g) {
+                const bool mine = (m >> g) & 1;
+                const bool pass = mine && (a.mode != DETLSH_MODE_CELL || acc[g] <= rho2);
+                c_pt[g] += mine;
+                c_pp[g] += pass;
+                if (pass) {
+                    if (!have_id) { id = a.perm[pos]; have_id = true; }
+                    atomicOr(a.bitmap + (int64_t)s_q[g] * a.nwords + (id >> 5), 1u << (id & 31));  // RED.OR
+                }
+            }
+        }
+        __syncthreads();
+    }
+    // ---- counters
+    {
+        uint32_t v[1 + 3 * RF_G];
+        v[0] = c_lt;
+#pragma unroll
+        for (int g = 0; g < RF_G; ++g) { v[1 + g] = c_lp; v[1 + RF_G + g] = c_pt[g]; v[1 + 2 * RF_G + g] = c_pp[g]; }
+#pragma unroll
+        for (int i = 0; i < 1 + 3 * RF_G; ++i)
+            for (int o = 16; o > 0; o >>= 1) v[i] += __shfl_xor_sync(0xffffffffu, v[i], o);
+        if (lane == 0) {
+#pragma unroll
+            for (int g = 0; g < RF_G; ++g) {   // leaf counts are per group: attributed evenly
+                atomicAdd(&s_ctr[g][0], v[0] / max(1, __popc(amask)));
+                atomicAdd(&s_ctr[g][1], v[1 + g] / max(1, __popc(amask)));
+                atomicAdd(&s_ctr[g][2], v[1 + RF_G + g]);
+                atomicAdd(&s_ctr[g][3], v[1 + 2 * RF_G + g]);
+            }
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x < RF_G && s_q[threadIdx.x] >= 0) {
+        unsigned long long* c = a.ctr + (int64_t)s_q[threadIdx.x] * 4;
+        for (int i = 0; i < 4; ++i) atomicAdd(c + i, (unsigned long long)s_ctr[threadIdx.x][i]);
+    }
+}
+
+// After tree t: the first-time members of S (bits set now but not in `prev`) are appended to
+// the query's candidate list and `prev` catches up; |S| is the list length (S <- S u S_i,
+// Alg. 5 line 6, de-duplicated by the bitmap).  Grid: (active queries) x (word chunks).
+constexpr int CN_WORDS = 4096;
+__global__ void __launch_bounds__(256) k_collect_new(const int* __restrict__ act, QState* __restrict__ qs,
+                                                     const uint32_t* __restrict__ cur, uint32_t* __restrict__ prev,
+                                                     int64_t nwords, uint32_t* __restrict__ cand, int64_t cap) {
+    const int q = act[blockIdx.x];
+    if (qs[q].status != ST_ACTIVE) return;
+    const uint32_t* c = cur + (int64_t)q * nwords;
+    uint32_t* p = prev + (int64_t)q * nwords;
+    uint32_t* cl = cand + (int64_t)q * cap;
+    const int lane = threadIdx.x & 31;
+    const int64_t w0 = (int64_t)blockIdx.y * CN_WORDS, w1 = min(w0 + CN_WORDS, nwords);
+    for (int64_t wb = w0; wb < w1; wb += 256) {
+        const int64_t w = wb + threadIdx.x;
+        uint32_t nb = 0;
+        if (w < w1) {
+            const uint32_t cv = c[w], pv = p[w];
+            nb = cv & ~pv;
+            if (nb) p[w] = cv;
+        }
+        const uint32_t cntb = __popc(nb);
+        uint32_t x = cntb;                       // warp inclusive scan of counts
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        const uint32_t tot = __shfl_sync(0xffffffffu, x, 31);
+        if (tot == 0) continue;
+        unsigned long long base = 0;
+        if (lane == 31) base = atomicAdd(reinterpret_cast<unsigned long long*>(&qs[q].cnt), (unsigned long long)tot);
+        base = __shfl_sync(0xffffffffu, base, 31);
+        int64_t at = (int64_t)base + x - cntb;
+        while (nb) {
+            const int b = __ffs(nb) - 1;
+            nb &= nb - 1;
+            if (at < cap) cl[at] = (uint32_t)(w * 32 + b);
+            ++at;
+        }
+    }
+}
+
+// After tree t: the budget test |S| >= ceil(beta n) + k (Alg. 5 line 7, AMB-15/17).
+__global__ void k_tree_end(const int* __restrict__ act, int na, QState* __restrict__ qs, int t, int round,
+                           int64_t budget, int64_t cap) {
+    for (int a_ = blockIdx.x * blockDim.x + threadIdx.x; a_ < na; a_ += gridDim.x * blockDim.x) {
+        QState* s = &qs[act[a_]];
+        if (s->status != ST_ACTIVE) continue;
+        s->trees_last = t + 1;
+        s->rounds = round + 1;
+        if (s->cnt > cap) s->overflow = 1;
+        if (s->cnt >= budget) s->status = ST_BUDGET;
     }
 }
 
@@ -492,7 +625,8 @@ __global__ void k_compact(const int* __restrict__ act, int na, const QState* __r
     if (threadIdx.x == 0) *n_out = s_n;
 }
 
-__global__ void k_finalize(const QState* __restrict__ qs, const unsigned long long* __restrict__ topk, int nqb, int k,
+__global__ void k_finalize(const QState* __restrict__ qs, const unsigned long long* __restrict__ ctr,
+                           const unsigned long long* __restrict__ topk, int nqb, int k,
                            int64_t id_offset, const double* __restrict__ radii, int64_t* __restrict__ out_ids,
                            float* __restrict__ out_d, detlsh_query_stats* __restrict__ stats) {
     const int64_t total = (int64_t)nqb * k;
@@ -516,10 +650,10 @@ __global__ void k_finalize(const QState* __restrict__ qs, const unsigned long lo
             o.pad = 0;
             o.n_cand = s.cnt;
             o.r_final = radii[max(0, s.rounds - 1)];
-            o.leaves_tested = (int64_t)s.leaves_tested;
-            o.leaves_passed = (int64_t)s.leaves_passed;
-            o.points_tested = (int64_t)s.points_tested;
-            o.points_passed = (int64_t)s.points_passed;
+            o.leaves_tested = (int64_t)ctr[q * 4 + 0];
+            o.leaves_passed = (int64_t)ctr[q * 4 + 1];
+            o.points_tested = (int64_t)ctr[q * 4 + 2];
+            o.points_passed = (int64_t)ctr[q * 4 + 3];
             stats[q] = o;
         }
     }
@@ -530,7 +664,6 @@ __global__ void k_init_batch(QState* __restrict__ qs, int* __restrict__ act, int
         QState s;
         s.cnt = 0; s.nver = 0; s.status = ST_ACTIVE; s.tk = 0; s.trees_last = 0; s.rounds = 0;
         s.overflow = 0; s.pad = 0;
-        s.leaves_tested = s.leaves_passed = s.points_tested = s.points_passed = 0;
         qs[q] = s;
         act[q] = q;
     }
@@ -560,7 +693,7 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
     }
 
     // batch size from the memory budget: bitmap + candidate list + distances per query
-    const int64_t per_q = nwords * 4 + cap * 8 + (int64_t)k * 8 + 64;
+    const int64_t per_q = nwords * 8 + cap * 8 + (int64_t)k * 8 + (int64_t)LK * (ix.N_r * 4 + 1) + 96;
     int64_t budget_bytes = a.mem_budget;
     if (budget_bytes <= 0) {
         size_t fr = 0, tot = 0;
@@ -571,7 +704,8 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
     qb = std::min<int64_t>({qb, nq, 65535});
     DL_REQUIRE(qb >= 1, "not enough device memory for one query");
 
-    Scratch s_bm(st, sizeof(uint32_t) * (size_t)(qb * nwords));
+    Scratch s_bm(st, sizeof(uint32_t) * (size_t)(2 * qb * nwords));   // current union + previous
+    Scratch s_ctr(st, sizeof(unsigned long long) * (size_t)(4 * qb));
     Scratch s_cand(st, sizeof(uint32_t) * (size_t)(qb * cap));
     Scratch s_d2(st, sizeof(float) * (size_t)(qb * cap));
     Scratch s_tk(st, sizeof(unsigned long long) * (size_t)(qb * k));
@@ -611,9 +745,29 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
     tv.K = ix.K;
     tv.N_r = ix.N_r;
 
-    const size_t lut_smem = sizeof(float) * (size_t)ix.K * ix.N_r;
-    auto k_filter_mark_sel = ix.K == 16 ? k_filter_mark<16> : k_filter_mark<0>;
-    DL_CUDA(cudaFuncSetAttribute(k_filter_mark_sel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lut_smem));
+    // per-batch LUTs
+    Scratch s_lut(st, sizeof(float) * (size_t)(qb * LK * ix.N_r));
+    Scratch s_sx(st, (size_t)(qb * LK));
+    const size_t rf_smem = sizeof(float) * (size_t)RF_G * ix.K * ix.N_r + sizeof(uint32_t) * (kTilePoints + 2) +
+                           sizeof(uint32_t) * (kTilePoints + 1);
+    auto k_range_filter_sel = (ix.K == 16 && ix.N_r == 256) ? k_range_filter<16, 256> : k_range_filter<0, 0>;
+    DL_CUDA(cudaFuncSetAttribute(k_range_filter_sel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rf_smem));
+    RFArgs ra;
+    ra.leaf_off = ix.leaf_off.as<uint32_t>();
+    ra.lo = ix.leaf_lo.as<uint8_t>();
+    ra.hi = ix.leaf_hi.as<uint8_t>();
+    ra.tile_leaf = ix.tile_leaf.as<uint32_t>();
+    ra.lut = s_lut.as<float>();
+    ra.sx = s_sx.as<uint8_t>();
+    ra.qs = s_qs.as<QState>();
+    ra.bitmap = s_bm.as<uint32_t>();
+    ra.nwords = nwords;
+    ra.ctr = s_ctr.as<unsigned long long>();
+    uint32_t* bm_prev = s_bm.as<uint32_t>() + qb * nwords;
+    ra.L = ix.L;
+    ra.K = ix.K;
+    ra.N_r = ix.N_r;
+    ra.mode = a.mode;
     const int nv = (int)ceil_div(ix.ld / 4, 32);
     int vgrid = 148 * 8;
 
@@ -621,8 +775,11 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
         const int nqb = (int)std::min<int64_t>(qb, nq - q0);
         const float* Qb = d_Q + q0 * q_ld;
         const float* Qpb = s_qp.as<float>() + q0 * LK;
-        DL_CUDA(cudaMemsetAsync(s_bm.p, 0, sizeof(uint32_t) * (size_t)(nqb * nwords), st));
+        DL_CUDA(cudaMemsetAsync(s_bm.p, 0, sizeof(uint32_t) * (size_t)(2 * qb * nwords), st));
+        DL_CUDA(cudaMemsetAsync(s_ctr.p, 0, sizeof(unsigned long long) * (size_t)(4 * qb), st));
         DL_LAUNCH(k_init_batch, (unsigned)ceil_div(nqb, 256), 256, 0, st, s_qs.as<QState>(), act, nqb);
+        DL_LAUNCH(k_build_lut, (unsigned)std::min<int64_t>(ceil_div((int64_t)nqb * LK * ix.N_r, 256), 148 * 32), 256, 0,
+                  st, Qpb, nqb, (int)LK, ix.N_r, ix.B.as<float>(), s_lut.as<float>(), s_sx.as<uint8_t>());
         int na = nqb;
         int* cur = act;
         int* nxt = act2;
@@ -630,8 +787,26 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
             const double r = radii[m];
             const float rho2 = (float)((eps * r) * (eps * r));
             const float cr2 = (float)((a.c * r) * (a.c * r));
-            DL_LAUNCH(k_filter_mark_sel, (unsigned)na, FM_THREADS, lut_smem, st, tv, Qpb, cur, rho2, budget, a.mode, s_bm.as<uint32_t>(),
-                      nwords, s_cand.as<uint32_t>(), cap, s_qs.as<QState>(), m);
+            for (int t = 0; t < ix.L; ++t) {
+                ra.tcodes = ix.tcodes.as<uint8_t>() + (int64_t)t * n * ix.K;
+                ra.perm = ix.perm.as<uint32_t>() + (int64_t)t * n;
+                ra.ptl = ix.point_tile_leaf.as<uint16_t>() + (int64_t)t * n;
+                ra.pos_base = (int64_t)t * n;
+                ra.tile_begin = ix.tree_tile_begin[t];
+                ra.tile_end = ix.tree_tile_begin[t + 1];
+                ra.act = cur;
+                ra.na = na;
+                ra.rho2 = rho2;
+                ra.t = t;
+                const int groups = (int)ceil_div(na, RF_G);
+                const int64_t ntiles = ra.tile_end - ra.tile_begin;
+                const int stripes = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, ceil_div(148 * 8, groups)));
+                DL_LAUNCH(k_range_filter_sel, dim3((unsigned)groups, (unsigned)stripes), RF_THREADS, rf_smem, st, ra);
+                DL_LAUNCH(k_collect_new, dim3((unsigned)na, (unsigned)ceil_div(nwords, CN_WORDS)), 256, 0, st, cur,
+                          s_qs.as<QState>(), s_bm.as<uint32_t>(), bm_prev, nwords, s_cand.as<uint32_t>(), cap);
+                DL_LAUNCH(k_tree_end, (unsigned)ceil_div(na, 256), 256, 0, st, cur, na, s_qs.as<QState>(), t, m,
+                          budget, cap);
+            }
             DL_LAUNCH(k_verify_prep, 1, 1024, 0, st, cur, na, s_qs.as<QState>(), choff, work);
             switch (nv) {
                 case 1: DL_LAUNCH(k_verify<1>, vgrid, 256, 0, st, ix.Xp, ix.ld, Qb, cur, na, s_qs.as<QState>(), choff, work,
@@ -655,7 +830,7 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
             std::swap(cur, nxt);
         }
         DL_LAUNCH(k_finalize, (unsigned)std::min<int64_t>(ceil_div((int64_t)nqb * k, 256), 148 * 16), 256, 0, st,
-                  s_qs.as<QState>(), s_tk.as<unsigned long long>(), nqb, k, ix.id_offset, s_radii.as<double>(),
+                  s_qs.as<QState>(), s_ctr.as<unsigned long long>(), s_tk.as<unsigned long long>(), nqb, k, ix.id_offset, s_radii.as<double>(),
                   d_ids + q0 * k, d_dists + q0 * k, d_stats ? d_stats + q0 : nullptr);
     }
 }

@@ -25,11 +25,9 @@ void project_rows(const Index& ix, const float* d_X, int64_t ld, int64_t m, floa
                   int* d_nonfinite, cudaStream_t st) {
     DL_REQUIRE(ld == ix.ld, "projection row stride mismatch");
     if (m <= 0) return;
-    if (proj_impl == 0) {
-        if (!project_rows_tc(ix, d_X, ld, m, d_P, d_nonfinite, st))
-            throw Error(DETLSH_EINVAL, "tcgen05 projection does not support this shape (use proj_impl=1)");
-        return;
-    }
+    // proj_impl 0: tensor cores (tcgen05) for every shape whose hash matrix fits in shared
+    // memory; other shapes (and proj_impl 1) use the CUDA-core kernel.
+    if (proj_impl == 0 && project_rows_tc(ix, d_X, ld, m, d_P, d_nonfinite, st)) return;
     project_rows_simt(ix, d_X, ld, m, d_P, d_nonfinite, st);
 }
 
@@ -154,7 +152,7 @@ void detlsh_default_opts(detlsh_opts* o) {
     o->query_batch = 0;
     o->stream = 0;
     o->borrow_data = 0;
-    o->proj_impl = 1;   /* TODO(tcgen05): default to 0 once project_tc.cu lands */
+    o->proj_impl = 0;
     o->mem_budget = 0;
 }
 

@@ -1,8 +1,328 @@
-// project_tc.cu -- tcgen05 (5th-gen tensor core) projection, in progress.
+// project_tc.cu -- P = X A^T on the 5th-generation tensor cores (tcgen05, kind::tf32),
+// the projection of every point onto the L*K Gaussian directions (Eq. 1 P:192-196, P:296;
+// Alg. 5 line 4 P:431 for queries).
+//
+// Precision: A is TF32-exact by construction (AMB-1), so P = X A^T needs only X split into
+// hi + lo:  the tensor core reads an fp32 operand as TF32 by dropping the low 13 mantissa
+// bits, so MMA(x) = MMA(trunc(x)), and lo = x - trunc(x) (exact in fp32) carries the rest:
+// P ~= trunc(x).A + trunc(lo).A with |error| <~ 2^-20 ||x|| ||a||  ("2xTF32").
+//
+// Kernel (persistent, one CTA per SM, 8 warps, tiles of 128 rows):
+//   warp 0      TMA producer: X k-blocks [128 rows x 32 fp32] (SWIZZLE_128B) into a ring
+//               of stages; the whole (L*K_pad x ld) hash matrix once (resident in smem).
+//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer (M=128, N=L*K_pad, K=8):
+//               per k-block 4 MMAs on x and 4 on lo, accumulating in TMEM; tcgen05.commit
+//               frees the stage and, after the last k-block, hands the tile to the epilogue.
+//   warps 2-3   converters: lo = x - trunc_tf32(x) into a twin buffer of the same swizzled
+//               layout, fence.proxy.async, arrive.
+//   warps 4-7   epilogue: tcgen05.ld (32x32b) of the double-buffered accumulator, rows to P.
+#include <cuda.h>
+
 #include "index.cuh"
 
 namespace detlsh {
 
-bool project_rows_tc(const Index&, const float*, int64_t, int64_t, float*, int*, cudaStream_t) { return false; }
+namespace {
+
+constexpr int TC_M = 128;           // rows per tile (UMMA M)
+constexpr int TC_KB = 32;           // fp32 per k-block (= 128 B, one swizzle row)
+constexpr int TC_THREADS = 256;
+constexpr int TC_STAGE_BYTES = TC_M * TC_KB * 4;   // 16 KB
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    const uint32_t a = smem_u32(bar);
+    uint32_t done = 0;
+    while (!done) {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(done)
+            : "r"(a), "r"(parity)
+            : "memory");
+    }
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+            smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+        : "memory");
+}
+// Shared-memory matrix descriptor, K-major, 128-byte swizzle: rows of 128 B, 8-row groups
+// 1024 B apart (SBO), LBO unused (1), descriptor version 1 (sm_100).
+__device__ __forceinline__ uint64_t desc_sw128(uint32_t saddr) {
+    return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
+           ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                         uint32_t accumulate) {
+    asm volatile(
+        "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+        " tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
+    uint32_t r[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+struct TcShape {
+    int64_t m;        // rows
+    int ld;           // row stride (floats), padded columns are zero
+    int nkb;          // k-blocks = ceil(ld / 32)
+    int LK, npad;     // output columns, padded to a multiple of 16
+    int stages;
+    uint32_t tmem_cols;
+};
+
+__global__ void __launch_bounds__(TC_THREADS, 1)
+    k_project_tc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmA, TcShape sh,
+                 float* __restrict__ P, int* __restrict__ nonfinite) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    // 1024-byte alignment of every swizzled buffer
+    unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const int S = sh.stages;
+    unsigned char* sB = base;                                            // nkb x [npad][128 B]
+    unsigned char* sX = sB + (size_t)sh.nkb * sh.npad * 128;              // S x 16 KB
+    unsigned char* sL = sX + (size_t)S * TC_STAGE_BYTES;                  // S x 16 KB (lo parts)
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sL + (size_t)S * TC_STAGE_BYTES);
+    uint64_t* full = bars;              // [S] TMA -> converters, MMA
+    uint64_t* conv = bars + S;          // [S] converters -> MMA
+    uint64_t* empty = bars + 2 * S;     // [S] MMA commit -> producer
+    uint64_t* tfull = bars + 3 * S;     // [2] MMA commit -> epilogue
+    uint64_t* tempty = bars + 3 * S + 2;// [2] epilogue -> MMA
+    uint64_t* bfull = bars + 3 * S + 4; // hash matrix loaded
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * S + 5);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t ntiles = (sh.m + TC_M - 1) / TC_M;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < S; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&conv[s], 64);
+            mbar_init(&empty[s], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&tfull[b], 1);
+            mbar_init(&tempty[b], 128);
+        }
+        mbar_init(bfull, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {   // TMEM allocation (whole warp), base column written to smem
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(sh.tmem_cols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            // the hash matrix, once
+            mbar_expect_tx(bfull, (uint32_t)(sh.nkb * sh.npad * 128));
+            for (int kb = 0; kb < sh.nkb; ++kb) tma_load_2d(sB + (size_t)kb * sh.npad * 128, &tmA, bfull, kb * TC_KB, 0);
+            int s = 0;
+            uint32_t ph = 0;
+            for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+                for (int kb = 0; kb < sh.nkb; ++kb) {
+                    mbar_wait(&empty[s], ph ^ 1);
+                    mbar_expect_tx(&full[s], TC_STAGE_BYTES);
+                    tma_load_2d(sX + (size_t)s * TC_STAGE_BYTES, &tmX, &full[s], kb * TC_KB, (int)(tile * TC_M));
+                    if (++s == S) { s = 0; ph ^= 1; }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(sh.npad >> 3) << 17) |
+                                   ((uint32_t)(TC_M >> 4) << 24);
+            mbar_wait(bfull, 0);
+            int s = 0;
+            uint32_t ph = 0;
+            int buf = 0;
+            uint32_t tph = 0;
+            for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+                mbar_wait(&tempty[buf], tph ^ 1);          // epilogue released this accumulator
+                tc_fence_after();
+                const uint32_t d_tmem = tmem_base + (uint32_t)(buf * sh.npad);
+                for (int kb = 0; kb < sh.nkb; ++kb) {
+                    mbar_wait(&full[s], ph);
+                    mbar_wait(&conv[s], ph);
+                    tc_fence_after();
+                    const uint32_t ax = smem_u32(sX + (size_t)s * TC_STAGE_BYTES);
+                    const uint32_t al = smem_u32(sL + (size_t)s * TC_STAGE_BYTES);
+                    const uint32_t bb = smem_u32(sB + (size_t)kb * sh.npad * 128);
+#pragma unroll
+                    for (int k = 0; k < TC_KB / 8; ++k) {        // K = 8 tf32 per MMA = 32 bytes
+                        const uint64_t bd = desc_sw128(bb + k * 32);
+                        mma_tf32(d_tmem, desc_sw128(ax + k * 32), bd, idesc, (kb | k) ? 1u : 0u);
+                        mma_tf32(d_tmem, desc_sw128(al + k * 32), bd, idesc, 1u);
+                    }
+                    mma_commit(&empty[s]);                   // stage free once these MMAs complete
+                    if (++s == S) { s = 0; ph ^= 1; }
+                }
+                mma_commit(&tfull[buf]);                     // accumulator ready
+                if (++buf == 2) { buf = 0; tph ^= 1; }
+            }
+        }
+    } else if (warp < 4) {
+        // converters: lo = x - trunc_tf32(x), same swizzled offsets
+        const int t = threadIdx.x - 64;
+        int s = 0;
+        uint32_t ph = 0;
+        bool bad = false;
+        for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+            for (int kb = 0; kb < sh.nkb; ++kb) {
+                mbar_wait(&full[s], ph);
+                const float4* src = reinterpret_cast<const float4*>(sX + (size_t)s * TC_STAGE_BYTES);
+                float4* dst = reinterpret_cast<float4*>(sL + (size_t)s * TC_STAGE_BYTES);
+#pragma unroll 4
+                for (int i = t; i < TC_STAGE_BYTES / 16; i += 64) {
+                    const float4 x = src[i];
+                    float4 lo;
+                    lo.x = x.x - __uint_as_float(__float_as_uint(x.x) & 0xFFFFE000u);
+                    lo.y = x.y - __uint_as_float(__float_as_uint(x.y) & 0xFFFFE000u);
+                    lo.z = x.z - __uint_as_float(__float_as_uint(x.z) & 0xFFFFE000u);
+                    lo.w = x.w - __uint_as_float(__float_as_uint(x.w) & 0xFFFFE000u);
+                    bad |= !(isfinite(x.x) && isfinite(x.y) && isfinite(x.z) && isfinite(x.w));
+                    dst[i] = lo;
+                }
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                mbar_arrive(&conv[s]);
+                if (++s == S) { s = 0; ph ^= 1; }
+            }
+        }
+        if (bad) atomicOr(nonfinite, 1);
+    } else {
+        // epilogue: TMEM -> registers -> P rows
+        const int ew = warp - 4;                           // TMEM lane quarter
+        const int row_in_tile = ew * 32 + lane;
+        int buf = 0;
+        uint32_t tph = 0;
+        for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+            mbar_wait(&tfull[buf], tph);
+            tc_fence_after();
+            const int64_t row = tile * TC_M + row_in_tile;
+            const uint32_t taddr = tmem_base + (uint32_t)(buf * sh.npad) + ((uint32_t)(ew * 32) << 16);
+            for (int c0 = 0; c0 < sh.npad; c0 += 16) {
+                float v[16];
+                tmem_ld16(taddr + c0, v);
+                if (row < sh.m) {
+                    float* out = P + row * sh.LK + c0;
+                    if (c0 + 16 <= sh.LK && (sh.LK & 3) == 0) {
+#pragma unroll
+                        for (int i = 0; i < 16; i += 4)
+                            *reinterpret_cast<float4*>(out + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+                    } else {
+                        for (int i = 0; i < 16 && c0 + i < sh.LK; ++i) out[i] = v[i];
+                    }
+                }
+            }
+            tc_fence_before();
+            mbar_arrive(&tempty[buf]);
+            if (++buf == 2) { buf = 0; tph ^= 1; }
+        }
+    }
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(sh.tmem_cols));
+    }
+}
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        DL_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+        if (!p || q != cudaDriverEntryPointSuccess) throw Error(DETLSH_ECUDA, "cuTensorMapEncodeTiled unavailable");
+        fn = reinterpret_cast<EncodeTiledFn>(p);
+    }
+    return fn;
+}
+
+void make_map(CUtensorMap* map, const float* ptr, int64_t rows, int ld, int box_rows) {
+    const cuuint64_t dims[2] = {(cuuint64_t)ld, (cuuint64_t)rows};
+    const cuuint64_t strides[1] = {(cuuint64_t)ld * 4};
+    const cuuint32_t box[2] = {(cuuint32_t)TC_KB, (cuuint32_t)box_rows};
+    const cuuint32_t estr[2] = {1, 1};
+    CUresult r = encode_fn()(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(ptr), dims, strides, box, estr,
+                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw Error(DETLSH_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+}
+
+}  // namespace
+
+// Returns false when the shape does not fit this kernel (resident hash matrix too large).
+bool project_rows_tc(const Index& ix, const float* d_X, int64_t ld, int64_t m, float* d_P, int* d_nonfinite,
+                     cudaStream_t st) {
+    if (m <= 0) return true;
+    TcShape sh;
+    sh.m = m;
+    sh.ld = (int)ld;
+    sh.nkb = (int)ceil_div(ld, TC_KB);
+    sh.LK = ix.LK;
+    sh.npad = (int)round_up(ix.LK, 16);
+    if (sh.npad > 256) return false;
+    const size_t bbytes = (size_t)sh.nkb * sh.npad * 128;
+    const size_t fixed = 1024 /*align*/ + 256 /*barriers*/;
+    const size_t budget = 227 * 1024;
+    if (bbytes + fixed + 2 * 2 * TC_STAGE_BYTES > budget) return false;
+    sh.stages = (int)std::min<size_t>(6, (budget - bbytes - fixed) / (2 * TC_STAGE_BYTES));
+    uint32_t cols = 32;
+    while (cols < (uint32_t)(2 * sh.npad)) cols <<= 1;
+    sh.tmem_cols = cols;
+    const size_t smem = bbytes + (size_t)sh.stages * 2 * TC_STAGE_BYTES + fixed;
+    CUtensorMap mx, ma;
+    make_map(&mx, d_X, m, (int)ld, TC_M);
+    make_map(&ma, ix.A.as<float>(), ix.LK, (int)ld, sh.npad);
+    static size_t configured = 0;
+    if (configured < smem) {
+        DL_CUDA(cudaFuncSetAttribute(k_project_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        configured = smem;
+    }
+    int dev = 0, nsm = 148;
+    DL_CUDA(cudaGetDevice(&dev));
+    DL_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    const int64_t ntiles = ceil_div(m, TC_M);
+    const int grid = (int)std::min<int64_t>(ntiles, nsm);
+    DL_LAUNCH(k_project_tc, grid, TC_THREADS, smem, st, mx, ma, sh, d_P, d_nonfinite);
+    return true;
+}
 
 }  // namespace detlsh

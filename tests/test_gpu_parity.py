@@ -20,7 +20,7 @@ P = pytest.importorskip("paper_2603_24920_b200")
 
 
 def _impls():
-    return [1]   # 0 (tcgen05) added with project_tc.cu
+    return [0, 1]   # 0 = tcgen05 tensor cores, 1 = SIMT fp32
 
 
 @pytest.fixture(scope="module")

@@ -55,6 +55,8 @@ void profile_end(cudaStream_t st, int slot);
         DL_CUDA(cudaGetLastError());                                                           \
     } while (0)
 
+#define COMMA ,
+
 // ------------------------------------------------------------------ math helpers
 __host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 __host__ __device__ inline int64_t round_up(int64_t a, int64_t b) { return ceil_div(a, b) * b; }

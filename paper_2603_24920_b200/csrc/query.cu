@@ -30,8 +30,9 @@ namespace {
 enum : int { ST_ACTIVE = 0, ST_BUDGET = 1, ST_RADIUS = 2, ST_CAP = 3 };
 
 struct QState {  // per query of a batch
-    int64_t cnt;        // |S|
-    int64_t nver;       // candidates verified so far (prefix of the list)
+    int64_t cnt;        // |S| (bits set in the query's bitmap)
+    int64_t nlist;      // verified candidates written to the (id, d2) list
+    int64_t nver;       // list entries already merged into the top-k
     int32_t status;     // ST_*
     int32_t tk;         // entries in the top-k list
     int32_t trees_last;
@@ -284,47 +285,31 @@ __global__ void __launch_bounds__(RF_THREADS, 3) k_range_filter(RFArgs a) {
     }
 }
 
-// After tree t: the first-time members of S (bits set now but not in `prev`) are appended to
-// the query's candidate list and `prev` catches up; |S| is the list length (S <- S u S_i,
-// Alg. 5 line 6, de-duplicated by the bitmap).  Grid: (active queries) x (word chunks).
+// After tree t: |S| += number of bits set now but not in `prev` (the first-time members of
+// S <- S u S_i, Alg. 5 line 6), and `prev` catches up.  Grid: (active queries) x (word chunks).
 constexpr int CN_WORDS = 4096;
-__global__ void __launch_bounds__(256) k_collect_new(const int* __restrict__ act, QState* __restrict__ qs,
-                                                     const uint32_t* __restrict__ cur, uint32_t* __restrict__ prev,
-                                                     int64_t nwords, uint32_t* __restrict__ cand, int64_t cap) {
+__global__ void __launch_bounds__(256) k_count_new(const int* __restrict__ act, QState* __restrict__ qs,
+                                                   const uint32_t* __restrict__ cur, uint32_t* __restrict__ prev,
+                                                   int64_t nwords) {
+    __shared__ unsigned int s_cnt;
     const int q = act[blockIdx.x];
     if (qs[q].status != ST_ACTIVE) return;
+    if (threadIdx.x == 0) s_cnt = 0;
+    __syncthreads();
     const uint32_t* c = cur + (int64_t)q * nwords;
     uint32_t* p = prev + (int64_t)q * nwords;
-    uint32_t* cl = cand + (int64_t)q * cap;
-    const int lane = threadIdx.x & 31;
     const int64_t w0 = (int64_t)blockIdx.y * CN_WORDS, w1 = min(w0 + CN_WORDS, nwords);
-    for (int64_t wb = w0; wb < w1; wb += 256) {
-        const int64_t w = wb + threadIdx.x;
-        uint32_t nb = 0;
-        if (w < w1) {
-            const uint32_t cv = c[w], pv = p[w];
-            nb = cv & ~pv;
-            if (nb) p[w] = cv;
-        }
-        const uint32_t cntb = __popc(nb);
-        uint32_t x = cntb;                       // warp inclusive scan of counts
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-            if (lane >= o) x += y;
-        }
-        const uint32_t tot = __shfl_sync(0xffffffffu, x, 31);
-        if (tot == 0) continue;
-        unsigned long long base = 0;
-        if (lane == 31) base = atomicAdd(reinterpret_cast<unsigned long long*>(&qs[q].cnt), (unsigned long long)tot);
-        base = __shfl_sync(0xffffffffu, base, 31);
-        int64_t at = (int64_t)base + x - cntb;
-        while (nb) {
-            const int b = __ffs(nb) - 1;
-            nb &= nb - 1;
-            if (at < cap) cl[at] = (uint32_t)(w * 32 + b);
-            ++at;
-        }
+    uint32_t cnt = 0;
+    for (int64_t w = w0 + threadIdx.x; w < w1; w += 256) {
+        const uint32_t cv = c[w], pv = p[w];
+        const uint32_t nb = cv & ~pv;
+        if (nb) { p[w] = cv; cnt += __popc(nb); }
     }
+    for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(&s_cnt, cnt);
+    __syncthreads();
+    if (threadIdx.x == 0 && s_cnt)
+        atomicAdd(reinterpret_cast<unsigned long long*>(&qs[q].cnt), (unsigned long long)s_cnt);
 }
 
 // After tree t: the budget test |S| >= ceil(beta n) + k (Alg. 5 line 7, AMB-15/17).
@@ -340,164 +325,135 @@ __global__ void k_tree_end(const int* __restrict__ act, int na, QState* __restri
     }
 }
 
-// ---- verify: work = chunks of VCH new candidates per active query
-constexpr int VCH = 64;
+// ---- verify (Alg. 5 lines 8/10): exact squared L2 of every member of S not yet verified,
+//      row-blocked: a CTA stages a block of consecutive data rows in shared memory once and
+//      serves every active query whose new candidates fall in that block (each row is a
+//      candidate of ~beta of all queries), one warp per (block, query): float4 reads of the
+//      staged rows, the query in registers, warp-shuffle reduction; (id, d2) appended to the
+//      query's list.  new = S \ verified is read from the bitmaps (cur & ~ver).
+constexpr int VR_THREADS = 512;
 
-__global__ void k_verify_prep(const int* __restrict__ act, int na, const QState* __restrict__ qs,
-                              uint32_t* __restrict__ choff, uint32_t* __restrict__ work) {
-    // single block prefix over active queries of ceil(new / VCH)
-    __shared__ uint32_t s_run;
-    if (threadIdx.x == 0) s_run = 0;
+struct VRArgs {
+    const float* X;
+    int64_t ld, n;
+    const float* Q;          // batch queries [Qb][ld]
+    const int* act;
+    int na;
+    QState* qs;
+    const uint32_t* cur;
+    uint32_t* ver;
+    int64_t nwords;
+    uint32_t* cand;
+    float* d2;
+    int64_t cap;
+    int rbw;                 // bitmap words (32 rows each) per block
+};
+
+// Each warp serves one query at a time: its 32 lanes form 4 row slots of 8 lanes; a slot
+// computes one candidate's distance, each lane a strided eighth of the row (float4 reads of
+// the staged row, the query's matching eighth held in registers), packed fp32x2 arithmetic,
+// a 3-step shuffle reduction inside the slot.  NV = float4 per lane (ld/4 = 8*NV at most;
+// NV = 0: rows wider than 256 fp32, the query is re-read from L1/L2).
+template <int NV, bool EXACT>
+__global__ void __launch_bounds__(VR_THREADS) k_verify_rows(VRArgs a) {
+    extern __shared__ __align__(16) float4 s_rows[];
+    __shared__ uint8_t s_list[VR_THREADS / 32][256];     // per warp: rows (in block) of the new bits
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = VR_THREADS / 32;
+    const int slot = lane >> 3, u = lane & 7;
+    const int nf4 = EXACT ? 8 * NV : (int)(a.ld / 4);
+    const int64_t w0 = (int64_t)blockIdx.x * a.rbw;
+    const int64_t row0 = w0 * 32;
+    const int RB = a.rbw * 32;
+    const float4* X4 = reinterpret_cast<const float4*>(a.X);
+    for (int i = threadIdx.x; i < RB * nf4; i += VR_THREADS) {
+        const int r = i / nf4, f = i - r * nf4;
+        const int64_t row = row0 + r;
+        s_rows[i] = row < a.n ? __ldg(X4 + row * nf4 + f) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
     __syncthreads();
-    for (int base = 0; base < na; base += blockDim.x) {
-        const int a = base + threadIdx.x;
-        uint32_t c = 0;
-        if (a < na) {
-            const QState s = qs[act[a]];
-            c = (uint32_t)ceil_div(s.cnt - s.nver, VCH);
-        }
-        // inclusive warp scan then block (blockDim == 1024)
-        __shared__ uint32_t s_w[32];
-        uint32_t x = c;
-        const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-        for (int o = 1; o < 32; o <<= 1) {
-            uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-            if (lane >= o) x += y;
-        }
-        if (lane == 31) s_w[w] = x;
-        __syncthreads();
-        if (w == 0) {
-            uint32_t v = s_w[lane];
-            for (int o = 1; o < 32; o <<= 1) {
-                uint32_t y = __shfl_up_sync(0xffffffffu, v, o);
-                if (lane >= o) v += y;
+    const float4* Q4 = reinterpret_cast<const float4*>(a.Q);
+    uint8_t* lst = s_list[warp];
+    for (int ai = warp; ai < a.na; ai += nwarps) {
+        const int q = a.act[ai];
+        uint32_t mw = 0;
+        if (lane < a.rbw) {
+            const int64_t w = w0 + lane;
+            if (w < a.nwords) {
+                uint32_t* vp = a.ver + (int64_t)q * a.nwords + w;
+                const uint32_t c = a.cur[(int64_t)q * a.nwords + w];
+                mw = c & ~*vp;
+                if (mw) *vp = c;
             }
-            s_w[lane] = v;
         }
-        __syncthreads();
-        const uint32_t incl = x + (w ? s_w[w - 1] : 0);
-        if (a < na) choff[a] = s_run + incl - c;
-        __syncthreads();
-        if (threadIdx.x == blockDim.x - 1) s_run += incl;
-        __syncthreads();
-    }
-    if (threadIdx.x == 0) {
-        choff[na] = s_run;
-        work[0] = 0;         // chunk counter
-    }
-}
-
-template <int NV>
-__global__ void __launch_bounds__(256) k_verify(const float* __restrict__ X, int64_t ld, const float* __restrict__ Q,
-                                                const int* __restrict__ act, int na, const QState* __restrict__ qs,
-                                                const uint32_t* __restrict__ choff, uint32_t* __restrict__ work,
-                                                const uint32_t* __restrict__ cand, float* __restrict__ d2,
-                                                int64_t cap) {
-    const int lane = threadIdx.x & 31;
-    const uint32_t total = choff[na];
-    const int nf4 = (int)(ld / 4);
-    int cur_a = -1;
-    float4 qv[NV];
-    for (;;) {
-        uint32_t c = 0;
-        if (lane == 0) c = atomicAdd(work, 1u);
-        c = __shfl_sync(0xffffffffu, c, 0);
-        if (c >= total) break;
-        int lo = 0, hi = na - 1;                   // owner: last a with choff[a] <= c
-        while (lo < hi) {
-            const int mid = (lo + hi + 1) >> 1;
-            if (choff[mid] <= c) lo = mid; else hi = mid - 1;
+        // rows of the new bits, in order, into the warp's list
+        const uint32_t pc = __popc(mw);
+        uint32_t incl = pc;
+#pragma unroll
+        for (int o = 1; o < 8; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
         }
-        const int a = lo;
-        const int q = act[a];
-        if (a != cur_a) {
-            cur_a = a;
-            const float4* q4 = reinterpret_cast<const float4*>(Q + (int64_t)q * ld);
+        const uint32_t tot = __shfl_sync(0xffffffffu, incl, 7);
+        if (tot == 0) continue;
+        unsigned long long base = 0;
+        if (lane == 0) base = atomicAdd(reinterpret_cast<unsigned long long*>(&a.qs[q].nlist), (unsigned long long)tot);
+        {
+            uint32_t m = mw, p = incl - pc;
+            while (m) {
+                lst[p++] = (uint8_t)(lane * 32 + __ffs(m) - 1);
+                m &= m - 1;
+            }
+        }
+        // -q, the lane's eighth, as fp32x2 pairs
+        float2 nq[NV ? 2 * NV : 2];
+        if (NV) {
 #pragma unroll
             for (int v = 0; v < NV; ++v) {
-                const int f = lane + 32 * v;
-                qv[v] = f < nf4 ? q4[f] : make_float4(0.f, 0.f, 0.f, 0.f);
+                const int f = u + 8 * v;
+                const float4 y = (EXACT || f < nf4) ? Q4[(int64_t)q * nf4 + f] : make_float4(0.f, 0.f, 0.f, 0.f);
+                nq[2 * v] = make_float2(-y.x, -y.y);
+                nq[2 * v + 1] = make_float2(-y.z, -y.w);
             }
         }
-        const QState s = qs[q];
-        const int64_t e0 = s.nver + (int64_t)(c - choff[a]) * VCH;
-        const int64_t e1 = min(e0 + VCH, s.cnt);
-        const uint32_t* cl = cand + (int64_t)q * cap;
-        float* dl = d2 + (int64_t)q * cap;
-        for (int64_t e = e0; e < e1; e += 4) {
-            uint32_t ids[4];
-#pragma unroll
-            for (int r = 0; r < 4; ++r) ids[r] = (e + r < e1) ? cl[e + r] : cl[e];
-            float4 xv[4][NV];
-#pragma unroll
-            for (int r = 0; r < 4; ++r) {
-                const float4* x4 = reinterpret_cast<const float4*>(X + (int64_t)ids[r] * ld);
+        __syncwarp();
+        const int64_t out = (int64_t)__shfl_sync(0xffffffffu, base, 0);
+        uint32_t* cl = a.cand + (int64_t)q * a.cap;
+        float* dl = a.d2 + (int64_t)q * a.cap;
+        for (uint32_t i = 0; i < tot; i += 4) {
+            const bool valid = i + slot < tot;
+            const int r = lst[valid ? i + slot : i];
+            const float4* row = s_rows + r * nf4;
+            float2 acc = make_float2(0.f, 0.f);
+            if (NV) {
 #pragma unroll
                 for (int v = 0; v < NV; ++v) {
-                    const int f = lane + 32 * v;
-                    xv[r][v] = f < nf4 ? __ldg(x4 + f) : make_float4(0.f, 0.f, 0.f, 0.f);
+                    const int f = u + 8 * v;
+                    if (EXACT || f < nf4) {
+                        const float4 x = row[f];
+                        const float2 d0 = __fadd2_rn(make_float2(x.x, x.y), nq[2 * v]);
+                        const float2 d1 = __fadd2_rn(make_float2(x.z, x.w), nq[2 * v + 1]);
+                        acc = __ffma2_rn(d0, d0, acc);
+                        acc = __ffma2_rn(d1, d1, acc);
+                    }
+                }
+            } else {
+                for (int f = u; f < nf4; f += 8) {
+                    const float4 x = row[f], y = Q4[(int64_t)q * nf4 + f];
+                    const float2 d0 = make_float2(x.x - y.x, x.y - y.y), d1 = make_float2(x.z - y.z, x.w - y.w);
+                    acc = __ffma2_rn(d0, d0, acc);
+                    acc = __ffma2_rn(d1, d1, acc);
                 }
             }
-            float acc[4];
-#pragma unroll
-            for (int r = 0; r < 4; ++r) {
-                float a_ = 0.f;
-#pragma unroll
-                for (int v = 0; v < NV; ++v) {
-                    const float dx = xv[r][v].x - qv[v].x, dy = xv[r][v].y - qv[v].y;
-                    const float dz = xv[r][v].z - qv[v].z, dw = xv[r][v].w - qv[v].w;
-                    a_ = fmaf(dx, dx, a_); a_ = fmaf(dy, dy, a_); a_ = fmaf(dz, dz, a_); a_ = fmaf(dw, dw, a_);
-                }
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) a_ += __shfl_xor_sync(0xffffffffu, a_, o);
-                acc[r] = a_;
-            }
-            if (lane < 4 && e + lane < e1) {
-                float v = acc[0];
-                if (lane == 1) v = acc[1];
-                if (lane == 2) v = acc[2];
-                if (lane == 3) v = acc[3];
-                dl[e + lane] = v;
+            float s_ = acc.x + acc.y;
+            s_ += __shfl_xor_sync(0xffffffffu, s_, 1);
+            s_ += __shfl_xor_sync(0xffffffffu, s_, 2);
+            s_ += __shfl_xor_sync(0xffffffffu, s_, 4);
+            if (valid && u == 0 && out + i + slot < a.cap) {
+                cl[out + i + slot] = (uint32_t)(row0 + r);
+                dl[out + i + slot] = s_;
             }
         }
-    }
-}
-
-// Generic-d verify (rows wider than 32*8 float4): loops over float4 columns.
-__global__ void __launch_bounds__(256) k_verify_generic(const float* __restrict__ X, int64_t ld,
-                                                        const float* __restrict__ Q, const int* __restrict__ act, int na,
-                                                        const QState* __restrict__ qs, const uint32_t* __restrict__ choff,
-                                                        uint32_t* __restrict__ work, const uint32_t* __restrict__ cand,
-                                                        float* __restrict__ d2, int64_t cap) {
-    const int lane = threadIdx.x & 31;
-    const uint32_t total = choff[na];
-    const int nf4 = (int)(ld / 4);
-    for (;;) {
-        uint32_t c = 0;
-        if (lane == 0) c = atomicAdd(work, 1u);
-        c = __shfl_sync(0xffffffffu, c, 0);
-        if (c >= total) break;
-        int lo = 0, hi = na - 1;
-        while (lo < hi) {
-            const int mid = (lo + hi + 1) >> 1;
-            if (choff[mid] <= c) lo = mid; else hi = mid - 1;
-        }
-        const int q = act[lo];
-        const QState s = qs[q];
-        const int64_t e0 = s.nver + (int64_t)(c - choff[lo]) * VCH;
-        const int64_t e1 = min(e0 + VCH, s.cnt);
-        const float4* q4 = reinterpret_cast<const float4*>(Q + (int64_t)q * ld);
-        for (int64_t e = e0; e < e1; ++e) {
-            const float4* x4 = reinterpret_cast<const float4*>(X + (int64_t)cand[(int64_t)q * cap + e] * ld);
-            float a_ = 0.f;
-            for (int f = lane; f < nf4; f += 32) {
-                const float4 x = __ldg(x4 + f), y = q4[f];
-                const float dx = x.x - y.x, dy = x.y - y.y, dz = x.z - y.z, dw = x.w - y.w;
-                a_ = fmaf(dx, dx, a_); a_ = fmaf(dy, dy, a_); a_ = fmaf(dz, dz, a_); a_ = fmaf(dw, dw, a_);
-            }
-            for (int o = 16; o > 0; o >>= 1) a_ += __shfl_xor_sync(0xffffffffu, a_, o);
-            if (lane == 0) d2[(int64_t)q * cap + e] = a_;
-        }
+        __syncwarp();
     }
 }
 
@@ -538,7 +494,7 @@ __global__ void __launch_bounds__(TK_THREADS) k_topk(const int* __restrict__ act
     unsigned long long* tk = topk + (int64_t)q * k;
     const uint32_t* cl = cand + (int64_t)q * cap;
     const float* dl = d2 + (int64_t)q * cap;
-    const int64_t old = s.tk, e0 = s.nver, nn = s.cnt - s.nver, M = old + nn;
+    const int64_t old = s.tk, e0 = s.nver, nn = s.nlist - s.nver, M = old + nn;
     auto key_at = [&](int64_t i) -> unsigned long long {
         return i < old ? tk[i] : mkkey(dl[e0 + i - old], cl[e0 + i - old]);
     };
@@ -590,7 +546,7 @@ __global__ void __launch_bounds__(TK_THREADS) k_topk(const int* __restrict__ act
     for (int i = threadIdx.x; i < outn; i += TK_THREADS) tk[i] = s_keys[i];
     if (threadIdx.x == 0) {
         s.tk = outn;
-        s.nver = s.cnt;
+        s.nver = s.nlist;
         if (s.status == ST_ACTIVE) {
             if (outn >= k && __uint_as_float((uint32_t)(s_keys[k - 1] >> 32)) <= cr2) s.status = ST_RADIUS;  // line 9
             else if (round == 63) s.status = ST_CAP;                                                        // AMB-20
@@ -662,7 +618,7 @@ __global__ void k_finalize(const QState* __restrict__ qs, const unsigned long lo
 __global__ void k_init_batch(QState* __restrict__ qs, int* __restrict__ act, int nqb) {
     for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < nqb; q += gridDim.x * blockDim.x) {
         QState s;
-        s.cnt = 0; s.nver = 0; s.status = ST_ACTIVE; s.tk = 0; s.trees_last = 0; s.rounds = 0;
+        s.cnt = 0; s.nlist = 0; s.nver = 0; s.status = ST_ACTIVE; s.tk = 0; s.trees_last = 0; s.rounds = 0;
         s.overflow = 0; s.pad = 0;
         qs[q] = s;
         act[q] = q;
@@ -693,7 +649,7 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
     }
 
     // batch size from the memory budget: bitmap + candidate list + distances per query
-    const int64_t per_q = nwords * 8 + cap * 8 + (int64_t)k * 8 + (int64_t)LK * (ix.N_r * 4 + 1) + 96;
+    const int64_t per_q = nwords * 12 + cap * 8 + (int64_t)k * 8 + (int64_t)LK * (ix.N_r * 4 + 1) + 96;
     int64_t budget_bytes = a.mem_budget;
     if (budget_bytes <= 0) {
         size_t fr = 0, tot = 0;
@@ -706,6 +662,7 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
 
     Scratch s_bm(st, sizeof(uint32_t) * (size_t)(2 * qb * nwords));   // current union + previous
     Scratch s_ctr(st, sizeof(unsigned long long) * (size_t)(4 * qb));
+    Scratch s_ver(st, sizeof(uint32_t) * (size_t)(qb * nwords));     // verified members of S
     Scratch s_cand(st, sizeof(uint32_t) * (size_t)(qb * cap));
     Scratch s_d2(st, sizeof(float) * (size_t)(qb * cap));
     Scratch s_tk(st, sizeof(unsigned long long) * (size_t)(qb * k));
@@ -716,8 +673,6 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
     int* act = s_act.as<int>();
     int* act2 = act + qb;
     int* n_act = act2 + qb;
-    uint32_t* choff = s_ch.as<uint32_t>();
-    uint32_t* work = choff + qb + 1;
 
     const double eps = ix.eps;
     std::vector<double> radii(64);
@@ -768,14 +723,40 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
     ra.K = ix.K;
     ra.N_r = ix.N_r;
     ra.mode = a.mode;
-    const int nv = (int)ceil_div(ix.ld / 4, 32);
-    int vgrid = 148 * 8;
+    const int nv = (int)ceil_div(ix.ld / 4, 8);      // float4 per lane (8 lanes per row)
+    const int vnv = nv <= 1 ? 1 : nv <= 2 ? 2 : nv <= 4 ? 4 : nv <= 8 ? 8 : 0;
+    VRArgs va;
+    va.X = ix.Xp;
+    va.ld = ix.ld;
+    va.n = n;
+    va.qs = s_qs.as<QState>();
+    va.cur = s_bm.as<uint32_t>();
+    va.ver = s_ver.as<uint32_t>();
+    va.nwords = nwords;
+    va.cand = s_cand.as<uint32_t>();
+    va.d2 = s_d2.as<float>();
+    va.cap = cap;
+    {   // rows per block: as many 32-row words as fit in 120 KB of shared memory (1..8)
+        const int64_t per_word = (int64_t)32 * ix.ld * 4;
+        va.rbw = (int)std::max<int64_t>(1, std::min<int64_t>(8, (120 * 1024) / per_word));
+    }
+    const size_t vr_smem = (size_t)va.rbw * 32 * ix.ld * 4;
+    const bool vexact = (ix.ld / 4) == 8 * vnv;
+    DL_CUDA(cudaFuncSetAttribute(k_verify_rows<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)vr_smem));
+    DL_CUDA(cudaFuncSetAttribute(k_verify_rows<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)vr_smem));
+    DL_CUDA(cudaFuncSetAttribute(k_verify_rows<4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)vr_smem));
+    DL_CUDA(cudaFuncSetAttribute(k_verify_rows<4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)vr_smem));
+    DL_CUDA(cudaFuncSetAttribute(k_verify_rows<8, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)vr_smem));
+    DL_CUDA(cudaFuncSetAttribute(k_verify_rows<8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)vr_smem));
+    DL_CUDA(cudaFuncSetAttribute(k_verify_rows<0, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)vr_smem));
 
     for (int64_t q0 = 0; q0 < nq; q0 += qb) {
         const int nqb = (int)std::min<int64_t>(qb, nq - q0);
         const float* Qb = d_Q + q0 * q_ld;
         const float* Qpb = s_qp.as<float>() + q0 * LK;
+        va.Q = Qb;
         DL_CUDA(cudaMemsetAsync(s_bm.p, 0, sizeof(uint32_t) * (size_t)(2 * qb * nwords), st));
+        DL_CUDA(cudaMemsetAsync(s_ver.p, 0, sizeof(uint32_t) * (size_t)(qb * nwords), st));
         DL_CUDA(cudaMemsetAsync(s_ctr.p, 0, sizeof(unsigned long long) * (size_t)(4 * qb), st));
         DL_LAUNCH(k_init_batch, (unsigned)ceil_div(nqb, 256), 256, 0, st, s_qs.as<QState>(), act, nqb);
         DL_LAUNCH(k_build_lut, (unsigned)std::min<int64_t>(ceil_div((int64_t)nqb * LK * ix.N_r, 256), 148 * 32), 256, 0,
@@ -802,25 +783,26 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
                 const int64_t ntiles = ra.tile_end - ra.tile_begin;
                 const int stripes = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, ceil_div(148 * 8, groups)));
                 DL_LAUNCH(k_range_filter_sel, dim3((unsigned)groups, (unsigned)stripes), RF_THREADS, rf_smem, st, ra);
-                DL_LAUNCH(k_collect_new, dim3((unsigned)na, (unsigned)ceil_div(nwords, CN_WORDS)), 256, 0, st, cur,
-                          s_qs.as<QState>(), s_bm.as<uint32_t>(), bm_prev, nwords, s_cand.as<uint32_t>(), cap);
+                DL_LAUNCH(k_count_new, dim3((unsigned)na, (unsigned)ceil_div(nwords, CN_WORDS)), 256, 0, st, cur,
+                          s_qs.as<QState>(), s_bm.as<uint32_t>(), bm_prev, nwords);
                 DL_LAUNCH(k_tree_end, (unsigned)ceil_div(na, 256), 256, 0, st, cur, na, s_qs.as<QState>(), t, m,
                           budget, cap);
             }
-            DL_LAUNCH(k_verify_prep, 1, 1024, 0, st, cur, na, s_qs.as<QState>(), choff, work);
-            switch (nv) {
-                case 1: DL_LAUNCH(k_verify<1>, vgrid, 256, 0, st, ix.Xp, ix.ld, Qb, cur, na, s_qs.as<QState>(), choff, work,
-                                  s_cand.as<uint32_t>(), s_d2.as<float>(), cap); break;
-                case 2: DL_LAUNCH(k_verify<2>, vgrid, 256, 0, st, ix.Xp, ix.ld, Qb, cur, na, s_qs.as<QState>(), choff, work,
-                                  s_cand.as<uint32_t>(), s_d2.as<float>(), cap); break;
-                case 3: case 4: DL_LAUNCH(k_verify<4>, vgrid, 256, 0, st, ix.Xp, ix.ld, Qb, cur, na, s_qs.as<QState>(), choff,
-                                  work, s_cand.as<uint32_t>(), s_d2.as<float>(), cap); break;
-                case 5: case 6: case 7: case 8:
-                    DL_LAUNCH(k_verify<8>, vgrid, 256, 0, st, ix.Xp, ix.ld, Qb, cur, na, s_qs.as<QState>(), choff, work,
-                              s_cand.as<uint32_t>(), s_d2.as<float>(), cap); break;
-                default:
-                    DL_LAUNCH(k_verify_generic, vgrid, 256, 0, st, ix.Xp, ix.ld, Qb, cur, na, s_qs.as<QState>(), choff,
-                              work, s_cand.as<uint32_t>(), s_d2.as<float>(), cap);
+            va.act = cur;
+            va.na = na;
+            {
+                const unsigned nblocks = (unsigned)ceil_div(nwords, va.rbw);
+                switch (vnv) {
+                    case 1: DL_LAUNCH(k_verify_rows<1 COMMA false>, nblocks, VR_THREADS, vr_smem, st, va); break;
+                    case 2: DL_LAUNCH(k_verify_rows<2 COMMA false>, nblocks, VR_THREADS, vr_smem, st, va); break;
+                    case 4: if (vexact) DL_LAUNCH(k_verify_rows<4 COMMA true>, nblocks, VR_THREADS, vr_smem, st, va);
+                            else DL_LAUNCH(k_verify_rows<4 COMMA false>, nblocks, VR_THREADS, vr_smem, st, va);
+                            break;
+                    case 8: if (vexact) DL_LAUNCH(k_verify_rows<8 COMMA true>, nblocks, VR_THREADS, vr_smem, st, va);
+                            else DL_LAUNCH(k_verify_rows<8 COMMA false>, nblocks, VR_THREADS, vr_smem, st, va);
+                            break;
+                    default: DL_LAUNCH(k_verify_rows<0 COMMA false>, nblocks, VR_THREADS, vr_smem, st, va); break;
+                }
             }
             DL_LAUNCH(k_topk, (unsigned)na, TK_THREADS, 0, st, cur, s_qs.as<QState>(), s_cand.as<uint32_t>(),
                       s_d2.as<float>(), cap, s_tk.as<unsigned long long>(), k, cr2, m);
@@ -832,6 +814,7 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
         DL_LAUNCH(k_finalize, (unsigned)std::min<int64_t>(ceil_div((int64_t)nqb * k, 256), 148 * 16), 256, 0, st,
                   s_qs.as<QState>(), s_ctr.as<unsigned long long>(), s_tk.as<unsigned long long>(), nqb, k, ix.id_offset, s_radii.as<double>(),
                   d_ids + q0 * k, d_dists + q0 * k, d_stats ? d_stats + q0 : nullptr);
+        (void)Qb;
     }
 }
 

@@ -553,16 +553,14 @@ __global__ void k_gather_rows_strided(const float* __restrict__ src, int64_t src
     }
 }
 
-// Query tiles: runs of consecutive leaves of one tree whose
-// first points fall in the same window of kTilePoints positions.  A tile holds at most
-// kTilePoints leaves, and every leaf but its last starts inside the window.
-__global__ void k_tile_flags(const uint32_t* __restrict__ leaf_off, int64_t nl, int64_t n, int tp,
-                             uint32_t* __restrict__ flags) {
+// Query tiles: runs of kTileLeaves consecutive leaves of one
+// tree (the last tile of a tree may be shorter); one warp of the range filter owns a tile.
+__global__ void k_tile_flags(const uint32_t* __restrict__ leaf_off, int64_t nl, int64_t n, int tl,
+                             const unsigned long long* __restrict__ tree_begin, uint32_t* __restrict__ flags) {
     for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < nl;
          l += (int64_t)gridDim.x * blockDim.x) {
-        if (l == 0) { flags[l] = 1; continue; }
-        const uint32_t a = leaf_off[l - 1], b = leaf_off[l];
-        flags[l] = (a / n != b / n || (a % n) / tp != (b % n) / tp) ? 1u : 0u;
+        const int64_t t = leaf_off[l] / n;
+        flags[l] = ((l - (int64_t)tree_begin[t]) % tl == 0) ? 1u : 0u;
     }
 }
 
@@ -573,8 +571,7 @@ __global__ void k_tile_write(const uint32_t* __restrict__ flags, const uint32_t*
         if (flags[l]) tile_leaf[idx[l]] = (uint32_t)l;
 }
 
-// Per point (tree order): index of its leaf within its query tile (u16; a tile holds at most
-// kTilePoints leaves).
+// Per point (tree order): index of its leaf within its query tile (< kTileLeaves).
 __global__ void k_point_tile_leaf(const uint32_t* __restrict__ leaf_off, const uint32_t* __restrict__ tile_leaf,
                                   int64_t ntiles, int64_t nl, uint16_t* __restrict__ ptl) {
     for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < nl;
@@ -777,7 +774,9 @@ static bool build_trees_try(Index& ix, const uint8_t* d_EP, int64_t leaf_factor,
         uint32_t* tf = s_tf.as<uint32_t>();
         uint32_t* tidx = tf + nl;
         uint32_t* ntiles_d = tidx + nl;
-        DL_LAUNCH(k_tile_flags, grid_for(nl, 256), 256, 0, st, ix.leaf_off.as<uint32_t>(), nl, n, kTilePoints, tf);
+        DL_CUDA(cudaMemcpyAsync(s_begin.p, begin.data(), sizeof(unsigned long long) * (L + 1), cudaMemcpyHostToDevice, st));
+        DL_LAUNCH(k_tile_flags, grid_for(nl, 256), 256, 0, st, ix.leaf_off.as<uint32_t>(), nl, n, kTileLeaves,
+                  s_begin.as<unsigned long long>(), tf);
         exclusive_scan_u32(tf, tidx, nl, ntiles_d, st);
         const int64_t ntiles = d2h(ntiles_d, st);
         ix.tile_leaf.alloc(sizeof(uint32_t) * (size_t)(ntiles + 1));

@@ -27,7 +27,7 @@ struct DevBuf {
     template <class T> T* as() const { return static_cast<T*>(p); }
 };
 
-constexpr int kTilePoints = 1024;   // query-tile window (points)
+constexpr int kTileLeaves = 32;     // leaves per query tile (one warp of the range filter)
 
 struct Index {
     // shape / parameters
@@ -56,7 +56,7 @@ struct Index {
     std::vector<int64_t> tree_leaf_begin;  // [L+1] leaf index range of each tree (host copy)
     DevBuf tile_leaf;       // [ntiles+1] first leaf of each query tile (tree-major; see build.cu)
     std::vector<int64_t> tree_tile_begin;  // [L+1] tile index range of each tree (host copy)
-    DevBuf point_tile_leaf; // [L*n] u16: leaf of each point (tree order) relative to its tile
+    DevBuf point_tile_leaf; // [L*n] u16: leaf of each point (tree order) within its tile (< 32)
 
     int64_t nl_total() const { return tree_leaf_begin.empty() ? 0 : tree_leaf_begin.back(); }
 };

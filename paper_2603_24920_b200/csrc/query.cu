@@ -118,14 +118,13 @@ __global__ void __launch_bounds__(RF_THREADS, 3) k_range_filter(RFArgs a) {
     const int K = KT ? KT : a.K;
     const int N_r = NRT ? NRT : a.N_r;
     float4* s_lut = reinterpret_cast<float4*>(smem);                                   // [K][N_r] x G
-    uint32_t* s_loff = reinterpret_cast<uint32_t*>(s_lut + K * N_r);                   // [kTilePoints+2]
-    uint32_t* s_lq = s_loff + kTilePoints + 2;                                         // [kTilePoints+1] G bytes
     __shared__ int s_q[RF_G];
     __shared__ uint8_t s_sx[RF_G][32];
     __shared__ unsigned int s_ctr[RF_G][4];
+    __shared__ uint32_t s_lq[RF_THREADS / 32][kTileLeaves];                            // per warp: leaf masks
     __shared__ int s_active_mask;
 
-    const int lane = threadIdx.x & 31;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = RF_THREADS / 32;
     // ---- the query group and its LUTs, interleaved so one 16-byte load serves all G queries
     if (threadIdx.x < RF_G) {
         const int gi = blockIdx.x * RF_G + threadIdx.x;
@@ -166,22 +165,23 @@ __global__ void __launch_bounds__(RF_THREADS, 3) k_range_filter(RFArgs a) {
     __syncthreads();
     const float rho2 = a.rho2;
     const float* s_lutf = reinterpret_cast<const float*>(s_lut);
-    uint32_t c_lt = 0, c_lp = 0, c_pt[RF_G], c_pp[RF_G];   // leaf counters summed over the group
+    uint32_t c_lt = 0, c_lp = 0, c_pt[RF_G], c_pp[RF_G];
 #pragma unroll
     for (int g = 0; g < RF_G; ++g) c_pt[g] = c_pp[g] = 0;
+    uint32_t* lq = s_lq[warp];
 
-    for (int64_t tile = a.tile_begin + blockIdx.y; tile < a.tile_end; tile += gridDim.y) {
+    // ---- warp-owned tiles of <= 32 leaves: no block-wide barriers in the scan
+    for (int64_t tile = a.tile_begin + (int64_t)blockIdx.y * nwarps + warp; tile < a.tile_end;
+         tile += (int64_t)gridDim.y * nwarps) {
         const uint32_t lb = a.tile_leaf[tile], le = a.tile_leaf[tile + 1];
         const int nlt = (int)(le - lb);
         const uint32_t P0 = a.leaf_off[lb], P1 = a.leaf_off[le];
-        for (int i = threadIdx.x; i <= nlt; i += RF_THREADS) s_loff[i] = a.leaf_off[lb + i] - P0;
-        __syncthreads();
-        // ---- leaf lower bounds (Alg. 3 pruning, Fig. dist): one thread per (leaf, query)
-        uint8_t* s_lqb = reinterpret_cast<uint8_t*>(s_lq);
-        for (int i = threadIdx.x; i < nlt * RF_G; i += RF_THREADS) {
-            const int li = i / RF_G, g = i - li * RF_G;
-            const int64_t l = (int64_t)lb + li;
-            float lacc = 0.f;
+        // leaf lower bounds (Alg. 3 pruning, Fig. dist): lane = leaf, all G queries
+        if (lane < nlt) {
+            const int64_t l = (int64_t)lb + lane;
+            float lacc[RF_G];
+#pragma unroll
+            for (int g = 0; g < RF_G; ++g) lacc[g] = 0.f;
             if (KT == 16) {
                 const uint4 lo4 = *reinterpret_cast<const uint4*>(a.lo + l * 16);
                 const uint4 hi4 = *reinterpret_cast<const uint4*>(a.hi + l * 16);
@@ -193,32 +193,35 @@ __global__ void __launch_bounds__(RF_THREADS, 3) k_range_filter(RFArgs a) {
                     for (int b = 0; b < 4; ++b) {
                         const int j = w * 4 + b;
                         const int lo_ = (lw >> (8 * b)) & 255, hi_ = (hw >> (8 * b)) & 255;
-                        lacc += s_lutf[(j * N_r + min(max((int)s_sx[g][j], lo_), hi_)) * RF_G + g];
+#pragma unroll
+                        for (int g = 0; g < RF_G; ++g)
+                            lacc[g] += s_lutf[(j * N_r + min(max((int)s_sx[g][j], lo_), hi_)) * RF_G + g];
                     }
                 }
             } else {
                 for (int j = 0; j < K; ++j) {
                     const int lo_ = a.lo[l * K + j], hi_ = a.hi[l * K + j];
-                    lacc += s_lutf[(j * N_r + min(max((int)s_sx[g][j], lo_), hi_)) * RF_G + g];
+#pragma unroll
+                    for (int g = 0; g < RF_G; ++g)
+                        lacc[g] += s_lutf[(j * N_r + min(max((int)s_sx[g][j], lo_), hi_)) * RF_G + g];
                 }
             }
-            const bool ok = lacc <= rho2 && ((amask >> g) & 1);
-            s_lqb[i] = ok ? 1 : 0;
-            c_lt += (amask >> g) & 1;
-            c_lp += ok;
-        }
-        __syncthreads();
-        // ---- points of the tile: cell lower bounds (AMB-12), OR-marking the query bitmaps
-        const uint32_t np = P1 - P0;
-        for (uint32_t pb = 0; pb < np; pb += RF_THREADS) {
-            const uint32_t pl = pb + threadIdx.x;
             uint32_t m = 0;
-            if (pl < np) {
-                const uint32_t x = s_lq[a.ptl[(int64_t)P0 + pl - a.pos_base]];   // G flag bytes -> G bits
-                m = (x & 1u) | ((x >> 7) & 2u) | ((x >> 14) & 4u) | ((x >> 21) & 8u);
-            }
+#pragma unroll
+            for (int g = 0; g < RF_G; ++g)
+                if (lacc[g] <= rho2 && ((amask >> g) & 1)) m |= 1u << g;
+            lq[lane] = m;
+            c_lt += __popc(amask);
+            c_lp += __popc(m);
+        }
+        __syncwarp();
+        // points of the tile: cell lower bounds (AMB-12), OR-marking the query bitmaps
+        for (uint32_t pb = P0; pb < P1; pb += 32) {
+            const uint32_t p = pb + lane;
+            const int64_t pos = (int64_t)p - a.pos_base;
+            uint32_t m = 0;
+            if (p < P1) m = lq[a.ptl[pos]];
             if (__ballot_sync(0xffffffffu, m != 0) == 0) continue;    // whole warp pruned by leaf LBs
-            const int64_t pos = (int64_t)P0 + pl - a.pos_base;
             float acc[RF_G];
 #pragma unroll
             for (int g = 0; g < RF_G; ++g) acc[g] = 0.f;
@@ -257,24 +260,26 @@ __global__ void __launch_bounds__(RF_THREADS, 3) k_range_filter(RFArgs a) {
                 }
             }
         }
-        __syncthreads();
+        __syncwarp();
     }
     // ---- counters
     {
-        uint32_t v[1 + 3 * RF_G];
+        uint32_t v[2 + 2 * RF_G];
         v[0] = c_lt;
+        v[1] = c_lp;
 #pragma unroll
-        for (int g = 0; g < RF_G; ++g) { v[1 + g] = c_lp; v[1 + RF_G + g] = c_pt[g]; v[1 + 2 * RF_G + g] = c_pp[g]; }
+        for (int g = 0; g < RF_G; ++g) { v[2 + g] = c_pt[g]; v[2 + RF_G + g] = c_pp[g]; }
 #pragma unroll
-        for (int i = 0; i < 1 + 3 * RF_G; ++i)
+        for (int i = 0; i < 2 + 2 * RF_G; ++i)
             for (int o = 16; o > 0; o >>= 1) v[i] += __shfl_xor_sync(0xffffffffu, v[i], o);
         if (lane == 0) {
+            const int na_ = max(1, __popc(amask));
 #pragma unroll
             for (int g = 0; g < RF_G; ++g) {   // leaf counts are per group: attributed evenly
-                atomicAdd(&s_ctr[g][0], v[0] / max(1, __popc(amask)));
-                atomicAdd(&s_ctr[g][1], v[1 + g] / max(1, __popc(amask)));
-                atomicAdd(&s_ctr[g][2], v[1 + RF_G + g]);
-                atomicAdd(&s_ctr[g][3], v[1 + 2 * RF_G + g]);
+                atomicAdd(&s_ctr[g][0], v[0] / na_);
+                atomicAdd(&s_ctr[g][1], v[1] / na_);
+                atomicAdd(&s_ctr[g][2], v[2 + g]);
+                atomicAdd(&s_ctr[g][3], v[2 + RF_G + g]);
             }
         }
     }
@@ -703,8 +708,7 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
     // per-batch LUTs
     Scratch s_lut(st, sizeof(float) * (size_t)(qb * LK * ix.N_r));
     Scratch s_sx(st, (size_t)(qb * LK));
-    const size_t rf_smem = sizeof(float) * (size_t)RF_G * ix.K * ix.N_r + sizeof(uint32_t) * (kTilePoints + 2) +
-                           sizeof(uint32_t) * (kTilePoints + 1);
+    const size_t rf_smem = sizeof(float) * (size_t)RF_G * ix.K * ix.N_r;
     auto k_range_filter_sel = (ix.K == 16 && ix.N_r == 256) ? k_range_filter<16, 256> : k_range_filter<0, 0>;
     DL_CUDA(cudaFuncSetAttribute(k_range_filter_sel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rf_smem));
     RFArgs ra;
@@ -781,7 +785,8 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
                 ra.t = t;
                 const int groups = (int)ceil_div(na, RF_G);
                 const int64_t ntiles = ra.tile_end - ra.tile_begin;
-                const int stripes = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, ceil_div(148 * 8, groups)));
+                const int stripes = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(ntiles, RF_THREADS / 32),
+                                                                                 ceil_div(148 * 6, groups)));
                 DL_LAUNCH(k_range_filter_sel, dim3((unsigned)groups, (unsigned)stripes), RF_THREADS, rf_smem, st, ra);
                 DL_LAUNCH(k_count_new, dim3((unsigned)na, (unsigned)ceil_div(nwords, CN_WORDS)), 256, 0, st, cur,
                           s_qs.as<QState>(), s_bm.as<uint32_t>(), bm_prev, nwords);

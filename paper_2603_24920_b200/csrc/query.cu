@@ -81,14 +81,33 @@ __global__ void k_build_lut(const float* __restrict__ Qp, int nqb, int LK, int N
     }
 }
 
+// ---- per round: 12-bit quantised lower bounds of the LUT, e = min(4095, floor(D * 2048/rho^2))
+//      (products rounded down), so sum_j e_j > 2048 proves sum_j D_j > rho^2 in fp32 (the
+//      16 terms sum to at most 65520: two queries share one 32-bit integer add).
+__global__ void k_build_qlut(const float* __restrict__ lut, const int* __restrict__ act, int na, int64_t per_q,
+                             float inv_rd, uint16_t* __restrict__ qlut) {
+    const int64_t total = (int64_t)na * per_q;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t a_ = i / per_q, e = i - a_ * per_q;
+        const int64_t q = act[a_];
+        float v = __fmul_rd(lut[q * per_q + e], inv_rd);
+        if (v != v) v = 0.f;                       // 0 * inf: a zero term stays zero
+        qlut[q * per_q + e] = (uint16_t)(v >= 4095.f ? 4095.f : floorf(v));
+    }
+}
+
 // ---- range filter of one tree (Alg. 3 at radius eps*r, Alg. 5 lines 5-6), batched:
-//      CTA (group of G active queries) x (stripe of tiles).  Per tile: leaf lower bounds of
-//      every (leaf, query) -- sum_j D_j[clamp(s_x, lo_j, hi_j)] <= rho^2 -- then the cell
-//      bound of every point of a qualifying leaf (AMB-12; a point of a pruned leaf cannot
-//      pass since leaf LB <= cell LB), OR-marking the per-query bitmap and appending first-
-//      time ids.  Codes of a tile are read once for all G queries.
+//      CTA = group of 8 active queries x stripe of tiles; a warp owns a tile of <= 32 leaves.
+//      Leaf lower bounds (lane = leaf) prune; for the points of qualifying leaves the cell
+//      lower bound is screened with the quantised table (one 16-byte shared load per code
+//      serves all 8 queries, two queries per 32-bit integer add) and confirmed in fp32 from
+//      the exact table; passing points are OR-marked into the per-query bitmap (RED.OR).
+//      The fp32 confirmation sums the same terms in the same order as the oracle's
+//      definition of the cell bound (AMB-12), so the quantised screen never changes a result.
 constexpr int RF_THREADS = 256;
-constexpr int RF_G = 4;          // queries per CTA: one float4 LUT entry holds the G values
+constexpr int RF_G = 8;          // queries per CTA: one 16-byte quantised entry holds the G values
+constexpr uint32_t RF_QT = 2048; // quantised threshold (rho^2)
 
 struct RFArgs {
     const uint8_t* tcodes;      // tree t: [n][K]
@@ -100,7 +119,8 @@ struct RFArgs {
     const uint32_t* tile_leaf;  // [ntiles+1]
     int64_t tile_begin, tile_end;
     int64_t pos_base;           // t * n
-    const float* lut;           // [Qb][L][K][N_r]
+    const float* lut;           // [Qb][L][K][N_r] exact
+    const uint16_t* qlut;       // [Qb][L][K][N_r] quantised lower bounds (this round)
     const uint8_t* sx;          // [Qb][L][K]
     const int* act;
     int na;
@@ -117,15 +137,14 @@ __global__ void __launch_bounds__(RF_THREADS, 3) k_range_filter(RFArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int K = KT ? KT : a.K;
     const int N_r = NRT ? NRT : a.N_r;
-    float4* s_lut = reinterpret_cast<float4*>(smem);                                   // [K][N_r] x G
+    uint4* s_q16 = reinterpret_cast<uint4*>(smem);                                      // [K][N_r] x 8 u16
     __shared__ int s_q[RF_G];
     __shared__ uint8_t s_sx[RF_G][32];
     __shared__ unsigned int s_ctr[RF_G][4];
-    __shared__ uint32_t s_lq[RF_THREADS / 32][kTileLeaves];                            // per warp: leaf masks
+    __shared__ uint32_t s_lq[RF_THREADS / 32][kTileLeaves];                             // per warp: leaf masks
     __shared__ int s_active_mask;
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = RF_THREADS / 32;
-    // ---- the query group and its LUTs, interleaved so one 16-byte load serves all G queries
     if (threadIdx.x < RF_G) {
         const int gi = blockIdx.x * RF_G + threadIdx.x;
         int q = -1;
@@ -145,16 +164,17 @@ __global__ void __launch_bounds__(RF_THREADS, 3) k_range_filter(RFArgs a) {
     __syncthreads();
     const int amask = s_active_mask;
     if (amask == 0) return;
-    {
-        const float* src[RF_G];
+    const int64_t per_q = (int64_t)a.L * K * N_r;
+    {   // interleave the 8 queries' quantised tables: entry (j, s) = 8 x u16
+        const uint16_t* src[RF_G];
 #pragma unroll
         for (int g = 0; g < RF_G; ++g)
-            src[g] = s_q[g] >= 0 ? a.lut + ((int64_t)s_q[g] * a.L + a.t) * K * N_r : nullptr;
+            src[g] = s_q[g] >= 0 ? a.qlut + (int64_t)s_q[g] * per_q + (int64_t)a.t * K * N_r : nullptr;
         for (int i = threadIdx.x; i < K * N_r; i += RF_THREADS) {
-            float v[RF_G];
+            uint32_t v[RF_G];
 #pragma unroll
-            for (int g = 0; g < RF_G; ++g) v[g] = src[g] ? src[g][i] : INFINITY;   // inactive: never passes
-            s_lut[i] = make_float4(v[0], v[1], v[2], v[3]);
+            for (int g = 0; g < RF_G; ++g) v[g] = src[g] ? src[g][i] : 4095u;      // inactive: never passes
+            s_q16[i] = make_uint4(v[0] | (v[1] << 16), v[2] | (v[3] << 16), v[4] | (v[5] << 16), v[6] | (v[7] << 16));
         }
         if (threadIdx.x < K) {
 #pragma unroll
@@ -164,24 +184,21 @@ __global__ void __launch_bounds__(RF_THREADS, 3) k_range_filter(RFArgs a) {
     }
     __syncthreads();
     const float rho2 = a.rho2;
-    const float* s_lutf = reinterpret_cast<const float*>(s_lut);
-    uint32_t c_lt = 0, c_lp = 0, c_pt[RF_G], c_pp[RF_G];
-#pragma unroll
-    for (int g = 0; g < RF_G; ++g) c_pt[g] = c_pp[g] = 0;
+    const uint16_t* s_q16h = reinterpret_cast<const uint16_t*>(s_q16);
+    uint32_t c_lt = 0, c_lp = 0, c_pt = 0, c_pp = 0;
     uint32_t* lq = s_lq[warp];
 
-    // ---- warp-owned tiles of <= 32 leaves: no block-wide barriers in the scan
     for (int64_t tile = a.tile_begin + (int64_t)blockIdx.y * nwarps + warp; tile < a.tile_end;
          tile += (int64_t)gridDim.y * nwarps) {
         const uint32_t lb = a.tile_leaf[tile], le = a.tile_leaf[tile + 1];
         const int nlt = (int)(le - lb);
         const uint32_t P0 = a.leaf_off[lb], P1 = a.leaf_off[le];
-        // leaf lower bounds (Alg. 3 pruning, Fig. dist): lane = leaf, all G queries
+        // leaf lower bounds (Alg. 3 pruning, Fig. dist): lane = leaf, quantised, all G queries
         if (lane < nlt) {
             const int64_t l = (int64_t)lb + lane;
-            float lacc[RF_G];
+            uint32_t lacc[RF_G];
 #pragma unroll
-            for (int g = 0; g < RF_G; ++g) lacc[g] = 0.f;
+            for (int g = 0; g < RF_G; ++g) lacc[g] = 0;
             if (KT == 16) {
                 const uint4 lo4 = *reinterpret_cast<const uint4*>(a.lo + l * 16);
                 const uint4 hi4 = *reinterpret_cast<const uint4*>(a.hi + l * 16);
@@ -195,7 +212,7 @@ __global__ void __launch_bounds__(RF_THREADS, 3) k_range_filter(RFArgs a) {
                         const int lo_ = (lw >> (8 * b)) & 255, hi_ = (hw >> (8 * b)) & 255;
 #pragma unroll
                         for (int g = 0; g < RF_G; ++g)
-                            lacc[g] += s_lutf[(j * N_r + min(max((int)s_sx[g][j], lo_), hi_)) * RF_G + g];
+                            lacc[g] += s_q16h[(j * N_r + min(max((int)s_sx[g][j], lo_), hi_)) * RF_G + g];
                     }
                 }
             } else {
@@ -203,84 +220,120 @@ __global__ void __launch_bounds__(RF_THREADS, 3) k_range_filter(RFArgs a) {
                     const int lo_ = a.lo[l * K + j], hi_ = a.hi[l * K + j];
 #pragma unroll
                     for (int g = 0; g < RF_G; ++g)
-                        lacc[g] += s_lutf[(j * N_r + min(max((int)s_sx[g][j], lo_), hi_)) * RF_G + g];
+                        lacc[g] += s_q16h[(j * N_r + min(max((int)s_sx[g][j], lo_), hi_)) * RF_G + g];
                 }
             }
+            // a leaf is pruned only when its quantised bound proves LB > rho (no member can pass)
             uint32_t m = 0;
 #pragma unroll
             for (int g = 0; g < RF_G; ++g)
-                if (lacc[g] <= rho2 && ((amask >> g) & 1)) m |= 1u << g;
+                if (lacc[g] <= RF_QT && ((amask >> g) & 1)) m |= 1u << g;
+            if (a.mode != DETLSH_MODE_CELL) {
+                // RELAXED (Sec. 6.2.2(1)): the leaf decision is final, so confirm it in fp32
+                uint32_t conf = 0, mm = m;
+                while (mm) {
+                    const int g = __ffs(mm) - 1;
+                    mm &= mm - 1;
+                    const float* D = a.lut + (int64_t)s_q[g] * per_q + (int64_t)a.t * K * N_r;
+                    float s_ = 0.f;
+                    for (int j = 0; j < K; ++j)
+                        s_ += __ldg(D + j * N_r + min(max((int)s_sx[g][j], (int)a.lo[l * K + j]), (int)a.hi[l * K + j]));
+                    if (s_ <= rho2) conf |= 1u << g;
+                }
+                m = conf;
+            }
             lq[lane] = m;
             c_lt += __popc(amask);
             c_lp += __popc(m);
         }
         __syncwarp();
-        // points of the tile: cell lower bounds (AMB-12), OR-marking the query bitmaps
         for (uint32_t pb = P0; pb < P1; pb += 32) {
             const uint32_t p = pb + lane;
             const int64_t pos = (int64_t)p - a.pos_base;
             uint32_t m = 0;
             if (p < P1) m = lq[a.ptl[pos]];
             if (__ballot_sync(0xffffffffu, m != 0) == 0) continue;    // whole warp pruned by leaf LBs
-            float acc[RF_G];
-#pragma unroll
-            for (int g = 0; g < RF_G; ++g) acc[g] = 0.f;
+            c_pt += __popc(m);
+            uint4 c4 = make_uint4(0, 0, 0, 0);
+            uint32_t pass = m;
             if (m && a.mode == DETLSH_MODE_CELL) {
-                // terms summed in j order, as in the leaf bound, so leaf LB <= cell LB in fp32
                 if (KT == 16) {
-                    const uint4 c4 = *reinterpret_cast<const uint4*>(a.tcodes + pos * 16);
-#pragma unroll 1
-                    for (int w = 0; w < 4; ++w) {      // 4 codes per 32-bit word, j = 4w + b
+                    c4 = *reinterpret_cast<const uint4*>(a.tcodes + pos * 16);
+                    uint32_t acc0 = 0, acc1 = 0, acc2 = 0, acc3 = 0;   // 2 queries per word
+#pragma unroll
+                    for (int w = 0; w < 4; ++w) {
                         const uint32_t word = w == 0 ? c4.x : w == 1 ? c4.y : w == 2 ? c4.z : c4.w;
-                        const float4* row = s_lut + (w * 4) * N_r;
+                        const uint4* row = s_q16 + (w * 4) * N_r;
 #pragma unroll
                         for (int b = 0; b < 4; ++b) {
-                            const float4 v = row[b * N_r + ((word >> (8 * b)) & 255u)];
-                            acc[0] += v.x; acc[1] += v.y; acc[2] += v.z; acc[3] += v.w;
+                            const uint4 v = row[b * N_r + ((word >> (8 * b)) & 255u)];
+                            acc0 += v.x; acc1 += v.y; acc2 += v.z; acc3 += v.w;
                         }
                     }
-                } else {
-                    for (int j = 0; j < K; ++j) {
-                        const float4 v = s_lut[j * N_r + a.tcodes[pos * K + j]];
-                        acc[0] += v.x; acc[1] += v.y; acc[2] += v.z; acc[3] += v.w;
-                    }
-                }
-            }
-            uint32_t id = 0;
-            bool have_id = false;
+                    const uint32_t accs[4] = {acc0, acc1, acc2, acc3};
+                    uint32_t ok = 0;
 #pragma unroll
-            for (int g = 0; g < RF_G; ++g) {
-                const bool mine = (m >> g) & 1;
-                const bool pass = mine && (a.mode != DETLSH_MODE_CELL || acc[g] <= rho2);
-                c_pt[g] += mine;
-                c_pp[g] += pass;
-                if (pass) {
-                    if (!have_id) { id = a.perm[pos]; have_id = true; }
+                    for (int g = 0; g < RF_G; ++g)
+                        ok |= (((accs[g >> 1] >> (16 * (g & 1))) & 0xFFFFu) <= RF_QT ? 1u : 0u) << g;
+                    pass = m & ok;
+                } else {
+                    uint32_t acc[RF_G];
+#pragma unroll
+                    for (int g = 0; g < RF_G; ++g) acc[g] = 0;
+                    for (int j = 0; j < K; ++j) {
+                        const uint4 v = s_q16[j * N_r + a.tcodes[pos * K + j]];
+                        const uint32_t vw[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                        for (int g = 0; g < RF_G; ++g) acc[g] += (vw[g >> 1] >> (16 * (g & 1))) & 0xFFFFu;
+                    }
+                    uint32_t ok = 0;
+#pragma unroll
+                    for (int g = 0; g < RF_G; ++g) ok |= (acc[g] <= RF_QT ? 1u : 0u) << g;
+                    pass = m & ok;
+                }
+                // exact fp32 confirmation of the screened pairs (cell LB summed in j order)
+                uint32_t conf = 0;
+                while (pass) {
+                    const int g = __ffs(pass) - 1;
+                    pass &= pass - 1;
+                    const float* D = a.lut + (int64_t)s_q[g] * per_q + (int64_t)a.t * K * N_r;
+                    float s_ = 0.f;
+                    if (KT == 16) {
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) {
+                            const uint32_t word = (j >> 2) == 0 ? c4.x : (j >> 2) == 1 ? c4.y : (j >> 2) == 2 ? c4.z : c4.w;
+                            s_ += __ldg(D + j * N_r + ((word >> (8 * (j & 3))) & 255u));
+                        }
+                    } else {
+                        for (int j = 0; j < K; ++j) s_ += __ldg(D + j * N_r + a.tcodes[pos * K + j]);
+                    }
+                    if (s_ <= rho2) conf |= 1u << g;
+                }
+                pass = conf;
+            }
+            if (pass) {
+                c_pp += __popc(pass);
+                const uint32_t id = a.perm[pos];
+                while (pass) {
+                    const int g = __ffs(pass) - 1;
+                    pass &= pass - 1;
                     atomicOr(a.bitmap + (int64_t)s_q[g] * a.nwords + (id >> 5), 1u << (id & 31));  // RED.OR
                 }
             }
         }
         __syncwarp();
     }
-    // ---- counters
+    // ---- counters (point counters are per group as well; attributed evenly)
     {
-        uint32_t v[2 + 2 * RF_G];
-        v[0] = c_lt;
-        v[1] = c_lp;
+        uint32_t v[4] = {c_lt, c_lp, c_pt, c_pp};
 #pragma unroll
-        for (int g = 0; g < RF_G; ++g) { v[2 + g] = c_pt[g]; v[2 + RF_G + g] = c_pp[g]; }
-#pragma unroll
-        for (int i = 0; i < 2 + 2 * RF_G; ++i)
+        for (int i = 0; i < 4; ++i)
             for (int o = 16; o > 0; o >>= 1) v[i] += __shfl_xor_sync(0xffffffffu, v[i], o);
         if (lane == 0) {
             const int na_ = max(1, __popc(amask));
-#pragma unroll
-            for (int g = 0; g < RF_G; ++g) {   // leaf counts are per group: attributed evenly
-                atomicAdd(&s_ctr[g][0], v[0] / na_);
-                atomicAdd(&s_ctr[g][1], v[1] / na_);
-                atomicAdd(&s_ctr[g][2], v[2 + g]);
-                atomicAdd(&s_ctr[g][3], v[2 + RF_G + g]);
-            }
+            for (int g = 0; g < RF_G; ++g)
+                if ((amask >> g) & 1)
+                    for (int i = 0; i < 4; ++i) atomicAdd(&s_ctr[g][i], v[i] / na_);
         }
     }
     __syncthreads();
@@ -630,6 +683,14 @@ __global__ void k_init_batch(QState* __restrict__ qs, int* __restrict__ act, int
     }
 }
 
+// 2048 / rho2 rounded toward zero (a lower bound of the exact scale factor).
+float fdiv_rd_host(float num, float den) {
+    const double x = (double)num / (double)den;
+    float f = (float)x;
+    if (std::isfinite(x) && (double)f > x) f = std::nextafterf(f, 0.0f);
+    return f;
+}
+
 }  // namespace
 
 void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArgs& a, int64_t* d_ids,
@@ -708,7 +769,8 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
     // per-batch LUTs
     Scratch s_lut(st, sizeof(float) * (size_t)(qb * LK * ix.N_r));
     Scratch s_sx(st, (size_t)(qb * LK));
-    const size_t rf_smem = sizeof(float) * (size_t)RF_G * ix.K * ix.N_r;
+    const size_t rf_smem = sizeof(uint16_t) * (size_t)RF_G * ix.K * ix.N_r;
+    Scratch s_qlut(st, sizeof(uint16_t) * (size_t)(qb * LK * ix.N_r));
     auto k_range_filter_sel = (ix.K == 16 && ix.N_r == 256) ? k_range_filter<16, 256> : k_range_filter<0, 0>;
     DL_CUDA(cudaFuncSetAttribute(k_range_filter_sel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rf_smem));
     RFArgs ra;
@@ -717,6 +779,7 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
     ra.hi = ix.leaf_hi.as<uint8_t>();
     ra.tile_leaf = ix.tile_leaf.as<uint32_t>();
     ra.lut = s_lut.as<float>();
+    ra.qlut = s_qlut.as<uint16_t>();
     ra.sx = s_sx.as<uint8_t>();
     ra.qs = s_qs.as<QState>();
     ra.bitmap = s_bm.as<uint32_t>();
@@ -772,6 +835,12 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
             const double r = radii[m];
             const float rho2 = (float)((eps * r) * (eps * r));
             const float cr2 = (float)((a.c * r) * (a.c * r));
+            {   // quantised screen of this round: scale 2048 / rho^2 rounded down
+                const float inv_rd = fdiv_rd_host((float)RF_QT, rho2);
+                const int64_t per_q = LK * ix.N_r;
+                DL_LAUNCH(k_build_qlut, (unsigned)std::min<int64_t>(ceil_div(na * per_q, 256), 148 * 32), 256, 0, st,
+                          s_lut.as<float>(), cur, na, per_q, inv_rd, s_qlut.as<uint16_t>());
+            }
             for (int t = 0; t < ix.L; ++t) {
                 ra.tcodes = ix.tcodes.as<uint8_t>() + (int64_t)t * n * ix.K;
                 ra.perm = ix.perm.as<uint32_t>() + (int64_t)t * n;

@@ -198,7 +198,7 @@ detlsh_status detlsh_build_ex(const float* data, int64_t n, int32_t d, int32_t L
         if (o.borrow_data && dev && d % 8 == 0) {
             ix->Xp = data;
         } else {
-            ix->X.alloc(sizeof(float) * (size_t)n * ix->ld);
+            ix->X.alloc(sizeof(float) * (size_t)n * ix->ld, st);
             stage_rows(data, n, d, ix->ld, ix->X.as<float>(), st);
             ix->Xp = ix->X.as<float>();
         }

@@ -652,11 +652,12 @@ static void encode_all(const Index& ix, const float* d_P, int64_t m, uint8_t* d_
 // B5 + B6 for all L trees at once, from codes EP[n][LK] (data order).  Returns false if the
 // leaf list overflowed its capacity (the caller retries with a larger factor).
 static bool build_trees_try(Index& ix, const uint8_t* d_EP, int64_t leaf_factor, cudaStream_t st) {
+    Trace tr("trees");
     const int64_t n = ix.n, L = ix.L, total = n * L;
     const int K = ix.K, nb = ix.nb, LK = ix.LK, max_size = ix.max_size;
     DL_REQUIRE(total < (int64_t)0xFFFFFFFF, "L*n must be < 2^32");
 
-    ix.perm.alloc(sizeof(uint32_t) * (size_t)total);
+    ix.perm.alloc(sizeof(uint32_t) * (size_t)total, st);
     Scratch s_sort(st, sizeof(uint32_t) * (size_t)(3 * total));
     uint32_t* keys0 = s_sort.as<uint32_t>();
     uint32_t* keys1 = keys0 + total;
@@ -697,6 +698,7 @@ static bool build_trees_try(Index& ix, const uint8_t* d_EP, int64_t leaf_factor,
               max_size, act, n_act, (uint32_t)cap_active, leaves, n_leaves, (uint32_t)cap_leaves);
     s_starts.free_();
 
+    tr.mark("first layer sort+segments", st);
     // B6: level loop
     Scratch s_level(st, sizeof(uint32_t) * (size_t)(4 * cap_active + 4));
     int* split = s_level.as<int>();
@@ -738,6 +740,7 @@ static bool build_trees_try(Index& ix, const uint8_t* d_EP, int64_t leaf_factor,
     s_tmp.free_();
     s_zc.free_();
     s_level.free_();
+    tr.mark("split levels", st);
 
     // leaves in canonical order = ascending start position (DFS, 0-child first, keys ascending)
     const int64_t nl = d2h(n_leaves, st);
@@ -752,10 +755,10 @@ static bool build_trees_try(Index& ix, const uint8_t* d_EP, int64_t leaf_factor,
     while (bits < 32 && ((int64_t)1 << bits) < total) ++bits;
     bits = (int)round_up(bits, 8);
     bool lf = radix_sort_batched(lk0, lv0, lk1, lv1, nl, 1, bits, st);
-    ix.leaf_off.alloc(sizeof(uint32_t) * (size_t)(nl + 1));
-    ix.leaf_lo.alloc((size_t)nl * K);
-    ix.leaf_hi.alloc((size_t)nl * K);
-    ix.leaf_bits.alloc((size_t)nl * K);
+    ix.leaf_off.alloc(sizeof(uint32_t) * (size_t)(nl + 1), st);
+    ix.leaf_lo.alloc((size_t)nl * K, st);
+    ix.leaf_hi.alloc((size_t)nl * K, st);
+    ix.leaf_bits.alloc((size_t)nl * K, st);
     DL_LAUNCH(k_leaf_finalize, grid_for(nl, 256), 256, 0, st, leaves, lf ? lv1 : lv0, nl, perm, d_EP, n, LK, K, nb,
               ix.leaf_off.as<uint32_t>(), ix.leaf_lo.as<uint8_t>(), ix.leaf_hi.as<uint8_t>(),
               ix.leaf_bits.as<uint8_t>(), total);
@@ -763,11 +766,12 @@ static bool build_trees_try(Index& ix, const uint8_t* d_EP, int64_t leaf_factor,
     DL_LAUNCH(k_tree_begin, 1, 64, 0, st, ix.leaf_off.as<uint32_t>(), nl, n, (int)L, s_begin.as<unsigned long long>());
     std::vector<unsigned long long> begin(L + 1);
     DL_CUDA(cudaMemcpyAsync(begin.data(), s_begin.p, sizeof(unsigned long long) * (L + 1), cudaMemcpyDeviceToHost, st));
-    ix.tcodes.alloc((size_t)total * K);
+    ix.tcodes.alloc((size_t)total * K, st);
     DL_LAUNCH(k_gather_tcodes, grid_for(total, 256), 256, 0, st, perm, d_EP, n, (int)L, K, ix.tcodes.as<uint8_t>());
     DL_CUDA(cudaStreamSynchronize(st));
     ix.tree_leaf_begin.assign(begin.begin(), begin.end());
     ix.tree_leaf_begin[L] = nl;
+    tr.mark("leaf finalize+codes", st);
     // query tiles
     {
         Scratch s_tf(st, sizeof(uint32_t) * (size_t)(2 * nl + 2));
@@ -779,7 +783,7 @@ static bool build_trees_try(Index& ix, const uint8_t* d_EP, int64_t leaf_factor,
                   s_begin.as<unsigned long long>(), tf);
         exclusive_scan_u32(tf, tidx, nl, ntiles_d, st);
         const int64_t ntiles = d2h(ntiles_d, st);
-        ix.tile_leaf.alloc(sizeof(uint32_t) * (size_t)(ntiles + 1));
+        ix.tile_leaf.alloc(sizeof(uint32_t) * (size_t)(ntiles + 1), st);
         DL_LAUNCH(k_tile_write, grid_for(nl, 256), 256, 0, st, tf, tidx, nl, ix.tile_leaf.as<uint32_t>());
         const uint32_t last = (uint32_t)nl;
         DL_CUDA(cudaMemcpyAsync(ix.tile_leaf.as<uint32_t>() + ntiles, &last, sizeof(uint32_t), cudaMemcpyHostToDevice, st));
@@ -787,7 +791,7 @@ static bool build_trees_try(Index& ix, const uint8_t* d_EP, int64_t leaf_factor,
         Scratch s_tb(st, sizeof(unsigned long long) * (size_t)(L + 1));
         DL_LAUNCH(k_tree_tiles, 1, 64, 0, st, tidx, s_begin.as<unsigned long long>(), (int)L, (uint32_t)ntiles,
                   s_tb.as<unsigned long long>());
-        ix.point_tile_leaf.alloc(sizeof(uint16_t) * (size_t)total);
+        ix.point_tile_leaf.alloc(sizeof(uint16_t) * (size_t)total, st);
         DL_LAUNCH(k_point_tile_leaf, grid_for(nl, 256), 256, 0, st, ix.leaf_off.as<uint32_t>(), ix.tile_leaf.as<uint32_t>(),
                   ntiles, nl, ix.point_tile_leaf.as<uint16_t>());
         std::vector<unsigned long long> tb(L + 1);
@@ -795,6 +799,7 @@ static bool build_trees_try(Index& ix, const uint8_t* d_EP, int64_t leaf_factor,
         DL_CUDA(cudaStreamSynchronize(st));
         ix.tree_tile_begin.assign(tb.begin(), tb.end());
     }
+    tr.mark("tiles", st);
     return true;
 }
 
@@ -807,21 +812,22 @@ static void build_trees(Index& ix, const uint8_t* d_EP, cudaStream_t st) {
 
 void build_index(Index& ix, const float* d_data, int64_t data_ld, const float* bp_given, double sample_frac,
                  int proj_impl, cudaStream_t st) {
+    Trace tr("build");
     const int64_t n = ix.n;
     // B0: hash family
-    ix.A.alloc(sizeof(float) * (size_t)ix.LK * ix.ld);
+    ix.A.alloc(sizeof(float) * (size_t)ix.LK * ix.ld, st);
     DL_LAUNCH(k_hash_family, grid_for((int64_t)ix.LK * ix.ld, 256), 256, 0, st, ix.seed, ix.LK, ix.d, ix.ld,
               ix.A.as<float>());
     Scratch s_flag(st, sizeof(int));
     DL_CUDA(cudaMemsetAsync(s_flag.p, 0, sizeof(int), st));
     // B1-B3: breakpoints
-    ix.B.alloc(sizeof(float) * (size_t)ix.LK * (ix.N_r + 1));
+    ix.B.alloc(sizeof(float) * (size_t)ix.LK * (ix.N_r + 1), st);
     if (bp_given) {
         DL_CUDA(cudaMemcpyAsync(ix.B.p, bp_given, ix.B.bytes, cudaMemcpyDefault, st));
         ix.n_s = 0;
     } else {
         const int64_t n_s = detlsh_sample_size(n, ix.N_r, sample_frac);
-        ix.sample.alloc(sizeof(uint32_t) * (size_t)n_s);
+        ix.sample.alloc(sizeof(uint32_t) * (size_t)n_s, st);
         int64_t got = 0;
         sample_ids_device(ix.seed, 0, n, n, n_s, ix.sample.as<uint32_t>(), &got, st);
         DL_REQUIRE(got == n_s, "sample selection returned the wrong count");
@@ -831,8 +837,10 @@ void build_index(Index& ix, const float* d_data, int64_t data_ld, const float* b
         DL_LAUNCH(k_gather_rows, grid_for(n_s * 32, 256), 256, 0, st, d_data, data_ld, ix.sample.as<uint32_t>(), n_s,
                   s_xs.as<float>());
         project_rows(ix, s_xs.as<float>(), data_ld, n_s, s_ps.as<float>(), proj_impl, s_flag.as<int>(), st);
+        tr.mark("sample+sample projection", st);
         breakpoints_from_projections(s_ps.as<float>(), n_s, ix.LK, ix.N_r, ix.B.as<float>(), st);
     }
+    tr.mark("breakpoints", st);
     // B2 + B4: project every row and encode (chunked so P stays bounded)
     Scratch s_ep(st, (size_t)n * ix.LK);
     {
@@ -846,14 +854,16 @@ void build_index(Index& ix, const float* d_data, int64_t data_ld, const float* b
     }
     const int nonfinite = d2h(s_flag.as<int>(), st);
     DL_REQUIRE(!nonfinite, "data contains NaN or Inf");
+    tr.mark("project+encode", st);
     // B5 + B6
     build_trees(ix, s_ep.as<uint8_t>(), st);
+    tr.mark("trees", st);
 }
 
 void build_trees_from_codes(Index& ix, const uint8_t* d_codes, cudaStream_t st) { build_trees(ix, d_codes, st); }
 
 void build_index_hash_only(Index& ix, cudaStream_t st) {
-    ix.A.alloc(sizeof(float) * (size_t)ix.LK * ix.ld);
+    ix.A.alloc(sizeof(float) * (size_t)ix.LK * ix.ld, st);
     DL_LAUNCH(k_hash_family, grid_for((int64_t)ix.LK * ix.ld, 256), 256, 0, st, ix.seed, ix.LK, ix.d, ix.ld,
               ix.A.as<float>());
 }

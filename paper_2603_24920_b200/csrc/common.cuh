@@ -101,6 +101,16 @@ bool radix_sort_batched(uint32_t* k0, uint32_t* v0, uint32_t* k1, uint32_t* v1, 
 void exclusive_scan_u32(const uint32_t* in, uint32_t* out, int64_t n, uint32_t* d_total,
                         cudaStream_t st);
 
+// ------------------------------------------------------------------ host phase trace
+// DETLSH_TRACE=1: print host wall time per phase (synchronising the stream at each mark).
+struct Trace {
+    bool on;
+    double t0, last;
+    const char* what;
+    explicit Trace(const char* w);
+    void mark(const char* phase, cudaStream_t st);
+};
+
 // ------------------------------------------------------------------ scratch allocation
 // Stream-ordered device scratch (cudaMallocAsync from the device pool).
 struct Scratch {

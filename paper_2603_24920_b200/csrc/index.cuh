@@ -7,6 +7,8 @@
 
 namespace detlsh {
 
+// Index-owned device memory, stream-ordered from the device pool (no device-wide sync on
+// allocate/free); freed on the legacy default stream.
 struct DevBuf {
     void* p = nullptr;
     size_t bytes = 0;
@@ -14,13 +16,13 @@ struct DevBuf {
     DevBuf(const DevBuf&) = delete;
     DevBuf& operator=(const DevBuf&) = delete;
     ~DevBuf() { reset(); }
-    void alloc(size_t b) {
+    void alloc(size_t b, cudaStream_t st = 0) {
         reset();
-        if (b) DL_CUDA(cudaMalloc(&p, b));
+        if (b) DL_CUDA(cudaMallocAsync(&p, b, st));
         bytes = b;
     }
     void reset() {
-        if (p) cudaFree(p);
+        if (p) cudaFreeAsync(p, 0);
         p = nullptr;
         bytes = 0;
     }

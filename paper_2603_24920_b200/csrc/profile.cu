@@ -1,6 +1,8 @@
 // profile.cu -- per-kernel CUDA-event timing behind detlsh_profile_* (bench.py's live
 // roofline numbers).  Off by default; when on, every DL_LAUNCH records an event pair on
 // its own stream.
+#include <chrono>
+#include <cstdlib>
 #include <map>
 #include <mutex>
 #include <string>
@@ -65,6 +67,20 @@ void profile_begin(cudaStream_t st, const char* name, int* slot) {
 void profile_end(cudaStream_t st, int slot) {
     std::lock_guard<std::mutex> lk(g_mu);
     if (slot < (int)g_recs.size()) cudaEventRecord(g_recs[slot].b, st);
+}
+
+static double now_ms() {
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+Trace::Trace(const char* w) : on(std::getenv("DETLSH_TRACE") != nullptr), t0(now_ms()), last(t0), what(w) {}
+
+void Trace::mark(const char* phase, cudaStream_t st) {
+    if (!on) return;
+    cudaStreamSynchronize(st);
+    const double t = now_ms();
+    std::fprintf(stderr, "[detlsh %s] %-28s %8.3f ms (total %8.3f)\n", what, phase, t - last, t - t0);
+    last = t;
 }
 
 }  // namespace detlsh

@@ -810,6 +810,9 @@ static void build_trees(Index& ix, const uint8_t* d_EP, cudaStream_t st) {
     }
 }
 
+bool project_encode_tc(const Index& ix, const float* d_X, int64_t ld, int64_t m, uint8_t* d_EP, int* d_nonfinite,
+                       cudaStream_t st);
+
 void build_index(Index& ix, const float* d_data, int64_t data_ld, const float* bp_given, double sample_frac,
                  int proj_impl, cudaStream_t st) {
     Trace tr("build");
@@ -841,9 +844,10 @@ void build_index(Index& ix, const float* d_data, int64_t data_ld, const float* b
         breakpoints_from_projections(s_ps.as<float>(), n_s, ix.LK, ix.N_r, ix.B.as<float>(), st);
     }
     tr.mark("breakpoints", st);
-    // B2 + B4: project every row and encode (chunked so P stays bounded)
+    // B2 + B4: project every row and encode -- fused in the tensor-core epilogue when the
+    // shape fits, else projection (chunked so P stays bounded) + k_encode
     Scratch s_ep(st, (size_t)n * ix.LK);
-    {
+    if (!(proj_impl == 0 && project_encode_tc(ix, d_data, data_ld, n, s_ep.as<uint8_t>(), s_flag.as<int>(), st))) {
         const int64_t chunk = std::min<int64_t>(n, std::max<int64_t>(1 << 16, (int64_t)(1ll << 30) / (4 * ix.LK)));
         Scratch s_p(st, sizeof(float) * (size_t)(chunk * ix.LK));
         for (int64_t r0 = 0; r0 < n; r0 += chunk) {

@@ -98,11 +98,13 @@ struct TcShape {
     int LK, npad;     // output columns, padded to a multiple of 16
     int stages;
     uint32_t tmem_cols;
+    int N_r;          // > 0: fused Alg. 1 encode, codes instead of projections
 };
 
 __global__ void __launch_bounds__(TC_THREADS, 1)
     k_project_tc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmA, TcShape sh,
-                 float* __restrict__ P, int* __restrict__ nonfinite) {
+                 float* __restrict__ P, int* __restrict__ nonfinite, const float* __restrict__ B,
+                 uint8_t* __restrict__ EP) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     // 1024-byte alignment of every swizzled buffer
     unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -110,7 +112,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     unsigned char* sB = base;                                            // nkb x [npad][128 B]
     unsigned char* sX = sB + (size_t)sh.nkb * sh.npad * 128;              // S x 16 KB
     unsigned char* sL = sX + (size_t)S * TC_STAGE_BYTES;                  // S x 16 KB (lo parts)
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sL + (size_t)S * TC_STAGE_BYTES);
+    float* sT = reinterpret_cast<float*>(sL + (size_t)S * TC_STAGE_BYTES);   // encode table [LK][N_r]
+    const int tab_floats = sh.N_r > 0 ? sh.LK * sh.N_r : 0;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sT + tab_floats);
     uint64_t* full = bars;              // [S] TMA -> converters, MMA
     uint64_t* conv = bars + S;          // [S] converters -> MMA
     uint64_t* empty = bars + 2 * S;     // [S] MMA commit -> producer
@@ -223,9 +227,17 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         }
         if (bad) atomicOr(nonfinite, 1);
     } else {
-        // epilogue: TMEM -> registers -> P rows
+        // epilogue: TMEM -> registers -> P rows, or (fused Alg. 1) -> 8-bit codes
         const int ew = warp - 4;                           // TMEM lane quarter
         const int row_in_tile = ew * 32 + lane;
+        const int N_r = sh.N_r;
+        if (N_r > 0) {   // breakpoint table: c[r][t] = b_{t+1} (t < N_r-1), c[r][N_r-1] = +inf (AMB-6/7)
+            for (int i = threadIdx.x - 128; i < tab_floats; i += 128) {
+                const int r = i / N_r, t = i - r * N_r;
+                sT[i] = t < N_r - 1 ? B[(int64_t)r * (N_r + 1) + t + 1] : __int_as_float(0x7f800000);
+            }
+            asm volatile("bar.sync 1, 128;" ::: "memory");  // epilogue warps only
+        }
         int buf = 0;
         uint32_t tph = 0;
         for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
@@ -236,7 +248,28 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             for (int c0 = 0; c0 < sh.npad; c0 += 16) {
                 float v[16];
                 tmem_ld16(taddr + c0, v);
-                if (row < sh.m) {
+                if (N_r > 0) {
+                    // code = #{t in 1..N_r-1 : b_t < x}: branch-free lower bound over the table
+                    uint32_t packed[4] = {0, 0, 0, 0};
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) {
+                        const int r = c0 + i;
+                        int pos = 0;
+                        if (r < sh.LK) {
+                            const float* t = sT + r * N_r;
+                            for (int s = N_r >> 1; s > 0; s >>= 1) pos += (t[pos + s - 1] < v[i]) ? s : 0;
+                        }
+                        packed[i >> 2] |= (uint32_t)pos << (8 * (i & 3));
+                    }
+                    if (row < sh.m) {
+                        uint8_t* out = EP + row * sh.LK + c0;
+                        if (c0 + 16 <= sh.LK && (sh.LK & 15) == 0) {
+                            *reinterpret_cast<uint4*>(out) = make_uint4(packed[0], packed[1], packed[2], packed[3]);
+                        } else {
+                            for (int i = 0; i < 16 && c0 + i < sh.LK; ++i) out[i] = (uint8_t)(packed[i >> 2] >> (8 * (i & 3)));
+                        }
+                    }
+                } else if (row < sh.m) {
                     float* out = P + row * sh.LK + c0;
                     if (c0 + 16 <= sh.LK && (sh.LK & 3) == 0) {
 #pragma unroll
@@ -289,8 +322,9 @@ void make_map(CUtensorMap* map, const float* ptr, int64_t rows, int ld, int box_
 }  // namespace
 
 // Returns false when the shape does not fit this kernel (resident hash matrix too large).
-bool project_rows_tc(const Index& ix, const float* d_X, int64_t ld, int64_t m, float* d_P, int* d_nonfinite,
-                     cudaStream_t st) {
+// B != nullptr: fused encode (Alg. 1) -- writes codes EP[m][LK] instead of P.
+static bool launch_tc(const Index& ix, const float* d_X, int64_t ld, int64_t m, float* d_P, int* d_nonfinite,
+                      const float* B, uint8_t* EP, cudaStream_t st) {
     if (m <= 0) return true;
     TcShape sh;
     sh.m = m;
@@ -298,16 +332,18 @@ bool project_rows_tc(const Index& ix, const float* d_X, int64_t ld, int64_t m, f
     sh.nkb = (int)ceil_div(ld, TC_KB);
     sh.LK = ix.LK;
     sh.npad = (int)round_up(ix.LK, 16);
+    sh.N_r = B ? ix.N_r : 0;
     if (sh.npad > 256) return false;
     const size_t bbytes = (size_t)sh.nkb * sh.npad * 128;
+    const size_t tbytes = B ? sizeof(float) * (size_t)ix.LK * ix.N_r : 0;
     const size_t fixed = 1024 /*align*/ + 256 /*barriers*/;
     const size_t budget = 227 * 1024;
-    if (bbytes + fixed + 2 * 2 * TC_STAGE_BYTES > budget) return false;
-    sh.stages = (int)std::min<size_t>(6, (budget - bbytes - fixed) / (2 * TC_STAGE_BYTES));
+    if (bbytes + tbytes + fixed + 2 * 2 * TC_STAGE_BYTES > budget) return false;
+    sh.stages = (int)std::min<size_t>(6, (budget - bbytes - tbytes - fixed) / (2 * TC_STAGE_BYTES));
     uint32_t cols = 32;
     while (cols < (uint32_t)(2 * sh.npad)) cols <<= 1;
     sh.tmem_cols = cols;
-    const size_t smem = bbytes + (size_t)sh.stages * 2 * TC_STAGE_BYTES + fixed;
+    const size_t smem = bbytes + tbytes + (size_t)sh.stages * 2 * TC_STAGE_BYTES + fixed;
     CUtensorMap mx, ma;
     make_map(&mx, d_X, m, (int)ld, TC_M);
     make_map(&ma, ix.A.as<float>(), ix.LK, (int)ld, sh.npad);
@@ -321,8 +357,18 @@ bool project_rows_tc(const Index& ix, const float* d_X, int64_t ld, int64_t m, f
     DL_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
     const int64_t ntiles = ceil_div(m, TC_M);
     const int grid = (int)std::min<int64_t>(ntiles, nsm);
-    DL_LAUNCH(k_project_tc, grid, TC_THREADS, smem, st, mx, ma, sh, d_P, d_nonfinite);
+    DL_LAUNCH(k_project_tc, grid, TC_THREADS, smem, st, mx, ma, sh, d_P, d_nonfinite, B, EP);
     return true;
+}
+
+bool project_rows_tc(const Index& ix, const float* d_X, int64_t ld, int64_t m, float* d_P, int* d_nonfinite,
+                     cudaStream_t st) {
+    return launch_tc(ix, d_X, ld, m, d_P, d_nonfinite, nullptr, nullptr, st);
+}
+
+bool project_encode_tc(const Index& ix, const float* d_X, int64_t ld, int64_t m, uint8_t* d_EP, int* d_nonfinite,
+                       cudaStream_t st) {
+    return launch_tc(ix, d_X, ld, m, nullptr, d_nonfinite, ix.B.as<float>(), d_EP, st);
 }
 
 }  // namespace detlsh

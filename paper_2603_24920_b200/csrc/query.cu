@@ -31,8 +31,9 @@ enum : int { ST_ACTIVE = 0, ST_BUDGET = 1, ST_RADIUS = 2, ST_CAP = 3 };
 
 struct QState {  // per query of a batch
     int64_t cnt;        // |S| (bits set in the query's bitmap)
-    int64_t nlist;      // verified candidates written to the (id, d2) list
-    int64_t nver;       // list entries already merged into the top-k
+    int64_t nver;       // members of S verified and merged into the top-k
+    int64_t roff;       // this round's slot range [roff, roff + rcnt) in the round buffer
+    int64_t rcnt;
     int32_t status;     // ST_*
     int32_t tk;         // entries in the top-k list
     int32_t trees_last;
@@ -401,9 +402,8 @@ struct VRArgs {
     const uint32_t* cur;
     uint32_t* ver;
     int64_t nwords;
-    uint32_t* cand;
-    float* d2;
-    int64_t cap;
+    uint32_t* cand;          // round buffer: ids
+    float* d2;               // round buffer: squared distances
     int rbw;                 // bitmap words (32 rows each) per block
 };
 
@@ -454,7 +454,9 @@ __global__ void __launch_bounds__(VR_THREADS) k_verify_rows(VRArgs a) {
         const uint32_t tot = __shfl_sync(0xffffffffu, incl, 7);
         if (tot == 0) continue;
         unsigned long long base = 0;
-        if (lane == 0) base = atomicAdd(reinterpret_cast<unsigned long long*>(&a.qs[q].nlist), (unsigned long long)tot);
+        if (lane == 0)
+            base = (unsigned long long)a.qs[q].roff +
+                   atomicAdd(reinterpret_cast<unsigned long long*>(&a.qs[q].rcnt), (unsigned long long)tot);
         {
             uint32_t m = mw, p = incl - pc;
             while (m) {
@@ -475,8 +477,8 @@ __global__ void __launch_bounds__(VR_THREADS) k_verify_rows(VRArgs a) {
         }
         __syncwarp();
         const int64_t out = (int64_t)__shfl_sync(0xffffffffu, base, 0);
-        uint32_t* cl = a.cand + (int64_t)q * a.cap;
-        float* dl = a.d2 + (int64_t)q * a.cap;
+        uint32_t* cl = a.cand;
+        float* dl = a.d2;
         for (uint32_t i = 0; i < tot; i += 4) {
             const bool valid = i + slot < tot;
             const int r = lst[valid ? i + slot : i];
@@ -506,13 +508,57 @@ __global__ void __launch_bounds__(VR_THREADS) k_verify_rows(VRArgs a) {
             s_ += __shfl_xor_sync(0xffffffffu, s_, 1);
             s_ += __shfl_xor_sync(0xffffffffu, s_, 2);
             s_ += __shfl_xor_sync(0xffffffffu, s_, 4);
-            if (valid && u == 0 && out + i + slot < a.cap) {
+            if (valid && u == 0) {
                 cl[out + i + slot] = (uint32_t)(row0 + r);
                 dl[out + i + slot] = s_;
             }
         }
         __syncwarp();
     }
+}
+
+// ---- per round: slot ranges of the new members of S (|S| - verified) in the round buffer
+__global__ void __launch_bounds__(1024) k_round_offsets(const int* __restrict__ act, int na, QState* __restrict__ qs,
+                                                        unsigned long long* __restrict__ total) {
+    __shared__ unsigned long long s_w[32];
+    __shared__ unsigned long long s_run;
+    if (threadIdx.x == 0) s_run = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (int base = 0; base < na; base += 1024) {
+        const int a_ = base + threadIdx.x;
+        unsigned long long c = 0;
+        if (a_ < na) {
+            const QState s = qs[act[a_]];
+            c = (unsigned long long)(s.cnt - s.nver);
+        }
+        unsigned long long x = c;
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) s_w[w] = x;
+        __syncthreads();
+        if (w == 0) {
+            unsigned long long v = s_w[lane];
+            for (int o = 1; o < 32; o <<= 1) {
+                const unsigned long long y = __shfl_up_sync(0xffffffffu, v, o);
+                if (lane >= o) v += y;
+            }
+            s_w[lane] = v;
+        }
+        __syncthreads();
+        const unsigned long long incl = x + (w ? s_w[w - 1] : 0ull);
+        if (a_ < na) {
+            QState* s = &qs[act[a_]];
+            s->roff = (int64_t)(s_run + incl - c);
+            s->rcnt = 0;
+        }
+        __syncthreads();
+        if (threadIdx.x == 1023) s_run += incl;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *total = s_run;
 }
 
 // ---- top-k merge + termination test
@@ -541,7 +587,7 @@ __device__ void bitonic_sort_smem(unsigned long long* a, int n2) {
 
 __global__ void __launch_bounds__(TK_THREADS) k_topk(const int* __restrict__ act, QState* __restrict__ qs,
                                                      const uint32_t* __restrict__ cand, const float* __restrict__ d2,
-                                                     int64_t cap, unsigned long long* __restrict__ topk, int k,
+                                                     unsigned long long* __restrict__ topk, int k,
                                                      float cr2, int round) {
     __shared__ unsigned long long s_keys[TK_MAX];
     __shared__ uint32_t s_hist[256];
@@ -550,9 +596,9 @@ __global__ void __launch_bounds__(TK_THREADS) k_topk(const int* __restrict__ act
     const int q = act[blockIdx.x];
     QState s = qs[q];
     unsigned long long* tk = topk + (int64_t)q * k;
-    const uint32_t* cl = cand + (int64_t)q * cap;
-    const float* dl = d2 + (int64_t)q * cap;
-    const int64_t old = s.tk, e0 = s.nver, nn = s.nlist - s.nver, M = old + nn;
+    const uint32_t* cl = cand;
+    const float* dl = d2;
+    const int64_t old = s.tk, e0 = s.roff, nn = s.rcnt, M = old + nn;
     auto key_at = [&](int64_t i) -> unsigned long long {
         return i < old ? tk[i] : mkkey(dl[e0 + i - old], cl[e0 + i - old]);
     };
@@ -604,7 +650,8 @@ __global__ void __launch_bounds__(TK_THREADS) k_topk(const int* __restrict__ act
     for (int i = threadIdx.x; i < outn; i += TK_THREADS) tk[i] = s_keys[i];
     if (threadIdx.x == 0) {
         s.tk = outn;
-        s.nver = s.nlist;
+        s.nver += s.rcnt;
+        s.rcnt = 0;
         if (s.status == ST_ACTIVE) {
             if (outn >= k && __uint_as_float((uint32_t)(s_keys[k - 1] >> 32)) <= cr2) s.status = ST_RADIUS;  // line 9
             else if (round == 63) s.status = ST_CAP;                                                        // AMB-20
@@ -676,7 +723,7 @@ __global__ void k_finalize(const QState* __restrict__ qs, const unsigned long lo
 __global__ void k_init_batch(QState* __restrict__ qs, int* __restrict__ act, int nqb) {
     for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < nqb; q += gridDim.x * blockDim.x) {
         QState s;
-        s.cnt = 0; s.nlist = 0; s.nver = 0; s.status = ST_ACTIVE; s.tk = 0; s.trees_last = 0; s.rounds = 0;
+        s.cnt = 0; s.nver = 0; s.roff = 0; s.rcnt = 0; s.status = ST_ACTIVE; s.tk = 0; s.trees_last = 0; s.rounds = 0;
         s.overflow = 0; s.pad = 0;
         qs[q] = s;
         act[q] = q;
@@ -715,7 +762,8 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
     }
 
     // batch size from the memory budget: bitmap + candidate list + distances per query
-    const int64_t per_q = nwords * 12 + cap * 8 + (int64_t)k * 8 + (int64_t)LK * (ix.N_r * 4 + 1) + 96;
+    const int64_t per_q = nwords * 12 + (int64_t)k * 8 + (int64_t)LK * (ix.N_r * 6 + 1) + 96 +
+                          (int64_t)(std::min(1.0, a.beta * 2.0) * n) * 8;   // round buffer share
     int64_t budget_bytes = a.mem_budget;
     if (budget_bytes <= 0) {
         size_t fr = 0, tot = 0;
@@ -729,8 +777,9 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
     Scratch s_bm(st, sizeof(uint32_t) * (size_t)(2 * qb * nwords));   // current union + previous
     Scratch s_ctr(st, sizeof(unsigned long long) * (size_t)(4 * qb));
     Scratch s_ver(st, sizeof(uint32_t) * (size_t)(qb * nwords));     // verified members of S
-    Scratch s_cand(st, sizeof(uint32_t) * (size_t)(qb * cap));
-    Scratch s_d2(st, sizeof(float) * (size_t)(qb * cap));
+    Scratch s_round(st);                   // (id, d2) of this round's new members, grown on demand
+    int64_t round_cap = 0;
+    Scratch s_total(st, sizeof(unsigned long long));
     Scratch s_tk(st, sizeof(unsigned long long) * (size_t)(qb * k));
     Scratch s_qs(st, sizeof(QState) * (size_t)qb);
     Scratch s_act(st, sizeof(int) * (size_t)(2 * qb + 2));
@@ -800,9 +849,7 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
     va.cur = s_bm.as<uint32_t>();
     va.ver = s_ver.as<uint32_t>();
     va.nwords = nwords;
-    va.cand = s_cand.as<uint32_t>();
-    va.d2 = s_d2.as<float>();
-    va.cap = cap;
+
     {   // rows per block: as many 32-row words as fit in 120 KB of shared memory (1..8)
         const int64_t per_word = (int64_t)32 * ix.ld * 4;
         va.rbw = (int)std::max<int64_t>(1, std::min<int64_t>(8, (120 * 1024) / per_word));
@@ -862,6 +909,18 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
                 DL_LAUNCH(k_tree_end, (unsigned)ceil_div(na, 256), 256, 0, st, cur, na, s_qs.as<QState>(), t, m,
                           budget, cap);
             }
+            DL_LAUNCH(k_round_offsets, 1, 1024, 0, st, cur, na, s_qs.as<QState>(), s_total.as<unsigned long long>());
+            {
+                unsigned long long tot = 0;
+                DL_CUDA(cudaMemcpyAsync(&tot, s_total.p, sizeof(tot), cudaMemcpyDeviceToHost, st));
+                DL_CUDA(cudaStreamSynchronize(st));
+                if ((int64_t)tot > round_cap) {
+                    round_cap = (int64_t)(tot + tot / 2 + 1024);
+                    s_round.alloc((size_t)round_cap * 8);
+                }
+            }
+            va.cand = s_round.as<uint32_t>();
+            va.d2 = reinterpret_cast<float*>(s_round.as<uint32_t>() + round_cap);
             va.act = cur;
             va.na = na;
             {
@@ -878,8 +937,8 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
                     default: DL_LAUNCH(k_verify_rows<0 COMMA false>, nblocks, VR_THREADS, vr_smem, st, va); break;
                 }
             }
-            DL_LAUNCH(k_topk, (unsigned)na, TK_THREADS, 0, st, cur, s_qs.as<QState>(), s_cand.as<uint32_t>(),
-                      s_d2.as<float>(), cap, s_tk.as<unsigned long long>(), k, cr2, m);
+            DL_LAUNCH(k_topk, (unsigned)na, TK_THREADS, 0, st, cur, s_qs.as<QState>(), va.cand, va.d2,
+                      s_tk.as<unsigned long long>(), k, cr2, m);
             DL_LAUNCH(k_compact, 1, 1024, 0, st, cur, na, s_qs.as<QState>(), nxt, n_act);
             DL_CUDA(cudaMemcpyAsync(&na, n_act, sizeof(int), cudaMemcpyDeviceToHost, st));
             DL_CUDA(cudaStreamSynchronize(st));

@@ -31,6 +31,22 @@ void project_rows(const Index& ix, const float* d_X, int64_t ld, int64_t m, floa
     project_rows_simt(ix, d_X, ld, m, d_P, d_nonfinite, st);
 }
 
+cudaMemPool_t index_pool() {
+    static cudaMemPool_t pools[64] = {};
+    int dev = 0;
+    DL_CUDA(cudaGetDevice(&dev));
+    if (!pools[dev]) {
+        cudaMemPoolProps props = {};
+        props.allocType = cudaMemAllocationTypePinned;
+        props.location.type = cudaMemLocationTypeDevice;
+        props.location.id = dev;
+        DL_CUDA(cudaMemPoolCreate(&pools[dev], &props));
+        uint64_t thr = UINT64_MAX;
+        DL_CUDA(cudaMemPoolSetAttribute(pools[dev], cudaMemPoolAttrReleaseThreshold, &thr));
+    }
+    return pools[dev];
+}
+
 namespace {
 
 template <class F> detlsh_status guard(F&& f) {

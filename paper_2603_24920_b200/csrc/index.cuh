@@ -7,7 +7,11 @@
 
 namespace detlsh {
 
-// Index-owned device memory, stream-ordered from the device pool (no device-wide sync on
+// Pool for index-owned (long-lived) buffers, separate from the default pool that serves
+// per-call scratch, so the two lifetimes do not fragment each other (api.cu).
+cudaMemPool_t index_pool();
+
+// Index-owned device memory, stream-ordered from index_pool() (no device-wide sync on
 // allocate/free); freed on the legacy default stream.
 struct DevBuf {
     void* p = nullptr;
@@ -18,7 +22,7 @@ struct DevBuf {
     ~DevBuf() { reset(); }
     void alloc(size_t b, cudaStream_t st = 0) {
         reset();
-        if (b) DL_CUDA(cudaMallocAsync(&p, b, st));
+        if (b) DL_CUDA(cudaMallocFromPoolAsync(&p, b, index_pool(), st));
         bytes = b;
     }
     void reset() {

@@ -42,17 +42,6 @@ struct QState {  // per query of a batch
     int32_t pad;
 };
 
-struct TreeView {
-    const float* B;            // [LK][N_r+1]
-    const uint32_t* leaf_off;  // [nl+1]
-    const uint8_t* lo;         // [nl][K]
-    const uint8_t* hi;
-    const uint8_t* tcodes;     // [L*n][K]
-    const uint32_t* perm;      // [L*n]
-    const unsigned long long* tree_begin;  // [L+1]
-    int64_t n;
-    int L, K, N_r;
-};
 
 // ---- per-batch LUTs: D[q][t][j][s] = max(0, l_s - x, x - u_s)^2 for cell s = (b_s, b_{s+1}],
 //      l_0 = -inf, u_{N_r-1} = +inf (Fig. dist; AMB-7), and the query's own symbol
@@ -591,6 +580,9 @@ __global__ void __launch_bounds__(TK_THREADS) k_topk(const int* __restrict__ act
                                                      float cr2, int round) {
     __shared__ unsigned long long s_keys[TK_MAX];
     __shared__ uint32_t s_hist[256];
+    uint32_t* s_h12 = reinterpret_cast<uint32_t*>(s_keys);   // 4096 bins, dead before s_keys is filled
+    __shared__ uint32_t s_wsum[32];
+    __shared__ uint32_t s_bin, s_below;
     __shared__ unsigned long long s_prefix, s_mask, s_rem;
     __shared__ int s_n;
     const int q = act[blockIdx.x];
@@ -609,44 +601,107 @@ __global__ void __launch_bounds__(TK_THREADS) k_topk(const int* __restrict__ act
         for (int64_t i = threadIdx.x; i < M; i += TK_THREADS) s_keys[i] = key_at(i);
         outn = (int)M;
     } else {
-        // radix select of the k-th smallest key, 8 digits of 8 bits
-        for (int pass = 0; pass < 8; ++pass) {
-            const int shift = 56 - 8 * pass;
-            for (int i = threadIdx.x; i < 256; i += TK_THREADS) s_hist[i] = 0;
+        // pass 1: histogram of the top 12 key bits (sign, exponent, 3 mantissa bits of d2)
+        for (int i = threadIdx.x; i < 4096; i += TK_THREADS) s_h12[i] = 0;
+        __syncthreads();
+        for (int64_t i = threadIdx.x; i < M; i += TK_THREADS) atomicAdd(&s_h12[key_at(i) >> 52], 1u);
+        __syncthreads();
+        {   // the bin holding the k-th smallest key: block scan of 8 bins per thread
+            uint32_t loc[8], sum = 0;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) { loc[j] = s_h12[threadIdx.x * 8 + j]; sum += loc[j]; }
+            uint32_t x = sum;
+            const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+                if (lane >= o) x += y;
+            }
+            if (lane == 31) s_wsum[w] = x;
             __syncthreads();
-            const unsigned long long pre = s_prefix, msk = s_mask;
-            for (int64_t i = threadIdx.x; i < M; i += TK_THREADS) {
-                const unsigned long long key = key_at(i);
-                if ((key & msk) == pre) atomicAdd(&s_hist[(key >> shift) & 255u], 1u);
+            if (w == 0) {
+                uint32_t v = lane < TK_THREADS / 32 ? s_wsum[lane] : 0;
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t y = __shfl_up_sync(0xffffffffu, v, o);
+                    if (lane >= o) v += y;
+                }
+                if (lane < TK_THREADS / 32) s_wsum[lane] = v;
             }
             __syncthreads();
-            if (threadIdx.x == 0) {
-                unsigned long long cum = 0, rem = s_rem;
-                for (int dg = 0; dg < 256; ++dg) {
-                    if (cum + s_hist[dg] >= rem) {
-                        s_prefix = pre | ((unsigned long long)dg << shift);
-                        s_mask = msk | (0xFFull << shift);
-                        s_rem = rem - cum;
+            uint32_t before = x - sum + (w ? s_wsum[w - 1] : 0);
+            if (before < (uint32_t)k && before + sum >= (uint32_t)k) {
+                for (int j = 0; j < 8; ++j) {
+                    if (before + loc[j] >= (uint32_t)k) {
+                        s_bin = threadIdx.x * 8 + j;
+                        s_below = before;
                         break;
                     }
-                    cum += s_hist[dg];
+                    before += loc[j];
                 }
             }
             __syncthreads();
         }
-        const unsigned long long T = s_prefix;   // keys are unique: exactly k keys <= T
-        for (int64_t i = threadIdx.x; i < M; i += TK_THREADS) {
-            const unsigned long long key = key_at(i);
-            if (key <= T) s_keys[atomicAdd(&s_n, 1)] = key;
+        const uint32_t bin = s_bin, below = s_below, inbin = s_h12[bin];
+        __syncthreads();
+        if (below + inbin <= (uint32_t)TK_MAX) {
+            // pass 2: every key below or in that bin fits in shared memory; sort, keep k
+            for (int64_t i = threadIdx.x; i < M; i += TK_THREADS) {
+                const unsigned long long key = key_at(i);
+                if ((uint32_t)(key >> 52) <= bin) s_keys[atomicAdd(&s_n, 1)] = key;
+            }
+            __syncthreads();
+            outn = (int)(below + inbin);
+        } else {
+            // crowded bin: exact radix select of the k-th key inside it, 8-bit digits
+            if (threadIdx.x == 0) {
+                s_prefix = (unsigned long long)bin << 52;
+                s_mask = 0xFFFull << 52;
+                s_rem = (unsigned long long)(k - below);
+            }
+            __syncthreads();
+            for (int shift = 44; shift >= 0; shift -= 8) {
+                for (int i = threadIdx.x; i < 256; i += TK_THREADS) s_hist[i] = 0;
+                __syncthreads();
+                const unsigned long long pre = s_prefix, msk = s_mask;
+                for (int64_t i = threadIdx.x; i < M; i += TK_THREADS) {
+                    const unsigned long long key = key_at(i);
+                    if ((key & msk) == pre) atomicAdd(&s_hist[(key >> shift) & 255u], 1u);
+                }
+                __syncthreads();
+                if (threadIdx.x == 0) {
+                    unsigned long long cum = 0, rem = s_rem;
+                    for (int dg = 0; dg < 256; ++dg) {
+                        if (cum + s_hist[dg] >= rem) {
+                            s_prefix = pre | ((unsigned long long)dg << shift);
+                            s_mask = msk | (0xFFull << shift);
+                            s_rem = rem - cum;
+                            break;
+                        }
+                        cum += s_hist[dg];
+                    }
+                }
+                __syncthreads();
+            }
+            // the low 4 bits were never selected on (12 + 6*8 = 60): finish by exact compare
+            const unsigned long long T0 = s_prefix;
+            for (int64_t i = threadIdx.x; i < M; i += TK_THREADS) {
+                const unsigned long long key = key_at(i);
+                if (key < T0 + 16 && ((key >> 4) <= (T0 >> 4))) {
+                    const int slot = atomicAdd(&s_n, 1);
+                    if (slot < TK_MAX) s_keys[slot] = key;
+                }
+            }
+            __syncthreads();
+            outn = min(s_n, TK_MAX);
         }
-        outn = k;
     }
+    __syncthreads();
     __syncthreads();
     int n2 = 1;
     while (n2 < outn) n2 <<= 1;
     for (int i = outn + threadIdx.x; i < n2; i += TK_THREADS) s_keys[i] = ~0ull;
     __syncthreads();
     bitonic_sort_smem(s_keys, n2);
+    outn = min(outn, k);
     for (int i = threadIdx.x; i < outn; i += TK_THREADS) tk[i] = s_keys[i];
     if (threadIdx.x == 0) {
         s.tk = outn;
@@ -749,6 +804,7 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
     const int64_t nwords = ceil_div(n, 32);
     const int64_t cap = n;                                              // |S| <= n always
 
+    Trace tr("query");
     // Q0: project all queries once
     Scratch s_qp(st, sizeof(float) * (size_t)(nq * LK));
     Scratch s_flag(st, sizeof(int));
@@ -760,6 +816,7 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
         DL_CUDA(cudaStreamSynchronize(st));
         DL_REQUIRE(!bad, "queries contain NaN or Inf");
     }
+    tr.mark("project queries", st);
 
     // batch size from the memory budget: bitmap + candidate list + distances per query
     const int64_t per_q = nwords * 12 + (int64_t)k * 8 + (int64_t)LK * (ix.N_r * 6 + 1) + 96 +
@@ -797,23 +854,7 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
     }
     DL_CUDA(cudaMemcpyAsync(s_radii.p, radii.data(), sizeof(double) * 64, cudaMemcpyHostToDevice, st));
 
-    TreeView tv;
-    tv.B = ix.B.as<float>();
-    tv.leaf_off = ix.leaf_off.as<uint32_t>();
-    tv.lo = ix.leaf_lo.as<uint8_t>();
-    tv.hi = ix.leaf_hi.as<uint8_t>();
-    tv.tcodes = ix.tcodes.as<uint8_t>();
-    tv.perm = ix.perm.as<uint32_t>();
-    Scratch s_tb(st, sizeof(unsigned long long) * (size_t)(ix.L + 1));
-    {
-        std::vector<unsigned long long> tb(ix.tree_leaf_begin.begin(), ix.tree_leaf_begin.end());
-        DL_CUDA(cudaMemcpyAsync(s_tb.p, tb.data(), sizeof(unsigned long long) * tb.size(), cudaMemcpyHostToDevice, st));
-    }
-    tv.tree_begin = s_tb.as<unsigned long long>();
-    tv.n = n;
-    tv.L = ix.L;
-    tv.K = ix.K;
-    tv.N_r = ix.N_r;
+
 
     // per-batch LUTs
     Scratch s_lut(st, sizeof(float) * (size_t)(qb * LK * ix.N_r));
@@ -872,6 +913,7 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
         DL_CUDA(cudaMemsetAsync(s_bm.p, 0, sizeof(uint32_t) * (size_t)(2 * qb * nwords), st));
         DL_CUDA(cudaMemsetAsync(s_ver.p, 0, sizeof(uint32_t) * (size_t)(qb * nwords), st));
         DL_CUDA(cudaMemsetAsync(s_ctr.p, 0, sizeof(unsigned long long) * (size_t)(4 * qb), st));
+        tr.mark("batch setup", st);
         DL_LAUNCH(k_init_batch, (unsigned)ceil_div(nqb, 256), 256, 0, st, s_qs.as<QState>(), act, nqb);
         DL_LAUNCH(k_build_lut, (unsigned)std::min<int64_t>(ceil_div((int64_t)nqb * LK * ix.N_r, 256), 148 * 32), 256, 0,
                   st, Qpb, nqb, (int)LK, ix.N_r, ix.B.as<float>(), s_lut.as<float>(), s_sx.as<uint8_t>());
@@ -909,6 +951,7 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
                 DL_LAUNCH(k_tree_end, (unsigned)ceil_div(na, 256), 256, 0, st, cur, na, s_qs.as<QState>(), t, m,
                           budget, cap);
             }
+            tr.mark("filter (L trees)", st);
             DL_LAUNCH(k_round_offsets, 1, 1024, 0, st, cur, na, s_qs.as<QState>(), s_total.as<unsigned long long>());
             {
                 unsigned long long tot = 0;
@@ -937,13 +980,16 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
                     default: DL_LAUNCH(k_verify_rows<0 COMMA false>, nblocks, VR_THREADS, vr_smem, st, va); break;
                 }
             }
+            tr.mark("round buffer + verify", st);
             DL_LAUNCH(k_topk, (unsigned)na, TK_THREADS, 0, st, cur, s_qs.as<QState>(), va.cand, va.d2,
                       s_tk.as<unsigned long long>(), k, cr2, m);
+            tr.mark("top-k", st);
             DL_LAUNCH(k_compact, 1, 1024, 0, st, cur, na, s_qs.as<QState>(), nxt, n_act);
             DL_CUDA(cudaMemcpyAsync(&na, n_act, sizeof(int), cudaMemcpyDeviceToHost, st));
             DL_CUDA(cudaStreamSynchronize(st));
             std::swap(cur, nxt);
         }
+        tr.mark("rounds done", st);
         DL_LAUNCH(k_finalize, (unsigned)std::min<int64_t>(ceil_div((int64_t)nqb * k, 256), 148 * 16), 256, 0, st,
                   s_qs.as<QState>(), s_ctr.as<unsigned long long>(), s_tk.as<unsigned long long>(), nqb, k, ix.id_offset, s_radii.as<double>(),
                   d_ids + q0 * k, d_dists + q0 * k, d_stats ? d_stats + q0 : nullptr);

@@ -6,8 +6,8 @@ D = datagen.generate(2, nq=1000)
 c = D['cfg']
 Xd = torch.from_numpy(D['X']).cuda(); Qd = torch.from_numpy(D['Q']).cuda()
 o = P.default_opts(borrow_data=1)
-for it in range(4):
-    if it == 3: os.environ['DETLSH_TRACE'] = '1'
+for it in range(5):
+    if it >= 3: os.environ['DETLSH_TRACE'] = '1'
     torch.cuda.synchronize(); t = time.perf_counter()
     g = P.detlsh_build(Xd, c.L, c.K, c.N_r, c.index_seed, opts=o)
     torch.cuda.synchronize(); tb = time.perf_counter() - t

@@ -118,21 +118,44 @@ def peaks():
     return 6650.0, 1590.0, 1400.0, "fallback (B200_PROFILING.md)"
 
 
-def kernel_bytes(name: str, c, steps: int, st, n_local: int, nq: int) -> float | None:
-    """Algorithmic bytes of all launches of `name` in the timed region.
-    `st` = per-query stats of one step (identical every step: the computation is deterministic)."""
+def kernel_models(c, steps: int, st, n_local: int, nq: int, ld: int):
+    """Algorithmic work of all launches of each modelled kernel in the timed region
+    (DESIGN.md §5).  `st` = per-query stats of one step (the computation is deterministic,
+    every step does the same work)."""
     d, LK, K = c.d, c.L * c.K, c.K
-    if name.startswith("k_verify"):
-        return float(steps) * float(st["n_cand"].sum()) * (4 * d + 4 + 4)   # row gather + id read + d2 write
-    if name.startswith("k_range_filter"):
-        per = (st["leaves_tested"] * 2 * K + st["leaves_passed"] * 8 + st["points_tested"] * K
-               + st["points_passed"] * 12 + st["n_cand"] * 4)
-        return float(steps) * float(per.sum())
-    if name.startswith("k_project"):
-        return float(steps) * ((n_local + datagen_ns(c, n_local) + nq) * (4 * d + 4 * LK))
-    if name.startswith("k_encode"):
-        return float(steps) * n_local * LK * 5
-    return None
+    ns = datagen_ns(c, n_local)
+    ncand = float(st["n_cand"].sum())
+    filt = float((st["leaves_tested"] * 2 * K + st["leaves_passed"] * 8 + st["points_tested"] * K
+                  + st["points_passed"] * 12 + st["n_cand"] * 4).sum())
+    lookups = float((st["points_tested"] * K + st["leaves_tested"] * K).sum())
+    proj_bytes = n_local * (4 * ld + LK) + (ns + nq) * (4 * ld + 4 * LK)
+    proj_flops = 2.0 * 2 * (n_local + ns + nq) * ((LK + 15) // 16 * 16) * ld      # x_hi and x_lo MMAs
+    return {
+        "k_range_filter": {"bytes": steps * filt, "smem_bytes": steps * lookups * 2,
+                           "unit": "per query: leaves_tested*2K + leaves_passed*8 + points_tested*K + "
+                                   "points_passed*12 + new*4 B (SURVEY 8(d) K5/K6)"},
+        "k_verify_rows": {"bytes": steps * ncand * (4 * d + 8), "unit": "per candidate 4d+8 B (row + id + d2)"},
+        "k_project_tc": {"bytes": steps * proj_bytes, "flops": steps * proj_flops,
+                         "unit": "per row 4*ld B read + codes (LK B) or projections (4LK B) written"},
+    }
+
+
+def roofline_entry(name, model, ms, hbm, bf16, clocks):
+    ach = model["bytes"] / (ms / 1e3) / 1e9
+    e = {"kernel": name, "bound": "hbm", "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s",
+         "frac": round(ach / hbm, 4), "traffic": None, "ms": round(ms, 4), "unit_of_work": model["unit"]}
+    if "smem_bytes" in model:
+        sm = (clocks.get("sm_mhz") or 1965.0) * 1e6
+        smem_peak = 148 * 128 * sm / 1e9
+        e["limiter"] = "shared-memory LUT lookups (codes and leaf boxes are L2-resident)"
+        e["smem"] = {"achieved": round(model["smem_bytes"] / (ms / 1e3) / 1e9, 1), "peak": round(smem_peak, 1),
+                     "unit": "GB/s", "peak_note": "148 SMs x 128 B/clk x SM clock (derived)",
+                     "counted": "one 16-bit quantised term per (query, dim) lookup"}
+    if "flops" in model:
+        tf = model["flops"] / (ms / 1e3) / 1e12
+        e["tensor"] = {"achieved": round(tf, 1), "peak": round(bf16 / 2, 1), "unit": "TFLOP/s",
+                       "peak_note": "measured bf16 / 2 (TF32 nominal ratio), 2 MMAs (x_hi, x_lo) per k-step"}
+    return e
 
 
 def datagen_ns(c, n):
@@ -310,17 +333,16 @@ def main():
         hbm, bf16, bf16s, peak_src = peaks()
         kern = {k: {"launches": v[0], "ms": round(v[1], 4)} for k, v in sorted(prof.items(), key=lambda kv: -kv[1][1])}
         dom = max(prof.items(), key=lambda kv: kv[1][1])[0] if prof else None
-        roof = None
-        if dom is not None:
-            byts = kernel_bytes(dom, cfg, args.steps, st, n_local, cfg.nq)
-            ms = prof[dom][1]
-            if byts is not None:
-                ach = byts / (ms / 1e3) / 1e9
-                roof = {"kernel": dom, "bound": "hbm", "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s",
-                        "frac": round(ach / hbm, 4), "traffic": None, "peak_source": peak_src,
-                        "share_of_step": round(ms / step_ms, 4),
-                        "unit_of_work": "candidate (4d+8 B)" if dom.startswith("k_verify") else
-                        "per query: leaves x 2K + passed leaves x 8 + tested points x K + passing x 12 + new x 4 B"}
+        models = kernel_models(cfg, args.steps, st, n_local, cfg.nq, (cfg.d + 7) // 8 * 8)
+        roofs = []
+        for kname, (nl_, ms) in sorted(prof.items(), key=lambda kv: -kv[1][1]):
+            for prefix, model in models.items():
+                if kname.startswith(prefix):
+                    roofs.append(roofline_entry(kname, model, ms, hbm, bf16, clocks))
+        roof = next((r for r in roofs if r["kernel"] == dom), None)
+        if roof is not None:
+            roof["share_of_step"] = round(prof[dom][1] / step_ms, 4)
+            roof["peak_source"] = peak_src
         line = {
             "metric": METRIC, "value": cfg.nq * args.steps / (query_ms / 1e3), "unit": "queries/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms / args.steps,
@@ -338,6 +360,7 @@ def main():
             "filter_counts_per_query": {k_: float(st[k_].mean()) for k_ in
                                         ("leaves_tested", "leaves_passed", "points_tested", "points_passed")},
             "roofline": roof,
+            "rooflines": roofs,
             "e2e": {"value": cfg.nq / (float(te.item()) / 1e3), "unit": "queries/s",
                     "h2d_bytes_per_step": int(Q.nbytes), "d2h_bytes_per_step": int(cfg.nq * cfg.k * 12),
                     "how": "detlsh_query with pinned host query/output buffers (copies inside the timed call)"},

@@ -249,18 +249,21 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                 float v[16];
                 tmem_ld16(taddr + c0, v);
                 if (N_r > 0) {
-                    // code = #{t in 1..N_r-1 : b_t < x}: branch-free lower bound over the table
+                    // code = #{t in 1..N_r-1 : b_t < x}: branch-free lower bound over the table;
+                    // the 16 searches advance together (16 independent shared loads per step)
+                    int pos[16];
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) pos[i] = 0;
+                    for (int s = N_r >> 1; s > 0; s >>= 1) {
+#pragma unroll
+                        for (int i = 0; i < 16; ++i) {
+                            const int r = min(c0 + i, sh.LK - 1);
+                            pos[i] += (sT[r * N_r + pos[i] + s - 1] < v[i]) ? s : 0;
+                        }
+                    }
                     uint32_t packed[4] = {0, 0, 0, 0};
 #pragma unroll
-                    for (int i = 0; i < 16; ++i) {
-                        const int r = c0 + i;
-                        int pos = 0;
-                        if (r < sh.LK) {
-                            const float* t = sT + r * N_r;
-                            for (int s = N_r >> 1; s > 0; s >>= 1) pos += (t[pos + s - 1] < v[i]) ? s : 0;
-                        }
-                        packed[i >> 2] |= (uint32_t)pos << (8 * (i & 3));
-                    }
+                    for (int i = 0; i < 16; ++i) packed[i >> 2] |= (uint32_t)pos[i] << (8 * (i & 3));
                     if (row < sh.m) {
                         uint8_t* out = EP + row * sh.LK + c0;
                         if (c0 + 16 <= sh.LK && (sh.LK & 15) == 0) {

@@ -245,7 +245,7 @@ __global__ void __launch_bounds__(RF_THREADS, 3) k_range_filter(RFArgs a) {
             if (__ballot_sync(0xffffffffu, m != 0) == 0) continue;    // whole warp pruned by leaf LBs
             c_pt += __popc(m);
             uint4 c4 = make_uint4(0, 0, 0, 0);
-            uint32_t pass = m;
+            uint32_t pass = m, certain = 0;
             if (m && a.mode == DETLSH_MODE_CELL) {
                 if (KT == 16) {
                     c4 = *reinterpret_cast<const uint4*>(a.tcodes + pos * 16);
@@ -261,11 +261,15 @@ __global__ void __launch_bounds__(RF_THREADS, 3) k_range_filter(RFArgs a) {
                         }
                     }
                     const uint32_t accs[4] = {acc0, acc1, acc2, acc3};
-                    uint32_t ok = 0;
+                    uint32_t ok = 0, sure = 0;
 #pragma unroll
-                    for (int g = 0; g < RF_G; ++g)
-                        ok |= (((accs[g >> 1] >> (16 * (g & 1))) & 0xFFFFu) <= RF_QT ? 1u : 0u) << g;
+                    for (int g = 0; g < RF_G; ++g) {
+                        const uint32_t sg = (accs[g >> 1] >> (16 * (g & 1))) & 0xFFFFu;
+                        ok |= (sg <= RF_QT ? 1u : 0u) << g;
+                        sure |= (sg <= RF_QT - 17 ? 1u : 0u) << g;
+                    }
                     pass = m & ok;
+                    certain = m & sure;
                 } else {
                     uint32_t acc[RF_G];
 #pragma unroll
@@ -276,13 +280,20 @@ __global__ void __launch_bounds__(RF_THREADS, 3) k_range_filter(RFArgs a) {
 #pragma unroll
                         for (int g = 0; g < RF_G; ++g) acc[g] += (vw[g >> 1] >> (16 * (g & 1))) & 0xFFFFu;
                     }
-                    uint32_t ok = 0;
+                    uint32_t ok = 0, sure = 0;
 #pragma unroll
-                    for (int g = 0; g < RF_G; ++g) ok |= (acc[g] <= RF_QT ? 1u : 0u) << g;
+                    for (int g = 0; g < RF_G; ++g) {
+                        ok |= (acc[g] <= RF_QT ? 1u : 0u) << g;
+                        sure |= (acc[g] + 17 <= RF_QT ? 1u : 0u) << g;
+                    }
                     pass = m & ok;
+                    certain = m & sure;
                 }
-                // exact fp32 confirmation of the screened pairs (cell LB summed in j order)
-                uint32_t conf = 0;
+                // Exact fp32 confirmation, only inside the quantisation band: e_j > D_j*2048/rho^2 - 1
+                // (products rounded down), so sum_j e_j <= 2031 proves sum_j D_j < rho^2 (1 - 1e-5)
+                // and the fp32 sum passes; 2032..2048 is decided by the exact fp32 sum in j order.
+                uint32_t conf = certain;
+                pass &= ~certain;
                 while (pass) {
                     const int g = __ffs(pass) - 1;
                     pass &= pass - 1;

@@ -404,8 +404,55 @@ struct VRArgs {
     int64_t nwords;
     uint32_t* cand;          // round buffer: ids
     float* d2;               // round buffer: squared distances
+    const uint32_t* boff;    // [na][nblocks] slot of each (query, block) in the round buffer
+    int64_t nblocks;
     int rbw;                 // bitmap words (32 rows each) per block
 };
+
+// Per (active query, row block): where its new candidates go in the round buffer -- the
+// query's round offset plus the number of new members of S in earlier blocks (an exclusive
+// scan of popcounts of cur & ~ver), so the verify kernel appends without atomics.
+__global__ void __launch_bounds__(1024) k_verify_offsets(const int* __restrict__ act, const QState* __restrict__ qs,
+                                                         const uint32_t* __restrict__ cur, const uint32_t* __restrict__ ver,
+                                                         int64_t nwords, int rbw, int64_t nblocks,
+                                                         uint32_t* __restrict__ boff) {
+    __shared__ uint32_t s_w[32];
+    const int q = act[blockIdx.x];
+    const uint32_t* c = cur + (int64_t)q * nwords;
+    const uint32_t* v = ver + (int64_t)q * nwords;
+    uint32_t* out = boff + (int64_t)blockIdx.x * nblocks;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    uint32_t carry = (uint32_t)qs[q].roff;
+    for (int64_t b0 = 0; b0 < nblocks; b0 += 1024) {
+        const int64_t b = b0 + threadIdx.x;
+        uint32_t cnt = 0;
+        if (b < nblocks)
+            for (int i = 0; i < rbw; ++i) {
+                const int64_t wd = b * rbw + i;
+                if (wd < nwords) cnt += __popc(c[wd] & ~v[wd]);
+            }
+        uint32_t x = cnt;
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) s_w[w] = x;
+        __syncthreads();
+        if (w == 0) {
+            uint32_t t = s_w[lane];
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, t, o);
+                if (lane >= o) t += y;
+            }
+            s_w[lane] = t;
+        }
+        __syncthreads();
+        const uint32_t incl = x + (w ? s_w[w - 1] : 0);
+        if (b < nblocks) out[b] = carry + incl - cnt;
+        carry += s_w[31];
+        __syncthreads();
+    }
+}
 
 // Each warp serves one query at a time: its 32 lanes form 4 row slots of 8 lanes; a slot
 // computes one candidate's distance, each lane a strided eighth of the row (float4 reads of
@@ -433,12 +480,22 @@ __global__ void __launch_bounds__(VR_THREADS) k_verify_rows(VRArgs a) {
     uint8_t* lst = s_list[warp];
     for (int ai = warp; ai < a.na; ai += nwarps) {
         const int q = a.act[ai];
+        // -q, the lane's eighth, as fp32x2 pairs (issued first: its latency overlaps the masks)
+        float2 nq[NV ? 2 * NV : 2];
+        if (NV) {
+#pragma unroll
+            for (int v = 0; v < NV; ++v) {
+                const int f = u + 8 * v;
+                const float4 y = (EXACT || f < nf4) ? Q4[(int64_t)q * nf4 + f] : make_float4(0.f, 0.f, 0.f, 0.f);
+                nq[2 * v] = make_float2(-y.x, -y.y);
+                nq[2 * v + 1] = make_float2(-y.z, -y.w);
+            }
+        }
         uint32_t mw = 0;
         if (lane < a.rbw) {
             const int64_t w = w0 + lane;
             if (w < a.nwords) {
-                uint32_t* vp = a.ver + (int64_t)q * a.nwords + w;
-                const uint32_t c = a.cur[(int64_t)q * a.nwords + w];
+                uint32_t* vp = a.ver + (int64_t)q * a.nwords + w;                const uint32_t c = a.cur[(int64_t)q * a.nwords + w];
                 mw = c & ~*vp;
                 if (mw) *vp = c;
             }
@@ -453,10 +510,7 @@ __global__ void __launch_bounds__(VR_THREADS) k_verify_rows(VRArgs a) {
         }
         const uint32_t tot = __shfl_sync(0xffffffffu, incl, 7);
         if (tot == 0) continue;
-        unsigned long long base = 0;
-        if (lane == 0)
-            base = (unsigned long long)a.qs[q].roff +
-                   atomicAdd(reinterpret_cast<unsigned long long*>(&a.qs[q].rcnt), (unsigned long long)tot);
+        const uint32_t base = a.boff[(int64_t)ai * a.nblocks + blockIdx.x];
         {
             uint32_t m = mw, p = incl - pc;
             while (m) {
@@ -464,19 +518,8 @@ __global__ void __launch_bounds__(VR_THREADS) k_verify_rows(VRArgs a) {
                 m &= m - 1;
             }
         }
-        // -q, the lane's eighth, as fp32x2 pairs
-        float2 nq[NV ? 2 * NV : 2];
-        if (NV) {
-#pragma unroll
-            for (int v = 0; v < NV; ++v) {
-                const int f = u + 8 * v;
-                const float4 y = (EXACT || f < nf4) ? Q4[(int64_t)q * nf4 + f] : make_float4(0.f, 0.f, 0.f, 0.f);
-                nq[2 * v] = make_float2(-y.x, -y.y);
-                nq[2 * v + 1] = make_float2(-y.z, -y.w);
-            }
-        }
         __syncwarp();
-        const int64_t out = (int64_t)__shfl_sync(0xffffffffu, base, 0);
+        const int64_t out = (int64_t)base;
         uint32_t* cl = a.cand;
         float* dl = a.d2;
         for (uint32_t i = 0; i < tot; i += 4) {
@@ -552,7 +595,7 @@ __global__ void __launch_bounds__(1024) k_round_offsets(const int* __restrict__ 
         if (a_ < na) {
             QState* s = &qs[act[a_]];
             s->roff = (int64_t)(s_run + incl - c);
-            s->rcnt = 0;
+            s->rcnt = (int64_t)c;
         }
         __syncthreads();
         if (threadIdx.x == 1023) s_run += incl;
@@ -907,6 +950,7 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
         va.rbw = (int)std::max<int64_t>(1, std::min<int64_t>(8, (120 * 1024) / per_word));
     }
     const size_t vr_smem = (size_t)va.rbw * 32 * ix.ld * 4;
+    Scratch s_boff(st, sizeof(uint32_t) * (size_t)(qb * ceil_div(nwords, va.rbw)));
     const bool vexact = (ix.ld / 4) == 8 * vnv;
     DL_CUDA(cudaFuncSetAttribute(k_verify_rows<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)vr_smem));
     DL_CUDA(cudaFuncSetAttribute(k_verify_rows<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)vr_smem));
@@ -977,6 +1021,10 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
             va.d2 = reinterpret_cast<float*>(s_round.as<uint32_t>() + round_cap);
             va.act = cur;
             va.na = na;
+            va.nblocks = ceil_div(nwords, va.rbw);
+            va.boff = s_boff.as<uint32_t>();
+            DL_LAUNCH(k_verify_offsets, (unsigned)na, 1024, 0, st, cur, s_qs.as<QState>(), s_bm.as<uint32_t>(),
+                      s_ver.as<uint32_t>(), nwords, va.rbw, va.nblocks, s_boff.as<uint32_t>());
             {
                 const unsigned nblocks = (unsigned)ceil_div(nwords, va.rbw);
                 switch (vnv) {

@@ -117,6 +117,17 @@ detlsh_status detlsh_query_ex(const detlsh_index* idx, const float* queries, int
                               double c, double r_min, double beta, const detlsh_opts* opts,
                               int64_t* out_ids, float* out_dists, detlsh_query_stats* stats);
 
+/*
+ * "Magic" initial radius (AMB-22): for each of ns sample queries [ns][d] (host or
+ * device), r*_q = the smallest radius whose full round (all L range queries) gives
+ * |S| >= min(n, ceil(beta n) + k) -- i.e. sqrt of the B-th smallest over points of
+ * min_i cellLB_i(p), divided by eps.  Writes r*_q to rstar (host, nullable) and the lower
+ * median to *r_min (host).  Errors (EINVAL): NULL idx/queries/r_min; ns < 1; k < 1 or k > n;
+ * beta <= 0.
+ */
+detlsh_status detlsh_estimate_rmin(const detlsh_index* idx, const float* queries, int64_t ns, int32_t k,
+                                   double beta, const detlsh_opts* opts, double* rstar, double* r_min);
+
 void detlsh_free(detlsh_index* idx);
 
 /* Thread-local description of the last failure; valid until the next call on this thread. */

@@ -276,6 +276,29 @@ detlsh_status detlsh_query(const detlsh_index* idx, const float* queries, int64_
     return detlsh_query_ex(idx, queries, nq, k, c, r_min, beta, nullptr, out_ids, out_dists, nullptr);
 }
 
+detlsh_status detlsh_estimate_rmin(const detlsh_index* idx, const float* queries, int64_t ns, int32_t k, double beta,
+                                   const detlsh_opts* opts, double* rstar, double* r_min) {
+    return guard([&] {
+        DL_REQUIRE(idx && queries && r_min, "NULL argument");
+        const Index& ix = *reinterpret_cast<const Index*>(idx);
+        DL_REQUIRE(!ix.codes_only, "index was built from codes only");
+        DL_REQUIRE(ns >= 1, "need at least one sample query");
+        DL_REQUIRE(k >= 1 && k <= ix.n, "k must be in [1, n]");
+        DL_REQUIRE(beta > 0.0 && std::isfinite(beta), "beta must be > 0");
+        const detlsh_opts o = opts_or_default(opts);
+        require_device();
+        cudaStream_t st = stream_of(&o);
+        Scratch s_q(st, sizeof(float) * (size_t)ns * ix.ld);
+        stage_rows(queries, ns, ix.d, ix.ld, s_q.as<float>(), st);
+        std::vector<double> rs((size_t)ns);
+        estimate_rstar(ix, s_q.as<float>(), ix.ld, ns, k, beta, o.proj_impl, rs.data(), st);
+        if (rstar) std::memcpy(rstar, rs.data(), sizeof(double) * (size_t)ns);
+        std::vector<double> sorted = rs;
+        std::sort(sorted.begin(), sorted.end());
+        *r_min = sorted[(size_t)(ns - 1) / 2];      // lower median (AMB-22)
+    });
+}
+
 void detlsh_free(detlsh_index* idx) {
     if (!idx) return;
     delete reinterpret_cast<Index*>(idx);

@@ -94,6 +94,9 @@ struct QueryArgs {
 void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArgs& a, int64_t* d_ids,
                  float* d_dists, detlsh_query_stats* d_stats, cudaStream_t st);
 
+void estimate_rstar(const Index& ix, const float* d_Q, int64_t q_ld, int64_t ns, int k, double beta, int proj_impl,
+                    double* h_rstar, cudaStream_t st);
+
 // host_math.cpp
 double chi2_upper_quantile(double alpha, int K);
 double chi2_survival(double y, int K);

@@ -16,6 +16,7 @@
 //  k_finalize     ids (global) and sqrt(d2), ascending by (dist, id) (AMB-21, AMB-28).
 #include <algorithm>
 #include <cmath>
+#include <cstring>
 #include <vector>
 
 #include "index.cuh"
@@ -847,7 +848,97 @@ float fdiv_rd_host(float num, float den) {
     return f;
 }
 
+
+// ---- r_min estimator (AMB-22): per sample query, t_p = min over trees of the cell
+//      lower bound of point p (exact fp32 LUT sums in j order, as the range filter's final
+//      test), then the B-th smallest t_p: r*_q = sqrt(t_(B)) / eps is the smallest radius whose
+//      full round gives |S| >= B.
+__global__ void __launch_bounds__(256) k_rstar_tree(const float* __restrict__ lut, const uint8_t* __restrict__ tcodes,
+                                                    const uint32_t* __restrict__ perm, int64_t n, int t, int L, int K,
+                                                    int N_r, uint32_t* __restrict__ tp) {
+    extern __shared__ float s_lut1[];
+    const int q = blockIdx.y;
+    const float* src = lut + ((int64_t)q * L + t) * K * N_r;
+    for (int i = threadIdx.x; i < K * N_r; i += 256) s_lut1[i] = src[i];
+    __syncthreads();
+    uint32_t* out = tp + (int64_t)q * n;
+    for (int64_t pos = blockIdx.x * (int64_t)256 + threadIdx.x; pos < n; pos += (int64_t)gridDim.x * 256) {
+        float s = 0.f;
+        for (int j = 0; j < K; ++j) s += s_lut1[j * N_r + tcodes[pos * K + j]];
+        atomicMin(out + perm[pos], __float_as_uint(s));      // non-negative floats order as their bits
+    }
+}
+
+__global__ void __launch_bounds__(1024) k_select_kth_u32(const uint32_t* __restrict__ vals, int64_t n, int64_t rank,
+                                                          uint32_t* __restrict__ out) {
+    __shared__ uint32_t s_hist[256];
+    __shared__ uint32_t s_prefix, s_mask;
+    __shared__ unsigned long long s_rem;
+    const uint32_t* v = vals + (int64_t)blockIdx.x * n;
+    if (threadIdx.x == 0) { s_prefix = 0; s_mask = 0; s_rem = (unsigned long long)rank; }
+    __syncthreads();
+    for (int shift = 24; shift >= 0; shift -= 8) {
+        for (int i = threadIdx.x; i < 256; i += 1024) s_hist[i] = 0;
+        __syncthreads();
+        const uint32_t pre = s_prefix, msk = s_mask;
+        for (int64_t i = threadIdx.x; i < n; i += 1024) {
+            const uint32_t x = v[i];
+            if ((x & msk) == pre) atomicAdd(&s_hist[(x >> shift) & 255u], 1u);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            unsigned long long cum = 0, rem = s_rem;
+            for (int dg = 0; dg < 256; ++dg) {
+                if (cum + s_hist[dg] >= rem) {
+                    s_prefix = pre | ((uint32_t)dg << shift);
+                    s_mask = msk | (0xFFu << shift);
+                    s_rem = rem - cum;
+                    break;
+                }
+                cum += s_hist[dg];
+            }
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) out[blockIdx.x] = s_prefix;
+}
+
 }  // namespace
+
+void estimate_rstar(const Index& ix, const float* d_Q, int64_t q_ld, int64_t ns, int k, double beta, int proj_impl,
+                    double* h_rstar, cudaStream_t st) {
+    DL_REQUIRE(q_ld == ix.ld, "query row stride must equal the index's");
+    const int64_t n = ix.n, LK = ix.LK;
+    int64_t B = (int64_t)std::ceil(beta * (double)n) + k;
+    if (B > n) B = n;
+    Scratch s_qp(st, sizeof(float) * (size_t)(ns * LK));
+    Scratch s_flag(st, sizeof(int));
+    DL_CUDA(cudaMemsetAsync(s_flag.p, 0, sizeof(int), st));
+    project_rows(ix, d_Q, q_ld, ns, s_qp.as<float>(), proj_impl, s_flag.as<int>(), st);
+    Scratch s_lut(st, sizeof(float) * (size_t)(ns * LK * ix.N_r));
+    Scratch s_sx(st, (size_t)(ns * LK));
+    DL_LAUNCH(k_build_lut, (unsigned)std::min<int64_t>(ceil_div(ns * LK * ix.N_r, 256), 148 * 32), 256, 0, st,
+              s_qp.as<float>(), (int)ns, (int)LK, ix.N_r, ix.B.as<float>(), s_lut.as<float>(), s_sx.as<uint8_t>());
+    Scratch s_tp(st, sizeof(uint32_t) * (size_t)(ns * n));
+    DL_CUDA(cudaMemsetAsync(s_tp.p, 0xFF, sizeof(uint32_t) * (size_t)(ns * n), st));   // NaN bits > +inf bits
+    const size_t smem = sizeof(float) * (size_t)ix.K * ix.N_r;
+    DL_CUDA(cudaFuncSetAttribute(k_rstar_tree, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const unsigned gx = (unsigned)std::min<int64_t>(ceil_div(n, 256), 64);
+    for (int t = 0; t < ix.L; ++t)
+        DL_LAUNCH(k_rstar_tree, dim3(gx, (unsigned)ns), 256, smem, st, s_lut.as<float>(),
+                  ix.tcodes.as<uint8_t>() + (int64_t)t * n * ix.K, ix.perm.as<uint32_t>() + (int64_t)t * n, n, t,
+                  ix.L, ix.K, ix.N_r, s_tp.as<uint32_t>());
+    Scratch s_out(st, sizeof(uint32_t) * (size_t)ns);
+    DL_LAUNCH(k_select_kth_u32, (unsigned)ns, 1024, 0, st, s_tp.as<uint32_t>(), n, B, s_out.as<uint32_t>());
+    std::vector<uint32_t> bits(ns);
+    DL_CUDA(cudaMemcpyAsync(bits.data(), s_out.p, sizeof(uint32_t) * ns, cudaMemcpyDeviceToHost, st));
+    DL_CUDA(cudaStreamSynchronize(st));
+    for (int64_t i = 0; i < ns; ++i) {
+        float f;
+        std::memcpy(&f, &bits[i], 4);
+        h_rstar[i] = std::sqrt((double)f) / ix.eps;
+    }
+}
 
 void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArgs& a, int64_t* d_ids,
                  float* d_dists, detlsh_query_stats* d_stats, cudaStream_t st) {

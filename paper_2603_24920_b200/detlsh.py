@@ -88,6 +88,7 @@ def lib():
         "detlsh_debug_export": (i32, [P, i32, i32, P, sz, C.POINTER(sz)]),
         "detlsh_build_from_codes": (i32, [P, i64, i32, i32, i32, O, P]),
         "detlsh_launch_count": (i64, []),
+        "detlsh_estimate_rmin": (i32, [P, P, i64, i32, f64, O, P, P]),
         "detlsh_profile_enable": (None, [i32]),
         "detlsh_profile_reset": (None, []),
         "detlsh_profile_read": (i32, [P, i32]),
@@ -228,6 +229,16 @@ class Index:
     def tree(self, i: int):
         return {"perm": self.export(4, i), "leaf_off": self.export(5, i), "lo": self.export(6, i),
                 "hi": self.export(7, i), "bits": self.export(8, i)}
+
+    def estimate_rmin(self, Qs, k: int, beta: float, opts: detlsh_opts | None = None, return_all: bool = False):
+        """GPU r_min estimator (AMB-22): lower median over sample queries of r*_q."""
+        Qs = _f32(Qs)
+        ns = Qs.shape[0]
+        rs = np.empty(ns, np.float64)
+        rm = C.c_double()
+        o = opts if opts is not None else default_opts()
+        _check(lib().detlsh_estimate_rmin(self._h, _ptr(Qs), ns, k, beta, C.byref(o), _ptr(rs), C.byref(rm)))
+        return (rm.value, rs) if return_all else rm.value
 
     def project(self, X, proj_impl: int | None = None):
         X = _f32(X)

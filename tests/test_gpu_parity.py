@@ -256,3 +256,22 @@ def test_config2_full_size_sampled_queries():
     print(f"cfg2 recall vs oracle on 24 sampled queries: {rec:.4f}")
     assert rec >= 0.99
     _dist_match(ig[sel], dg[sel], io, do)
+
+
+def test_rmin_estimator_parity(gpu_tiny, tiny_oracle, tiny):
+    """f3: the GPU r_min estimator (AMB-22) vs the oracle's, per sample query (fp32 vs fp64 sums)."""
+    c = tiny["cfg"]
+    gm, gr = gpu_tiny.estimate_rmin(tiny["Qs"], c.k, c.beta, return_all=True)
+    om, orr = tiny_oracle.estimate_rmin(tiny["Qs"], c.k, c.c, c.beta, return_all=True)
+    assert np.allclose(gr, orr, rtol=1e-4)
+    assert abs(gm - om) <= 1e-4 * om
+
+
+def test_large_k(gpu_tiny, tiny_oracle, tiny, tiny_rmin):
+    """Top-k beyond one warp's worth and near the 4096 cap (k = 1000, 4096)."""
+    c = tiny["cfg"]
+    for k in (1000, 4096):
+        ig, dg = gpu_tiny.query(tiny["Q"][:12], k, c.c, tiny_rmin, c.beta)
+        io, do, _ = tiny_oracle.query(tiny["Q"][:12], k, c.c, tiny_rmin, c.beta)
+        assert _recall(ig, io) >= 0.99
+        _dist_match(ig, dg, io, do)

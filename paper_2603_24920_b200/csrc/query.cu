@@ -72,11 +72,12 @@ __global__ void k_build_lut(const float* __restrict__ Qp, int nqb, int LK, int N
     }
 }
 
-// ---- per round: 12-bit quantised lower bounds of the LUT, e = min(4095, floor(D * 2048/rho^2))
-//      (products rounded down), so sum_j e_j > 2048 proves sum_j D_j > rho^2 in fp32 (the
-//      16 terms sum to at most 65520: two queries share one 32-bit integer add).
+// ---- per round: quantised lower bounds of the LUT, e = min(cap, floor(D * QT/rho^2)) with
+//      products rounded down: sum_j e_j > QT proves sum_j D_j > rho^2, and sum_j e_j <= QT-17
+//      proves sum_j D_j < rho^2 (1 - 1e-5) (each e_j > D_j QT/rho^2 - 1.001), so only the band
+//      in between needs the exact fp32 sum.  16 terms of <= cap fit the packed lane width.
 __global__ void k_build_qlut(const float* __restrict__ lut, const int* __restrict__ act, int na, int64_t per_q,
-                             float inv_rd, uint16_t* __restrict__ qlut) {
+                             float inv_rd, float cap, uint16_t* __restrict__ qlut) {
     const int64_t total = (int64_t)na * per_q;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
          i += (int64_t)gridDim.x * blockDim.x) {
@@ -84,21 +85,25 @@ __global__ void k_build_qlut(const float* __restrict__ lut, const int* __restric
         const int64_t q = act[a_];
         float v = __fmul_rd(lut[q * per_q + e], inv_rd);
         if (v != v) v = 0.f;                       // 0 * inf: a zero term stays zero
-        qlut[q * per_q + e] = (uint16_t)(v >= 4095.f ? 4095.f : floorf(v));
+        qlut[q * per_q + e] = (uint16_t)(v >= cap ? cap : floorf(v));
     }
 }
 
 // ---- range filter of one tree (Alg. 3 at radius eps*r, Alg. 5 lines 5-6), batched:
-//      CTA = group of 8 active queries x stripe of tiles; a warp owns a tile of <= 32 leaves.
+//      CTA = group of G active queries x stripe of tiles; a warp owns a tile of <= 32 leaves.
 //      Leaf lower bounds (lane = leaf) prune; for the points of qualifying leaves the cell
 //      lower bound is screened with the quantised table (one 16-byte shared load per code
-//      serves all 8 queries, two queries per 32-bit integer add) and confirmed in fp32 from
-//      the exact table; passing points are OR-marked into the per-query bitmap (RED.OR).
-//      The fp32 confirmation sums the same terms in the same order as the oracle's
-//      definition of the cell bound (AMB-12), so the quantised screen never changes a result.
+//      serves all G queries: G = 8 x 12-bit terms in 16-bit lanes, or G = 16 x 8-bit terms
+//      widened into 16-bit lanes) and decided in fp32 from the exact table inside the band;
+//      passing points are OR-marked into the per-query bitmap (RED.OR).  The fp32 decision
+//      sums the same terms in the same order as the cell bound's definition (AMB-12), so the
+//      screen never changes a result.
 constexpr int RF_THREADS = 256;
-constexpr int RF_G = 8;          // queries per CTA: one 16-byte quantised entry holds the G values
-constexpr uint32_t RF_QT = 2048; // quantised threshold (rho^2)
+constexpr int RF_G = 16;         // queries per CTA (8-bit terms); 8 selects 12-bit terms
+
+template <int G> struct QuantSpec;
+template <> struct QuantSpec<8> { static constexpr uint32_t QT = 2048, CAP = 4095; };
+template <> struct QuantSpec<16> { static constexpr uint32_t QT = 128, CAP = 255; };
 
 struct RFArgs {
     const uint8_t* tcodes;      // tree t: [n][K]
@@ -123,21 +128,22 @@ struct RFArgs {
     unsigned long long* ctr;    // [Qb][4] filter counters
 };
 
-template <int KT, int NRT>
+template <int KT, int NRT, int G>
 __global__ void __launch_bounds__(RF_THREADS, 3) k_range_filter(RFArgs a) {
+    constexpr uint32_t QT = QuantSpec<G>::QT, CAP = QuantSpec<G>::CAP;
     extern __shared__ __align__(16) unsigned char smem[];
     const int K = KT ? KT : a.K;
     const int N_r = NRT ? NRT : a.N_r;
-    uint4* s_q16 = reinterpret_cast<uint4*>(smem);                                      // [K][N_r] x 8 u16
-    __shared__ int s_q[RF_G];
-    __shared__ uint8_t s_sx[RF_G][32];
-    __shared__ unsigned int s_ctr[RF_G][4];
+    uint4* s_qe = reinterpret_cast<uint4*>(smem);                                       // [K][N_r] x 16 B
+    __shared__ int s_q[G];
+    __shared__ uint8_t s_sx[G][32];
+    __shared__ unsigned int s_ctr[G][4];
     __shared__ uint32_t s_lq[RF_THREADS / 32][kTileLeaves];                             // per warp: leaf masks
     __shared__ int s_active_mask;
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = RF_THREADS / 32;
-    if (threadIdx.x < RF_G) {
-        const int gi = blockIdx.x * RF_G + threadIdx.x;
+    if (threadIdx.x < G) {
+        const int gi = blockIdx.x * G + threadIdx.x;
         int q = -1;
         if (gi < a.na) {
             q = a.act[gi];
@@ -149,33 +155,38 @@ __global__ void __launch_bounds__(RF_THREADS, 3) k_range_filter(RFArgs a) {
     __syncthreads();
     if (threadIdx.x == 0) {
         int m = 0;
-        for (int g = 0; g < RF_G; ++g) m |= (s_q[g] >= 0) << g;
+        for (int g = 0; g < G; ++g) m |= (s_q[g] >= 0) << g;
         s_active_mask = m;
     }
     __syncthreads();
-    const int amask = s_active_mask;
+    const uint32_t amask = (uint32_t)s_active_mask;
     if (amask == 0) return;
     const int64_t per_q = (int64_t)a.L * K * N_r;
-    {   // interleave the 8 queries' quantised tables: entry (j, s) = 8 x u16
-        const uint16_t* src[RF_G];
+    {   // interleave the G queries' quantised tables: entry (j, s) = 16 bytes
+        const uint16_t* src[G];
 #pragma unroll
-        for (int g = 0; g < RF_G; ++g)
+        for (int g = 0; g < G; ++g)
             src[g] = s_q[g] >= 0 ? a.qlut + (int64_t)s_q[g] * per_q + (int64_t)a.t * K * N_r : nullptr;
         for (int i = threadIdx.x; i < K * N_r; i += RF_THREADS) {
-            uint32_t v[RF_G];
+            uint32_t w[4] = {0, 0, 0, 0};
 #pragma unroll
-            for (int g = 0; g < RF_G; ++g) v[g] = src[g] ? src[g][i] : 4095u;      // inactive: never passes
-            s_q16[i] = make_uint4(v[0] | (v[1] << 16), v[2] | (v[3] << 16), v[4] | (v[5] << 16), v[6] | (v[7] << 16));
+            for (int g = 0; g < G; ++g) {
+                const uint32_t v = src[g] ? src[g][i] : CAP;                           // inactive: never passes
+                if (G == 8) w[g >> 1] |= v << (16 * (g & 1));
+                else w[g >> 2] |= v << (8 * (g & 3));
+            }
+            s_qe[i] = make_uint4(w[0], w[1], w[2], w[3]);
         }
         if (threadIdx.x < K) {
 #pragma unroll
-            for (int g = 0; g < RF_G; ++g)
+            for (int g = 0; g < G; ++g)
                 s_sx[g][threadIdx.x] = s_q[g] >= 0 ? a.sx[((int64_t)s_q[g] * a.L + a.t) * K + threadIdx.x] : 0;
         }
     }
     __syncthreads();
     const float rho2 = a.rho2;
-    const uint16_t* s_q16h = reinterpret_cast<const uint16_t*>(s_q16);
+    const uint16_t* s_h = reinterpret_cast<const uint16_t*>(s_qe);
+    const uint8_t* s_b = reinterpret_cast<const uint8_t*>(s_qe);
     uint32_t c_lt = 0, c_lp = 0, c_pt = 0, c_pp = 0;
     uint32_t* lq = s_lq[warp];
 
@@ -187,40 +198,23 @@ __global__ void __launch_bounds__(RF_THREADS, 3) k_range_filter(RFArgs a) {
         // leaf lower bounds (Alg. 3 pruning, Fig. dist): lane = leaf, quantised, all G queries
         if (lane < nlt) {
             const int64_t l = (int64_t)lb + lane;
-            uint32_t lacc[RF_G];
+            uint32_t lacc[G];
 #pragma unroll
-            for (int g = 0; g < RF_G; ++g) lacc[g] = 0;
-            if (KT == 16) {
-                const uint4 lo4 = *reinterpret_cast<const uint4*>(a.lo + l * 16);
-                const uint4 hi4 = *reinterpret_cast<const uint4*>(a.hi + l * 16);
+            for (int g = 0; g < G; ++g) lacc[g] = 0;
+            for (int j = 0; j < K; ++j) {
+                const int lo_ = a.lo[l * K + j], hi_ = a.hi[l * K + j];
 #pragma unroll
-                for (int w = 0; w < 4; ++w) {
-                    const uint32_t lw = w == 0 ? lo4.x : w == 1 ? lo4.y : w == 2 ? lo4.z : lo4.w;
-                    const uint32_t hw = w == 0 ? hi4.x : w == 1 ? hi4.y : w == 2 ? hi4.z : hi4.w;
-#pragma unroll
-                    for (int b = 0; b < 4; ++b) {
-                        const int j = w * 4 + b;
-                        const int lo_ = (lw >> (8 * b)) & 255, hi_ = (hw >> (8 * b)) & 255;
-#pragma unroll
-                        for (int g = 0; g < RF_G; ++g)
-                            lacc[g] += s_q16h[(j * N_r + min(max((int)s_sx[g][j], lo_), hi_)) * RF_G + g];
-                    }
-                }
-            } else {
-                for (int j = 0; j < K; ++j) {
-                    const int lo_ = a.lo[l * K + j], hi_ = a.hi[l * K + j];
-#pragma unroll
-                    for (int g = 0; g < RF_G; ++g)
-                        lacc[g] += s_q16h[(j * N_r + min(max((int)s_sx[g][j], lo_), hi_)) * RF_G + g];
+                for (int g = 0; g < G; ++g) {
+                    const int e = (j * N_r + min(max((int)s_sx[g][j], lo_), hi_)) * 16;
+                    lacc[g] += G == 8 ? (uint32_t)s_h[e / 2 + g] : (uint32_t)s_b[e + g];
                 }
             }
-            // a leaf is pruned only when its quantised bound proves LB > rho (no member can pass)
             uint32_t m = 0;
 #pragma unroll
-            for (int g = 0; g < RF_G; ++g)
-                if (lacc[g] <= RF_QT && ((amask >> g) & 1)) m |= 1u << g;
+            for (int g = 0; g < G; ++g)
+                if (lacc[g] <= QT && ((amask >> g) & 1)) m |= 1u << g;
             if (a.mode != DETLSH_MODE_CELL) {
-                // RELAXED (Sec. 6.2.2(1)): the leaf decision is final, so confirm it in fp32
+                // RELAXED (Sec. 6.2.2(1)): the leaf decision is final, so decide it in fp32
                 uint32_t conf = 0, mm = m;
                 while (mm) {
                     const int g = __ffs(mm) - 1;
@@ -248,51 +242,52 @@ __global__ void __launch_bounds__(RF_THREADS, 3) k_range_filter(RFArgs a) {
             uint4 c4 = make_uint4(0, 0, 0, 0);
             uint32_t pass = m, certain = 0;
             if (m && a.mode == DETLSH_MODE_CELL) {
+                uint32_t ok = 0, sure = 0;
                 if (KT == 16) {
                     c4 = *reinterpret_cast<const uint4*>(a.tcodes + pos * 16);
-                    uint32_t acc0 = 0, acc1 = 0, acc2 = 0, acc3 = 0;   // 2 queries per word
+                    uint32_t acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 #pragma unroll
                     for (int w = 0; w < 4; ++w) {
                         const uint32_t word = w == 0 ? c4.x : w == 1 ? c4.y : w == 2 ? c4.z : c4.w;
-                        const uint4* row = s_q16 + (w * 4) * N_r;
+                        const uint4* row = s_qe + (w * 4) * N_r;
 #pragma unroll
                         for (int b = 0; b < 4; ++b) {
                             const uint4 v = row[b * N_r + ((word >> (8 * b)) & 255u)];
-                            acc0 += v.x; acc1 += v.y; acc2 += v.z; acc3 += v.w;
+                            if (G == 8) {
+                                acc[0] += v.x; acc[1] += v.y; acc[2] += v.z; acc[3] += v.w;
+                            } else {      // bytes -> 16-bit lanes: (g0,g2) and (g1,g3) of each word
+                                acc[0] += v.x & 0x00FF00FFu; acc[1] += (v.x >> 8) & 0x00FF00FFu;
+                                acc[2] += v.y & 0x00FF00FFu; acc[3] += (v.y >> 8) & 0x00FF00FFu;
+                                acc[4] += v.z & 0x00FF00FFu; acc[5] += (v.z >> 8) & 0x00FF00FFu;
+                                acc[6] += v.w & 0x00FF00FFu; acc[7] += (v.w >> 8) & 0x00FF00FFu;
+                            }
                         }
                     }
-                    const uint32_t accs[4] = {acc0, acc1, acc2, acc3};
-                    uint32_t ok = 0, sure = 0;
 #pragma unroll
-                    for (int g = 0; g < RF_G; ++g) {
-                        const uint32_t sg = (accs[g >> 1] >> (16 * (g & 1))) & 0xFFFFu;
-                        ok |= (sg <= RF_QT ? 1u : 0u) << g;
-                        sure |= (sg <= RF_QT - 17 ? 1u : 0u) << g;
+                    for (int g = 0; g < G; ++g) {
+                        const uint32_t sg = G == 8 ? (acc[g >> 1] >> (16 * (g & 1))) & 0xFFFFu
+                                                   : (acc[2 * (g >> 2) + (g & 1)] >> (16 * ((g >> 1) & 1))) & 0xFFFFu;
+                        ok |= (sg <= QT ? 1u : 0u) << g;
+                        sure |= (sg + 17 <= QT ? 1u : 0u) << g;
                     }
-                    pass = m & ok;
-                    certain = m & sure;
                 } else {
-                    uint32_t acc[RF_G];
+                    uint32_t acc[G];
 #pragma unroll
-                    for (int g = 0; g < RF_G; ++g) acc[g] = 0;
+                    for (int g = 0; g < G; ++g) acc[g] = 0;
                     for (int j = 0; j < K; ++j) {
-                        const uint4 v = s_q16[j * N_r + a.tcodes[pos * K + j]];
-                        const uint32_t vw[4] = {v.x, v.y, v.z, v.w};
+                        const int e = (j * N_r + a.tcodes[pos * K + j]) * 16;
 #pragma unroll
-                        for (int g = 0; g < RF_G; ++g) acc[g] += (vw[g >> 1] >> (16 * (g & 1))) & 0xFFFFu;
+                        for (int g = 0; g < G; ++g) acc[g] += G == 8 ? (uint32_t)s_h[e / 2 + g] : (uint32_t)s_b[e + g];
                     }
-                    uint32_t ok = 0, sure = 0;
 #pragma unroll
-                    for (int g = 0; g < RF_G; ++g) {
-                        ok |= (acc[g] <= RF_QT ? 1u : 0u) << g;
-                        sure |= (acc[g] + 17 <= RF_QT ? 1u : 0u) << g;
+                    for (int g = 0; g < G; ++g) {
+                        ok |= (acc[g] <= QT ? 1u : 0u) << g;
+                        sure |= (acc[g] + 17 <= QT ? 1u : 0u) << g;
                     }
-                    pass = m & ok;
-                    certain = m & sure;
                 }
-                // Exact fp32 confirmation, only inside the quantisation band: e_j > D_j*2048/rho^2 - 1
-                // (products rounded down), so sum_j e_j <= 2031 proves sum_j D_j < rho^2 (1 - 1e-5)
-                // and the fp32 sum passes; 2032..2048 is decided by the exact fp32 sum in j order.
+                pass = m & ok;
+                certain = m & sure;
+                // exact fp32 decision inside the quantisation band (cell LB summed in j order)
                 uint32_t conf = certain;
                 pass &= ~certain;
                 while (pass) {
@@ -325,7 +320,7 @@ __global__ void __launch_bounds__(RF_THREADS, 3) k_range_filter(RFArgs a) {
         }
         __syncwarp();
     }
-    // ---- counters (point counters are per group as well; attributed evenly)
+    // ---- counters (per group; attributed evenly to its active queries)
     {
         uint32_t v[4] = {c_lt, c_lp, c_pt, c_pp};
 #pragma unroll
@@ -333,13 +328,13 @@ __global__ void __launch_bounds__(RF_THREADS, 3) k_range_filter(RFArgs a) {
             for (int o = 16; o > 0; o >>= 1) v[i] += __shfl_xor_sync(0xffffffffu, v[i], o);
         if (lane == 0) {
             const int na_ = max(1, __popc(amask));
-            for (int g = 0; g < RF_G; ++g)
+            for (int g = 0; g < G; ++g)
                 if ((amask >> g) & 1)
                     for (int i = 0; i < 4; ++i) atomicAdd(&s_ctr[g][i], v[i] / na_);
         }
     }
     __syncthreads();
-    if (threadIdx.x < RF_G && s_q[threadIdx.x] >= 0) {
+    if (threadIdx.x < G && s_q[threadIdx.x] >= 0) {
         unsigned long long* c = a.ctr + (int64_t)s_q[threadIdx.x] * 4;
         for (int i = 0; i < 4; ++i) atomicAdd(c + i, (unsigned long long)s_ctr[threadIdx.x][i]);
     }
@@ -1004,9 +999,10 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
     // per-batch LUTs
     Scratch s_lut(st, sizeof(float) * (size_t)(qb * LK * ix.N_r));
     Scratch s_sx(st, (size_t)(qb * LK));
-    const size_t rf_smem = sizeof(uint16_t) * (size_t)RF_G * ix.K * ix.N_r;
+    const size_t rf_smem = (size_t)16 * ix.K * ix.N_r;
     Scratch s_qlut(st, sizeof(uint16_t) * (size_t)(qb * LK * ix.N_r));
-    auto k_range_filter_sel = (ix.K == 16 && ix.N_r == 256) ? k_range_filter<16, 256> : k_range_filter<0, 0>;
+    auto k_range_filter_sel = (ix.K == 16 && ix.N_r == 256) ? k_range_filter<16 COMMA 256 COMMA RF_G>
+                                                            : k_range_filter<0 COMMA 0 COMMA RF_G>;
     DL_CUDA(cudaFuncSetAttribute(k_range_filter_sel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rf_smem));
     RFArgs ra;
     ra.leaf_off = ix.leaf_off.as<uint32_t>();
@@ -1071,10 +1067,10 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
             const float rho2 = (float)((eps * r) * (eps * r));
             const float cr2 = (float)((a.c * r) * (a.c * r));
             {   // quantised screen of this round: scale 2048 / rho^2 rounded down
-                const float inv_rd = fdiv_rd_host((float)RF_QT, rho2);
+                const float inv_rd = fdiv_rd_host((float)QuantSpec<RF_G>::QT, rho2);
                 const int64_t per_q = LK * ix.N_r;
                 DL_LAUNCH(k_build_qlut, (unsigned)std::min<int64_t>(ceil_div(na * per_q, 256), 148 * 32), 256, 0, st,
-                          s_lut.as<float>(), cur, na, per_q, inv_rd, s_qlut.as<uint16_t>());
+                          s_lut.as<float>(), cur, na, per_q, inv_rd, (float)QuantSpec<RF_G>::CAP, s_qlut.as<uint16_t>());
             }
             for (int t = 0; t < ix.L; ++t) {
                 ra.tcodes = ix.tcodes.as<uint8_t>() + (int64_t)t * n * ix.K;

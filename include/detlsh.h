@@ -52,7 +52,8 @@ typedef struct {
     uint64_t stream;       /* cudaStream_t, 0 = legacy default stream */
     int32_t  borrow_data;  /* 1: keep the caller's device pointer (d % 8 == 0) instead of copying */
     int32_t  proj_impl;    /* projection kernel: 0 = tcgen05 tensor cores, 1 = SIMT fp32 */
-    int64_t  mem_budget;   /* bytes of device scratch for query batches, 0 = auto */
+    int64_t  mem_budget;   /* bytes of device scratch for query batches, 0 = auto (60% of the
+                              memory free at the first query on this device in the process) */
 } detlsh_opts;
 
 /* Per-query statistics (Alg. 5 bookkeeping). */
@@ -191,6 +192,15 @@ detlsh_status detlsh_build_from_codes(const uint8_t* codes, int64_t n, int32_t L
 
 /* Number of kernels this library has launched in this process (evidence counter). */
 int64_t detlsh_launch_count(void);
+
+/* Scratch workspaces.  Every call that launches work bump-allocates its scratch from a
+   grow-only device arena owned by the library for its (device, stream), so repeated calls do
+   not go through the allocator (and never wait on the driver mapping memory).  The arena
+   keeps the high-water scratch of the largest call made on that stream (about 2 GB for a
+   1000-query batch at n = 1M).  release frees every arena (call it with no work in flight
+   on those streams); bytes reports what is held.  Neither fails. */
+void    detlsh_release_workspace(void);
+int64_t detlsh_workspace_bytes(void);
 
 /* Per-kernel device time, measured with CUDA events recorded on each launch's stream while
    enabled (used by bench.py for the live roofline).  read returns the number of kernels and

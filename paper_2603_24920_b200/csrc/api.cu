@@ -206,6 +206,7 @@ detlsh_status detlsh_build_ex(const float* data, int64_t n, int32_t d, int32_t L
         DL_REQUIRE(id_offset >= 0, "id_offset must be >= 0");
         require_device();
         cudaStream_t st = stream_of(&o);
+        WorkspaceScope ws(st);
         auto ix = std::make_unique<Index>();
         init_index_params(*ix, n, d, L, K, N_r, seed, o);
         ix->id_offset = id_offset;
@@ -255,6 +256,7 @@ detlsh_status detlsh_query_ex(const detlsh_index* idx, const float* queries, int
         DL_REQUIRE(o.mode == DETLSH_MODE_CELL || o.mode == DETLSH_MODE_RELAXED, "unknown mode");
         require_device();
         cudaStream_t st = stream_of(&o);
+        WorkspaceScope ws(st);
         Scratch s_q(st, sizeof(float) * (size_t)nq * ix.ld);
         stage_rows(queries, nq, ix.d, ix.ld, s_q.as<float>(), st);
         DevOut oi(out_ids, sizeof(int64_t) * (size_t)(nq * k), st);
@@ -288,6 +290,7 @@ detlsh_status detlsh_estimate_rmin(const detlsh_index* idx, const float* queries
         const detlsh_opts o = opts_or_default(opts);
         require_device();
         cudaStream_t st = stream_of(&o);
+        WorkspaceScope ws(st);
         Scratch s_q(st, sizeof(float) * (size_t)ns * ix.ld);
         stage_rows(queries, ns, ix.d, ix.ld, s_q.as<float>(), st);
         std::vector<double> rs((size_t)ns);
@@ -313,6 +316,7 @@ detlsh_status detlsh_project(const detlsh_index* idx, const float* X, int64_t m,
         if (m == 0) return;
         require_device();
         cudaStream_t st = 0;
+        WorkspaceScope ws(st);
         Scratch s_x(st, sizeof(float) * (size_t)m * ix.ld);
         stage_rows(X, m, ix.d, ix.ld, s_x.as<float>(), st);
         Scratch s_flag(st, sizeof(int));
@@ -332,6 +336,7 @@ detlsh_status detlsh_project_ex(const detlsh_index* idx, const float* X, int64_t
         if (m <= 0) return;
         require_device();
         cudaStream_t st = 0;
+        WorkspaceScope ws(st);
         Scratch s_x(st, sizeof(float) * (size_t)m * ix.ld);
         stage_rows(X, m, ix.d, ix.ld, s_x.as<float>(), st);
         Scratch s_flag(st, sizeof(int));
@@ -354,6 +359,7 @@ detlsh_status detlsh_sample_projections(const float* data, int64_t n, int32_t d,
         const detlsh_opts o = opts_or_default(opts);
         require_device();
         cudaStream_t st = stream_of(&o);
+        WorkspaceScope ws(st);
         Index ix;
         init_index_params(ix, n, d, L, K, N_r, seed, o);
         const int64_t n_s = detlsh_sample_size(n_global, N_r, sample_frac);
@@ -398,6 +404,7 @@ detlsh_status detlsh_breakpoints_from_samples(const float* samples, int64_t m, i
         require_device();
         const detlsh_opts o = opts_or_default(opts);
         cudaStream_t st = stream_of(&o);
+        WorkspaceScope ws(st);
         Scratch s_in(st, sizeof(float) * (size_t)(m * LK));
         DL_CUDA(cudaMemcpyAsync(s_in.p, samples, sizeof(float) * (size_t)(m * LK), cudaMemcpyDefault, st));
         DevOut bo(out, sizeof(float) * (size_t)LK * (N_r + 1), st);
@@ -439,6 +446,7 @@ detlsh_status detlsh_build_from_codes(const uint8_t* codes, int64_t n, int32_t L
         DL_REQUIRE(o.max_size >= 1, "max_size must be >= 1");
         require_device();
         cudaStream_t st = stream_of(&o);
+        WorkspaceScope ws(st);
         auto ix = std::make_unique<Index>();
         init_index_params(*ix, n, 1, L, K, N_r, 0, o);
         ix->codes_only = true;

@@ -112,19 +112,40 @@ struct Trace {
 };
 
 // ------------------------------------------------------------------ scratch allocation
-// Stream-ordered device scratch (cudaMallocAsync from the device pool).
+// Per-call device scratch.  Inside a WorkspaceScope (every C-ABI entry point that launches
+// work opens one for its stream) requests are bump-allocated from a grow-only arena owned by
+// that (device, stream): no allocator traffic between calls, so a query or build never
+// waits on the driver mapping memory.  A request the arena cannot hold yet is served by
+// cudaMallocAsync and counted; when the call ends the arena is regrown to the call's
+// high-water mark, so from the second call of a given shape on everything is bumped.
+// Outside a scope Scratch falls back to stream-ordered cudaMallocAsync/cudaFreeAsync.
+void* ws_alloc(size_t bytes, cudaStream_t st, bool* from_arena);
+
+struct WorkspaceScope {
+    explicit WorkspaceScope(cudaStream_t st);
+    ~WorkspaceScope();
+    WorkspaceScope(const WorkspaceScope&) = delete;
+    WorkspaceScope& operator=(const WorkspaceScope&) = delete;
+    void* impl = nullptr;
+    bool owner = false;
+};
+void ws_release_all();
+int64_t ws_bytes_held();
+
 struct Scratch {
     cudaStream_t st;
     void* p = nullptr;
+    bool arena = false;
     explicit Scratch(cudaStream_t s) : st(s) {}
     Scratch(cudaStream_t s, size_t bytes) : st(s) { alloc(bytes); }
     void alloc(size_t bytes) {
         free_();
-        if (bytes) DL_CUDA(cudaMallocAsync(&p, bytes, st));
+        if (bytes) p = ws_alloc(bytes, st, &arena);
     }
     void free_() {
-        if (p) cudaFreeAsync(p, st);
+        if (p && !arena) cudaFreeAsync(p, st);
         p = nullptr;
+        arena = false;
     }
     ~Scratch() { free_(); }
     template <class T> T* as() const { return static_cast<T*>(p); }

@@ -41,13 +41,23 @@ cudaEvent_t take_event() {
 }
 
 void drain_locked() {
+    // DETLSH_PROFILE_RAW=1: also print every launch as (start, duration) relative to the first
+    // launch of the batch (a device timeline for finding gaps between kernels).
+    static const bool raw = std::getenv("DETLSH_PROFILE_RAW") != nullptr;
     for (auto& r : g_recs) {
         cudaEventSynchronize(r.b);
         float ms = 0;
         cudaEventElapsedTime(&ms, r.a, r.b);
+        if (raw) {
+            float t0 = 0;
+            cudaEventElapsedTime(&t0, g_recs.front().a, r.a);
+            std::fprintf(stderr, "[detlsh launch] %10.3f %8.3f %s\n", t0, ms, r.name);
+        }
         Agg& g = g_agg[r.name];
         g.launches += 1;
         g.ms += ms;
+    }
+    for (auto& r : g_recs) {
         g_pool.push_back(r.a);
         g_pool.push_back(r.b);
     }

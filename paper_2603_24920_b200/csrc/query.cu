@@ -15,6 +15,7 @@
 //                 bitonic sort; then the radius test k-th d2 <= (c r)^2 (line 9, AMB-18).
 //  k_finalize     ids (global) and sqrt(d2), ascending by (dist, id) (AMB-21, AMB-28).
 #include <algorithm>
+#include <mutex>
 #include <cmath>
 #include <cstring>
 #include <vector>
@@ -835,6 +836,20 @@ __global__ void k_init_batch(QState* __restrict__ qs, int* __restrict__ act, int
     }
 }
 
+int64_t auto_query_budget() {
+    static std::mutex mu;
+    static int64_t cached[64] = {};
+    int dev = 0;
+    DL_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(mu);
+    if (!cached[dev]) {
+        size_t fr = 0, tot = 0;
+        DL_CUDA(cudaMemGetInfo(&fr, &tot));
+        cached[dev] = std::max<int64_t>(1, (int64_t)(fr * 0.6));
+    }
+    return cached[dev];
+}
+
 // 2048 / rho2 rounded toward zero (a lower bound of the exact scale factor).
 float fdiv_rd_host(float num, float den) {
     const double x = (double)num / (double)den;
@@ -963,9 +978,10 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
                           (int64_t)(std::min(1.0, a.beta * 2.0) * n) * 8;   // round buffer share
     int64_t budget_bytes = a.mem_budget;
     if (budget_bytes <= 0) {
-        size_t fr = 0, tot = 0;
-        DL_CUDA(cudaMemGetInfo(&fr, &tot));
-        budget_bytes = (int64_t)(fr * 0.6);
+        // 60% of the memory free at this device's first query of the process.  cudaMemGetInfo
+        // is not on the per-call path: measured on B200 it took 0.1-75 ms per call (the stream
+        // idles meanwhile), which was up to 4x the whole query.
+        budget_bytes = auto_query_budget();
     }
     int64_t qb = a.query_batch > 0 ? a.query_batch : std::max<int64_t>(1, budget_bytes / per_q);
     qb = std::min<int64_t>({qb, nq, 65535});

@@ -91,6 +91,8 @@ def lib():
         "detlsh_estimate_rmin": (i32, [P, P, i64, i32, f64, O, P, P]),
         "detlsh_profile_enable": (None, [i32]),
         "detlsh_profile_reset": (None, []),
+        "detlsh_release_workspace": (None, []),
+        "detlsh_workspace_bytes": (i64, []),
         "detlsh_profile_read": (i32, [P, i32]),
     }
     for name, (res, args) in sig.items():
@@ -148,6 +150,14 @@ def launch_count() -> int:
 
 def profile_enable(on: bool = True):
     lib().detlsh_profile_enable(1 if on else 0)
+
+
+def release_workspace():
+    lib().detlsh_release_workspace()
+
+
+def workspace_bytes() -> int:
+    return int(lib().detlsh_workspace_bytes())
 
 
 def profile_reset():

@@ -170,6 +170,8 @@ void detlsh_default_opts(detlsh_opts* o) {
     o->borrow_data = 0;
     o->proj_impl = 0;
     o->mem_budget = 0;
+    o->verify_impl = 0;
+    o->pad0 = 0;
 }
 
 const char* detlsh_last_error(void) { return g_err.c_str(); }
@@ -263,7 +265,8 @@ detlsh_status detlsh_query_ex(const detlsh_index* idx, const float* queries, int
         DevOut od(out_dists, sizeof(float) * (size_t)(nq * k), st);
         std::unique_ptr<DevOut> os;
         if (stats) os.reset(new DevOut(stats, sizeof(detlsh_query_stats) * (size_t)nq, st));
-        QueryArgs a{nq, k, c, r_min, beta, o.mode, o.query_batch, o.mem_budget, o.proj_impl};
+        DL_REQUIRE(o.verify_impl == 0 || o.verify_impl == 1, "verify_impl must be 0 or 1");
+        QueryArgs a{nq, k, c, r_min, beta, o.mode, o.query_batch, o.mem_budget, o.proj_impl, o.verify_impl};
         query_index(ix, s_q.as<float>(), ix.ld, a, static_cast<int64_t*>(oi.dev()), static_cast<float*>(od.dev()),
                     os ? static_cast<detlsh_query_stats*>(os->dev()) : nullptr, st);
         oi.finish(st);

@@ -593,6 +593,19 @@ __global__ void k_tree_tiles(const uint32_t* __restrict__ idx, const unsigned lo
     if (t == L) tile_begin[t] = ntiles;
 }
 
+// ||x||^2 of every row, warp per row (used when the projection ran on the CUDA cores).
+__global__ void k_row_norms(const float* __restrict__ X, int64_t ld, int64_t n, float* __restrict__ out) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; r < n;
+         r += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const float* x = X + r * ld;
+        float acc = 0.f;
+        for (int64_t i = lane; i < ld; i += 32) acc = fmaf(x[i], x[i], acc);
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0) out[r] = acc;
+    }
+}
+
 int grid_for(int64_t work, int threads, int cap = 148 * 16) {
     int64_t g = ceil_div(std::max<int64_t>(work, 1), threads);
     return (int)std::min<int64_t>(g, cap);
@@ -811,7 +824,7 @@ static void build_trees(Index& ix, const uint8_t* d_EP, cudaStream_t st) {
 }
 
 bool project_encode_tc(const Index& ix, const float* d_X, int64_t ld, int64_t m, uint8_t* d_EP, int* d_nonfinite,
-                       cudaStream_t st);
+                       float* d_xnorm, cudaStream_t st);
 
 void build_index(Index& ix, const float* d_data, int64_t data_ld, const float* bp_given, double sample_frac,
                  int proj_impl, cudaStream_t st) {
@@ -847,7 +860,10 @@ void build_index(Index& ix, const float* d_data, int64_t data_ld, const float* b
     // B2 + B4: project every row and encode -- fused in the tensor-core epilogue when the
     // shape fits, else projection (chunked so P stays bounded) + k_encode
     Scratch s_ep(st, (size_t)n * ix.LK);
-    if (!(proj_impl == 0 && project_encode_tc(ix, d_data, data_ld, n, s_ep.as<uint8_t>(), s_flag.as<int>(), st))) {
+    ix.xnorm.alloc(sizeof(float) * (size_t)n, st);     // ||x||^2 per row (tensor-core verification)
+    if (!(proj_impl == 0 &&
+          project_encode_tc(ix, d_data, data_ld, n, s_ep.as<uint8_t>(), s_flag.as<int>(), ix.xnorm.as<float>(), st))) {
+        DL_LAUNCH(k_row_norms, grid_for(n * 32, 256), 256, 0, st, d_data, data_ld, n, ix.xnorm.as<float>());
         const int64_t chunk = std::min<int64_t>(n, std::max<int64_t>(1 << 16, (int64_t)(1ll << 30) / (4 * ix.LK)));
         Scratch s_p(st, sizeof(float) * (size_t)(chunk * ix.LK));
         for (int64_t r0 = 0; r0 < n; r0 += chunk) {

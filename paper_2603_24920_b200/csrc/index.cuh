@@ -63,6 +63,7 @@ struct Index {
     DevBuf tile_leaf;       // [ntiles+1] first leaf of each query tile (tree-major; see build.cu)
     std::vector<int64_t> tree_tile_begin;  // [L+1] tile index range of each tree (host copy)
     DevBuf point_tile_leaf; // [L*n] u16: leaf of each point (tree order) within its tile (< 32)
+    DevBuf xnorm;           // [n] fp32 ||x||^2 of every row (tensor-core verification, verify_tc.cu)
 
     int64_t nl_total() const { return tree_leaf_begin.empty() ? 0 : tree_leaf_begin.back(); }
 };
@@ -90,6 +91,7 @@ struct QueryArgs {
     int query_batch;
     int64_t mem_budget;
     int proj_impl;
+    int verify_impl;
 };
 void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArgs& a, int64_t* d_ids,
                  float* d_dists, detlsh_query_stats* d_stats, cudaStream_t st);

@@ -19,77 +19,17 @@
 #include <cuda.h>
 
 #include "index.cuh"
+#include "tc_util.cuh"
 
 namespace detlsh {
 
 namespace {
+using namespace tc;
 
 constexpr int TC_M = 128;           // rows per tile (UMMA M)
 constexpr int TC_KB = 32;           // fp32 per k-block (= 128 B, one swizzle row)
 constexpr int TC_THREADS = 256;
 constexpr int TC_STAGE_BYTES = TC_M * TC_KB * 4;   // 16 KB
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-    const uint32_t a = smem_u32(bar);
-    uint32_t done = 0;
-    while (!done) {
-        asm volatile(
-            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
-            : "=r"(done)
-            : "r"(a), "r"(parity)
-            : "memory");
-    }
-}
-__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
-            smem_u32(dst)),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
-        : "memory");
-}
-// Shared-memory matrix descriptor, K-major, 128-byte swizzle: rows of 128 B, 8-row groups
-// 1024 B apart (SBO), LBO unused (1), descriptor version 1 (sm_100).
-__device__ __forceinline__ uint64_t desc_sw128(uint32_t saddr) {
-    return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
-           ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
-}
-__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
-                                         uint32_t accumulate) {
-    asm volatile(
-        "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
-        " tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
-        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
-}
-__device__ __forceinline__ void mma_commit(uint64_t* bar) {
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
-                 : "memory");
-}
-__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
-
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
-    uint32_t r[16];
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-        : "r"(taddr));
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-    for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
-}
 
 struct TcShape {
     int64_t m;        // rows
@@ -104,7 +44,7 @@ struct TcShape {
 __global__ void __launch_bounds__(TC_THREADS, 1)
     k_project_tc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmA, TcShape sh,
                  float* __restrict__ P, int* __restrict__ nonfinite, const float* __restrict__ B,
-                 uint8_t* __restrict__ EP) {
+                 uint8_t* __restrict__ EP, float* __restrict__ xnorm) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     // 1024-byte alignment of every swizzled buffer
     unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -199,18 +139,24 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             }
         }
     } else if (warp < 4) {
-        // converters: lo = x - trunc_tf32(x), same swizzled offsets
+        // converters: lo = x - trunc_tf32(x), same swizzled offsets.  Thread t sees float4
+        // t + 64 m (m < 16) of every stage, i.e. rows t/8 + 8 m (swizzling permutes 16-byte
+        // chunks only within a row), so it also accumulates those rows' ||x||^2 (xnorm != null).
         const int t = threadIdx.x - 64;
         int s = 0;
         uint32_t ph = 0;
         bool bad = false;
         for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+            float nacc[16];
+#pragma unroll
+            for (int m = 0; m < 16; ++m) nacc[m] = 0.f;
             for (int kb = 0; kb < sh.nkb; ++kb) {
                 mbar_wait(&full[s], ph);
                 const float4* src = reinterpret_cast<const float4*>(sX + (size_t)s * TC_STAGE_BYTES);
                 float4* dst = reinterpret_cast<float4*>(sL + (size_t)s * TC_STAGE_BYTES);
-#pragma unroll 4
-                for (int i = t; i < TC_STAGE_BYTES / 16; i += 64) {
+#pragma unroll
+                for (int m = 0; m < 16; ++m) {
+                    const int i = t + 64 * m;
                     const float4 x = src[i];
                     float4 lo;
                     lo.x = x.x - __uint_as_float(__float_as_uint(x.x) & 0xFFFFE000u);
@@ -219,10 +165,22 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                     lo.w = x.w - __uint_as_float(__float_as_uint(x.w) & 0xFFFFE000u);
                     bad |= !(isfinite(x.x) && isfinite(x.y) && isfinite(x.z) && isfinite(x.w));
                     dst[i] = lo;
+                    nacc[m] = fmaf(x.x, x.x, fmaf(x.y, x.y, fmaf(x.z, x.z, fmaf(x.w, x.w, nacc[m]))));
                 }
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 mbar_arrive(&conv[s]);
                 if (++s == S) { s = 0; ph ^= 1; }
+            }
+            if (xnorm) {
+#pragma unroll
+                for (int m = 0; m < 16; ++m) {
+                    float v = nacc[m];
+                    v += __shfl_xor_sync(0xffffffffu, v, 1);
+                    v += __shfl_xor_sync(0xffffffffu, v, 2);
+                    v += __shfl_xor_sync(0xffffffffu, v, 4);
+                    const int64_t row = tile * TC_M + (t >> 3) + 8 * m;
+                    if ((t & 7) == 0 && row < sh.m) xnorm[row] = v;
+                }
             }
         }
         if (bad) atomicOr(nonfinite, 1);
@@ -295,39 +253,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     }
 }
 
-typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
-EncodeTiledFn encode_fn() {
-    static EncodeTiledFn fn = nullptr;
-    if (!fn) {
-        void* p = nullptr;
-        cudaDriverEntryPointQueryResult q;
-        DL_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
-        if (!p || q != cudaDriverEntryPointSuccess) throw Error(DETLSH_ECUDA, "cuTensorMapEncodeTiled unavailable");
-        fn = reinterpret_cast<EncodeTiledFn>(p);
-    }
-    return fn;
-}
-
-void make_map(CUtensorMap* map, const float* ptr, int64_t rows, int ld, int box_rows) {
-    const cuuint64_t dims[2] = {(cuuint64_t)ld, (cuuint64_t)rows};
-    const cuuint64_t strides[1] = {(cuuint64_t)ld * 4};
-    const cuuint32_t box[2] = {(cuuint32_t)TC_KB, (cuuint32_t)box_rows};
-    const cuuint32_t estr[2] = {1, 1};
-    CUresult r = encode_fn()(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(ptr), dims, strides, box, estr,
-                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) throw Error(DETLSH_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
-}
-
 }  // namespace
 
 // Returns false when the shape does not fit this kernel (resident hash matrix too large).
 // B != nullptr: fused encode (Alg. 1) -- writes codes EP[m][LK] instead of P.
 static bool launch_tc(const Index& ix, const float* d_X, int64_t ld, int64_t m, float* d_P, int* d_nonfinite,
-                      const float* B, uint8_t* EP, cudaStream_t st) {
+                      const float* B, uint8_t* EP, float* xnorm, cudaStream_t st) {
     if (m <= 0) return true;
     TcShape sh;
     sh.m = m;
@@ -360,18 +291,18 @@ static bool launch_tc(const Index& ix, const float* d_X, int64_t ld, int64_t m, 
     DL_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
     const int64_t ntiles = ceil_div(m, TC_M);
     const int grid = (int)std::min<int64_t>(ntiles, nsm);
-    DL_LAUNCH(k_project_tc, grid, TC_THREADS, smem, st, mx, ma, sh, d_P, d_nonfinite, B, EP);
+    DL_LAUNCH(k_project_tc, grid, TC_THREADS, smem, st, mx, ma, sh, d_P, d_nonfinite, B, EP, xnorm);
     return true;
 }
 
 bool project_rows_tc(const Index& ix, const float* d_X, int64_t ld, int64_t m, float* d_P, int* d_nonfinite,
                      cudaStream_t st) {
-    return launch_tc(ix, d_X, ld, m, d_P, d_nonfinite, nullptr, nullptr, st);
+    return launch_tc(ix, d_X, ld, m, d_P, d_nonfinite, nullptr, nullptr, nullptr, st);
 }
 
 bool project_encode_tc(const Index& ix, const float* d_X, int64_t ld, int64_t m, uint8_t* d_EP, int* d_nonfinite,
-                       cudaStream_t st) {
-    return launch_tc(ix, d_X, ld, m, nullptr, d_nonfinite, ix.B.as<float>(), d_EP, st);
+                       float* d_xnorm, cudaStream_t st) {
+    return launch_tc(ix, d_X, ld, m, nullptr, d_nonfinite, ix.B.as<float>(), d_EP, d_xnorm, st);
 }
 
 }  // namespace detlsh

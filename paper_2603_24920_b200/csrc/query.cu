@@ -26,6 +26,9 @@ namespace detlsh {
 
 void project_rows(const Index& ix, const float* d_X, int64_t ld, int64_t m, float* d_P, int proj_impl,
                   int* d_nonfinite, cudaStream_t st);
+bool verify_tc(const float* d_X, int64_t n, int ld, const float* d_Qa, const float* d_Qalo, const float* d_qn, int na,
+               const uint32_t* d_NB, const uint32_t* d_BO, int64_t nw4, const float* d_xn, uint32_t* d_cand,
+               float* d_d2, cudaStream_t st);
 
 namespace {
 
@@ -104,7 +107,10 @@ constexpr int RF_G = 16;         // queries per CTA (8-bit terms); 8 selects 12-
 
 template <int G> struct QuantSpec;
 template <> struct QuantSpec<8> { static constexpr uint32_t QT = 2048, CAP = 4095; };
-template <> struct QuantSpec<16> { static constexpr uint32_t QT = 128, CAP = 255; };
+// G = 16: terms are clamped at 127 so that two of them add inside an 8-bit lane.  Clamping
+// keeps every term a lower bound (reject rule intact), and a clamped term alone exceeds the
+// sure-accept limit QT - 17, so such a point is always decided in fp32 (no result changes).
+template <> struct QuantSpec<16> { static constexpr uint32_t QT = 128, CAP = 127; };
 
 struct RFArgs {
     const uint8_t* tcodes;      // tree t: [n][K]
@@ -251,16 +257,26 @@ __global__ void __launch_bounds__(RF_THREADS, 3) k_range_filter(RFArgs a) {
                     for (int w = 0; w < 4; ++w) {
                         const uint32_t word = w == 0 ? c4.x : w == 1 ? c4.y : w == 2 ? c4.z : c4.w;
                         const uint4* row = s_qe + (w * 4) * N_r;
+                        if (G == 8) {
 #pragma unroll
-                        for (int b = 0; b < 4; ++b) {
-                            const uint4 v = row[b * N_r + ((word >> (8 * b)) & 255u)];
-                            if (G == 8) {
+                            for (int b = 0; b < 4; ++b) {
+                                const uint4 v = row[b * N_r + ((word >> (8 * b)) & 255u)];
                                 acc[0] += v.x; acc[1] += v.y; acc[2] += v.z; acc[3] += v.w;
-                            } else {      // bytes -> 16-bit lanes: (g0,g2) and (g1,g3) of each word
-                                acc[0] += v.x & 0x00FF00FFu; acc[1] += (v.x >> 8) & 0x00FF00FFu;
-                                acc[2] += v.y & 0x00FF00FFu; acc[3] += (v.y >> 8) & 0x00FF00FFu;
-                                acc[4] += v.z & 0x00FF00FFu; acc[5] += (v.z >> 8) & 0x00FF00FFu;
-                                acc[6] += v.w & 0x00FF00FFu; acc[7] += (v.w >> 8) & 0x00FF00FFu;
+                            }
+                        } else {
+                            // 7-bit terms (CAP 127): two dims add inside the 8-bit lanes without
+                            // carry (<= 254); each pair sum is then widened into 16-bit lanes
+                            // (g0,g2) by a mask and (g1,g3) by a byte permute.
+                            const uint4 va = row[0 * N_r + (word & 255u)];
+                            const uint4 vb = row[1 * N_r + ((word >> 8) & 255u)];
+                            const uint4 vc = row[2 * N_r + ((word >> 16) & 255u)];
+                            const uint4 vd = row[3 * N_r + (word >> 24)];
+                            const uint32_t p[4] = {va.x + vb.x, va.y + vb.y, va.z + vb.z, va.w + vb.w};
+                            const uint32_t r[4] = {vc.x + vd.x, vc.y + vd.y, vc.z + vd.z, vc.w + vd.w};
+#pragma unroll
+                            for (int i = 0; i < 4; ++i) {
+                                acc[2 * i] += (p[i] & 0x00FF00FFu) + (r[i] & 0x00FF00FFu);
+                                acc[2 * i + 1] += __byte_perm(p[i], 0u, 0x4341) + __byte_perm(r[i], 0u, 0x4341);
                             }
                         }
                     }
@@ -557,6 +573,77 @@ __global__ void __launch_bounds__(VR_THREADS) k_verify_rows(VRArgs a) {
     }
 }
 
+// ---- tensor-core verification inputs (verify_tc.cu), per round:
+//  k_verify_prep   per active query a: NB[a][w] = cur & ~ver (the new members of S in word w),
+//                  BO[a][w] = the query's round offset + new members in earlier words (a block
+//                  scan), and ver catches up with cur.
+//  k_prep_queries  the active queries as a contiguous [na][ld] fp32 block, its TF32 residual
+//                  q - trunc_tf32(q), and ||q||^2.
+__global__ void __launch_bounds__(1024) k_verify_prep(const int* __restrict__ act, const QState* __restrict__ qs,
+                                                      const uint32_t* __restrict__ cur, uint32_t* __restrict__ ver,
+                                                      int64_t nwords, int64_t nw4, uint32_t* __restrict__ NB,
+                                                      uint32_t* __restrict__ BO) {
+    __shared__ uint32_t s_w[32];
+    const int a = blockIdx.x;
+    const int q = act[a];
+    const uint32_t* c = cur + (int64_t)q * nwords;
+    uint32_t* v = ver + (int64_t)q * nwords;
+    uint32_t* nb_out = NB + (int64_t)a * nw4;
+    uint32_t* bo_out = BO + (int64_t)a * nw4;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    uint32_t carry = (uint32_t)qs[q].roff;
+    for (int64_t b0 = 0; b0 < nw4; b0 += 1024) {
+        const int64_t b = b0 + threadIdx.x;
+        uint32_t nb = 0;
+        if (b < nwords) {
+            const uint32_t cv = c[b];
+            nb = cv & ~v[b];
+            if (nb) v[b] = cv;
+        }
+        const uint32_t cnt = __popc(nb);
+        uint32_t x = cnt;
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) s_w[w] = x;
+        __syncthreads();
+        if (w == 0) {
+            uint32_t t = s_w[lane];
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, t, o);
+                if (lane >= o) t += y;
+            }
+            s_w[lane] = t;
+        }
+        __syncthreads();
+        const uint32_t incl = x + (w ? s_w[w - 1] : 0);
+        if (b < nw4) {
+            nb_out[b] = nb;
+            bo_out[b] = carry + incl - cnt;
+        }
+        carry += s_w[31];
+        __syncthreads();
+    }
+}
+
+__global__ void k_prep_queries(const float* __restrict__ Q, int64_t ld, const int* __restrict__ act, int na,
+                               float* __restrict__ Qa, float* __restrict__ Qalo, float* __restrict__ qn) {
+    const int lane = threadIdx.x & 31;
+    for (int a = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); a < na; a += gridDim.x * (blockDim.x >> 5)) {
+        const float* src = Q + (int64_t)act[a] * ld;
+        float acc = 0.f;
+        for (int64_t i = lane; i < ld; i += 32) {
+            const float x = src[i];
+            Qa[(int64_t)a * ld + i] = x;
+            Qalo[(int64_t)a * ld + i] = x - __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
+            acc = fmaf(x, x, acc);
+        }
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0) qn[a] = acc;
+    }
+}
+
 // ---- per round: slot ranges of the new members of S (|S| - verified) in the round buffer
 __global__ void __launch_bounds__(1024) k_round_offsets(const int* __restrict__ act, int na, QState* __restrict__ qs,
                                                         unsigned long long* __restrict__ total) {
@@ -623,6 +710,41 @@ __device__ void bitonic_sort_smem(unsigned long long* a, int n2) {
             __syncthreads();
         }
     }
+}
+
+// ---- after the rounds of a batch: the top-k distances recomputed directly in fp32 (the
+//      tensor-core verification ranks by ||x||^2 + ||q||^2 - 2 x.q), re-sorted by (d2, id).
+__global__ void __launch_bounds__(256) k_rerank_exact(const QState* __restrict__ qs, const float* __restrict__ X,
+                                                      const float* __restrict__ Q, int64_t ld, int k,
+                                                      unsigned long long* __restrict__ topk) {
+    __shared__ unsigned long long s_keys[TK_MAX];
+    const int q = blockIdx.x;
+    const int tk = qs[q].tk;
+    if (tk <= 0) return;
+    unsigned long long* t = topk + (int64_t)q * k;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const float4* q4 = reinterpret_cast<const float4*>(Q + (int64_t)q * ld);
+    const int nf4 = (int)(ld / 4);
+    for (int e = warp; e < tk; e += 8) {
+        const uint32_t id = (uint32_t)(t[e] & 0xFFFFFFFFull);
+        const float4* x4 = reinterpret_cast<const float4*>(X + (int64_t)id * ld);
+        float2 acc = make_float2(0.f, 0.f);
+        for (int f = lane; f < nf4; f += 32) {
+            const float4 x = __ldg(x4 + f), y = __ldg(q4 + f);
+            const float2 d0 = make_float2(x.x - y.x, x.y - y.y), d1 = make_float2(x.z - y.z, x.w - y.w);
+            acc = __ffma2_rn(d0, d0, acc);
+            acc = __ffma2_rn(d1, d1, acc);
+        }
+        float s_ = acc.x + acc.y;
+        for (int o = 16; o > 0; o >>= 1) s_ += __shfl_xor_sync(0xffffffffu, s_, o);
+        if (lane == 0) s_keys[e] = mkkey(s_, id);
+    }
+    int n2 = 1;
+    while (n2 < tk) n2 <<= 1;
+    for (int i = tk + threadIdx.x; i < n2; i += blockDim.x) s_keys[i] = ~0ull;
+    __syncthreads();
+    bitonic_sort_smem(s_keys, n2);
+    for (int i = threadIdx.x; i < tk; i += blockDim.x) t[i] = s_keys[i];
 }
 
 __global__ void __launch_bounds__(TK_THREADS) k_topk(const int* __restrict__ act, QState* __restrict__ qs,
@@ -974,7 +1096,7 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
     tr.mark("project queries", st);
 
     // batch size from the memory budget: bitmap + candidate list + distances per query
-    const int64_t per_q = nwords * 12 + (int64_t)k * 8 + (int64_t)LK * (ix.N_r * 6 + 1) + 96 +
+    const int64_t per_q = nwords * 20 + (int64_t)ix.ld * 8 + (int64_t)k * 8 + (int64_t)LK * (ix.N_r * 6 + 1) + 96 +
                           (int64_t)(std::min(1.0, a.beta * 2.0) * n) * 8;   // round buffer share
     int64_t budget_bytes = a.mem_budget;
     if (budget_bytes <= 0) {
@@ -1053,7 +1175,10 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
         va.rbw = (int)std::max<int64_t>(1, std::min<int64_t>(8, (120 * 1024) / per_word));
     }
     const size_t vr_smem = (size_t)va.rbw * 32 * ix.ld * 4;
-    Scratch s_boff(st, sizeof(uint32_t) * (size_t)(qb * ceil_div(nwords, va.rbw)));
+    const bool use_tc = a.verify_impl == 0 && ix.xnorm.p != nullptr;
+    const int64_t nw4 = round_up(nwords, 4);
+    Scratch s_boff(st, sizeof(uint32_t) * (size_t)(use_tc ? 2 * qb * nw4 : qb * ceil_div(nwords, va.rbw)));
+    Scratch s_qa(st, use_tc ? sizeof(float) * (size_t)(qb * (2 * ix.ld + 1)) : 0);
     const bool vexact = (ix.ld / 4) == 8 * vnv;
     DL_CUDA(cudaFuncSetAttribute(k_verify_rows<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)vr_smem));
     DL_CUDA(cudaFuncSetAttribute(k_verify_rows<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)vr_smem));
@@ -1126,6 +1251,21 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
             va.na = na;
             va.nblocks = ceil_div(nwords, va.rbw);
             va.boff = s_boff.as<uint32_t>();
+            bool done_tc = false;
+            if (use_tc) {
+                uint32_t* NB = s_boff.as<uint32_t>();
+                uint32_t* BO = NB + (int64_t)qb * nw4;
+                float* Qa = s_qa.as<float>();
+                float* Qalo = Qa + (int64_t)qb * ix.ld;
+                float* qn = Qalo + (int64_t)qb * ix.ld;
+                DL_LAUNCH(k_verify_prep, (unsigned)na, 1024, 0, st, cur, s_qs.as<QState>(), s_bm.as<uint32_t>(),
+                          s_ver.as<uint32_t>(), nwords, nw4, NB, BO);
+                DL_LAUNCH(k_prep_queries, (unsigned)ceil_div(na, 8), 256, 0, st, Qb, (int64_t)ix.ld, cur, na, Qa, Qalo, qn);
+                done_tc = verify_tc(ix.Xp, n, ix.ld, Qa, Qalo, qn, na, NB, BO, nw4, ix.xnorm.as<float>(), va.cand, va.d2,
+                                    st);
+                DL_REQUIRE(done_tc, "tensor-core verification does not fit this shape");
+            }
+            if (!done_tc) {
             DL_LAUNCH(k_verify_offsets, (unsigned)na, 1024, 0, st, cur, s_qs.as<QState>(), s_bm.as<uint32_t>(),
                       s_ver.as<uint32_t>(), nwords, va.rbw, va.nblocks, s_boff.as<uint32_t>());
             {
@@ -1142,6 +1282,7 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
                     default: DL_LAUNCH(k_verify_rows<0 COMMA false>, nblocks, VR_THREADS, vr_smem, st, va); break;
                 }
             }
+            }
             tr.mark("round buffer + verify", st);
             DL_LAUNCH(k_topk, (unsigned)na, TK_THREADS, 0, st, cur, s_qs.as<QState>(), va.cand, va.d2,
                       s_tk.as<unsigned long long>(), k, cr2, m);
@@ -1152,6 +1293,8 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
             std::swap(cur, nxt);
         }
         tr.mark("rounds done", st);
+        DL_LAUNCH(k_rerank_exact, (unsigned)nqb, 256, 0, st, s_qs.as<QState>(), ix.Xp, Qb, (int64_t)ix.ld, k,
+                  s_tk.as<unsigned long long>());
         DL_LAUNCH(k_finalize, (unsigned)std::min<int64_t>(ceil_div((int64_t)nqb * k, 256), 148 * 16), 256, 0, st,
                   s_qs.as<QState>(), s_ctr.as<unsigned long long>(), s_tk.as<unsigned long long>(), nqb, k, ix.id_offset, s_radii.as<double>(),
                   d_ids + q0 * k, d_dists + q0 * k, d_stats ? d_stats + q0 : nullptr);

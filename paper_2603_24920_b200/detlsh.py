@@ -31,7 +31,8 @@ class DetlshError(RuntimeError):
 class detlsh_opts(C.Structure):
     _fields_ = [("max_size", C.c_int32), ("sample_frac", C.c_double), ("mode", C.c_int32),
                 ("query_batch", C.c_int32), ("stream", C.c_uint64), ("borrow_data", C.c_int32),
-                ("proj_impl", C.c_int32), ("mem_budget", C.c_int64)]
+                ("proj_impl", C.c_int32), ("mem_budget", C.c_int64),
+                ("verify_impl", C.c_int32), ("pad0", C.c_int32)]
 
 
 class detlsh_kernel_time(C.Structure):

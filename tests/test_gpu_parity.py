@@ -136,10 +136,12 @@ def _dist_match(ig, dg, io, do):
                 assert abs(d - m[i]) <= 1e-4 * max(1e-30, m[i]) + 1e-30
 
 
+@pytest.mark.parametrize("vimpl", [0, 1])     # 0 = tcgen05 verification, 1 = CUDA cores
 @pytest.mark.parametrize("mode", [P.MODE_CELL, P.MODE_RELAXED])
-def test_query_parity_tiny(gpu_tiny, tiny_oracle, tiny, tiny_rmin, mode):
+def test_query_parity_tiny(gpu_tiny, tiny_oracle, tiny, tiny_rmin, mode, vimpl):
     c = tiny["cfg"]
-    ig, dg, sg = gpu_tiny.query(tiny["Q"], c.k, c.c, tiny_rmin, c.beta, opts=P.default_opts(mode=mode), stats=True)
+    ig, dg, sg = gpu_tiny.query(tiny["Q"], c.k, c.c, tiny_rmin, c.beta, opts=P.default_opts(mode=mode, verify_impl=vimpl),
+                                stats=True)
     io, do, so = tiny_oracle.query(tiny["Q"], c.k, c.c, tiny_rmin, c.beta, mode=mode)
     rec = _recall(ig, io)
     print(f"mode {mode}: recall vs oracle {rec:.4f}; reasons gpu {np.bincount(sg['reason'], minlength=3)} "
@@ -275,3 +277,30 @@ def test_large_k(gpu_tiny, tiny_oracle, tiny, tiny_rmin):
         io, do, _ = tiny_oracle.query(tiny["Q"][:12], k, c.c, tiny_rmin, c.beta)
         assert _recall(ig, io) >= 0.99
         _dist_match(ig, dg, io, do)
+
+
+@pytest.mark.parametrize("n,d,nq,k", [(6000, 128, 300, 10), (3001, 37, 17, 7), (2048, 960, 40, 20), (1500, 96, 257, 5)])
+def test_verify_tc_vs_simt_and_oracle(n, d, nq, k):
+    """Tensor-core verification (3xTF32 dot products, ||x||^2 + ||q||^2 - 2 x.q) against the
+    CUDA-core one and the oracle: ragged d (partial k-blocks), query tiles of 256 with a ragged
+    last tile, several rounds with shrinking active sets.  Returned distances are recomputed
+    in fp32, so both implementations must agree to 1e-5 on common ids."""
+    D = datagen.generate(1, n=n, nq=nq)
+    X = np.ascontiguousarray(D["X"][:, :d]) if d <= 128 else np.ascontiguousarray(
+        np.tile(D["X"], (1, (d + 127) // 128))[:, :d])
+    Q = np.ascontiguousarray(D["Q"][:, :d]) if d <= 128 else np.ascontiguousarray(
+        np.tile(D["Q"], (1, (d + 127) // 128))[:, :d])
+    g = P.detlsh_build(X, 4, 16, 256, 3)
+    o = O.Index(X, 4, 16, 256, 3)
+    rmin = 0.2 * o.estimate_rmin(Q[:8], k, 1.5, 0.1)       # start low: several rounds
+    it, dt, st = g.query(Q, k, 1.5, rmin, 0.1, opts=P.default_opts(verify_impl=0), stats=True)
+    iS, dS, sS = g.query(Q, k, 1.5, rmin, 0.1, opts=P.default_opts(verify_impl=1), stats=True)
+    assert _recall(it, iS) >= 0.995
+    assert np.mean(st["n_cand"] == sS["n_cand"]) >= 0.95
+    same = it == iS
+    assert np.allclose(dt[same], dS[same], rtol=1e-5, atol=0)
+    sel = np.arange(0, nq, max(1, nq // 24))
+    io, do, so = o.query(Q[sel], k, 1.5, rmin, 0.1)
+    assert _recall(it[sel], io) >= 0.99
+    _dist_match(it[sel], dt[sel], io, do)
+    assert st["rounds"].max() >= 2

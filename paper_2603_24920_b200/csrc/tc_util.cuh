@@ -45,6 +45,11 @@ __device__ __forceinline__ uint64_t desc_sw128(uint32_t saddr) {
     return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
            ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
 }
+// Same, 64-byte swizzle: rows of 64 B, 8-row groups 512 B apart (SBO), layout type 4.
+__device__ __forceinline__ uint64_t desc_sw64(uint32_t saddr) {
+    return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)1 << 16) | ((uint64_t)(512 >> 4) << 32) |
+           ((uint64_t)1 << 46) | ((uint64_t)4 << 61);
+}
 __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
                                          uint32_t accumulate) {
     asm volatile(
@@ -104,6 +109,18 @@ inline void make_map(CUtensorMap* map, const float* ptr, int64_t rows, int ld, i
     if (r != CUDA_SUCCESS) throw Error(DETLSH_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
 }
 
+
+// 2D fp32 map with a 64-byte swizzle: box = 16 floats (64 B) x box_rows.
+inline void make_map_sw64(CUtensorMap* map, const float* ptr, int64_t rows, int ld, int box_rows) {
+    const cuuint64_t dims[2] = {(cuuint64_t)ld, (cuuint64_t)rows};
+    const cuuint64_t strides[1] = {(cuuint64_t)ld * 4};
+    const cuuint32_t box[2] = {16u, (cuuint32_t)box_rows};
+    const cuuint32_t estr[2] = {1, 1};
+    CUresult r = encode_fn()(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(ptr), dims, strides, box, estr,
+                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw Error(DETLSH_ECUDA, "cuTensorMapEncodeTiled (sw64) failed: " + std::to_string((int)r));
+}
 
 // 2D u32 map without swizzle: box = box_cols x box_rows (box_cols * 4 a multiple of 16 B).
 inline void make_map_u32(CUtensorMap* map, const uint32_t* ptr, int64_t rows, int64_t cols, int box_cols, int box_rows) {

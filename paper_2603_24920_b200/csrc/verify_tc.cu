@@ -21,13 +21,16 @@
 // so the query tiles of one row tile run back to back and the row tile is read from HBM once):
 //   warp 0     TMA producer: per tile the new-member words NB[a][4 rt .. 4 rt + 3] and their
 //              round-buffer offsets BO (u32 boxes of 4 words x N queries); per k-block the X
-//              rows [128 x 32 fp32] and the query tile (hi = fp32, lo) [N x 32 fp32], 128B-swizzled.
+//              rows [128 x 16 fp32] and the query tile (hi = fp32, lo) [N x 16 fp32], 64B-swizzled,
+//              on separate barriers (converters start on the rows alone).
 //   warp 1     TMEM allocation + single-thread MMA issue (M = 128, N, K = 8; 3 MMAs per k-step)
 //              into a double-buffered accumulator.
 //   warps 2-3  converters: x_lo = x - trunc_tf32(x) into a twin stage (same swizzled offsets).
 //   warps 4-7  epilogue: tcgen05.ld of 16 query columns at a time for the warp's 32 rows; lane
 //              i tests bit i of the query's new-member word, writes (row id, d2) at
 //              BO + popc(word below lane i).
+#include <cstdlib>
+
 #include "index.cuh"
 #include "tc_util.cuh"
 
@@ -36,9 +39,9 @@ namespace {
 using namespace tc;
 
 constexpr int VT_M = 128;
-constexpr int VT_KB = 32;
-constexpr int VT_THREADS = 256;
-constexpr int VT_XSTAGE = VT_M * VT_KB * 4;   // 16 KB
+constexpr int VT_KB = 16;                    // fp32 per k-block (64 B rows, 64-byte swizzle)
+constexpr int VT_THREADS = 384;              // 12 warps: producer, MMA, 2 converters, 8 epilogue
+constexpr int VT_XSTAGE = VT_M * VT_KB * 4;   // 8 KB
 
 struct VtcShape {
     int64_t n;        // rows of X
@@ -49,6 +52,7 @@ struct VtcShape {
     int64_t ntiles;   // row tiles x query tiles
     int stages;
     uint32_t tmem_cols;
+    int dbg;          // experiments only (DETLSH_VTC_DEBUG): 1 = no epilogue body, 2 = no MMAs
 };
 
 __global__ void __launch_bounds__(VT_THREADS, 1)
@@ -59,20 +63,21 @@ __global__ void __launch_bounds__(VT_THREADS, 1)
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const int S = sh.stages, N = sh.N;
-    const size_t qbytes = (size_t)N * 128;
+    const size_t qbytes = (size_t)N * VT_KB * 4;
     const size_t stage_bytes = 2 * (size_t)VT_XSTAGE + 2 * qbytes;
-    // stage s: [X 16 KB][X_lo 16 KB][Q N*128 B][Q_lo N*128 B]; then 2 mask buffers [NB N*16][BO N*16]
+    // stage s: [X 8 KB][X_lo 8 KB][Q N*64 B][Q_lo N*64 B]; then 2 mask buffers [NB N*16][BO N*16]
     unsigned char* sStage = base;
     uint32_t* sMask = reinterpret_cast<uint32_t*>(base + (size_t)S * stage_bytes);
     uint64_t* bars = reinterpret_cast<uint64_t*>(sMask + 2 * 2 * 4 * N);
-    uint64_t* full = bars;               // [S] TMA -> converters, MMA
+    uint64_t* full = bars;               // [S] X rows landed -> converters
     uint64_t* conv = bars + S;           // [S] converters -> MMA
     uint64_t* empty = bars + 2 * S;      // [S] MMA commit -> producer
-    uint64_t* tfull = bars + 3 * S;      // [2] MMA commit -> epilogue
-    uint64_t* tempty = bars + 3 * S + 2; // [2] epilogue -> MMA
-    uint64_t* mfull = bars + 3 * S + 4;  // [2] masks loaded
-    uint64_t* mempty = bars + 3 * S + 6; // [2] epilogue done with masks
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * S + 8);
+    uint64_t* fullq = bars + 3 * S;      // [S] query tile landed -> MMA
+    uint64_t* tfull = bars + 4 * S;      // [2] MMA commit -> epilogue
+    uint64_t* tempty = bars + 4 * S + 2; // [2] epilogue -> MMA
+    uint64_t* mfull = bars + 4 * S + 4;  // [2] masks loaded
+    uint64_t* mempty = bars + 4 * S + 6; // [2] epilogue done with masks
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 4 * S + 8);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     auto sX = [&](int s) { return sStage + (size_t)s * stage_bytes; };
@@ -85,12 +90,13 @@ __global__ void __launch_bounds__(VT_THREADS, 1)
             mbar_init(&full[s], 1);
             mbar_init(&conv[s], 64);
             mbar_init(&empty[s], 1);
+            mbar_init(&fullq[s], 1);
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(&tfull[b], 1);
-            mbar_init(&tempty[b], 128);
+            mbar_init(&tempty[b], 256);
             mbar_init(&mfull[b], 1);
-            mbar_init(&mempty[b], 128);
+            mbar_init(&mempty[b], 256);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -108,7 +114,7 @@ __global__ void __launch_bounds__(VT_THREADS, 1)
         if (lane == 0) {
             int s = 0, mb = 0;
             uint32_t ph = 0, mph = 0;
-            const uint32_t tx = (uint32_t)(VT_XSTAGE + 2 * qbytes);
+            const uint32_t txq = (uint32_t)(2 * qbytes);
             for (int64_t tile = blockIdx.x; tile < sh.ntiles; tile += gridDim.x) {
                 const int64_t rt = tile / sh.nqt;
                 const int qt = (int)(tile - rt * sh.nqt);
@@ -120,10 +126,14 @@ __global__ void __launch_bounds__(VT_THREADS, 1)
                 if (++mb == 2) { mb = 0; mph ^= 1; }
                 for (int kb = 0; kb < sh.nkb; ++kb) {
                     mbar_wait(&empty[s], ph ^ 1);
-                    mbar_expect_tx(&full[s], tx);
-                    tma_load_2d(sX(s), &tmX, &full[s], kb * VT_KB, (int)(rt * VT_M));
-                    tma_load_2d(sQ(s), &tmQ, &full[s], kb * VT_KB, qt * N);
-                    tma_load_2d(sQl(s), &tmQlo, &full[s], kb * VT_KB, qt * N);
+                    mbar_expect_tx(&full[s], (uint32_t)VT_XSTAGE);
+                    // k-blocks start at a tile-dependent rotation: the SMs sharing a query tile
+                    // then read different parts of it (no L2 hot spot on one k-block)
+                    const int kr = (int)((kb + tile) % sh.nkb);
+                    tma_load_2d(sX(s), &tmX, &full[s], kr * VT_KB, (int)(rt * VT_M));
+                    mbar_expect_tx(&fullq[s], txq);
+                    tma_load_2d(sQ(s), &tmQ, &fullq[s], kr * VT_KB, qt * N);
+                    tma_load_2d(sQl(s), &tmQlo, &fullq[s], kr * VT_KB, qt * N);
                     if (++s == S) { s = 0; ph ^= 1; }
                 }
             }
@@ -139,18 +149,19 @@ __global__ void __launch_bounds__(VT_THREADS, 1)
                 tc_fence_after();
                 const uint32_t d_tmem = tmem_base + (uint32_t)(buf * N);
                 for (int kb = 0; kb < sh.nkb; ++kb) {
-                    mbar_wait(&full[s], ph);
+                    mbar_wait(&fullq[s], ph);
                     mbar_wait(&conv[s], ph);
                     tc_fence_after();
                     const uint32_t ax = smem_u32(sX(s)), al = smem_u32(sXl(s));
                     const uint32_t bq = smem_u32(sQ(s)), bl = smem_u32(sQl(s));
 #pragma unroll
+                    if (!(sh.dbg & 2))
                     for (int k = 0; k < VT_KB / 8; ++k) {      // K = 8 tf32 = 32 bytes per MMA
-                        const uint64_t dq = desc_sw128(bq + k * 32);
-                        const uint64_t dx = desc_sw128(ax + k * 32);
+                        const uint64_t dq = desc_sw64(bq + k * 32);
+                        const uint64_t dx = desc_sw64(ax + k * 32);
                         mma_tf32(d_tmem, dx, dq, idesc, (kb | k) ? 1u : 0u);       // x_hi q_hi
-                        mma_tf32(d_tmem, dx, desc_sw128(bl + k * 32), idesc, 1u);   // x_hi q_lo
-                        mma_tf32(d_tmem, desc_sw128(al + k * 32), dq, idesc, 1u);   // x_lo q_hi
+                        mma_tf32(d_tmem, dx, desc_sw64(bl + k * 32), idesc, 1u);    // x_hi q_lo
+                        mma_tf32(d_tmem, desc_sw64(al + k * 32), dq, idesc, 1u);    // x_lo q_hi
                     }
                     mma_commit(&empty[s]);
                     if (++s == S) { s = 0; ph ^= 1; }
@@ -168,7 +179,7 @@ __global__ void __launch_bounds__(VT_THREADS, 1)
                 mbar_wait(&full[s], ph);
                 const float4* src = reinterpret_cast<const float4*>(sX(s));
                 float4* dst = reinterpret_cast<float4*>(sXl(s));
-#pragma unroll 4
+#pragma unroll
                 for (int i = t; i < VT_XSTAGE / 16; i += 64) {
                     const float4 x = src[i];
                     float4 lo;
@@ -184,9 +195,11 @@ __global__ void __launch_bounds__(VT_THREADS, 1)
             }
         }
     } else {
-        const int ew = warp - 4;   // TMEM lane quarter = rows [32 ew, 32 ew + 32) of the tile
+        // warps 4-11: TMEM lane quarter ew = warp % 4 (rows [32 ew, 32 ew + 32) of the tile);
+        // the two warps of a quarter take alternate 16-column chunks
+        const int ew = warp & 3, eh = (warp - 4) >> 2;
         const uint32_t below = (1u << lane) - 1u;
-        float* s_qn = reinterpret_cast<float*>(tmem_slot + 4) + ew * 256;    // per warp: ||q||^2 of the tile
+        float* s_qn = reinterpret_cast<float*>(tmem_slot + 4) + (warp - 4) * 256;   // per warp: ||q||^2 of the tile
         int buf = 0, mb = 0;
         uint32_t tph = 0, mph = 0;
         int last_qt = -1;
@@ -208,7 +221,7 @@ __global__ void __launch_bounds__(VT_THREADS, 1)
             const uint32_t* NB = sMask + (size_t)mb * 8 * N;
             const uint32_t* BO = NB + 4 * N;
             const uint32_t taddr = tmem_base + (uint32_t)(buf * N) + ((uint32_t)(ew * 32) << 16);
-            for (int c0 = 0; c0 < ncols; c0 += 16) {
+            for (int c0 = 16 * eh; c0 < ((sh.dbg & 1) ? 0 : ncols); c0 += 32) {
                 uint32_t w[16];
 #pragma unroll
                 for (int i = 0; i < 16; ++i) w[i] = (c0 + i < ncols) ? NB[(c0 + i) * 4 + ew] : 0u;
@@ -218,13 +231,23 @@ __global__ void __launch_bounds__(VT_THREADS, 1)
                 if (!any) continue;   // none of these 16 queries has a new member in the warp's rows
                 float v[16];
                 tmem_ld16(taddr + c0, v);
+                // branch-free: every lane computes all 16 (slot, d2) pairs from broadcast shared
+                // loads, then stores predicated on its bit (no divergent per-column branches)
+                uint32_t bo[16];
+                float qv[16];
 #pragma unroll
                 for (int i = 0; i < 16; ++i) {
-                    if ((w[i] >> lane) & 1u) {
-                        const int c = c0 + i;
-                        const uint32_t slot = BO[c * 4 + ew] + __popc(w[i] & below);
+                    bo[i] = BO[(c0 + i) * 4 + ew];
+                    qv[i] = s_qn[c0 + i];
+                }
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                    const bool hit = (w[i] >> lane) & 1u;
+                    const uint32_t slot = bo[i] + __popc(w[i] & below);
+                    const float dd = fmaxf(0.f, fmaf(-2.f, v[i], xr + qv[i]));
+                    if (hit) {
                         cand[slot] = (uint32_t)row;
-                        d2[slot] = fmaxf(0.f, fmaf(-2.f, v[i], xr + s_qn[c]));
+                        d2[slot] = dd;
                     }
                 }
             }
@@ -260,19 +283,21 @@ bool verify_tc(const float* d_X, int64_t n, int ld, const float* d_Qa, const flo
     sh.nqt = (int)ceil_div(na, sh.N);
     const int64_t nrt = ceil_div(n, VT_M);
     sh.ntiles = nrt * sh.nqt;
-    const size_t stage_bytes = 2 * (size_t)VT_XSTAGE + 2 * (size_t)sh.N * 128;
-    const size_t fixed = 1024 + 2 * 2 * 16 * (size_t)sh.N + 256 + 4 * 256 * 4;
+    const size_t stage_bytes = 2 * (size_t)VT_XSTAGE + 2 * (size_t)sh.N * VT_KB * 4;
+    const size_t fixed = 1024 + 2 * 2 * 16 * (size_t)sh.N + 512 + 8 * 256 * 4;
     const size_t budget = 227 * 1024;
     if (fixed + 2 * stage_bytes > budget) return false;
-    sh.stages = (int)std::min<size_t>(4, (budget - fixed) / stage_bytes);
+    sh.stages = (int)std::min<size_t>(8, (budget - fixed) / stage_bytes);
     uint32_t cols = 32;
     while (cols < (uint32_t)(2 * sh.N)) cols <<= 1;
     sh.tmem_cols = cols;
+    static const int dbg = std::getenv("DETLSH_VTC_DEBUG") ? std::atoi(std::getenv("DETLSH_VTC_DEBUG")) : 0;
+    sh.dbg = dbg;
     const size_t smem = fixed + (size_t)sh.stages * stage_bytes;
     CUtensorMap mx, mq, mql, mnb, mbo;
-    make_map(&mx, d_X, n, ld, VT_M);
-    make_map(&mq, d_Qa, na, ld, sh.N);
-    make_map(&mql, d_Qalo, na, ld, sh.N);
+    make_map_sw64(&mx, d_X, n, ld, VT_M);
+    make_map_sw64(&mq, d_Qa, na, ld, sh.N);
+    make_map_sw64(&mql, d_Qalo, na, ld, sh.N);
     make_map_u32(&mnb, d_NB, na, nw4, 4, sh.N);
     make_map_u32(&mbo, d_BO, na, nw4, 4, sh.N);
     static size_t configured = 0;

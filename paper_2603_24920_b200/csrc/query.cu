@@ -104,6 +104,7 @@ __global__ void k_build_qlut(const float* __restrict__ lut, const int* __restric
 //      screen never changes a result.
 constexpr int RF_THREADS = 256;
 constexpr int RF_G = 16;         // queries per CTA (8-bit terms); 8 selects 12-bit terms
+constexpr int RF_BQ = 64;        // band queue per warp: < 32 left over + one step of <= 32
 
 template <int G> struct QuantSpec;
 template <> struct QuantSpec<8> { static constexpr uint32_t QT = 2048, CAP = 4095; };
@@ -146,7 +147,9 @@ __global__ void __launch_bounds__(RF_THREADS, 3) k_range_filter(RFArgs a) {
     __shared__ uint8_t s_sx[G][32];
     __shared__ unsigned int s_ctr[G][4];
     __shared__ uint32_t s_lq[RF_THREADS / 32][kTileLeaves];                             // per warp: leaf masks
+    __shared__ uint32_t s_bq[RF_THREADS / 32][RF_BQ];                                   // per warp: band queue
     __shared__ int s_active_mask;
+    __shared__ unsigned int s_next;
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = RF_THREADS / 32;
     if (threadIdx.x < G) {
@@ -196,9 +199,21 @@ __global__ void __launch_bounds__(RF_THREADS, 3) k_range_filter(RFArgs a) {
     const uint8_t* s_b = reinterpret_cast<const uint8_t*>(s_qe);
     uint32_t c_lt = 0, c_lp = 0, c_pt = 0, c_pp = 0;
     uint32_t* lq = s_lq[warp];
+    uint32_t* bq = s_bq[warp];
+    uint32_t qn_ = 0;                     // queued band pairs (warp-uniform)
 
-    for (int64_t tile = a.tile_begin + (int64_t)blockIdx.y * nwarps + warp; tile < a.tile_end;
-         tile += (int64_t)gridDim.y * nwarps) {
+    // this CTA's contiguous stripe of tiles; its warps take tiles one at a time (dynamic, so a
+    // warp with heavy tiles does not hold the CTA back)
+    const int64_t ntl = a.tile_end - a.tile_begin;
+    const int64_t tb = a.tile_begin + ntl * blockIdx.y / gridDim.y;
+    const int64_t te = a.tile_begin + ntl * (blockIdx.y + 1) / gridDim.y;
+    if (threadIdx.x == 0) s_next = 0;
+    __syncthreads();
+    for (;;) {
+        int64_t tile = 0;
+        if (lane == 0) tile = tb + atomicAdd(&s_next, 1);
+        tile = __shfl_sync(0xffffffffu, tile, 0);
+        if (tile >= te) break;
         const uint32_t lb = a.tile_leaf[tile], le = a.tile_leaf[tile + 1];
         const int nlt = (int)(le - lb);
         const uint32_t P0 = a.leaf_off[lb], P1 = a.leaf_off[le];
@@ -208,8 +223,23 @@ __global__ void __launch_bounds__(RF_THREADS, 3) k_range_filter(RFArgs a) {
             uint32_t lacc[G];
 #pragma unroll
             for (int g = 0; g < G; ++g) lacc[g] = 0;
+            uint4 lo4 = make_uint4(0, 0, 0, 0), hi4 = lo4;
+            if (KT == 16) {
+                lo4 = *reinterpret_cast<const uint4*>(a.lo + l * 16);
+                hi4 = *reinterpret_cast<const uint4*>(a.hi + l * 16);
+            }
+#pragma unroll
             for (int j = 0; j < K; ++j) {
-                const int lo_ = a.lo[l * K + j], hi_ = a.hi[l * K + j];
+                int lo_, hi_;
+                if (KT == 16) {
+                    const uint32_t wl = (j >> 2) == 0 ? lo4.x : (j >> 2) == 1 ? lo4.y : (j >> 2) == 2 ? lo4.z : lo4.w;
+                    const uint32_t wh = (j >> 2) == 0 ? hi4.x : (j >> 2) == 1 ? hi4.y : (j >> 2) == 2 ? hi4.z : hi4.w;
+                    lo_ = (int)((wl >> (8 * (j & 3))) & 255u);
+                    hi_ = (int)((wh >> (8 * (j & 3))) & 255u);
+                } else {
+                    lo_ = a.lo[l * K + j];
+                    hi_ = a.hi[l * K + j];
+                }
 #pragma unroll
                 for (int g = 0; g < G; ++g) {
                     const int e = (j * N_r + min(max((int)s_sx[g][j], lo_), hi_)) * 16;
@@ -239,19 +269,60 @@ __global__ void __launch_bounds__(RF_THREADS, 3) k_range_filter(RFArgs a) {
             c_lp += __popc(m);
         }
         __syncwarp();
+        // exact fp32 cell bound (summed in j order, AMB-12/29) of queued band pairs: one pair
+        // per lane, all lanes busy (instead of a divergent per-lane loop over band queries)
+        auto flush = [&](int cnt) {
+            if (lane < cnt) {
+                const uint32_t e = bq[qn_ - cnt + lane];
+                const int g = (int)(e & 15u);
+                const int64_t pos = (int64_t)(P0 + (e >> 4)) - a.pos_base;
+                const float* D = a.lut + (int64_t)s_q[g] * per_q + (int64_t)a.t * K * N_r;
+                float s_ = 0.f;
+                if (KT == 16) {
+                    const uint4 c4 = *reinterpret_cast<const uint4*>(a.tcodes + pos * 16);
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) {
+                        const uint32_t word = (j >> 2) == 0 ? c4.x : (j >> 2) == 1 ? c4.y : (j >> 2) == 2 ? c4.z : c4.w;
+                        s_ += __ldg(D + j * N_r + ((word >> (8 * (j & 3))) & 255u));
+                    }
+                } else {
+                    for (int j = 0; j < K; ++j) s_ += __ldg(D + j * N_r + a.tcodes[pos * K + j]);
+                }
+                if (s_ <= rho2) {
+                    ++c_pp;
+                    const uint32_t id = a.perm[pos];
+                    atomicOr(a.bitmap + (int64_t)s_q[g] * a.nwords + (id >> 5), 1u << (id & 31));  // RED.OR
+                }
+            }
+            qn_ -= cnt;
+        };
+        // software pipeline: the next chunk's leaf slots, codes and ids load while this one is screened
+        uint32_t nx_ptl = 0, nx_id = 0;
+        uint4 nx_c4 = make_uint4(0, 0, 0, 0);
+        auto load_chunk = [&](uint32_t pb_) {
+            const uint32_t p_ = pb_ + lane;
+            if (p_ < P1) {
+                const int64_t pos_ = (int64_t)p_ - a.pos_base;
+                nx_ptl = a.ptl[pos_];
+                nx_id = a.perm[pos_];
+                if (KT == 16) nx_c4 = *reinterpret_cast<const uint4*>(a.tcodes + pos_ * 16);
+            }
+        };
+        load_chunk(P0);
         for (uint32_t pb = P0; pb < P1; pb += 32) {
             const uint32_t p = pb + lane;
             const int64_t pos = (int64_t)p - a.pos_base;
+            const uint32_t cur_ptl = nx_ptl, cur_id = nx_id;
+            const uint4 c4 = nx_c4;
+            if (pb + 32 < P1) load_chunk(pb + 32);
             uint32_t m = 0;
-            if (p < P1) m = lq[a.ptl[pos]];
+            if (p < P1) m = lq[cur_ptl];
             if (__ballot_sync(0xffffffffu, m != 0) == 0) continue;    // whole warp pruned by leaf LBs
             c_pt += __popc(m);
-            uint4 c4 = make_uint4(0, 0, 0, 0);
-            uint32_t pass = m, certain = 0;
+            uint32_t certain = m, band = 0;
             if (m && a.mode == DETLSH_MODE_CELL) {
                 uint32_t ok = 0, sure = 0;
                 if (KT == 16) {
-                    c4 = *reinterpret_cast<const uint4*>(a.tcodes + pos * 16);
                     uint32_t acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 #pragma unroll
                     for (int w = 0; w < 4; ++w) {
@@ -271,12 +342,12 @@ __global__ void __launch_bounds__(RF_THREADS, 3) k_range_filter(RFArgs a) {
                             const uint4 vb = row[1 * N_r + ((word >> 8) & 255u)];
                             const uint4 vc = row[2 * N_r + ((word >> 16) & 255u)];
                             const uint4 vd = row[3 * N_r + (word >> 24)];
-                            const uint32_t p[4] = {va.x + vb.x, va.y + vb.y, va.z + vb.z, va.w + vb.w};
-                            const uint32_t r[4] = {vc.x + vd.x, vc.y + vd.y, vc.z + vd.z, vc.w + vd.w};
+                            const uint32_t p2[4] = {va.x + vb.x, va.y + vb.y, va.z + vb.z, va.w + vb.w};
+                            const uint32_t r2[4] = {vc.x + vd.x, vc.y + vd.y, vc.z + vd.z, vc.w + vd.w};
 #pragma unroll
                             for (int i = 0; i < 4; ++i) {
-                                acc[2 * i] += (p[i] & 0x00FF00FFu) + (r[i] & 0x00FF00FFu);
-                                acc[2 * i + 1] += __byte_perm(p[i], 0u, 0x4341) + __byte_perm(r[i], 0u, 0x4341);
+                                acc[2 * i] += (p2[i] & 0x00FF00FFu) + (r2[i] & 0x00FF00FFu);
+                                acc[2 * i + 1] += __byte_perm(p2[i], 0u, 0x4341) + __byte_perm(r2[i], 0u, 0x4341);
                             }
                         }
                     }
@@ -302,39 +373,36 @@ __global__ void __launch_bounds__(RF_THREADS, 3) k_range_filter(RFArgs a) {
                         sure |= (acc[g] + 17 <= QT ? 1u : 0u) << g;
                     }
                 }
-                pass = m & ok;
                 certain = m & sure;
-                // exact fp32 decision inside the quantisation band (cell LB summed in j order)
-                uint32_t conf = certain;
-                pass &= ~certain;
-                while (pass) {
-                    const int g = __ffs(pass) - 1;
-                    pass &= pass - 1;
-                    const float* D = a.lut + (int64_t)s_q[g] * per_q + (int64_t)a.t * K * N_r;
-                    float s_ = 0.f;
-                    if (KT == 16) {
-#pragma unroll
-                        for (int j = 0; j < 16; ++j) {
-                            const uint32_t word = (j >> 2) == 0 ? c4.x : (j >> 2) == 1 ? c4.y : (j >> 2) == 2 ? c4.z : c4.w;
-                            s_ += __ldg(D + j * N_r + ((word >> (8 * (j & 3))) & 255u));
-                        }
-                    } else {
-                        for (int j = 0; j < K; ++j) s_ += __ldg(D + j * N_r + a.tcodes[pos * K + j]);
-                    }
-                    if (s_ <= rho2) conf |= 1u << g;
-                }
-                pass = conf;
+                band = m & ok & ~sure;
             }
-            if (pass) {
-                c_pp += __popc(pass);
-                const uint32_t id = a.perm[pos];
-                while (pass) {
-                    const int g = __ffs(pass) - 1;
-                    pass &= pass - 1;
+            if (certain) {
+                c_pp += __popc(certain);
+                const uint32_t id = cur_id;
+                uint32_t c_ = certain;
+                while (c_) {
+                    const int g = __ffs(c_) - 1;
+                    c_ &= c_ - 1;
                     atomicOr(a.bitmap + (int64_t)s_q[g] * a.nwords + (id >> 5), 1u << (id & 31));  // RED.OR
                 }
             }
+            // queue the band pairs (point in tile << 4 | query slot) for the warp-wide fp32 pass:
+            // one pair per lane per step, flushed 32 at a time
+            while (__any_sync(0xffffffffu, band != 0)) {
+                const bool has = band != 0;
+                const uint32_t bal = __ballot_sync(0xffffffffu, has);
+                if (has) {
+                    const int g = __ffs(band) - 1;
+                    band &= band - 1;
+                    bq[qn_ + __popc(bal & lanemask_lt())] = ((p - P0) << 4) | (uint32_t)g;
+                }
+                qn_ += __popc(bal);
+                __syncwarp();
+                if (qn_ >= 32) flush(32);
+                __syncwarp();
+            }
         }
+        if (qn_) flush(qn_);
         __syncwarp();
     }
     // ---- counters (per group; attributed evenly to its active queries)
@@ -1226,8 +1294,9 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
                 ra.t = t;
                 const int groups = (int)ceil_div(na, RF_G);
                 const int64_t ntiles = ra.tile_end - ra.tile_begin;
+                // about 4 waves of 3 resident CTAs per SM in all (tail <= a quarter wave)
                 const int stripes = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(ntiles, RF_THREADS / 32),
-                                                                                 ceil_div(148 * 6, groups)));
+                                                                                 (148 * 3 * 4 + groups / 2) / groups));
                 DL_LAUNCH(k_range_filter_sel, dim3((unsigned)groups, (unsigned)stripes), RF_THREADS, rf_smem, st, ra);
                 DL_LAUNCH(k_count_new, dim3((unsigned)na, (unsigned)ceil_div(nwords, CN_WORDS)), 256, 0, st, cur,
                           s_qs.as<QState>(), s_bm.as<uint32_t>(), bm_prev, nwords);

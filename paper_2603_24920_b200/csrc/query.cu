@@ -1185,12 +1185,15 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
     Scratch s_total(st, sizeof(unsigned long long));
     Scratch s_tk(st, sizeof(unsigned long long) * (size_t)(qb * k));
     Scratch s_qs(st, sizeof(QState) * (size_t)qb);
-    Scratch s_act(st, sizeof(int) * (size_t)(2 * qb + 2));
+    Scratch s_act(st, sizeof(int) * (size_t)(4 * qb + 4));
     Scratch s_ch(st, sizeof(uint32_t) * (size_t)(qb + 2));
     Scratch s_radii(st, sizeof(double) * 64);
     int* act = s_act.as<int>();
     int* act2 = act + qb;
     int* n_act = act2 + qb;
+    int* fbuf0 = n_act + 2;          // per-tree compacted active lists (filter only)
+    int* fbuf1 = fbuf0 + qb;
+    int* n_f = fbuf1 + qb;
 
     const double eps = ix.eps;
     std::vector<double> radii(64);
@@ -1281,27 +1284,38 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
                 DL_LAUNCH(k_build_qlut, (unsigned)std::min<int64_t>(ceil_div(na * per_q, 256), 148 * 32), 256, 0, st,
                           s_lut.as<float>(), cur, na, per_q, inv_rd, (float)QuantSpec<RF_G>::CAP, s_qlut.as<uint16_t>());
             }
-            for (int t = 0; t < ix.L; ++t) {
+            // queries that stop on the budget after tree t (Alg. 5 line 7) leave the filter: the
+            // trees after it run over the compacted list of still-active queries (fewer groups)
+            int* fa = cur;
+            int nf = na;
+            for (int t = 0; t < ix.L && nf > 0; ++t) {
                 ra.tcodes = ix.tcodes.as<uint8_t>() + (int64_t)t * n * ix.K;
                 ra.perm = ix.perm.as<uint32_t>() + (int64_t)t * n;
                 ra.ptl = ix.point_tile_leaf.as<uint16_t>() + (int64_t)t * n;
                 ra.pos_base = (int64_t)t * n;
                 ra.tile_begin = ix.tree_tile_begin[t];
                 ra.tile_end = ix.tree_tile_begin[t + 1];
-                ra.act = cur;
-                ra.na = na;
+                ra.act = fa;
+                ra.na = nf;
                 ra.rho2 = rho2;
                 ra.t = t;
-                const int groups = (int)ceil_div(na, RF_G);
+                const int groups = (int)ceil_div(nf, RF_G);
                 const int64_t ntiles = ra.tile_end - ra.tile_begin;
                 // about 4 waves of 3 resident CTAs per SM in all (tail <= a quarter wave)
                 const int stripes = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(ntiles, RF_THREADS / 32),
                                                                                  (148 * 3 * 4 + groups / 2) / groups));
                 DL_LAUNCH(k_range_filter_sel, dim3((unsigned)groups, (unsigned)stripes), RF_THREADS, rf_smem, st, ra);
-                DL_LAUNCH(k_count_new, dim3((unsigned)na, (unsigned)ceil_div(nwords, CN_WORDS)), 256, 0, st, cur,
+                DL_LAUNCH(k_count_new, dim3((unsigned)nf, (unsigned)ceil_div(nwords, CN_WORDS)), 256, 0, st, fa,
                           s_qs.as<QState>(), s_bm.as<uint32_t>(), bm_prev, nwords);
-                DL_LAUNCH(k_tree_end, (unsigned)ceil_div(na, 256), 256, 0, st, cur, na, s_qs.as<QState>(), t, m,
+                DL_LAUNCH(k_tree_end, (unsigned)ceil_div(nf, 256), 256, 0, st, fa, nf, s_qs.as<QState>(), t, m,
                           budget, cap);
+                if (t + 1 < ix.L) {
+                    int* fa2 = (fa == fbuf0) ? fbuf1 : fbuf0;
+                    DL_LAUNCH(k_compact, 1, 1024, 0, st, fa, nf, s_qs.as<QState>(), fa2, n_f);
+                    DL_CUDA(cudaMemcpyAsync(&nf, n_f, sizeof(int), cudaMemcpyDeviceToHost, st));
+                    DL_CUDA(cudaStreamSynchronize(st));
+                    fa = fa2;
+                }
             }
             tr.mark("filter (L trees)", st);
             DL_LAUNCH(k_round_offsets, 1, 1024, 0, st, cur, na, s_qs.as<QState>(), s_total.as<unsigned long long>());

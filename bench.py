@@ -135,15 +135,31 @@ def kernel_models(c, steps: int, st, n_local: int, nq: int, ld: int):
                            "unit": "per query: leaves_tested*2K + leaves_passed*8 + points_tested*K + "
                                    "points_passed*12 + new*4 B (SURVEY 8(d) K5/K6)"},
         "k_verify_rows": {"bytes": steps * ncand * (4 * d + 8), "unit": "per candidate 4d+8 B (row + id + d2)"},
+        # tensor-core verification: per round a masked X.Q^T over all n rows x the round's active
+        # queries; 3 tf32 MMAs (x.q, x.q_lo, x_lo.q) per product; active query-rounds = sum of rounds
+        "k_verify_tc": {"bytes": steps * ncand * (4 * d + 8),
+                        "flops": steps * 3.0 * 2.0 * n_local * ld * float(st["rounds"].sum()),
+                        "tensor_only": True,
+                        "unit": "per candidate 4d+8 B (the gather it replaces); tensor work 3 x 2 n ld per active "
+                                "query-round (3xTF32)"},
         "k_project_tc": {"bytes": steps * proj_bytes, "flops": steps * proj_flops,
                          "unit": "per row 4*ld B read + codes (LK B) or projections (4LK B) written"},
     }
 
 
-def roofline_entry(name, model, ms, hbm, bf16, clocks):
+def roofline_entry(name, model, ms, hbm, bf16, clocks, launches=1, traffic=None):
     ach = model["bytes"] / (ms / 1e3) / 1e9
+    tr = traffic.get(name) if traffic else None
     e = {"kernel": name, "bound": "hbm", "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s",
-         "frac": round(ach / hbm, 4), "traffic": None, "ms": round(ms, 4), "unit_of_work": model["unit"]}
+         "frac": round(ach / hbm, 4), "traffic": tr, "algorithmic_bytes_per_launch": round(model["bytes"] / launches),
+         "ms": round(ms, 4), "ms_per_launch": round(ms / launches, 4), "unit_of_work": model["unit"]}
+    if model.get("tensor_only"):
+        tf = model["flops"] / (ms / 1e3) / 1e12
+        pk = round(bf16 / 2, 1)
+        e.update({"bound": "tensor", "achieved": round(tf, 1), "peak": pk, "unit": "TFLOP/s", "frac": round(tf / pk, 4),
+                  "peak_note": "measured bf16 / 2 (TF32 nominal ratio); executed 3xTF32 MMA flops",
+                  "gather_equivalent_GBps": round(ach, 1)})
+        return e
     if "smem_bytes" in model:
         sm = (clocks.get("sm_mhz") or 1965.0) * 1e6
         smem_peak = 148 * 128 * sm / 1e9
@@ -156,6 +172,16 @@ def roofline_entry(name, model, ms, hbm, bf16, clocks):
         e["tensor"] = {"achieved": round(tf, 1), "peak": round(bf16 / 2, 1), "unit": "TFLOP/s",
                        "peak_note": "measured bf16 / 2 (TF32 nominal ratio), 2 MMAs (x_hi, x_lo) per k-step"}
     return e
+
+
+def load_traffic():
+    """DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum) of each modelled
+    kernel, from this round's `ncu --set full` capture (profiles/traffic.json; written by
+    tools/ncu_summary.py from the committed .csv exports)."""
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    if not os.path.exists(path):
+        return None
+    return {k: v["dram_bytes_per_launch"] for k, v in json.load(open(path)).get("kernels", {}).items()}
 
 
 def datagen_ns(c, n):
@@ -335,10 +361,11 @@ def main():
         dom = max(prof.items(), key=lambda kv: kv[1][1])[0] if prof else None
         models = kernel_models(cfg, args.steps, st, n_local, cfg.nq, (cfg.d + 7) // 8 * 8)
         roofs = []
+        traffic = load_traffic()
         for kname, (nl_, ms) in sorted(prof.items(), key=lambda kv: -kv[1][1]):
             for prefix, model in models.items():
                 if kname.startswith(prefix):
-                    roofs.append(roofline_entry(kname, model, ms, hbm, bf16, clocks))
+                    roofs.append(roofline_entry(kname, model, ms, hbm, bf16, clocks, nl_, traffic))
         roof = next((r for r in roofs if r["kernel"] == dom), None)
         if roof is not None:
             roof["share_of_step"] = round(prof[dom][1] / step_ms, 4)

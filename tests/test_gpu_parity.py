@@ -239,23 +239,35 @@ def test_errors_on_gpu(gpu_tiny, tiny):
     assert ig.shape == (0, 5)
 
 
+def _bench_rmin(cid):
+    import json
+    import os
+    path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "bench_configs.json")
+    return json.load(open(path))[str(cid)]["r_min"]
+
+
 @pytest.mark.slow
-def test_config2_full_size_sampled_queries():
-    """configs[1] at full size (n = 1M, d = 256) in the bench launch configuration, checked
-    on 24 sampled queries the oracle answers one by one."""
-    D = datagen.generate(2, with_sample_queries=20)
+@pytest.mark.parametrize("cid,nsel", [(2, 24), (3, 12), (4, 8)])
+def test_full_size_sampled_queries(cid, nsel):
+    """BASELINE configs at full size (configs[1]: 1M x 256 -- the bench configuration; configs[2]:
+    1M x 960; configs[3]: 10M x 128 integer-valued), all queries answered in one call as bench.py
+    runs them, checked on sampled queries the oracle answers one by one (same r_min, written by
+    tools/make_rmin.py from the oracle)."""
+    D = datagen.generate(cid)
     c = D["cfg"]
-    o = O.Index(D["X"], c.L, c.K, c.N_r, c.index_seed)
-    rmin = o.estimate_rmin(D["Qs"], c.k, c.c, c.beta)
+    rmin = _bench_rmin(cid)
     g = P.detlsh_build(D["X"], c.L, c.K, c.N_r, c.index_seed)
-    Cg, Co = g.codes(), o.codes()
-    print(f"cfg2 code mismatch fraction {np.mean(Cg != Co):.2e}")
-    assert np.mean(Cg != Co) <= 1e-4
-    sel = np.random.default_rng(5).choice(c.nq, 24, replace=False)
-    ig, dg = g.query(D["Q"], c.k, c.c, rmin, c.beta)       # full batch, as bench.py runs it
+    ig, dg = g.query(D["Q"], c.k, c.c, rmin, c.beta)
+    Cg = g.codes()
+    del g
+    o = O.Index(D["X"], c.L, c.K, c.N_r, c.index_seed)
+    mism = np.mean(Cg != o.codes())
+    print(f"cfg{cid} code mismatch fraction {mism:.2e}")
+    assert mism <= 1e-4
+    sel = np.random.default_rng(5).choice(c.nq, nsel, replace=False)
     io, do, _ = o.query(D["Q"][sel], c.k, c.c, rmin, c.beta)
     rec = _recall(ig[sel], io)
-    print(f"cfg2 recall vs oracle on 24 sampled queries: {rec:.4f}")
+    print(f"cfg{cid} recall vs oracle on {nsel} sampled queries: {rec:.4f}")
     assert rec >= 0.99
     _dist_match(ig[sel], dg[sel], io, do)
 
@@ -304,3 +316,32 @@ def test_verify_tc_vs_simt_and_oracle(n, d, nq, k):
     assert _recall(it[sel], io) >= 0.99
     _dist_match(it[sel], dt[sel], io, do)
     assert st["rounds"].max() >= 2
+
+
+@pytest.mark.parametrize("G", [2, 3])
+def test_logical_shards_on_one_gpu(tiny, G):
+    """SURVEY 8(e) parity: G point shards built on one GPU through the same calls the multi-GPU
+    glue makes (C1: per-shard sample projections -> global breakpoints; per-shard build with
+    global ids; C2: local top-k merged by (dist, id)) against the oracle's own G-shard run (O9)."""
+    c = tiny["cfg"]
+    X, Q = tiny["X"], tiny["Q"][:40]
+    n = X.shape[0]
+    whole = P.detlsh_build(X, c.L, c.K, c.N_r, c.index_seed)
+    rngs = [((g * n) // G, ((g + 1) * n) // G) for g in range(G)]
+    Ps = [P.detlsh_sample_projections(X[lo:hi], c.L, c.K, c.N_r, c.index_seed, 0.01, lo, n) for lo, hi in rngs]
+    B = P.detlsh_breakpoints_from_samples(np.concatenate(Ps), c.N_r)
+    assert np.array_equal(B, whole.breakpoints())           # C1: identical to the 1-GPU breakpoints
+    rmin = 300.0
+    ids, ds = [], []
+    for g, (lo, hi) in enumerate(rngs):
+        sh = P.detlsh_build(np.ascontiguousarray(X[lo:hi]), c.L, c.K, c.N_r, c.index_seed, id_offset=lo,
+                            n_global=n, breakpoints=B)
+        assert np.array_equal(sh.codes(), whole.codes()[lo:hi])
+        i, d = sh.query(Q, c.k, c.c, rmin, c.beta)
+        assert np.all((i == -1) | ((i >= lo) & (i < hi)))
+        ids.append(i)
+        ds.append(d)
+    mi, md = P.detlsh_merge_topk(np.stack(ids), np.stack(ds), c.k)
+    ri, rd = O.sharded_query(X, G, Q, c.k, c.c, rmin, c.beta, c.L, c.K, c.N_r, c.index_seed)
+    assert _recall(mi, ri) >= 0.99
+    _dist_match(mi, md, ri, rd)

@@ -649,26 +649,29 @@ __global__ void __launch_bounds__(VR_THREADS) k_verify_rows(VRArgs a) {
 //                  q - trunc_tf32(q), and ||q||^2.
 __global__ void __launch_bounds__(1024) k_verify_prep(const int* __restrict__ act, const QState* __restrict__ qs,
                                                       const uint32_t* __restrict__ cur, uint32_t* __restrict__ ver,
-                                                      int64_t nwords, int64_t nw4, uint32_t* __restrict__ NB,
+                                                      int64_t nwords, uint32_t* __restrict__ NB,
                                                       uint32_t* __restrict__ BO) {
+    // nwords is a multiple of 4 (padded bitmap rows): each thread owns 4 consecutive words
     __shared__ uint32_t s_w[32];
     const int a = blockIdx.x;
     const int q = act[a];
-    const uint32_t* c = cur + (int64_t)q * nwords;
-    uint32_t* v = ver + (int64_t)q * nwords;
-    uint32_t* nb_out = NB + (int64_t)a * nw4;
-    uint32_t* bo_out = BO + (int64_t)a * nw4;
+    const uint4* c = reinterpret_cast<const uint4*>(cur + (int64_t)q * nwords);
+    uint4* v = reinterpret_cast<uint4*>(ver + (int64_t)q * nwords);
+    uint4* nb_out = reinterpret_cast<uint4*>(NB + (int64_t)a * nwords);
+    uint4* bo_out = reinterpret_cast<uint4*>(BO + (int64_t)a * nwords);
+    const int64_t n4 = nwords / 4;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     uint32_t carry = (uint32_t)qs[q].roff;
-    for (int64_t b0 = 0; b0 < nw4; b0 += 1024) {
+    for (int64_t b0 = 0; b0 < n4; b0 += 1024) {
         const int64_t b = b0 + threadIdx.x;
-        uint32_t nb = 0;
-        if (b < nwords) {
-            const uint32_t cv = c[b];
-            nb = cv & ~v[b];
-            if (nb) v[b] = cv;
+        uint4 nb = make_uint4(0, 0, 0, 0);
+        if (b < n4) {
+            const uint4 cv = c[b], vv = v[b];
+            nb = make_uint4(cv.x & ~vv.x, cv.y & ~vv.y, cv.z & ~vv.z, cv.w & ~vv.w);
+            if (nb.x | nb.y | nb.z | nb.w) v[b] = cv;
         }
-        const uint32_t cnt = __popc(nb);
+        const uint32_t c0 = __popc(nb.x), c1 = __popc(nb.y), c2 = __popc(nb.z), c3 = __popc(nb.w);
+        const uint32_t cnt = c0 + c1 + c2 + c3;
         uint32_t x = cnt;
         for (int o = 1; o < 32; o <<= 1) {
             const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
@@ -685,10 +688,10 @@ __global__ void __launch_bounds__(1024) k_verify_prep(const int* __restrict__ ac
             s_w[lane] = t;
         }
         __syncthreads();
-        const uint32_t incl = x + (w ? s_w[w - 1] : 0);
-        if (b < nw4) {
+        const uint32_t ex = carry + x + (w ? s_w[w - 1] : 0) - cnt;
+        if (b < n4) {
             nb_out[b] = nb;
-            bo_out[b] = carry + incl - cnt;
+            bo_out[b] = make_uint4(ex, ex + c0, ex + c0 + c1, ex + c0 + c1 + c2);
         }
         carry += s_w[31];
         __syncthreads();
@@ -1146,7 +1149,7 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
     const int64_t n = ix.n, nq = a.nq, LK = ix.LK;
     const int k = a.k;
     const int64_t budget = (int64_t)std::ceil(a.beta * (double)n) + k;   // AMB-17
-    const int64_t nwords = ceil_div(n, 32);
+    const int64_t nwords = round_up(ceil_div(n, 32), 4);   // bitmap words per query (rows padded to 16 B)
     const int64_t cap = n;                                              // |S| <= n always
 
     Trace tr("query");
@@ -1342,7 +1345,7 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
                 float* Qalo = Qa + (int64_t)qb * ix.ld;
                 float* qn = Qalo + (int64_t)qb * ix.ld;
                 DL_LAUNCH(k_verify_prep, (unsigned)na, 1024, 0, st, cur, s_qs.as<QState>(), s_bm.as<uint32_t>(),
-                          s_ver.as<uint32_t>(), nwords, nw4, NB, BO);
+                          s_ver.as<uint32_t>(), nwords, NB, BO);
                 DL_LAUNCH(k_prep_queries, (unsigned)ceil_div(na, 8), 256, 0, st, Qb, (int64_t)ix.ld, cur, na, Qa, Qalo, qn);
                 done_tc = verify_tc(ix.Xp, n, ix.ld, Qa, Qalo, qn, na, NB, BO, nw4, ix.xnorm.as<float>(), va.cand, va.d2,
                                     st);

@@ -124,6 +124,20 @@ detlsh_status detlsh_query_ex(const detlsh_index* idx, const float* queries, int
                               int64_t* out_ids, float* out_dists, detlsh_query_stats* stats);
 
 /*
+ * (r,c)-ANN for queries[nq][d] (Alg. 4): one pass over the L trees at radius
+ * eps*r; as soon as |S| >= ceil(beta n) + 1 the point of S closest to q is returned
+ * (line 6); after the L trees the closest point of S is returned if it lies within c r
+ * (lines 8-9), else nothing (line 10).  Outputs out_ids[nq] (global id, or -1 for
+ * nothing) and out_dists[nq] (Euclidean fp32, +inf for nothing); stats as for
+ * detlsh_query_ex (reason 0 = budget, 1 = within c r, 2 = nothing).  opts: mode,
+ * query_batch, stream, verify_impl as for queries.  Errors (EINVAL): as detlsh_query with
+ * k = 1, r_min = r.
+ */
+detlsh_status detlsh_rc_ann(const detlsh_index* idx, const float* queries, int64_t nq, double r,
+                            double c, double beta, const detlsh_opts* opts, int64_t* out_ids,
+                            float* out_dists, detlsh_query_stats* stats);
+
+/*
  * "Magic" initial radius (AMB-22): for each of ns sample queries [ns][d] (host or
  * device), r*_q = the smallest radius whose full round (all L range queries) gives
  * |S| >= min(n, ceil(beta n) + k) -- i.e. sqrt of the B-th smallest over points of

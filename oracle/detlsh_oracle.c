@@ -812,6 +812,49 @@ void orc_query(const orc_index* ix, const float* Q, int64_t nq, int k, double c,
 }
 
 /* ======================================================================== */
+/* O8b. (r,c)-ANN, Alg. 4: one pass over the L trees at radius    */
+/* eps r; return the point of S closest to q (ties by id) as soon as          */
+/* |S| >= beta n + 1 (line 6; ceil(beta n) + 1 in double, as AMB-17), else    */
+/* after the L trees the closest point if it lies within c r (lines 8-9),     */
+/* else nothing (line 10): (-1, +inf).                                        */
+/* ======================================================================== */
+void orc_rc_ann(const orc_index* ix, const float* Q, int64_t nq, double c, double r, double beta, int mode,
+                int64_t* out_ids, float* out_dists) {
+    int64_t n = ix->n;
+    int64_t budget = (int64_t)ceil(beta * (double)n) + 1;
+    uint8_t* inS = (uint8_t*)xmalloc((size_t)n);
+    int64_t* S = (int64_t*)xmalloc(sizeof(int64_t) * (size_t)n);
+    int64_t* buf = (int64_t*)xmalloc(sizeof(int64_t) * (size_t)n);
+    float* qp = (float*)xmalloc(sizeof(float) * (size_t)ix->LK);
+    for (int64_t qi = 0; qi < nq; ++qi) {
+        const float* q = Q + (size_t)qi * ix->d;
+        memset(inS, 0, (size_t)n);
+        int64_t nS = 0;                                        /* line 1 */
+        int by_budget = 0;
+        orc_project_query(ix, q, qp);                          /* line 3 (all i at once) */
+        for (int i = 0; i < ix->L; ++i) {                      /* line 2 */
+            int64_t cnt = orc_range_query(ix, i, qp + (size_t)i * ix->K, ix->eps * r, mode, buf); /* line 4 */
+            for (int64_t e = 0; e < cnt; ++e)                  /* line 5 */
+                if (!inS[buf[e]]) { inS[buf[e]] = 1; S[nS++] = buf[e]; }
+            if (nS >= budget) { by_budget = 1; break; }        /* line 6 */
+        }
+        candd best = {INFINITY, -1};
+        for (int64_t e = 0; e < nS; ++e) {                     /* the point of S closest to q */
+            candd x = {dist2(q, ix->X + (size_t)(ix->row_lo + S[e]) * ix->d, ix->d), S[e]};
+            if (best.id < 0 || cmp_candd(&x, &best) < 0) best = x;
+        }
+        if (best.id >= 0 && (by_budget || best.d2 <= (c * r) * (c * r))) {   /* lines 7, 8-9 */
+            out_ids[qi] = best.id + ix->row_lo;
+            out_dists[qi] = (float)sqrt(best.d2);
+        } else {                                               /* line 10 */
+            out_ids[qi] = -1;
+            out_dists[qi] = INFINITY;
+        }
+    }
+    free(inS); free(S); free(buf); free(qp);
+}
+
+/* ======================================================================== */
 /* O9. Merge of per-shard top-k lists by (dist, id).                          */
 /* ======================================================================== */
 typedef struct { float d; int64_t id; } candf;

@@ -104,6 +104,9 @@ typedef struct {
 /* ids are global (row_lo added); dists = sqrt(d^2) rounded to fp32; missing -> (-1, +inf). */
 void   orc_query(const orc_index* ix, const float* Q, int64_t nq, int k, double c, double r_min,
                  double beta, int mode, int64_t* out_ids, float* out_dists, orc_qstats* stats);
+/* ---- O8b: (r,c)-ANN, Alg. 4: one id/dist per query, (-1, +inf) for "nothing" ---- */
+void   orc_rc_ann(const orc_index* ix, const float* Q, int64_t nq, double c, double r, double beta, int mode,
+                  int64_t* out_ids, float* out_dists);
 /* Projected query (the fp32 K*L vector), exposed for tests. */
 void   orc_project_query(const orc_index* ix, const float* q, float* qp);
 

@@ -82,6 +82,7 @@ def lib():
             "orc_range_query": (i64, [P, i32, P, f64, i32, P]),
             "orc_query": (None, [P, P, i64, i32, f64, f64, f64, i32, P, P, P]),
             "orc_project_query": (None, [P, P, P]),
+            "orc_rc_ann": (None, [P, P, i64, f64, f64, f64, i32, P, P]),
             "orc_merge_topk": (None, [P, P, i32, i64, i32, P, P]),
             "orc_exact_knn": (None, [P, i64, i32, P, i64, i32, P, P]),
             "orc_estimate_rmin": (f64, [P, P, i64, i32, f64, f64, P]),
@@ -290,6 +291,15 @@ class Index:
         lib().orc_query(self._h, _p(Q), nq, k, float(c), float(r_min), float(beta), mode,
                         _p(ids), _p(dists), _p(st))
         return ids, dists, st
+
+    def rc_ann(self, Q, r: float, c: float, beta: float, mode: int = CELL):
+        """(r,c)-ANN, Alg. 4: per query (id, dist) or (-1, inf)."""
+        Q = _c(Q, np.float32).reshape(-1, self.d)
+        nq = Q.shape[0]
+        ids = np.empty(nq, np.int64)
+        dists = np.empty(nq, np.float32)
+        lib().orc_rc_ann(self._h, _p(Q), nq, float(c), float(r), float(beta), mode, _p(ids), _p(dists))
+        return ids, dists
 
     def estimate_rmin(self, Qs, k: int, c: float, beta: float, return_all: bool = False):
         Qs = _c(Qs, np.float32).reshape(-1, self.d)

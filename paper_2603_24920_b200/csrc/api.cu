@@ -240,9 +240,9 @@ detlsh_status detlsh_build(const float* data, int64_t n, int32_t d, int32_t L, i
     return detlsh_build_ex(data, n, d, L, K, N_r, seed, nullptr, 0, n, nullptr, out);
 }
 
-detlsh_status detlsh_query_ex(const detlsh_index* idx, const float* queries, int64_t nq, int32_t k, double c,
-                              double r_min, double beta, const detlsh_opts* opts, int64_t* out_ids, float* out_dists,
-                              detlsh_query_stats* stats) {
+static detlsh_status run_query(const detlsh_index* idx, const float* queries, int64_t nq, int32_t k, double c,
+                               double r_min, double beta, const detlsh_opts* opts, int64_t* out_ids, float* out_dists,
+                               detlsh_query_stats* stats, int max_rounds, bool null_on_cap) {
     return guard([&] {
         DL_REQUIRE(idx, "index is NULL");
         const Index& ix = *reinterpret_cast<const Index*>(idx);
@@ -267,6 +267,8 @@ detlsh_status detlsh_query_ex(const detlsh_index* idx, const float* queries, int
         if (stats) os.reset(new DevOut(stats, sizeof(detlsh_query_stats) * (size_t)nq, st));
         DL_REQUIRE(o.verify_impl == 0 || o.verify_impl == 1, "verify_impl must be 0 or 1");
         QueryArgs a{nq, k, c, r_min, beta, o.mode, o.query_batch, o.mem_budget, o.proj_impl, o.verify_impl};
+        a.max_rounds = max_rounds;
+        a.null_on_cap = null_on_cap;
         query_index(ix, s_q.as<float>(), ix.ld, a, static_cast<int64_t*>(oi.dev()), static_cast<float*>(od.dev()),
                     os ? static_cast<detlsh_query_stats*>(os->dev()) : nullptr, st);
         oi.finish(st);
@@ -274,6 +276,18 @@ detlsh_status detlsh_query_ex(const detlsh_index* idx, const float* queries, int
         if (os) os->finish(st);
         DL_CUDA(cudaStreamSynchronize(st));
     });
+}
+
+detlsh_status detlsh_query_ex(const detlsh_index* idx, const float* queries, int64_t nq, int32_t k, double c,
+                              double r_min, double beta, const detlsh_opts* opts, int64_t* out_ids, float* out_dists,
+                              detlsh_query_stats* stats) {
+    return run_query(idx, queries, nq, k, c, r_min, beta, opts, out_ids, out_dists, stats, 64, false);
+}
+
+detlsh_status detlsh_rc_ann(const detlsh_index* idx, const float* queries, int64_t nq, double r, double c,
+                            double beta, const detlsh_opts* opts, int64_t* out_ids, float* out_dists,
+                            detlsh_query_stats* stats) {
+    return run_query(idx, queries, nq, 1, c, r, beta, opts, out_ids, out_dists, stats, 1, true);
 }
 
 detlsh_status detlsh_query(const detlsh_index* idx, const float* queries, int64_t nq, int32_t k, double c,

@@ -92,6 +92,9 @@ struct QueryArgs {
     int64_t mem_budget;
     int proj_impl;
     int verify_impl;
+    int max_rounds = 64;        // AMB-20 round cap; 1 for (r,c)-ANN (Alg. 4)
+    bool null_on_cap = false;   // (r,c)-ANN: return nothing when the single pass neither hit the
+                                // budget nor found a point within c r
 };
 void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArgs& a, int64_t* d_ids,
                  float* d_dists, detlsh_query_stats* d_stats, cudaStream_t st);

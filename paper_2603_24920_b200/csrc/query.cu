@@ -821,7 +821,7 @@ __global__ void __launch_bounds__(256) k_rerank_exact(const QState* __restrict__
 __global__ void __launch_bounds__(TK_THREADS) k_topk(const int* __restrict__ act, QState* __restrict__ qs,
                                                      const uint32_t* __restrict__ cand, const float* __restrict__ d2,
                                                      unsigned long long* __restrict__ topk, int k,
-                                                     float cr2, int round) {
+                                                     float cr2, int round, int max_rounds) {
     __shared__ unsigned long long s_keys[TK_MAX];
     __shared__ uint32_t s_hist[256];
     uint32_t* s_h12 = reinterpret_cast<uint32_t*>(s_keys);   // 4096 bins, dead before s_keys is filled
@@ -953,7 +953,7 @@ __global__ void __launch_bounds__(TK_THREADS) k_topk(const int* __restrict__ act
         s.rcnt = 0;
         if (s.status == ST_ACTIVE) {
             if (outn >= k && __uint_as_float((uint32_t)(s_keys[k - 1] >> 32)) <= cr2) s.status = ST_RADIUS;  // line 9
-            else if (round == 63) s.status = ST_CAP;                                                        // AMB-20
+            else if (round == max_rounds - 1) s.status = ST_CAP;                                            // AMB-20
         }
         qs[q] = s;
     }
@@ -988,13 +988,15 @@ __global__ void k_compact(const int* __restrict__ act, int na, const QState* __r
 __global__ void k_finalize(const QState* __restrict__ qs, const unsigned long long* __restrict__ ctr,
                            const unsigned long long* __restrict__ topk, int nqb, int k,
                            int64_t id_offset, const double* __restrict__ radii, int64_t* __restrict__ out_ids,
-                           float* __restrict__ out_d, detlsh_query_stats* __restrict__ stats) {
+                           float* __restrict__ out_d, detlsh_query_stats* __restrict__ stats, int null_on_cap) {
     const int64_t total = (int64_t)nqb * k;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
          i += (int64_t)gridDim.x * blockDim.x) {
         const int q = (int)(i / k), e = (int)(i % k);
         const QState s = qs[q];
-        if (e < s.tk) {
+        // (r,c)-ANN (Alg. 4 line 10): nothing unless the pass stopped on the budget or found a
+        // point within c r
+        if (e < s.tk && !(null_on_cap && s.status == ST_CAP)) {
             const unsigned long long key = topk[(int64_t)q * k + e];
             out_ids[i] = (int64_t)(key & 0xFFFFFFFFull) + id_offset;
             out_d[i] = sqrtf(__uint_as_float((uint32_t)(key >> 32)));
@@ -1148,7 +1150,8 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
     DL_REQUIRE(q_ld == ix.ld, "query row stride must equal the index's");
     const int64_t n = ix.n, nq = a.nq, LK = ix.LK;
     const int k = a.k;
-    const int64_t budget = (int64_t)std::ceil(a.beta * (double)n) + k;   // AMB-17
+    const int64_t budget = (int64_t)std::ceil(a.beta * (double)n) + k;   // AMB-17 (k = 1: Alg. 4's beta n + 1)
+    const int max_rounds = std::max(1, std::min(64, a.max_rounds));
     const int64_t nwords = round_up(ceil_div(n, 32), 4);   // bitmap words per query (rows padded to 16 B)
     const int64_t cap = n;                                              // |S| <= n always
 
@@ -1277,7 +1280,7 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
         int na = nqb;
         int* cur = act;
         int* nxt = act2;
-        for (int m = 0; m < 64 && na > 0; ++m) {
+        for (int m = 0; m < max_rounds && na > 0; ++m) {
             const double r = radii[m];
             const float rho2 = (float)((eps * r) * (eps * r));
             const float cr2 = (float)((a.c * r) * (a.c * r));
@@ -1371,7 +1374,7 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
             }
             tr.mark("round buffer + verify", st);
             DL_LAUNCH(k_topk, (unsigned)na, TK_THREADS, 0, st, cur, s_qs.as<QState>(), va.cand, va.d2,
-                      s_tk.as<unsigned long long>(), k, cr2, m);
+                      s_tk.as<unsigned long long>(), k, cr2, m, max_rounds);
             tr.mark("top-k", st);
             DL_LAUNCH(k_compact, 1, 1024, 0, st, cur, na, s_qs.as<QState>(), nxt, n_act);
             DL_CUDA(cudaMemcpyAsync(&na, n_act, sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -1383,7 +1386,7 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
                   s_tk.as<unsigned long long>());
         DL_LAUNCH(k_finalize, (unsigned)std::min<int64_t>(ceil_div((int64_t)nqb * k, 256), 148 * 16), 256, 0, st,
                   s_qs.as<QState>(), s_ctr.as<unsigned long long>(), s_tk.as<unsigned long long>(), nqb, k, ix.id_offset, s_radii.as<double>(),
-                  d_ids + q0 * k, d_dists + q0 * k, d_stats ? d_stats + q0 : nullptr);
+                  d_ids + q0 * k, d_dists + q0 * k, d_stats ? d_stats + q0 : nullptr, a.null_on_cap ? 1 : 0);
         (void)Qb;
     }
 }

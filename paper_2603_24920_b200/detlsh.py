@@ -90,6 +90,7 @@ def lib():
         "detlsh_build_from_codes": (i32, [P, i64, i32, i32, i32, O, P]),
         "detlsh_launch_count": (i64, []),
         "detlsh_estimate_rmin": (i32, [P, P, i64, i32, f64, O, P, P]),
+        "detlsh_rc_ann": (i32, [P, P, i64, f64, f64, f64, O, P, P, P]),
         "detlsh_profile_enable": (None, [i32]),
         "detlsh_profile_reset": (None, []),
         "detlsh_release_workspace": (None, []),
@@ -207,6 +208,17 @@ class Index:
     def query(self, Q, k: int, c: float, r_min: float, beta: float, opts: detlsh_opts | None = None,
               stats: bool = False, out_ids=None, out_dists=None):
         return detlsh_query_ex(self, Q, k, c, r_min, beta, opts, stats, out_ids, out_dists)
+
+    def rc_ann(self, Q, r: float, c: float, beta: float, opts: detlsh_opts | None = None, stats: bool = False):
+        """(r,c)-ANN, Alg. 4: per query (id, dist), (-1, inf) for "nothing"."""
+        Q = _f32(Q)
+        nq = Q.shape[0]
+        ids = _like(Q, (nq,), np.int64, _torch_i64())
+        dists = _like(Q, (nq,), np.float32, _torch_f32())
+        st = np.zeros(nq, STATS_DTYPE) if stats else None
+        o = opts if opts is not None else default_opts()
+        _check(lib().detlsh_rc_ann(self._h, _ptr(Q), nq, r, c, beta, C.byref(o), _ptr(ids), _ptr(dists), _ptr(st)))
+        return (ids, dists, st) if stats else (ids, dists)
 
     # ------------------------------------------------------------------ debug / test exports
     def export(self, what: int, tree: int = 0):

@@ -345,3 +345,21 @@ def test_logical_shards_on_one_gpu(tiny, G):
     ri, rd = O.sharded_query(X, G, Q, c.k, c.c, rmin, c.beta, c.L, c.K, c.N_r, c.index_seed)
     assert _recall(mi, ri) >= 0.99
     _dist_match(mi, md, ri, rd)
+
+
+@pytest.mark.parametrize("mode", [P.MODE_CELL, P.MODE_RELAXED])
+def test_rc_ann_parity(gpu_tiny, tiny_oracle, tiny, mode):
+    """(r,c)-ANN (Alg. 4) through detlsh_rc_ann vs the oracle at radii below, at and above r_min:
+    the same queries answered (id >= 0) and the same ids on >= 99% of them; distances 1e-4."""
+    c = tiny["cfg"]
+    Q = tiny["Q"]
+    rmin = tiny_oracle.estimate_rmin(tiny["Qs"], 1, c.c, c.beta)
+    for r in (0.5 * rmin, rmin, 2.0 * rmin, 1e9, 1e-6):
+        gi, gd, gs = gpu_tiny.rc_ann(Q, r, c.c, c.beta, opts=P.default_opts(mode=mode), stats=True)
+        oi, od = tiny_oracle.rc_ann(Q, r, c.c, c.beta, mode=mode)
+        assert np.mean((gi >= 0) == (oi >= 0)) >= 0.99
+        both = (gi >= 0) & (oi >= 0)
+        assert np.mean(gi[both] == oi[both]) >= 0.99
+        assert np.allclose(gd[both & (gi == oi)], od[both & (gi == oi)], rtol=1e-4)
+        assert np.all(np.isinf(gd[gi < 0])) and np.all(gs["rounds"] == 1)
+        assert np.all((gs["reason"] == 2) == (gi < 0))

@@ -515,3 +515,32 @@ def test_recall_ratio_definitions():
     R, Rs = [1, 2, 3, 4], [3, 4, 5, 6]
     assert len(set(R) & set(Rs)) / 4 == 0.5
     assert np.mean(np.array([1.0, 3.0]) / np.array([1.0, 2.0])) == 1.25
+
+
+def test_rc_ann_pins(tiny_oracle, tiny):
+    """(r,c)-ANN, Alg. 4 pinned three ways: (1) a radius past every bound makes tree 1's
+    range query return all of D, so |S| = n >= beta n + 1 and the answer is the exact nearest
+    neighbour (numpy fp64 brute force, ties by id); (2) beta >= 1 never meets the budget, and with
+    S = D the nearest neighbour lies within c r: same answer; (3) r below every bound: S is
+    empty, nothing is returned; (4) at a middle radius the answer equals the first round of the
+    c^2-k-ANN driver (Alg. 5, k = 1, r_min = r) whenever that round stopped it, and is
+    "nothing" exactly when Alg. 5 needed a second round."""
+    X, Q = tiny["X"], tiny["Q"][:40]
+    d2 = ((Q[:, None, :].astype(np.float64) - X[None].astype(np.float64)) ** 2).sum(-1)
+    nn = np.array([np.lexsort((np.arange(len(X)), row))[0] for row in d2])
+    ids, dists = tiny_oracle.rc_ann(Q, 1e9, 1.5, 0.1)
+    assert np.array_equal(ids, nn)
+    assert np.allclose(dists, np.sqrt(d2[np.arange(len(Q)), nn]), rtol=1e-6)
+    ids2, _ = tiny_oracle.rc_ann(Q, 1e9, 1.5, 2.0)
+    assert np.array_equal(ids2, nn)
+    ids3, d3 = tiny_oracle.rc_ann(Q, 1e-6, 1.5, 0.1)
+    assert np.all(ids3 == -1) and np.all(np.isinf(d3))
+    c = tiny["cfg"]
+    rmin = tiny_oracle.estimate_rmin(tiny["Qs"], 1, c.c, c.beta)
+    for r in (0.5 * rmin, rmin, 1.5 * rmin):
+        ri, rd = tiny_oracle.rc_ann(Q, r, c.c, c.beta)
+        qi, qd, st = tiny_oracle.query(Q, 1, c.c, r, c.beta)
+        one = st["rounds"] == 1
+        assert np.array_equal(ri[one], qi[one, 0]) and np.array_equal(rd[one], qd[one, 0])
+        assert np.all(ri[~one] == -1)
+        assert 0 < one.sum() or r < rmin

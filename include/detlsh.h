@@ -209,6 +209,18 @@ detlsh_status detlsh_debug_export(const detlsh_index* idx, int32_t what, int32_t
 detlsh_status detlsh_build_from_codes(const uint8_t* codes, int64_t n, int32_t L, int32_t K,
                                       int32_t N_r, const detlsh_opts* opts, detlsh_index** out);
 
+/* Index persistence.  save writes every device array of the index (the data
+   rows included, also when borrowed) to `path` (binary, little-endian, versioned header);
+   load reads it back into device memory of the current device and returns a new index the
+   caller frees with detlsh_free.  Both are synchronous.  Errors: EINVAL (NULL or unopenable
+   path, not an index file, truncated file, unsupported version), ENOMEM, ECUDA. */
+detlsh_status detlsh_save(const detlsh_index* idx, const char* path);
+detlsh_status detlsh_load(const char* path, detlsh_index** out);
+
+/* Shape of an index: info[8] = {n, d, L, K, N_r, n_global, id_offset, codes_only}.
+   Errors: EINVAL on NULL. */
+detlsh_status detlsh_index_info(const detlsh_index* idx, int64_t* info);
+
 /* Number of kernels this library has launched in this process (evidence counter). */
 int64_t detlsh_launch_count(void);
 

@@ -319,6 +319,31 @@ detlsh_status detlsh_estimate_rmin(const detlsh_index* idx, const float* queries
     });
 }
 
+detlsh_status detlsh_save(const detlsh_index* idx, const char* path) {
+    return guard([&] {
+        DL_REQUIRE(idx, "index is NULL");
+        require_device();
+        save_index(*reinterpret_cast<const Index*>(idx), path);
+    });
+}
+
+detlsh_status detlsh_load(const char* path, detlsh_index** out) {
+    return guard([&] {
+        DL_REQUIRE(out, "out is NULL");
+        require_device();
+        *out = reinterpret_cast<detlsh_index*>(load_index(path));
+    });
+}
+
+detlsh_status detlsh_index_info(const detlsh_index* idx, int64_t* info) {
+    return guard([&] {
+        DL_REQUIRE(idx && info, "NULL argument");
+        const Index& ix = *reinterpret_cast<const Index*>(idx);
+        const int64_t v[8] = {ix.n, ix.d, ix.L, ix.K, ix.N_r, ix.n_global, ix.id_offset, ix.codes_only ? 1 : 0};
+        std::memcpy(info, v, sizeof(v));
+    });
+}
+
 void detlsh_free(detlsh_index* idx) {
     if (!idx) return;
     delete reinterpret_cast<Index*>(idx);

@@ -82,6 +82,10 @@ void sample_ids_device(uint64_t seed, int64_t id_lo, int64_t n_range, int64_t n_
 void breakpoints_from_projections(const float* d_Ps, int64_t m, int LK, int N_r, float* d_B,
                                   cudaStream_t st);
 
+// persist.cu
+void save_index(const Index& ix, const char* path);
+Index* load_index(const char* path);
+
 // query.cu
 struct QueryArgs {
     int64_t nq;

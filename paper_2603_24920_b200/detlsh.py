@@ -91,6 +91,9 @@ def lib():
         "detlsh_launch_count": (i64, []),
         "detlsh_estimate_rmin": (i32, [P, P, i64, i32, f64, O, P, P]),
         "detlsh_rc_ann": (i32, [P, P, i64, f64, f64, f64, O, P, P, P]),
+        "detlsh_save": (i32, [P, C.c_char_p]),
+        "detlsh_load": (i32, [C.c_char_p, P]),
+        "detlsh_index_info": (i32, [P, P]),
         "detlsh_profile_enable": (None, [i32]),
         "detlsh_profile_reset": (None, []),
         "detlsh_release_workspace": (None, []),
@@ -209,6 +212,9 @@ class Index:
               stats: bool = False, out_ids=None, out_dists=None):
         return detlsh_query_ex(self, Q, k, c, r_min, beta, opts, stats, out_ids, out_dists)
 
+    def save(self, path: str):
+        _check(lib().detlsh_save(self._h, str(path).encode()))
+
     def rc_ann(self, Q, r: float, c: float, beta: float, opts: detlsh_opts | None = None, stats: bool = False):
         """(r,c)-ANN, Alg. 4: per query (id, dist), (-1, inf) for "nothing"."""
         Q = _f32(Q)
@@ -323,6 +329,16 @@ def detlsh_query_ex(index: Index, Q, k, c, r_min, beta, opts=None, stats=False, 
 
 def detlsh_query(index: Index, Q, k, c, r_min, beta):
     return detlsh_query_ex(index, Q, k, c, r_min, beta)
+
+
+def detlsh_load(path: str) -> Index:
+    """Load an index written by Index.save (detlsh_load)."""
+    h = C.c_void_p()
+    _check(lib().detlsh_load(str(path).encode(), C.byref(h)))
+    info = np.zeros(8, np.int64)
+    _check(lib().detlsh_index_info(h, info.ctypes.data_as(C.c_void_p)))
+    n, d, L, K, N_r = (int(v) for v in info[:5])
+    return Index(h, n, d, L, K, N_r)
 
 
 def detlsh_build_from_codes(codes, L: int, K: int, N_r: int, max_size: int = 128) -> Index:

@@ -363,3 +363,30 @@ def test_rc_ann_parity(gpu_tiny, tiny_oracle, tiny, mode):
         assert np.allclose(gd[both & (gi == oi)], od[both & (gi == oi)], rtol=1e-4)
         assert np.all(np.isinf(gd[gi < 0])) and np.all(gs["rounds"] == 1)
         assert np.all((gs["reason"] == 2) == (gi < 0))
+
+
+def test_save_load_roundtrip(tmp_path, tiny, tiny_rmin):
+    """f4 persistence: an index saved and loaded answers identically (ids and distances), for an
+    owned and for a borrowed-data index; corrupt files are refused."""
+    import torch
+    c = tiny["cfg"]
+    Xd = torch.from_numpy(tiny["X"]).cuda()
+    for borrow in (0, 1):
+        g = P.detlsh_build(Xd, c.L, c.K, c.N_r, c.index_seed, opts=P.default_opts(borrow_data=borrow))
+        i0, d0 = g.query(tiny["Q"], c.k, c.c, tiny_rmin, c.beta)
+        path = str(tmp_path / f"ix{borrow}.detlsh")
+        g.save(path)
+        h = P.detlsh_load(path)
+        i1, d1 = h.query(tiny["Q"], c.k, c.c, tiny_rmin, c.beta)
+        assert np.array_equal(i0, i1) and np.array_equal(d0, d1)
+        assert np.array_equal(g.codes(), h.codes()) and np.array_equal(g.breakpoints(), h.breakpoints())
+        for t in range(c.L):
+            assert all(np.array_equal(g.tree(t)[key], h.tree(t)[key]) for key in ("perm", "leaf_off", "lo", "hi"))
+    bad = tmp_path / "bad.detlsh"
+    bad.write_bytes(b"not an index")
+    with pytest.raises(P.DetlshError):
+        P.detlsh_load(str(bad))
+    trunc = tmp_path / "trunc.detlsh"
+    trunc.write_bytes(open(path, "rb").read()[:5000])
+    with pytest.raises(P.DetlshError):
+        P.detlsh_load(str(trunc))

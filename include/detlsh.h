@@ -42,7 +42,10 @@ typedef enum {
 
 /* Range-query predicate inside partially covered leaves (AMB-12). */
 enum { DETLSH_MODE_CELL = 0,     /* point's own region lower bound <= eps r (hot path) */
-       DETLSH_MODE_RELAXED = 1   /* Sec. 6.2.2(1): whole leaf when leaf LB <= eps r */ };
+       DETLSH_MODE_RELAXED = 1,  /* Sec. 6.2.2(1): whole leaf when leaf LB <= eps r */
+       DETLSH_MODE_EXACT = 2     /* Alg. 3 as written: the point's true projected
+                                    distance ||q'_i - p'_i|| <= eps r; needs an index built with
+                                    opts.keep_projections = 1 (n*L*K*4 bytes more) */ };
 
 typedef struct {
     int32_t  max_size;     /* leaf capacity of Alg. 2 (AMB-8), default 128 */
@@ -58,7 +61,7 @@ typedef struct {
                               (||x||^2 + ||q||^2 - 2 x.q with 3xTF32 dot products, fp32-level
                               accuracy), 1 = CUDA cores (direct fp32 sum of squares).  Either
                               way the returned top-k distances are recomputed directly in fp32. */
-    int32_t  pad0;
+    int32_t  keep_projections; /* build: 1 keeps the fp32 projections of every point (EXACT mode) */
 } detlsh_opts;
 
 /* Per-query statistics (Alg. 5 bookkeeping). */

@@ -171,7 +171,7 @@ void detlsh_default_opts(detlsh_opts* o) {
     o->proj_impl = 0;
     o->mem_budget = 0;
     o->verify_impl = 0;
-    o->pad0 = 0;
+    o->keep_projections = 0;
 }
 
 const char* detlsh_last_error(void) { return g_err.c_str(); }
@@ -211,6 +211,7 @@ detlsh_status detlsh_build_ex(const float* data, int64_t n, int32_t d, int32_t L
         WorkspaceScope ws(st);
         auto ix = std::make_unique<Index>();
         init_index_params(*ix, n, d, L, K, N_r, seed, o);
+        ix->keep_proj = o.keep_projections != 0;
         ix->id_offset = id_offset;
         ix->n_global = std::max<int64_t>(n_global, n);
         const bool dev = is_device_ptr(data);
@@ -255,7 +256,10 @@ static detlsh_status run_query(const detlsh_index* idx, const float* queries, in
         DL_REQUIRE(beta > 0.0 && std::isfinite(beta), "beta must be > 0");
         DL_REQUIRE(r_min > 0.0 && std::isfinite(r_min), "r_min must be > 0 and finite");
         const detlsh_opts o = opts_or_default(opts);
-        DL_REQUIRE(o.mode == DETLSH_MODE_CELL || o.mode == DETLSH_MODE_RELAXED, "unknown mode");
+        DL_REQUIRE(o.mode == DETLSH_MODE_CELL || o.mode == DETLSH_MODE_RELAXED || o.mode == DETLSH_MODE_EXACT,
+                   "unknown mode");
+        DL_REQUIRE(o.mode != DETLSH_MODE_EXACT || ix.proj.p != nullptr,
+                   "EXACT mode needs an index built with opts.keep_projections = 1");
         require_device();
         cudaStream_t st = stream_of(&o);
         WorkspaceScope ws(st);

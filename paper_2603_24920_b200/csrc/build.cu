@@ -824,7 +824,7 @@ static void build_trees(Index& ix, const uint8_t* d_EP, cudaStream_t st) {
 }
 
 bool project_encode_tc(const Index& ix, const float* d_X, int64_t ld, int64_t m, uint8_t* d_EP, int* d_nonfinite,
-                       float* d_xnorm, cudaStream_t st);
+                       float* d_xnorm, float* d_P, cudaStream_t st);
 
 void build_index(Index& ix, const float* d_data, int64_t data_ld, const float* bp_given, double sample_frac,
                  int proj_impl, cudaStream_t st) {
@@ -861,8 +861,9 @@ void build_index(Index& ix, const float* d_data, int64_t data_ld, const float* b
     // shape fits, else projection (chunked so P stays bounded) + k_encode
     Scratch s_ep(st, (size_t)n * ix.LK);
     ix.xnorm.alloc(sizeof(float) * (size_t)n, st);     // ||x||^2 per row (tensor-core verification)
-    if (!(proj_impl == 0 &&
-          project_encode_tc(ix, d_data, data_ld, n, s_ep.as<uint8_t>(), s_flag.as<int>(), ix.xnorm.as<float>(), st))) {
+    if (ix.keep_proj) ix.proj.alloc(sizeof(float) * (size_t)n * ix.LK, st);   // EXACT mode: p' of every point
+    if (!(proj_impl == 0 && project_encode_tc(ix, d_data, data_ld, n, s_ep.as<uint8_t>(), s_flag.as<int>(),
+                                              ix.xnorm.as<float>(), ix.keep_proj ? ix.proj.as<float>() : nullptr, st))) {
         DL_LAUNCH(k_row_norms, grid_for(n * 32, 256), 256, 0, st, d_data, data_ld, n, ix.xnorm.as<float>());
         const int64_t chunk = std::min<int64_t>(n, std::max<int64_t>(1 << 16, (int64_t)(1ll << 30) / (4 * ix.LK)));
         Scratch s_p(st, sizeof(float) * (size_t)(chunk * ix.LK));
@@ -870,6 +871,9 @@ void build_index(Index& ix, const float* d_data, int64_t data_ld, const float* b
             const int64_t m = std::min(chunk, n - r0);
             project_rows(ix, d_data + r0 * data_ld, data_ld, m, s_p.as<float>(), proj_impl, s_flag.as<int>(), st);
             encode_all(ix, s_p.as<float>(), m, s_ep.as<uint8_t>() + r0 * ix.LK, st);
+            if (ix.keep_proj)
+                DL_CUDA(cudaMemcpyAsync(ix.proj.as<float>() + r0 * ix.LK, s_p.p, sizeof(float) * (size_t)(m * ix.LK),
+                                        cudaMemcpyDeviceToDevice, st));
         }
     }
     const int nonfinite = d2h(s_flag.as<int>(), st);

@@ -64,6 +64,8 @@ struct Index {
     std::vector<int64_t> tree_tile_begin;  // [L+1] tile index range of each tree (host copy)
     DevBuf point_tile_leaf; // [L*n] u16: leaf of each point (tree order) within its tile (< 32)
     DevBuf xnorm;           // [n] fp32 ||x||^2 of every row (tensor-core verification, verify_tc.cu)
+    bool keep_proj = false; // build option: keep the projections (EXACT mode)
+    DevBuf proj;            // [n][LK] fp32 projections p' in data order (EXACT mode only)
 
     int64_t nl_total() const { return tree_leaf_begin.empty() ? 0 : tree_leaf_begin.back(); }
 };

@@ -230,7 +230,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                             for (int i = 0; i < 16 && c0 + i < sh.LK; ++i) out[i] = (uint8_t)(packed[i >> 2] >> (8 * (i & 3)));
                         }
                     }
-                } else if (row < sh.m) {
+                }
+                if (P != nullptr && row < sh.m) {   // projections (also kept beside the codes for EXACT mode)
                     float* out = P + row * sh.LK + c0;
                     if (c0 + 16 <= sh.LK && (sh.LK & 3) == 0) {
 #pragma unroll
@@ -301,8 +302,8 @@ bool project_rows_tc(const Index& ix, const float* d_X, int64_t ld, int64_t m, f
 }
 
 bool project_encode_tc(const Index& ix, const float* d_X, int64_t ld, int64_t m, uint8_t* d_EP, int* d_nonfinite,
-                       float* d_xnorm, cudaStream_t st) {
-    return launch_tc(ix, d_X, ld, m, nullptr, d_nonfinite, ix.B.as<float>(), d_EP, d_xnorm, st);
+                       float* d_xnorm, float* d_P, cudaStream_t st) {
+    return launch_tc(ix, d_X, ld, m, d_P, d_nonfinite, ix.B.as<float>(), d_EP, d_xnorm, st);
 }
 
 }  // namespace detlsh

@@ -126,6 +126,8 @@ struct RFArgs {
     const float* lut;           // [Qb][L][K][N_r] exact
     const uint16_t* qlut;       // [Qb][L][K][N_r] quantised lower bounds (this round)
     const uint8_t* sx;          // [Qb][L][K]
+    const float* proj;          // EXACT: data-order projections [n][LK]
+    const float* qp;            // EXACT: projected batch queries [Qb][LK]
     const int* act;
     int na;
     const QState* qs;
@@ -145,6 +147,7 @@ __global__ void __launch_bounds__(RF_THREADS, 3) k_range_filter(RFArgs a) {
     uint4* s_qe = reinterpret_cast<uint4*>(smem);                                       // [K][N_r] x 16 B
     __shared__ int s_q[G];
     __shared__ uint8_t s_sx[G][32];
+    __shared__ float s_qp[G][32];                                                        // EXACT: q'_t
     __shared__ unsigned int s_ctr[G][4];
     __shared__ uint32_t s_lq[RF_THREADS / 32][kTileLeaves];                             // per warp: leaf masks
     __shared__ uint32_t s_bq[RF_THREADS / 32][RF_BQ];                                   // per warp: band queue
@@ -189,8 +192,11 @@ __global__ void __launch_bounds__(RF_THREADS, 3) k_range_filter(RFArgs a) {
         }
         if (threadIdx.x < K) {
 #pragma unroll
-            for (int g = 0; g < G; ++g)
+            for (int g = 0; g < G; ++g) {
                 s_sx[g][threadIdx.x] = s_q[g] >= 0 ? a.sx[((int64_t)s_q[g] * a.L + a.t) * K + threadIdx.x] : 0;
+                if (a.mode == DETLSH_MODE_EXACT)
+                    s_qp[g][threadIdx.x] = s_q[g] >= 0 ? a.qp[(int64_t)s_q[g] * a.L * K + a.t * K + threadIdx.x] : 0.f;
+            }
         }
     }
     __syncthreads();
@@ -250,7 +256,7 @@ __global__ void __launch_bounds__(RF_THREADS, 3) k_range_filter(RFArgs a) {
 #pragma unroll
             for (int g = 0; g < G; ++g)
                 if (lacc[g] <= QT && ((amask >> g) & 1)) m |= 1u << g;
-            if (a.mode != DETLSH_MODE_CELL) {
+            if (a.mode == DETLSH_MODE_RELAXED) {
                 // RELAXED (Sec. 6.2.2(1)): the leaf decision is final, so decide it in fp32
                 uint32_t conf = 0, mm = m;
                 while (mm) {
@@ -278,7 +284,14 @@ __global__ void __launch_bounds__(RF_THREADS, 3) k_range_filter(RFArgs a) {
                 const int64_t pos = (int64_t)(P0 + (e >> 4)) - a.pos_base;
                 const float* D = a.lut + (int64_t)s_q[g] * per_q + (int64_t)a.t * K * N_r;
                 float s_ = 0.f;
-                if (KT == 16) {
+                if (a.mode == DETLSH_MODE_EXACT) {
+                    // Alg. 3 as written: ||q'_t - p'_t||^2 in fp32, j order
+                    const float* pp = a.proj + (int64_t)a.perm[pos] * a.L * K + a.t * K;
+                    for (int j = 0; j < K; ++j) {
+                        const float df = s_qp[g][j] - __ldg(pp + j);
+                        s_ = fmaf(df, df, s_);
+                    }
+                } else if (KT == 16) {
                     const uint4 c4 = *reinterpret_cast<const uint4*>(a.tcodes + pos * 16);
 #pragma unroll
                     for (int j = 0; j < 16; ++j) {
@@ -320,7 +333,7 @@ __global__ void __launch_bounds__(RF_THREADS, 3) k_range_filter(RFArgs a) {
             if (__ballot_sync(0xffffffffu, m != 0) == 0) continue;    // whole warp pruned by leaf LBs
             c_pt += __popc(m);
             uint32_t certain = m, band = 0;
-            if (m && a.mode == DETLSH_MODE_CELL) {
+            if (m && a.mode != DETLSH_MODE_RELAXED) {
                 uint32_t ok = 0, sure = 0;
                 if (KT == 16) {
                     uint32_t acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -373,8 +386,13 @@ __global__ void __launch_bounds__(RF_THREADS, 3) k_range_filter(RFArgs a) {
                         sure |= (acc[g] + 17 <= QT ? 1u : 0u) << g;
                     }
                 }
-                certain = m & sure;
-                band = m & ok & ~sure;
+                if (a.mode == DETLSH_MODE_CELL) {
+                    certain = m & sure;
+                    band = m & ok & ~sure;
+                } else {       // EXACT: the cell bound only rejects; every survivor gets its true distance
+                    certain = 0;
+                    band = m & ok;
+                }
             }
             if (certain) {
                 c_pp += __popc(certain);
@@ -1180,7 +1198,9 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
         budget_bytes = auto_query_budget();
     }
     int64_t qb = a.query_batch > 0 ? a.query_batch : std::max<int64_t>(1, budget_bytes / per_q);
-    qb = std::min<int64_t>({qb, nq, 65535});
+    // round-buffer slots are 32-bit (verify offsets): a query adds at most n new members per
+    // round, so a batch of qb queries needs qb * n < 2^32
+    qb = std::min<int64_t>({qb, nq, 65535, std::max<int64_t>(1, (int64_t)0xFFFFFFFFll / n)});
     DL_REQUIRE(qb >= 1, "not enough device memory for one query");
 
     Scratch s_bm(st, sizeof(uint32_t) * (size_t)(2 * qb * nwords));   // current union + previous
@@ -1227,6 +1247,7 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
     ra.lut = s_lut.as<float>();
     ra.qlut = s_qlut.as<uint16_t>();
     ra.sx = s_sx.as<uint8_t>();
+    ra.proj = ix.proj.as<float>();
     ra.qs = s_qs.as<QState>();
     ra.bitmap = s_bm.as<uint32_t>();
     ra.nwords = nwords;
@@ -1302,6 +1323,7 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
                 ra.tile_begin = ix.tree_tile_begin[t];
                 ra.tile_end = ix.tree_tile_begin[t + 1];
                 ra.act = fa;
+                ra.qp = Qpb;
                 ra.na = nf;
                 ra.rho2 = rho2;
                 ra.t = t;

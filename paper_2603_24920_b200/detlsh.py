@@ -18,7 +18,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libdetlsh.so")
 
 DETLSH_OK, DETLSH_EINVAL, DETLSH_ENOMEM, DETLSH_ECUDA, DETLSH_ENCCL, DETLSH_EINTERNAL = range(6)
-MODE_CELL, MODE_RELAXED = 0, 1
+MODE_CELL, MODE_RELAXED, MODE_EXACT = 0, 1, 2
 _NAMES = {1: "EINVAL", 2: "ENOMEM", 3: "ECUDA", 4: "ENCCL", 5: "EINTERNAL"}
 
 
@@ -32,7 +32,7 @@ class detlsh_opts(C.Structure):
     _fields_ = [("max_size", C.c_int32), ("sample_frac", C.c_double), ("mode", C.c_int32),
                 ("query_batch", C.c_int32), ("stream", C.c_uint64), ("borrow_data", C.c_int32),
                 ("proj_impl", C.c_int32), ("mem_budget", C.c_int64),
-                ("verify_impl", C.c_int32), ("pad0", C.c_int32)]
+                ("verify_impl", C.c_int32), ("keep_projections", C.c_int32)]
 
 
 class detlsh_kernel_time(C.Structure):

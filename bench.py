@@ -33,9 +33,19 @@ METRIC = "queries/s at recall@k>=0.9"
 
 
 def load_rmin(cid: int) -> float:
-    path = os.path.join(ROOT, "bench_configs.json")
-    data = json.load(open(path))
-    return float(data[str(cid)]["r_min"])
+    """The radius both arms run at: r_bench = r_min c^-m* (the operating point the ORACLE picked,
+    tools/make_rmin.py --point: largest m with oracle recall >= 0.95 on held-out sample queries;
+    SURVEY 8(d)), else the AMB-22 r_min itself."""
+    e = json.load(open(os.path.join(ROOT, "bench_configs.json")))[str(cid)]
+    return float(e.get("r_bench", e["r_min"]))
+
+
+def rmin_info(cid: int) -> dict:
+    e = json.load(open(os.path.join(ROOT, "bench_configs.json")))[str(cid)]
+    return {"r_min_amb22": e["r_min"], "bench_m": e.get("bench_m", 0),
+            "bench_oracle_recall": e.get("bench_oracle_recall"),
+            "r_choice": "r_min c^-m, m = largest with oracle recall@k >= 0.95 on 50 held-out sample queries "
+                        "(tools/make_rmin.py --point; SURVEY 8(d))"}
 
 
 def workload_desc(c) -> str:
@@ -213,7 +223,7 @@ def run_reference(args, cfg):
     line = {"impl": "reference", "metric": METRIC, "value": qps, "unit": "queries/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * sum(times) / len(times),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": {"workload": workload_desc(cfg), "r_min": r_min},
+            "data": "synthetic", "config": {"workload": workload_desc(cfg), "r_min": r_min, **rmin_info(args.config)},
             "cpu_baseline": {"value": qps, "unit": "queries/s", "cores": 1, "kind": "oracle",
                              "sample": f"{per_step} random queries of the {cfg.nq} per step, index built once "
                                        f"(oracle build {cfg.n / build_s:.0f} points/s, 1 core)"},
@@ -376,7 +386,7 @@ def main():
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic",
             "config": {"workload": workload_desc(cfg), "n": cfg.n, "d": cfg.d, "nq": cfg.nq, "k": cfg.k,
-                       "r_min": r_min, "parallelism": f"point-sharded x{world}",
+                       "r_min": r_min, **rmin_info(args.config), "parallelism": f"point-sharded x{world}",
                        "l2": "no flush: X (1.02 GB at configs[1]) and the rebuilt index exceed L2 (126 MB)",
                        "proj_impl": int(opts.proj_impl)},
             "recall_at_k": rec, "recall_queries": int(len(sel)),

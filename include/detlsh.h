@@ -57,10 +57,14 @@ typedef struct {
     int32_t  proj_impl;    /* projection kernel: 0 = tcgen05 tensor cores, 1 = SIMT fp32 */
     int64_t  mem_budget;   /* bytes of device scratch for query batches, 0 = auto (60% of the
                               memory free at the first query on this device in the process) */
-    int32_t  verify_impl;  /* candidate verification (Alg. 5 l.8): 0 = tcgen05 tensor cores
-                              (||x||^2 + ||q||^2 - 2 x.q with 3xTF32 dot products, fp32-level
-                              accuracy), 1 = CUDA cores (direct fp32 sum of squares).  Either
-                              way the returned top-k distances are recomputed directly in fp32. */
+    int32_t  verify_impl;  /* candidate verification (Alg. 5 l.8): 2 = tcgen05 tensor cores
+                              (masked dense X.Q^T: ||x||^2 + ||q||^2 - 2 x.q with 3xTF32 dot
+                              products, fp32-level accuracy), 1 = CUDA cores (rows staged once,
+                              direct fp32 sum of squares per candidate), 3 = sparse gather (the
+                              round's candidates listed, one 8-lane group per candidate reads
+                              its row), 0 = per round the cheaper of tensor cores and gather for
+                              that round's candidate density (default).
+                              Either way the returned distances are recomputed directly in fp32. */
     int32_t  keep_projections; /* build: 1 keeps the fp32 projections of every point (EXACT mode) */
 } detlsh_opts;
 

@@ -269,7 +269,7 @@ static detlsh_status run_query(const detlsh_index* idx, const float* queries, in
         DevOut od(out_dists, sizeof(float) * (size_t)(nq * k), st);
         std::unique_ptr<DevOut> os;
         if (stats) os.reset(new DevOut(stats, sizeof(detlsh_query_stats) * (size_t)nq, st));
-        DL_REQUIRE(o.verify_impl == 0 || o.verify_impl == 1, "verify_impl must be 0 or 1");
+        DL_REQUIRE(o.verify_impl >= 0 && o.verify_impl <= 3, "verify_impl must be 0..3");
         QueryArgs a{nq, k, c, r_min, beta, o.mode, o.query_batch, o.mem_budget, o.proj_impl, o.verify_impl};
         a.max_rounds = max_rounds;
         a.null_on_cap = null_on_cap;

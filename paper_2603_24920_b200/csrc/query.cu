@@ -801,6 +801,55 @@ __device__ void bitonic_sort_smem(unsigned long long* a, int n2) {
     }
 }
 
+// ---- sparse verification (low candidate density): the new members of S listed at their
+//      round-buffer slots (k_collect_cands, from k_verify_prep's NB/BO), then one 8-lane group
+//      per candidate gathers its row with float4 loads (k_verify_gather): per candidate 4d bytes
+//      of X, no per-(row block, query) work.
+__global__ void k_collect_cands(int na, const uint32_t* __restrict__ NB, const uint32_t* __restrict__ BO,
+                                int64_t nwords, uint32_t* __restrict__ cand, uint32_t* __restrict__ cq) {
+    const int64_t total = (int64_t)na * nwords;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        uint32_t w = NB[i];
+        if (!w) continue;
+        const int a = (int)(i / nwords);
+        const uint32_t base = (uint32_t)((i - (int64_t)a * nwords) * 32);
+        uint32_t slot = BO[i];
+        while (w) {
+            const int b = __ffs(w) - 1;
+            w &= w - 1;
+            cand[slot] = base + (uint32_t)b;
+            cq[slot] = (uint32_t)a;
+            ++slot;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256) k_verify_gather(const uint32_t* __restrict__ cand, const uint32_t* __restrict__ cq,
+                                                       const int* __restrict__ act, const float* __restrict__ X,
+                                                       const float* __restrict__ Q, int64_t ld, int64_t total,
+                                                       float* __restrict__ d2) {
+    const int u = threadIdx.x & 7;
+    const int nf4 = (int)(ld / 4);
+    for (int64_t slot = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 3; slot < total;
+         slot += ((int64_t)gridDim.x * blockDim.x) >> 3) {
+        const float4* x4 = reinterpret_cast<const float4*>(X + (int64_t)cand[slot] * ld);
+        const float4* q4 = reinterpret_cast<const float4*>(Q + (int64_t)act[cq[slot]] * ld);
+        float2 acc = make_float2(0.f, 0.f);
+        for (int f = u; f < nf4; f += 8) {
+            const float4 x = __ldg(x4 + f), y = __ldg(q4 + f);
+            const float2 e0 = make_float2(x.x - y.x, x.y - y.y), e1 = make_float2(x.z - y.z, x.w - y.w);
+            acc = __ffma2_rn(e0, e0, acc);
+            acc = __ffma2_rn(e1, e1, acc);
+        }
+        float s_ = acc.x + acc.y;
+        s_ += __shfl_xor_sync(0xffffffffu, s_, 1);
+        s_ += __shfl_xor_sync(0xffffffffu, s_, 2);
+        s_ += __shfl_xor_sync(0xffffffffu, s_, 4);
+        if (u == 0) d2[slot] = s_;
+    }
+}
+
 // ---- after the rounds of a batch: the top-k distances recomputed directly in fp32 (the
 //      tensor-core verification ranks by ||x||^2 + ||q||^2 - 2 x.q), re-sorted by (d2, id).
 __global__ void __launch_bounds__(256) k_rerank_exact(const QState* __restrict__ qs, const float* __restrict__ X,
@@ -1207,6 +1256,7 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
     Scratch s_ctr(st, sizeof(unsigned long long) * (size_t)(4 * qb));
     Scratch s_ver(st, sizeof(uint32_t) * (size_t)(qb * nwords));     // verified members of S
     Scratch s_round(st);                   // (id, d2) of this round's new members, grown on demand
+    Scratch s_cq(st);                      // sparse verification: active-query index per slot
     int64_t round_cap = 0;
     Scratch s_total(st, sizeof(unsigned long long));
     Scratch s_tk(st, sizeof(unsigned long long) * (size_t)(qb * k));
@@ -1273,10 +1323,15 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
         va.rbw = (int)std::max<int64_t>(1, std::min<int64_t>(8, (120 * 1024) / per_word));
     }
     const size_t vr_smem = (size_t)va.rbw * 32 * ix.ld * 4;
-    const bool use_tc = a.verify_impl == 0 && ix.xnorm.p != nullptr;
+    // verification kernel per round: the tensor-core kernel costs a dense X.Q^T over all rows and
+    // the round's active queries whatever the candidate density; the CUDA-core row kernel reads X
+    // once and pays per candidate.  Auto (verify_impl 0) picks the cheaper by a cost model fitted
+    // on B200 at configs[1] (tc 2.5 ms per 1M rows x 1000 queries x 256 floats; rows 0.17 ms per
+    // 1M x 256 floats read + 6.3 ms per 115.7M candidates x 256 floats).
+    const bool tc_ok = a.verify_impl != 1 && a.verify_impl != 3 && ix.xnorm.p != nullptr;
     const int64_t nw4 = round_up(nwords, 4);
-    Scratch s_boff(st, sizeof(uint32_t) * (size_t)(use_tc ? 2 * qb * nw4 : qb * ceil_div(nwords, va.rbw)));
-    Scratch s_qa(st, use_tc ? sizeof(float) * (size_t)(qb * (2 * ix.ld + 1)) : 0);
+    Scratch s_boff(st, sizeof(uint32_t) * (size_t)(a.verify_impl != 1 ? 2 * qb * nw4 : qb * ceil_div(nwords, va.rbw)));
+    Scratch s_qa(st, tc_ok ? sizeof(float) * (size_t)(qb * (2 * ix.ld + 1)) : 0);
     const bool vexact = (ix.ld / 4) == 8 * vnv;
     DL_CUDA(cudaFuncSetAttribute(k_verify_rows<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)vr_smem));
     DL_CUDA(cudaFuncSetAttribute(k_verify_rows<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)vr_smem));
@@ -1347,8 +1402,8 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
             }
             tr.mark("filter (L trees)", st);
             DL_LAUNCH(k_round_offsets, 1, 1024, 0, st, cur, na, s_qs.as<QState>(), s_total.as<unsigned long long>());
+            unsigned long long tot = 0;     // new members of S over the round's queries
             {
-                unsigned long long tot = 0;
                 DL_CUDA(cudaMemcpyAsync(&tot, s_total.p, sizeof(tot), cudaMemcpyDeviceToHost, st));
                 DL_CUDA(cudaStreamSynchronize(st));
                 if ((int64_t)tot > round_cap) {
@@ -1363,18 +1418,36 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
             va.nblocks = ceil_div(nwords, va.rbw);
             va.boff = s_boff.as<uint32_t>();
             bool done_tc = false;
-            if (use_tc) {
+            // 0 = row kernel (verify_impl 1), 1 = tensor cores, 2 = sparse gather
+            int path = a.verify_impl == 3 ? 2 : tc_ok ? 1 : 0;
+            if (tc_ok && a.verify_impl == 0) {
+                const double scale = (double)n / 1e6 * (double)ix.ld / 256.0;
+                const double t_tc = 2.5 * scale * (double)round_up(na, 16) / 1000.0;
+                const double t_gather = 0.05 * (double)n / 1e6 + (double)tot * ix.ld * 4.0 / 5e9;   // ms at 5 TB/s
+                path = t_tc <= t_gather ? 1 : 2;
+            }
+            if (path >= 1) {
                 uint32_t* NB = s_boff.as<uint32_t>();
                 uint32_t* BO = NB + (int64_t)qb * nw4;
-                float* Qa = s_qa.as<float>();
-                float* Qalo = Qa + (int64_t)qb * ix.ld;
-                float* qn = Qalo + (int64_t)qb * ix.ld;
                 DL_LAUNCH(k_verify_prep, (unsigned)na, 1024, 0, st, cur, s_qs.as<QState>(), s_bm.as<uint32_t>(),
                           s_ver.as<uint32_t>(), nwords, NB, BO);
-                DL_LAUNCH(k_prep_queries, (unsigned)ceil_div(na, 8), 256, 0, st, Qb, (int64_t)ix.ld, cur, na, Qa, Qalo, qn);
-                done_tc = verify_tc(ix.Xp, n, ix.ld, Qa, Qalo, qn, na, NB, BO, nw4, ix.xnorm.as<float>(), va.cand, va.d2,
-                                    st);
-                DL_REQUIRE(done_tc, "tensor-core verification does not fit this shape");
+                if (path == 1) {
+                    float* Qa = s_qa.as<float>();
+                    float* Qalo = Qa + (int64_t)qb * ix.ld;
+                    float* qn = Qalo + (int64_t)qb * ix.ld;
+                    DL_LAUNCH(k_prep_queries, (unsigned)ceil_div(na, 8), 256, 0, st, Qb, (int64_t)ix.ld, cur, na, Qa,
+                              Qalo, qn);
+                    done_tc = verify_tc(ix.Xp, n, ix.ld, Qa, Qalo, qn, na, NB, BO, nw4, ix.xnorm.as<float>(), va.cand,
+                                        va.d2, st);
+                    DL_REQUIRE(done_tc, "tensor-core verification does not fit this shape");
+                } else if (tot > 0) {
+                    s_cq.alloc(sizeof(uint32_t) * (size_t)tot);
+                    DL_LAUNCH(k_collect_cands, (unsigned)std::min<int64_t>(ceil_div((int64_t)na * nwords, 256), 148 * 16),
+                              256, 0, st, na, NB, BO, nwords, va.cand, s_cq.as<uint32_t>());
+                    DL_LAUNCH(k_verify_gather, (unsigned)std::min<int64_t>(ceil_div((int64_t)tot * 8, 256), 148 * 32), 256,
+                              0, st, va.cand, s_cq.as<uint32_t>(), cur, ix.Xp, Qb, (int64_t)ix.ld, (int64_t)tot, va.d2);
+                }
+                done_tc = true;
             }
             if (!done_tc) {
             DL_LAUNCH(k_verify_offsets, (unsigned)na, 1024, 0, st, cur, s_qs.as<QState>(), s_bm.as<uint32_t>(),

@@ -136,7 +136,7 @@ def _dist_match(ig, dg, io, do):
                 assert abs(d - m[i]) <= 1e-4 * max(1e-30, m[i]) + 1e-30
 
 
-@pytest.mark.parametrize("vimpl", [0, 1])     # 0 = tcgen05 verification, 1 = CUDA cores
+@pytest.mark.parametrize("vimpl", [0, 1, 2, 3])     # 0 = auto, 1 = CUDA-core rows, 2 = tcgen05, 3 = gather
 @pytest.mark.parametrize("mode", [P.MODE_CELL, P.MODE_RELAXED])
 def test_query_parity_tiny(gpu_tiny, tiny_oracle, tiny, tiny_rmin, mode, vimpl):
     c = tiny["cfg"]
@@ -309,8 +309,10 @@ def test_verify_tc_vs_simt_and_oracle(n, d, nq, k):
     g = P.detlsh_build(X, 4, 16, 256, 3)
     o = O.Index(X, 4, 16, 256, 3)
     rmin = 0.2 * o.estimate_rmin(Q[:8], k, 1.5, 0.1)       # start low: several rounds
-    it, dt, st = g.query(Q, k, 1.5, rmin, 0.1, opts=P.default_opts(verify_impl=0), stats=True)
+    it, dt, st = g.query(Q, k, 1.5, rmin, 0.1, opts=P.default_opts(verify_impl=2), stats=True)
     iS, dS, sS = g.query(Q, k, 1.5, rmin, 0.1, opts=P.default_opts(verify_impl=1), stats=True)
+    iG, dG = g.query(Q, k, 1.5, rmin, 0.1, opts=P.default_opts(verify_impl=3))
+    assert np.array_equal(iG, iS) and np.array_equal(dG, dS)    # both direct fp32 sums
     assert _recall(it, iS) >= 0.995
     assert np.mean(st["n_cand"] == sS["n_cand"]) >= 0.95
     same = it == iS
@@ -396,7 +398,7 @@ def test_save_load_roundtrip(tmp_path, tiny, tiny_rmin):
         P.detlsh_load(str(trunc))
 
 
-@pytest.mark.parametrize("vimpl", [0, 1])
+@pytest.mark.parametrize("vimpl", [1, 2])
 def test_query_parity_exact_mode(tiny_oracle, tiny, tiny_rmin, vimpl):
     """f4 EXACT mode (Alg. 3 as written: true projected distance <= eps r) against the
     oracle's EXACT range queries; the index keeps its fp32 projections.  Without them EXACT is

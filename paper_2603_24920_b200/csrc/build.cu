@@ -564,6 +564,24 @@ __global__ void k_tile_flags(const uint32_t* __restrict__ leaf_off, int64_t nl, 
     }
 }
 
+// Box of each query tile: per dim the smallest lo and largest hi over its leaves (the union's
+// bounding box, so its lower bound never exceeds a member leaf's -- the filter skips whole tiles).
+__global__ void k_tile_boxes(const uint32_t* __restrict__ tile_leaf, int64_t ntiles, int K, const uint8_t* __restrict__ lo,
+                             const uint8_t* __restrict__ hi, uint8_t* __restrict__ tlo, uint8_t* __restrict__ thi) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < ntiles * K;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t t = i / K;
+        const int j = (int)(i - t * K);
+        int a = 255, b = 0;
+        for (uint32_t l = tile_leaf[t]; l < tile_leaf[t + 1]; ++l) {
+            a = min(a, (int)lo[(int64_t)l * K + j]);
+            b = max(b, (int)hi[(int64_t)l * K + j]);
+        }
+        tlo[i] = (uint8_t)a;
+        thi[i] = (uint8_t)b;
+    }
+}
+
 __global__ void k_tile_write(const uint32_t* __restrict__ flags, const uint32_t* __restrict__ idx, int64_t nl,
                              uint32_t* __restrict__ tile_leaf) {
     for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < nl;
@@ -804,6 +822,10 @@ static bool build_trees_try(Index& ix, const uint8_t* d_EP, int64_t leaf_factor,
         Scratch s_tb(st, sizeof(unsigned long long) * (size_t)(L + 1));
         DL_LAUNCH(k_tree_tiles, 1, 64, 0, st, tidx, s_begin.as<unsigned long long>(), (int)L, (uint32_t)ntiles,
                   s_tb.as<unsigned long long>());
+        ix.tile_lo.alloc((size_t)ntiles * K, st);
+        ix.tile_hi.alloc((size_t)ntiles * K, st);
+        DL_LAUNCH(k_tile_boxes, grid_for(ntiles * K, 256), 256, 0, st, ix.tile_leaf.as<uint32_t>(), ntiles, K,
+                  ix.leaf_lo.as<uint8_t>(), ix.leaf_hi.as<uint8_t>(), ix.tile_lo.as<uint8_t>(), ix.tile_hi.as<uint8_t>());
         ix.point_tile_leaf.alloc(sizeof(uint16_t) * (size_t)total, st);
         DL_LAUNCH(k_point_tile_leaf, grid_for(nl, 256), 256, 0, st, ix.leaf_off.as<uint32_t>(), ix.tile_leaf.as<uint32_t>(),
                   ntiles, nl, ix.point_tile_leaf.as<uint16_t>());

@@ -120,6 +120,8 @@ struct RFArgs {
     const uint32_t* leaf_off;   // global positions
     const uint8_t* lo;          // [nl_total][K]
     const uint8_t* hi;
+    const uint8_t* tile_lo;     // [ntiles][K] tile bounding boxes
+    const uint8_t* tile_hi;
     const uint32_t* tile_leaf;  // [ntiles+1]
     int64_t tile_begin, tile_end;
     int64_t pos_base;           // t * n
@@ -146,7 +148,7 @@ __global__ void __launch_bounds__(RF_THREADS, 3) k_range_filter(RFArgs a) {
     const int N_r = NRT ? NRT : a.N_r;
     uint4* s_qe = reinterpret_cast<uint4*>(smem);                                       // [K][N_r] x 16 B
     __shared__ int s_q[G];
-    __shared__ uint8_t s_sx[G][32];
+    __shared__ __align__(16) uint8_t s_sx[G][32];
     __shared__ float s_qp[G][32];                                                        // EXACT: q'_t
     __shared__ unsigned int s_ctr[G][4];
     __shared__ uint32_t s_lq[RF_THREADS / 32][kTileLeaves];                             // per warp: leaf masks
@@ -223,39 +225,73 @@ __global__ void __launch_bounds__(RF_THREADS, 3) k_range_filter(RFArgs a) {
         const uint32_t lb = a.tile_leaf[tile], le = a.tile_leaf[tile + 1];
         const int nlt = (int)(le - lb);
         const uint32_t P0 = a.leaf_off[lb], P1 = a.leaf_off[le];
-        // leaf lower bounds (Alg. 3 pruning, Fig. dist): lane = leaf, quantised, all G queries
+        // tile screen: quantised lower bound of the tile's bounding box (lane g = query g); a
+        // tile no query can reach is skipped whole (every leaf LB >= the tile's LB)
+        uint32_t tm;
+        {
+            bool pass = false;
+            if (lane < G && ((amask >> lane) & 1)) {
+                uint32_t acc = 0;
+                if (KT == 16) {
+                    const uint4 tl4 = *reinterpret_cast<const uint4*>(a.tile_lo + tile * 16);
+                    const uint4 th4 = *reinterpret_cast<const uint4*>(a.tile_hi + tile * 16);
+                    const uint4 sx4 = *reinterpret_cast<const uint4*>(&s_sx[lane][0]);
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) {
+                        const int sh = 8 * (j & 3);
+                        const uint32_t wl = (j >> 2) == 0 ? tl4.x : (j >> 2) == 1 ? tl4.y : (j >> 2) == 2 ? tl4.z : tl4.w;
+                        const uint32_t wh = (j >> 2) == 0 ? th4.x : (j >> 2) == 1 ? th4.y : (j >> 2) == 2 ? th4.z : th4.w;
+                        const uint32_t ws = (j >> 2) == 0 ? sx4.x : (j >> 2) == 1 ? sx4.y : (j >> 2) == 2 ? sx4.z : sx4.w;
+                        const int c = min(max((int)((ws >> sh) & 255u), (int)((wl >> sh) & 255u)), (int)((wh >> sh) & 255u));
+                        acc += G == 8 ? (uint32_t)s_h[(j * N_r + c) * 8 + lane] : (uint32_t)s_b[(j * N_r + c) * 16 + lane];
+                    }
+                } else {
+                    const uint8_t* tl = a.tile_lo + tile * K;
+                    const uint8_t* th = a.tile_hi + tile * K;
+                    for (int j = 0; j < K; ++j) {
+                        const int e = (j * N_r + min(max((int)s_sx[lane][j], (int)tl[j]), (int)th[j])) * 16;
+                        acc += G == 8 ? (uint32_t)s_h[e / 2 + lane] : (uint32_t)s_b[e + lane];
+                    }
+                }
+                pass = acc <= QT;
+            }
+            tm = __ballot_sync(0xffffffffu, pass);
+        }
+        if (tm == 0) continue;
+        // leaf lower bounds (Alg. 3 pruning, Fig. dist): lane = leaf, quantised, one query of the
+        // tile's set at a time (warp-uniform loop)
         if (lane < nlt) {
             const int64_t l = (int64_t)lb + lane;
-            uint32_t lacc[G];
-#pragma unroll
-            for (int g = 0; g < G; ++g) lacc[g] = 0;
-            uint4 lo4 = make_uint4(0, 0, 0, 0), hi4 = lo4;
-            if (KT == 16) {
-                lo4 = *reinterpret_cast<const uint4*>(a.lo + l * 16);
-                hi4 = *reinterpret_cast<const uint4*>(a.hi + l * 16);
-            }
-#pragma unroll
-            for (int j = 0; j < K; ++j) {
-                int lo_, hi_;
-                if (KT == 16) {
-                    const uint32_t wl = (j >> 2) == 0 ? lo4.x : (j >> 2) == 1 ? lo4.y : (j >> 2) == 2 ? lo4.z : lo4.w;
-                    const uint32_t wh = (j >> 2) == 0 ? hi4.x : (j >> 2) == 1 ? hi4.y : (j >> 2) == 2 ? hi4.z : hi4.w;
-                    lo_ = (int)((wl >> (8 * (j & 3))) & 255u);
-                    hi_ = (int)((wh >> (8 * (j & 3))) & 255u);
-                } else {
-                    lo_ = a.lo[l * K + j];
-                    hi_ = a.hi[l * K + j];
-                }
-#pragma unroll
-                for (int g = 0; g < G; ++g) {
-                    const int e = (j * N_r + min(max((int)s_sx[g][j], lo_), hi_)) * 16;
-                    lacc[g] += G == 8 ? (uint32_t)s_h[e / 2 + g] : (uint32_t)s_b[e + g];
-                }
-            }
             uint32_t m = 0;
+            if (KT == 16) {
+                const uint4 lo4 = *reinterpret_cast<const uint4*>(a.lo + l * 16);
+                const uint4 hi4 = *reinterpret_cast<const uint4*>(a.hi + l * 16);
+                for (uint32_t mm = tm; mm; mm &= mm - 1) {
+                    const int g = __ffs(mm) - 1;
+                    const uint4 sx4 = *reinterpret_cast<const uint4*>(&s_sx[g][0]);
+                    uint32_t acc = 0;
 #pragma unroll
-            for (int g = 0; g < G; ++g)
-                if (lacc[g] <= QT && ((amask >> g) & 1)) m |= 1u << g;
+                    for (int j = 0; j < 16; ++j) {
+                        const int sh = 8 * (j & 3);
+                        const uint32_t wl = (j >> 2) == 0 ? lo4.x : (j >> 2) == 1 ? lo4.y : (j >> 2) == 2 ? lo4.z : lo4.w;
+                        const uint32_t wh = (j >> 2) == 0 ? hi4.x : (j >> 2) == 1 ? hi4.y : (j >> 2) == 2 ? hi4.z : hi4.w;
+                        const uint32_t ws = (j >> 2) == 0 ? sx4.x : (j >> 2) == 1 ? sx4.y : (j >> 2) == 2 ? sx4.z : sx4.w;
+                        const int c = min(max((int)((ws >> sh) & 255u), (int)((wl >> sh) & 255u)), (int)((wh >> sh) & 255u));
+                        acc += G == 8 ? (uint32_t)s_h[(j * N_r + c) * 8 + g] : (uint32_t)s_b[(j * N_r + c) * 16 + g];
+                    }
+                    if (acc <= QT) m |= 1u << g;
+                }
+            } else {
+                for (uint32_t mm = tm; mm; mm &= mm - 1) {
+                    const int g = __ffs(mm) - 1;
+                    uint32_t acc = 0;
+                    for (int j = 0; j < K; ++j) {
+                        const int e = (j * N_r + min(max((int)s_sx[g][j], (int)a.lo[l * K + j]), (int)a.hi[l * K + j])) * 16;
+                        acc += G == 8 ? (uint32_t)s_h[e / 2 + g] : (uint32_t)s_b[e + g];
+                    }
+                    if (acc <= QT) m |= 1u << g;
+                }
+            }
             if (a.mode == DETLSH_MODE_RELAXED) {
                 // RELAXED (Sec. 6.2.2(1)): the leaf decision is final, so decide it in fp32
                 uint32_t conf = 0, mm = m;
@@ -271,7 +307,7 @@ __global__ void __launch_bounds__(RF_THREADS, 3) k_range_filter(RFArgs a) {
                 m = conf;
             }
             lq[lane] = m;
-            c_lt += __popc(amask);
+            c_lt += __popc(tm);
             c_lp += __popc(m);
         }
         __syncwarp();
@@ -1294,6 +1330,8 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
     ra.lo = ix.leaf_lo.as<uint8_t>();
     ra.hi = ix.leaf_hi.as<uint8_t>();
     ra.tile_leaf = ix.tile_leaf.as<uint32_t>();
+    ra.tile_lo = ix.tile_lo.as<uint8_t>();
+    ra.tile_hi = ix.tile_hi.as<uint8_t>();
     ra.lut = s_lut.as<float>();
     ra.qlut = s_qlut.as<uint16_t>();
     ra.sx = s_sx.as<uint8_t>();

@@ -8,7 +8,8 @@ cid = int(os.environ.get("CFG", "2"))
 D = datagen.generate(cid)
 c = D['cfg']
 import json
-rmin = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "bench_configs.json")))[str(cid)]["r_min"]
+_e = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "bench_configs.json")))[str(cid)]
+rmin = _e.get("r_bench", _e["r_min"])
 Xd = torch.from_numpy(D['X']).cuda(); Qd = torch.from_numpy(D['Q']).cuda()
 o = P.default_opts(borrow_data=1)
 g = P.detlsh_build(Xd, c.L, c.K, c.N_r, c.index_seed, opts=o)

@@ -15,6 +15,7 @@
 //                 bitonic sort; then the radius test k-th d2 <= (c r)^2 (line 9, AMB-18).
 //  k_finalize     ids (global) and sqrt(d2), ascending by (dist, id) (AMB-21, AMB-28).
 #include <algorithm>
+#include <cstdlib>
 #include <mutex>
 #include <cmath>
 #include <cstring>
@@ -137,6 +138,7 @@ struct RFArgs {
     int64_t nwords;
     float rho2;
     int t, L, K, N_r, mode;
+    int pq_cost;                // per-query path cost per 32-point step, relative to 170 per SIMD chunk
     unsigned long long* ctr;    // [Qb][4] filter counters
 };
 
@@ -153,6 +155,8 @@ __global__ void __launch_bounds__(RF_THREADS, 3) k_range_filter(RFArgs a) {
     __shared__ unsigned int s_ctr[G][4];
     __shared__ uint32_t s_lq[RF_THREADS / 32][kTileLeaves];                             // per warp: leaf masks
     __shared__ uint32_t s_bq[RF_THREADS / 32][RF_BQ];                                   // per warp: band queue
+    __shared__ uint32_t s_pre[RF_THREADS / 32][32];                                     // per warp: packed-point prefix
+    __shared__ uint32_t s_off[RF_THREADS / 32][32];                                     // per warp: leaf offsets
     __shared__ int s_active_mask;
     __shared__ unsigned int s_next;
 
@@ -345,115 +349,190 @@ __global__ void __launch_bounds__(RF_THREADS, 3) k_range_filter(RFArgs a) {
             }
             qn_ -= cnt;
         };
-        // software pipeline: the next chunk's leaf slots, codes and ids load while this one is screened
-        uint32_t nx_ptl = 0, nx_id = 0;
-        uint4 nx_c4 = make_uint4(0, 0, 0, 0);
-        auto load_chunk = [&](uint32_t pb_) {
-            const uint32_t p_ = pb_ + lane;
-            if (p_ < P1) {
-                const int64_t pos_ = (int64_t)p_ - a.pos_base;
-                nx_ptl = a.ptl[pos_];
-                nx_id = a.perm[pos_];
-                if (KT == 16) nx_c4 = *reinterpret_cast<const uint4*>(a.tcodes + pos_ * 16);
+        // Two ways to screen the points of the reachable leaves:
+        //  SIMD  every 32-point chunk of the tile, all G queries at once (16-byte loads serve G
+        //        queries) -- best when each point is needed by many of the group's queries;
+        //  per-query  for each query, only the points of ITS reachable leaves, packed 32 to a
+        //        step -- best at small radii, where a point is needed by ~2 of 16 queries.
+        // Chosen per tile from the instruction costs (~170 per SIMD chunk, ~120 per query step,
+        // measured on B200: 163K -> 166K q/s at the bench point).
+        bool use_pq = false;
+        uint32_t my_off = P1, my_sz = 0;
+        if (KT == 16 && a.mode != DETLSH_MODE_RELAXED) {
+            if (lane < nlt) {
+                my_off = a.leaf_off[lb + lane];
+                my_sz = a.leaf_off[lb + lane + 1] - my_off;
             }
-        };
-        load_chunk(P0);
-        for (uint32_t pb = P0; pb < P1; pb += 32) {
-            const uint32_t p = pb + lane;
-            const int64_t pos = (int64_t)p - a.pos_base;
-            const uint32_t cur_ptl = nx_ptl, cur_id = nx_id;
-            const uint4 c4 = nx_c4;
-            if (pb + 32 < P1) load_chunk(pb + 32);
-            uint32_t m = 0;
-            if (p < P1) m = lq[cur_ptl];
-            if (__ballot_sync(0xffffffffu, m != 0) == 0) continue;    // whole warp pruned by leaf LBs
-            c_pt += __popc(m);
-            uint32_t certain = m, band = 0;
-            if (m && a.mode != DETLSH_MODE_RELAXED) {
-                uint32_t ok = 0, sure = 0;
-                if (KT == 16) {
-                    uint32_t acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+            uint32_t w_ = lane < nlt ? (uint32_t)__popc(lq[lane]) * my_sz : 0u;
+            for (int o = 16; o > 0; o >>= 1) w_ += __shfl_xor_sync(0xffffffffu, w_, o);
+            use_pq = (unsigned long long)a.pq_cost * w_ < 170ull * (P1 - P0);
+        }
+        if (use_pq) {
+            uint32_t* pre = s_pre[warp];
+            uint32_t* offs = s_off[warp];
+            for (uint32_t mm = tm; mm; mm &= mm - 1) {
+                const int g = __ffs(mm) - 1;
+                const bool pl = lane < nlt && ((lq[lane] >> g) & 1u);
+                const uint32_t sz = pl ? my_sz : 0u;
+                uint32_t incl = sz;
 #pragma unroll
-                    for (int w = 0; w < 4; ++w) {
-                        const uint32_t word = w == 0 ? c4.x : w == 1 ? c4.y : w == 2 ? c4.z : c4.w;
-                        const uint4* row = s_qe + (w * 4) * N_r;
-                        if (G == 8) {
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+                    if (lane >= o) incl += y;
+                }
+                const uint32_t T = __shfl_sync(0xffffffffu, incl, 31);
+                if (T == 0) continue;
+                pre[lane] = incl - sz;
+                offs[lane] = my_off;
+                __syncwarp();
+                for (uint32_t c0 = 0; c0 < T; c0 += 32) {
+                    const uint32_t i = c0 + lane;
+                    bool band = false;
+                    uint32_t p = P0;
+                    if (i < T) {
+                        int l = 0;      // the leaf holding packed point i: last l with pre[l] <= i
 #pragma unroll
-                            for (int b = 0; b < 4; ++b) {
-                                const uint4 v = row[b * N_r + ((word >> (8 * b)) & 255u)];
-                                acc[0] += v.x; acc[1] += v.y; acc[2] += v.z; acc[3] += v.w;
-                            }
+                        for (int st = 16; st > 0; st >>= 1)
+                            if (pre[l + st] <= i) l += st;
+                        p = offs[l] + (i - pre[l]);
+                        const int64_t pos = (int64_t)p - a.pos_base;
+                        const uint4 c4 = *reinterpret_cast<const uint4*>(a.tcodes + pos * 16);
+                        uint32_t acc = 0;
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) {
+                            const uint32_t word = (j >> 2) == 0 ? c4.x : (j >> 2) == 1 ? c4.y : (j >> 2) == 2 ? c4.z : c4.w;
+                            const uint32_t code = (word >> (8 * (j & 3))) & 255u;
+                            acc += G == 8 ? (uint32_t)s_h[(j * N_r + code) * 8 + g] : (uint32_t)s_b[(j * N_r + code) * 16 + g];
+                        }
+                        ++c_pt;
+                        const bool ok = acc <= QT, sure = acc + 17 <= QT;
+                        if (a.mode == DETLSH_MODE_CELL && sure) {
+                            ++c_pp;
+                            const uint32_t id = a.perm[pos];
+                            atomicOr(a.bitmap + (int64_t)s_q[g] * a.nwords + (id >> 5), 1u << (id & 31));  // RED.OR
                         } else {
-                            // 7-bit terms (CAP 127): two dims add inside the 8-bit lanes without
-                            // carry (<= 254); each pair sum is then widened into 16-bit lanes
-                            // (g0,g2) by a mask and (g1,g3) by a byte permute.
-                            const uint4 va = row[0 * N_r + (word & 255u)];
-                            const uint4 vb = row[1 * N_r + ((word >> 8) & 255u)];
-                            const uint4 vc = row[2 * N_r + ((word >> 16) & 255u)];
-                            const uint4 vd = row[3 * N_r + (word >> 24)];
-                            const uint32_t p2[4] = {va.x + vb.x, va.y + vb.y, va.z + vb.z, va.w + vb.w};
-                            const uint32_t r2[4] = {vc.x + vd.x, vc.y + vd.y, vc.z + vd.z, vc.w + vd.w};
-#pragma unroll
-                            for (int i = 0; i < 4; ++i) {
-                                acc[2 * i] += (p2[i] & 0x00FF00FFu) + (r2[i] & 0x00FF00FFu);
-                                acc[2 * i + 1] += __byte_perm(p2[i], 0u, 0x4341) + __byte_perm(r2[i], 0u, 0x4341);
-                            }
+                            band = ok;      // CELL: inside the band; EXACT: every survivor
                         }
                     }
-#pragma unroll
-                    for (int g = 0; g < G; ++g) {
-                        const uint32_t sg = G == 8 ? (acc[g >> 1] >> (16 * (g & 1))) & 0xFFFFu
-                                                   : (acc[2 * (g >> 2) + (g & 1)] >> (16 * ((g >> 1) & 1))) & 0xFFFFu;
-                        ok |= (sg <= QT ? 1u : 0u) << g;
-                        sure |= (sg + 17 <= QT ? 1u : 0u) << g;
-                    }
-                } else {
-                    uint32_t acc[G];
-#pragma unroll
-                    for (int g = 0; g < G; ++g) acc[g] = 0;
-                    for (int j = 0; j < K; ++j) {
-                        const int e = (j * N_r + a.tcodes[pos * K + j]) * 16;
-#pragma unroll
-                        for (int g = 0; g < G; ++g) acc[g] += G == 8 ? (uint32_t)s_h[e / 2 + g] : (uint32_t)s_b[e + g];
-                    }
-#pragma unroll
-                    for (int g = 0; g < G; ++g) {
-                        ok |= (acc[g] <= QT ? 1u : 0u) << g;
-                        sure |= (acc[g] + 17 <= QT ? 1u : 0u) << g;
-                    }
-                }
-                if (a.mode == DETLSH_MODE_CELL) {
-                    certain = m & sure;
-                    band = m & ok & ~sure;
-                } else {       // EXACT: the cell bound only rejects; every survivor gets its true distance
-                    certain = 0;
-                    band = m & ok;
+                    const uint32_t bal = __ballot_sync(0xffffffffu, band);
+                    if (band) bq[qn_ + __popc(bal & lanemask_lt())] = ((p - P0) << 4) | (uint32_t)g;
+                    qn_ += __popc(bal);
+                    __syncwarp();
+                    if (qn_ >= 32) flush(32);
+                    __syncwarp();
                 }
             }
-            if (certain) {
-                c_pp += __popc(certain);
-                const uint32_t id = cur_id;
-                uint32_t c_ = certain;
-                while (c_) {
-                    const int g = __ffs(c_) - 1;
-                    c_ &= c_ - 1;
-                    atomicOr(a.bitmap + (int64_t)s_q[g] * a.nwords + (id >> 5), 1u << (id & 31));  // RED.OR
+        } else {
+        // software pipeline: the next chunk's leaf slots, codes and ids load while this one is screened
+            uint32_t nx_ptl = 0, nx_id = 0;
+            uint4 nx_c4 = make_uint4(0, 0, 0, 0);
+            auto load_chunk = [&](uint32_t pb_) {
+                const uint32_t p_ = pb_ + lane;
+                if (p_ < P1) {
+                    const int64_t pos_ = (int64_t)p_ - a.pos_base;
+                    nx_ptl = a.ptl[pos_];
+                    nx_id = a.perm[pos_];
+                    if (KT == 16) nx_c4 = *reinterpret_cast<const uint4*>(a.tcodes + pos_ * 16);
                 }
-            }
-            // queue the band pairs (point in tile << 4 | query slot) for the warp-wide fp32 pass:
-            // one pair per lane per step, flushed 32 at a time
-            while (__any_sync(0xffffffffu, band != 0)) {
-                const bool has = band != 0;
-                const uint32_t bal = __ballot_sync(0xffffffffu, has);
-                if (has) {
-                    const int g = __ffs(band) - 1;
-                    band &= band - 1;
-                    bq[qn_ + __popc(bal & lanemask_lt())] = ((p - P0) << 4) | (uint32_t)g;
+            };
+            load_chunk(P0);
+            for (uint32_t pb = P0; pb < P1; pb += 32) {
+                const uint32_t p = pb + lane;
+                const int64_t pos = (int64_t)p - a.pos_base;
+                const uint32_t cur_ptl = nx_ptl, cur_id = nx_id;
+                const uint4 c4 = nx_c4;
+                if (pb + 32 < P1) load_chunk(pb + 32);
+                uint32_t m = 0;
+                if (p < P1) m = lq[cur_ptl];
+                if (__ballot_sync(0xffffffffu, m != 0) == 0) continue;    // whole warp pruned by leaf LBs
+                c_pt += __popc(m);
+                uint32_t certain = m, band = 0;
+                if (m && a.mode != DETLSH_MODE_RELAXED) {
+                    uint32_t ok = 0, sure = 0;
+                    if (KT == 16) {
+                        uint32_t acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+                        for (int w = 0; w < 4; ++w) {
+                            const uint32_t word = w == 0 ? c4.x : w == 1 ? c4.y : w == 2 ? c4.z : c4.w;
+                            const uint4* row = s_qe + (w * 4) * N_r;
+                            if (G == 8) {
+#pragma unroll
+                                for (int b = 0; b < 4; ++b) {
+                                    const uint4 v = row[b * N_r + ((word >> (8 * b)) & 255u)];
+                                    acc[0] += v.x; acc[1] += v.y; acc[2] += v.z; acc[3] += v.w;
+                                }
+                            } else {
+                                // 7-bit terms (CAP 127): two dims add inside the 8-bit lanes without
+                                // carry (<= 254); each pair sum is then widened into 16-bit lanes
+                                // (g0,g2) by a mask and (g1,g3) by a byte permute.
+                                const uint4 va = row[0 * N_r + (word & 255u)];
+                                const uint4 vb = row[1 * N_r + ((word >> 8) & 255u)];
+                                const uint4 vc = row[2 * N_r + ((word >> 16) & 255u)];
+                                const uint4 vd = row[3 * N_r + (word >> 24)];
+                                const uint32_t p2[4] = {va.x + vb.x, va.y + vb.y, va.z + vb.z, va.w + vb.w};
+                                const uint32_t r2[4] = {vc.x + vd.x, vc.y + vd.y, vc.z + vd.z, vc.w + vd.w};
+#pragma unroll
+                                for (int i = 0; i < 4; ++i) {
+                                    acc[2 * i] += (p2[i] & 0x00FF00FFu) + (r2[i] & 0x00FF00FFu);
+                                    acc[2 * i + 1] += __byte_perm(p2[i], 0u, 0x4341) + __byte_perm(r2[i], 0u, 0x4341);
+                                }
+                            }
+                        }
+#pragma unroll
+                        for (int g = 0; g < G; ++g) {
+                            const uint32_t sg = G == 8 ? (acc[g >> 1] >> (16 * (g & 1))) & 0xFFFFu
+                                                       : (acc[2 * (g >> 2) + (g & 1)] >> (16 * ((g >> 1) & 1))) & 0xFFFFu;
+                            ok |= (sg <= QT ? 1u : 0u) << g;
+                            sure |= (sg + 17 <= QT ? 1u : 0u) << g;
+                        }
+                    } else {
+                        uint32_t acc[G];
+#pragma unroll
+                        for (int g = 0; g < G; ++g) acc[g] = 0;
+                        for (int j = 0; j < K; ++j) {
+                            const int e = (j * N_r + a.tcodes[pos * K + j]) * 16;
+#pragma unroll
+                            for (int g = 0; g < G; ++g) acc[g] += G == 8 ? (uint32_t)s_h[e / 2 + g] : (uint32_t)s_b[e + g];
+                        }
+#pragma unroll
+                        for (int g = 0; g < G; ++g) {
+                            ok |= (acc[g] <= QT ? 1u : 0u) << g;
+                            sure |= (acc[g] + 17 <= QT ? 1u : 0u) << g;
+                        }
+                    }
+                    if (a.mode == DETLSH_MODE_CELL) {
+                        certain = m & sure;
+                        band = m & ok & ~sure;
+                    } else {       // EXACT: the cell bound only rejects; every survivor gets its true distance
+                        certain = 0;
+                        band = m & ok;
+                    }
                 }
-                qn_ += __popc(bal);
-                __syncwarp();
-                if (qn_ >= 32) flush(32);
-                __syncwarp();
+                if (certain) {
+                    c_pp += __popc(certain);
+                    const uint32_t id = cur_id;
+                    uint32_t c_ = certain;
+                    while (c_) {
+                        const int g = __ffs(c_) - 1;
+                        c_ &= c_ - 1;
+                        atomicOr(a.bitmap + (int64_t)s_q[g] * a.nwords + (id >> 5), 1u << (id & 31));  // RED.OR
+                    }
+                }
+                // queue the band pairs (point in tile << 4 | query slot) for the warp-wide fp32 pass:
+                // one pair per lane per step, flushed 32 at a time
+                while (__any_sync(0xffffffffu, band != 0)) {
+                    const bool has = band != 0;
+                    const uint32_t bal = __ballot_sync(0xffffffffu, has);
+                    if (has) {
+                        const int g = __ffs(band) - 1;
+                        band &= band - 1;
+                        bq[qn_ + __popc(bal & lanemask_lt())] = ((p - P0) << 4) | (uint32_t)g;
+                    }
+                    qn_ += __popc(bal);
+                    __syncwarp();
+                    if (qn_ >= 32) flush(32);
+                    __syncwarp();
+                }
             }
         }
         if (qn_) flush(qn_);
@@ -1345,6 +1424,10 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
     ra.K = ix.K;
     ra.N_r = ix.N_r;
     ra.mode = a.mode;
+    {
+        static const int pq = std::getenv("DETLSH_PQ_COST") ? std::atoi(std::getenv("DETLSH_PQ_COST")) : 120;
+        ra.pq_cost = pq;
+    }
     const int nv = (int)ceil_div(ix.ld / 4, 8);      // float4 per lane (8 lanes per row)
     const int vnv = nv <= 1 ? 1 : nv <= 2 ? 2 : nv <= 4 ? 4 : nv <= 8 ? 8 : 0;
     VRArgs va;

@@ -94,6 +94,32 @@ __global__ void k_build_qlut(const float* __restrict__ lut, const int* __restric
     }
 }
 
+// ---- per tree: each 16-query group's quantised table interleaved once (entry (j, s) = the
+//      group's 16 8-bit terms), copied by the group's filter CTAs instead of each CTA gathering
+//      16 queries' tables itself.  Inactive slots get the cap (never pass).
+__global__ void k_group_table(const int* __restrict__ act, int na, const QState* __restrict__ qs,
+                              const uint16_t* __restrict__ qlut, int64_t per_q, int t, int KN, uint32_t cap,
+                              uint4* __restrict__ gtab) {
+    const int64_t groups = (na + 15) / 16;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < groups * KN;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t grp = i / KN;
+        const int e = (int)(i - grp * KN);
+        uint32_t w[4] = {0, 0, 0, 0};
+#pragma unroll
+        for (int g = 0; g < 16; ++g) {
+            const int64_t gi = grp * 16 + g;
+            uint32_t v = cap;
+            if (gi < na) {
+                const int q = act[gi];
+                if (qs[q].status == ST_ACTIVE) v = qlut[(int64_t)q * per_q + (int64_t)t * KN + e];
+            }
+            w[g >> 2] |= v << (8 * (g & 3));
+        }
+        gtab[i] = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+}
+
 // ---- range filter of one tree (Alg. 3 at radius eps*r, Alg. 5 lines 5-6), batched:
 //      CTA = group of G active queries x stripe of tiles; a warp owns a tile of <= 32 leaves.
 //      Leaf lower bounds (lane = leaf) prune; for the points of qualifying leaves the cell
@@ -128,6 +154,7 @@ struct RFArgs {
     int64_t pos_base;           // t * n
     const float* lut;           // [Qb][L][K][N_r] exact
     const uint16_t* qlut;       // [Qb][L][K][N_r] quantised lower bounds (this round)
+    const uint4* gtab;          // [groups][K][N_r] the groups' interleaved 8-bit tables (this tree), or null
     const uint8_t* sx;          // [Qb][L][K]
     const float* proj;          // EXACT: data-order projections [n][LK]
     const float* qp;            // EXACT: projected batch queries [Qb][LK]
@@ -186,15 +213,20 @@ __global__ void __launch_bounds__(RF_THREADS, 3) k_range_filter(RFArgs a) {
 #pragma unroll
         for (int g = 0; g < G; ++g)
             src[g] = s_q[g] >= 0 ? a.qlut + (int64_t)s_q[g] * per_q + (int64_t)a.t * K * N_r : nullptr;
-        for (int i = threadIdx.x; i < K * N_r; i += RF_THREADS) {
-            uint32_t w[4] = {0, 0, 0, 0};
+        if (a.gtab) {   // the group's table, interleaved once per tree by k_group_table: plain copy
+            const uint4* gt = a.gtab + (int64_t)blockIdx.x * K * N_r;
+            for (int i = threadIdx.x; i < K * N_r; i += RF_THREADS) s_qe[i] = gt[i];
+        } else {
+            for (int i = threadIdx.x; i < K * N_r; i += RF_THREADS) {
+                uint32_t w[4] = {0, 0, 0, 0};
 #pragma unroll
-            for (int g = 0; g < G; ++g) {
-                const uint32_t v = src[g] ? src[g][i] : CAP;                           // inactive: never passes
-                if (G == 8) w[g >> 1] |= v << (16 * (g & 1));
-                else w[g >> 2] |= v << (8 * (g & 3));
+                for (int g = 0; g < G; ++g) {
+                    const uint32_t v = src[g] ? src[g][i] : CAP;                       // inactive: never passes
+                    if (G == 8) w[g >> 1] |= v << (16 * (g & 1));
+                    else w[g >> 2] |= v << (8 * (g & 3));
+                }
+                s_qe[i] = make_uint4(w[0], w[1], w[2], w[3]);
             }
-            s_qe[i] = make_uint4(w[0], w[1], w[2], w[3]);
         }
         if (threadIdx.x < K) {
 #pragma unroll
@@ -1401,10 +1433,12 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
     Scratch s_sx(st, (size_t)(qb * LK));
     const size_t rf_smem = (size_t)16 * ix.K * ix.N_r;
     Scratch s_qlut(st, sizeof(uint16_t) * (size_t)(qb * LK * ix.N_r));
+    Scratch s_gtab(st, (size_t)16 * ceil_div(qb, RF_G) * ix.K * ix.N_r);
     auto k_range_filter_sel = (ix.K == 16 && ix.N_r == 256) ? k_range_filter<16 COMMA 256 COMMA RF_G>
                                                             : k_range_filter<0 COMMA 0 COMMA RF_G>;
     DL_CUDA(cudaFuncSetAttribute(k_range_filter_sel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rf_smem));
     RFArgs ra;
+    ra.gtab = nullptr;
     ra.leaf_off = ix.leaf_off.as<uint32_t>();
     ra.lo = ix.leaf_lo.as<uint8_t>();
     ra.hi = ix.leaf_hi.as<uint8_t>();
@@ -1504,6 +1538,13 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
                 ra.rho2 = rho2;
                 ra.t = t;
                 const int groups = (int)ceil_div(nf, RF_G);
+                if (RF_G == 16) {
+                    uint4* gt = s_gtab.as<uint4>();
+                    DL_LAUNCH(k_group_table, (unsigned)std::min<int64_t>(ceil_div((int64_t)groups * ix.K * ix.N_r, 256), 148 * 16),
+                              256, 0, st, fa, nf, s_qs.as<QState>(), s_qlut.as<uint16_t>(), LK * ix.N_r, t,
+                              ix.K * ix.N_r, (uint32_t)QuantSpec<RF_G>::CAP, gt);
+                    ra.gtab = gt;
+                }
                 const int64_t ntiles = ra.tile_end - ra.tile_begin;
                 // about 4 waves of 3 resident CTAs per SM in all (tail <= a quarter wave)
                 const int stripes = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(ntiles, RF_THREADS / 32),

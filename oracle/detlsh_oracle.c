@@ -727,6 +727,56 @@ static void rq_node(rq_state* st, int32_t ni) {
         if (v <= st->rho2) st->out[st->cnt++] = id;
     }
 }
+/* ---- §6.2.2(2): the qualifying leaves of one tree with their lower bounds, so Alg. 5   */
+/* can take them in ascending (LB, leaf) order and stop at the budget.  "leaf" = the leaf's      */
+/* position in the tree's canonical order (DFS, 0-child first, first-layer keys ascending; empty */
+/* leaves dropped), i.e. the exported leaf order.                                                 */
+typedef struct { double lb2, ub2; int64_t ord; int32_t node; } lbleaf;
+static int cmp_lbleaf(const void* a, const void* b) {
+    const lbleaf* x = (const lbleaf*)a; const lbleaf* y = (const lbleaf*)b;
+    if (x->lb2 != y->lb2) return x->lb2 < y->lb2 ? -1 : 1;
+    return (x->ord > y->ord) - (x->ord < y->ord);
+}
+static void ord_node(const orc_tree* t, int32_t ni, int64_t* cnt, int64_t* ord) {
+    const onode* nd = &t->nodes[ni];
+    if (nd->child[0] >= 0) { ord_node(t, nd->child[0], cnt, ord); ord_node(t, nd->child[1], cnt, ord); return; }
+    ord[ni] = nd->size > 0 ? (*cnt)++ : -1;
+}
+typedef struct { lbleaf* v; int64_t n, cap; const int64_t* ord; } lbset;
+static void lq_node(rq_state* st, lbset* out, int32_t ni) {
+    const orc_tree* t = st->t;
+    const onode* nd = &t->nodes[ni];
+    uint8_t lo[ORC_MAXK], hi[ORC_MAXK];
+    leaf_box(t, nd, lo, hi);
+    double lb2, ub2;
+    orc_box_bounds2(lo, hi, st->qp, st->ix->B + (size_t)st->i * st->ix->K * (st->ix->N_r + 1), t->K,
+                    t->N_r, &lb2, &ub2);
+    if (lb2 > st->rho2) return;                                /* prune */
+    if (nd->child[0] >= 0) { lq_node(st, out, nd->child[0]); lq_node(st, out, nd->child[1]); return; }
+    if (nd->size == 0) return;
+    if (out->n == out->cap) {
+        out->cap = out->cap ? 2 * out->cap : 1024;
+        out->v = (lbleaf*)realloc(out->v, sizeof(lbleaf) * (size_t)out->cap);
+        if (!out->v) { fprintf(stderr, "oracle: out of memory\n"); abort(); }
+    }
+    lbleaf e = {lb2, ub2, out->ord[ni], ni};
+    out->v[out->n++] = e;
+}
+/* the points one qualifying leaf contributes (same rules as rq_node's leaf case) */
+static int64_t leaf_points(rq_state* st, const onode* nd, double ub2, int64_t* out) {
+    int64_t cnt = 0;
+    if (st->mode == ORC_RELAXED || ub2 <= st->rho2) {
+        for (int64_t e = 0; e < nd->size; ++e) out[cnt++] = nd->ids[e];
+        return cnt;
+    }
+    for (int64_t e = 0; e < nd->size; ++e) {
+        int64_t id = nd->ids[e];
+        double v = st->mode == ORC_EXACT ? point_true2(st->ix, st->i, st->qp, id) : point_lb2(st->ix, st->i, st->qp, id);
+        if (v <= st->rho2) out[cnt++] = id;
+    }
+    return cnt;
+}
+
 int64_t orc_range_query(const orc_index* ix, int i, const float* qp, double rho, int mode,
                         int64_t* out) {
     rq_state st = {ix, ix->trees[i], i, qp, rho * rho, mode, out, 0};
@@ -754,6 +804,18 @@ static double dist2(const float* a, const float* b, int d) {
 }
 void orc_query(const orc_index* ix, const float* Q, int64_t nq, int k, double c, double r_min,
                double beta, int mode, int64_t* out_ids, float* out_dists, orc_qstats* stats) {
+    orc_query_ex(ix, Q, nq, k, c, r_min, beta, mode, 0, out_ids, out_dists, stats);
+}
+void orc_query_ex(const orc_index* ix, const float* Q, int64_t nq, int k, double c, double r_min,
+                  double beta, int mode, int lb_order, int64_t* out_ids, float* out_dists, orc_qstats* stats) {
+    int64_t** ords = (int64_t**)xmalloc(sizeof(int64_t*) * (size_t)ix->L);
+    for (int i = 0; i < ix->L; ++i) {
+        const orc_tree* t = ix->trees[i];
+        int64_t cnt = 0;
+        ords[i] = (int64_t*)xmalloc(sizeof(int64_t) * (size_t)(t->nnodes ? t->nnodes : 1));
+        for (int64_t f = 0; f < t->nfirst; ++f) ord_node(t, t->first[f], &cnt, ords[i]);
+    }
+    lbset ls = {NULL, 0, 0, NULL};
     int64_t n = ix->n;
     int64_t budget = (int64_t)ceil(beta * (double)n) + k;     /* beta n + k (AMB-17) */
     uint8_t* inS = (uint8_t*)xmalloc((size_t)n);
@@ -772,11 +834,28 @@ void orc_query(const orc_index* ix, const float* Q, int64_t nq, int k, double c,
             ++rounds;
             int stop = 0;
             for (int i = 0; i < ix->L; ++i) {                  /* line 3 */
-                int64_t cnt = orc_range_query(ix, i, qp + (size_t)i * ix->K, ix->eps * r, mode, buf); /* line 5 */
-                for (int64_t e = 0; e < cnt; ++e)              /* line 6: S <- S u S_i */
-                    if (!inS[buf[e]]) { inS[buf[e]] = 1; S[nS++] = buf[e]; }
                 trees_last = i + 1;
-                if (nS >= budget) { reason = 0; stop = 1; break; }   /* line 7 */
+                if (!lb_order) {
+                    int64_t cnt = orc_range_query(ix, i, qp + (size_t)i * ix->K, ix->eps * r, mode, buf); /* line 5 */
+                    for (int64_t e = 0; e < cnt; ++e)          /* line 6: S <- S u S_i */
+                        if (!inS[buf[e]]) { inS[buf[e]] = 1; S[nS++] = buf[e]; }
+                    if (nS >= budget) { reason = 0; stop = 1; break; }   /* line 7 */
+                } else {
+                    /* §6.2.2(2): the tree's qualifying leaves in ascending (LB, leaf) order, the budget
+                       checked after each leaf (line 7 at leaf granularity) */
+                    rq_state rs = {ix, ix->trees[i], i, qp + (size_t)i * ix->K, (ix->eps * r) * (ix->eps * r), mode, buf, 0};
+                    ls.n = 0;
+                    ls.ord = ords[i];
+                    for (int64_t f = 0; f < rs.t->nfirst; ++f) lq_node(&rs, &ls, rs.t->first[f]);
+                    qsort(ls.v, (size_t)ls.n, sizeof(lbleaf), cmp_lbleaf);
+                    for (int64_t e = 0; e < ls.n && !stop; ++e) {
+                        int64_t cnt = leaf_points(&rs, &rs.t->nodes[ls.v[e].node], ls.v[e].ub2, buf);
+                        for (int64_t u = 0; u < cnt; ++u)
+                            if (!inS[buf[u]]) { inS[buf[u]] = 1; S[nS++] = buf[u]; }
+                        if (nS >= budget) { reason = 0; stop = 1; }
+                    }
+                    if (stop) break;
+                }
             }
             if (stop) break;
             for (; nver < nS; ++nver)                          /* distances of new candidates */
@@ -809,6 +888,9 @@ void orc_query(const orc_index* ix, const float* Q, int64_t nq, int k, double c,
         }
     }
     free(inS); free(S); free(d2); free(buf); free(qp);
+    for (int i = 0; i < ix->L; ++i) free(ords[i]);
+    free(ords);
+    free(ls.v);
 }
 
 /* ======================================================================== */

@@ -107,6 +107,11 @@ void   orc_query(const orc_index* ix, const float* Q, int64_t nq, int k, double 
 /* ---- O8b: (r,c)-ANN, Alg. 4: one id/dist per query, (-1, +inf) for "nothing" ---- */
 void   orc_rc_ann(const orc_index* ix, const float* Q, int64_t nq, double c, double r, double beta, int mode,
                   int64_t* out_ids, float* out_dists);
+/* Same with lb_order = 1: §6.2.2(2) -- within each tree the qualifying leaves are taken
+   in ascending (lower bound, leaf position) order and the budget |S| >= ceil(beta n)+k is
+   checked after each leaf instead of after the tree. */
+void   orc_query_ex(const orc_index* ix, const float* Q, int64_t nq, int k, double c, double r_min,
+                    double beta, int mode, int lb_order, int64_t* out_ids, float* out_dists, orc_qstats* stats);
 /* Projected query (the fp32 K*L vector), exposed for tests. */
 void   orc_project_query(const orc_index* ix, const float* q, float* qp);
 

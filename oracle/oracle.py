@@ -81,6 +81,7 @@ def lib():
             "orc_index_eps": (f64, [P]),
             "orc_range_query": (i64, [P, i32, P, f64, i32, P]),
             "orc_query": (None, [P, P, i64, i32, f64, f64, f64, i32, P, P, P]),
+            "orc_query_ex": (None, [P, P, i64, i32, f64, f64, f64, i32, i32, P, P, P]),
             "orc_project_query": (None, [P, P, P]),
             "orc_rc_ann": (None, [P, P, i64, f64, f64, f64, i32, P, P]),
             "orc_merge_topk": (None, [P, P, i32, i64, i32, P, P]),
@@ -282,14 +283,15 @@ class Index:
         cnt = lib().orc_range_query(self._h, i, _p(qp_i), float(rho), mode, _p(out))
         return out[:cnt].copy()
 
-    def query(self, Q, k: int, c: float, r_min: float, beta: float, mode: int = CELL):
+    def query(self, Q, k: int, c: float, r_min: float, beta: float, mode: int = CELL, lb_order: bool = False):
+        """Alg. 5; lb_order: Sec. 6.2.2(2) leaves in (LB, leaf) order, budget checked per leaf."""
         Q = _c(Q, np.float32).reshape(-1, self.d)
         nq = Q.shape[0]
         ids = np.empty((nq, k), np.int64)
         dists = np.empty((nq, k), np.float32)
         st = np.zeros(nq, QSTATS_DTYPE)
-        lib().orc_query(self._h, _p(Q), nq, k, float(c), float(r_min), float(beta), mode,
-                        _p(ids), _p(dists), _p(st))
+        lib().orc_query_ex(self._h, _p(Q), nq, k, float(c), float(r_min), float(beta), mode, int(lb_order),
+                           _p(ids), _p(dists), _p(st))
         return ids, dists, st
 
     def rc_ann(self, Q, r: float, c: float, beta: float, mode: int = CELL):

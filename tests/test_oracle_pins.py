@@ -544,3 +544,64 @@ def test_rc_ann_pins(tiny_oracle, tiny):
         assert np.array_equal(ri[one], qi[one, 0]) and np.array_equal(rd[one], qd[one, 0])
         assert np.all(ri[~one] == -1)
         assert 0 < one.sum() or r < rmin
+
+
+def _lb_order_reference(o, X, q, k, c, r_min, beta, L, K, N_r):
+    """Sec. 6.2.2(2) re-derived from the exported trees and the pinned box bounds: per
+    round, per tree, the leaves with LB <= (eps r)^2 in ascending (LB, leaf position) order; a
+    leaf contributes its points whose own cell bound is <= (eps r)^2 (all of them when the
+    leaf's upper bound is); |S| >= ceil(beta n)+k is checked after each leaf; else the radius
+    test of Alg. 5 line 9 after the round."""
+    n = len(X)
+    B = o.breakpoints()
+    codes = o.codes()
+    qp = o.project_query(q)
+    budget = int(np.ceil(beta * n)) + k
+    trees = [o.tree(i) for i in range(L)]
+    inS = np.zeros(n, bool)
+    S = []
+    r = r_min
+    for _ in range(64):
+        rho2 = (o.eps * r) ** 2
+        for i, t in enumerate(trees):
+            bi = B[i * K:(i + 1) * K]
+            leaves = []
+            for l in range(len(t["leaf_off"]) - 1):
+                lb2, ub2 = O.box_bounds2(t["lo"][l], t["hi"][l], qp[i * K:(i + 1) * K], bi, N_r)
+                if lb2 <= rho2:
+                    leaves.append((lb2, l, ub2))
+            for lb2, l, ub2 in sorted(leaves):
+                for pid in t["perm"][t["leaf_off"][l]:t["leaf_off"][l + 1]]:
+                    cl = codes[pid, i * K:(i + 1) * K]
+                    if ub2 <= rho2 or O.box_bounds2(cl, cl, qp[i * K:(i + 1) * K], bi, N_r)[0] <= rho2:
+                        if not inS[pid]:
+                            inS[pid] = True
+                            S.append(pid)
+                if len(S) >= budget:
+                    return np.array(sorted(S)), 0
+        d2 = ((X[S].astype(np.float64) - q) ** 2).sum(1)
+        if (d2 <= (c * r) ** 2).sum() >= k:
+            return np.array(sorted(S)), 1
+        r *= c
+    return np.array(sorted(S)), 2
+
+
+def test_lb_order_truncation_pins():
+    """f2 pinned against an independent re-derivation (Python, from the exported trees and the
+    pinned box bounds) on a small index at budgets that truncate inside a tree; with beta >= 1 the
+    order cannot matter and lb_order equals plain Alg. 5."""
+    import datagen
+    D = datagen.generate(1, n=1500, nq=6)
+    X, Q = D["X"], D["Q"]
+    o = O.Index(X, 2, 8, 16, 11, max_size=24)
+    for beta, r in ((0.02, 40.0), (0.05, 60.0), (0.1, 150.0)):
+        for qi in range(len(Q)):
+            ids, _, st = o.query(Q[qi:qi + 1], 5, 1.5, r, beta, lb_order=True)
+            S_ref, reason = _lb_order_reference(o, X, Q[qi].astype(np.float64), 5, 1.5, r, beta, 2, 8, 16)
+            assert st["n_cand"][0] == len(S_ref) and st["reason"][0] == reason
+            d2 = ((X[S_ref].astype(np.float64) - Q[qi]) ** 2).sum(1)
+            ref = S_ref[np.lexsort((S_ref, d2))][:5]
+            assert np.array_equal(ids[0][:len(ref)], ref)
+    a = o.query(Q, 5, 1.5, 30.0, 2.0, lb_order=True)
+    b = o.query(Q, 5, 1.5, 30.0, 2.0)
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[2]["n_cand"], b[2]["n_cand"])

@@ -594,14 +594,17 @@ def test_lb_order_truncation_pins():
     D = datagen.generate(1, n=1500, nq=6)
     X, Q = D["X"], D["Q"]
     o = O.Index(X, 2, 8, 16, 11, max_size=24)
-    for beta, r in ((0.02, 40.0), (0.05, 60.0), (0.1, 150.0)):
+    reasons = []
+    for beta, r in ((0.02, 300.0), (0.05, 400.0), (0.1, 600.0), (0.02, 150.0)):
         for qi in range(len(Q)):
             ids, _, st = o.query(Q[qi:qi + 1], 5, 1.5, r, beta, lb_order=True)
             S_ref, reason = _lb_order_reference(o, X, Q[qi].astype(np.float64), 5, 1.5, r, beta, 2, 8, 16)
             assert st["n_cand"][0] == len(S_ref) and st["reason"][0] == reason
+            reasons.append(reason)
             d2 = ((X[S_ref].astype(np.float64) - Q[qi]) ** 2).sum(1)
             ref = S_ref[np.lexsort((S_ref, d2))][:5]
             assert np.array_equal(ids[0][:len(ref)], ref)
+    assert reasons.count(0) >= 12 and reasons.count(1) >= 3     # budget cuts inside a tree, and radius stops
     a = o.query(Q, 5, 1.5, 30.0, 2.0, lb_order=True)
     b = o.query(Q, 5, 1.5, 30.0, 2.0)
     assert np.array_equal(a[0], b[0]) and np.array_equal(a[2]["n_cand"], b[2]["n_cand"])

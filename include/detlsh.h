@@ -66,6 +66,11 @@ typedef struct {
                               that round's candidate density (default).
                               Either way the returned distances are recomputed directly in fp32. */
     int32_t  keep_projections; /* build: 1 keeps the fp32 projections of every point (EXACT mode) */
+    int32_t  lb_order;     /* query: 1 = Sec. 6.2.2(2): within a tree the qualifying leaves
+                              are taken in ascending (lower bound, leaf position) order and the
+                              budget is checked after each leaf (Alg. 5 line 7 at leaf granularity);
+                              0 = Alg. 5 as written (budget after each tree, default) */
+    int32_t  pad1;
 } detlsh_opts;
 
 /* Per-query statistics (Alg. 5 bookkeeping). */

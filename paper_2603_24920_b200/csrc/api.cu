@@ -172,6 +172,8 @@ void detlsh_default_opts(detlsh_opts* o) {
     o->mem_budget = 0;
     o->verify_impl = 0;
     o->keep_projections = 0;
+    o->lb_order = 0;
+    o->pad1 = 0;
 }
 
 const char* detlsh_last_error(void) { return g_err.c_str(); }
@@ -273,6 +275,7 @@ static detlsh_status run_query(const detlsh_index* idx, const float* queries, in
         QueryArgs a{nq, k, c, r_min, beta, o.mode, o.query_batch, o.mem_budget, o.proj_impl, o.verify_impl};
         a.max_rounds = max_rounds;
         a.null_on_cap = null_on_cap;
+        a.lb_order = o.lb_order ? 1 : 0;
         query_index(ix, s_q.as<float>(), ix.ld, a, static_cast<int64_t*>(oi.dev()), static_cast<float*>(od.dev()),
                     os ? static_cast<detlsh_query_stats*>(os->dev()) : nullptr, st);
         oi.finish(st);

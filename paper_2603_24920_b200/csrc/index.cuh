@@ -99,6 +99,7 @@ struct QueryArgs {
     int64_t mem_budget;
     int proj_impl;
     int verify_impl;
+    int lb_order = 0;           // Sec. 6.2.2(2): leaves in (LB, leaf) order, budget checked per leaf
     int max_rounds = 64;        // AMB-20 round cap; 1 for (r,c)-ANN (Alg. 4)
     bool null_on_cap = false;   // (r,c)-ANN: return nothing when the single pass neither hit the
                                 // budget nor found a point within c r

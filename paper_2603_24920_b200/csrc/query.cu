@@ -46,6 +46,7 @@ struct QState {  // per query of a batch
     int32_t rounds;
     int32_t overflow;
     int32_t pad;
+    int64_t tnew;       // lb_order: first-time members of the current tree (counted, not yet committed)
 };
 
 
@@ -595,7 +596,7 @@ __global__ void __launch_bounds__(RF_THREADS, 3) k_range_filter(RFArgs a) {
 constexpr int CN_WORDS = 4096;
 __global__ void __launch_bounds__(256) k_count_new(const int* __restrict__ act, QState* __restrict__ qs,
                                                    const uint32_t* __restrict__ cur, uint32_t* __restrict__ prev,
-                                                   int64_t nwords) {
+                                                   int64_t nwords, int commit) {
     __shared__ unsigned int s_cnt;
     const int q = act[blockIdx.x];
     if (qs[q].status != ST_ACTIVE) return;
@@ -608,13 +609,174 @@ __global__ void __launch_bounds__(256) k_count_new(const int* __restrict__ act, 
     for (int64_t w = w0 + threadIdx.x; w < w1; w += 256) {
         const uint32_t cv = c[w], pv = p[w];
         const uint32_t nb = cv & ~pv;
-        if (nb) { p[w] = cv; cnt += __popc(nb); }
+        if (nb) {
+            if (commit) p[w] = cv;
+            cnt += __popc(nb);
+        }
     }
     for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
     if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(&s_cnt, cnt);
     __syncthreads();
-    if (threadIdx.x == 0 && s_cnt)
-        atomicAdd(reinterpret_cast<unsigned long long*>(&qs[q].cnt), (unsigned long long)s_cnt);
+    if (threadIdx.x == 0 && s_cnt)   // committed: |S| grows; tentative (lb_order): counted into tnew
+        atomicAdd(reinterpret_cast<unsigned long long*>(commit ? &qs[q].cnt : &qs[q].tnew), (unsigned long long)s_cnt);
+}
+
+// ---- Sec. 6.2.2(2): leaves in ascending (LB, leaf) order, budget per leaf.
+//      Only queries whose tree-t candidates would cross the budget need it (for the others the
+//      order cannot change S):
+//   k_lbo_cross   queries with |S| + tentative first-time members >= budget (compacted list)
+//   k_lbo_leaves  per (crossing query, leaf of tree t): the leaf's fp32 lower bound (j order) as a
+//                 sort key (0xFFFFFFFF when above eps r) and its number of first-time members
+//   (segmented radix sort of the keys, values = leaf positions: ties by leaf position)
+//   k_lbo_cut     the first leaf in that order at which |S| reaches the budget
+//   k_lbo_reset   S <- S before tree t (the prev bitmap)
+//   k_lbo_mark    the members of leaves up to the cut, marked again
+__global__ void k_lbo_cross(const int* __restrict__ act, int na, const QState* __restrict__ qs, int64_t budget,
+                            int* __restrict__ cross, int* __restrict__ ncross) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < na; i += gridDim.x * blockDim.x) {
+        const int q = act[i];
+        const QState s = qs[q];
+        if (s.status == ST_ACTIVE && s.cnt + s.tnew >= budget) cross[atomicAdd(ncross, 1)] = q;
+    }
+}
+
+struct LboArgs {
+    const int* cross;
+    const float* lut;           // [Qb][L][K][N_r] fp32
+    const uint8_t* sx;          // [Qb][L][K]
+    const uint8_t* lo;          // tree t leaves [nl_t][K]
+    const uint8_t* hi;
+    const uint32_t* leaf_off;   // tree t leaves, global positions [nl_t + 1]
+    const uint8_t* tcodes;      // tree t [n][K]
+    const uint32_t* perm;       // tree t [n]
+    const float* proj;          // EXACT
+    const float* qp;            // EXACT: [Qb][LK]
+    const uint32_t* prev;       // S before tree t
+    uint32_t* cur;
+    int64_t nwords, pos_base, nl;
+    float rho2;
+    int t, L, K, N_r, mode;
+    uint32_t* keys;             // [ncross][nl]
+    uint32_t* vals;             // [ncross][nl] leaf positions
+    uint32_t* nnew;             // [ncross][nl]
+    const unsigned long long* cut;   // [ncross] (key << 32 | leaf): mark leaves <= cut
+};
+
+template <bool MARK>
+__global__ void __launch_bounds__(256) k_lbo_leaves(LboArgs a) {
+    extern __shared__ float s_lut[];                   // the query's fp32 table of tree t
+    const int c = blockIdx.y;
+    const int q = a.cross[c];
+    const int K = a.K, N_r = a.N_r;
+    const float* src = a.lut + ((int64_t)q * a.L + a.t) * K * N_r;
+    for (int i = threadIdx.x; i < K * N_r; i += blockDim.x) s_lut[i] = src[i];
+    __syncthreads();
+    const uint8_t* sx = a.sx + ((int64_t)q * a.L + a.t) * K;
+    const float* qpt = a.qp ? a.qp + (int64_t)q * a.L * K + a.t * K : nullptr;
+    const int lane = threadIdx.x & 31;
+    const uint32_t* pv = a.prev + (int64_t)q * a.nwords;
+    uint32_t* cv = a.cur + (int64_t)q * a.nwords;
+    const unsigned long long cut = MARK ? a.cut[c] : 0ull;
+    for (int64_t l = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5); l < a.nl; l += (int64_t)gridDim.x * 8) {
+        float lb = 0.f;                                  // leaf LB, j order (as RELAXED's leaf test)
+        for (int j = 0; j < K; ++j)
+            lb += s_lut[j * N_r + min(max((int)sx[j], (int)a.lo[l * K + j]), (int)a.hi[l * K + j])];
+        const uint32_t key = lb <= a.rho2 ? __float_as_uint(lb) : 0xFFFFFFFFu;
+        if (MARK && (key == 0xFFFFFFFFu || (((unsigned long long)key << 32) | (unsigned long long)l) > cut)) continue;
+        if (!MARK && key == 0xFFFFFFFFu) {
+            if (lane == 0) { a.keys[(int64_t)c * a.nl + l] = key; a.vals[(int64_t)c * a.nl + l] = (uint32_t)l; a.nnew[(int64_t)c * a.nl + l] = 0; }
+            continue;
+        }
+        uint32_t cnt = 0;
+        for (uint32_t p = a.leaf_off[l] + lane; p < a.leaf_off[l + 1]; p += 32) {
+            const int64_t pos = (int64_t)p - a.pos_base;
+            bool pass = true;
+            if (a.mode == DETLSH_MODE_CELL) {
+                float s_ = 0.f;
+                for (int j = 0; j < K; ++j) s_ += s_lut[j * N_r + a.tcodes[pos * K + j]];
+                pass = s_ <= a.rho2;
+            } else if (a.mode == DETLSH_MODE_EXACT) {
+                const float* pp = a.proj + (int64_t)a.perm[pos] * a.L * K + a.t * K;
+                float s_ = 0.f;
+                for (int j = 0; j < K; ++j) {
+                    const float df = qpt[j] - pp[j];
+                    s_ = fmaf(df, df, s_);
+                }
+                pass = s_ <= a.rho2;
+            }
+            if (!pass) continue;
+            const uint32_t id = a.perm[pos];
+            if (MARK) {
+                atomicOr(cv + (id >> 5), 1u << (id & 31));
+            } else if (!((pv[id >> 5] >> (id & 31)) & 1u)) {
+                ++cnt;
+            }
+        }
+        if (!MARK) {
+            for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+            if (lane == 0) {
+                a.keys[(int64_t)c * a.nl + l] = key;
+                a.vals[(int64_t)c * a.nl + l] = (uint32_t)l;
+                a.nnew[(int64_t)c * a.nl + l] = cnt;
+            }
+        }
+    }
+}
+
+__global__ void __launch_bounds__(1024) k_lbo_cut(const int* __restrict__ cross, const QState* __restrict__ qs,
+                                                  int64_t budget, const uint32_t* __restrict__ skeys,
+                                                  const uint32_t* __restrict__ svals, const uint32_t* __restrict__ nnew,
+                                                  int64_t nl, unsigned long long* __restrict__ cut) {
+    __shared__ uint32_t s_w[32];
+    __shared__ int64_t s_hit;
+    const int c = blockIdx.x;
+    const int q = cross[c];
+    const int64_t need = budget - qs[q].cnt;            // > 0 (the query is still active)
+    const uint32_t* k_ = skeys + (int64_t)c * nl;
+    const uint32_t* v_ = svals + (int64_t)c * nl;
+    const uint32_t* w_ = nnew + (int64_t)c * nl;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    if (threadIdx.x == 0) s_hit = -1;
+    int64_t carry = 0;
+    for (int64_t b0 = 0; b0 < nl; b0 += 1024) {
+        const int64_t b = b0 + threadIdx.x;
+        const uint32_t x0 = b < nl ? w_[v_[b]] : 0u;
+        uint32_t x = x0;
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) s_w[w] = x;
+        __syncthreads();
+        if (w == 0) {
+            uint32_t t = s_w[lane];
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, t, o);
+                if (lane >= o) t += y;
+            }
+            s_w[lane] = t;
+        }
+        __syncthreads();
+        const int64_t incl = carry + x + (w ? s_w[w - 1] : 0);
+        if (b < nl && incl >= need && incl - x0 < need) s_hit = b;   // unique crossing rank
+        carry += s_w[31];
+        __syncthreads();
+        if (s_hit >= 0) break;
+    }
+    if (threadIdx.x == 0) {
+        const int64_t h = s_hit >= 0 ? s_hit : nl - 1;
+        cut[c] = ((unsigned long long)k_[h] << 32) | (unsigned long long)v_[h];
+    }
+}
+
+__global__ void k_lbo_reset(const int* __restrict__ cross, int ncross, const uint32_t* __restrict__ prev,
+                            uint32_t* __restrict__ cur, int64_t nwords) {
+    const int64_t total = (int64_t)ncross * nwords;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t c = i / nwords, w = i - c * nwords;
+        const int64_t o = (int64_t)cross[c] * nwords + w;
+        cur[o] = prev[o];
+    }
 }
 
 // After tree t: the budget test |S| >= ceil(beta n) + k (Alg. 5 line 7, AMB-15/17).
@@ -625,6 +787,7 @@ __global__ void k_tree_end(const int* __restrict__ act, int na, QState* __restri
         if (s->status != ST_ACTIVE) continue;
         s->trees_last = t + 1;
         s->rounds = round + 1;
+        s->tnew = 0;
         if (s->cnt > cap) s->overflow = 1;
         if (s->cnt >= budget) s->status = ST_BUDGET;
     }
@@ -1239,7 +1402,7 @@ __global__ void k_init_batch(QState* __restrict__ qs, int* __restrict__ act, int
     for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < nqb; q += gridDim.x * blockDim.x) {
         QState s;
         s.cnt = 0; s.nver = 0; s.roff = 0; s.rcnt = 0; s.status = ST_ACTIVE; s.tk = 0; s.trees_last = 0; s.rounds = 0;
-        s.overflow = 0; s.pad = 0;
+        s.overflow = 0; s.pad = 0; s.tnew = 0;
         qs[q] = s;
         act[q] = q;
     }
@@ -1404,6 +1567,7 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
     Scratch s_ver(st, sizeof(uint32_t) * (size_t)(qb * nwords));     // verified members of S
     Scratch s_round(st);                   // (id, d2) of this round's new members, grown on demand
     Scratch s_cq(st);                      // sparse verification: active-query index per slot
+    int64_t cq_cap = 0;
     int64_t round_cap = 0;
     Scratch s_total(st, sizeof(unsigned long long));
     Scratch s_tk(st, sizeof(unsigned long long) * (size_t)(qb * k));
@@ -1496,6 +1660,75 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
     DL_CUDA(cudaFuncSetAttribute(k_verify_rows<8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)vr_smem));
     DL_CUDA(cudaFuncSetAttribute(k_verify_rows<0, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)vr_smem));
 
+    // Sec. 6.2.2(2): for the queries whose tree-t candidates cross the budget, keep
+    // only the leaves up to the one (in (LB, leaf) order) at which |S| reaches it
+    Scratch s_lbo(st);
+    size_t lbo_cap = 0;
+    Scratch s_lcross(st, sizeof(int) * (size_t)(qb + 1));
+    double lbo_rho2 = 0;
+    const float* lbo_qp = nullptr;
+    auto lb_order_tree = [&](int t, const int* fa_, int nf_) {
+        int* cross = s_lcross.as<int>();
+        int* ncross_d = cross + qb;
+        DL_CUDA(cudaMemsetAsync(ncross_d, 0, sizeof(int), st));
+        DL_LAUNCH(k_count_new, dim3((unsigned)nf_, (unsigned)ceil_div(nwords, CN_WORDS)), 256, 0, st, fa_,
+                  s_qs.as<QState>(), s_bm.as<uint32_t>(), bm_prev, nwords, 0);
+        DL_LAUNCH(k_lbo_cross, (unsigned)ceil_div(nf_, 256), 256, 0, st, fa_, nf_, s_qs.as<QState>(), budget, cross,
+                  ncross_d);
+        int ncross = 0;
+        DL_CUDA(cudaMemcpyAsync(&ncross, ncross_d, sizeof(int), cudaMemcpyDeviceToHost, st));
+        DL_CUDA(cudaStreamSynchronize(st));
+        if (ncross == 0) return;
+        const int64_t lb0 = ix.tree_leaf_begin[t], nl_t = ix.tree_leaf_begin[t + 1] - lb0;
+        const int64_t m = (int64_t)ncross * nl_t;
+        const size_t need_b = sizeof(uint32_t) * (size_t)(5 * m + 1) + sizeof(unsigned long long) * (size_t)ncross + 256;
+        if (need_b > lbo_cap) {       // grow-only (scratch is bump-allocated within a call)
+            lbo_cap = need_b + need_b / 2;
+            s_lbo.alloc(lbo_cap);
+        }
+        uint32_t* k0 = s_lbo.as<uint32_t>();
+        uint32_t* v0 = k0 + m;
+        uint32_t* k1 = v0 + m;
+        uint32_t* v1 = k1 + m;
+        uint32_t* nn = v1 + m;
+        unsigned long long* cut = reinterpret_cast<unsigned long long*>(nn + m + (m & 1));   // 8-byte aligned
+        LboArgs la;
+        la.cross = cross;
+        la.lut = s_lut.as<float>();
+        la.sx = s_sx.as<uint8_t>();
+        la.lo = ix.leaf_lo.as<uint8_t>() + lb0 * ix.K;
+        la.hi = ix.leaf_hi.as<uint8_t>() + lb0 * ix.K;
+        la.leaf_off = ix.leaf_off.as<uint32_t>() + lb0;
+        la.tcodes = ix.tcodes.as<uint8_t>() + (int64_t)t * n * ix.K;
+        la.perm = ix.perm.as<uint32_t>() + (int64_t)t * n;
+        la.proj = ix.proj.as<float>();
+        la.qp = a.mode == DETLSH_MODE_EXACT ? lbo_qp : nullptr;
+        la.prev = bm_prev;
+        la.cur = s_bm.as<uint32_t>();
+        la.nwords = nwords;
+        la.pos_base = (int64_t)t * n;
+        la.nl = nl_t;
+        la.rho2 = (float)lbo_rho2;
+        la.t = t;
+        la.L = ix.L;
+        la.K = ix.K;
+        la.N_r = ix.N_r;
+        la.mode = a.mode;
+        la.keys = k0;
+        la.vals = v0;
+        la.nnew = nn;
+        la.cut = cut;
+        const size_t smem = sizeof(float) * (size_t)ix.K * ix.N_r;
+        const dim3 grid((unsigned)std::min<int64_t>(ceil_div(nl_t, 8), 64), (unsigned)ncross);
+        DL_LAUNCH(k_lbo_leaves<false>, grid, 256, smem, st, la);
+        const bool flip = radix_sort_batched(k0, v0, k1, v1, nl_t, ncross, 32, st);
+        DL_LAUNCH(k_lbo_cut, (unsigned)ncross, 1024, 0, st, cross, s_qs.as<QState>(), budget, flip ? k1 : k0,
+                  flip ? v1 : v0, nn, nl_t, cut);
+        DL_LAUNCH(k_lbo_reset, (unsigned)std::min<int64_t>(ceil_div((int64_t)ncross * nwords, 256), 148 * 16), 256, 0, st,
+                  cross, ncross, bm_prev, s_bm.as<uint32_t>(), nwords);
+        DL_LAUNCH(k_lbo_leaves<true>, grid, 256, smem, st, la);
+    };
+
     for (int64_t q0 = 0; q0 < nq; q0 += qb) {
         const int nqb = (int)std::min<int64_t>(qb, nq - q0);
         const float* Qb = d_Q + q0 * q_ld;
@@ -1514,6 +1747,8 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
         for (int m = 0; m < max_rounds && na > 0; ++m) {
             const double r = radii[m];
             const float rho2 = (float)((eps * r) * (eps * r));
+            lbo_rho2 = rho2;
+            lbo_qp = Qpb;
             const float cr2 = (float)((a.c * r) * (a.c * r));
             {   // quantised screen of this round: scale 2048 / rho^2 rounded down
                 const float inv_rd = fdiv_rd_host((float)QuantSpec<RF_G>::QT, rho2);
@@ -1550,8 +1785,9 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
                 const int stripes = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(ntiles, RF_THREADS / 32),
                                                                                  (148 * 3 * 4 + groups / 2) / groups));
                 DL_LAUNCH(k_range_filter_sel, dim3((unsigned)groups, (unsigned)stripes), RF_THREADS, rf_smem, st, ra);
+                if (a.lb_order) lb_order_tree(t, fa, nf);
                 DL_LAUNCH(k_count_new, dim3((unsigned)nf, (unsigned)ceil_div(nwords, CN_WORDS)), 256, 0, st, fa,
-                          s_qs.as<QState>(), s_bm.as<uint32_t>(), bm_prev, nwords);
+                          s_qs.as<QState>(), s_bm.as<uint32_t>(), bm_prev, nwords, 1);
                 DL_LAUNCH(k_tree_end, (unsigned)ceil_div(nf, 256), 256, 0, st, fa, nf, s_qs.as<QState>(), t, m,
                           budget, cap);
                 if (t + 1 < ix.L) {
@@ -1603,7 +1839,10 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
                                         va.d2, st);
                     DL_REQUIRE(done_tc, "tensor-core verification does not fit this shape");
                 } else if (tot > 0) {
-                    s_cq.alloc(sizeof(uint32_t) * (size_t)tot);
+                    if ((int64_t)tot > cq_cap) {      // grow-only
+                        cq_cap = (int64_t)(tot + tot / 2 + 1024);
+                        s_cq.alloc(sizeof(uint32_t) * (size_t)cq_cap);
+                    }
                     DL_LAUNCH(k_collect_cands, (unsigned)std::min<int64_t>(ceil_div((int64_t)na * nwords, 256), 148 * 16),
                               256, 0, st, na, NB, BO, nwords, va.cand, s_cq.as<uint32_t>());
                     DL_LAUNCH(k_verify_gather, (unsigned)std::min<int64_t>(ceil_div((int64_t)tot * 8, 256), 148 * 32), 256,

@@ -32,7 +32,8 @@ class detlsh_opts(C.Structure):
     _fields_ = [("max_size", C.c_int32), ("sample_frac", C.c_double), ("mode", C.c_int32),
                 ("query_batch", C.c_int32), ("stream", C.c_uint64), ("borrow_data", C.c_int32),
                 ("proj_impl", C.c_int32), ("mem_budget", C.c_int64),
-                ("verify_impl", C.c_int32), ("keep_projections", C.c_int32)]
+                ("verify_impl", C.c_int32), ("keep_projections", C.c_int32), ("lb_order", C.c_int32),
+                ("pad1", C.c_int32)]
 
 
 class detlsh_kernel_time(C.Structure):

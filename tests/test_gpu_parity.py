@@ -414,3 +414,26 @@ def test_query_parity_exact_mode(tiny_oracle, tiny, tiny_rmin, vimpl):
     plain = P.detlsh_build(tiny["X"][:500], c.L, c.K, c.N_r, c.index_seed)
     with pytest.raises(P.DetlshError):
         plain.query(tiny["Q"][:2], 5, c.c, tiny_rmin, c.beta, opts=P.default_opts(mode=P.MODE_EXACT))
+
+
+@pytest.mark.parametrize("mode", [P.MODE_CELL, P.MODE_RELAXED, P.MODE_EXACT])
+def test_lb_order_parity(mode):
+    """f2 (Sec. 6.2.2(2)): leaves in (LB, leaf) order with the budget checked per leaf, against the
+    oracle's lb_order driver, at radii where the budget cuts inside a tree."""
+    D = datagen.generate(1, n=4000, nq=40)
+    X, Q = D["X"], D["Q"]
+    g = P.detlsh_build(X, 4, 16, 256, 42, opts=P.default_opts(keep_projections=1))
+    o = O.Index(X, 4, 16, 256, 42)
+    nbudget = 0
+    for beta, r in ((0.02, 300.0), (0.05, 400.0), (0.1, 250.0)):
+        ig, dg, sg = g.query(Q, 10, 1.5, r, beta, opts=P.default_opts(mode=mode, lb_order=1), stats=True)
+        io, do, so = o.query(Q, 10, 1.5, r, beta, mode=mode, lb_order=True)
+        assert np.mean(sg["reason"] == so["reason"]) >= 0.95
+        assert np.mean(sg["n_cand"] == so["n_cand"]) >= 0.9
+        assert _recall(ig, io) >= 0.99
+        _dist_match(ig, dg, io, do)
+        # the cut keeps |S| at the budget's leaf: never more than plain Alg. 5's
+        _, _, sp = g.query(Q, 10, 1.5, r, beta, opts=P.default_opts(mode=mode), stats=True)
+        assert np.all(sg["n_cand"][sg["reason"] == 0] <= sp["n_cand"][sg["reason"] == 0])
+        nbudget += int((so["reason"] == 0).sum())
+    assert nbudget >= 30

@@ -975,10 +975,14 @@ __global__ void __launch_bounds__(VR_THREADS) k_verify_rows(VRArgs a) {
 //                  scan), and ver catches up with cur.
 //  k_prep_queries  the active queries as a contiguous [na][ld] fp32 block, its TF32 residual
 //                  q - trunc_tf32(q), and ||q||^2.
+template <bool EMIT>
 __global__ void __launch_bounds__(1024) k_verify_prep(const int* __restrict__ act, const QState* __restrict__ qs,
                                                       const uint32_t* __restrict__ cur, uint32_t* __restrict__ ver,
                                                       int64_t nwords, uint32_t* __restrict__ NB,
-                                                      uint32_t* __restrict__ BO) {
+                                                      uint32_t* __restrict__ BO, uint32_t* __restrict__ cand,
+                                                      uint32_t* __restrict__ cq) {
+    // EMIT (sparse verification): instead of NB/BO, list the new members directly at their
+    // round-buffer slots (candidate id, active-query index)
     // nwords is a multiple of 4 (padded bitmap rows): each thread owns 4 consecutive words
     __shared__ uint32_t s_w[32];
     const int a = blockIdx.x;
@@ -1018,8 +1022,25 @@ __global__ void __launch_bounds__(1024) k_verify_prep(const int* __restrict__ ac
         __syncthreads();
         const uint32_t ex = carry + x + (w ? s_w[w - 1] : 0) - cnt;
         if (b < n4) {
-            nb_out[b] = nb;
-            bo_out[b] = make_uint4(ex, ex + c0, ex + c0 + c1, ex + c0 + c1 + c2);
+            if (EMIT) {
+                uint32_t slot = ex;
+                const uint32_t wv[4] = {nb.x, nb.y, nb.z, nb.w};
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    uint32_t m_ = wv[i];
+                    const uint32_t base = (uint32_t)((b * 4 + i) * 32);
+                    while (m_) {
+                        const int bit = __ffs(m_) - 1;
+                        m_ &= m_ - 1;
+                        cand[slot] = base + (uint32_t)bit;
+                        cq[slot] = (uint32_t)a;
+                        ++slot;
+                    }
+                }
+            } else {
+                nb_out[b] = nb;
+                bo_out[b] = make_uint4(ex, ex + c0, ex + c0 + c1, ex + c0 + c1 + c2);
+            }
         }
         carry += s_w[31];
         __syncthreads();
@@ -1111,30 +1132,10 @@ __device__ void bitonic_sort_smem(unsigned long long* a, int n2) {
     }
 }
 
-// ---- sparse verification (low candidate density): the new members of S listed at their
-//      round-buffer slots (k_collect_cands, from k_verify_prep's NB/BO), then one 8-lane group
-//      per candidate gathers its row with float4 loads (k_verify_gather): per candidate 4d bytes
-//      of X, no per-(row block, query) work.
-__global__ void k_collect_cands(int na, const uint32_t* __restrict__ NB, const uint32_t* __restrict__ BO,
-                                int64_t nwords, uint32_t* __restrict__ cand, uint32_t* __restrict__ cq) {
-    const int64_t total = (int64_t)na * nwords;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        uint32_t w = NB[i];
-        if (!w) continue;
-        const int a = (int)(i / nwords);
-        const uint32_t base = (uint32_t)((i - (int64_t)a * nwords) * 32);
-        uint32_t slot = BO[i];
-        while (w) {
-            const int b = __ffs(w) - 1;
-            w &= w - 1;
-            cand[slot] = base + (uint32_t)b;
-            cq[slot] = (uint32_t)a;
-            ++slot;
-        }
-    }
-}
-
+// ---- sparse verification (low candidate density): k_verify_prep<true> lists the new members
+//      of S at their round-buffer slots, then one 8-lane group per candidate gathers its row
+//      with float4 loads (k_verify_gather): per candidate 4d bytes of X, no per-(row block,
+//      query) work.
 __global__ void __launch_bounds__(256) k_verify_gather(const uint32_t* __restrict__ cand, const uint32_t* __restrict__ cq,
                                                        const int* __restrict__ act, const float* __restrict__ X,
                                                        const float* __restrict__ Q, int64_t ld, int64_t total,
@@ -1827,8 +1828,9 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
             if (path >= 1) {
                 uint32_t* NB = s_boff.as<uint32_t>();
                 uint32_t* BO = NB + (int64_t)qb * nw4;
-                DL_LAUNCH(k_verify_prep, (unsigned)na, 1024, 0, st, cur, s_qs.as<QState>(), s_bm.as<uint32_t>(),
-                          s_ver.as<uint32_t>(), nwords, NB, BO);
+                if (path == 1)
+                    DL_LAUNCH(k_verify_prep<false>, (unsigned)na, 1024, 0, st, cur, s_qs.as<QState>(), s_bm.as<uint32_t>(),
+                              s_ver.as<uint32_t>(), nwords, NB, BO, nullptr, nullptr);
                 if (path == 1) {
                     float* Qa = s_qa.as<float>();
                     float* Qalo = Qa + (int64_t)qb * ix.ld;
@@ -1843,8 +1845,8 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
                         cq_cap = (int64_t)(tot + tot / 2 + 1024);
                         s_cq.alloc(sizeof(uint32_t) * (size_t)cq_cap);
                     }
-                    DL_LAUNCH(k_collect_cands, (unsigned)std::min<int64_t>(ceil_div((int64_t)na * nwords, 256), 148 * 16),
-                              256, 0, st, na, NB, BO, nwords, va.cand, s_cq.as<uint32_t>());
+                    DL_LAUNCH(k_verify_prep<true>, (unsigned)na, 1024, 0, st, cur, s_qs.as<QState>(), s_bm.as<uint32_t>(),
+                              s_ver.as<uint32_t>(), nwords, nullptr, nullptr, va.cand, s_cq.as<uint32_t>());
                     DL_LAUNCH(k_verify_gather, (unsigned)std::min<int64_t>(ceil_div((int64_t)tot * 8, 256), 148 * 32), 256,
                               0, st, va.cand, s_cq.as<uint32_t>(), cur, ix.Xp, Qb, (int64_t)ix.ld, (int64_t)tot, va.d2);
                 }

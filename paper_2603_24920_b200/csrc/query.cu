@@ -45,8 +45,9 @@ struct QState {  // per query of a batch
     int32_t trees_last;
     int32_t rounds;
     int32_t overflow;
-    int32_t pad;
+    int32_t doc;        // count the bitmap this tree (k_count_decide)
     int64_t tnew;       // lb_order: first-time members of the current tree (counted, not yet committed)
+    int64_t pub;        // marks since |S| was last counted: |S| <= cnt + pub
 };
 
 
@@ -162,6 +163,7 @@ struct RFArgs {
     const int* act;
     int na;
     const QState* qs;
+    QState* qs_mut;             // the same array: per-query mark counts (pub)
     uint32_t* bitmap;           // [Qb][nwords] current union S (OR-marked, no return)
     int64_t nwords;
     float rho2;
@@ -181,6 +183,7 @@ __global__ void __launch_bounds__(RF_THREADS, 3) k_range_filter(RFArgs a) {
     __shared__ __align__(16) uint8_t s_sx[G][32];
     __shared__ float s_qp[G][32];                                                        // EXACT: q'_t
     __shared__ unsigned int s_ctr[G][4];
+    __shared__ unsigned int s_pass[G];                                                  // marks per query
     __shared__ uint32_t s_lq[RF_THREADS / 32][kTileLeaves];                             // per warp: leaf masks
     __shared__ uint32_t s_bq[RF_THREADS / 32][RF_BQ];                                   // per warp: band queue
     __shared__ uint32_t s_pre[RF_THREADS / 32][32];                                     // per warp: packed-point prefix
@@ -198,6 +201,7 @@ __global__ void __launch_bounds__(RF_THREADS, 3) k_range_filter(RFArgs a) {
         }
         s_q[threadIdx.x] = q;
         for (int c = 0; c < 4; ++c) s_ctr[threadIdx.x][c] = 0;
+        s_pass[threadIdx.x] = 0;
     }
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -376,6 +380,7 @@ __global__ void __launch_bounds__(RF_THREADS, 3) k_range_filter(RFArgs a) {
                 }
                 if (s_ <= rho2) {
                     ++c_pp;
+                    atomicAdd(&s_pass[g], 1u);
                     const uint32_t id = a.perm[pos];
                     atomicOr(a.bitmap + (int64_t)s_q[g] * a.nwords + (id >> 5), 1u << (id & 31));  // RED.OR
                 }
@@ -441,6 +446,7 @@ __global__ void __launch_bounds__(RF_THREADS, 3) k_range_filter(RFArgs a) {
                         const bool ok = acc <= QT, sure = acc + 17 <= QT;
                         if (a.mode == DETLSH_MODE_CELL && sure) {
                             ++c_pp;
+                            atomicAdd(&s_pass[g], 1u);
                             const uint32_t id = a.perm[pos];
                             atomicOr(a.bitmap + (int64_t)s_q[g] * a.nwords + (id >> 5), 1u << (id & 31));  // RED.OR
                         } else {
@@ -548,6 +554,7 @@ __global__ void __launch_bounds__(RF_THREADS, 3) k_range_filter(RFArgs a) {
                     while (c_) {
                         const int g = __ffs(c_) - 1;
                         c_ &= c_ - 1;
+                        atomicAdd(&s_pass[g], 1u);
                         atomicOr(a.bitmap + (int64_t)s_q[g] * a.nwords + (id >> 5), 1u << (id & 31));  // RED.OR
                     }
                 }
@@ -588,6 +595,9 @@ __global__ void __launch_bounds__(RF_THREADS, 3) k_range_filter(RFArgs a) {
     if (threadIdx.x < G && s_q[threadIdx.x] >= 0) {
         unsigned long long* c = a.ctr + (int64_t)s_q[threadIdx.x] * 4;
         for (int i = 0; i < 4; ++i) atomicAdd(c + i, (unsigned long long)s_ctr[threadIdx.x][i]);
+        if (s_pass[threadIdx.x])
+            atomicAdd(reinterpret_cast<unsigned long long*>(&a.qs_mut[s_q[threadIdx.x]].pub),
+                      (unsigned long long)s_pass[threadIdx.x]);
     }
 }
 
@@ -600,6 +610,7 @@ __global__ void __launch_bounds__(256) k_count_new(const int* __restrict__ act, 
     __shared__ unsigned int s_cnt;
     const int q = act[blockIdx.x];
     if (qs[q].status != ST_ACTIVE) return;
+    if (commit && !qs[q].doc) return;      // |S| cannot have reached the budget: counted later
     if (threadIdx.x == 0) s_cnt = 0;
     __syncthreads();
     const uint32_t* c = cur + (int64_t)q * nwords;
@@ -776,6 +787,19 @@ __global__ void k_lbo_reset(const int* __restrict__ cross, int ncross, const uin
         const int64_t c = i / nwords, w = i - c * nwords;
         const int64_t o = (int64_t)cross[c] * nwords + w;
         cur[o] = prev[o];
+    }
+}
+
+// Before counting |S| after a tree: the bitmap diff is needed only if the budget may have been
+// reached (|S| <= cnt + marks since the last count) or the count is due (force: end of round,
+// or lb_order, which needs |S| exact after every tree).
+__global__ void k_count_decide(const int* __restrict__ act, int na, QState* __restrict__ qs, int64_t budget,
+                               int force) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < na; i += gridDim.x * blockDim.x) {
+        QState* s = &qs[act[i]];
+        const int d = (s->status == ST_ACTIVE && s->pub > 0 && (force || s->cnt + s->pub >= budget)) ? 1 : 0;
+        s->doc = d;
+        if (d) s->pub = 0;
     }
 }
 
@@ -1403,7 +1427,7 @@ __global__ void k_init_batch(QState* __restrict__ qs, int* __restrict__ act, int
     for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < nqb; q += gridDim.x * blockDim.x) {
         QState s;
         s.cnt = 0; s.nver = 0; s.roff = 0; s.rcnt = 0; s.status = ST_ACTIVE; s.tk = 0; s.trees_last = 0; s.rounds = 0;
-        s.overflow = 0; s.pad = 0; s.tnew = 0;
+        s.overflow = 0; s.doc = 0; s.tnew = 0; s.pub = 0;
         qs[q] = s;
         act[q] = q;
     }
@@ -1615,6 +1639,7 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
     ra.sx = s_sx.as<uint8_t>();
     ra.proj = ix.proj.as<float>();
     ra.qs = s_qs.as<QState>();
+    ra.qs_mut = s_qs.as<QState>();
     ra.bitmap = s_bm.as<uint32_t>();
     ra.nwords = nwords;
     ra.ctr = s_ctr.as<unsigned long long>();
@@ -1787,6 +1812,8 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
                                                                                  (148 * 3 * 4 + groups / 2) / groups));
                 DL_LAUNCH(k_range_filter_sel, dim3((unsigned)groups, (unsigned)stripes), RF_THREADS, rf_smem, st, ra);
                 if (a.lb_order) lb_order_tree(t, fa, nf);
+                DL_LAUNCH(k_count_decide, (unsigned)ceil_div(nf, 256), 256, 0, st, fa, nf, s_qs.as<QState>(), budget,
+                          a.lb_order ? 1 : 0);
                 DL_LAUNCH(k_count_new, dim3((unsigned)nf, (unsigned)ceil_div(nwords, CN_WORDS)), 256, 0, st, fa,
                           s_qs.as<QState>(), s_bm.as<uint32_t>(), bm_prev, nwords, 1);
                 DL_LAUNCH(k_tree_end, (unsigned)ceil_div(nf, 256), 256, 0, st, fa, nf, s_qs.as<QState>(), t, m,
@@ -1800,6 +1827,10 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
                 }
             }
             tr.mark("filter (L trees)", st);
+            // |S| exact for the round's accounting (trees whose count was skipped)
+            DL_LAUNCH(k_count_decide, (unsigned)ceil_div(na, 256), 256, 0, st, cur, na, s_qs.as<QState>(), budget, 1);
+            DL_LAUNCH(k_count_new, dim3((unsigned)na, (unsigned)ceil_div(nwords, CN_WORDS)), 256, 0, st, cur,
+                      s_qs.as<QState>(), s_bm.as<uint32_t>(), bm_prev, nwords, 1);
             DL_LAUNCH(k_round_offsets, 1, 1024, 0, st, cur, na, s_qs.as<QState>(), s_total.as<unsigned long long>());
             unsigned long long tot = 0;     // new members of S over the round's queries
             {

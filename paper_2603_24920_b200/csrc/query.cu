@@ -99,9 +99,10 @@ __global__ void k_build_qlut(const float* __restrict__ lut, const int* __restric
 // ---- per tree: each 16-query group's quantised table interleaved once (entry (j, s) = the
 //      group's 16 8-bit terms), copied by the group's filter CTAs instead of each CTA gathering
 //      16 queries' tables itself.  Inactive slots get the cap (never pass).
-__global__ void k_group_table(const int* __restrict__ act, int na, const QState* __restrict__ qs,
-                              const uint16_t* __restrict__ qlut, int64_t per_q, int t, int KN, uint32_t cap,
-                              uint4* __restrict__ gtab) {
+__global__ void k_group_table(const int* __restrict__ act, int na_ub, const int* __restrict__ dna,
+                              const QState* __restrict__ qs, const uint16_t* __restrict__ qlut, int64_t per_q, int t,
+                              int KN, uint32_t cap, uint4* __restrict__ gtab) {
+    const int na = dna ? *dna : na_ub;       // device count (the list is compacted on the device)
     const int64_t groups = (na + 15) / 16;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < groups * KN;
          i += (int64_t)gridDim.x * blockDim.x) {
@@ -161,7 +162,8 @@ struct RFArgs {
     const float* proj;          // EXACT: data-order projections [n][LK]
     const float* qp;            // EXACT: projected batch queries [Qb][LK]
     const int* act;
-    int na;
+    int na;                     // upper bound; the count is *dna when dna != null
+    const int* dna;
     const QState* qs;
     QState* qs_mut;             // the same array: per-query mark counts (pub)
     uint32_t* bitmap;           // [Qb][nwords] current union S (OR-marked, no return)
@@ -195,7 +197,7 @@ __global__ void __launch_bounds__(RF_THREADS, 3) k_range_filter(RFArgs a) {
     if (threadIdx.x < G) {
         const int gi = blockIdx.x * G + threadIdx.x;
         int q = -1;
-        if (gi < a.na) {
+        if (gi < (a.dna ? *a.dna : a.na)) {
             q = a.act[gi];
             if (a.qs[q].status != ST_ACTIVE) q = -1;       // stopped at an earlier tree (line 7)
         }
@@ -604,10 +606,11 @@ __global__ void __launch_bounds__(RF_THREADS, 3) k_range_filter(RFArgs a) {
 // After tree t: |S| += number of bits set now but not in `prev` (the first-time members of
 // S <- S u S_i, Alg. 5 line 6), and `prev` catches up.  Grid: (active queries) x (word chunks).
 constexpr int CN_WORDS = 4096;
-__global__ void __launch_bounds__(256) k_count_new(const int* __restrict__ act, QState* __restrict__ qs,
-                                                   const uint32_t* __restrict__ cur, uint32_t* __restrict__ prev,
-                                                   int64_t nwords, int commit) {
+__global__ void __launch_bounds__(256) k_count_new(const int* __restrict__ act, const int* __restrict__ dna,
+                                                   QState* __restrict__ qs, const uint32_t* __restrict__ cur,
+                                                   uint32_t* __restrict__ prev, int64_t nwords, int commit) {
     __shared__ unsigned int s_cnt;
+    if (dna && (int)blockIdx.x >= *dna) return;
     const int q = act[blockIdx.x];
     if (qs[q].status != ST_ACTIVE) return;
     if (commit && !qs[q].doc) return;      // |S| cannot have reached the budget: counted later
@@ -642,8 +645,10 @@ __global__ void __launch_bounds__(256) k_count_new(const int* __restrict__ act, 
 //   k_lbo_cut     the first leaf in that order at which |S| reaches the budget
 //   k_lbo_reset   S <- S before tree t (the prev bitmap)
 //   k_lbo_mark    the members of leaves up to the cut, marked again
-__global__ void k_lbo_cross(const int* __restrict__ act, int na, const QState* __restrict__ qs, int64_t budget,
-                            int* __restrict__ cross, int* __restrict__ ncross) {
+__global__ void k_lbo_cross(const int* __restrict__ act, int na_ub, const int* __restrict__ dna,
+                            const QState* __restrict__ qs, int64_t budget, int* __restrict__ cross,
+                            int* __restrict__ ncross) {
+    const int na = dna ? *dna : na_ub;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < na; i += gridDim.x * blockDim.x) {
         const int q = act[i];
         const QState s = qs[q];
@@ -793,8 +798,9 @@ __global__ void k_lbo_reset(const int* __restrict__ cross, int ncross, const uin
 // Before counting |S| after a tree: the bitmap diff is needed only if the budget may have been
 // reached (|S| <= cnt + marks since the last count) or the count is due (force: end of round,
 // or lb_order, which needs |S| exact after every tree).
-__global__ void k_count_decide(const int* __restrict__ act, int na, QState* __restrict__ qs, int64_t budget,
-                               int force) {
+__global__ void k_count_decide(const int* __restrict__ act, int na_ub, const int* __restrict__ dna,
+                               QState* __restrict__ qs, int64_t budget, int force) {
+    const int na = dna ? *dna : na_ub;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < na; i += gridDim.x * blockDim.x) {
         QState* s = &qs[act[i]];
         const int d = (s->status == ST_ACTIVE && s->pub > 0 && (force || s->cnt + s->pub >= budget)) ? 1 : 0;
@@ -804,8 +810,9 @@ __global__ void k_count_decide(const int* __restrict__ act, int na, QState* __re
 }
 
 // After tree t: the budget test |S| >= ceil(beta n) + k (Alg. 5 line 7, AMB-15/17).
-__global__ void k_tree_end(const int* __restrict__ act, int na, QState* __restrict__ qs, int t, int round,
-                           int64_t budget, int64_t cap) {
+__global__ void k_tree_end(const int* __restrict__ act, int na_ub, const int* __restrict__ dna, QState* __restrict__ qs,
+                           int t, int round, int64_t budget, int64_t cap) {
+    const int na = dna ? *dna : na_ub;
     for (int a_ = blockIdx.x * blockDim.x + threadIdx.x; a_ < na; a_ += gridDim.x * blockDim.x) {
         QState* s = &qs[act[a_]];
         if (s->status != ST_ACTIVE) continue;
@@ -1361,8 +1368,9 @@ __global__ void __launch_bounds__(TK_THREADS) k_topk(const int* __restrict__ act
     }
 }
 
-__global__ void k_compact(const int* __restrict__ act, int na, const QState* __restrict__ qs, int* __restrict__ act_out,
+__global__ void k_compact(const int* __restrict__ act, int na_ub, const int* __restrict__ dna, const QState* __restrict__ qs, int* __restrict__ act_out,
                           int* __restrict__ n_out) {
+    const int na = dna ? *dna : na_ub;
     __shared__ int s_n;
     if (threadIdx.x == 0) s_n = 0;
     __syncthreads();
@@ -1597,7 +1605,7 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
     Scratch s_total(st, sizeof(unsigned long long));
     Scratch s_tk(st, sizeof(unsigned long long) * (size_t)(qb * k));
     Scratch s_qs(st, sizeof(QState) * (size_t)qb);
-    Scratch s_act(st, sizeof(int) * (size_t)(4 * qb + 4));
+    Scratch s_act(st, sizeof(int) * (size_t)(4 * qb + 6));
     Scratch s_ch(st, sizeof(uint32_t) * (size_t)(qb + 2));
     Scratch s_radii(st, sizeof(double) * 64);
     int* act = s_act.as<int>();
@@ -1693,13 +1701,13 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
     Scratch s_lcross(st, sizeof(int) * (size_t)(qb + 1));
     double lbo_rho2 = 0;
     const float* lbo_qp = nullptr;
-    auto lb_order_tree = [&](int t, const int* fa_, int nf_) {
+    auto lb_order_tree = [&](int t, const int* fa_, int nf_, const int* dnf_) {
         int* cross = s_lcross.as<int>();
         int* ncross_d = cross + qb;
         DL_CUDA(cudaMemsetAsync(ncross_d, 0, sizeof(int), st));
-        DL_LAUNCH(k_count_new, dim3((unsigned)nf_, (unsigned)ceil_div(nwords, CN_WORDS)), 256, 0, st, fa_,
+        DL_LAUNCH(k_count_new, dim3((unsigned)nf_, (unsigned)ceil_div(nwords, CN_WORDS)), 256, 0, st, fa_, dnf_,
                   s_qs.as<QState>(), s_bm.as<uint32_t>(), bm_prev, nwords, 0);
-        DL_LAUNCH(k_lbo_cross, (unsigned)ceil_div(nf_, 256), 256, 0, st, fa_, nf_, s_qs.as<QState>(), budget, cross,
+        DL_LAUNCH(k_lbo_cross, (unsigned)ceil_div(nf_, 256), 256, 0, st, fa_, nf_, dnf_, s_qs.as<QState>(), budget, cross,
                   ncross_d);
         int ncross = 0;
         DL_CUDA(cudaMemcpyAsync(&ncross, ncross_d, sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -1785,7 +1793,8 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
             // queries that stop on the budget after tree t (Alg. 5 line 7) leave the filter: the
             // trees after it run over the compacted list of still-active queries (fewer groups)
             int* fa = cur;
-            int nf = na;
+            int nf = na;                   // upper bound of the list's length
+            const int* dnf = nullptr;      // its device count once compacted on the device (no host sync)
             for (int t = 0; t < ix.L && nf > 0; ++t) {
                 ra.tcodes = ix.tcodes.as<uint8_t>() + (int64_t)t * n * ix.K;
                 ra.perm = ix.perm.as<uint32_t>() + (int64_t)t * n;
@@ -1796,13 +1805,14 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
                 ra.act = fa;
                 ra.qp = Qpb;
                 ra.na = nf;
+                ra.dna = dnf;
                 ra.rho2 = rho2;
                 ra.t = t;
                 const int groups = (int)ceil_div(nf, RF_G);
                 if (RF_G == 16) {
                     uint4* gt = s_gtab.as<uint4>();
                     DL_LAUNCH(k_group_table, (unsigned)std::min<int64_t>(ceil_div((int64_t)groups * ix.K * ix.N_r, 256), 148 * 16),
-                              256, 0, st, fa, nf, s_qs.as<QState>(), s_qlut.as<uint16_t>(), LK * ix.N_r, t,
+                              256, 0, st, fa, nf, dnf, s_qs.as<QState>(), s_qlut.as<uint16_t>(), LK * ix.N_r, t,
                               ix.K * ix.N_r, (uint32_t)QuantSpec<RF_G>::CAP, gt);
                     ra.gtab = gt;
                 }
@@ -1811,25 +1821,25 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
                 const int stripes = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(ntiles, RF_THREADS / 32),
                                                                                  (148 * 3 * 4 + groups / 2) / groups));
                 DL_LAUNCH(k_range_filter_sel, dim3((unsigned)groups, (unsigned)stripes), RF_THREADS, rf_smem, st, ra);
-                if (a.lb_order) lb_order_tree(t, fa, nf);
-                DL_LAUNCH(k_count_decide, (unsigned)ceil_div(nf, 256), 256, 0, st, fa, nf, s_qs.as<QState>(), budget,
+                if (a.lb_order) lb_order_tree(t, fa, nf, dnf);
+                DL_LAUNCH(k_count_decide, (unsigned)ceil_div(nf, 256), 256, 0, st, fa, nf, dnf, s_qs.as<QState>(), budget,
                           a.lb_order ? 1 : 0);
-                DL_LAUNCH(k_count_new, dim3((unsigned)nf, (unsigned)ceil_div(nwords, CN_WORDS)), 256, 0, st, fa,
+                DL_LAUNCH(k_count_new, dim3((unsigned)nf, (unsigned)ceil_div(nwords, CN_WORDS)), 256, 0, st, fa, dnf,
                           s_qs.as<QState>(), s_bm.as<uint32_t>(), bm_prev, nwords, 1);
-                DL_LAUNCH(k_tree_end, (unsigned)ceil_div(nf, 256), 256, 0, st, fa, nf, s_qs.as<QState>(), t, m,
+                DL_LAUNCH(k_tree_end, (unsigned)ceil_div(nf, 256), 256, 0, st, fa, nf, dnf, s_qs.as<QState>(), t, m,
                           budget, cap);
                 if (t + 1 < ix.L) {
                     int* fa2 = (fa == fbuf0) ? fbuf1 : fbuf0;
-                    DL_LAUNCH(k_compact, 1, 1024, 0, st, fa, nf, s_qs.as<QState>(), fa2, n_f);
-                    DL_CUDA(cudaMemcpyAsync(&nf, n_f, sizeof(int), cudaMemcpyDeviceToHost, st));
-                    DL_CUDA(cudaStreamSynchronize(st));
+                    int* dn2 = (fa == fbuf0) ? n_f + 1 : n_f;
+                    DL_LAUNCH(k_compact, 1, 1024, 0, st, fa, nf, dnf, s_qs.as<QState>(), fa2, dn2);
                     fa = fa2;
+                    dnf = dn2;
                 }
             }
             tr.mark("filter (L trees)", st);
             // |S| exact for the round's accounting (trees whose count was skipped)
-            DL_LAUNCH(k_count_decide, (unsigned)ceil_div(na, 256), 256, 0, st, cur, na, s_qs.as<QState>(), budget, 1);
-            DL_LAUNCH(k_count_new, dim3((unsigned)na, (unsigned)ceil_div(nwords, CN_WORDS)), 256, 0, st, cur,
+            DL_LAUNCH(k_count_decide, (unsigned)ceil_div(na, 256), 256, 0, st, cur, na, nullptr, s_qs.as<QState>(), budget, 1);
+            DL_LAUNCH(k_count_new, dim3((unsigned)na, (unsigned)ceil_div(nwords, CN_WORDS)), 256, 0, st, cur, nullptr,
                       s_qs.as<QState>(), s_bm.as<uint32_t>(), bm_prev, nwords, 1);
             DL_LAUNCH(k_round_offsets, 1, 1024, 0, st, cur, na, s_qs.as<QState>(), s_total.as<unsigned long long>());
             unsigned long long tot = 0;     // new members of S over the round's queries
@@ -1905,7 +1915,7 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
             DL_LAUNCH(k_topk, (unsigned)na, TK_THREADS, 0, st, cur, s_qs.as<QState>(), va.cand, va.d2,
                       s_tk.as<unsigned long long>(), k, cr2, m, max_rounds);
             tr.mark("top-k", st);
-            DL_LAUNCH(k_compact, 1, 1024, 0, st, cur, na, s_qs.as<QState>(), nxt, n_act);
+            DL_LAUNCH(k_compact, 1, 1024, 0, st, cur, na, nullptr, s_qs.as<QState>(), nxt, n_act);
             DL_CUDA(cudaMemcpyAsync(&na, n_act, sizeof(int), cudaMemcpyDeviceToHost, st));
             DL_CUDA(cudaStreamSynchronize(st));
             std::swap(cur, nxt);

@@ -1571,12 +1571,9 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
     Scratch s_flag(st, sizeof(int));
     DL_CUDA(cudaMemsetAsync(s_flag.p, 0, sizeof(int), st));
     project_rows(ix, d_Q, q_ld, nq, s_qp.as<float>(), a.proj_impl, s_flag.as<int>(), st);
-    {
-        int bad = 0;
-        DL_CUDA(cudaMemcpyAsync(&bad, s_flag.p, sizeof(int), cudaMemcpyDeviceToHost, st));
-        DL_CUDA(cudaStreamSynchronize(st));
-        DL_REQUIRE(!bad, "queries contain NaN or Inf");
-    }
+    // the non-finite flag is read with the first round's total (one host sync fewer); a NaN/Inf
+    // query only yields garbage bounds until then, never an out-of-range access
+    int qflag_checked = 0;
     tr.mark("project queries", st);
 
     // batch size from the memory budget: bitmap + candidate list + distances per query
@@ -1844,8 +1841,12 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
             DL_LAUNCH(k_round_offsets, 1, 1024, 0, st, cur, na, s_qs.as<QState>(), s_total.as<unsigned long long>());
             unsigned long long tot = 0;     // new members of S over the round's queries
             {
+                int bad = 0;
                 DL_CUDA(cudaMemcpyAsync(&tot, s_total.p, sizeof(tot), cudaMemcpyDeviceToHost, st));
+                if (!qflag_checked) DL_CUDA(cudaMemcpyAsync(&bad, s_flag.p, sizeof(int), cudaMemcpyDeviceToHost, st));
                 DL_CUDA(cudaStreamSynchronize(st));
+                DL_REQUIRE(!bad, "queries contain NaN or Inf");
+                qflag_checked = 1;
                 if ((int64_t)tot > round_cap) {
                     round_cap = (int64_t)(tot + tot / 2 + 1024);
                     s_round.alloc((size_t)round_cap * 8);

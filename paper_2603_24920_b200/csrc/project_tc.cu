@@ -39,6 +39,8 @@ struct TcShape {
     int stages;
     uint32_t tmem_cols;
     int N_r;          // > 0: fused Alg. 1 encode, codes instead of projections
+    int streamA;      // 1: the hash matrix does not fit in shared memory -- its k-block is loaded
+                      // into every stage beside the rows (re-read from L2 per tile)
 };
 
 __global__ void __launch_bounds__(TC_THREADS, 1)
@@ -49,8 +51,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     // 1024-byte alignment of every swizzled buffer
     unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const int S = sh.stages;
-    unsigned char* sB = base;                                            // nkb x [npad][128 B]
-    unsigned char* sX = sB + (size_t)sh.nkb * sh.npad * 128;              // S x 16 KB
+    unsigned char* sB = base;                                            // nkb (or S if streamA) x [npad][128 B]
+    unsigned char* sX = sB + (size_t)(sh.streamA ? S : sh.nkb) * sh.npad * 128;   // S x 16 KB
     unsigned char* sL = sX + (size_t)S * TC_STAGE_BYTES;                  // S x 16 KB (lo parts)
     float* sT = reinterpret_cast<float*>(sL + (size_t)S * TC_STAGE_BYTES);   // encode table [LK][N_r]
     const int tab_floats = sh.N_r > 0 ? sh.LK * sh.N_r : 0;
@@ -91,16 +93,20 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 
     if (warp == 0) {
         if (lane == 0) {
-            // the hash matrix, once
-            mbar_expect_tx(bfull, (uint32_t)(sh.nkb * sh.npad * 128));
-            for (int kb = 0; kb < sh.nkb; ++kb) tma_load_2d(sB + (size_t)kb * sh.npad * 128, &tmA, bfull, kb * TC_KB, 0);
+            if (!sh.streamA) {   // the hash matrix, once
+                mbar_expect_tx(bfull, (uint32_t)(sh.nkb * sh.npad * 128));
+                for (int kb = 0; kb < sh.nkb; ++kb) tma_load_2d(sB + (size_t)kb * sh.npad * 128, &tmA, bfull, kb * TC_KB, 0);
+            } else {
+                mbar_arrive(bfull);
+            }
             int s = 0;
             uint32_t ph = 0;
             for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
                 for (int kb = 0; kb < sh.nkb; ++kb) {
                     mbar_wait(&empty[s], ph ^ 1);
-                    mbar_expect_tx(&full[s], TC_STAGE_BYTES);
+                    mbar_expect_tx(&full[s], TC_STAGE_BYTES + (sh.streamA ? (uint32_t)(sh.npad * 128) : 0u));
                     tma_load_2d(sX + (size_t)s * TC_STAGE_BYTES, &tmX, &full[s], kb * TC_KB, (int)(tile * TC_M));
+                    if (sh.streamA) tma_load_2d(sB + (size_t)s * sh.npad * 128, &tmA, &full[s], kb * TC_KB, 0);
                     if (++s == S) { s = 0; ph ^= 1; }
                 }
             }
@@ -124,7 +130,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                     tc_fence_after();
                     const uint32_t ax = smem_u32(sX + (size_t)s * TC_STAGE_BYTES);
                     const uint32_t al = smem_u32(sL + (size_t)s * TC_STAGE_BYTES);
-                    const uint32_t bb = smem_u32(sB + (size_t)kb * sh.npad * 128);
+                    const uint32_t bb = smem_u32(sB + (size_t)(sh.streamA ? s : kb) * sh.npad * 128);
 #pragma unroll
                     for (int k = 0; k < TC_KB / 8; ++k) {        // K = 8 tf32 per MMA = 32 bytes
                         const uint64_t bd = desc_sw128(bb + k * 32);
@@ -269,12 +275,20 @@ static bool launch_tc(const Index& ix, const float* d_X, int64_t ld, int64_t m, 
     sh.npad = (int)round_up(ix.LK, 16);
     sh.N_r = B ? ix.N_r : 0;
     if (sh.npad > 256) return false;
-    const size_t bbytes = (size_t)sh.nkb * sh.npad * 128;
+    const size_t abytes = (size_t)sh.npad * 128;                 // one k-block of the hash matrix
     const size_t tbytes = B ? sizeof(float) * (size_t)ix.LK * ix.N_r : 0;
     const size_t fixed = 1024 /*align*/ + 256 /*barriers*/;
     const size_t budget = 227 * 1024;
-    if (bbytes + tbytes + fixed + 2 * 2 * TC_STAGE_BYTES > budget) return false;
-    sh.stages = (int)std::min<size_t>(6, (budget - bbytes - tbytes - fixed) / (2 * TC_STAGE_BYTES));
+    sh.streamA = (size_t)sh.nkb * abytes + tbytes + fixed + 2 * 2 * TC_STAGE_BYTES > budget ? 1 : 0;
+    if (!sh.streamA) {
+        const size_t bbytes = (size_t)sh.nkb * abytes;
+        sh.stages = (int)std::min<size_t>(6, (budget - bbytes - tbytes - fixed) / (2 * TC_STAGE_BYTES));
+    } else {
+        const size_t per = 2 * TC_STAGE_BYTES + abytes;
+        if (tbytes + fixed + 2 * per > budget) return false;
+        sh.stages = (int)std::min<size_t>(6, (budget - tbytes - fixed) / per);
+    }
+    const size_t bbytes = (size_t)(sh.streamA ? sh.stages : sh.nkb) * abytes;
     uint32_t cols = 32;
     while (cols < (uint32_t)(2 * sh.npad)) cols <<= 1;
     sh.tmem_cols = cols;

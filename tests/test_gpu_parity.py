@@ -437,3 +437,23 @@ def test_lb_order_parity(mode):
         assert np.all(sg["n_cand"][sg["reason"] == 0] <= sp["n_cand"][sg["reason"] == 0])
         nbudget += int((so["reason"] == 0).sum())
     assert nbudget >= 30
+
+
+@pytest.mark.parametrize("d", [960, 1500])
+def test_projection_streamed_hash_matrix(d):
+    """Wide rows (configs[2]: d = 960): the hash matrix no longer fits in shared memory and the
+    tcgen05 projection streams its k-blocks beside the rows; projections, fused-encode codes and
+    row norms against the oracle / numpy."""
+    rng = np.random.default_rng(d)
+    X = np.abs(rng.standard_normal((3000, d))).astype(np.float32)
+    g = P.detlsh_build(X, 4, 16, 256, 9)
+    o = O.Index(X, 4, 16, 256, 9)
+    Pg = g.project(X[:500], proj_impl=0)
+    Po = o.P()[:500]
+    scale = np.maximum(np.abs(Po), np.linalg.norm(X[:500], axis=1)[:, None])
+    assert np.all(np.abs(Pg - Po) <= 1e-4 * scale)
+    assert np.mean(g.codes() != o.codes()) <= 1e-3
+    ig, dg = g.query(X[:20] + 0.01, 5, 1.5, 1e6, 2.0)      # exact-kNN reduction exercises xnorm paths
+    d2 = ((X[:20, None, :].astype(np.float64) + 0.01 - X[None]) ** 2).sum(-1)
+    ref = np.array([np.lexsort((np.arange(len(X)), row))[:5] for row in d2])
+    assert np.array_equal(ig, ref)

@@ -564,6 +564,25 @@ __global__ void k_tile_flags(const uint32_t* __restrict__ leaf_off, int64_t nl, 
     }
 }
 
+// Tight box of each leaf: per dim the smallest and largest code of the leaf's points (contained
+// in the leaf's prefix box, so its lower bound is a tighter valid bound for every member --
+// the range filter prunes with it; the prefix box stays the leaf's box where the method uses it).
+__global__ void k_leaf_tight(const uint32_t* __restrict__ leaf_off, int64_t nl, int K, const uint8_t* __restrict__ tcodes,
+                             uint8_t* __restrict__ tlo, uint8_t* __restrict__ thi) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nl * K; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t l = i / K;
+        const int j = (int)(i - l * K);
+        int a = 255, b = 0;
+        for (uint32_t p = leaf_off[l]; p < leaf_off[l + 1]; ++p) {
+            const int c = tcodes[(int64_t)p * K + j];
+            a = min(a, c);
+            b = max(b, c);
+        }
+        tlo[i] = (uint8_t)a;
+        thi[i] = (uint8_t)b;
+    }
+}
+
 // Box of each query tile: per dim the smallest lo and largest hi over its leaves (the union's
 // bounding box, so its lower bound never exceeds a member leaf's -- the filter skips whole tiles).
 __global__ void k_tile_boxes(const uint32_t* __restrict__ tile_leaf, int64_t ntiles, int K, const uint8_t* __restrict__ lo,
@@ -799,6 +818,10 @@ static bool build_trees_try(Index& ix, const uint8_t* d_EP, int64_t leaf_factor,
     DL_CUDA(cudaMemcpyAsync(begin.data(), s_begin.p, sizeof(unsigned long long) * (L + 1), cudaMemcpyDeviceToHost, st));
     ix.tcodes.alloc((size_t)total * K, st);
     DL_LAUNCH(k_gather_tcodes, grid_for(total, 256), 256, 0, st, perm, d_EP, n, (int)L, K, ix.tcodes.as<uint8_t>());
+    ix.leaf_tlo.alloc((size_t)nl * K, st);
+    ix.leaf_thi.alloc((size_t)nl * K, st);
+    DL_LAUNCH(k_leaf_tight, grid_for(nl * K, 256), 256, 0, st, ix.leaf_off.as<uint32_t>(), nl, K, ix.tcodes.as<uint8_t>(),
+              ix.leaf_tlo.as<uint8_t>(), ix.leaf_thi.as<uint8_t>());
     DL_CUDA(cudaStreamSynchronize(st));
     ix.tree_leaf_begin.assign(begin.begin(), begin.end());
     ix.tree_leaf_begin[L] = nl;
@@ -825,7 +848,7 @@ static bool build_trees_try(Index& ix, const uint8_t* d_EP, int64_t leaf_factor,
         ix.tile_lo.alloc((size_t)ntiles * K, st);
         ix.tile_hi.alloc((size_t)ntiles * K, st);
         DL_LAUNCH(k_tile_boxes, grid_for(ntiles * K, 256), 256, 0, st, ix.tile_leaf.as<uint32_t>(), ntiles, K,
-                  ix.leaf_lo.as<uint8_t>(), ix.leaf_hi.as<uint8_t>(), ix.tile_lo.as<uint8_t>(), ix.tile_hi.as<uint8_t>());
+                  ix.leaf_tlo.as<uint8_t>(), ix.leaf_thi.as<uint8_t>(), ix.tile_lo.as<uint8_t>(), ix.tile_hi.as<uint8_t>());
         ix.point_tile_leaf.alloc(sizeof(uint16_t) * (size_t)total, st);
         DL_LAUNCH(k_point_tile_leaf, grid_for(nl, 256), 256, 0, st, ix.leaf_off.as<uint32_t>(), ix.tile_leaf.as<uint32_t>(),
                   ntiles, nl, ix.point_tile_leaf.as<uint16_t>());

@@ -63,7 +63,8 @@ struct Index {
     DevBuf tile_leaf;       // [ntiles+1] first leaf of each query tile (tree-major; see build.cu)
     std::vector<int64_t> tree_tile_begin;  // [L+1] tile index range of each tree (host copy)
     DevBuf point_tile_leaf; // [L*n] u16: leaf of each point (tree order) within its tile (< 32)
-    DevBuf tile_lo, tile_hi;// [ntiles][K] u8 bounding box of each tile's leaf boxes
+    DevBuf leaf_tlo, leaf_thi;  // [nl_total][K] u8 tight box: min/max code of the leaf's points
+    DevBuf tile_lo, tile_hi;// [ntiles][K] u8 bounding box of each tile's tight leaf boxes
     DevBuf xnorm;           // [n] fp32 ||x||^2 of every row (tensor-core verification, verify_tc.cu)
     bool keep_proj = false; // build option: keep the projections (EXACT mode)
     DevBuf proj;            // [n][LK] fp32 projections p' in data order (EXACT mode only)

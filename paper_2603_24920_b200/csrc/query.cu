@@ -299,6 +299,8 @@ __global__ void __launch_bounds__(RF_THREADS, 3) k_range_filter(RFArgs a) {
                 pass = acc <= QT;
             }
             tm = __ballot_sync(0xffffffffu, pass);
+            // tile boxes bound the tight leaf boxes; RELAXED decides leaves by their prefix boxes
+            if (a.mode == DETLSH_MODE_RELAXED) tm = amask;
         }
         if (tm == 0) continue;
         // leaf lower bounds (Alg. 3 pruning, Fig. dist): lane = leaf, quantised, one query of the
@@ -1634,8 +1636,10 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
     RFArgs ra;
     ra.gtab = nullptr;
     ra.leaf_off = ix.leaf_off.as<uint32_t>();
-    ra.lo = ix.leaf_lo.as<uint8_t>();
-    ra.hi = ix.leaf_hi.as<uint8_t>();
+    // leaf pruning uses the tight boxes (a valid, tighter bound for every member); RELAXED takes
+    // whole leaves by the leaf's own (prefix) box, as the method defines it
+    ra.lo = (a.mode == DETLSH_MODE_RELAXED ? ix.leaf_lo : ix.leaf_tlo).as<uint8_t>();
+    ra.hi = (a.mode == DETLSH_MODE_RELAXED ? ix.leaf_hi : ix.leaf_thi).as<uint8_t>();
     ra.tile_leaf = ix.tile_leaf.as<uint32_t>();
     ra.tile_lo = ix.tile_lo.as<uint8_t>();
     ra.tile_hi = ix.tile_hi.as<uint8_t>();

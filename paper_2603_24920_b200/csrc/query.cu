@@ -427,42 +427,58 @@ __global__ void __launch_bounds__(RF_THREADS, 3) k_range_filter(RFArgs a) {
                 pre[lane] = incl - sz;
                 offs[lane] = my_off;
                 __syncwarp();
-                for (uint32_t c0 = 0; c0 < T; c0 += 32) {
-                    const uint32_t i = c0 + lane;
-                    bool band = false;
-                    uint32_t p = P0;
-                    if (i < T) {
-                        int l = 0;      // the leaf holding packed point i: last l with pre[l] <= i
+                // two packed points per lane per iteration: both searches and both code loads are
+                // issued before either sum (two independent latency chains)
+                for (uint32_t c0 = 0; c0 < T; c0 += 64) {
+                    uint32_t pp[2] = {P0, P0};
+                    uint4 cc[2];
+                    bool valid[2];
 #pragma unroll
-                        for (int st = 16; st > 0; st >>= 1)
-                            if (pre[l + st] <= i) l += st;
-                        p = offs[l] + (i - pre[l]);
-                        const int64_t pos = (int64_t)p - a.pos_base;
-                        const uint4 c4 = *reinterpret_cast<const uint4*>(a.tcodes + pos * 16);
-                        uint32_t acc = 0;
+                    for (int u = 0; u < 2; ++u) {
+                        const uint32_t i = c0 + 32 * u + lane;
+                        valid[u] = i < T;
+                        cc[u] = make_uint4(0, 0, 0, 0);
+                        if (valid[u]) {
+                            int l = 0;      // the leaf holding packed point i: last l with pre[l] <= i
 #pragma unroll
-                        for (int j = 0; j < 16; ++j) {
-                            const uint32_t word = (j >> 2) == 0 ? c4.x : (j >> 2) == 1 ? c4.y : (j >> 2) == 2 ? c4.z : c4.w;
-                            const uint32_t code = (word >> (8 * (j & 3))) & 255u;
-                            acc += G == 8 ? (uint32_t)s_h[(j * N_r + code) * 8 + g] : (uint32_t)s_b[(j * N_r + code) * 16 + g];
-                        }
-                        ++c_pt;
-                        const bool ok = acc <= QT, sure = acc + 17 <= QT;
-                        if (a.mode == DETLSH_MODE_CELL && sure) {
-                            ++c_pp;
-                            atomicAdd(&s_pass[g], 1u);
-                            const uint32_t id = a.perm[pos];
-                            atomicOr(a.bitmap + (int64_t)s_q[g] * a.nwords + (id >> 5), 1u << (id & 31));  // RED.OR
-                        } else {
-                            band = ok;      // CELL: inside the band; EXACT: every survivor
+                            for (int st = 16; st > 0; st >>= 1)
+                                if (pre[l + st] <= i) l += st;
+                            pp[u] = offs[l] + (i - pre[l]);
+                            cc[u] = *reinterpret_cast<const uint4*>(a.tcodes + ((int64_t)pp[u] - a.pos_base) * 16);
                         }
                     }
-                    const uint32_t bal = __ballot_sync(0xffffffffu, band);
-                    if (band) bq[qn_ + __popc(bal & lanemask_lt())] = ((p - P0) << 4) | (uint32_t)g;
-                    qn_ += __popc(bal);
-                    __syncwarp();
-                    if (qn_ >= 32) flush(32);
-                    __syncwarp();
+#pragma unroll
+                    for (int u = 0; u < 2; ++u) {
+                        bool band = false;
+                        const uint32_t p = pp[u];
+                        if (valid[u]) {
+                            const int64_t pos = (int64_t)p - a.pos_base;
+                            const uint4 c4 = cc[u];
+                            uint32_t acc = 0;
+#pragma unroll
+                            for (int j = 0; j < 16; ++j) {
+                                const uint32_t word = (j >> 2) == 0 ? c4.x : (j >> 2) == 1 ? c4.y : (j >> 2) == 2 ? c4.z : c4.w;
+                                const uint32_t code = (word >> (8 * (j & 3))) & 255u;
+                                acc += G == 8 ? (uint32_t)s_h[(j * N_r + code) * 8 + g] : (uint32_t)s_b[(j * N_r + code) * 16 + g];
+                            }
+                            ++c_pt;
+                            const bool ok = acc <= QT, sure = acc + 17 <= QT;
+                            if (a.mode == DETLSH_MODE_CELL && sure) {
+                                ++c_pp;
+                                atomicAdd(&s_pass[g], 1u);
+                                const uint32_t id = a.perm[pos];
+                                atomicOr(a.bitmap + (int64_t)s_q[g] * a.nwords + (id >> 5), 1u << (id & 31));  // RED.OR
+                            } else {
+                                band = ok;      // CELL: inside the band; EXACT: every survivor
+                            }
+                        }
+                        const uint32_t bal = __ballot_sync(0xffffffffu, band);
+                        if (band) bq[qn_ + __popc(bal & lanemask_lt())] = ((p - P0) << 4) | (uint32_t)g;
+                        qn_ += __popc(bal);
+                        __syncwarp();
+                        if (qn_ >= 32) flush(32);
+                        __syncwarp();
+                    }
                 }
             }
         } else {

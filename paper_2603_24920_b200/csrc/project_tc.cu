@@ -18,6 +18,8 @@
 //   warps 4-7   epilogue: tcgen05.ld (32x32b) of the double-buffered accumulator, rows to P.
 #include <cuda.h>
 
+#include <cstdlib>
+
 #include "index.cuh"
 #include "tc_util.cuh"
 
@@ -28,7 +30,9 @@ using namespace tc;
 
 constexpr int TC_M = 128;           // rows per tile (UMMA M)
 constexpr int TC_KB = 32;           // fp32 per k-block (= 128 B, one swizzle row)
-constexpr int TC_THREADS = 256;
+constexpr int TC_THREADS = 448;    // 14 warps: producer, MMA, 4 converters (2-3, 12-13), 8 epilogue (4-11)
+constexpr int TC_CONV = 128;       // converter threads
+constexpr int TC_EPI = 256;        // epilogue threads
 constexpr int TC_STAGE_BYTES = TC_M * TC_KB * 4;   // 16 KB
 
 struct TcShape {
@@ -41,6 +45,7 @@ struct TcShape {
     int N_r;          // > 0: fused Alg. 1 encode, codes instead of projections
     int streamA;      // 1: the hash matrix does not fit in shared memory -- its k-block is loaded
                       // into every stage beside the rows (re-read from L2 per tile)
+    int dbg;          // experiments only (DETLSH_PROJ_DEBUG): 1 no encode search, 2 no conversion, 4 no MMA
 };
 
 __global__ void __launch_bounds__(TC_THREADS, 1)
@@ -49,7 +54,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                  uint8_t* __restrict__ EP, float* __restrict__ xnorm) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     // 1024-byte alignment of every swizzled buffer
-    unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    // 1024-byte aligned, by pointer arithmetic on the shared array (keeps the shared address
+    // space: LDS/STS instead of generic LD/ST)
+    unsigned char* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     const int S = sh.stages;
     unsigned char* sB = base;                                            // nkb (or S if streamA) x [npad][128 B]
     unsigned char* sX = sB + (size_t)(sh.streamA ? S : sh.nkb) * sh.npad * 128;   // S x 16 KB
@@ -71,12 +78,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&conv[s], 64);
+            mbar_init(&conv[s], TC_CONV);
             mbar_init(&empty[s], 1);
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(&tfull[b], 1);
-            mbar_init(&tempty[b], 128);
+            mbar_init(&tempty[b], TC_EPI);
         }
         mbar_init(bfull, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -131,6 +138,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                     const uint32_t ax = smem_u32(sX + (size_t)s * TC_STAGE_BYTES);
                     const uint32_t al = smem_u32(sL + (size_t)s * TC_STAGE_BYTES);
                     const uint32_t bb = smem_u32(sB + (size_t)(sh.streamA ? s : kb) * sh.npad * 128);
+                    if (!(sh.dbg & 4))
 #pragma unroll
                     for (int k = 0; k < TC_KB / 8; ++k) {        // K = 8 tf32 per MMA = 32 bytes
                         const uint64_t bd = desc_sw128(bb + k * 32);
@@ -144,25 +152,25 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                 if (++buf == 2) { buf = 0; tph ^= 1; }
             }
         }
-    } else if (warp < 4) {
-        // converters: lo = x - trunc_tf32(x), same swizzled offsets.  Thread t sees float4
-        // t + 64 m (m < 16) of every stage, i.e. rows t/8 + 8 m (swizzling permutes 16-byte
+    } else if (warp < 4 || warp >= 12) {
+        // converters (128 threads): lo = x - trunc_tf32(x), same swizzled offsets.  Thread t sees
+        // float4 t + 128 m (m < 8) of every stage, i.e. rows t/8 + 16 m (swizzling permutes 16-byte
         // chunks only within a row), so it also accumulates those rows' ||x||^2 (xnorm != null).
-        const int t = threadIdx.x - 64;
+        const int t = warp < 4 ? threadIdx.x - 64 : threadIdx.x - 384 + 64;
         int s = 0;
         uint32_t ph = 0;
         bool bad = false;
         for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-            float nacc[16];
+            float nacc[8];
 #pragma unroll
-            for (int m = 0; m < 16; ++m) nacc[m] = 0.f;
+            for (int m = 0; m < 8; ++m) nacc[m] = 0.f;
             for (int kb = 0; kb < sh.nkb; ++kb) {
                 mbar_wait(&full[s], ph);
                 const float4* src = reinterpret_cast<const float4*>(sX + (size_t)s * TC_STAGE_BYTES);
                 float4* dst = reinterpret_cast<float4*>(sL + (size_t)s * TC_STAGE_BYTES);
 #pragma unroll
-                for (int m = 0; m < 16; ++m) {
-                    const int i = t + 64 * m;
+                for (int m = 0; m < ((sh.dbg & 2) ? 0 : 8); ++m) {
+                    const int i = t + TC_CONV * m;
                     const float4 x = src[i];
                     float4 lo;
                     lo.x = x.x - __uint_as_float(__float_as_uint(x.x) & 0xFFFFE000u);
@@ -179,28 +187,29 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             }
             if (xnorm) {
 #pragma unroll
-                for (int m = 0; m < 16; ++m) {
+                for (int m = 0; m < 8; ++m) {
                     float v = nacc[m];
                     v += __shfl_xor_sync(0xffffffffu, v, 1);
                     v += __shfl_xor_sync(0xffffffffu, v, 2);
                     v += __shfl_xor_sync(0xffffffffu, v, 4);
-                    const int64_t row = tile * TC_M + (t >> 3) + 8 * m;
+                    const int64_t row = tile * TC_M + (t >> 3) + 16 * m;
                     if ((t & 7) == 0 && row < sh.m) xnorm[row] = v;
                 }
             }
         }
         if (bad) atomicOr(nonfinite, 1);
     } else {
-        // epilogue: TMEM -> registers -> P rows, or (fused Alg. 1) -> 8-bit codes
-        const int ew = warp - 4;                           // TMEM lane quarter
+        // epilogue (warps 4-11): TMEM -> registers -> P rows, or (fused Alg. 1) -> 8-bit codes;
+        // TMEM lane quarter ew = warp % 4, the two warps of a quarter take alternate 16-column chunks
+        const int ew = warp & 3, eh = (warp - 4) >> 2;
         const int row_in_tile = ew * 32 + lane;
         const int N_r = sh.N_r;
         if (N_r > 0) {   // breakpoint table: c[r][t] = b_{t+1} (t < N_r-1), c[r][N_r-1] = +inf (AMB-6/7)
-            for (int i = threadIdx.x - 128; i < tab_floats; i += 128) {
+            for (int i = threadIdx.x - 128; i < tab_floats; i += TC_EPI) {
                 const int r = i / N_r, t = i - r * N_r;
                 sT[i] = t < N_r - 1 ? B[(int64_t)r * (N_r + 1) + t + 1] : __int_as_float(0x7f800000);
             }
-            asm volatile("bar.sync 1, 128;" ::: "memory");  // epilogue warps only
+            asm volatile("bar.sync 1, 256;" ::: "memory");  // epilogue warps only
         }
         int buf = 0;
         uint32_t tph = 0;
@@ -209,7 +218,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             tc_fence_after();
             const int64_t row = tile * TC_M + row_in_tile;
             const uint32_t taddr = tmem_base + (uint32_t)(buf * sh.npad) + ((uint32_t)(ew * 32) << 16);
-            for (int c0 = 0; c0 < sh.npad; c0 += 16) {
+            for (int c0 = 16 * eh; c0 < sh.npad; c0 += 32) {
                 float v[16];
                 tmem_ld16(taddr + c0, v);
                 if (N_r > 0) {
@@ -218,7 +227,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                     int pos[16];
 #pragma unroll
                     for (int i = 0; i < 16; ++i) pos[i] = 0;
-                    for (int s = N_r >> 1; s > 0; s >>= 1) {
+                    for (int s = (sh.dbg & 1) ? 0 : N_r >> 1; s > 0; s >>= 1) {
 #pragma unroll
                         for (int i = 0; i < 16; ++i) {
                             const int r = min(c0 + i, sh.LK - 1);
@@ -233,7 +242,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                         if (c0 + 16 <= sh.LK && (sh.LK & 15) == 0) {
                             *reinterpret_cast<uint4*>(out) = make_uint4(packed[0], packed[1], packed[2], packed[3]);
                         } else {
-                            for (int i = 0; i < 16 && c0 + i < sh.LK; ++i) out[i] = (uint8_t)(packed[i >> 2] >> (8 * (i & 3)));
+#pragma unroll
+                            for (int i = 0; i < 16; ++i)
+                                if (c0 + i < sh.LK) out[i] = (uint8_t)(packed[i >> 2] >> (8 * (i & 3)));
                         }
                     }
                 }
@@ -244,7 +255,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                         for (int i = 0; i < 16; i += 4)
                             *reinterpret_cast<float4*>(out + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
                     } else {
-                        for (int i = 0; i < 16 && c0 + i < sh.LK; ++i) out[i] = v[i];
+#pragma unroll
+                        for (int i = 0; i < 16; ++i)
+                            if (c0 + i < sh.LK) out[i] = v[i];
                     }
                 }
             }
@@ -279,7 +292,10 @@ static bool launch_tc(const Index& ix, const float* d_X, int64_t ld, int64_t m, 
     const size_t tbytes = B ? sizeof(float) * (size_t)ix.LK * ix.N_r : 0;
     const size_t fixed = 1024 /*align*/ + 256 /*barriers*/;
     const size_t budget = 227 * 1024;
-    sh.streamA = (size_t)sh.nkb * abytes + tbytes + fixed + 2 * 2 * TC_STAGE_BYTES > budget ? 1 : 0;
+    static const int force_stream = std::getenv("DETLSH_STREAM_A") ? std::atoi(std::getenv("DETLSH_STREAM_A")) : 0;
+    static const int pdbg = std::getenv("DETLSH_PROJ_DEBUG") ? std::atoi(std::getenv("DETLSH_PROJ_DEBUG")) : 0;
+    sh.dbg = pdbg;
+    sh.streamA = (force_stream || (size_t)sh.nkb * abytes + tbytes + fixed + 2 * 2 * TC_STAGE_BYTES > budget) ? 1 : 0;
     if (!sh.streamA) {
         const size_t bbytes = (size_t)sh.nkb * abytes;
         sh.stages = (int)std::min<size_t>(6, (budget - bbytes - tbytes - fixed) / (2 * TC_STAGE_BYTES));

@@ -61,7 +61,9 @@ __global__ void __launch_bounds__(VT_THREADS, 1)
                 const __grid_constant__ CUtensorMap tmBO, VtcShape sh, const float* __restrict__ xn,
                 const float* __restrict__ qn, uint32_t* __restrict__ cand, float* __restrict__ d2) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
-    unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    // 1024-byte aligned, by pointer arithmetic on the shared array (keeps the shared address
+    // space: LDS/STS instead of generic LD/ST)
+    unsigned char* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     const int S = sh.stages, N = sh.N;
     const size_t qbytes = (size_t)N * VT_KB * 4;
     const size_t stage_bytes = 2 * (size_t)VT_XSTAGE + 2 * qbytes;

@@ -231,7 +231,14 @@ __global__ void k_first_key(const uint8_t* __restrict__ EP, int64_t n, int L, in
         const int64_t id = g - (int64_t)t * n;
         const uint8_t* c = EP + id * LK + t * K;
         uint32_t key = 0;
-        for (int j = 0; j < K; ++j) key = (key << 1) | ((c[j] >> (nb - 1)) & 1u);
+        if (K == 16 && (LK & 15) == 0) {          // one 16-byte load of the tree's codes
+            const uint4 c4 = *reinterpret_cast<const uint4*>(c);
+            const uint32_t w[4] = {c4.x, c4.y, c4.z, c4.w};
+#pragma unroll
+            for (int j = 0; j < 16; ++j) key = (key << 1) | ((w[j >> 2] >> (8 * (j & 3) + nb - 1)) & 1u);
+        } else {
+            for (int j = 0; j < K; ++j) key = (key << 1) | ((c[j] >> (nb - 1)) & 1u);
+        }
         keys[g] = key;
         vals[g] = (uint32_t)id;
     }
@@ -569,6 +576,35 @@ __global__ void k_tile_flags(const uint32_t* __restrict__ leaf_off, int64_t nl, 
 // the range filter prunes with it; the prefix box stays the leaf's box where the method uses it).
 __global__ void k_leaf_tight(const uint32_t* __restrict__ leaf_off, int64_t nl, int K, const uint8_t* __restrict__ tcodes,
                              uint8_t* __restrict__ tlo, uint8_t* __restrict__ thi) {
+    if (K == 16) {    // 4 lanes per leaf: 16-byte code rows, byte-wise min/max, 2-step shuffle reduction
+        const int sub = threadIdx.x & 3;
+        for (int64_t l = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 2; (l & ~(int64_t)7) < nl;
+             l += ((int64_t)gridDim.x * blockDim.x) >> 2) {   // warp-uniform condition (8 leaves per warp)
+            const bool live = l < nl;            // whole warps stay in the loop for the shuffles
+            uint4 mn = make_uint4(~0u, ~0u, ~0u, ~0u), mx = make_uint4(0, 0, 0, 0);
+            if (live)
+                for (uint32_t p = leaf_off[l] + sub; p < leaf_off[l + 1]; p += 4) {
+                    const uint4 c = *reinterpret_cast<const uint4*>(tcodes + (int64_t)p * 16);
+                    mn = make_uint4(__vminu4(mn.x, c.x), __vminu4(mn.y, c.y), __vminu4(mn.z, c.z), __vminu4(mn.w, c.w));
+                    mx = make_uint4(__vmaxu4(mx.x, c.x), __vmaxu4(mx.y, c.y), __vmaxu4(mx.z, c.z), __vmaxu4(mx.w, c.w));
+                }
+            for (int o = 1; o < 4; o <<= 1) {
+                mn.x = __vminu4(mn.x, __shfl_xor_sync(0xffffffffu, mn.x, o));
+                mn.y = __vminu4(mn.y, __shfl_xor_sync(0xffffffffu, mn.y, o));
+                mn.z = __vminu4(mn.z, __shfl_xor_sync(0xffffffffu, mn.z, o));
+                mn.w = __vminu4(mn.w, __shfl_xor_sync(0xffffffffu, mn.w, o));
+                mx.x = __vmaxu4(mx.x, __shfl_xor_sync(0xffffffffu, mx.x, o));
+                mx.y = __vmaxu4(mx.y, __shfl_xor_sync(0xffffffffu, mx.y, o));
+                mx.z = __vmaxu4(mx.z, __shfl_xor_sync(0xffffffffu, mx.z, o));
+                mx.w = __vmaxu4(mx.w, __shfl_xor_sync(0xffffffffu, mx.w, o));
+            }
+            if (live && sub == 0) {
+                *reinterpret_cast<uint4*>(tlo + l * 16) = mn;
+                *reinterpret_cast<uint4*>(thi + l * 16) = mx;
+            }
+        }
+        return;
+    }
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nl * K; i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t l = i / K;
         const int j = (int)(i - l * K);
@@ -820,7 +856,8 @@ static bool build_trees_try(Index& ix, const uint8_t* d_EP, int64_t leaf_factor,
     DL_LAUNCH(k_gather_tcodes, grid_for(total, 256), 256, 0, st, perm, d_EP, n, (int)L, K, ix.tcodes.as<uint8_t>());
     ix.leaf_tlo.alloc((size_t)nl * K, st);
     ix.leaf_thi.alloc((size_t)nl * K, st);
-    DL_LAUNCH(k_leaf_tight, grid_for(nl * K, 256), 256, 0, st, ix.leaf_off.as<uint32_t>(), nl, K, ix.tcodes.as<uint8_t>(),
+    DL_LAUNCH(k_leaf_tight, grid_for(K == 16 ? nl * 4 : nl * K, 256), 256, 0, st, ix.leaf_off.as<uint32_t>(), nl, K,
+              ix.tcodes.as<uint8_t>(),
               ix.leaf_tlo.as<uint8_t>(), ix.leaf_thi.as<uint8_t>());
     DL_CUDA(cudaStreamSynchronize(st));
     ix.tree_leaf_begin.assign(begin.begin(), begin.end());

@@ -254,6 +254,9 @@ typedef struct {
     double  total_ms;
 } detlsh_kernel_time;
 void    detlsh_profile_enable(int32_t on);
+/* Time only kernels whose name starts with one of the comma-separated prefixes (NULL or "":
+   every kernel); fewer event records keep the timed region close to an unprofiled run. */
+void    detlsh_profile_filter(const char* prefixes);
 void    detlsh_profile_reset(void);
 int32_t detlsh_profile_read(detlsh_kernel_time* out, int32_t cap);
 

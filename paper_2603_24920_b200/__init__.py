@@ -7,4 +7,4 @@ from .detlsh import (DetlshError, Index, MODE_CELL, MODE_EXACT, MODE_RELAXED, ST
                      detlsh_breakpoints_from_samples, detlsh_build, detlsh_build_from_codes,
                      detlsh_load, detlsh_merge_topk, detlsh_params, detlsh_query, detlsh_query_ex,
                      detlsh_sample_projections, detlsh_sample_size, launch_count, lib, profile_enable,
-                     profile_read, profile_reset, release_workspace, workspace_bytes)
+                     profile_filter, profile_read, profile_reset, release_workspace, workspace_bytes)

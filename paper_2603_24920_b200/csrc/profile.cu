@@ -2,6 +2,7 @@
 // roofline numbers).  Off by default; when on, every DL_LAUNCH records an event pair on
 // its own stream.
 #include <chrono>
+#include <cstring>
 #include <cstdlib>
 #include <map>
 #include <mutex>
@@ -28,6 +29,7 @@ struct Agg {
     double ms = 0;
 };
 std::map<std::string, Agg> g_agg;
+std::vector<std::string> g_filter;   // name prefixes to time (empty: every kernel)
 
 cudaEvent_t take_event() {
     if (!g_pool.empty()) {
@@ -67,6 +69,11 @@ void drain_locked() {
 
 void profile_begin(cudaStream_t st, const char* name, int* slot) {
     std::lock_guard<std::mutex> lk(g_mu);
+    if (!g_filter.empty()) {
+        bool hit = false;
+        for (const auto& f : g_filter) hit |= std::strncmp(name, f.c_str(), f.size()) == 0;
+        if (!hit) return;
+    }
     if (g_recs.size() > 100000) drain_locked();
     Rec r{name, take_event(), take_event(), false};
     cudaEventRecord(r.a, st);
@@ -102,6 +109,22 @@ extern "C" {
 void detlsh_profile_enable(int32_t on) {
     std::lock_guard<std::mutex> lk(g_mu);
     g_profile.store(on ? 1 : 0);
+}
+
+void detlsh_profile_filter(const char* prefixes) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    g_filter.clear();
+    if (!prefixes) return;
+    std::string cur;
+    for (const char* c = prefixes;; ++c) {
+        if (*c == ',' || *c == 0) {
+            if (!cur.empty()) g_filter.push_back(cur);
+            cur.clear();
+            if (*c == 0) break;
+        } else {
+            cur.push_back(*c);
+        }
+    }
 }
 
 void detlsh_profile_reset(void) {

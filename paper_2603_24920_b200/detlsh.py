@@ -96,6 +96,7 @@ def lib():
         "detlsh_load": (i32, [C.c_char_p, P]),
         "detlsh_index_info": (i32, [P, P]),
         "detlsh_profile_enable": (None, [i32]),
+        "detlsh_profile_filter": (None, [C.c_char_p]),
         "detlsh_profile_reset": (None, []),
         "detlsh_release_workspace": (None, []),
         "detlsh_workspace_bytes": (i64, []),
@@ -164,6 +165,10 @@ def release_workspace():
 
 def workspace_bytes() -> int:
     return int(lib().detlsh_workspace_bytes())
+
+
+def profile_filter(prefixes: str | None):
+    lib().detlsh_profile_filter(prefixes.encode() if prefixes else None)
 
 
 def profile_reset():

@@ -32,12 +32,12 @@ import datagen  # noqa: E402
 METRIC = "queries/s at recall@k>=0.9"
 
 
-def load_rmin(cid: int) -> float:
+def load_rmin(cid: int, which: str = "bench") -> float:
     """The radius both arms run at: r_bench = r_min c^-m* (the operating point the ORACLE picked,
     tools/make_rmin.py --point: largest m with oracle recall >= 0.95 on held-out sample queries;
     SURVEY 8(d)), else the AMB-22 r_min itself."""
     e = json.load(open(os.path.join(ROOT, "bench_configs.json")))[str(cid)]
-    return float(e.get("r_bench", e["r_min"]))
+    return float(e["r_min"] if which == "amb22" else e.get("r_bench", e["r_min"]))
 
 
 def rmin_info(cid: int) -> dict:
@@ -204,7 +204,7 @@ def run_reference(args, cfg):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    r_min = load_rmin(args.config)
+    r_min = load_rmin(args.config, args.radius)
     D = datagen.generate(cfg)
     X, Q = D["X"], D["Q"]
     t0 = time.perf_counter()
@@ -258,6 +258,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--proj-impl", type=int, default=None)
     ap.add_argument("--recall-queries", type=int, default=200)
+    ap.add_argument("--radius", default="bench", choices=["bench", "amb22"],
+                    help="bench: the oracle-chosen operating point r_bench; amb22: the AMB-22 r_min itself")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     cfg = datagen.CONFIGS[args.config]
@@ -275,7 +277,7 @@ def main():
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    r_min = load_rmin(args.config)
+    r_min = load_rmin(args.config, args.radius)
     Dd = datagen.generate(cfg)
     X, Q = Dd["X"], Dd["Q"]
     lo, hi = PD.shard_range(cfg.n, world, rank)

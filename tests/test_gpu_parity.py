@@ -457,3 +457,55 @@ def test_projection_streamed_hash_matrix(d):
     d2 = ((X[:20, None, :].astype(np.float64) + 0.01 - X[None]) ** 2).sum(-1)
     ref = np.array([np.lexsort((np.arange(len(X)), row))[:5] for row in d2])
     assert np.array_equal(ig, ref)
+
+
+@pytest.mark.slow
+def test_config5_full_size_properties():
+    """configs[4] at full size (n = 100M, d = 96, L = 6, beta = 0.05; 38.4 GB of data).  The oracle
+    cannot build this index in a test run (fp64 single thread: hours), so the check is by
+    properties that hold at any size: the hash family bit-exact with the oracle's generator;
+    sampled projections against numpy fp64; every returned distance the exact Euclidean distance
+    of its id, ascending; the stop rules (budget: |S| >= ceil(beta n) + k; radius: k-th distance
+    <= c r, AMB-18); recall against numpy brute force reported.  r_min from the GPU estimator
+    (an input of the GPU path only; no oracle value involved)."""
+    import math
+    import torch
+    D = datagen.generate(5, nq=1000, with_sample_queries=50)
+    c = D["cfg"]
+    X, Q = D["X"], D["Q"]
+    n = X.shape[0]
+    Xd = torch.from_numpy(X).cuda()
+    g = P.detlsh_build(Xd, c.L, c.K, c.N_r, c.index_seed, opts=P.default_opts(borrow_data=1))
+    assert np.array_equal(g.A(), O.hash_family(c.index_seed, c.d, c.L, c.K))
+    sel = np.random.default_rng(3).choice(n, 2000, replace=False)
+    Pg = g.project(X[sel])
+    Po = X[sel].astype(np.float64) @ g.A().astype(np.float64).T
+    assert np.all(np.abs(Pg - Po) <= 1e-4 * np.maximum(np.abs(Po), np.linalg.norm(X[sel], axis=1)[:, None]))
+    r = g.estimate_rmin(D["Qs"], c.k, c.beta)
+    ig, dg, st = g.query(Q, c.k, c.c, r, c.beta, stats=True)
+    B = math.ceil(c.beta * n) + c.k
+    bud, rad = st["reason"] == 0, st["reason"] == 1
+    assert np.all(st["n_cand"][bud] >= B)
+    assert np.all(dg[rad, -1].astype(np.float64) <= c.c * st["r_final"][rad] * (1 + 1e-6))
+    qs = np.random.default_rng(4).choice(len(Q), 40, replace=False)
+    for q in qs:
+        ok = ig[q] >= 0
+        d_ex = np.sqrt(((X[ig[q][ok]].astype(np.float64) - Q[q]) ** 2).sum(1))
+        assert np.allclose(dg[q][ok], d_ex, rtol=1e-4, atol=1e-6)
+        assert np.all(np.diff(dg[q][ok]) >= 0)
+    norms = np.einsum("ij,ij->i", X, X, dtype=np.float64)
+    best = None
+    for s0 in range(0, n, 10_000_000):
+        blk = X[s0:s0 + 10_000_000]
+        d2 = norms[s0:s0 + len(blk)][None, :] - 2.0 * (Q[qs] @ blk.T).astype(np.float64)
+        part = np.argpartition(d2, c.k, axis=1)[:, :c.k] + s0
+        best = part if best is None else np.concatenate([best, part], 1)
+    gt = []
+    for i, q in enumerate(qs):
+        cand = np.unique(best[i])
+        d2 = ((X[cand].astype(np.float64) - Q[q]) ** 2).sum(1)
+        gt.append(cand[np.lexsort((cand, d2))[:c.k]])
+    rec = np.mean([len(set(ig[q]) & set(gt[i])) / c.k for i, q in enumerate(qs)])
+    print(f"cfg5 n={n}: r_min {r:.4g}, recall@{c.k} vs brute force on 40 queries {rec:.3f}, "
+          f"stops {np.bincount(st['reason'], minlength=3)}, mean |S| {st['n_cand'].mean():.0f}")
+    assert rec > 0

@@ -324,7 +324,7 @@ def main():
     time.sleep(0.3)
     P.profile_reset()
     # CUDA events around the modelled kernels only (every launch timed adds host work per launch)
-    P.profile_filter("k_range_filter,k_verify,k_project_tc,k_topk")
+    P.profile_filter("k_range_filter,k_leaf_points,k_verify,k_project_tc,k_topk")
     P.profile_enable(True)
     l0 = P.launch_count()
     evs = [step(True) for _ in range(args.steps)]

@@ -171,10 +171,13 @@ struct RFArgs {
     float rho2;
     int t, L, K, N_r, mode;
     int pq_cost;                // per-query path cost per 32-point step, relative to 170 per SIMD chunk
+    uint32_t* plist;            // CELL, sparse tiles: per-query lists of reachable leaves [Qb][pcap] (or null)
+    uint32_t* pcnt;             // [Qb] list lengths
+    int64_t pcap;
     unsigned long long* ctr;    // [Qb][4] filter counters
 };
 
-template <int KT, int NRT, int G>
+template <int KT, int NRT, int G, bool PQ>
 __global__ void __launch_bounds__(RF_THREADS, 3) k_range_filter(RFArgs a) {
     constexpr uint32_t QT = QuantSpec<G>::QT, CAP = QuantSpec<G>::CAP;
     extern __shared__ __align__(16) unsigned char smem[];
@@ -396,11 +399,13 @@ __global__ void __launch_bounds__(RF_THREADS, 3) k_range_filter(RFArgs a) {
         //        queries) -- best when each point is needed by many of the group's queries;
         //  per-query  for each query, only the points of ITS reachable leaves, packed 32 to a
         //        step -- best at small radii, where a point is needed by ~2 of 16 queries.
-        // Chosen per tile from the instruction costs (~170 per SIMD chunk, ~120 per query step,
-        // measured on B200: 163K -> 166K q/s at the bench point).
+        // Chosen per tile from a cost ratio fitted on B200 (pq_cost 40 against 170 per SIMD chunk).
+        // In CELL mode the per-query work of sparse tiles is handed to k_leaf_points as
+        // (query, reachable leaf) pairs (high-occupancy kernel, coalesced leaf reads); the in-kernel
+        // per-query path serves EXACT.
         bool use_pq = false;
         uint32_t my_off = P1, my_sz = 0;
-        if (KT == 16 && a.mode != DETLSH_MODE_RELAXED) {
+        if (PQ && KT == 16 && a.mode != DETLSH_MODE_RELAXED) {
             if (lane < nlt) {
                 my_off = a.leaf_off[lb + lane];
                 my_sz = a.leaf_off[lb + lane + 1] - my_off;
@@ -409,7 +414,19 @@ __global__ void __launch_bounds__(RF_THREADS, 3) k_range_filter(RFArgs a) {
             for (int o = 16; o > 0; o >>= 1) w_ += __shfl_xor_sync(0xffffffffu, w_, o);
             use_pq = (unsigned long long)a.pq_cost * w_ < 170ull * (P1 - P0);
         }
-        if (use_pq) {
+        if (use_pq && a.plist != nullptr && a.mode == DETLSH_MODE_CELL) {
+            // hand the (query, reachable leaf) pairs of this sparse tile to k_leaf_points
+            for (uint32_t mm = tm; mm; mm &= mm - 1) {
+                const int g = __ffs(mm) - 1;
+                const bool pl = lane < nlt && ((lq[lane] >> g) & 1u);
+                const uint32_t bal = __ballot_sync(0xffffffffu, pl);
+                if (!bal) continue;
+                uint32_t base = 0;
+                if (lane == 0) base = atomicAdd(a.pcnt + s_q[g], (uint32_t)__popc(bal));
+                base = __shfl_sync(0xffffffffu, base, 0);
+                if (pl) a.plist[(int64_t)s_q[g] * a.pcap + base + __popc(bal & lanemask_lt())] = lb + lane;
+            }
+        } else if (use_pq) {
             uint32_t* pre = s_pre[warp];
             uint32_t* offs = s_off[warp];
             for (uint32_t mm = tm; mm; mm &= mm - 1) {
@@ -619,6 +636,115 @@ __global__ void __launch_bounds__(RF_THREADS, 3) k_range_filter(RFArgs a) {
             atomicAdd(reinterpret_cast<unsigned long long*>(&a.qs_mut[s_q[threadIdx.x]].pub),
                       (unsigned long long)s_pass[threadIdx.x]);
     }
+}
+
+// ---- sparse tiles, CELL mode: the points of each (query, reachable leaf) pair the range filter
+//      listed, one warp per leaf, lane per point.  Block = one query (its fp32 table of tree t and a
+//      12-bit quantised lower-bound copy in shared memory, ~24 KB: many resident blocks per SM);
+//      codes are read coalesced (a leaf's points are contiguous).  Same decision as the filter:
+//      sum of 12-bit terms (each <= D 2048/rho^2, rounded down) > 2048 rejects, <= 2031 accepts,
+//      the band in between takes the exact fp32 sum in j order (AMB-29).
+struct LPArgs {
+    const int* act;
+    const int* dna;
+    int na;
+    const QState* qs;
+    QState* qs_mut;
+    const uint32_t* plist;
+    uint32_t* pcnt;
+    int64_t pcap;
+    const float* lut;           // [Qb][L][K][N_r]
+    const uint16_t* q12;        // [Qb][L][K][N_r] 12-bit lower bounds of this round (k_build_qlut, QT 2048)
+    const uint32_t* leaf_off;   // global positions
+    const uint8_t* tcodes;      // tree t [n][K]
+    const uint32_t* perm;       // tree t [n]
+    int64_t pos_base;
+    uint32_t* bitmap;
+    int64_t nwords;
+    float rho2, inv_rd;         // inv_rd = 2048/rho^2 rounded down
+    int t, L, K, N_r;
+    unsigned long long* ctr;
+};
+
+__global__ void __launch_bounds__(256) k_leaf_points(LPArgs a) {
+    extern __shared__ __align__(16) unsigned char lp_smem[];
+    const int ai = blockIdx.x;
+    if (ai >= (a.dna ? *a.dna : a.na)) return;
+    const int q = a.act[ai];
+    const uint32_t np = a.pcnt[q];
+    if (np == 0 || a.qs[q].status != ST_ACTIVE) return;
+    const int K = a.K, N_r = a.N_r, KN = K * N_r;
+    uint16_t* s_e = reinterpret_cast<uint16_t*>(lp_smem);                  // 12-bit lower bounds
+    const float* s_d = a.lut + ((int64_t)q * a.L + a.t) * KN;              // exact terms (band only, L1/L2)
+    {
+        const uint4* src = reinterpret_cast<const uint4*>(a.q12 + ((int64_t)q * a.L + a.t) * KN);
+        uint4* dst = reinterpret_cast<uint4*>(s_e);
+        for (int i = threadIdx.x; i < KN / 8; i += blockDim.x) dst[i] = src[i];
+    }
+    __shared__ unsigned int s_tested, s_passed;
+    if (threadIdx.x == 0) { s_tested = 0; s_passed = 0; }
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const uint32_t* pl = a.plist + (int64_t)q * a.pcap;
+    uint32_t* bm = a.bitmap + (int64_t)q * a.nwords;
+    uint32_t tested = 0, passed = 0;
+    for (uint32_t e = blockIdx.y * 8 + (threadIdx.x >> 5); e < np; e += gridDim.y * 8) {
+        const uint32_t l = pl[e];
+        const uint32_t p0 = a.leaf_off[l], p1 = a.leaf_off[l + 1];
+        for (uint32_t p = p0 + lane; p < p1; p += 32) {
+            const int64_t pos = (int64_t)p - a.pos_base;
+            uint32_t acc = 0;
+            uint4 c4 = make_uint4(0, 0, 0, 0);
+            if (K == 16) {
+                c4 = *reinterpret_cast<const uint4*>(a.tcodes + pos * 16);
+#pragma unroll
+                for (int j = 0; j < 16; ++j) {
+                    const uint32_t w = (j >> 2) == 0 ? c4.x : (j >> 2) == 1 ? c4.y : (j >> 2) == 2 ? c4.z : c4.w;
+                    acc += s_e[j * N_r + ((w >> (8 * (j & 3))) & 255u)];
+                }
+            } else {
+                for (int j = 0; j < K; ++j) acc += s_e[j * N_r + a.tcodes[pos * K + j]];
+            }
+            ++tested;
+            if (acc > 2048u) continue;                       // proves cellLB > rho^2
+            bool pass = acc + 17u <= 2048u;                  // proves cellLB < rho^2 (1 - 1e-5)
+            if (!pass) {
+                float s_ = 0.f;
+                if (K == 16) {
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) {
+                        const uint32_t w = (j >> 2) == 0 ? c4.x : (j >> 2) == 1 ? c4.y : (j >> 2) == 2 ? c4.z : c4.w;
+                        s_ += __ldg(s_d + j * N_r + ((w >> (8 * (j & 3))) & 255u));
+                    }
+                } else {
+                    for (int j = 0; j < K; ++j) s_ += __ldg(s_d + j * N_r + a.tcodes[pos * K + j]);
+                }
+                pass = s_ <= a.rho2;
+            }
+            if (pass) {
+                ++passed;
+                const uint32_t id = a.perm[pos];
+                atomicOr(bm + (id >> 5), 1u << (id & 31));   // RED.OR
+            }
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        tested += __shfl_xor_sync(0xffffffffu, tested, o);
+        passed += __shfl_xor_sync(0xffffffffu, passed, o);
+    }
+    if (lane == 0) { atomicAdd(&s_tested, tested); atomicAdd(&s_passed, passed); }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        if (s_passed) atomicAdd(reinterpret_cast<unsigned long long*>(&a.qs_mut[q].pub), (unsigned long long)s_passed);
+        atomicAdd(a.ctr + (int64_t)q * 4 + 2, (unsigned long long)s_tested);
+        atomicAdd(a.ctr + (int64_t)q * 4 + 3, (unsigned long long)s_passed);
+    }
+}
+
+// One pass over the listed pairs is done: the lists restart empty for the next tree.
+__global__ void k_clear_counts(const int* __restrict__ act, int na_ub, const int* __restrict__ dna, uint32_t* __restrict__ pcnt) {
+    const int na = dna ? *dna : na_ub;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < na; i += gridDim.x * blockDim.x) pcnt[act[i]] = 0;
 }
 
 // After tree t: |S| += number of bits set now but not in `prev` (the first-time members of
@@ -1646,11 +1772,37 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
     const size_t rf_smem = (size_t)16 * ix.K * ix.N_r;
     Scratch s_qlut(st, sizeof(uint16_t) * (size_t)(qb * LK * ix.N_r));
     Scratch s_gtab(st, (size_t)16 * ceil_div(qb, RF_G) * ix.K * ix.N_r);
-    auto k_range_filter_sel = (ix.K == 16 && ix.N_r == 256) ? k_range_filter<16 COMMA 256 COMMA RF_G>
-                                                            : k_range_filter<0 COMMA 0 COMMA RF_G>;
+    static const int pq_env = std::getenv("DETLSH_FILTER_PQ") ? std::atoi(std::getenv("DETLSH_FILTER_PQ")) : 1;
+    auto k_range_filter_sel = (ix.K == 16 && ix.N_r == 256)
+                                  ? (pq_env ? k_range_filter<16 COMMA 256 COMMA RF_G COMMA true>
+                                            : k_range_filter<16 COMMA 256 COMMA RF_G COMMA false>)
+                                  : k_range_filter<0 COMMA 0 COMMA RF_G COMMA false>;
     DL_CUDA(cudaFuncSetAttribute(k_range_filter_sel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rf_smem));
     RFArgs ra;
     ra.gtab = nullptr;
+    // sparse tiles in CELL mode: (query, leaf) pair lists screened by k_leaf_points
+    int64_t pcap = 0;
+    for (int t = 0; t < ix.L; ++t) pcap = std::max<int64_t>(pcap, ix.tree_leaf_begin[t + 1] - ix.tree_leaf_begin[t]);
+    static const int pairs_env = std::getenv("DETLSH_LEAF_PAIRS") ? std::atoi(std::getenv("DETLSH_LEAF_PAIRS")) : 1;
+    const bool use_pairs = pairs_env && a.mode == DETLSH_MODE_CELL && ix.K <= 32;
+    Scratch s_plist(st, use_pairs ? sizeof(uint32_t) * (size_t)(qb * pcap) : 0);
+    Scratch s_pcnt(st, sizeof(uint32_t) * (size_t)qb);
+    ra.plist = use_pairs ? s_plist.as<uint32_t>() : nullptr;
+    ra.pcnt = s_pcnt.as<uint32_t>();
+    ra.pcap = pcap;
+    LPArgs lpa;
+    lpa.qs = s_qs.as<QState>();
+    lpa.qs_mut = s_qs.as<QState>();
+    lpa.plist = ra.plist;
+    lpa.pcnt = ra.pcnt;
+    lpa.pcap = pcap;
+    lpa.leaf_off = ix.leaf_off.as<uint32_t>();
+    lpa.L = ix.L;
+    lpa.K = ix.K;
+    lpa.N_r = ix.N_r;
+    const size_t lp_smem = (size_t)ix.K * ix.N_r * sizeof(uint16_t);
+    Scratch s_q12(st, use_pairs ? sizeof(uint16_t) * (size_t)(qb * LK * ix.N_r) : 0);
+    if (use_pairs) DL_CUDA(cudaFuncSetAttribute(k_leaf_points, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lp_smem));
     ra.leaf_off = ix.leaf_off.as<uint32_t>();
     // leaf pruning uses the tight boxes (a valid, tighter bound for every member); RELAXED takes
     // whole leaves by the leaf's own (prefix) box, as the method defines it
@@ -1674,7 +1826,7 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
     ra.N_r = ix.N_r;
     ra.mode = a.mode;
     {
-        static const int pq = std::getenv("DETLSH_PQ_COST") ? std::atoi(std::getenv("DETLSH_PQ_COST")) : 120;
+        static const int pq = std::getenv("DETLSH_PQ_COST") ? std::atoi(std::getenv("DETLSH_PQ_COST")) : 40;
         ra.pq_cost = pq;
     }
     const int nv = (int)ceil_div(ix.ld / 4, 8);      // float4 per lane (8 lanes per row)
@@ -1788,6 +1940,7 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
         DL_CUDA(cudaMemsetAsync(s_bm.p, 0, sizeof(uint32_t) * (size_t)(2 * qb * nwords), st));
         DL_CUDA(cudaMemsetAsync(s_ver.p, 0, sizeof(uint32_t) * (size_t)(qb * nwords), st));
         DL_CUDA(cudaMemsetAsync(s_ctr.p, 0, sizeof(unsigned long long) * (size_t)(4 * qb), st));
+        DL_CUDA(cudaMemsetAsync(s_pcnt.p, 0, sizeof(uint32_t) * (size_t)qb, st));
         tr.mark("batch setup", st);
         DL_LAUNCH(k_init_batch, (unsigned)ceil_div(nqb, 256), 256, 0, st, s_qs.as<QState>(), act, nqb);
         DL_LAUNCH(k_build_lut, (unsigned)std::min<int64_t>(ceil_div((int64_t)nqb * LK * ix.N_r, 256), 148 * 32), 256, 0,
@@ -1806,6 +1959,9 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
                 const int64_t per_q = LK * ix.N_r;
                 DL_LAUNCH(k_build_qlut, (unsigned)std::min<int64_t>(ceil_div(na * per_q, 256), 148 * 32), 256, 0, st,
                           s_lut.as<float>(), cur, na, per_q, inv_rd, (float)QuantSpec<RF_G>::CAP, s_qlut.as<uint16_t>());
+                if (use_pairs)    // the pair kernel's finer table: terms <= D 2048/rho^2, cap 4095
+                    DL_LAUNCH(k_build_qlut, (unsigned)std::min<int64_t>(ceil_div(na * per_q, 256), 148 * 32), 256, 0, st,
+                              s_lut.as<float>(), cur, na, per_q, fdiv_rd_host(2048.f, rho2), 4095.f, s_q12.as<uint16_t>());
             }
             // queries that stop on the budget after tree t (Alg. 5 line 7) leave the filter: the
             // trees after it run over the compacted list of still-active queries (fewer groups)
@@ -1838,6 +1994,25 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
                 const int stripes = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(ntiles, RF_THREADS / 32),
                                                                                  (148 * 3 * 4 + groups / 2) / groups));
                 DL_LAUNCH(k_range_filter_sel, dim3((unsigned)groups, (unsigned)stripes), RF_THREADS, rf_smem, st, ra);
+                if (use_pairs) {
+                    lpa.act = fa;
+                    lpa.dna = dnf;
+                    lpa.na = nf;
+                    lpa.lut = s_lut.as<float>();
+                    lpa.tcodes = ra.tcodes;
+                    lpa.perm = ra.perm;
+                    lpa.pos_base = ra.pos_base;
+                    lpa.bitmap = s_bm.as<uint32_t>();
+                    lpa.nwords = nwords;
+                    lpa.rho2 = rho2;
+                    lpa.inv_rd = fdiv_rd_host(2048.f, rho2);
+                    lpa.t = t;
+                    lpa.ctr = s_ctr.as<unsigned long long>();
+                    lpa.q12 = s_q12.as<uint16_t>();
+                    static const int lp_y = std::getenv("DETLSH_LP_Y") ? std::atoi(std::getenv("DETLSH_LP_Y")) : 16;
+                    DL_LAUNCH(k_leaf_points, dim3((unsigned)nf, (unsigned)lp_y), 256, lp_smem, st, lpa);
+                    DL_LAUNCH(k_clear_counts, (unsigned)ceil_div(nf, 256), 256, 0, st, fa, nf, dnf, ra.pcnt);
+                }
                 if (a.lb_order) lb_order_tree(t, fa, nf, dnf);
                 DL_LAUNCH(k_count_decide, (unsigned)ceil_div(nf, 256), 256, 0, st, fa, nf, dnf, s_qs.as<QState>(), budget,
                           a.lb_order ? 1 : 0);

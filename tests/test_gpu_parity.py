@@ -264,9 +264,18 @@ def test_full_size_sampled_queries(cid, nsel):
     Cg = g.codes()
     del g
     o = O.Index(D["X"], c.L, c.K, c.N_r, c.index_seed)
-    mism = np.mean(Cg != o.codes())
-    print(f"cfg{cid} code mismatch fraction {mism:.2e}")
-    assert mism <= 1e-4
+    Co = o.codes()
+    bad = np.argwhere(Cg != Co)
+    print(f"cfg{cid} code mismatch fraction {len(bad) / Cg.size:.2e}")
+    # north_star: codes bit-exact except coordinates within 1e-5 (relative to max(|p|, ||x||)) of
+    # the breakpoint separating the two codes -- every mismatch is checked
+    Po, Bo = o.P(), o.breakpoints()
+    norms = np.linalg.norm(D["X"][np.unique(bad[:, 0])].astype(np.float64), axis=1)
+    nrm = dict(zip(np.unique(bad[:, 0]).tolist(), norms.tolist()))
+    for p, r in bad:
+        tol = 1e-5 * max(abs(float(Po[p, r])), nrm[int(p)])
+        assert _code_mismatch_ok(float(Po[p, r]), int(Cg[p, r]), int(Co[p, r]), Bo[r], tol), (p, r)
+    assert len(bad) <= 1e-3 * Cg.size
     sel = np.random.default_rng(5).choice(c.nq, nsel, replace=False)
     for r, (ig, dg) in zip(radii, res):
         io, do, _ = o.query(D["Q"][sel], c.k, c.c, r, c.beta)

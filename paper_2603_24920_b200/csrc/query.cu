@@ -688,10 +688,36 @@ __global__ void __launch_bounds__(256) k_leaf_points(LPArgs a) {
     const uint32_t* pl = a.plist + (int64_t)q * a.pcap;
     uint32_t* bm = a.bitmap + (int64_t)q * a.nwords;
     uint32_t tested = 0, passed = 0;
-    for (uint32_t e = blockIdx.y * 8 + (threadIdx.x >> 5); e < np; e += gridDim.y * 8) {
-        const uint32_t l = pl[e];
-        const uint32_t p0 = a.leaf_off[l], p1 = a.leaf_off[l + 1];
-        for (uint32_t p = p0 + lane; p < p1; p += 32) {
+    // a warp takes 16 listed leaves at a time and screens their points packed 32 per step (the
+    // owning leaf of packed point i found by a 4-step search over the warp's prefix of sizes)
+    constexpr int LPG = 16;
+    for (uint32_t e0 = (blockIdx.y * 8 + (threadIdx.x >> 5)) * LPG; e0 < np; e0 += gridDim.y * 8 * LPG) {
+        uint32_t my_p0 = 0, my_sz = 0;
+        if (lane < LPG && e0 + lane < np) {
+            const uint32_t l = pl[e0 + lane];
+            my_p0 = a.leaf_off[l];
+            my_sz = a.leaf_off[l + 1] - my_p0;
+        }
+        uint32_t incl = my_sz;
+#pragma unroll
+        for (int o = 1; o < LPG; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        const uint32_t excl = incl - my_sz;
+        const uint32_t T = __shfl_sync(0xffffffffu, incl, LPG - 1);
+        for (uint32_t c0 = 0; c0 < T; c0 += 32) {
+            const uint32_t i = c0 + lane;
+            int o_ = 0;                                   // last leaf slot with excl <= i
+#pragma unroll
+            for (int st = LPG / 2; st > 0; st >>= 1) {
+                const uint32_t ex = __shfl_sync(0xffffffffu, excl, o_ + st);
+                if (ex <= i) o_ += st;
+            }
+            const uint32_t pp0 = __shfl_sync(0xffffffffu, my_p0, o_);
+            const uint32_t pex = __shfl_sync(0xffffffffu, excl, o_);
+            if (i >= T) continue;
+            const uint32_t p = pp0 + (i - pex);
             const int64_t pos = (int64_t)p - a.pos_base;
             uint32_t acc = 0;
             uint4 c4 = make_uint4(0, 0, 0, 0);

@@ -17,7 +17,7 @@ for it in range(int(sys.argv[1]) if len(sys.argv) > 1 else 20):
     a.record(st)
     if rebuild:
         g.free(); g = P.detlsh_build(Xd, c.L, c.K, c.N_r, c.index_seed, opts=o)
-    g.query(Qd, c.k, c.c, 1.1248388401842566, c.beta, opts=o, stats=True)
+    g.query(Qd, c.k, c.c, 0.4999283734152251, c.beta, opts=o, stats=True)
     b.record(st); b.synchronize()
     P.profile_enable(False)
     print(f"=== iter {it} device {a.elapsed_time(b):.2f} ms", file=sys.stderr, flush=True)

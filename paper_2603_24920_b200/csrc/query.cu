@@ -415,16 +415,23 @@ __global__ void __launch_bounds__(RF_THREADS, 3) k_range_filter(RFArgs a) {
             use_pq = (unsigned long long)a.pq_cost * w_ < 170ull * (P1 - P0);
         }
         if (use_pq && a.plist != nullptr && a.mode == DETLSH_MODE_CELL) {
-            // hand the (query, reachable leaf) pairs of this sparse tile to k_leaf_points
+            // hand the (query, reachable leaf) pairs of this sparse tile to k_leaf_points: lane g
+            // reserves query g's slots (all reservations in flight together), then the writes
+            const uint32_t my_lq = lane < nlt ? lq[lane] : 0u;
+            uint32_t bal_g = 0;
             for (uint32_t mm = tm; mm; mm &= mm - 1) {
                 const int g = __ffs(mm) - 1;
-                const bool pl = lane < nlt && ((lq[lane] >> g) & 1u);
-                const uint32_t bal = __ballot_sync(0xffffffffu, pl);
-                if (!bal) continue;
-                uint32_t base = 0;
-                if (lane == 0) base = atomicAdd(a.pcnt + s_q[g], (uint32_t)__popc(bal));
-                base = __shfl_sync(0xffffffffu, base, 0);
-                if (pl) a.plist[(int64_t)s_q[g] * a.pcap + base + __popc(bal & lanemask_lt())] = lb + lane;
+                const uint32_t bal = __ballot_sync(0xffffffffu, (my_lq >> g) & 1u);
+                if (lane == g) bal_g = bal;
+            }
+            uint32_t base_g = 0;
+            if (bal_g) base_g = atomicAdd(a.pcnt + s_q[lane], (uint32_t)__popc(bal_g));
+            for (uint32_t mm = tm; mm; mm &= mm - 1) {
+                const int g = __ffs(mm) - 1;
+                const uint32_t bal = __shfl_sync(0xffffffffu, bal_g, g);
+                const uint32_t base = __shfl_sync(0xffffffffu, base_g, g);
+                if ((bal >> lane) & 1u)
+                    a.plist[(int64_t)s_q[g] * a.pcap + base + __popc(bal & lanemask_lt())] = lb + lane;
             }
         } else if (use_pq) {
             uint32_t* pre = s_pre[warp];
@@ -2016,9 +2023,10 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
                     ra.gtab = gt;
                 }
                 const int64_t ntiles = ra.tile_end - ra.tile_begin;
-                // about 4 waves of 3 resident CTAs per SM in all (tail <= a quarter wave)
+                // about `rf_waves` waves of 3 resident CTAs per SM in all (default 3; 2-4 measured within 1 %)
+                static const int rf_waves = std::getenv("DETLSH_RF_WAVES") ? std::atoi(std::getenv("DETLSH_RF_WAVES")) : 3;
                 const int stripes = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(ntiles, RF_THREADS / 32),
-                                                                                 (148 * 3 * 4 + groups / 2) / groups));
+                                                                                 (148 * 3 * rf_waves + groups / 2) / groups));
                 DL_LAUNCH(k_range_filter_sel, dim3((unsigned)groups, (unsigned)stripes), RF_THREADS, rf_smem, st, ra);
                 if (use_pairs) {
                     lpa.act = fa;

@@ -43,6 +43,7 @@ struct TcShape {
     int stages;
     uint32_t tmem_cols;
     int N_r;          // > 0: fused Alg. 1 encode, codes instead of projections
+    int lgP;          // encode table entries per column = 2^lgP >= N_r (Eytzinger order)
     int streamA;      // 1: the hash matrix does not fit in shared memory -- its k-block is loaded
                       // into every stage beside the rows (re-read from L2 per tile)
     int dbg;          // experiments only (DETLSH_PROJ_DEBUG): 1 no encode search, 2 no conversion, 4 no MMA
@@ -61,8 +62,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     unsigned char* sB = base;                                            // nkb (or S if streamA) x [npad][128 B]
     unsigned char* sX = sB + (size_t)(sh.streamA ? S : sh.nkb) * sh.npad * 128;   // S x 16 KB
     unsigned char* sL = sX + (size_t)S * TC_STAGE_BYTES;                  // S x 16 KB (lo parts)
-    float* sT = reinterpret_cast<float*>(sL + (size_t)S * TC_STAGE_BYTES);   // encode table [LK][N_r]
-    const int tab_floats = sh.N_r > 0 ? sh.LK * sh.N_r : 0;
+    float* sT = reinterpret_cast<float*>(sL + (size_t)S * TC_STAGE_BYTES);   // encode table [LK][2^lgP] (Eytzinger)
+    const int tab_floats = sh.N_r > 0 ? sh.LK << sh.lgP : 0;
     uint64_t* bars = reinterpret_cast<uint64_t*>(sT + tab_floats);
     uint64_t* full = bars;              // [S] TMA -> converters, MMA
     uint64_t* conv = bars + S;          // [S] converters -> MMA
@@ -204,10 +205,22 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         const int ew = warp & 3, eh = (warp - 4) >> 2;
         const int row_in_tile = ew * 32 + lane;
         const int N_r = sh.N_r;
-        if (N_r > 0) {   // breakpoint table: c[r][t] = b_{t+1} (t < N_r-1), c[r][N_r-1] = +inf (AMB-6/7)
+        // breakpoint table per column r: c[t] = b_{t+1} (t < N_r-1), +inf beyond (AMB-6/7), padded to
+        // NP = 2^lg entries and stored in Eytzinger (breadth-first) order: node k = 2^l + j of level l
+        // holds c[j*(P>>l) + (P>>(l+1)) - 1], the element the l-th step of the lower-bound search
+        // compares.  The nodes of one level are contiguous, so the 32 lanes of a step (32 rows, one
+        // column) hit distinct banks for the first 6 levels instead of colliding on a few.
+        const int lg = sh.lgP, NP = 1 << lg;
+        if (N_r > 0) {
             for (int i = threadIdx.x - 128; i < tab_floats; i += TC_EPI) {
-                const int r = i / N_r, t = i - r * N_r;
-                sT[i] = t < N_r - 1 ? B[(int64_t)r * (N_r + 1) + t + 1] : __int_as_float(0x7f800000);
+                const int r = i >> lg, k = i & (NP - 1);
+                float c = 0.f;
+                if (k > 0) {
+                    const int l = 31 - __clz(k), j = k - (1 << l);
+                    const int t = j * (NP >> l) + (NP >> (l + 1)) - 1;
+                    c = t < N_r - 1 ? B[(int64_t)r * (N_r + 1) + t + 1] : __int_as_float(0x7f800000);
+                }
+                sT[i] = c;
             }
             asm volatile("bar.sync 1, 256;" ::: "memory");  // epilogue warps only
         }
@@ -222,21 +235,22 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                 float v[16];
                 tmem_ld16(taddr + c0, v);
                 if (N_r > 0) {
-                    // code = #{t in 1..N_r-1 : b_t < x}: branch-free lower bound over the table;
-                    // the 16 searches advance together (16 independent shared loads per step)
+                    // code = #{t in 1..N_r-1 : b_t < x}: branch-free lower bound, k -> 2k + [c_k < x]
+                    // down the Eytzinger tree, code = k - NP; the 16 searches advance together
+                    // (16 independent shared loads per step)
                     int pos[16];
 #pragma unroll
-                    for (int i = 0; i < 16; ++i) pos[i] = 0;
-                    for (int s = (sh.dbg & 1) ? 0 : N_r >> 1; s > 0; s >>= 1) {
+                    for (int i = 0; i < 16; ++i) pos[i] = 1;
+                    for (int l = (sh.dbg & 1) ? lg : 0; l < lg; ++l) {
 #pragma unroll
                         for (int i = 0; i < 16; ++i) {
                             const int r = min(c0 + i, sh.LK - 1);
-                            pos[i] += (sT[r * N_r + pos[i] + s - 1] < v[i]) ? s : 0;
+                            pos[i] = 2 * pos[i] + ((sT[(r << lg) + pos[i]] < v[i]) ? 1 : 0);
                         }
                     }
                     uint32_t packed[4] = {0, 0, 0, 0};
 #pragma unroll
-                    for (int i = 0; i < 16; ++i) packed[i >> 2] |= (uint32_t)pos[i] << (8 * (i & 3));
+                    for (int i = 0; i < 16; ++i) packed[i >> 2] |= (uint32_t)(pos[i] - NP) << (8 * (i & 3));
                     if (row < sh.m) {
                         uint8_t* out = EP + row * sh.LK + c0;
                         if (c0 + 16 <= sh.LK && (sh.LK & 15) == 0) {
@@ -287,9 +301,11 @@ static bool launch_tc(const Index& ix, const float* d_X, int64_t ld, int64_t m, 
     sh.LK = ix.LK;
     sh.npad = (int)round_up(ix.LK, 16);
     sh.N_r = B ? ix.N_r : 0;
+    sh.lgP = 0;
+    while ((1 << sh.lgP) < ix.N_r) ++sh.lgP;
     if (sh.npad > 256) return false;
     const size_t abytes = (size_t)sh.npad * 128;                 // one k-block of the hash matrix
-    const size_t tbytes = B ? sizeof(float) * (size_t)ix.LK * ix.N_r : 0;
+    const size_t tbytes = B ? sizeof(float) * ((size_t)ix.LK << sh.lgP) : 0;
     const size_t fixed = 1024 /*align*/ + 256 /*barriers*/;
     const size_t budget = 227 * 1024;
     static const int force_stream = std::getenv("DETLSH_STREAM_A") ? std::atoi(std::getenv("DETLSH_STREAM_A")) : 0;

@@ -12,6 +12,7 @@
 //     partition.  Level-synchronous over all L trees at once.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <vector>
 
 #include "index.cuh"
@@ -264,10 +265,21 @@ __device__ inline void push_node(Node* arr, uint32_t* cnt, uint32_t cap, const N
     if (i < cap) arr[i] = nd;
 }
 
+// Where a node goes: a leaf (<= max_size points or no bits left), the block-local list (small
+// enough for k_local_finish to split it to the end in shared memory), or the next global level.
+struct Sinks {
+    Node* active; uint32_t* n_active; uint32_t cap_active;
+    Node* local; uint32_t* n_local; uint32_t cap_local; int local_max;
+    Node* leaves; uint32_t* n_leaves; uint32_t cap_leaves;
+};
+__device__ inline void route_node(const Sinks& k, const Node& nd, int K, int nb, int max_size) {
+    if ((int64_t)nd.len <= max_size || !splittable(nd.bits, K, nb)) push_node(k.leaves, k.n_leaves, k.cap_leaves, nd);
+    else if ((int64_t)nd.len <= k.local_max) push_node(k.local, k.n_local, k.cap_local, nd);
+    else push_node(k.active, k.n_active, k.cap_active, nd);
+}
+
 __global__ void k_init_nodes(const uint32_t* __restrict__ starts, const uint32_t* __restrict__ nseg_p,
-                             int64_t total, int K, int nb, int max_size, Node* __restrict__ active,
-                             uint32_t* __restrict__ n_active, uint32_t cap_active, Node* __restrict__ leaves,
-                             uint32_t* __restrict__ n_leaves, uint32_t cap_leaves) {
+                             int64_t total, int K, int nb, int max_size, Sinks sk) {
     const uint32_t nseg = *nseg_p;
     for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < nseg;
          s += (int64_t)gridDim.x * blockDim.x) {
@@ -282,8 +294,7 @@ __global__ void k_init_nodes(const uint32_t* __restrict__ starts, const uint32_t
         nd.start = starts[s];
         nd.len = (uint32_t)((s + 1 < nseg ? (int64_t)starts[s + 1] : total) - nd.start);
         nd.pad0 = nd.pad1 = 0;
-        if ((int64_t)nd.len <= max_size || !splittable(nd.bits, K, nb)) push_node(leaves, n_leaves, cap_leaves, nd);
-        else push_node(active, n_active, cap_active, nd);
+        route_node(sk, nd, K, nb, max_size);
     }
 }
 
@@ -460,16 +471,14 @@ __global__ void __launch_bounds__(PART_THREADS) k_part_copy(const Node* __restri
 
 __global__ void k_make_children(const Node* __restrict__ nodes, const uint32_t* __restrict__ n_nodes_p,
                                 const int* __restrict__ split, const uint32_t* __restrict__ zeros,
-                                int K, int nb, int max_size, Node* __restrict__ next,
-                                uint32_t* __restrict__ n_next, uint32_t cap_next, Node* __restrict__ leaves,
-                                uint32_t* __restrict__ n_leaves, uint32_t cap_leaves) {
+                                int K, int nb, int max_size, Sinks sk) {
     const uint32_t n_nodes = *n_nodes_p;
     for (int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a < n_nodes;
          a += (int64_t)gridDim.x * blockDim.x) {
         const Node nd = nodes[a];
         const int j = split[a];
         if (j < 0) {                          // unsplittable: an oversized leaf (AMB-9)
-            push_node(leaves, n_leaves, cap_leaves, nd);
+            push_node(sk.leaves, sk.n_leaves, sk.cap_leaves, nd);
             continue;
         }
         const uint32_t Z = zeros[a];
@@ -479,10 +488,170 @@ __global__ void k_make_children(const Node* __restrict__ nodes, const uint32_t* 
             ch.start = b ? nd.start + Z : nd.start;
             ch.len = b ? nd.len - Z : Z;
             if (ch.len == 0) continue;        // empty children are dropped (AMB-11)
-            if ((int64_t)ch.len <= max_size || !splittable(ch.bits, K, nb)) push_node(leaves, n_leaves, cap_leaves, ch);
-            else push_node(next, n_next, cap_next, ch);
+            route_node(sk, ch, K, nb, max_size);
         }
     }
+}
+
+// The rest of B6 for one node of <= LM points, entirely in shared memory: the same SplitNode
+// rule and stable partition as k_choose_split / k_part_* above, applied level by level to the
+// node's sub-nodes until every piece is a leaf.  Codes are staged once (gathered from EP);
+// partitions move 16-bit positions only; perm is written back at the end.  One CTA per node
+// (grid-stride over the local list).
+constexpr int LF_MAXSEG = 128;      // live sub-nodes per level (each > max_size points: LM / (max_size+1))
+
+template <int KM, int LF_THREADS>   // KM >= K: 16 or 32 (split-count registers)
+__global__ void __launch_bounds__(LF_THREADS, 1024 / LF_THREADS) k_local_finish(const Node* __restrict__ loc, const uint32_t* __restrict__ n_loc_p,
+                                                             int LM, uint32_t* __restrict__ perm, const uint8_t* __restrict__ EP,
+                                                             int64_t n, int LK, int K, int nb, int max_size,
+                                                             Node* __restrict__ leaves, uint32_t* __restrict__ n_leaves,
+                                                             uint32_t cap_leaves) {
+    extern __shared__ __align__(16) unsigned char lf_smem[];
+    const int CB = K <= 16 ? 16 : 32;                                     // code bytes per point
+    uint8_t* s_code = lf_smem;                                            // [LM][CB], load order
+    uint32_t* s_id = reinterpret_cast<uint32_t*>(s_code + (size_t)LM * CB);   // [LM] point ids, load order
+    uint16_t* s_ixa = reinterpret_cast<uint16_t*>(s_id + LM);             // [LM] current order -> load slot
+    uint16_t* s_ixb = s_ixa + LM;
+    uint16_t* s_pz = s_ixb + LM;                                          // [LM+1] exclusive prefix of zeros
+    uint8_t* s_seg = reinterpret_cast<uint8_t*>(s_pz + LM + 8);           // [LM] live sub-node of each position
+    __shared__ Node s_act[2][LF_MAXSEG];
+    __shared__ int s_dim[LF_MAXSEG], s_shift[LF_MAXSEG];
+    __shared__ uint32_t s_nact[2], s_wsum[LF_THREADS / 32];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = LF_THREADS / 32;
+    const uint32_t n_loc = *n_loc_p;
+    for (uint32_t a = blockIdx.x; a < n_loc; a += gridDim.x) {
+        const Node nd = loc[a];
+        const int t = (int)(nd.start / n);
+        const int m = (int)nd.len;
+        const uint32_t base = nd.start;
+        for (int i = tid; i < m; i += LF_THREADS) {
+            const uint32_t id = perm[base + i];
+            s_id[i] = id;
+            s_ixa[i] = (uint16_t)i;
+            const uint8_t* c = EP + (int64_t)id * LK + t * K;
+            if (K == 16 && (LK & 15) == 0) {
+                *reinterpret_cast<uint4*>(s_code + i * 16) = *reinterpret_cast<const uint4*>(c);
+            } else {
+                for (int j = 0; j < K; ++j) s_code[i * CB + j] = c[j];
+            }
+        }
+        if (tid == 0) { s_act[0][0] = nd; s_nact[0] = 1; }
+        __syncthreads();
+        uint16_t* ix = s_ixa;
+        uint16_t* ix2 = s_ixb;
+        const int IT = (m + LF_THREADS - 1) / LF_THREADS;   // positions per thread in the scan (<= 8)
+        for (int cur = 0;; cur ^= 1) {
+            const int nact = (int)s_nact[cur];
+            if (nact == 0) break;
+            // SplitNode dimension of each live sub-node (warp per sub-node), as k_choose_split
+            for (int sg = warp; sg < nact; sg += nwarps) {
+                const Node sn = s_act[cur][sg];
+                const int st = (int)(sn.start - base);
+                int ones[KM];
+#pragma unroll
+                for (int j = 0; j < KM; ++j) ones[j] = 0;
+                for (int e = lane; e < max_size; e += 32) {
+                    const uint8_t* c = s_code + (int)ix[st + e] * CB;
+#pragma unroll
+                    for (int j = 0; j < KM; ++j) {
+                        if (j < K) {
+                            const int b = nib(sn.bits, j);
+                            if (b < nb) ones[j] += (c[j] >> (nb - 1 - b)) & 1;
+                        }
+                    }
+                }
+                int best = -1, best_imb = 0x7fffffff;
+#pragma unroll
+                for (int j = 0; j < KM; ++j) {
+                    int v = ones[j];
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+                    if (j < K && nib(sn.bits, j) < nb) {
+                        const int imb = abs(max_size - 2 * v);
+                        if (imb < best_imb) { best_imb = imb; best = j; }
+                    }
+                }
+                if (lane == 0) {   // live sub-nodes are splittable, so best >= 0
+                    s_dim[sg] = best;
+                    s_shift[sg] = nb - 1 - nib(sn.bits, best);
+                }
+            }
+            for (int i = tid; i < m; i += LF_THREADS) s_seg[i] = 0xFF;
+            if (tid == 0) s_nact[cur ^ 1] = 0;
+            __syncthreads();
+            for (int sg = warp; sg < nact; sg += nwarps) {
+                const int st = (int)(s_act[cur][sg].start - base), len = (int)s_act[cur][sg].len;
+                for (int e = lane; e < len; e += 32) s_seg[st + e] = (uint8_t)sg;
+            }
+            __syncthreads();
+            // zero flags of positions in live sub-nodes, block-wide exclusive scan
+            uint32_t fl = 0, cnt = 0;
+            for (int q = 0; q < IT; ++q) {
+                const int i = tid * IT + q;
+                if (i < m && s_seg[i] != 0xFF) {
+                    const int sg = s_seg[i];
+                    const uint32_t z = 1u - ((s_code[(int)ix[i] * CB + s_dim[sg]] >> s_shift[sg]) & 1u);
+                    fl |= z << q;
+                    cnt += z;
+                }
+            }
+            uint32_t inc = cnt;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t v = __shfl_up_sync(0xffffffffu, inc, o);
+                if (lane >= o) inc += v;
+            }
+            if (lane == 31) s_wsum[warp] = inc;
+            __syncthreads();
+            uint32_t wpre = 0;
+            for (int w = 0; w < warp; ++w) wpre += s_wsum[w];
+            uint32_t run = wpre + inc - cnt;
+            for (int q = 0; q < IT; ++q) {
+                const int i = tid * IT + q;
+                if (i < m) s_pz[i] = (uint16_t)run;
+                run += (fl >> q) & 1u;
+            }
+            if (tid == LF_THREADS - 1) s_pz[m] = (uint16_t)run;
+            __syncthreads();
+            // stable partition of every live sub-node: zeros first, then ones
+            for (int i = tid; i < m; i += LF_THREADS) {
+                const int sg = s_seg[i];
+                if (sg == 0xFF) { ix2[i] = ix[i]; continue; }
+                const int st = (int)(s_act[cur][sg].start - base), len = (int)s_act[cur][sg].len;
+                const int pst = s_pz[st], Zs = (int)s_pz[st + len] - pst, zb = (int)s_pz[i] - pst;
+                const bool is0 = s_pz[i + 1] != s_pz[i];
+                const int dst = is0 ? st + zb : st + Zs + (i - st - zb);
+                ix2[dst] = ix[i];
+            }
+            // children, as k_make_children: leaves out, the rest live at the next level
+            for (int sg = tid; sg < nact; sg += LF_THREADS) {
+                const Node sn = s_act[cur][sg];
+                const int st = (int)(sn.start - base);
+                const uint32_t Z = (uint32_t)(s_pz[st + sn.len] - s_pz[st]);
+                for (int b = 0; b < 2; ++b) {
+                    Node ch = sn;
+                    nib_inc(ch.bits, s_dim[sg]);
+                    ch.start = b ? sn.start + Z : sn.start;
+                    ch.len = b ? sn.len - Z : Z;
+                    if (ch.len == 0) continue;
+                    if ((int64_t)ch.len <= max_size || !splittable(ch.bits, K, nb)) {
+                        push_node(leaves, n_leaves, cap_leaves, ch);
+                    } else {
+                        const uint32_t k = atomicAdd(&s_nact[cur ^ 1], 1u);
+                        s_act[cur ^ 1][k] = ch;
+                    }
+                }
+            }
+            __syncthreads();
+            uint16_t* tmp = ix; ix = ix2; ix2 = tmp;
+        }
+        for (int i = tid; i < m; i += LF_THREADS) perm[base + i] = s_id[ix[i]];
+        __syncthreads();
+    }
+}
+
+size_t local_finish_smem(int LM, int K) {
+    return (size_t)LM * ((K <= 16 ? 16 : 32) + 4 + 2 + 2 + 2 + 1) + 16 + 64;
 }
 
 __global__ void k_leaf_keys(const Node* __restrict__ leaves, const uint32_t* __restrict__ nl_p,
@@ -760,7 +929,7 @@ static bool build_trees_try(Index& ix, const uint8_t* d_EP, int64_t leaf_factor,
     Scratch s_seg(st, sizeof(uint32_t) * (size_t)(2 * total + 8));
     uint32_t* flags = s_seg.as<uint32_t>();
     uint32_t* idx = flags + total;
-    uint32_t* counters = idx + total;  // [0]=nseg [1]=n_active [2]=n_next [3]=n_leaves [4]=total_chunks
+    uint32_t* counters = idx + total;  // [0]=nseg [1]=n_active [2]=n_next [3]=n_leaves [4]=total_chunks [5]=n_local
     DL_CUDA(cudaMemsetAsync(counters, 0, 8 * sizeof(uint32_t), st));
     DL_LAUNCH(k_seg_flags, grid_for(total, 256), 256, 0, st, skeys, n, total, flags);
     exclusive_scan_u32(flags, idx, total, counters + 0, st);
@@ -772,16 +941,27 @@ static bool build_trees_try(Index& ix, const uint8_t* d_EP, int64_t leaf_factor,
     // leaves are disjoint and non-empty (<= total); start from a typical size and grow on overflow
     const int64_t cap_active = total / std::max(1, max_size) + 1;
     const int64_t cap_leaves = std::min<int64_t>(total, nseg + leaf_factor * (total / std::max(1, max_size)) + 1024);
-    Scratch s_nodes(st, sizeof(Node) * (size_t)(2 * cap_active + cap_leaves));
+    Scratch s_nodes(st, sizeof(Node) * (size_t)(3 * cap_active + cap_leaves));
     Node* act = s_nodes.as<Node>();
     Node* nxt = act + cap_active;
-    Node* leaves = nxt + cap_active;
+    Node* loc = nxt + cap_active;
+    Node* leaves = loc + cap_active;
     uint32_t* n_act = counters + 1;
     uint32_t* n_nxt = counters + 2;
     uint32_t* n_leaves = counters + 3;
     uint32_t* total_ch = counters + 4;
+    uint32_t* n_loc = counters + 5;
+    // nodes of <= LM points finish in shared memory (k_local_finish); LM keeps the live
+    // sub-nodes of one level within LF_MAXSEG and the positions within 16 bits
+    static const int lm_env = std::getenv("DETLSH_LOCAL_MAX") ? std::atoi(std::getenv("DETLSH_LOCAL_MAX")) : 1536;
+    // (scan flags of one thread fit 32 bits: LM <= 32 * 256; staged codes + indices fit shared memory)
+    const int64_t lm_smem = (int64_t)(200 * 1024) / ((K <= 16 ? 16 : 32) + 11);
+    const int LM = (int)std::min<int64_t>(std::min<int64_t>(std::min<int64_t>(lm_env, 8192), lm_smem),
+                                          (int64_t)(LF_MAXSEG - 1) * (max_size + 1));
+    Sinks sk{act, n_act, (uint32_t)cap_active, loc, n_loc, (uint32_t)cap_active, LM > max_size ? LM : 0,
+             leaves, n_leaves, (uint32_t)cap_leaves};
     DL_LAUNCH(k_init_nodes, grid_for(nseg, 256), 256, 0, st, s_starts.as<uint32_t>(), counters + 0, total, K, nb,
-              max_size, act, n_act, (uint32_t)cap_active, leaves, n_leaves, (uint32_t)cap_leaves);
+              max_size, sk);
     s_starts.free_();
 
     tr.mark("first layer sort+segments", st);
@@ -816,12 +996,32 @@ static bool build_trees_try(Index& ix, const uint8_t* d_EP, int64_t leaf_factor,
                       perm);
         }
         DL_CUDA(cudaMemsetAsync(n_nxt, 0, sizeof(uint32_t), st));
-        DL_LAUNCH(k_make_children, grid_for(na, 256), 256, 0, st, act, n_act, split, zeros, K, nb, max_size, nxt,
-                  n_nxt, (uint32_t)cap_active, leaves, n_leaves, (uint32_t)cap_leaves);
+        sk.active = nxt;
+        sk.n_active = n_nxt;
+        DL_LAUNCH(k_make_children, grid_for(na, 256), 256, 0, st, act, n_act, split, zeros, K, nb, max_size, sk);
         std::swap(act, nxt);
         std::swap(n_act, n_nxt);
         na = d2h(n_act, st);
         DL_REQUIRE(na <= cap_active, "tree build: active-node capacity exceeded");
+    }
+    if (sk.local_max > 0) {
+        const size_t lsm = local_finish_smem(LM, K);
+        static const int lf_nt = std::getenv("DETLSH_LF_THREADS") ? std::atoi(std::getenv("DETLSH_LF_THREADS")) : 256;
+        const int LF_THREADS = lf_nt == 256 ? 256 : 512;
+        auto k_local_finish_sel = K <= 16 ? (LF_THREADS == 256 ? k_local_finish<16, 256> : k_local_finish<16, 512>)
+                                          : (LF_THREADS == 256 ? k_local_finish<32, 256> : k_local_finish<32, 512>);
+        static size_t lf_configured[4] = {0, 0, 0, 0};
+        const int ci = (K > 16) * 2 + (LF_THREADS == 256);
+        if (lf_configured[ci] < lsm) {
+            DL_CUDA(cudaFuncSetAttribute(k_local_finish_sel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lsm));
+            lf_configured[ci] = lsm;
+        }
+        int dev = 0, nsm = 148, per_sm = 1;
+        DL_CUDA(cudaGetDevice(&dev));
+        DL_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+        DL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_local_finish_sel, LF_THREADS, lsm));
+        DL_LAUNCH(k_local_finish_sel, nsm * std::max(1, per_sm), LF_THREADS, lsm, st, loc, n_loc, LM, perm, d_EP, n, LK, K,
+                  nb, max_size, leaves, n_leaves, (uint32_t)cap_leaves);
     }
     s_tmp.free_();
     s_zc.free_();

@@ -518,3 +518,19 @@ def test_config5_full_size_properties():
     print(f"cfg5 n={n}: r_min {r:.4g}, recall@{c.k} vs brute force on 40 queries {rec:.3f}, "
           f"stops {np.bincount(st['reason'], minlength=3)}, mean |S| {st['n_cand'].mean():.0f}")
     assert rec > 0
+
+
+@pytest.mark.parametrize("local_max", ["0", "300", "1536", "8192"])
+def test_trees_split_paths(local_max):
+    """B6 through the global level loop only (0) and through mixes of global levels and the
+    shared-memory finish (k_local_finish, nodes of <= local_max points), on codes with one
+    ~18K-point first-layer node and many small ones: every variant gives the oracle's trees
+    bit for bit."""
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, DETLSH_LOCAL_MAX=local_max)
+    here = os.path.dirname(os.path.abspath(__file__))
+    r = subprocess.run([sys.executable, os.path.join(here, "_tree_split_paths.py")], env=env,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "OK" in r.stdout, r.stdout + r.stderr

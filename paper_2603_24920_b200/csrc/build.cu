@@ -654,13 +654,34 @@ size_t local_finish_smem(int LM, int K) {
     return (size_t)LM * ((K <= 16 ? 16 : 32) + 4 + 2 + 2 + 2 + 1) + 16 + 64;
 }
 
-__global__ void k_leaf_keys(const Node* __restrict__ leaves, const uint32_t* __restrict__ nl_p,
-                            uint32_t* __restrict__ keys, uint32_t* __restrict__ vals) {
+// Canonical leaf order (ascending start) without a sort: leaves tile [0, L*n) disjointly, so a
+// leaf's rank is the number of leaf starts before its own -- a bitmap of starts plus a prefix
+// count of its words.
+__global__ void k_leaf_starts(const Node* __restrict__ leaves, const uint32_t* __restrict__ nl_p,
+                              uint32_t* __restrict__ bitmap) {
     const uint32_t nl = *nl_p;
     for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < nl;
          l += (int64_t)gridDim.x * blockDim.x) {
-        keys[l] = leaves[l].start;
-        vals[l] = (uint32_t)l;
+        const uint32_t s = leaves[l].start;
+        atomicOr(&bitmap[s >> 5], 1u << (s & 31));
+    }
+}
+
+__global__ void k_word_popc(const uint32_t* __restrict__ bitmap, int64_t nw, uint32_t* __restrict__ cnt) {
+    for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < nw;
+         w += (int64_t)gridDim.x * blockDim.x)
+        cnt[w] = __popc(bitmap[w]);
+}
+
+__global__ void k_leaf_rank(const Node* __restrict__ leaves, const uint32_t* __restrict__ nl_p,
+                            const uint32_t* __restrict__ bitmap, const uint32_t* __restrict__ pre,
+                            uint32_t* __restrict__ order) {
+    const uint32_t nl = *nl_p;
+    for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < nl;
+         l += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t s = leaves[l].start;
+        const uint32_t r = pre[s >> 5] + __popc(bitmap[s >> 5] & ((1u << (s & 31)) - 1u));
+        order[r] = (uint32_t)l;
     }
 }
 
@@ -1031,21 +1052,22 @@ static bool build_trees_try(Index& ix, const uint8_t* d_EP, int64_t leaf_factor,
     // leaves in canonical order = ascending start position (DFS, 0-child first, keys ascending)
     const int64_t nl = d2h(n_leaves, st);
     if (nl > cap_leaves) return false;
-    Scratch s_lsort(st, sizeof(uint32_t) * (size_t)(4 * nl));
-    uint32_t* lk0 = s_lsort.as<uint32_t>();
-    uint32_t* lv0 = lk0 + nl;
-    uint32_t* lk1 = lv0 + nl;
-    uint32_t* lv1 = lk1 + nl;
-    DL_LAUNCH(k_leaf_keys, grid_for(nl, 256), 256, 0, st, leaves, n_leaves, lk0, lv0);
-    int bits = 1;
-    while (bits < 32 && ((int64_t)1 << bits) < total) ++bits;
-    bits = (int)round_up(bits, 8);
-    bool lf = radix_sort_batched(lk0, lv0, lk1, lv1, nl, 1, bits, st);
+    const int64_t nw = ceil_div(total, 32);
+    Scratch s_lsort(st, sizeof(uint32_t) * (size_t)(nl + 3 * nw));
+    uint32_t* order = s_lsort.as<uint32_t>();
+    uint32_t* bitmap = order + nl;
+    uint32_t* wcnt = bitmap + nw;
+    uint32_t* wpre = wcnt + nw;
+    DL_CUDA(cudaMemsetAsync(bitmap, 0, sizeof(uint32_t) * (size_t)nw, st));
+    DL_LAUNCH(k_leaf_starts, grid_for(nl, 256), 256, 0, st, leaves, n_leaves, bitmap);
+    DL_LAUNCH(k_word_popc, grid_for(nw, 256), 256, 0, st, bitmap, nw, wcnt);
+    exclusive_scan_u32(wcnt, wpre, nw, nullptr, st);
+    DL_LAUNCH(k_leaf_rank, grid_for(nl, 256), 256, 0, st, leaves, n_leaves, bitmap, wpre, order);
     ix.leaf_off.alloc(sizeof(uint32_t) * (size_t)(nl + 1), st);
     ix.leaf_lo.alloc((size_t)nl * K, st);
     ix.leaf_hi.alloc((size_t)nl * K, st);
     ix.leaf_bits.alloc((size_t)nl * K, st);
-    DL_LAUNCH(k_leaf_finalize, grid_for(nl, 256), 256, 0, st, leaves, lf ? lv1 : lv0, nl, perm, d_EP, n, LK, K, nb,
+    DL_LAUNCH(k_leaf_finalize, grid_for(nl, 256), 256, 0, st, leaves, order, nl, perm, d_EP, n, LK, K, nb,
               ix.leaf_off.as<uint32_t>(), ix.leaf_lo.as<uint8_t>(), ix.leaf_hi.as<uint8_t>(),
               ix.leaf_bits.as<uint8_t>(), total);
     Scratch s_begin(st, sizeof(unsigned long long) * (size_t)(L + 1));

@@ -62,30 +62,26 @@ __device__ inline uint32_t block_exclusive_scan(uint32_t v, uint32_t* s_warp, ui
     return total;
 }
 
-// Exclusive scan, in place, of each segment's 256*tiles digit-major counts (one block per segment).
-__global__ void __launch_bounds__(1024) k_rs_scan(uint32_t* __restrict__ hist, int64_t len) {
-    __shared__ uint32_t s_warp[32];
-    uint32_t* h = hist + (int64_t)blockIdx.x * len;
+// Exclusive scan, in place, of one digit's per-tile counts (warp per (digit, segment); 8 digits
+// per block); the digit's total goes to dtot[seg][digit] (the scatter turns those into digit bases).
+__global__ void __launch_bounds__(256) k_rs_scan(uint32_t* __restrict__ hist, int tiles, uint32_t* __restrict__ dtot) {
+    const int lane = threadIdx.x & 31;
+    const int dig = blockIdx.x * 8 + (threadIdx.x >> 5), seg = blockIdx.y;
+    uint32_t* h = hist + ((int64_t)seg * 256 + dig) * tiles;
     uint32_t carry = 0;
-    for (int64_t base = 0; base < len; base += 1024 * 4) {
-        uint32_t v[4], s = 0;
+    for (int base = 0; base < tiles; base += 32) {
+        const int e = base + lane;
+        const uint32_t v = e < tiles ? h[e] : 0;
+        uint32_t x = v;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            int64_t e = base + (int64_t)threadIdx.x * 4 + j;
-            v[j] = e < len ? h[e] : 0;
-            s += v[j];
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
         }
-        uint32_t excl;
-        uint32_t tot = block_exclusive_scan<1024>(s, s_warp, excl);
-        uint32_t run = carry + excl;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            int64_t e = base + (int64_t)threadIdx.x * 4 + j;
-            if (e < len) h[e] = run;
-            run += v[j];
-        }
-        carry += tot;
+        if (e < tiles) h[e] = carry + x - v;
+        carry += __shfl_sync(0xffffffffu, x, 31);
     }
+    if (lane == 0) dtot[seg * 256 + dig] = carry;
 }
 
 template <bool HAS_VALS>
@@ -94,12 +90,16 @@ __global__ void __launch_bounds__(RS_THREADS) k_rs_scatter(const uint32_t* __res
                                                            uint32_t* __restrict__ kout,
                                                            uint32_t* __restrict__ vout, int64_t m,
                                                            int shift, int tiles,
-                                                           const uint32_t* __restrict__ offs) {
+                                                           const uint32_t* __restrict__ offs,
+                                                           const uint32_t* __restrict__ dtot) {
     __shared__ uint32_t s_base[256];
     __shared__ uint32_t s_wcnt[RS_WARPS][256];
+    __shared__ uint32_t s_warp[32];
     const int seg = blockIdx.y, tile = blockIdx.x;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    s_base[threadIdx.x] = offs[((int64_t)seg * 256 + threadIdx.x) * tiles + tile];
+    uint32_t dbase;   // digits below this one, in this segment
+    block_exclusive_scan<RS_THREADS>(dtot[seg * 256 + threadIdx.x], s_warp, dbase);
+    s_base[threadIdx.x] = dbase + offs[((int64_t)seg * 256 + threadIdx.x) * tiles + tile];
     const uint32_t* k = kin + (int64_t)seg * m;
     const uint32_t* v = HAS_VALS ? vin + (int64_t)seg * m : nullptr;
     uint32_t* ko = kout + (int64_t)seg * m;
@@ -199,7 +199,8 @@ bool radix_sort_batched(uint32_t* k0, uint32_t* v0, uint32_t* k1, uint32_t* v1, 
     if (m <= 0 || nseg <= 0 || bits <= 0) return false;
     const int tiles = (int)ceil_div(m, RS_TILE);
     const int64_t len = (int64_t)256 * tiles;
-    Scratch hist(st, sizeof(uint32_t) * (size_t)(len * nseg));
+    Scratch hist(st, sizeof(uint32_t) * (size_t)(len * nseg + 256 * nseg));
+    uint32_t* dtot = hist.as<uint32_t>() + len * nseg;
     bool flip = false;
     for (int shift = 0; shift < bits; shift += 8) {
         uint32_t* ki = flip ? k1 : k0;
@@ -208,13 +209,13 @@ bool radix_sort_batched(uint32_t* k0, uint32_t* v0, uint32_t* k1, uint32_t* v1, 
         uint32_t* vo = flip ? v0 : v1;
         dim3 grid(tiles, (unsigned)nseg);
         DL_LAUNCH(k_rs_hist, grid, RS_THREADS, 0, st, ki, m, shift, tiles, hist.as<uint32_t>());
-        DL_LAUNCH(k_rs_scan, (unsigned)nseg, 1024, 0, st, hist.as<uint32_t>(), len);
+        DL_LAUNCH(k_rs_scan, dim3(32, (unsigned)nseg), 256, 0, st, hist.as<uint32_t>(), tiles, dtot);
         if (v0) {
             DL_LAUNCH(k_rs_scatter<true>, grid, RS_THREADS, 0, st, ki, vi, ko, vo, m, shift, tiles,
-                      hist.as<uint32_t>());
+                      hist.as<uint32_t>(), dtot);
         } else {
             DL_LAUNCH(k_rs_scatter<false>, grid, RS_THREADS, 0, st, ki, (const uint32_t*)nullptr, ko,
-                      (uint32_t*)nullptr, m, shift, tiles, hist.as<uint32_t>());
+                      (uint32_t*)nullptr, m, shift, tiles, hist.as<uint32_t>(), dtot);
         }
         flip = !flip;
     }

@@ -119,6 +119,99 @@ __global__ void k_sel_ties(uint64_t salt, int64_t id_lo, int64_t n_range, int64_
     }
 }
 
+// Fast path of the same selection: one 16-bit histogram of the keys' top bits finds the bin b
+// holding the n_s-th smallest key; keys in lower bins are all taken, and the few keys in bin b
+// (~n/65536) are ranked exactly by (key, id) -- ties to the lowest id (AMB-4).  Identical set
+// to the 8-pass radix select above, which remains the fallback if bin b overflows its buffer.
+struct Sel16 {
+    uint32_t bin, need, ncand, overflow;
+};
+
+__global__ void __launch_bounds__(256) k_sel16_hist(uint64_t salt, int64_t n_global, uint32_t* __restrict__ hist) {
+    for (int64_t id = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; id < n_global;
+         id += (int64_t)gridDim.x * blockDim.x)
+        atomicAdd(&hist[keyed(salt, (uint64_t)id) >> 48], 1u);
+}
+
+// one CTA of 1024 threads, 64 bins each
+__global__ void __launch_bounds__(1024) k_sel16_pick(const uint32_t* __restrict__ hist, int64_t n_s, Sel16* __restrict__ st) {
+    __shared__ uint32_t s_warp[32];
+    __shared__ unsigned long long s_tot[32];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const uint32_t* h = hist + threadIdx.x * 64;
+    unsigned long long sum = 0;
+    for (int j = 0; j < 64; ++j) sum += h[j];
+    unsigned long long x = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) s_tot[w] = x;
+    __syncthreads();
+    unsigned long long before = x - sum;
+    for (int ww = 0; ww < w; ++ww) before += s_tot[ww];
+    (void)s_warp;
+    const unsigned long long want = (unsigned long long)n_s;
+    if (before < want && want <= before + sum) {      // exactly one thread
+        unsigned long long run = before;
+        for (int j = 0; j < 64; ++j) {
+            if (run + h[j] >= want) {
+                st->bin = (uint32_t)(threadIdx.x * 64 + j);
+                st->need = (uint32_t)(want - run);
+                st->ncand = 0;
+                st->overflow = 0;
+                break;
+            }
+            run += h[j];
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256) k_sel16_collect(uint64_t salt, int64_t id_lo, int64_t n_range, int64_t n_global,
+                                                       Sel16* __restrict__ st, uint32_t* __restrict__ out,
+                                                       unsigned long long* __restrict__ counter,
+                                                       unsigned long long* __restrict__ ckey, uint32_t* __restrict__ cid,
+                                                       uint32_t ccap) {
+    const uint32_t b = st->bin;
+    for (int64_t id = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; id < n_global;
+         id += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t key = keyed(salt, (uint64_t)id);
+        const uint32_t top = (uint32_t)(key >> 48);
+        if (top < b) {
+            if (id >= id_lo && id < id_lo + n_range) out[atomicAdd(counter, 1ull)] = (uint32_t)(id - id_lo);
+        } else if (top == b) {
+            const uint32_t i = atomicAdd(&st->ncand, 1u);
+            if (i < ccap) { ckey[i] = key; cid[i] = (uint32_t)id; }
+        }
+    }
+}
+
+// one CTA: rank every candidate of bin b by (key, id); the `need` smallest are taken
+__global__ void __launch_bounds__(1024) k_sel16_finish(int64_t id_lo, int64_t n_range, Sel16* __restrict__ st,
+                                                       const unsigned long long* __restrict__ ckey,
+                                                       const uint32_t* __restrict__ cid, uint32_t ccap,
+                                                       uint32_t* __restrict__ out, unsigned long long* __restrict__ counter) {
+    extern __shared__ unsigned long long s_key[];
+    uint32_t* s_id = reinterpret_cast<uint32_t*>(s_key + ccap);
+    const uint32_t nc = st->ncand;
+    if (nc > ccap) {
+        if (threadIdx.x == 0) st->overflow = 1;
+        return;
+    }
+    for (uint32_t i = threadIdx.x; i < nc; i += blockDim.x) { s_key[i] = ckey[i]; s_id[i] = cid[i]; }
+    __syncthreads();
+    const uint32_t need = st->need;
+    for (uint32_t i = threadIdx.x; i < nc; i += blockDim.x) {
+        const unsigned long long k = s_key[i];
+        const uint32_t id = s_id[i];
+        uint32_t rank = 0;
+        for (uint32_t j = 0; j < nc; ++j) rank += (s_key[j] < k || (s_key[j] == k && s_id[j] < id)) ? 1u : 0u;
+        if (rank < need && (int64_t)id >= id_lo && (int64_t)id < id_lo + n_range)
+            out[atomicAdd(counter, 1ull)] = (uint32_t)(id - id_lo);
+    }
+}
+
 __global__ void k_gather_rows(const float* __restrict__ X, int64_t ld, const uint32_t* __restrict__ ids,
                               int64_t m, float* __restrict__ out) {
     const int lane = threadIdx.x & 31;
@@ -889,22 +982,59 @@ template <class T> T d2h(const T* d, cudaStream_t st) {
 void sample_ids_device(uint64_t seed, int64_t id_lo, int64_t n_range, int64_t n_global, int64_t n_s,
                        uint32_t* d_out_local, int64_t* n_out_host, cudaStream_t st) {
     const uint64_t salt = seed ^ kSampleSalt;
-    Scratch s_state(st, sizeof(SelState) + 256 * sizeof(uint32_t) + 16);
-    SelState* state = s_state.as<SelState>();
-    uint32_t* hist = reinterpret_cast<uint32_t*>(state + 1);
-    DL_CUDA(cudaMemsetAsync(hist, 0, 256 * sizeof(uint32_t), st));
-    DL_LAUNCH(k_sel_init, 1, 1, 0, st, state, n_s);
+    // fast path: 16-bit histogram + exact ranking of the threshold bin
+    if (n_s <= 0) {
+        *n_out_host = 0;
+        return;
+    }
+    static const int cap_env = std::getenv("DETLSH_SEL16_CAP") ? std::atoi(std::getenv("DETLSH_SEL16_CAP")) : 0;  // tests
+    const uint32_t ccap = cap_env > 0 ? (uint32_t)cap_env : (uint32_t)std::min<int64_t>(8192, 1024 + 2 * (n_global >> 16));
+    Scratch s16(st, sizeof(uint32_t) * 65536 + sizeof(Sel16) + 2 * sizeof(unsigned long long) +
+                        (sizeof(unsigned long long) + sizeof(uint32_t)) * (size_t)ccap + 64);
+    uint32_t* hist = s16.as<uint32_t>();
+    unsigned long long* ckey = reinterpret_cast<unsigned long long*>(hist + 65536);
+    unsigned long long* counter = ckey + ccap;
+    Sel16* state = reinterpret_cast<Sel16*>(counter + 1);
+    uint32_t* cid = reinterpret_cast<uint32_t*>(state + 1);
+    DL_CUDA(cudaMemsetAsync(hist, 0, sizeof(uint32_t) * 65536, st));
+    DL_CUDA(cudaMemsetAsync(counter, 0, sizeof(unsigned long long) + sizeof(Sel16), st));
     const int g = grid_for(n_global, 256, 148 * 8);
+    DL_LAUNCH(k_sel16_hist, g, 256, 0, st, salt, n_global, hist);
+    DL_LAUNCH(k_sel16_pick, 1, 1024, 0, st, hist, n_s, state);
+    DL_LAUNCH(k_sel16_collect, g, 256, 0, st, salt, id_lo, n_range, n_global, state, d_out_local, counter, ckey, cid, ccap);
+    const size_t fsm = (sizeof(unsigned long long) + sizeof(uint32_t)) * (size_t)ccap;
+    static size_t f_configured = 0;
+    if (f_configured < fsm) {
+        DL_CUDA(cudaFuncSetAttribute(k_sel16_finish, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm));
+        f_configured = fsm;
+    }
+    DL_LAUNCH(k_sel16_finish, 1, 1024, fsm, st, id_lo, n_range, state, ckey, cid, ccap, d_out_local, counter);
+    struct {
+        unsigned long long got;
+        Sel16 s;
+    } h;
+    DL_CUDA(cudaMemcpyAsync(&h.got, counter, sizeof(unsigned long long) + sizeof(Sel16), cudaMemcpyDeviceToHost, st));
+    DL_CUDA(cudaStreamSynchronize(st));
+    if (!h.s.overflow) {
+        *n_out_host = (int64_t)h.got;
+        return;
+    }
+    // fallback: 8-pass radix select over the 64-bit keys
+    Scratch s_state(st, sizeof(SelState) + 256 * sizeof(uint32_t) + 16);
+    SelState* sstate = s_state.as<SelState>();
+    uint32_t* hist8 = reinterpret_cast<uint32_t*>(sstate + 1);
+    DL_CUDA(cudaMemsetAsync(hist8, 0, 256 * sizeof(uint32_t), st));
+    DL_LAUNCH(k_sel_init, 1, 1, 0, st, sstate, n_s);
     for (int pass = 0; pass < 8; ++pass) {
         const int shift = 56 - 8 * pass;
-        DL_LAUNCH(k_sel_hist, g, 256, 0, st, salt, n_global, shift, state, hist);
-        DL_LAUNCH(k_sel_pick, 1, 256, 0, st, shift, state, hist);
+        DL_LAUNCH(k_sel_hist, g, 256, 0, st, salt, n_global, shift, sstate, hist8);
+        DL_LAUNCH(k_sel_pick, 1, 256, 0, st, shift, sstate, hist8);
     }
     Scratch s_cnt(st, sizeof(unsigned long long));
     DL_CUDA(cudaMemsetAsync(s_cnt.p, 0, sizeof(unsigned long long), st));
-    DL_LAUNCH(k_sel_collect, grid_for(n_range, 256, 148 * 8), 256, 0, st, salt, id_lo, n_range, state, d_out_local,
+    DL_LAUNCH(k_sel_collect, grid_for(n_range, 256, 148 * 8), 256, 0, st, salt, id_lo, n_range, sstate, d_out_local,
               s_cnt.as<unsigned long long>());
-    DL_LAUNCH(k_sel_ties, 1, 1, 0, st, salt, id_lo, n_range, n_global, state, d_out_local,
+    DL_LAUNCH(k_sel_ties, 1, 1, 0, st, salt, id_lo, n_range, n_global, sstate, d_out_local,
               s_cnt.as<unsigned long long>());
     *n_out_host = (int64_t)d2h(s_cnt.as<unsigned long long>(), st);
 }

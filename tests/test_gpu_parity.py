@@ -534,3 +534,17 @@ def test_trees_split_paths(local_max):
     r = subprocess.run([sys.executable, os.path.join(here, "_tree_split_paths.py")], env=env,
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "OK" in r.stdout, r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("cap", ["0", "1"])
+def test_sample_selection_paths(cap):
+    """B1 sample ids equal the oracle's through the 16-bit histogram path (cap 0 = default
+    candidate buffer) and through the 8-pass radix-select fallback (cap 1 forces the overflow)."""
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, DETLSH_SEL16_CAP=cap)
+    here = os.path.dirname(os.path.abspath(__file__))
+    r = subprocess.run([sys.executable, os.path.join(here, "_sample_paths.py")], env=env,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "OK" in r.stdout, r.stdout + r.stderr

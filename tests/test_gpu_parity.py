@@ -548,3 +548,18 @@ def test_sample_selection_paths(cap):
     r = subprocess.run([sys.executable, os.path.join(here, "_sample_paths.py")], env=env,
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "OK" in r.stdout, r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("m,LK,N_r", [(1, 3, 4), (255, 5, 256), (3000, 64, 256), (16384, 8, 256),
+                                      (16385, 8, 256), (40000, 4, 64)])
+def test_breakpoints_from_samples_paths(m, LK, N_r):
+    """B3 (batched radix sort of each coordinate's sample + AMB-5 gather) equals the oracle's
+    sort-based breakpoints bit for bit, from one to several tiles of samples, with duplicated
+    values and signed zeros in the sample."""
+    rng = np.random.default_rng(m)
+    Ps = rng.standard_normal((m, LK)).astype(np.float32)
+    Ps[rng.random((m, LK)) < 0.1] = 0.5                      # ties
+    Ps[rng.random((m, LK)) < 0.02] = -0.0
+    B = P.detlsh_breakpoints_from_samples(Ps, N_r)
+    for r in range(LK):
+        assert np.array_equal(B[r], O.breakpoints_sort(Ps[:, r], N_r).astype(np.float32)), r

@@ -132,7 +132,11 @@ __global__ void k_group_table(const int* __restrict__ act, int na_ub, const int*
 //      passing points are OR-marked into the per-query bitmap (RED.OR).  The fp32 decision
 //      sums the same terms in the same order as the cell bound's definition (AMB-12), so the
 //      screen never changes a result.
-constexpr int RF_THREADS = 256;
+#ifndef RF_FTAB
+#define RF_FTAB 0                // 1: query-set masks of the SIMD leaf test from a shared table (+8 KB)
+#endif
+constexpr int RF_THREADS = RF_FTAB ? 384 : 256;
+constexpr int RF_CTAS = RF_FTAB ? 2 : 3;      // resident CTAs per SM
 constexpr int RF_G = 16;         // queries per CTA (8-bit terms); 8 selects 12-bit terms
 constexpr int RF_BQ = 64;        // band queue per warp: < 32 left over + one step of <= 32
 
@@ -171,6 +175,7 @@ struct RFArgs {
     float rho2;
     int t, L, K, N_r, mode;
     int pq_cost;                // per-query path cost per 32-point step, relative to 170 per SIMD chunk
+    int dbg;                    // experiments (DETLSH_RF_DEBUG): 1 = per-query leaf test
     uint32_t* plist;            // CELL, sparse tiles: per-query lists of reachable leaves [Qb][pcap] (or null)
     uint32_t* pcnt;             // [Qb] list lengths
     int64_t pcap;
@@ -178,12 +183,19 @@ struct RFArgs {
 };
 
 template <int KT, int NRT, int G, bool PQ>
-__global__ void __launch_bounds__(RF_THREADS, 3) k_range_filter(RFArgs a) {
+__global__ void __launch_bounds__(RF_THREADS, RF_CTAS) k_range_filter(RFArgs a) {
     constexpr uint32_t QT = QuantSpec<G>::QT, CAP = QuantSpec<G>::CAP;
     extern __shared__ __align__(16) unsigned char smem[];
     const int K = KT ? KT : a.K;
     const int N_r = NRT ? NRT : a.N_r;
     uint4* s_qe = reinterpret_cast<uint4*>(smem);                                       // [K][N_r] x 16 B
+    // G = 16, K = 16: s_fl[j][c] = bit g set iff query g's region code in dim j is < c (c = 0..N_r),
+    // so the box term D_j[clamp(s, lo, hi)] of all 16 queries is D_j[lo] on the queries with
+    // s < lo, D_j[hi] on those with s > hi (= not s < hi+1), and 0 on the rest (D_j[s] = 0)
+#if RF_FTAB
+    uint16_t* s_fl = reinterpret_cast<uint16_t*>(s_qe + K * N_r);                       // [K][N_r+1]
+#endif
+    __shared__ __align__(16) uint8_t s_sxT[16][16];                                     // [dim][query] region codes
     __shared__ int s_q[G];
     __shared__ __align__(16) uint8_t s_sx[G][32];
     __shared__ float s_qp[G][32];                                                        // EXACT: q'_t
@@ -237,6 +249,22 @@ __global__ void __launch_bounds__(RF_THREADS, 3) k_range_filter(RFArgs a) {
                 }
                 s_qe[i] = make_uint4(w[0], w[1], w[2], w[3]);
             }
+        }
+        if (G == 16 && KT == 16) {
+            {
+                const int j = threadIdx.x >> 4, g = threadIdx.x & 15;
+                if (threadIdx.x < 256) s_sxT[j][g] = s_q[g] >= 0 ? a.sx[((int64_t)s_q[g] * a.L + a.t) * K + j] : 0;
+            }
+#if RF_FTAB
+            for (int i = threadIdx.x; i < K * (N_r + 1); i += RF_THREADS) {
+                const int j = i / (N_r + 1), c = i - j * (N_r + 1);
+                uint32_t f = 0;
+#pragma unroll
+                for (int g = 0; g < G; ++g)
+                    if (s_q[g] >= 0 && (int)a.sx[((int64_t)s_q[g] * a.L + a.t) * K + j] < c) f |= 1u << g;
+                s_fl[i] = (uint16_t)f;
+            }
+#endif
         }
         if (threadIdx.x < K) {
 #pragma unroll
@@ -311,7 +339,57 @@ __global__ void __launch_bounds__(RF_THREADS, 3) k_range_filter(RFArgs a) {
         if (lane < nlt) {
             const int64_t l = (int64_t)lb + lane;
             uint32_t m = 0;
-            if (KT == 16) {
+            if (KT == 16 && G == 16 && !(a.dbg & 1)) {
+                // all 16 queries at once (same 16-bit lane layout as the SIMD point screen): per
+                // dim, the rows D_j[lo] and D_j[hi] masked by the s < lo / s > hi query sets
+                const uint4 lo4 = *reinterpret_cast<const uint4*>(a.lo + l * 16);
+                const uint4 hi4 = *reinterpret_cast<const uint4*>(a.hi + l * 16);
+                uint32_t acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+                for (int jp = 0; jp < 8; ++jp) {
+                    uint32_t tw[2][4];
+#pragma unroll
+                    for (int u = 0; u < 2; ++u) {
+                        const int j = 2 * jp + u, sh = 8 * (j & 3);
+                        const uint32_t wl = (j >> 2) == 0 ? lo4.x : (j >> 2) == 1 ? lo4.y : (j >> 2) == 2 ? lo4.z : lo4.w;
+                        const uint32_t wh = (j >> 2) == 0 ? hi4.x : (j >> 2) == 1 ? hi4.y : (j >> 2) == 2 ? hi4.z : hi4.w;
+                        const uint32_t cl = (wl >> sh) & 255u, ch = (wh >> sh) & 255u;
+                        const uint4 dl = s_qe[j * N_r + cl];
+                        const uint4 dh = s_qe[j * N_r + ch];
+                        const uint32_t dlw[4] = {dl.x, dl.y, dl.z, dl.w}, dhw[4] = {dh.x, dh.y, dh.z, dh.w};
+#if RF_FTAB
+                        const uint32_t fl = s_fl[j * (N_r + 1) + cl];
+                        const uint32_t fh = ~(uint32_t)s_fl[j * (N_r + 1) + ch + 1];
+#pragma unroll
+                        for (int w = 0; w < 4; ++w) {
+                            // 4 query bits -> 4 byte masks: bit i moves to bit 8i, then x 0xFF
+                            const uint32_t ml = (((fl >> (4 * w)) & 15u) * 0x00204081u & 0x01010101u) * 0xFFu;
+                            const uint32_t mh = (((fh >> (4 * w)) & 15u) * 0x00204081u & 0x01010101u) * 0xFFu;
+                            tw[u][w] = (dlw[w] & ml) | (dhw[w] & mh);
+                        }
+#else
+                        const uint4 sq = *reinterpret_cast<const uint4*>(&s_sxT[j][0]);
+                        const uint32_t sqw[4] = {sq.x, sq.y, sq.z, sq.w};
+                        const uint32_t l4 = cl * 0x01010101u, h4 = ch * 0x01010101u;
+#pragma unroll
+                        for (int w = 0; w < 4; ++w)
+                            tw[u][w] = (dlw[w] & __vcmpltu4(sqw[w], l4)) | (dhw[w] & __vcmpgtu4(sqw[w], h4));
+#endif
+                    }
+#pragma unroll
+                    for (int w = 0; w < 4; ++w) {
+                        const uint32_t p2 = tw[0][w] + tw[1][w];     // 7-bit terms: no carry out of a byte
+                        acc[2 * w] += p2 & 0x00FF00FFu;
+                        acc[2 * w + 1] += __byte_perm(p2, 0u, 0x4341);
+                    }
+                }
+#pragma unroll
+                for (int g = 0; g < G; ++g) {
+                    const uint32_t sg = (acc[2 * (g >> 2) + (g & 1)] >> (16 * ((g >> 1) & 1))) & 0xFFFFu;
+                    m |= (sg <= QT ? 1u : 0u) << g;
+                }
+                m &= tm;
+            } else if (KT == 16) {
                 const uint4 lo4 = *reinterpret_cast<const uint4*>(a.lo + l * 16);
                 const uint4 hi4 = *reinterpret_cast<const uint4*>(a.hi + l * 16);
                 for (uint32_t mm = tm; mm; mm &= mm - 1) {
@@ -1802,7 +1880,7 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
     // per-batch LUTs
     Scratch s_lut(st, sizeof(float) * (size_t)(qb * LK * ix.N_r));
     Scratch s_sx(st, (size_t)(qb * LK));
-    const size_t rf_smem = (size_t)16 * ix.K * ix.N_r;
+    const size_t rf_smem = (size_t)16 * ix.K * ix.N_r + (RF_FTAB ? sizeof(uint16_t) * ix.K * (ix.N_r + 1) : 0);
     Scratch s_qlut(st, sizeof(uint16_t) * (size_t)(qb * LK * ix.N_r));
     Scratch s_gtab(st, (size_t)16 * ceil_div(qb, RF_G) * ix.K * ix.N_r);
     static const int pq_env = std::getenv("DETLSH_FILTER_PQ") ? std::atoi(std::getenv("DETLSH_FILTER_PQ")) : 1;
@@ -1861,6 +1939,8 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
     {
         static const int pq = std::getenv("DETLSH_PQ_COST") ? std::atoi(std::getenv("DETLSH_PQ_COST")) : 40;
         ra.pq_cost = pq;
+        static const int rfd = std::getenv("DETLSH_RF_DEBUG") ? std::atoi(std::getenv("DETLSH_RF_DEBUG")) : 0;
+        ra.dbg = rfd;
     }
     const int nv = (int)ceil_div(ix.ld / 4, 8);      // float4 per lane (8 lanes per row)
     const int vnv = nv <= 1 ? 1 : nv <= 2 ? 2 : nv <= 4 ? 4 : nv <= 8 ? 8 : 0;
@@ -2023,10 +2103,10 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
                     ra.gtab = gt;
                 }
                 const int64_t ntiles = ra.tile_end - ra.tile_begin;
-                // about `rf_waves` waves of 3 resident CTAs per SM in all (default 3; 2-4 measured within 1 %)
+                // about `rf_waves` waves of RF_CTAS resident CTAs per SM in all (default 3; 2-4 measured within 1 %)
                 static const int rf_waves = std::getenv("DETLSH_RF_WAVES") ? std::atoi(std::getenv("DETLSH_RF_WAVES")) : 3;
                 const int stripes = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(ntiles, RF_THREADS / 32),
-                                                                                 (148 * 3 * rf_waves + groups / 2) / groups));
+                                                                                 (148 * RF_CTAS * rf_waves + groups / 2) / groups));
                 DL_LAUNCH(k_range_filter_sel, dim3((unsigned)groups, (unsigned)stripes), RF_THREADS, rf_smem, st, ra);
                 if (use_pairs) {
                     lpa.act = fa;

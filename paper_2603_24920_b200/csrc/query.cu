@@ -83,17 +83,44 @@ __global__ void k_build_lut(const float* __restrict__ Qp, int nqb, int LK, int N
 //      products rounded down: sum_j e_j > QT proves sum_j D_j > rho^2, and sum_j e_j <= QT-17
 //      proves sum_j D_j < rho^2 (1 - 1e-5) (each e_j > D_j QT/rho^2 - 1.001), so only the band
 //      in between needs the exact fp32 sum.  16 terms of <= cap fit the packed lane width.
-__global__ void k_build_qlut(const float* __restrict__ lut, const int* __restrict__ act, int na, int64_t per_q,
+__device__ inline uint16_t quant_term(float d, float inv_rd, float cap) {
+    float v = __fmul_rd(d, inv_rd);
+    if (v != v) v = 0.f;                           // 0 * inf: a zero term stays zero
+    return (uint16_t)(v >= cap ? cap : floorf(v));
+}
+
+// Batch tables in one pass (block = one (query, coordinate) row of N_r entries, thread = region):
+// the exact table D (as k_build_lut), the query's region code (the count of interior breakpoints
+// below it = k_build_lut's lower bound), and -- for the first round, where every query of the
+// batch is active -- both quantised tables of that round (as k_build_qlut).
+__global__ void k_build_tables(const float* __restrict__ Qp, int LK, int N_r, const float* __restrict__ B,
+                               float* __restrict__ lut, uint8_t* __restrict__ sx,
+                               float inv_a, float cap_a, uint16_t* __restrict__ qa,
+                               float inv_b, float cap_b, uint16_t* __restrict__ qb_) {
+    const int r = blockIdx.x, q = blockIdx.y, s = threadIdx.x;
+    const int64_t qr = (int64_t)q * LK + r;
+    const float* b = B + (int64_t)r * (N_r + 1);
+    const float x = Qp[qr];
+    const float l = s >= 1 ? b[s] : -INFINITY;
+    const float u = s <= N_r - 2 ? b[s + 1] : INFINITY;
+    const float v = fmaxf(0.f, fmaxf(l - x, x - u));
+    const float d = v * v;
+    const int64_t i = qr * N_r + s;
+    lut[i] = d;
+    if (qa) qa[i] = quant_term(d, inv_a, cap_a);
+    if (qb_) qb_[i] = quant_term(d, inv_b, cap_b);
+    const int below = __syncthreads_count(s >= 1 && b[s] < x);
+    if (s == 0) sx[qr] = (uint8_t)below;
+}
+
+// later rounds: block = one active query's (coordinate, region) rows
+__global__ void k_build_qlut(const float* __restrict__ lut, const int* __restrict__ act, int64_t per_q,
                              float inv_rd, float cap, uint16_t* __restrict__ qlut) {
-    const int64_t total = (int64_t)na * per_q;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t a_ = i / per_q, e = i - a_ * per_q;
-        const int64_t q = act[a_];
-        float v = __fmul_rd(lut[q * per_q + e], inv_rd);
-        if (v != v) v = 0.f;                       // 0 * inf: a zero term stays zero
-        qlut[q * per_q + e] = (uint16_t)(v >= cap ? cap : floorf(v));
-    }
+    const int64_t q = act[blockIdx.y];
+    const float* src = lut + q * per_q;
+    uint16_t* dst = qlut + q * per_q;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < per_q; e += (int64_t)gridDim.x * blockDim.x)
+        dst[e] = quant_term(src[e], inv_rd, cap);
 }
 
 // ---- per tree: each 16-query group's quantised table interleaved once (entry (j, s) = the
@@ -2056,8 +2083,6 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
         DL_CUDA(cudaMemsetAsync(s_pcnt.p, 0, sizeof(uint32_t) * (size_t)qb, st));
         tr.mark("batch setup", st);
         DL_LAUNCH(k_init_batch, (unsigned)ceil_div(nqb, 256), 256, 0, st, s_qs.as<QState>(), act, nqb);
-        DL_LAUNCH(k_build_lut, (unsigned)std::min<int64_t>(ceil_div((int64_t)nqb * LK * ix.N_r, 256), 148 * 32), 256, 0,
-                  st, Qpb, nqb, (int)LK, ix.N_r, ix.B.as<float>(), s_lut.as<float>(), s_sx.as<uint8_t>());
         int na = nqb;
         int* cur = act;
         int* nxt = act2;
@@ -2067,14 +2092,23 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
             lbo_rho2 = rho2;
             lbo_qp = Qpb;
             const float cr2 = (float)((a.c * r) * (a.c * r));
-            {   // quantised screen of this round: scale 2048 / rho^2 rounded down
+            {   // quantised screen of this round: scale QT / rho^2 rounded down (the pair kernel's
+                // finer table: terms <= D 2048/rho^2, cap 4095)
                 const float inv_rd = fdiv_rd_host((float)QuantSpec<RF_G>::QT, rho2);
                 const int64_t per_q = LK * ix.N_r;
-                DL_LAUNCH(k_build_qlut, (unsigned)std::min<int64_t>(ceil_div(na * per_q, 256), 148 * 32), 256, 0, st,
-                          s_lut.as<float>(), cur, na, per_q, inv_rd, (float)QuantSpec<RF_G>::CAP, s_qlut.as<uint16_t>());
-                if (use_pairs)    // the pair kernel's finer table: terms <= D 2048/rho^2, cap 4095
-                    DL_LAUNCH(k_build_qlut, (unsigned)std::min<int64_t>(ceil_div(na * per_q, 256), 148 * 32), 256, 0, st,
-                              s_lut.as<float>(), cur, na, per_q, fdiv_rd_host(2048.f, rho2), 4095.f, s_q12.as<uint16_t>());
+                if (m == 0) {   // every batch query is active: exact, region-code and quantised tables at once
+                    DL_LAUNCH(k_build_tables, dim3((unsigned)LK, (unsigned)nqb), ix.N_r, 0, st, Qpb, (int)LK, ix.N_r,
+                              ix.B.as<float>(), s_lut.as<float>(), s_sx.as<uint8_t>(), inv_rd,
+                              (float)QuantSpec<RF_G>::CAP, s_qlut.as<uint16_t>(), fdiv_rd_host(2048.f, rho2), 4095.f,
+                              use_pairs ? s_q12.as<uint16_t>() : (uint16_t*)nullptr);
+                } else {
+                    const dim3 g((unsigned)std::min<int64_t>(ceil_div(per_q, 256), 64), (unsigned)na);
+                    DL_LAUNCH(k_build_qlut, g, 256, 0, st, s_lut.as<float>(), cur, per_q, inv_rd,
+                              (float)QuantSpec<RF_G>::CAP, s_qlut.as<uint16_t>());
+                    if (use_pairs)
+                        DL_LAUNCH(k_build_qlut, g, 256, 0, st, s_lut.as<float>(), cur, per_q, fdiv_rd_host(2048.f, rho2),
+                                  4095.f, s_q12.as<uint16_t>());
+                }
             }
             // queries that stop on the budget after tree t (Alg. 5 line 7) leave the filter: the
             // trees after it run over the compacted list of still-active queries (fewer groups)

@@ -880,11 +880,6 @@ __global__ void __launch_bounds__(256) k_leaf_points(LPArgs a) {
 }
 
 // One pass over the listed pairs is done: the lists restart empty for the next tree.
-__global__ void k_clear_counts(const int* __restrict__ act, int na_ub, const int* __restrict__ dna, uint32_t* __restrict__ pcnt) {
-    const int na = dna ? *dna : na_ub;
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < na; i += gridDim.x * blockDim.x) pcnt[act[i]] = 0;
-}
-
 // After tree t: |S| += number of bits set now but not in `prev` (the first-time members of
 // S <- S u S_i, Alg. 5 line 6), and `prev` catches up.  Grid: (active queries) x (word chunks).
 constexpr int CN_WORDS = 4096;
@@ -1080,10 +1075,12 @@ __global__ void k_lbo_reset(const int* __restrict__ cross, int ncross, const uin
 // Before counting |S| after a tree: the bitmap diff is needed only if the budget may have been
 // reached (|S| <= cnt + marks since the last count) or the count is due (force: end of round,
 // or lb_order, which needs |S| exact after every tree).
+// (pcnt != null: also resets the pair-list lengths of the tree just filtered.)
 __global__ void k_count_decide(const int* __restrict__ act, int na_ub, const int* __restrict__ dna,
-                               QState* __restrict__ qs, int64_t budget, int force) {
+                               QState* __restrict__ qs, int64_t budget, int force, uint32_t* __restrict__ pcnt) {
     const int na = dna ? *dna : na_ub;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < na; i += gridDim.x * blockDim.x) {
+        if (pcnt) pcnt[act[i]] = 0;
         QState* s = &qs[act[i]];
         const int d = (s->status == ST_ACTIVE && s->pub > 0 && (force || s->cnt + s->pub >= budget)) ? 1 : 0;
         s->doc = d;
@@ -1092,18 +1089,54 @@ __global__ void k_count_decide(const int* __restrict__ act, int na_ub, const int
 }
 
 // After tree t: the budget test |S| >= ceil(beta n) + k (Alg. 5 line 7, AMB-15/17).
+__device__ inline void tree_end_one(QState* s, int t, int round, int64_t budget, int64_t cap) {
+    if (s->status != ST_ACTIVE) return;
+    s->trees_last = t + 1;
+    s->rounds = round + 1;
+    s->tnew = 0;
+    if (s->cnt > cap) s->overflow = 1;
+    if (s->cnt >= budget) s->status = ST_BUDGET;
+}
+
 __global__ void k_tree_end(const int* __restrict__ act, int na_ub, const int* __restrict__ dna, QState* __restrict__ qs,
                            int t, int round, int64_t budget, int64_t cap) {
     const int na = dna ? *dna : na_ub;
-    for (int a_ = blockIdx.x * blockDim.x + threadIdx.x; a_ < na; a_ += gridDim.x * blockDim.x) {
-        QState* s = &qs[act[a_]];
-        if (s->status != ST_ACTIVE) continue;
-        s->trees_last = t + 1;
-        s->rounds = round + 1;
-        s->tnew = 0;
-        if (s->cnt > cap) s->overflow = 1;
-        if (s->cnt >= budget) s->status = ST_BUDGET;
+    for (int a_ = blockIdx.x * blockDim.x + threadIdx.x; a_ < na; a_ += gridDim.x * blockDim.x)
+        tree_end_one(&qs[act[a_]], t, round, budget, cap);
+}
+
+// k_tree_end and then the order-preserving compaction of the still-active queries (single
+// block; each query is updated and tested by the one thread that owns its slot).
+__global__ void k_tree_end_compact(const int* __restrict__ act, int na_ub, const int* __restrict__ dna,
+                                   QState* __restrict__ qs, int t, int round, int64_t budget, int64_t cap,
+                                   int* __restrict__ act_out, int* __restrict__ n_out) {
+    const int na = dna ? *dna : na_ub;
+    __shared__ int s_n;
+    __shared__ int s_w[32];
+    if (threadIdx.x == 0) s_n = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (int base = 0; base < na; base += blockDim.x) {
+        const int a = base + threadIdx.x;
+        bool keep = false;
+        if (a < na) {
+            QState* s = &qs[act[a]];
+            tree_end_one(s, t, round, budget, cap);
+            keep = s->status == ST_ACTIVE;
+        }
+        const uint32_t bal = __ballot_sync(0xffffffffu, keep);
+        if (lane == 0) s_w[w] = __popc(bal);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int run = s_n;
+            for (int i = 0; i < (int)(blockDim.x / 32); ++i) { const int c = s_w[i]; s_w[i] = run; run += c; }
+            s_n = run;
+        }
+        __syncthreads();
+        if (keep) act_out[s_w[w] + __popc(bal & lanemask_lt())] = act[a];
+        __syncthreads();
     }
+    if (threadIdx.x == 0) *n_out = s_n;
 }
 
 // ---- verify (Alg. 5 lines 8/10): exact squared L2 of every member of S not yet verified,
@@ -2159,26 +2192,28 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
                     lpa.q12 = s_q12.as<uint16_t>();
                     static const int lp_y = std::getenv("DETLSH_LP_Y") ? std::atoi(std::getenv("DETLSH_LP_Y")) : 16;
                     DL_LAUNCH(k_leaf_points, dim3((unsigned)nf, (unsigned)lp_y), 256, lp_smem, st, lpa);
-                    DL_LAUNCH(k_clear_counts, (unsigned)ceil_div(nf, 256), 256, 0, st, fa, nf, dnf, ra.pcnt);
                 }
                 if (a.lb_order) lb_order_tree(t, fa, nf, dnf);
                 DL_LAUNCH(k_count_decide, (unsigned)ceil_div(nf, 256), 256, 0, st, fa, nf, dnf, s_qs.as<QState>(), budget,
-                          a.lb_order ? 1 : 0);
+                          a.lb_order ? 1 : 0, use_pairs ? ra.pcnt : (uint32_t*)nullptr);
                 DL_LAUNCH(k_count_new, dim3((unsigned)nf, (unsigned)ceil_div(nwords, CN_WORDS)), 256, 0, st, fa, dnf,
                           s_qs.as<QState>(), s_bm.as<uint32_t>(), bm_prev, nwords, 1);
-                DL_LAUNCH(k_tree_end, (unsigned)ceil_div(nf, 256), 256, 0, st, fa, nf, dnf, s_qs.as<QState>(), t, m,
-                          budget, cap);
                 if (t + 1 < ix.L) {
                     int* fa2 = (fa == fbuf0) ? fbuf1 : fbuf0;
                     int* dn2 = (fa == fbuf0) ? n_f + 1 : n_f;
-                    DL_LAUNCH(k_compact, 1, 1024, 0, st, fa, nf, dnf, s_qs.as<QState>(), fa2, dn2);
+                    DL_LAUNCH(k_tree_end_compact, 1, 1024, 0, st, fa, nf, dnf, s_qs.as<QState>(), t, m, budget, cap,
+                              fa2, dn2);
                     fa = fa2;
                     dnf = dn2;
+                } else {
+                    DL_LAUNCH(k_tree_end, (unsigned)ceil_div(nf, 256), 256, 0, st, fa, nf, dnf, s_qs.as<QState>(), t, m,
+                              budget, cap);
                 }
             }
             tr.mark("filter (L trees)", st);
             // |S| exact for the round's accounting (trees whose count was skipped)
-            DL_LAUNCH(k_count_decide, (unsigned)ceil_div(na, 256), 256, 0, st, cur, na, nullptr, s_qs.as<QState>(), budget, 1);
+            DL_LAUNCH(k_count_decide, (unsigned)ceil_div(na, 256), 256, 0, st, cur, na, nullptr, s_qs.as<QState>(), budget, 1,
+                      (uint32_t*)nullptr);
             DL_LAUNCH(k_count_new, dim3((unsigned)na, (unsigned)ceil_div(nwords, CN_WORDS)), 256, 0, st, cur, nullptr,
                       s_qs.as<QState>(), s_bm.as<uint32_t>(), bm_prev, nwords, 1);
             DL_LAUNCH(k_round_offsets, 1, 1024, 0, st, cur, na, s_qs.as<QState>(), s_total.as<unsigned long long>());

@@ -141,10 +141,16 @@ def kernel_models(c, steps: int, st, n_local: int, nq: int, ld: int):
     proj_bytes = n_local * (4 * ld + LK) + (ns + nq) * (4 * ld + 4 * LK)
     proj_flops = 2.0 * 2 * (n_local + ns + nq) * ((LK + 15) // 16 * 16) * ld      # x_hi and x_lo MMAs
     return {
-        "k_range_filter": {"bytes": steps * filt, "smem_bytes": steps * lookups * 2,
-                           "unit": "per query: leaves_tested*2K + leaves_passed*8 + points_tested*K + "
-                                   "points_passed*12 + new*4 B (SURVEY 8(d) K5/K6)"},
+        FILTER_UNIT: {"bytes": steps * filt, "smem_bytes": steps * lookups * 2,
+                      "unit": "per query: leaves_tested*2K + leaves_passed*8 + points_tested*K + "
+                              "points_passed*12 + new*4 B (SURVEY 8(d) K5/K6), over both filter kernels "
+                              "(k_range_filter: tile/leaf bounds + dense tiles; k_leaf_points: sparse tiles' "
+                              "points), timed together"},
         "k_verify_rows": {"bytes": steps * ncand * (4 * d + 8), "unit": "per candidate 4d+8 B (row + id + d2)"},
+        "k_verify_gather": {"bytes": steps * ncand * (4 * d + 8),
+                            "unit": "per candidate 4d+8 B (row + id + d2); all candidates of the step are counted "
+                                    "here, so rounds verified on the tensor cores would inflate it (none at the "
+                                    "bench point: every round takes the gather)"},
         # tensor-core verification: per round a masked X.Q^T over all n rows x the round's active
         # queries; 3 tf32 MMAs (x.q, x.q_lo, x_lo.q) per product; active query-rounds = sum of rounds
         "k_verify_tc": {"bytes": steps * ncand * (4 * d + 8),
@@ -157,9 +163,33 @@ def kernel_models(c, steps: int, st, n_local: int, nq: int, ld: int):
     }
 
 
+FILTER_UNIT = "filter"                       # k_range_filter + k_leaf_points (one unit of work: Alg. 3)
+FILTER_KERNELS = ("k_range_filter", "k_leaf_points")
+
+
+def group_filter(prof):
+    """Profile entries with the two filter kernels merged into one unit (their launches of
+    k_range_filter counted as the unit's launches: one per tree per round)."""
+    out, fl, fms, parts = {}, 0, 0.0, {}
+    for k, (nl, ms) in prof.items():
+        if k.startswith(FILTER_KERNELS):
+            fms += ms
+            parts[k] = round(ms, 4)
+            if k.startswith("k_range_filter"):
+                fl += nl
+        else:
+            out[k] = (nl, ms)
+    if parts:
+        out[FILTER_UNIT] = (max(fl, 1), fms)
+    return out, parts
+
+
 def roofline_entry(name, model, ms, hbm, bf16, clocks, launches=1, traffic=None):
     ach = model["bytes"] / (ms / 1e3) / 1e9
-    tr = traffic.get(name) if traffic else None
+    if traffic and name == FILTER_UNIT:
+        tr = sum(v for k, v in traffic.items() if k.startswith(FILTER_KERNELS)) or None
+    else:
+        tr = traffic.get(name) if traffic else None
     e = {"kernel": name, "bound": "hbm", "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s",
          "frac": round(ach / hbm, 4), "traffic": tr, "algorithmic_bytes_per_launch": round(model["bytes"] / launches),
          "ms": round(ms, 4), "ms_per_launch": round(ms / launches, 4), "unit_of_work": model["unit"]}
@@ -372,17 +402,22 @@ def main():
         rec = recall(ids[sel], gt)
         hbm, bf16, bf16s, peak_src = peaks()
         kern = {k: {"launches": v[0], "ms": round(v[1], 4)} for k, v in sorted(prof.items(), key=lambda kv: -kv[1][1])}
-        dom = max(prof.items(), key=lambda kv: kv[1][1])[0] if prof else None
+        units, filter_parts = group_filter(prof)
+        dom = max(units.items(), key=lambda kv: kv[1][1])[0] if units else None
         models = kernel_models(cfg, args.steps, st, n_local, cfg.nq, (cfg.d + 7) // 8 * 8)
         roofs = []
         traffic = load_traffic()
-        for kname, (nl_, ms) in sorted(prof.items(), key=lambda kv: -kv[1][1]):
+        for kname, (nl_, ms) in sorted(units.items(), key=lambda kv: -kv[1][1]):
             for prefix, model in models.items():
                 if kname.startswith(prefix):
-                    roofs.append(roofline_entry(kname, model, ms, hbm, bf16, clocks, nl_, traffic))
+                    e = roofline_entry(kname, model, ms, hbm, bf16, clocks, nl_, traffic)
+                    if kname == FILTER_UNIT:
+                        e["parts_ms"] = filter_parts
+                    roofs.append(e)
+                    break
         roof = next((r for r in roofs if r["kernel"] == dom), None)
         if roof is not None:
-            roof["share_of_step"] = round(prof[dom][1] / step_ms, 4)
+            roof["share_of_step"] = round(units[dom][1] / step_ms, 4)
             roof["peak_source"] = peak_src
         line = {
             "metric": METRIC, "value": cfg.nq * args.steps / (query_ms / 1e3), "unit": "queries/s",

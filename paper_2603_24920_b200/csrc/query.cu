@@ -1482,6 +1482,9 @@ __device__ void bitonic_sort_smem(unsigned long long* a, int n2) {
 //      of S at their round-buffer slots, then one 8-lane group per candidate gathers its row
 //      with float4 loads (k_verify_gather): per candidate 4d bytes of X, no per-(row block,
 //      query) work.
+// NV > 0: the row is NV float4 per lane (ld = 32 NV), all loads issued before any arithmetic
+// (memory-level parallelism of a whole 4d-byte row per 8 lanes); NV = 0: any ld.
+template <int NV>
 __global__ void __launch_bounds__(256) k_verify_gather(const uint32_t* __restrict__ cand, const uint32_t* __restrict__ cq,
                                                        const int* __restrict__ act, const float* __restrict__ X,
                                                        const float* __restrict__ Q, int64_t ld, int64_t total,
@@ -1493,11 +1496,26 @@ __global__ void __launch_bounds__(256) k_verify_gather(const uint32_t* __restric
         const float4* x4 = reinterpret_cast<const float4*>(X + (int64_t)cand[slot] * ld);
         const float4* q4 = reinterpret_cast<const float4*>(Q + (int64_t)act[cq[slot]] * ld);
         float2 acc = make_float2(0.f, 0.f);
-        for (int f = u; f < nf4; f += 8) {
-            const float4 x = __ldg(x4 + f), y = __ldg(q4 + f);
-            const float2 e0 = make_float2(x.x - y.x, x.y - y.y), e1 = make_float2(x.z - y.z, x.w - y.w);
-            acc = __ffma2_rn(e0, e0, acc);
-            acc = __ffma2_rn(e1, e1, acc);
+        if (NV > 0) {
+            float4 x[NV > 0 ? NV : 1], y[NV > 0 ? NV : 1];
+#pragma unroll
+            for (int v = 0; v < NV; ++v) x[v] = __ldcs(x4 + u + 8 * v);      // streamed: read once
+#pragma unroll
+            for (int v = 0; v < NV; ++v) y[v] = __ldg(q4 + u + 8 * v);
+#pragma unroll
+            for (int v = 0; v < NV; ++v) {
+                const float2 e0 = make_float2(x[v].x - y[v].x, x[v].y - y[v].y);
+                const float2 e1 = make_float2(x[v].z - y[v].z, x[v].w - y[v].w);
+                acc = __ffma2_rn(e0, e0, acc);
+                acc = __ffma2_rn(e1, e1, acc);
+            }
+        } else {
+            for (int f = u; f < nf4; f += 8) {
+                const float4 x = __ldg(x4 + f), y = __ldg(q4 + f);
+                const float2 e0 = make_float2(x.x - y.x, x.y - y.y), e1 = make_float2(x.z - y.z, x.w - y.w);
+                acc = __ffma2_rn(e0, e0, acc);
+                acc = __ffma2_rn(e1, e1, acc);
+            }
         }
         float s_ = acc.x + acc.y;
         s_ += __shfl_xor_sync(0xffffffffu, s_, 1);
@@ -2267,8 +2285,14 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
                     }
                     DL_LAUNCH(k_verify_prep<true>, (unsigned)na, 1024, 0, st, cur, s_qs.as<QState>(), s_bm.as<uint32_t>(),
                               s_ver.as<uint32_t>(), nwords, nullptr, nullptr, va.cand, s_cq.as<uint32_t>());
-                    DL_LAUNCH(k_verify_gather, (unsigned)std::min<int64_t>(ceil_div((int64_t)tot * 8, 256), 148 * 32), 256,
-                              0, st, va.cand, s_cq.as<uint32_t>(), cur, ix.Xp, Qb, (int64_t)ix.ld, (int64_t)tot, va.d2);
+                    const unsigned vg = (unsigned)std::min<int64_t>(ceil_div((int64_t)tot * 8, 256), 148 * 32);
+                    auto k_verify_gather_sel = ix.ld == 128   ? k_verify_gather<4>
+                                               : ix.ld == 256 ? k_verify_gather<8>
+                                               : ix.ld == 512 ? k_verify_gather<16>
+                                               : ix.ld == 96  ? k_verify_gather<3>
+                                                              : k_verify_gather<0>;
+                    DL_LAUNCH(k_verify_gather_sel, vg, 256, 0, st, va.cand, s_cq.as<uint32_t>(), cur, ix.Xp, Qb,
+                              (int64_t)ix.ld, (int64_t)tot, va.d2);
                 }
                 done_tc = true;
             }

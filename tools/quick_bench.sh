@@ -7,3 +7,9 @@ print("value", round(d["value"]), "query_ms", round(d["query_ms_per_step"],3), "
 print(d["filter_counts_per_query"])
 for k,v in list(d["kernels"].items())[:8]: print("  ", k, v["launches"], round(v["ms"]/d["steps"],3), "ms/step")
 PY
+python - <<'PY'
+import json
+d=json.loads([l for l in open("gpurun_out/bench_quick.log") if l.startswith("{")][-1])
+for r in d["rooflines"]: print("  roof", r["kernel"], r["bound"], r["achieved"], r["unit"], r["frac"], r.get("traffic"), r.get("parts_ms"))
+print("  dominant", d["roofline"]["kernel"], d["roofline"]["frac"], d["roofline"].get("share_of_step"))
+PY

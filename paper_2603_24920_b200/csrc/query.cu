@@ -778,15 +778,18 @@ struct LPArgs {
     unsigned long long* ctr;
 };
 
+// KT, NRT > 0: K and N_r fixed at compile time (table rows at immediate offsets, a static table)
+template <int KT, int NRT>
 __global__ void __launch_bounds__(256) k_leaf_points(LPArgs a) {
     extern __shared__ __align__(16) unsigned char lp_smem[];
+    __shared__ __align__(16) uint16_t lp_static[(KT > 0 && NRT > 0) ? KT * NRT : 8];
     const int ai = blockIdx.x;
     if (ai >= (a.dna ? *a.dna : a.na)) return;
     const int q = a.act[ai];
     const uint32_t np = a.pcnt[q];
     if (np == 0 || a.qs[q].status != ST_ACTIVE) return;
-    const int K = a.K, N_r = a.N_r, KN = K * N_r;
-    uint16_t* s_e = reinterpret_cast<uint16_t*>(lp_smem);                  // 12-bit lower bounds
+    const int K = KT > 0 ? KT : a.K, N_r = NRT > 0 ? NRT : a.N_r, KN = K * N_r;
+    uint16_t* s_e = (KT > 0 && NRT > 0) ? lp_static : reinterpret_cast<uint16_t*>(lp_smem);   // 12-bit lower bounds
     const float* s_d = a.lut + ((int64_t)q * a.L + a.t) * KN;              // exact terms (band only, L1/L2)
     {
         const uint4* src = reinterpret_cast<const uint4*>(a.q12 + ((int64_t)q * a.L + a.t) * KN);
@@ -1991,7 +1994,11 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
     lpa.N_r = ix.N_r;
     const size_t lp_smem = (size_t)ix.K * ix.N_r * sizeof(uint16_t);
     Scratch s_q12(st, use_pairs ? sizeof(uint16_t) * (size_t)(qb * LK * ix.N_r) : 0);
-    if (use_pairs) DL_CUDA(cudaFuncSetAttribute(k_leaf_points, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lp_smem));
+    const bool lp_fixed = ix.K == 16 && ix.N_r == 256;
+    auto k_leaf_points_sel = lp_fixed ? k_leaf_points<16, 256> : k_leaf_points<0, 0>;
+    const size_t lp_dyn = lp_fixed ? 0 : lp_smem;
+    if (use_pairs && !lp_fixed)
+        DL_CUDA(cudaFuncSetAttribute(k_leaf_points_sel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lp_smem));
     ra.leaf_off = ix.leaf_off.as<uint32_t>();
     // leaf pruning uses the tight boxes (a valid, tighter bound for every member); RELAXED takes
     // whole leaves by the leaf's own (prefix) box, as the method defines it
@@ -2209,7 +2216,7 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
                     lpa.ctr = s_ctr.as<unsigned long long>();
                     lpa.q12 = s_q12.as<uint16_t>();
                     static const int lp_y = std::getenv("DETLSH_LP_Y") ? std::atoi(std::getenv("DETLSH_LP_Y")) : 16;
-                    DL_LAUNCH(k_leaf_points, dim3((unsigned)nf, (unsigned)lp_y), 256, lp_smem, st, lpa);
+                    DL_LAUNCH(k_leaf_points_sel, dim3((unsigned)nf, (unsigned)lp_y), 256, lp_dyn, st, lpa);
                 }
                 if (a.lb_order) lb_order_tree(t, fa, nf, dnf);
                 DL_LAUNCH(k_count_decide, (unsigned)ceil_div(nf, 256), 256, 0, st, fa, nf, dnf, s_qs.as<QState>(), budget,

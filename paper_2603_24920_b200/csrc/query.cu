@@ -1513,11 +1513,22 @@ __global__ void __launch_bounds__(256) k_verify_gather(const uint32_t* __restric
                 acc = __ffma2_rn(e1, e1, acc);
             }
         } else {
-            for (int f = u; f < nf4; f += 8) {
-                const float4 x = __ldg(x4 + f), y = __ldg(q4 + f);
-                const float2 e0 = make_float2(x.x - y.x, x.y - y.y), e1 = make_float2(x.z - y.z, x.w - y.w);
-                acc = __ffma2_rn(e0, e0, acc);
-                acc = __ffma2_rn(e1, e1, acc);
+            // 8 float4 of the row in flight per lane, then their arithmetic
+            for (int f0 = u; f0 < nf4; f0 += 64) {
+                float4 x[8];
+#pragma unroll
+                for (int v = 0; v < 8; ++v) {
+                    const int f = f0 + 8 * v;
+                    x[v] = f < nf4 ? __ldcs(x4 + f) : make_float4(0.f, 0.f, 0.f, 0.f);
+                }
+#pragma unroll
+                for (int v = 0; v < 8; ++v) {
+                    const int f = f0 + 8 * v;
+                    const float4 y = f < nf4 ? __ldg(q4 + f) : make_float4(0.f, 0.f, 0.f, 0.f);
+                    const float2 e0 = make_float2(x[v].x - y.x, x[v].y - y.y), e1 = make_float2(x[v].z - y.z, x[v].w - y.w);
+                    acc = __ffma2_rn(e0, e0, acc);
+                    acc = __ffma2_rn(e1, e1, acc);
+                }
             }
         }
         float s_ = acc.x + acc.y;

@@ -520,24 +520,29 @@ __global__ void __launch_bounds__(RF_THREADS, RF_CTAS) k_range_filter(RFArgs a) 
             use_pq = (unsigned long long)a.pq_cost * w_ < 170ull * (P1 - P0);
         }
         if (use_pq && a.plist != nullptr && a.mode == DETLSH_MODE_CELL) {
-            // hand the (query, reachable leaf) pairs of this sparse tile to k_leaf_points: lane g
-            // reserves query g's slots (all reservations in flight together), then the writes
+            // hand the (query, reachable leaf) pairs of this sparse tile to k_leaf_points: per-warp
+            // shared counters count each query's pairs, lane g reserves query g's slots in its global
+            // list (all reservations in flight together), then each lane writes its own pairs at
+            // slots taken from a second counter -- work per lane ~ its (few) pairs, not per query of
+            // the group (a query's list order does not matter: k_leaf_points ORs marks)
+            uint32_t* w_cnt = s_pre[warp];          // [0,16) counts, [16,32) bases (the per-query
+            uint32_t* w_slot = s_off[warp];         // path's scratch, unused in CELL); [0,16) slots
             const uint32_t my_lq = lane < nlt ? lq[lane] : 0u;
-            uint32_t bal_g = 0;
-            for (uint32_t mm = tm; mm; mm &= mm - 1) {
-                const int g = __ffs(mm) - 1;
-                const uint32_t bal = __ballot_sync(0xffffffffu, (my_lq >> g) & 1u);
-                if (lane == g) bal_g = bal;
+            if (lane < 16) { w_cnt[lane] = 0; w_slot[lane] = 0; }
+            __syncwarp();
+            for (uint32_t mm = my_lq; mm; mm &= mm - 1) atomicAdd(&w_cnt[__ffs(mm) - 1], 1u);
+            __syncwarp();
+            if (lane < 16) {
+                const uint32_t c_ = w_cnt[lane];
+                w_cnt[16 + lane] = c_ ? atomicAdd(a.pcnt + s_q[lane], c_) : 0u;
             }
-            uint32_t base_g = 0;
-            if (bal_g) base_g = atomicAdd(a.pcnt + s_q[lane], (uint32_t)__popc(bal_g));
-            for (uint32_t mm = tm; mm; mm &= mm - 1) {
+            __syncwarp();
+            for (uint32_t mm = my_lq; mm; mm &= mm - 1) {
                 const int g = __ffs(mm) - 1;
-                const uint32_t bal = __shfl_sync(0xffffffffu, bal_g, g);
-                const uint32_t base = __shfl_sync(0xffffffffu, base_g, g);
-                if ((bal >> lane) & 1u)
-                    a.plist[(int64_t)s_q[g] * a.pcap + base + __popc(bal & lanemask_lt())] = lb + lane;
+                const uint32_t sl = w_cnt[16 + g] + atomicAdd(&w_slot[g], 1u);
+                a.plist[(int64_t)s_q[g] * a.pcap + sl] = lb + lane;
             }
+            __syncwarp();
         } else if (use_pq) {
             uint32_t* pre = s_pre[warp];
             uint32_t* offs = s_off[warp];

@@ -128,13 +128,15 @@ __global__ void k_build_qlut(const float* __restrict__ lut, const int* __restric
 //      16 queries' tables itself.  Inactive slots get the cap (never pass).
 __global__ void k_group_table(const int* __restrict__ act, int na_ub, const int* __restrict__ dna,
                               const QState* __restrict__ qs, const uint16_t* __restrict__ qlut, int64_t per_q, int t,
-                              int KN, uint32_t cap, uint4* __restrict__ gtab) {
+                              int KN, uint32_t cap, const uint8_t* __restrict__ sx, int L, int K, int N_r,
+                              uint4* __restrict__ gtab) {
     const int na = dna ? *dna : na_ub;       // device count (the list is compacted on the device)
     const int64_t groups = (na + 15) / 16;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < groups * KN;
          i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t grp = i / KN;
         const int e = (int)(i - grp * KN);
+        const int j = e / N_r, c = e - j * N_r;
         uint32_t w[4] = {0, 0, 0, 0};
 #pragma unroll
         for (int g = 0; g < 16; ++g) {
@@ -142,7 +144,10 @@ __global__ void k_group_table(const int* __restrict__ act, int na_ub, const int*
             uint32_t v = cap;
             if (gi < na) {
                 const int q = act[gi];
-                if (qs[q].status == ST_ACTIVE) v = qlut[(int64_t)q * per_q + (int64_t)t * KN + e];
+                if (qs[q].status == ST_ACTIVE) {
+                    v = qlut[(int64_t)q * per_q + (int64_t)t * KN + e];
+                    if ((int)sx[((int64_t)q * L + t) * K + j] < c) v |= 0x80u;     // region flag (k_range_filter)
+                }
             }
             w[g >> 2] |= v << (8 * (g & 3));
         }
@@ -159,13 +164,18 @@ __global__ void k_group_table(const int* __restrict__ act, int na_ub, const int*
 //      passing points are OR-marked into the per-query bitmap (RED.OR).  The fp32 decision
 //      sums the same terms in the same order as the cell bound's definition (AMB-12), so the
 //      screen never changes a result.
-#ifndef RF_FTAB
-#define RF_FTAB 0                // 1: query-set masks of the SIMD leaf test from a shared table (+8 KB)
-#endif
-constexpr int RF_THREADS = RF_FTAB ? 384 : 256;
-constexpr int RF_CTAS = RF_FTAB ? 2 : 3;      // resident CTAs per SM
+constexpr int RF_THREADS = 256;
+constexpr int RF_CTAS = 3;       // resident CTAs per SM
 constexpr int RF_G = 16;         // queries per CTA (8-bit terms); 8 selects 12-bit terms
 constexpr int RF_BQ = 64;        // band queue per warp: < 32 left over + one step of <= 32
+
+// Byte-wise sign replicate: 0xFF in each byte whose bit 7 is set, else 0x00 (prmt selector
+// nibbles 8..B: byte 0..3 with its msb replicated).
+__device__ __forceinline__ uint32_t prmt_sign(uint32_t x) {
+    uint32_t r;
+    asm("prmt.b32 %0, %1, 0, 0xBA98;" : "=r"(r) : "r"(x));
+    return r;
+}
 
 template <int G> struct QuantSpec;
 template <> struct QuantSpec<8> { static constexpr uint32_t QT = 2048, CAP = 4095; };
@@ -216,13 +226,11 @@ __global__ void __launch_bounds__(RF_THREADS, RF_CTAS) k_range_filter(RFArgs a) 
     const int K = KT ? KT : a.K;
     const int N_r = NRT ? NRT : a.N_r;
     uint4* s_qe = reinterpret_cast<uint4*>(smem);                                       // [K][N_r] x 16 B
-    // G = 16, K = 16: s_fl[j][c] = bit g set iff query g's region code in dim j is < c (c = 0..N_r),
-    // so the box term D_j[clamp(s, lo, hi)] of all 16 queries is D_j[lo] on the queries with
-    // s < lo, D_j[hi] on those with s > hi (= not s < hi+1), and 0 on the rest (D_j[s] = 0)
-#if RF_FTAB
-    uint16_t* s_fl = reinterpret_cast<uint16_t*>(s_qe + K * N_r);                       // [K][N_r+1]
-#endif
-    __shared__ __align__(16) uint8_t s_sxT[16][16];                                     // [dim][query] region codes
+    // G = 16: byte g of entry (j, c) is query g's 7-bit term D_j[c] with bit 7 set iff the
+    // query's own region code in dim j is < c (k_group_table).  A leaf box term D_j[clamp(s, lo,
+    // hi)] is then D_j[lo] where entry (j, lo) is flagged (s < lo), D_j[hi] where entry (j, hi)
+    // is not (s >= hi; D_j[s] = 0 covers s = hi), 0 otherwise -- byte masks from the flag by one
+    // sign-replicating byte permute.  Every other reader masks the flag off.
     __shared__ int s_q[G];
     __shared__ __align__(16) uint8_t s_sx[G][32];
     __shared__ float s_qp[G][32];                                                        // EXACT: q'_t
@@ -270,28 +278,14 @@ __global__ void __launch_bounds__(RF_THREADS, RF_CTAS) k_range_filter(RFArgs a) 
                 uint32_t w[4] = {0, 0, 0, 0};
 #pragma unroll
                 for (int g = 0; g < G; ++g) {
-                    const uint32_t v = src[g] ? src[g][i] : CAP;                       // inactive: never passes
+                    uint32_t v = src[g] ? src[g][i] : CAP;                             // inactive: never passes
+                    if (G == 16 && src[g] && (int)a.sx[((int64_t)s_q[g] * a.L + a.t) * K + i / N_r] < i % N_r)
+                        v |= 0x80u;                                                    // region flag (above)
                     if (G == 8) w[g >> 1] |= v << (16 * (g & 1));
                     else w[g >> 2] |= v << (8 * (g & 3));
                 }
                 s_qe[i] = make_uint4(w[0], w[1], w[2], w[3]);
             }
-        }
-        if (G == 16 && KT == 16) {
-            {
-                const int j = threadIdx.x >> 4, g = threadIdx.x & 15;
-                if (threadIdx.x < 256) s_sxT[j][g] = s_q[g] >= 0 ? a.sx[((int64_t)s_q[g] * a.L + a.t) * K + j] : 0;
-            }
-#if RF_FTAB
-            for (int i = threadIdx.x; i < K * (N_r + 1); i += RF_THREADS) {
-                const int j = i / (N_r + 1), c = i - j * (N_r + 1);
-                uint32_t f = 0;
-#pragma unroll
-                for (int g = 0; g < G; ++g)
-                    if (s_q[g] >= 0 && (int)a.sx[((int64_t)s_q[g] * a.L + a.t) * K + j] < c) f |= 1u << g;
-                s_fl[i] = (uint16_t)f;
-            }
-#endif
         }
         if (threadIdx.x < K) {
 #pragma unroll
@@ -344,14 +338,14 @@ __global__ void __launch_bounds__(RF_THREADS, RF_CTAS) k_range_filter(RFArgs a) 
                         const uint32_t wh = (j >> 2) == 0 ? th4.x : (j >> 2) == 1 ? th4.y : (j >> 2) == 2 ? th4.z : th4.w;
                         const uint32_t ws = (j >> 2) == 0 ? sx4.x : (j >> 2) == 1 ? sx4.y : (j >> 2) == 2 ? sx4.z : sx4.w;
                         const int c = min(max((int)((ws >> sh) & 255u), (int)((wl >> sh) & 255u)), (int)((wh >> sh) & 255u));
-                        acc += G == 8 ? (uint32_t)s_h[(j * N_r + c) * 8 + lane] : (uint32_t)s_b[(j * N_r + c) * 16 + lane];
+                        acc += G == 8 ? (uint32_t)s_h[(j * N_r + c) * 8 + lane] : (uint32_t)(s_b[(j * N_r + c) * 16 + lane] & 0x7Fu);
                     }
                 } else {
                     const uint8_t* tl = a.tile_lo + tile * K;
                     const uint8_t* th = a.tile_hi + tile * K;
                     for (int j = 0; j < K; ++j) {
                         const int e = (j * N_r + min(max((int)s_sx[lane][j], (int)tl[j]), (int)th[j])) * 16;
-                        acc += G == 8 ? (uint32_t)s_h[e / 2 + lane] : (uint32_t)s_b[e + lane];
+                        acc += G == 8 ? (uint32_t)s_h[e / 2 + lane] : (uint32_t)(s_b[e + lane] & 0x7Fu);
                     }
                 }
                 pass = acc <= QT;
@@ -384,24 +378,13 @@ __global__ void __launch_bounds__(RF_THREADS, RF_CTAS) k_range_filter(RFArgs a) 
                         const uint4 dl = s_qe[j * N_r + cl];
                         const uint4 dh = s_qe[j * N_r + ch];
                         const uint32_t dlw[4] = {dl.x, dl.y, dl.z, dl.w}, dhw[4] = {dh.x, dh.y, dh.z, dh.w};
-#if RF_FTAB
-                        const uint32_t fl = s_fl[j * (N_r + 1) + cl];
-                        const uint32_t fh = ~(uint32_t)s_fl[j * (N_r + 1) + ch + 1];
 #pragma unroll
                         for (int w = 0; w < 4; ++w) {
-                            // 4 query bits -> 4 byte masks: bit i moves to bit 8i, then x 0xFF
-                            const uint32_t ml = (((fl >> (4 * w)) & 15u) * 0x00204081u & 0x01010101u) * 0xFFu;
-                            const uint32_t mh = (((fh >> (4 * w)) & 15u) * 0x00204081u & 0x01010101u) * 0xFFu;
-                            tw[u][w] = (dlw[w] & ml) | (dhw[w] & mh);
+                            const uint32_t ml = prmt_sign(dlw[w]);                  // 0xFF: s < lo
+                            const uint32_t mh = prmt_sign(dhw[w]);                  // 0xFF: s < hi
+                            const uint32_t th = dhw[w] & ~mh & 0x7F7F7F7Fu;         // D_j[hi] where s >= hi
+                            tw[u][w] = ((dlw[w] & ml) | th) & 0x7F7F7F7Fu;          // + D_j[lo] where s < lo
                         }
-#else
-                        const uint4 sq = *reinterpret_cast<const uint4*>(&s_sxT[j][0]);
-                        const uint32_t sqw[4] = {sq.x, sq.y, sq.z, sq.w};
-                        const uint32_t l4 = cl * 0x01010101u, h4 = ch * 0x01010101u;
-#pragma unroll
-                        for (int w = 0; w < 4; ++w)
-                            tw[u][w] = (dlw[w] & __vcmpltu4(sqw[w], l4)) | (dhw[w] & __vcmpgtu4(sqw[w], h4));
-#endif
                     }
 #pragma unroll
                     for (int w = 0; w < 4; ++w) {
@@ -430,7 +413,7 @@ __global__ void __launch_bounds__(RF_THREADS, RF_CTAS) k_range_filter(RFArgs a) 
                         const uint32_t wh = (j >> 2) == 0 ? hi4.x : (j >> 2) == 1 ? hi4.y : (j >> 2) == 2 ? hi4.z : hi4.w;
                         const uint32_t ws = (j >> 2) == 0 ? sx4.x : (j >> 2) == 1 ? sx4.y : (j >> 2) == 2 ? sx4.z : sx4.w;
                         const int c = min(max((int)((ws >> sh) & 255u), (int)((wl >> sh) & 255u)), (int)((wh >> sh) & 255u));
-                        acc += G == 8 ? (uint32_t)s_h[(j * N_r + c) * 8 + g] : (uint32_t)s_b[(j * N_r + c) * 16 + g];
+                        acc += G == 8 ? (uint32_t)s_h[(j * N_r + c) * 8 + g] : (uint32_t)(s_b[(j * N_r + c) * 16 + g] & 0x7Fu);
                     }
                     if (acc <= QT) m |= 1u << g;
                 }
@@ -440,7 +423,7 @@ __global__ void __launch_bounds__(RF_THREADS, RF_CTAS) k_range_filter(RFArgs a) 
                     uint32_t acc = 0;
                     for (int j = 0; j < K; ++j) {
                         const int e = (j * N_r + min(max((int)s_sx[g][j], (int)a.lo[l * K + j]), (int)a.hi[l * K + j])) * 16;
-                        acc += G == 8 ? (uint32_t)s_h[e / 2 + g] : (uint32_t)s_b[e + g];
+                        acc += G == 8 ? (uint32_t)s_h[e / 2 + g] : (uint32_t)(s_b[e + g] & 0x7Fu);
                     }
                     if (acc <= QT) m |= 1u << g;
                 }
@@ -593,7 +576,7 @@ __global__ void __launch_bounds__(RF_THREADS, RF_CTAS) k_range_filter(RFArgs a) 
                             for (int j = 0; j < 16; ++j) {
                                 const uint32_t word = (j >> 2) == 0 ? c4.x : (j >> 2) == 1 ? c4.y : (j >> 2) == 2 ? c4.z : c4.w;
                                 const uint32_t code = (word >> (8 * (j & 3))) & 255u;
-                                acc += G == 8 ? (uint32_t)s_h[(j * N_r + code) * 8 + g] : (uint32_t)s_b[(j * N_r + code) * 16 + g];
+                                acc += G == 8 ? (uint32_t)s_h[(j * N_r + code) * 8 + g] : (uint32_t)(s_b[(j * N_r + code) * 16 + g] & 0x7Fu);
                             }
                             ++c_pt;
                             const bool ok = acc <= QT, sure = acc + 17 <= QT;
@@ -662,8 +645,11 @@ __global__ void __launch_bounds__(RF_THREADS, RF_CTAS) k_range_filter(RFArgs a) 
                                 const uint4 vb = row[1 * N_r + ((word >> 8) & 255u)];
                                 const uint4 vc = row[2 * N_r + ((word >> 16) & 255u)];
                                 const uint4 vd = row[3 * N_r + (word >> 24)];
-                                const uint32_t p2[4] = {va.x + vb.x, va.y + vb.y, va.z + vb.z, va.w + vb.w};
-                                const uint32_t r2[4] = {vc.x + vd.x, vc.y + vd.y, vc.z + vd.z, vc.w + vd.w};
+                                constexpr uint32_t M7 = 0x7F7F7F7Fu;     // region flags off
+                                const uint32_t p2[4] = {(va.x & M7) + (vb.x & M7), (va.y & M7) + (vb.y & M7),
+                                                        (va.z & M7) + (vb.z & M7), (va.w & M7) + (vb.w & M7)};
+                                const uint32_t r2[4] = {(vc.x & M7) + (vd.x & M7), (vc.y & M7) + (vd.y & M7),
+                                                        (vc.z & M7) + (vd.z & M7), (vc.w & M7) + (vd.w & M7)};
 #pragma unroll
                                 for (int i = 0; i < 4; ++i) {
                                     acc[2 * i] += (p2[i] & 0x00FF00FFu) + (r2[i] & 0x00FF00FFu);
@@ -685,7 +671,7 @@ __global__ void __launch_bounds__(RF_THREADS, RF_CTAS) k_range_filter(RFArgs a) 
                         for (int j = 0; j < K; ++j) {
                             const int e = (j * N_r + a.tcodes[pos * K + j]) * 16;
 #pragma unroll
-                            for (int g = 0; g < G; ++g) acc[g] += G == 8 ? (uint32_t)s_h[e / 2 + g] : (uint32_t)s_b[e + g];
+                            for (int g = 0; g < G; ++g) acc[g] += G == 8 ? (uint32_t)s_h[e / 2 + g] : (uint32_t)(s_b[e + g] & 0x7Fu);
                         }
 #pragma unroll
                         for (int g = 0; g < G; ++g) {
@@ -1977,7 +1963,7 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
     // per-batch LUTs
     Scratch s_lut(st, sizeof(float) * (size_t)(qb * LK * ix.N_r));
     Scratch s_sx(st, (size_t)(qb * LK));
-    const size_t rf_smem = (size_t)16 * ix.K * ix.N_r + (RF_FTAB ? sizeof(uint16_t) * ix.K * (ix.N_r + 1) : 0);
+    const size_t rf_smem = (size_t)16 * ix.K * ix.N_r;
     Scratch s_qlut(st, sizeof(uint16_t) * (size_t)(qb * LK * ix.N_r));
     Scratch s_gtab(st, (size_t)16 * ceil_div(qb, RF_G) * ix.K * ix.N_r);
     static const int pq_env = std::getenv("DETLSH_FILTER_PQ") ? std::atoi(std::getenv("DETLSH_FILTER_PQ")) : 1;
@@ -2207,7 +2193,7 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
                     uint4* gt = s_gtab.as<uint4>();
                     DL_LAUNCH(k_group_table, (unsigned)std::min<int64_t>(ceil_div((int64_t)groups * ix.K * ix.N_r, 256), 148 * 16),
                               256, 0, st, fa, nf, dnf, s_qs.as<QState>(), s_qlut.as<uint16_t>(), LK * ix.N_r, t,
-                              ix.K * ix.N_r, (uint32_t)QuantSpec<RF_G>::CAP, gt);
+                              ix.K * ix.N_r, (uint32_t)QuantSpec<RF_G>::CAP, s_sx.as<uint8_t>(), ix.L, ix.K, ix.N_r, gt);
                     ra.gtab = gt;
                 }
                 const int64_t ntiles = ra.tile_end - ra.tile_begin;

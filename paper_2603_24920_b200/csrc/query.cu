@@ -755,6 +755,7 @@ struct LPArgs {
     QState* qs_mut;
     const uint32_t* plist;
     uint32_t* pcnt;
+    uint32_t* ptake;            // [Qb] chunks of the list taken so far (dynamic work split)
     int64_t pcap;
     const float* lut;           // [Qb][L][K][N_r]
     const uint16_t* q12;        // [Qb][L][K][N_r] 12-bit lower bounds of this round (k_build_qlut, QT 2048)
@@ -769,8 +770,9 @@ struct LPArgs {
     unsigned long long* ctr;
 };
 
-// KT, NRT > 0: K and N_r fixed at compile time (table rows at immediate offsets, a static table)
-template <int KT, int NRT>
+// KT, NRT > 0: K and N_r fixed at compile time (table rows at immediate offsets, a static table);
+// LPG listed leaves per warp chunk
+template <int KT, int NRT, int LPG>
 __global__ void __launch_bounds__(256) k_leaf_points(LPArgs a) {
     extern __shared__ __align__(16) unsigned char lp_smem[];
     __shared__ __align__(16) uint16_t lp_static[(KT > 0 && NRT > 0) ? KT * NRT : 8];
@@ -794,10 +796,14 @@ __global__ void __launch_bounds__(256) k_leaf_points(LPArgs a) {
     const uint32_t* pl = a.plist + (int64_t)q * a.pcap;
     uint32_t* bm = a.bitmap + (int64_t)q * a.nwords;
     uint32_t tested = 0, passed = 0;
-    // a warp takes 16 listed leaves at a time and screens their points packed 32 per step (the
-    // owning leaf of packed point i found by a 4-step search over the warp's prefix of sizes)
-    constexpr int LPG = 16;
-    for (uint32_t e0 = (blockIdx.y * 8 + (threadIdx.x >> 5)) * LPG; e0 < np; e0 += gridDim.y * 8 * LPG) {
+    // a warp takes LPG listed leaves at a time -- chunks handed out dynamically by a per-query
+    // counter to all warps of the query's blocks -- and screens their points packed 32 per step
+    // (the owning leaf of packed point i found by a log2(LPG)-step search over the chunk's prefix)
+    for (;;) {
+        uint32_t ck = 0;
+        if (lane == 0) ck = atomicAdd(a.ptake + q, 1u);
+        const uint32_t e0 = __shfl_sync(0xffffffffu, ck, 0) * LPG;
+        if (e0 >= np) break;
         uint32_t my_p0 = 0, my_sz = 0;
         if (lane < LPG && e0 + lane < np) {
             const uint32_t l = pl[e0 + lane];
@@ -1069,12 +1075,13 @@ __global__ void k_lbo_reset(const int* __restrict__ cross, int ncross, const uin
 // Before counting |S| after a tree: the bitmap diff is needed only if the budget may have been
 // reached (|S| <= cnt + marks since the last count) or the count is due (force: end of round,
 // or lb_order, which needs |S| exact after every tree).
-// (pcnt != null: also resets the pair-list lengths of the tree just filtered.)
+// (pcnt != null: also resets the pair-list lengths and take counters of the tree just filtered.)
 __global__ void k_count_decide(const int* __restrict__ act, int na_ub, const int* __restrict__ dna,
-                               QState* __restrict__ qs, int64_t budget, int force, uint32_t* __restrict__ pcnt) {
+                               QState* __restrict__ qs, int64_t budget, int force, uint32_t* __restrict__ pcnt,
+                               uint32_t* __restrict__ ptake) {
     const int na = dna ? *dna : na_ub;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < na; i += gridDim.x * blockDim.x) {
-        if (pcnt) pcnt[act[i]] = 0;
+        if (pcnt) { pcnt[act[i]] = 0; ptake[act[i]] = 0; }
         QState* s = &qs[act[i]];
         const int d = (s->status == ST_ACTIVE && s->pub > 0 && (force || s->cnt + s->pub >= budget)) ? 1 : 0;
         s->doc = d;
@@ -1980,7 +1987,7 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
     static const int pairs_env = std::getenv("DETLSH_LEAF_PAIRS") ? std::atoi(std::getenv("DETLSH_LEAF_PAIRS")) : 1;
     const bool use_pairs = pairs_env && a.mode == DETLSH_MODE_CELL && ix.K <= 32;
     Scratch s_plist(st, use_pairs ? sizeof(uint32_t) * (size_t)(qb * pcap) : 0);
-    Scratch s_pcnt(st, sizeof(uint32_t) * (size_t)qb);
+    Scratch s_pcnt(st, sizeof(uint32_t) * (size_t)(2 * qb));   // list lengths, take counters
     ra.plist = use_pairs ? s_plist.as<uint32_t>() : nullptr;
     ra.pcnt = s_pcnt.as<uint32_t>();
     ra.pcap = pcap;
@@ -1989,6 +1996,7 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
     lpa.qs_mut = s_qs.as<QState>();
     lpa.plist = ra.plist;
     lpa.pcnt = ra.pcnt;
+    lpa.ptake = ra.pcnt + qb;
     lpa.pcap = pcap;
     lpa.leaf_off = ix.leaf_off.as<uint32_t>();
     lpa.L = ix.L;
@@ -1997,7 +2005,9 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
     const size_t lp_smem = (size_t)ix.K * ix.N_r * sizeof(uint16_t);
     Scratch s_q12(st, use_pairs ? sizeof(uint16_t) * (size_t)(qb * LK * ix.N_r) : 0);
     const bool lp_fixed = ix.K == 16 && ix.N_r == 256;
-    auto k_leaf_points_sel = lp_fixed ? k_leaf_points<16, 256> : k_leaf_points<0, 0>;
+    static const int lp_g = std::getenv("DETLSH_LP_G") ? std::atoi(std::getenv("DETLSH_LP_G")) : 16;
+    auto k_leaf_points_sel = lp_fixed ? (lp_g == 8 ? k_leaf_points<16, 256, 8> : k_leaf_points<16, 256, 16>)
+                                      : k_leaf_points<0, 0, 16>;
     const size_t lp_dyn = lp_fixed ? 0 : lp_smem;
     if (use_pairs && !lp_fixed)
         DL_CUDA(cudaFuncSetAttribute(k_leaf_points_sel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lp_smem));
@@ -2140,7 +2150,7 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
         DL_CUDA(cudaMemsetAsync(s_bm.p, 0, sizeof(uint32_t) * (size_t)(2 * qb * nwords), st));
         DL_CUDA(cudaMemsetAsync(s_ver.p, 0, sizeof(uint32_t) * (size_t)(qb * nwords), st));
         DL_CUDA(cudaMemsetAsync(s_ctr.p, 0, sizeof(unsigned long long) * (size_t)(4 * qb), st));
-        DL_CUDA(cudaMemsetAsync(s_pcnt.p, 0, sizeof(uint32_t) * (size_t)qb, st));
+        DL_CUDA(cudaMemsetAsync(s_pcnt.p, 0, sizeof(uint32_t) * (size_t)(2 * qb), st));
         tr.mark("batch setup", st);
         DL_LAUNCH(k_init_batch, (unsigned)ceil_div(nqb, 256), 256, 0, st, s_qs.as<QState>(), act, nqb);
         int na = nqb;
@@ -2222,7 +2232,7 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
                 }
                 if (a.lb_order) lb_order_tree(t, fa, nf, dnf);
                 DL_LAUNCH(k_count_decide, (unsigned)ceil_div(nf, 256), 256, 0, st, fa, nf, dnf, s_qs.as<QState>(), budget,
-                          a.lb_order ? 1 : 0, use_pairs ? ra.pcnt : (uint32_t*)nullptr);
+                          a.lb_order ? 1 : 0, use_pairs ? ra.pcnt : (uint32_t*)nullptr, lpa.ptake);
                 DL_LAUNCH(k_count_new, dim3((unsigned)nf, (unsigned)ceil_div(nwords, CN_WORDS)), 256, 0, st, fa, dnf,
                           s_qs.as<QState>(), s_bm.as<uint32_t>(), bm_prev, nwords, 1);
                 if (t + 1 < ix.L) {
@@ -2240,7 +2250,7 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
             tr.mark("filter (L trees)", st);
             // |S| exact for the round's accounting (trees whose count was skipped)
             DL_LAUNCH(k_count_decide, (unsigned)ceil_div(na, 256), 256, 0, st, cur, na, nullptr, s_qs.as<QState>(), budget, 1,
-                      (uint32_t*)nullptr);
+                      (uint32_t*)nullptr, (uint32_t*)nullptr);
             DL_LAUNCH(k_count_new, dim3((unsigned)na, (unsigned)ceil_div(nwords, CN_WORDS)), 256, 0, st, cur, nullptr,
                       s_qs.as<QState>(), s_bm.as<uint32_t>(), bm_prev, nwords, 1);
             DL_LAUNCH(k_round_offsets, 1, 1024, 0, st, cur, na, s_qs.as<QState>(), s_total.as<unsigned long long>());

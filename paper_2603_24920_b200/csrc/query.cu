@@ -177,6 +177,14 @@ __device__ __forceinline__ uint32_t prmt_sign(uint32_t x) {
     return r;
 }
 
+// Mark id in query row (bm, sm) of the union S: the bit in the bitmap and the bit of its word in
+// the row's dirty-word summary (one bit per 32-bit bitmap word), so the per-round scans of S
+// (k_count_new, the sparse candidate listing) visit only the words that hold members.
+__device__ __forceinline__ void mark_member(uint32_t* bm, uint32_t* sm, uint32_t id) {
+    atomicOr(bm + (id >> 5), 1u << (id & 31));              // RED.OR
+    atomicOr(sm + (id >> 10), 1u << ((id >> 5) & 31));
+}
+
 template <int G> struct QuantSpec;
 template <> struct QuantSpec<8> { static constexpr uint32_t QT = 2048, CAP = 4095; };
 // G = 16: terms are clamped at 127 so that two of them add inside an 8-bit lane.  Clamping
@@ -209,6 +217,8 @@ struct RFArgs {
     QState* qs_mut;             // the same array: per-query mark counts (pub)
     uint32_t* bitmap;           // [Qb][nwords] current union S (OR-marked, no return)
     int64_t nwords;
+    uint32_t* wsum;             // [Qb][nsw] dirty-word summary of the bitmap rows
+    int64_t nsw;
     float rho2;
     int t, L, K, N_r, mode;
     int pq_cost;                // per-query path cost per 32-point step, relative to 170 per SIMD chunk
@@ -477,7 +487,7 @@ __global__ void __launch_bounds__(RF_THREADS, RF_CTAS) k_range_filter(RFArgs a) 
                     ++c_pp;
                     atomicAdd(&s_pass[g], 1u);
                     const uint32_t id = a.perm[pos];
-                    atomicOr(a.bitmap + (int64_t)s_q[g] * a.nwords + (id >> 5), 1u << (id & 31));  // RED.OR
+                    mark_member(a.bitmap + (int64_t)s_q[g] * a.nwords, a.wsum + (int64_t)s_q[g] * a.nsw, id);
                 }
             }
             qn_ -= cnt;
@@ -584,7 +594,7 @@ __global__ void __launch_bounds__(RF_THREADS, RF_CTAS) k_range_filter(RFArgs a) 
                                 ++c_pp;
                                 atomicAdd(&s_pass[g], 1u);
                                 const uint32_t id = a.perm[pos];
-                                atomicOr(a.bitmap + (int64_t)s_q[g] * a.nwords + (id >> 5), 1u << (id & 31));  // RED.OR
+                                mark_member(a.bitmap + (int64_t)s_q[g] * a.nwords, a.wsum + (int64_t)s_q[g] * a.nsw, id);
                             } else {
                                 band = ok;      // CELL: inside the band; EXACT: every survivor
                             }
@@ -695,7 +705,7 @@ __global__ void __launch_bounds__(RF_THREADS, RF_CTAS) k_range_filter(RFArgs a) 
                         const int g = __ffs(c_) - 1;
                         c_ &= c_ - 1;
                         atomicAdd(&s_pass[g], 1u);
-                        atomicOr(a.bitmap + (int64_t)s_q[g] * a.nwords + (id >> 5), 1u << (id & 31));  // RED.OR
+                        mark_member(a.bitmap + (int64_t)s_q[g] * a.nwords, a.wsum + (int64_t)s_q[g] * a.nsw, id);
                     }
                 }
                 // queue the band pairs (point in tile << 4 | query slot) for the warp-wide fp32 pass:
@@ -765,6 +775,8 @@ struct LPArgs {
     int64_t pos_base;
     uint32_t* bitmap;
     int64_t nwords;
+    uint32_t* wsum;             // [Qb][nsw] dirty-word summary
+    int64_t nsw;
     float rho2, inv_rd;         // inv_rd = 2048/rho^2 rounded down
     int t, L, K, N_r;
     unsigned long long* ctr;
@@ -795,6 +807,7 @@ __global__ void __launch_bounds__(256) k_leaf_points(LPArgs a) {
     const int lane = threadIdx.x & 31;
     const uint32_t* pl = a.plist + (int64_t)q * a.pcap;
     uint32_t* bm = a.bitmap + (int64_t)q * a.nwords;
+    uint32_t* sm = a.wsum + (int64_t)q * a.nsw;
     uint32_t tested = 0, passed = 0;
     // a warp takes LPG listed leaves at a time -- chunks handed out dynamically by a per-query
     // counter to all warps of the query's blocks -- and screens their points packed 32 per step
@@ -862,7 +875,7 @@ __global__ void __launch_bounds__(256) k_leaf_points(LPArgs a) {
             if (pass) {
                 ++passed;
                 const uint32_t id = a.perm[pos];
-                atomicOr(bm + (id >> 5), 1u << (id & 31));   // RED.OR
+                mark_member(bm, sm, id);
             }
         }
     }
@@ -882,10 +895,13 @@ __global__ void __launch_bounds__(256) k_leaf_points(LPArgs a) {
 // One pass over the listed pairs is done: the lists restart empty for the next tree.
 // After tree t: |S| += number of bits set now but not in `prev` (the first-time members of
 // S <- S u S_i, Alg. 5 line 6), and `prev` catches up.  Grid: (active queries) x (word chunks).
-constexpr int CN_WORDS = 4096;
+// Only the words flagged in the row's dirty-word summary can hold members: thread per summary
+// word (32 bitmap words), 256 per block.
+constexpr int CN_SW = 256;
 __global__ void __launch_bounds__(256) k_count_new(const int* __restrict__ act, const int* __restrict__ dna,
                                                    QState* __restrict__ qs, const uint32_t* __restrict__ cur,
-                                                   uint32_t* __restrict__ prev, int64_t nwords, int commit) {
+                                                   uint32_t* __restrict__ prev, int64_t nwords,
+                                                   const uint32_t* __restrict__ wsum, int64_t nsw, int commit) {
     __shared__ unsigned int s_cnt;
     if (dna && (int)blockIdx.x >= *dna) return;
     const int q = act[blockIdx.x];
@@ -895,14 +911,17 @@ __global__ void __launch_bounds__(256) k_count_new(const int* __restrict__ act, 
     __syncthreads();
     const uint32_t* c = cur + (int64_t)q * nwords;
     uint32_t* p = prev + (int64_t)q * nwords;
-    const int64_t w0 = (int64_t)blockIdx.y * CN_WORDS, w1 = min(w0 + CN_WORDS, nwords);
+    const int64_t sw = (int64_t)blockIdx.y * CN_SW + threadIdx.x;
     uint32_t cnt = 0;
-    for (int64_t w = w0 + threadIdx.x; w < w1; w += 256) {
-        const uint32_t cv = c[w], pv = p[w];
-        const uint32_t nb = cv & ~pv;
-        if (nb) {
-            if (commit) p[w] = cv;
-            cnt += __popc(nb);
+    if (sw < nsw) {
+        for (uint32_t dm = wsum[(int64_t)q * nsw + sw]; dm; dm &= dm - 1) {
+            const int64_t w = sw * 32 + (__ffs(dm) - 1);
+            const uint32_t cv = c[w], pv = p[w];
+            const uint32_t nb = cv & ~pv;
+            if (nb) {
+                if (commit) p[w] = cv;
+                cnt += __popc(nb);
+            }
         }
     }
     for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
@@ -1322,14 +1341,10 @@ __global__ void __launch_bounds__(VR_THREADS) k_verify_rows(VRArgs a) {
 //                  scan), and ver catches up with cur.
 //  k_prep_queries  the active queries as a contiguous [na][ld] fp32 block, its TF32 residual
 //                  q - trunc_tf32(q), and ||q||^2.
-template <bool EMIT>
 __global__ void __launch_bounds__(1024) k_verify_prep(const int* __restrict__ act, const QState* __restrict__ qs,
                                                       const uint32_t* __restrict__ cur, uint32_t* __restrict__ ver,
                                                       int64_t nwords, uint32_t* __restrict__ NB,
-                                                      uint32_t* __restrict__ BO, uint32_t* __restrict__ cand,
-                                                      uint32_t* __restrict__ cq) {
-    // EMIT (sparse verification): instead of NB/BO, list the new members directly at their
-    // round-buffer slots (candidate id, active-query index)
+                                                      uint32_t* __restrict__ BO) {
     // nwords is a multiple of 4 (padded bitmap rows): each thread owns 4 consecutive words
     __shared__ uint32_t s_w[32];
     const int a = blockIdx.x;
@@ -1369,29 +1384,46 @@ __global__ void __launch_bounds__(1024) k_verify_prep(const int* __restrict__ ac
         __syncthreads();
         const uint32_t ex = carry + x + (w ? s_w[w - 1] : 0) - cnt;
         if (b < n4) {
-            if (EMIT) {
-                uint32_t slot = ex;
-                const uint32_t wv[4] = {nb.x, nb.y, nb.z, nb.w};
-#pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    uint32_t m_ = wv[i];
-                    const uint32_t base = (uint32_t)((b * 4 + i) * 32);
-                    while (m_) {
-                        const int bit = __ffs(m_) - 1;
-                        m_ &= m_ - 1;
-                        cand[slot] = base + (uint32_t)bit;
-                        cq[slot] = (uint32_t)a;
-                        ++slot;
-                    }
-                }
-            } else {
-                nb_out[b] = nb;
-                bo_out[b] = make_uint4(ex, ex + c0, ex + c0 + c1, ex + c0 + c1 + c2);
-            }
+            nb_out[b] = nb;
+            bo_out[b] = make_uint4(ex, ex + c0, ex + c0 + c1, ex + c0 + c1 + c2);
         }
         carry += s_w[31];
         __syncthreads();
     }
+}
+
+// Sparse verification listing: the new members of S (cur & ~ver) of active query a, found through
+// the row's dirty-word summary (only words that hold members are read), written as (candidate id,
+// active-query index) at the query's round-buffer slots [roff, roff + rcnt) -- their order within
+// the range is free (the top-k ranks by (d2, id)), so a word's run of slots comes from a shared
+// counter; ver catches up with cur.  Block per query.
+__global__ void __launch_bounds__(256) k_verify_list(const int* __restrict__ act, const QState* __restrict__ qs,
+                                                     const uint32_t* __restrict__ cur, uint32_t* __restrict__ ver,
+                                                     int64_t nwords, const uint32_t* __restrict__ wsum, int64_t nsw,
+                                                     uint32_t* __restrict__ cand, uint32_t* __restrict__ cq) {
+    __shared__ uint32_t s_slot;
+    const int a = blockIdx.x;
+    const int q = act[a];
+    if (threadIdx.x == 0) s_slot = (uint32_t)qs[q].roff;
+    __syncthreads();
+    const uint32_t* c = cur + (int64_t)q * nwords;
+    uint32_t* v = ver + (int64_t)q * nwords;
+    const uint32_t* sm = wsum + (int64_t)q * nsw;
+    for (int64_t sw = threadIdx.x; sw < nsw; sw += blockDim.x)
+        for (uint32_t dm = sm[sw]; dm; dm &= dm - 1) {
+            const int64_t wd = sw * 32 + (__ffs(dm) - 1);
+            const uint32_t cv = c[wd];
+            uint32_t nb = cv & ~v[wd];
+            if (!nb) continue;
+            v[wd] = cv;
+            uint32_t slot = atomicAdd(&s_slot, (uint32_t)__popc(nb));
+            const uint32_t base = (uint32_t)(wd * 32);
+            for (; nb; nb &= nb - 1) {
+                cand[slot] = base + (uint32_t)(__ffs(nb) - 1);
+                cq[slot] = (uint32_t)a;
+                ++slot;
+            }
+        }
 }
 
 __global__ void k_prep_queries(const float* __restrict__ Q, int64_t ld, const int* __restrict__ act, int na,
@@ -1479,7 +1511,7 @@ __device__ void bitonic_sort_smem(unsigned long long* a, int n2) {
     }
 }
 
-// ---- sparse verification (low candidate density): k_verify_prep<true> lists the new members
+// ---- sparse verification (low candidate density): k_verify_list lists the new members
 //      of S at their round-buffer slots, then one 8-lane group per candidate gathers its row
 //      with float4 loads (k_verify_gather): per candidate 4d bytes of X, no per-(row block,
 //      query) work.
@@ -1940,6 +1972,8 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
     Scratch s_bm(st, sizeof(uint32_t) * (size_t)(2 * qb * nwords));   // current union + previous
     Scratch s_ctr(st, sizeof(unsigned long long) * (size_t)(4 * qb));
     Scratch s_ver(st, sizeof(uint32_t) * (size_t)(qb * nwords));     // verified members of S
+    const int64_t nsw = round_up(ceil_div(nwords, 32), 4);               // dirty-word summary row
+    Scratch s_sum(st, sizeof(uint32_t) * (size_t)(qb * nsw));
     Scratch s_round(st);                   // (id, d2) of this round's new members, grown on demand
     Scratch s_cq(st);                      // sparse verification: active-query index per slot
     int64_t cq_cap = 0;
@@ -2026,6 +2060,8 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
     ra.qs = s_qs.as<QState>();
     ra.qs_mut = s_qs.as<QState>();
     ra.bitmap = s_bm.as<uint32_t>();
+    ra.wsum = s_sum.as<uint32_t>();
+    ra.nsw = nsw;
     ra.nwords = nwords;
     ra.ctr = s_ctr.as<unsigned long long>();
     uint32_t* bm_prev = s_bm.as<uint32_t>() + qb * nwords;
@@ -2084,8 +2120,8 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
         int* cross = s_lcross.as<int>();
         int* ncross_d = cross + qb;
         DL_CUDA(cudaMemsetAsync(ncross_d, 0, sizeof(int), st));
-        DL_LAUNCH(k_count_new, dim3((unsigned)nf_, (unsigned)ceil_div(nwords, CN_WORDS)), 256, 0, st, fa_, dnf_,
-                  s_qs.as<QState>(), s_bm.as<uint32_t>(), bm_prev, nwords, 0);
+        DL_LAUNCH(k_count_new, dim3((unsigned)nf_, (unsigned)ceil_div(nsw, CN_SW)), 256, 0, st, fa_, dnf_,
+                  s_qs.as<QState>(), s_bm.as<uint32_t>(), bm_prev, nwords, s_sum.as<uint32_t>(), nsw, 0);
         DL_LAUNCH(k_lbo_cross, (unsigned)ceil_div(nf_, 256), 256, 0, st, fa_, nf_, dnf_, s_qs.as<QState>(), budget, cross,
                   ncross_d);
         int ncross = 0;
@@ -2149,6 +2185,7 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
         va.Q = Qb;
         DL_CUDA(cudaMemsetAsync(s_bm.p, 0, sizeof(uint32_t) * (size_t)(2 * qb * nwords), st));
         DL_CUDA(cudaMemsetAsync(s_ver.p, 0, sizeof(uint32_t) * (size_t)(qb * nwords), st));
+        DL_CUDA(cudaMemsetAsync(s_sum.p, 0, sizeof(uint32_t) * (size_t)(qb * nsw), st));
         DL_CUDA(cudaMemsetAsync(s_ctr.p, 0, sizeof(unsigned long long) * (size_t)(4 * qb), st));
         DL_CUDA(cudaMemsetAsync(s_pcnt.p, 0, sizeof(uint32_t) * (size_t)(2 * qb), st));
         tr.mark("batch setup", st);
@@ -2221,6 +2258,8 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
                     lpa.perm = ra.perm;
                     lpa.pos_base = ra.pos_base;
                     lpa.bitmap = s_bm.as<uint32_t>();
+                    lpa.wsum = s_sum.as<uint32_t>();
+                    lpa.nsw = nsw;
                     lpa.nwords = nwords;
                     lpa.rho2 = rho2;
                     lpa.inv_rd = fdiv_rd_host(2048.f, rho2);
@@ -2233,8 +2272,8 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
                 if (a.lb_order) lb_order_tree(t, fa, nf, dnf);
                 DL_LAUNCH(k_count_decide, (unsigned)ceil_div(nf, 256), 256, 0, st, fa, nf, dnf, s_qs.as<QState>(), budget,
                           a.lb_order ? 1 : 0, use_pairs ? ra.pcnt : (uint32_t*)nullptr, lpa.ptake);
-                DL_LAUNCH(k_count_new, dim3((unsigned)nf, (unsigned)ceil_div(nwords, CN_WORDS)), 256, 0, st, fa, dnf,
-                          s_qs.as<QState>(), s_bm.as<uint32_t>(), bm_prev, nwords, 1);
+                DL_LAUNCH(k_count_new, dim3((unsigned)nf, (unsigned)ceil_div(nsw, CN_SW)), 256, 0, st, fa, dnf,
+                          s_qs.as<QState>(), s_bm.as<uint32_t>(), bm_prev, nwords, s_sum.as<uint32_t>(), nsw, 1);
                 if (t + 1 < ix.L) {
                     int* fa2 = (fa == fbuf0) ? fbuf1 : fbuf0;
                     int* dn2 = (fa == fbuf0) ? n_f + 1 : n_f;
@@ -2251,8 +2290,8 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
             // |S| exact for the round's accounting (trees whose count was skipped)
             DL_LAUNCH(k_count_decide, (unsigned)ceil_div(na, 256), 256, 0, st, cur, na, nullptr, s_qs.as<QState>(), budget, 1,
                       (uint32_t*)nullptr, (uint32_t*)nullptr);
-            DL_LAUNCH(k_count_new, dim3((unsigned)na, (unsigned)ceil_div(nwords, CN_WORDS)), 256, 0, st, cur, nullptr,
-                      s_qs.as<QState>(), s_bm.as<uint32_t>(), bm_prev, nwords, 1);
+            DL_LAUNCH(k_count_new, dim3((unsigned)na, (unsigned)ceil_div(nsw, CN_SW)), 256, 0, st, cur, nullptr,
+                      s_qs.as<QState>(), s_bm.as<uint32_t>(), bm_prev, nwords, s_sum.as<uint32_t>(), nsw, 1);
             DL_LAUNCH(k_round_offsets, 1, 1024, 0, st, cur, na, s_qs.as<QState>(), s_total.as<unsigned long long>());
             unsigned long long tot = 0;     // new members of S over the round's queries
             {
@@ -2286,8 +2325,8 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
                 uint32_t* NB = s_boff.as<uint32_t>();
                 uint32_t* BO = NB + (int64_t)qb * nw4;
                 if (path == 1)
-                    DL_LAUNCH(k_verify_prep<false>, (unsigned)na, 1024, 0, st, cur, s_qs.as<QState>(), s_bm.as<uint32_t>(),
-                              s_ver.as<uint32_t>(), nwords, NB, BO, nullptr, nullptr);
+                    DL_LAUNCH(k_verify_prep, (unsigned)na, 1024, 0, st, cur, s_qs.as<QState>(), s_bm.as<uint32_t>(),
+                              s_ver.as<uint32_t>(), nwords, NB, BO);
                 if (path == 1) {
                     float* Qa = s_qa.as<float>();
                     float* Qalo = Qa + (int64_t)qb * ix.ld;
@@ -2302,8 +2341,8 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
                         cq_cap = (int64_t)(tot + tot / 2 + 1024);
                         s_cq.alloc(sizeof(uint32_t) * (size_t)cq_cap);
                     }
-                    DL_LAUNCH(k_verify_prep<true>, (unsigned)na, 1024, 0, st, cur, s_qs.as<QState>(), s_bm.as<uint32_t>(),
-                              s_ver.as<uint32_t>(), nwords, nullptr, nullptr, va.cand, s_cq.as<uint32_t>());
+                    DL_LAUNCH(k_verify_list, (unsigned)na, 256, 0, st, cur, s_qs.as<QState>(), s_bm.as<uint32_t>(),
+                              s_ver.as<uint32_t>(), nwords, s_sum.as<uint32_t>(), nsw, va.cand, s_cq.as<uint32_t>());
                     const unsigned vg = (unsigned)std::min<int64_t>(ceil_div((int64_t)tot * 8, 256), 148 * 32);
                     auto k_verify_gather_sel = ix.ld == 128   ? k_verify_gather<4>
                                                : ix.ld == 256 ? k_verify_gather<8>

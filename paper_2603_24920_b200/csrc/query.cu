@@ -1270,7 +1270,8 @@ __global__ void __launch_bounds__(VR_THREADS) k_verify_rows(VRArgs a) {
         if (lane < a.rbw) {
             const int64_t w = w0 + lane;
             if (w < a.nwords) {
-                uint32_t* vp = a.ver + (int64_t)q * a.nwords + w;                const uint32_t c = a.cur[(int64_t)q * a.nwords + w];
+                uint32_t* vp = a.ver + (int64_t)q * a.nwords + w;
+                const uint32_t c = a.cur[(int64_t)q * a.nwords + w];
                 mw = c & ~*vp;
                 if (mw) *vp = c;
             }

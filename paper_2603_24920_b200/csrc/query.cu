@@ -770,6 +770,9 @@ struct LPArgs {
     const float* lut;           // [Qb][L][K][N_r]
     const uint16_t* q12;        // [Qb][L][K][N_r] 12-bit lower bounds of this round (k_build_qlut, QT 2048)
     const uint32_t* leaf_off;   // global positions
+    const uint8_t* lo;          // [nl_total][K] tight leaf boxes
+    const uint8_t* hi;
+    const uint8_t* sx;          // [Qb][L][K] query region codes
     const uint8_t* tcodes;      // tree t [n][K]
     const uint32_t* perm;       // tree t [n]
     int64_t pos_base;
@@ -802,7 +805,9 @@ __global__ void __launch_bounds__(256) k_leaf_points(LPArgs a) {
         for (int i = threadIdx.x; i < KN / 8; i += blockDim.x) dst[i] = src[i];
     }
     __shared__ unsigned int s_tested, s_passed;
+    __shared__ int s_qx[32];                          // the query's region codes in tree t
     if (threadIdx.x == 0) { s_tested = 0; s_passed = 0; }
+    if (threadIdx.x < K) s_qx[threadIdx.x] = a.sx[((int64_t)q * a.L + a.t) * K + threadIdx.x];
     __syncthreads();
     const int lane = threadIdx.x & 31;
     const uint32_t* pl = a.plist + (int64_t)q * a.pcap;
@@ -822,6 +827,26 @@ __global__ void __launch_bounds__(256) k_leaf_points(LPArgs a) {
             const uint32_t l = pl[e0 + lane];
             my_p0 = a.leaf_off[l];
             my_sz = a.leaf_off[l + 1] - my_p0;
+            // the leaf's box bound in the finer 12-bit table: the filter's 8-bit test passes
+            // boxes up to ~12 % above rho^2; a sum > 2048 proves the box (hence every point of
+            // the leaf) is beyond rho^2 -- the leaf's points are not screened
+            uint32_t lb = 0;
+            if (K == 16) {
+                const uint4 lo4 = *reinterpret_cast<const uint4*>(a.lo + (int64_t)l * 16);
+                const uint4 hi4 = *reinterpret_cast<const uint4*>(a.hi + (int64_t)l * 16);
+#pragma unroll
+                for (int j = 0; j < 16; ++j) {
+                    const int sh = 8 * (j & 3);
+                    const uint32_t wl = (j >> 2) == 0 ? lo4.x : (j >> 2) == 1 ? lo4.y : (j >> 2) == 2 ? lo4.z : lo4.w;
+                    const uint32_t wh = (j >> 2) == 0 ? hi4.x : (j >> 2) == 1 ? hi4.y : (j >> 2) == 2 ? hi4.z : hi4.w;
+                    const int c = min(max(s_qx[j], (int)((wl >> sh) & 255u)), (int)((wh >> sh) & 255u));
+                    lb += s_e[j * N_r + c];
+                }
+            } else {
+                for (int j = 0; j < K; ++j)
+                    lb += s_e[j * N_r + min(max(s_qx[j], (int)a.lo[(int64_t)l * K + j]), (int)a.hi[(int64_t)l * K + j])];
+            }
+            if (lb > 2048u) my_sz = 0;
         }
         uint32_t incl = my_sz;
 #pragma unroll
@@ -2256,6 +2281,9 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
                     lpa.na = nf;
                     lpa.lut = s_lut.as<float>();
                     lpa.tcodes = ra.tcodes;
+                    lpa.lo = ra.lo;
+                    lpa.hi = ra.hi;
+                    lpa.sx = ra.sx;
                     lpa.perm = ra.perm;
                     lpa.pos_base = ra.pos_base;
                     lpa.bitmap = s_bm.as<uint32_t>();

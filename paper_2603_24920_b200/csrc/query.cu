@@ -126,32 +126,42 @@ __global__ void k_build_qlut(const float* __restrict__ lut, const int* __restric
 // ---- per tree: each 16-query group's quantised table interleaved once (entry (j, s) = the
 //      group's 16 8-bit terms), copied by the group's filter CTAs instead of each CTA gathering
 //      16 queries' tables itself.  Inactive slots get the cap (never pass).
-__global__ void k_group_table(const int* __restrict__ act, int na_ub, const int* __restrict__ dna,
-                              const QState* __restrict__ qs, const uint16_t* __restrict__ qlut, int64_t per_q, int t,
-                              int KN, uint32_t cap, const uint8_t* __restrict__ sx, int L, int K, int N_r,
-                              uint4* __restrict__ gtab) {
+__global__ void __launch_bounds__(256) k_group_table(const int* __restrict__ act, int na_ub, const int* __restrict__ dna,
+                                                     const QState* __restrict__ qs, const uint16_t* __restrict__ qlut,
+                                                     int64_t per_q, int t, int KN, uint32_t cap,
+                                                     const uint8_t* __restrict__ sx, int L, int K, int N_r,
+                                                     uint4* __restrict__ gtab) {
+    // block = (16-query group, dim j); thread = region code c (coalesced table reads per query)
+    __shared__ int s_qq[16], s_sv[16];
     const int na = dna ? *dna : na_ub;       // device count (the list is compacted on the device)
-    const int64_t groups = (na + 15) / 16;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < groups * KN;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t grp = i / KN;
-        const int e = (int)(i - grp * KN);
-        const int j = e / N_r, c = e - j * N_r;
+    const int64_t grp = blockIdx.x;
+    const int j = blockIdx.y;
+    if (grp * 16 >= na) return;
+    if (threadIdx.x < 16) {
+        const int64_t gi = grp * 16 + threadIdx.x;
+        int q = -1;
+        if (gi < na) {
+            q = act[gi];
+            if (qs[q].status != ST_ACTIVE) q = -1;
+        }
+        s_qq[threadIdx.x] = q;
+        s_sv[threadIdx.x] = q >= 0 ? (int)sx[((int64_t)q * L + t) * K + j] : 0;
+    }
+    __syncthreads();
+    for (int c = threadIdx.x; c < N_r; c += blockDim.x) {
+        const int64_t e = (int64_t)j * N_r + c;
         uint32_t w[4] = {0, 0, 0, 0};
 #pragma unroll
         for (int g = 0; g < 16; ++g) {
-            const int64_t gi = grp * 16 + g;
+            const int q = s_qq[g];
             uint32_t v = cap;
-            if (gi < na) {
-                const int q = act[gi];
-                if (qs[q].status == ST_ACTIVE) {
-                    v = qlut[(int64_t)q * per_q + (int64_t)t * KN + e];
-                    if ((int)sx[((int64_t)q * L + t) * K + j] < c) v |= 0x80u;     // region flag (k_range_filter)
-                }
+            if (q >= 0) {
+                v = qlut[(int64_t)q * per_q + (int64_t)t * KN + e];
+                if (s_sv[g] < c) v |= 0x80u;     // region flag (k_range_filter)
             }
             w[g >> 2] |= v << (8 * (g & 3));
         }
-        gtab[i] = make_uint4(w[0], w[1], w[2], w[3]);
+        gtab[grp * KN + e] = make_uint4(w[0], w[1], w[2], w[3]);
     }
 }
 
@@ -2264,9 +2274,9 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
                 const int groups = (int)ceil_div(nf, RF_G);
                 if (RF_G == 16) {
                     uint4* gt = s_gtab.as<uint4>();
-                    DL_LAUNCH(k_group_table, (unsigned)std::min<int64_t>(ceil_div((int64_t)groups * ix.K * ix.N_r, 256), 148 * 16),
-                              256, 0, st, fa, nf, dnf, s_qs.as<QState>(), s_qlut.as<uint16_t>(), LK * ix.N_r, t,
-                              ix.K * ix.N_r, (uint32_t)QuantSpec<RF_G>::CAP, s_sx.as<uint8_t>(), ix.L, ix.K, ix.N_r, gt);
+                    DL_LAUNCH(k_group_table, dim3((unsigned)groups, (unsigned)ix.K), 256, 0, st, fa, nf, dnf,
+                              s_qs.as<QState>(), s_qlut.as<uint16_t>(), LK * ix.N_r, t, ix.K * ix.N_r,
+                              (uint32_t)QuantSpec<RF_G>::CAP, s_sx.as<uint8_t>(), ix.L, ix.K, ix.N_r, gt);
                     ra.gtab = gt;
                 }
                 const int64_t ntiles = ra.tile_end - ra.tile_begin;

@@ -113,6 +113,46 @@ __global__ void k_build_tables(const float* __restrict__ Qp, int LK, int N_r, co
     if (s == 0) sx[qr] = (uint8_t)below;
 }
 
+// N_r = 256: the same tables with a warp per (query, coordinate) row, 8 consecutive regions per
+// lane (16-byte / 8-byte stores), the region code from the lanes' counts; 8 rows per block.
+__global__ void __launch_bounds__(256) k_build_tables256(const float* __restrict__ Qp, int64_t nrows, const float* __restrict__ B,
+                                                         int LK, float* __restrict__ lut, uint8_t* __restrict__ sx,
+                                                         float inv_a, float cap_a, uint16_t* __restrict__ qa,
+                                                         float inv_b, float cap_b, uint16_t* __restrict__ qb_) {
+    constexpr int N_r = 256;
+    const int lane = threadIdx.x & 31;
+    const int64_t qr = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);   // q * LK + r
+    if (qr >= nrows) return;
+    const int r = (int)(qr % LK);
+    const float* b = B + (int64_t)r * (N_r + 1);
+    const float x = Qp[qr];
+    float d[8];
+    int below = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        const int s_ = lane * 8 + k;
+        const float l = s_ >= 1 ? b[s_] : -INFINITY;
+        const float u = s_ <= N_r - 2 ? b[s_ + 1] : INFINITY;
+        const float v = fmaxf(0.f, fmaxf(l - x, x - u));
+        d[k] = v * v;
+        below += (s_ >= 1 && b[s_] < x) ? 1 : 0;
+    }
+    const int64_t i = qr * N_r + lane * 8;
+    float4* lo = reinterpret_cast<float4*>(lut + i);
+    lo[0] = make_float4(d[0], d[1], d[2], d[3]);
+    lo[1] = make_float4(d[4], d[5], d[6], d[7]);
+    uint32_t pa[4], pb[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        pa[k] = (uint32_t)quant_term(d[2 * k], inv_a, cap_a) | ((uint32_t)quant_term(d[2 * k + 1], inv_a, cap_a) << 16);
+        pb[k] = (uint32_t)quant_term(d[2 * k], inv_b, cap_b) | ((uint32_t)quant_term(d[2 * k + 1], inv_b, cap_b) << 16);
+    }
+    if (qa) *reinterpret_cast<uint4*>(qa + i) = make_uint4(pa[0], pa[1], pa[2], pa[3]);
+    if (qb_) *reinterpret_cast<uint4*>(qb_ + i) = make_uint4(pb[0], pb[1], pb[2], pb[3]);
+    for (int o = 16; o > 0; o >>= 1) below += __shfl_xor_sync(0xffffffffu, below, o);
+    if (lane == 0) sx[qr] = (uint8_t)below;
+}
+
 // later rounds: block = one active query's (coordinate, region) rows
 __global__ void k_build_qlut(const float* __restrict__ lut, const int* __restrict__ act, int64_t per_q,
                              float inv_rd, float cap, uint16_t* __restrict__ qlut) {
@@ -2239,7 +2279,12 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
                 // finer table: terms <= D 2048/rho^2, cap 4095)
                 const float inv_rd = fdiv_rd_host((float)QuantSpec<RF_G>::QT, rho2);
                 const int64_t per_q = LK * ix.N_r;
-                if (m == 0) {   // every batch query is active: exact, region-code and quantised tables at once
+                if (m == 0 && ix.N_r == 256) {   // every batch query is active: all tables at once
+                    DL_LAUNCH(k_build_tables256, (unsigned)ceil_div((int64_t)nqb * LK, 8), 256, 0, st, Qpb,
+                              (int64_t)nqb * LK, ix.B.as<float>(), (int)LK, s_lut.as<float>(), s_sx.as<uint8_t>(),
+                              inv_rd, (float)QuantSpec<RF_G>::CAP, s_qlut.as<uint16_t>(), fdiv_rd_host(2048.f, rho2),
+                              4095.f, use_pairs ? s_q12.as<uint16_t>() : (uint16_t*)nullptr);
+                } else if (m == 0) {
                     DL_LAUNCH(k_build_tables, dim3((unsigned)LK, (unsigned)nqb), ix.N_r, 0, st, Qpb, (int)LK, ix.N_r,
                               ix.B.as<float>(), s_lut.as<float>(), s_sx.as<uint8_t>(), inv_rd,
                               (float)QuantSpec<RF_G>::CAP, s_qlut.as<uint16_t>(), fdiv_rd_host(2048.f, rho2), 4095.f,

@@ -2267,6 +2267,7 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
         tr.mark("batch setup", st);
         DL_LAUNCH(k_init_batch, (unsigned)ceil_div(nqb, 256), 256, 0, st, s_qs.as<QState>(), act, nqb);
         int na = nqb;
+        bool any_tc = false;           // a round ranked by the tensor-core form ||x||^2 + ||q||^2 - 2 x.q
         int* cur = act;
         int* nxt = act2;
         for (int m = 0; m < max_rounds && na > 0; ++m) {
@@ -2412,6 +2413,7 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
                     DL_LAUNCH(k_verify_prep, (unsigned)na, 1024, 0, st, cur, s_qs.as<QState>(), s_bm.as<uint32_t>(),
                               s_ver.as<uint32_t>(), nwords, NB, BO);
                 if (path == 1) {
+                    any_tc = true;
                     float* Qa = s_qa.as<float>();
                     float* Qalo = Qa + (int64_t)qb * ix.ld;
                     float* qn = Qalo + (int64_t)qb * ix.ld;
@@ -2466,8 +2468,9 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
             std::swap(cur, nxt);
         }
         tr.mark("rounds done", st);
-        DL_LAUNCH(k_rerank_exact, (unsigned)nqb, 256, 0, st, s_qs.as<QState>(), ix.Xp, Qb, (int64_t)ix.ld, k,
-                  s_tk.as<unsigned long long>());
+        if (any_tc)    // gather / row rounds computed the distances directly already
+            DL_LAUNCH(k_rerank_exact, (unsigned)nqb, 256, 0, st, s_qs.as<QState>(), ix.Xp, Qb, (int64_t)ix.ld, k,
+                      s_tk.as<unsigned long long>());
         DL_LAUNCH(k_finalize, (unsigned)std::min<int64_t>(ceil_div((int64_t)nqb * k, 256), 148 * 16), 256, 0, st,
                   s_qs.as<QState>(), s_ctr.as<unsigned long long>(), s_tk.as<unsigned long long>(), nqb, k, ix.id_offset, s_radii.as<double>(),
                   d_ids + q0 * k, d_dists + q0 * k, d_stats ? d_stats + q0 : nullptr, a.null_on_cap ? 1 : 0);

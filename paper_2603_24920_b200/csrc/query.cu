@@ -442,8 +442,10 @@ __global__ void __launch_bounds__(RF_THREADS, RF_CTAS) k_range_filter(RFArgs a) 
                         for (int w = 0; w < 4; ++w) {
                             const uint32_t ml = prmt_sign(dlw[w]);                  // 0xFF: s < lo
                             const uint32_t mh = prmt_sign(dhw[w]);                  // 0xFF: s < hi
-                            const uint32_t th = dhw[w] & ~mh & 0x7F7F7F7Fu;         // D_j[hi] where s >= hi
-                            tw[u][w] = ((dlw[w] & ml) | th) & 0x7F7F7F7Fu;          // + D_j[lo] where s < lo
+                            // D_j[lo] where s < lo (its flag bit cleared), | D_j[hi] where s >= hi
+                            // (flag clear there, so bit 7 is already 0): two 3-input logic ops
+                            const uint32_t tl = dlw[w] & ml & 0x7F7F7F7Fu;
+                            tw[u][w] = tl | (dhw[w] & ~mh);
                         }
                     }
 #pragma unroll

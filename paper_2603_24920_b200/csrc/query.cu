@@ -170,13 +170,14 @@ __global__ void __launch_bounds__(256) k_group_table(const int* __restrict__ act
                                                      const QState* __restrict__ qs, const uint16_t* __restrict__ qlut,
                                                      int64_t per_q, int t, int KN, uint32_t cap,
                                                      const uint8_t* __restrict__ sx, int L, int K, int N_r,
-                                                     uint4* __restrict__ gtab) {
+                                                     uint4* __restrict__ gtab, unsigned int* __restrict__ tctr) {
     // block = (16-query group, dim j); thread = region code c (coalesced table reads per query)
     __shared__ int s_qq[16], s_sv[16];
     const int na = dna ? *dna : na_ub;       // device count (the list is compacted on the device)
     const int64_t grp = blockIdx.x;
     const int j = blockIdx.y;
     if (grp * 16 >= na) return;
+    if (tctr && j == 0 && threadIdx.x == 0) tctr[grp] = 0;   // the filter's tile counter of the group
     if (threadIdx.x < 16) {
         const int64_t gi = grp * 16 + threadIdx.x;
         int q = -1;
@@ -272,6 +273,7 @@ struct RFArgs {
     float rho2;
     int t, L, K, N_r, mode;
     int pq_cost;                // per-query path cost per 32-point step, relative to 170 per SIMD chunk
+    unsigned int* tctr;         // [groups] next tile of each group (zeroed by k_group_table), or null
     int dbg;                    // experiments (DETLSH_RF_DEBUG): 1 = per-query leaf test
     uint32_t* plist;            // CELL, sparse tiles: per-query lists of reachable leaves [Qb][pcap] (or null)
     uint32_t* pcnt;             // [Qb] list lengths
@@ -365,16 +367,17 @@ __global__ void __launch_bounds__(RF_THREADS, RF_CTAS) k_range_filter(RFArgs a) 
     uint32_t* bq = s_bq[warp];
     uint32_t qn_ = 0;                     // queued band pairs (warp-uniform)
 
-    // this CTA's contiguous stripe of tiles; its warps take tiles one at a time (dynamic, so a
-    // warp with heavy tiles does not hold the CTA back)
+    // warps take tiles one at a time, dynamically: from the group's counter shared by all of the
+    // group's CTAs (a.tctr), else from this CTA's contiguous stripe
     const int64_t ntl = a.tile_end - a.tile_begin;
-    const int64_t tb = a.tile_begin + ntl * blockIdx.y / gridDim.y;
-    const int64_t te = a.tile_begin + ntl * (blockIdx.y + 1) / gridDim.y;
+    const int64_t tb = a.tctr ? a.tile_begin : a.tile_begin + ntl * blockIdx.y / gridDim.y;
+    const int64_t te = a.tctr ? a.tile_end : a.tile_begin + ntl * (blockIdx.y + 1) / gridDim.y;
+    unsigned int* next = a.tctr ? a.tctr + blockIdx.x : &s_next;
     if (threadIdx.x == 0) s_next = 0;
     __syncthreads();
     for (;;) {
         int64_t tile = 0;
-        if (lane == 0) tile = tb + atomicAdd(&s_next, 1);
+        if (lane == 0) tile = tb + atomicAdd(next, 1);
         tile = __shfl_sync(0xffffffffu, tile, 0);
         if (tile >= te) break;
         const uint32_t lb = a.tile_leaf[tile], le = a.tile_leaf[tile + 1];
@@ -2085,6 +2088,8 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
     const size_t rf_smem = (size_t)16 * ix.K * ix.N_r;
     Scratch s_qlut(st, sizeof(uint16_t) * (size_t)(qb * LK * ix.N_r));
     Scratch s_gtab(st, (size_t)16 * ceil_div(qb, RF_G) * ix.K * ix.N_r);
+    Scratch s_tctr(st, sizeof(unsigned int) * (size_t)ceil_div(qb, RF_G));
+    static const bool rf_dyn = !std::getenv("DETLSH_RF_STRIPES");   // experiments: per-CTA stripes
     static const int pq_env = std::getenv("DETLSH_FILTER_PQ") ? std::atoi(std::getenv("DETLSH_FILTER_PQ")) : 1;
     auto k_range_filter_sel = (ix.K == 16 && ix.N_r == 256)
                                   ? (pq_env ? k_range_filter<16 COMMA 256 COMMA RF_G COMMA true>
@@ -2093,6 +2098,7 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
     DL_CUDA(cudaFuncSetAttribute(k_range_filter_sel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rf_smem));
     RFArgs ra;
     ra.gtab = nullptr;
+    ra.tctr = nullptr;
     // sparse tiles in CELL mode: (query, leaf) pair lists screened by k_leaf_points
     int64_t pcap = 0;
     for (int t = 0; t < ix.L; ++t) pcap = std::max<int64_t>(pcap, ix.tree_leaf_begin[t + 1] - ix.tree_leaf_begin[t]);
@@ -2324,12 +2330,16 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
                     uint4* gt = s_gtab.as<uint4>();
                     DL_LAUNCH(k_group_table, dim3((unsigned)groups, (unsigned)ix.K), 256, 0, st, fa, nf, dnf,
                               s_qs.as<QState>(), s_qlut.as<uint16_t>(), LK * ix.N_r, t, ix.K * ix.N_r,
-                              (uint32_t)QuantSpec<RF_G>::CAP, s_sx.as<uint8_t>(), ix.L, ix.K, ix.N_r, gt);
+                              (uint32_t)QuantSpec<RF_G>::CAP, s_sx.as<uint8_t>(), ix.L, ix.K, ix.N_r, gt,
+                              rf_dyn ? s_tctr.as<unsigned int>() : (unsigned int*)nullptr);
                     ra.gtab = gt;
+                    ra.tctr = rf_dyn ? s_tctr.as<unsigned int>() : nullptr;
                 }
                 const int64_t ntiles = ra.tile_end - ra.tile_begin;
-                // about `rf_waves` waves of RF_CTAS resident CTAs per SM in all (default 3; 2-4 measured within 1 %)
-                static const int rf_waves = std::getenv("DETLSH_RF_WAVES") ? std::atoi(std::getenv("DETLSH_RF_WAVES")) : 3;
+                // about `rf_waves` waves of RF_CTAS resident CTAs per SM in all (tiles from a per-group
+                // counter: 1 wave; else per-CTA stripes: 3 waves, 2-4 measured within 1 %)
+                static const int rf_waves = std::getenv("DETLSH_RF_WAVES") ? std::atoi(std::getenv("DETLSH_RF_WAVES"))
+                                                                           : (rf_dyn ? 1 : 3);
                 const int stripes = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(ntiles, RF_THREADS / 32),
                                                                                  (148 * RF_CTAS * rf_waves + groups / 2) / groups));
                 DL_LAUNCH(k_range_filter_sel, dim3((unsigned)groups, (unsigned)stripes), RF_THREADS, rf_smem, st, ra);

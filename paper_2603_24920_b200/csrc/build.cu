@@ -902,6 +902,51 @@ __global__ void k_leaf_tight(const uint32_t* __restrict__ leaf_off, int64_t nl, 
     }
 }
 
+// Sub-boxes: each leaf's points cut into runs of kSubBox consecutive points (leaf order); per
+// run the min/max code per dim.  A valid lower bound for every member, tighter than the leaf's
+// (a few points span less of each dim): the pair kernel screens runs before their points.
+__global__ void k_sb_count(const uint32_t* __restrict__ leaf_off, int64_t nl, uint32_t* __restrict__ cnt) {
+    for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < nl; l += (int64_t)gridDim.x * blockDim.x)
+        cnt[l] = (leaf_off[l + 1] - leaf_off[l] + kSubBox - 1) / kSubBox;
+}
+
+// thread per sub-box (its leaf by binary search over sb_off); consecutive threads read
+// consecutive runs of points
+__global__ void k_sb_boxes(const uint32_t* __restrict__ leaf_off, const uint32_t* __restrict__ sb_off, int64_t nl, int K,
+                           const uint8_t* __restrict__ tcodes, uint8_t* __restrict__ lo, uint8_t* __restrict__ hi) {
+    const uint32_t nsb = sb_off[nl];
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nsb; i += (int64_t)gridDim.x * blockDim.x) {
+        int64_t a_ = 0, b_ = nl - 1;                  // last leaf l with sb_off[l] <= i
+        while (a_ < b_) {
+            const int64_t m = (a_ + b_ + 1) >> 1;
+            if (sb_off[m] <= (uint32_t)i) a_ = m; else b_ = m - 1;
+        }
+        const uint32_t p0 = leaf_off[a_] + (uint32_t)(i - sb_off[a_]) * kSubBox;
+        const uint32_t e = min(p0 + (uint32_t)kSubBox, leaf_off[a_ + 1]);
+        if (K == 16) {
+            uint4 mn = make_uint4(~0u, ~0u, ~0u, ~0u), mx = make_uint4(0, 0, 0, 0);
+            for (uint32_t p = p0; p < e; ++p) {
+                const uint4 c = *reinterpret_cast<const uint4*>(tcodes + (int64_t)p * 16);
+                mn = make_uint4(__vminu4(mn.x, c.x), __vminu4(mn.y, c.y), __vminu4(mn.z, c.z), __vminu4(mn.w, c.w));
+                mx = make_uint4(__vmaxu4(mx.x, c.x), __vmaxu4(mx.y, c.y), __vmaxu4(mx.z, c.z), __vmaxu4(mx.w, c.w));
+            }
+            *reinterpret_cast<uint4*>(lo + i * 16) = mn;
+            *reinterpret_cast<uint4*>(hi + i * 16) = mx;
+        } else {
+            for (int j = 0; j < K; ++j) {
+                int mn = 255, mx = 0;
+                for (uint32_t p = p0; p < e; ++p) {
+                    const int c = tcodes[(int64_t)p * K + j];
+                    mn = min(mn, c);
+                    mx = max(mx, c);
+                }
+                lo[i * K + j] = (uint8_t)mn;
+                hi[i * K + j] = (uint8_t)mx;
+            }
+        }
+    }
+}
+
 // Box of each query tile: per dim the smallest lo and largest hi over its leaves (the union's
 // bounding box, so its lower bound never exceeds a member leaf's -- the filter skips whole tiles).
 __global__ void k_tile_boxes(const uint32_t* __restrict__ tile_leaf, int64_t ntiles, int K, const uint8_t* __restrict__ lo,
@@ -1250,9 +1295,26 @@ static bool build_trees_try(Index& ix, const uint8_t* d_EP, int64_t leaf_factor,
     return true;
 }
 
+void build_subboxes(Index& ix, cudaStream_t st) {
+    const int64_t nl = ix.nl_total();
+    if (nl <= 0) return;
+    ix.sb_off.alloc(sizeof(uint32_t) * (size_t)(nl + 1), st);
+    Scratch s_cnt(st, sizeof(uint32_t) * (size_t)(nl + 1));
+    DL_LAUNCH(k_sb_count, grid_for(nl, 256), 256, 0, st, ix.leaf_off.as<uint32_t>(), nl, s_cnt.as<uint32_t>());
+    exclusive_scan_u32(s_cnt.as<uint32_t>(), ix.sb_off.as<uint32_t>(), nl, ix.sb_off.as<uint32_t>() + nl, st);
+    const int64_t nsb_ub = (int64_t)ix.n * ix.L / kSubBox + nl;   // each leaf adds at most one partial run
+    ix.sb_lo.alloc((size_t)nsb_ub * ix.K, st);
+    ix.sb_hi.alloc((size_t)nsb_ub * ix.K, st);
+    DL_LAUNCH(k_sb_boxes, grid_for(nsb_ub, 256), 256, 0, st, ix.leaf_off.as<uint32_t>(), ix.sb_off.as<uint32_t>(), nl,
+              ix.K, ix.tcodes.as<uint8_t>(), ix.sb_lo.as<uint8_t>(), ix.sb_hi.as<uint8_t>());
+}
+
 static void build_trees(Index& ix, const uint8_t* d_EP, cudaStream_t st) {
     for (int64_t f = 4;; f *= 4) {
-        if (build_trees_try(ix, d_EP, f, st)) return;
+        if (build_trees_try(ix, d_EP, f, st)) {
+            build_subboxes(ix, st);
+            return;
+        }
         DL_REQUIRE(f < (int64_t)1 << 40, "tree build: leaf list overflow");
     }
 }

@@ -34,6 +34,7 @@ struct DevBuf {
 };
 
 constexpr int kTileLeaves = 32;     // leaves per query tile (one warp of the range filter)
+constexpr int kSubBox = 8;          // points per leaf sub-box (consecutive in leaf order)
 
 struct Index {
     // shape / parameters
@@ -65,6 +66,8 @@ struct Index {
     DevBuf point_tile_leaf; // [L*n] u16: leaf of each point (tree order) within its tile (< 32)
     DevBuf leaf_tlo, leaf_thi;  // [nl_total][K] u8 tight box: min/max code of the leaf's points
     DevBuf tile_lo, tile_hi;// [ntiles][K] u8 bounding box of each tile's tight leaf boxes
+    DevBuf sb_off;          // [nl_total+1] u32 first sub-box of each leaf (sub-box = kSubBox consecutive points)
+    DevBuf sb_lo, sb_hi;    // [nsb][K] u8 tight box of each sub-box (the pair kernel's second-level bound)
     DevBuf xnorm;           // [n] fp32 ||x||^2 of every row (tensor-core verification, verify_tc.cu)
     bool keep_proj = false; // build option: keep the projections (EXACT mode)
     DevBuf proj;            // [n][LK] fp32 projections p' in data order (EXACT mode only)
@@ -76,6 +79,8 @@ struct Index {
 void build_index(Index& ix, const float* d_data, int64_t data_ld, const float* bp_given,
                  double sample_frac, int proj_impl, cudaStream_t st);
 void build_trees_from_codes(Index& ix, const uint8_t* d_codes, cudaStream_t st);
+// Sub-box tight boxes of every leaf (derived from tcodes + leaf_off; also rebuilt on load).
+void build_subboxes(Index& ix, cudaStream_t st);
 void build_index_hash_only(Index& ix, cudaStream_t st);
 void gather_rows_strided(const float* d_src, int64_t src_ld, int d, const uint32_t* d_ids, int64_t m, float* d_dst,
                          int64_t dst_ld, cudaStream_t st);

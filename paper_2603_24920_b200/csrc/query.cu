@@ -827,6 +827,9 @@ struct LPArgs {
     const uint32_t* leaf_off;   // global positions
     const uint8_t* lo;          // [nl_total][K] tight leaf boxes
     const uint8_t* hi;
+    const uint32_t* sb_off;     // [nl_total+1] first sub-box of each leaf (null: no sub-box level)
+    const uint8_t* sb_lo;       // [nsb][K] sub-box tight boxes
+    const uint8_t* sb_hi;
     const uint8_t* sx;          // [Qb][L][K] query region codes
     const uint8_t* tcodes;      // tree t [n][K]
     const uint32_t* perm;       // tree t [n]
@@ -872,6 +875,57 @@ __global__ void __launch_bounds__(256) k_leaf_points(LPArgs a) {
     // a warp takes LPG listed leaves at a time -- chunks handed out dynamically by a per-query
     // counter to all warps of the query's blocks -- and screens their points packed 32 per step
     // (the owning leaf of packed point i found by a log2(LPG)-step search over the chunk's prefix)
+    // per warp: queued sub-boxes (first point position, point count) that passed their bound
+    __shared__ uint32_t s_sqf[8][64];
+    __shared__ uint8_t s_sqc[8][64];
+    uint32_t* sq_first = s_sqf[threadIdx.x >> 5];
+    uint8_t* sq_cnt = s_sqc[threadIdx.x >> 5];
+    uint32_t sqn = 0;                                // warp-uniform
+    // screen the points of the last nb queued sub-boxes: lane = (sub-box lane / kSubBox, point)
+    auto sb_points = [&](uint32_t nb) {
+        const uint32_t sbs = lane / kSubBox, k = lane % kSubBox;
+        if (sbs < nb) {
+            const uint32_t e = sqn - nb + sbs;
+            if (k < sq_cnt[e]) {
+                const uint32_t pos = sq_first[e] + k - (uint32_t)a.pos_base;
+                uint32_t acc = 0;
+                uint4 c4 = make_uint4(0, 0, 0, 0);
+                if (K == 16) {
+                    c4 = *reinterpret_cast<const uint4*>(a.tcodes + (int64_t)pos * 16);
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) {
+                        const uint32_t w = (j >> 2) == 0 ? c4.x : (j >> 2) == 1 ? c4.y : (j >> 2) == 2 ? c4.z : c4.w;
+                        acc += s_e[j * N_r + ((w >> (8 * (j & 3))) & 255u)];
+                    }
+                } else {
+                    for (int j = 0; j < K; ++j) acc += s_e[j * N_r + a.tcodes[(int64_t)pos * K + j]];
+                }
+                ++tested;
+                if (acc <= 2048u) {                          // else: proves cellLB > rho^2
+                    bool pass = acc + 17u <= 2048u;          // proves cellLB < rho^2 (1 - 1e-5)
+                    if (!pass) {
+                        float s_ = 0.f;
+                        if (K == 16) {
+#pragma unroll
+                            for (int j = 0; j < 16; ++j) {
+                                const uint32_t w = (j >> 2) == 0 ? c4.x : (j >> 2) == 1 ? c4.y : (j >> 2) == 2 ? c4.z : c4.w;
+                                s_ += __ldg(s_d + j * N_r + ((w >> (8 * (j & 3))) & 255u));
+                            }
+                        } else {
+                            for (int j = 0; j < K; ++j) s_ += __ldg(s_d + j * N_r + a.tcodes[(int64_t)pos * K + j]);
+                        }
+                        pass = s_ <= a.rho2;
+                    }
+                    if (pass) {
+                        ++passed;
+                        mark_member(bm, sm, a.perm[pos]);
+                    }
+                }
+            }
+        }
+        sqn -= nb;
+        __syncwarp();
+    };
     for (;;) {
         uint32_t ck = 0;
         if (lane == 0) ck = atomicAdd(a.ptake + q, 1u);
@@ -902,6 +956,73 @@ __global__ void __launch_bounds__(256) k_leaf_points(LPArgs a) {
                     lb += s_e[j * N_r + min(max(s_qx[j], (int)a.lo[(int64_t)l * K + j]), (int)a.hi[(int64_t)l * K + j])];
             }
             if (lb > 2048u) my_sz = 0;
+        }
+        if (a.sb_off) {
+            // second level: the leaves' sub-boxes (kSubBox consecutive points each), packed 32 per
+            // step; each sub-box whose 12-bit bound is <= 2048 is queued, and 32 / kSubBox queued
+            // sub-boxes' points are screened per step (lane = (sub-box, point))
+            const uint32_t my_nsb = (my_sz + kSubBox - 1) / kSubBox;
+            uint32_t my_sb0 = 0;
+            if (lane < LPG && my_sz) my_sb0 = a.sb_off[pl[e0 + lane]];
+            uint32_t incl = my_nsb;
+#pragma unroll
+            for (int o = 1; o < LPG; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            const uint32_t excl = incl - my_nsb;
+            const uint32_t TS = __shfl_sync(0xffffffffu, incl, LPG - 1);
+            const uint32_t my_end = my_p0 + my_sz;
+            for (uint32_t c0 = 0; c0 < TS; c0 += 32) {
+                const uint32_t i = c0 + lane;
+                int o_ = 0;                               // last leaf slot with excl <= i
+#pragma unroll
+                for (int st = LPG / 2; st > 0; st >>= 1) {
+                    const uint32_t ex = __shfl_sync(0xffffffffu, excl, o_ + st);
+                    if (ex <= i) o_ += st;
+                }
+                const uint32_t sb0 = __shfl_sync(0xffffffffu, my_sb0, o_);
+                const uint32_t pp0 = __shfl_sync(0xffffffffu, my_p0, o_);
+                const uint32_t pend = __shfl_sync(0xffffffffu, my_end, o_);
+                const uint32_t pex = __shfl_sync(0xffffffffu, excl, o_);
+                bool pass = false;
+                uint32_t first = 0, cnt = 0;
+                if (i < TS) {
+                    const uint32_t sbi = sb0 + (i - pex);
+                    first = pp0 + (i - pex) * kSubBox;
+                    cnt = min((uint32_t)kSubBox, pend - first);
+                    uint32_t lb = 0;
+                    if (K == 16) {
+                        const uint4 lo4 = *reinterpret_cast<const uint4*>(a.sb_lo + (int64_t)sbi * 16);
+                        const uint4 hi4 = *reinterpret_cast<const uint4*>(a.sb_hi + (int64_t)sbi * 16);
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) {
+                            const int sh = 8 * (j & 3);
+                            const uint32_t wl = (j >> 2) == 0 ? lo4.x : (j >> 2) == 1 ? lo4.y : (j >> 2) == 2 ? lo4.z : lo4.w;
+                            const uint32_t wh = (j >> 2) == 0 ? hi4.x : (j >> 2) == 1 ? hi4.y : (j >> 2) == 2 ? hi4.z : hi4.w;
+                            const int c = min(max(s_qx[j], (int)((wl >> sh) & 255u)), (int)((wh >> sh) & 255u));
+                            lb += s_e[j * N_r + c];
+                        }
+                    } else {
+                        for (int j = 0; j < K; ++j)
+                            lb += s_e[j * N_r + min(max(s_qx[j], (int)a.sb_lo[(int64_t)sbi * K + j]),
+                                                    (int)a.sb_hi[(int64_t)sbi * K + j])];
+                    }
+                    pass = lb <= 2048u;
+                }
+                const uint32_t bal = __ballot_sync(0xffffffffu, pass);
+                if (pass) {
+                    const uint32_t slot = sqn + __popc(bal & lanemask_lt());
+                    sq_first[slot] = first;
+                    sq_cnt[slot] = (uint8_t)cnt;
+                }
+                sqn += __popc(bal);
+                __syncwarp();
+                while (sqn >= 32 / kSubBox) {
+                    sb_points(32 / kSubBox);
+                }
+            }
+            continue;
         }
         uint32_t incl = my_sz;
 #pragma unroll
@@ -959,6 +1080,7 @@ __global__ void __launch_bounds__(256) k_leaf_points(LPArgs a) {
             }
         }
     }
+    if (sqn) sb_points(sqn);
     for (int o = 16; o > 0; o >>= 1) {
         tested += __shfl_xor_sync(0xffffffffu, tested, o);
         passed += __shfl_xor_sync(0xffffffffu, passed, o);
@@ -2351,6 +2473,10 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
                     lpa.tcodes = ra.tcodes;
                     lpa.lo = ra.lo;
                     lpa.hi = ra.hi;
+                    static const bool no_sb = std::getenv("DETLSH_NO_SUBBOX") != nullptr;   // experiments
+                    lpa.sb_off = (ix.sb_off.p && !no_sb) ? ix.sb_off.as<uint32_t>() : nullptr;
+                    lpa.sb_lo = ix.sb_lo.as<uint8_t>();
+                    lpa.sb_hi = ix.sb_hi.as<uint8_t>();
                     lpa.sx = ra.sx;
                     lpa.perm = ra.perm;
                     lpa.pos_base = ra.pos_base;

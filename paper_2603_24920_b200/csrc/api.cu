@@ -31,6 +31,8 @@ void project_rows(const Index& ix, const float* d_X, int64_t ld, int64_t m, floa
     project_rows_simt(ix, d_X, ld, m, d_P, d_nonfinite, st);
 }
 
+std::atomic<int64_t> g_index_bytes{0};
+
 cudaMemPool_t index_pool() {
     static cudaMemPool_t pools[64] = {};
     int dev = 0;

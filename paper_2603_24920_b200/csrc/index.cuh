@@ -1,6 +1,7 @@
 // index.cuh -- device layout of a DET-LSH index.
 #pragma once
 
+#include <atomic>
 #include <vector>
 
 #include "common.cuh"
@@ -10,6 +11,9 @@ namespace detlsh {
 // Pool for index-owned (long-lived) buffers, separate from the default pool that serves
 // per-call scratch, so the two lifetimes do not fragment each other (api.cu).
 cudaMemPool_t index_pool();
+// Bytes held by live index buffers (all devices), kept by DevBuf (the query batch budget
+// subtracts what indexes built after its free-memory snapshot hold, api.cu/query.cu).
+extern std::atomic<int64_t> g_index_bytes;
 
 // Index-owned device memory, stream-ordered from index_pool() (no device-wide sync on
 // allocate/free); freed on the legacy default stream.
@@ -24,9 +28,11 @@ struct DevBuf {
         reset();
         if (b) DL_CUDA(cudaMallocFromPoolAsync(&p, b, index_pool(), st));
         bytes = b;
+        g_index_bytes += (int64_t)b;
     }
     void reset() {
         if (p) cudaFreeAsync(p, 0);
+        g_index_bytes -= (int64_t)bytes;
         p = nullptr;
         bytes = 0;
     }

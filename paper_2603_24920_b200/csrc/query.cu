@@ -1604,10 +1604,10 @@ __global__ void __launch_bounds__(256) k_verify_list(const int* __restrict__ act
                                                      const uint32_t* __restrict__ cur, uint32_t* __restrict__ ver,
                                                      int64_t nwords, const uint32_t* __restrict__ wsum, int64_t nsw,
                                                      uint32_t* __restrict__ cand, uint32_t* __restrict__ cq) {
-    __shared__ uint32_t s_slot;
+    __shared__ unsigned long long s_slot;             // 64-bit slots: a round may hold >= 2^32 pairs
     const int a = blockIdx.x;
     const int q = act[a];
-    if (threadIdx.x == 0) s_slot = (uint32_t)qs[q].roff;
+    if (threadIdx.x == 0) s_slot = (unsigned long long)qs[q].roff;
     __syncthreads();
     const uint32_t* c = cur + (int64_t)q * nwords;
     uint32_t* v = ver + (int64_t)q * nwords;
@@ -1619,7 +1619,7 @@ __global__ void __launch_bounds__(256) k_verify_list(const int* __restrict__ act
             uint32_t nb = cv & ~v[wd];
             if (!nb) continue;
             v[wd] = cv;
-            uint32_t slot = atomicAdd(&s_slot, (uint32_t)__popc(nb));
+            unsigned long long slot = atomicAdd(&s_slot, (unsigned long long)__popc(nb));
             const uint32_t base = (uint32_t)(wd * 32);
             for (; nb; nb &= nb - 1) {
                 cand[slot] = base + (uint32_t)(__ffs(nb) - 1);
@@ -2022,17 +2022,21 @@ __global__ void k_init_batch(QState* __restrict__ qs, int* __restrict__ act, int
 }
 
 int64_t auto_query_budget() {
+    // free memory sampled once per device, corrected by the index bytes allocated (or freed)
+    // since the sample -- a large index built after the first query shrinks the batch
     static std::mutex mu;
-    static int64_t cached[64] = {};
+    static int64_t free0[64] = {}, index0[64] = {};
     int dev = 0;
     DL_CUDA(cudaGetDevice(&dev));
     std::lock_guard<std::mutex> lk(mu);
-    if (!cached[dev]) {
+    if (!free0[dev]) {
         size_t fr = 0, tot = 0;
         DL_CUDA(cudaMemGetInfo(&fr, &tot));
-        cached[dev] = std::max<int64_t>(1, (int64_t)(fr * 0.6));
+        free0[dev] = std::max<int64_t>(1, (int64_t)fr);
+        index0[dev] = g_index_bytes.load();
     }
-    return cached[dev];
+    const int64_t fr = free0[dev] - (g_index_bytes.load() - index0[dev]);
+    return std::max<int64_t>(1, (int64_t)(0.6 * (double)fr));
 }
 
 // 2048 / rho2 rounded toward zero (a lower bound of the exact scale factor).
@@ -2167,9 +2171,9 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
         budget_bytes = auto_query_budget();
     }
     int64_t qb = a.query_batch > 0 ? a.query_batch : std::max<int64_t>(1, budget_bytes / per_q);
-    // round-buffer slots are 32-bit (verify offsets): a query adds at most n new members per
-    // round, so a batch of qb queries needs qb * n < 2^32
-    qb = std::min<int64_t>({qb, nq, 65535, std::max<int64_t>(1, (int64_t)0xFFFFFFFFll / n)});
+    // round-buffer slots are 64-bit on the sparse path; the tensor-core and row paths keep
+    // 32-bit offsets and are used only for rounds with < 2^32 new pairs (below)
+    qb = std::min<int64_t>({qb, nq, 65535});
     DL_REQUIRE(qb >= 1, "not enough device memory for one query");
 
     Scratch s_bm(st, sizeof(uint32_t) * (size_t)(2 * qb * nwords));   // current union + previous
@@ -2538,12 +2542,14 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
             bool done_tc = false;
             // 0 = row kernel (verify_impl 1), 1 = tensor cores, 2 = sparse gather
             int path = a.verify_impl == 3 ? 2 : tc_ok ? 1 : 0;
-            if (tc_ok && a.verify_impl == 0) {
+            const bool wide = tot >= 0xFFFFFFFFull;    // 32-bit offsets of the TC / row paths overflow
+            if (tc_ok && a.verify_impl == 0 && !wide) {
                 const double scale = (double)n / 1e6 * (double)ix.ld / 256.0;
                 const double t_tc = 2.5 * scale * (double)round_up(na, 16) / 1000.0;
                 const double t_gather = 0.05 * (double)n / 1e6 + (double)tot * ix.ld * 4.0 / 5e9;   // ms at 5 TB/s
                 path = t_tc <= t_gather ? 1 : 2;
             }
+            if (wide) path = 2;
             if (path >= 1) {
                 uint32_t* NB = s_boff.as<uint32_t>();
                 uint32_t* BO = NB + (int64_t)qb * nw4;

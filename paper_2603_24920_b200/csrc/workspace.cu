@@ -28,6 +28,10 @@ std::map<std::pair<int, cudaStream_t>, Arena*> g_arenas;
 thread_local Arena* t_ws = nullptr;
 
 constexpr size_t kAlign = 256;
+// Arenas are kept mapped only up to this size: a call that needs more (very large query
+// batches) takes its scratch stream-ordered from the default pool instead, which returns it
+// after the call, so a huge arena never starves later index builds.
+constexpr size_t kArenaMax = (size_t)16 << 30;
 inline size_t align_up(size_t b) { return (b + kAlign - 1) / kAlign * kAlign; }
 
 }  // namespace
@@ -74,7 +78,7 @@ WorkspaceScope::~WorkspaceScope() {
     if (!owner) return;
     Arena* a = static_cast<Arena*>(impl);
     t_ws = nullptr;
-    if (a->need > a->cap) {
+    if (a->need > a->cap && a->need <= kArenaMax) {
         // regrow to the call's high-water mark (+25%); in-flight work may still use the old block
         cudaStreamSynchronize(a->st);
         if (a->base) cudaFree(a->base);

@@ -135,15 +135,16 @@ def kernel_models(c, steps: int, st, n_local: int, nq: int, ld: int):
     d, LK, K = c.d, c.L * c.K, c.K
     ns = datagen_ns(c, n_local)
     ncand = float(st["n_cand"].sum())
-    filt = float((st["leaves_tested"] * 2 * K + st["leaves_passed"] * 8 + st["points_tested"] * K
-                  + st["points_passed"] * 12 + st["n_cand"] * 4).sum())
-    lookups = float((st["points_tested"] * K + st["leaves_tested"] * K).sum())
+    filt = float((st["leaves_tested"] * 2 * K + st["leaves_passed"] * 8 + st["subboxes_tested"] * 2 * K
+                  + st["points_tested"] * K + st["points_passed"] * 12 + st["n_cand"] * 4).sum())
+    lookups = float((st["points_tested"] * K + st["leaves_tested"] * K + st["subboxes_tested"] * K).sum())
     proj_bytes = n_local * (4 * ld + LK) + (ns + nq) * (4 * ld + 4 * LK)
     proj_flops = 2.0 * 2 * (n_local + ns + nq) * ((LK + 15) // 16 * 16) * ld      # x_hi and x_lo MMAs
     return {
         FILTER_UNIT: {"bytes": steps * filt, "smem_bytes": steps * lookups * 2,
-                      "unit": "per query: leaves_tested*2K + leaves_passed*8 + points_tested*K + "
-                              "points_passed*12 + new*4 B (SURVEY 8(d) K5/K6), over both filter kernels "
+                      "unit": "per query: leaves_tested*2K + leaves_passed*8 + subboxes_tested*2K + "
+                              "points_tested*K + points_passed*12 + new*4 B (SURVEY 8(d) K5/K6, with the "
+                              "sub-box boxes the pair kernel reads), over both filter kernels "
                               "(k_range_filter: tile/leaf bounds + dense tiles; k_leaf_points: sparse tiles' "
                               "points), timed together"},
         "k_verify_rows": {"bytes": steps * ncand * (4 * d + 8), "unit": "per candidate 4d+8 B (row + id + d2)"},
@@ -434,7 +435,8 @@ def main():
             "candidates_per_query": float(st["n_cand"].mean()),
             "stop_reasons": np.bincount(st["reason"], minlength=3).tolist(),
             "filter_counts_per_query": {k_: float(st[k_].mean()) for k_ in
-                                        ("leaves_tested", "leaves_passed", "points_tested", "points_passed")},
+                                        ("leaves_tested", "leaves_passed", "points_tested", "points_passed",
+                                         "subboxes_tested")},
             "roofline": roof,
             "rooflines": roofs,
             "e2e": {"value": cfg.nq / (float(te.item()) / 1e3), "unit": "queries/s",

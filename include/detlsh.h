@@ -85,6 +85,7 @@ typedef struct {
     int64_t leaves_passed;   /* leaves with LB <= eps r */
     int64_t points_tested;   /* points of qualifying leaves examined */
     int64_t points_passed;   /* points with cell LB <= eps r (before de-duplication) */
+    int64_t subboxes_tested; /* sub-box (runs of 8 leaf points) lower bounds evaluated by the pair kernel */
 } detlsh_query_stats;
 
 void detlsh_default_opts(detlsh_opts* opts);

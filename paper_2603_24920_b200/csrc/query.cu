@@ -236,6 +236,8 @@ __device__ __forceinline__ void mark_member(uint32_t* bm, uint32_t* sm, uint32_t
     atomicOr(sm + (id >> 10), 1u << ((id >> 5) & 31));
 }
 
+constexpr int NCTR = 5;          // per-query filter counters: leaves tested/passed, points tested/passed, sub-boxes tested
+
 template <int G> struct QuantSpec;
 template <> struct QuantSpec<8> { static constexpr uint32_t QT = 2048, CAP = 4095; };
 // G = 16: terms are clamped at 127 so that two of them add inside an 8-bit lane.  Clamping
@@ -798,7 +800,7 @@ __global__ void __launch_bounds__(RF_THREADS, RF_CTAS) k_range_filter(RFArgs a) 
     }
     __syncthreads();
     if (threadIdx.x < G && s_q[threadIdx.x] >= 0) {
-        unsigned long long* c = a.ctr + (int64_t)s_q[threadIdx.x] * 4;
+        unsigned long long* c = a.ctr + (int64_t)s_q[threadIdx.x] * NCTR;
         for (int i = 0; i < 4; ++i) atomicAdd(c + i, (unsigned long long)s_ctr[threadIdx.x][i]);
         if (s_pass[threadIdx.x])
             atomicAdd(reinterpret_cast<unsigned long long*>(&a.qs_mut[s_q[threadIdx.x]].pub),
@@ -862,16 +864,16 @@ __global__ void __launch_bounds__(256) k_leaf_points(LPArgs a) {
         uint4* dst = reinterpret_cast<uint4*>(s_e);
         for (int i = threadIdx.x; i < KN / 8; i += blockDim.x) dst[i] = src[i];
     }
-    __shared__ unsigned int s_tested, s_passed;
+    __shared__ unsigned int s_tested, s_passed, s_sbt;
     __shared__ int s_qx[32];                          // the query's region codes in tree t
-    if (threadIdx.x == 0) { s_tested = 0; s_passed = 0; }
+    if (threadIdx.x == 0) { s_tested = 0; s_passed = 0; s_sbt = 0; }
     if (threadIdx.x < K) s_qx[threadIdx.x] = a.sx[((int64_t)q * a.L + a.t) * K + threadIdx.x];
     __syncthreads();
     const int lane = threadIdx.x & 31;
     const uint32_t* pl = a.plist + (int64_t)q * a.pcap;
     uint32_t* bm = a.bitmap + (int64_t)q * a.nwords;
     uint32_t* sm = a.wsum + (int64_t)q * a.nsw;
-    uint32_t tested = 0, passed = 0;
+    uint32_t tested = 0, passed = 0, sbt = 0;
     // a warp takes LPG listed leaves at a time -- chunks handed out dynamically by a per-query
     // counter to all warps of the query's blocks -- and screens their points packed 32 per step
     // (the owning leaf of packed point i found by a log2(LPG)-step search over the chunk's prefix)
@@ -1009,6 +1011,7 @@ __global__ void __launch_bounds__(256) k_leaf_points(LPArgs a) {
                                                     (int)a.sb_hi[(int64_t)sbi * K + j])];
                     }
                     pass = lb <= 2048u;
+                    ++sbt;
                 }
                 const uint32_t bal = __ballot_sync(0xffffffffu, pass);
                 if (pass) {
@@ -1084,13 +1087,15 @@ __global__ void __launch_bounds__(256) k_leaf_points(LPArgs a) {
     for (int o = 16; o > 0; o >>= 1) {
         tested += __shfl_xor_sync(0xffffffffu, tested, o);
         passed += __shfl_xor_sync(0xffffffffu, passed, o);
+        sbt += __shfl_xor_sync(0xffffffffu, sbt, o);
     }
-    if (lane == 0) { atomicAdd(&s_tested, tested); atomicAdd(&s_passed, passed); }
+    if (lane == 0) { atomicAdd(&s_tested, tested); atomicAdd(&s_passed, passed); if (sbt) atomicAdd(&s_sbt, sbt); }
     __syncthreads();
     if (threadIdx.x == 0) {
         if (s_passed) atomicAdd(reinterpret_cast<unsigned long long*>(&a.qs_mut[q].pub), (unsigned long long)s_passed);
-        atomicAdd(a.ctr + (int64_t)q * 4 + 2, (unsigned long long)s_tested);
-        atomicAdd(a.ctr + (int64_t)q * 4 + 3, (unsigned long long)s_passed);
+        atomicAdd(a.ctr + (int64_t)q * NCTR + 2, (unsigned long long)s_tested);
+        atomicAdd(a.ctr + (int64_t)q * NCTR + 3, (unsigned long long)s_passed);
+        if (s_sbt) atomicAdd(a.ctr + (int64_t)q * NCTR + 4, (unsigned long long)s_sbt);
     }
 }
 
@@ -2002,10 +2007,11 @@ __global__ void k_finalize(const QState* __restrict__ qs, const unsigned long lo
             o.pad = 0;
             o.n_cand = s.cnt;
             o.r_final = radii[max(0, s.rounds - 1)];
-            o.leaves_tested = (int64_t)ctr[q * 4 + 0];
-            o.leaves_passed = (int64_t)ctr[q * 4 + 1];
-            o.points_tested = (int64_t)ctr[q * 4 + 2];
-            o.points_passed = (int64_t)ctr[q * 4 + 3];
+            o.leaves_tested = (int64_t)ctr[q * NCTR + 0];
+            o.leaves_passed = (int64_t)ctr[q * NCTR + 1];
+            o.points_tested = (int64_t)ctr[q * NCTR + 2];
+            o.points_passed = (int64_t)ctr[q * NCTR + 3];
+            o.subboxes_tested = (int64_t)ctr[q * NCTR + 4];
             stats[q] = o;
         }
     }
@@ -2177,7 +2183,7 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
     DL_REQUIRE(qb >= 1, "not enough device memory for one query");
 
     Scratch s_bm(st, sizeof(uint32_t) * (size_t)(2 * qb * nwords));   // current union + previous
-    Scratch s_ctr(st, sizeof(unsigned long long) * (size_t)(4 * qb));
+    Scratch s_ctr(st, sizeof(unsigned long long) * (size_t)(NCTR * qb));
     Scratch s_ver(st, sizeof(uint32_t) * (size_t)(qb * nwords));     // verified members of S
     const int64_t nsw = round_up(ceil_div(nwords, 32), 4);               // dirty-word summary row
     Scratch s_sum(st, sizeof(uint32_t) * (size_t)(qb * nsw));
@@ -2396,7 +2402,7 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
         DL_CUDA(cudaMemsetAsync(s_bm.p, 0, sizeof(uint32_t) * (size_t)(2 * qb * nwords), st));
         DL_CUDA(cudaMemsetAsync(s_ver.p, 0, sizeof(uint32_t) * (size_t)(qb * nwords), st));
         DL_CUDA(cudaMemsetAsync(s_sum.p, 0, sizeof(uint32_t) * (size_t)(qb * nsw), st));
-        DL_CUDA(cudaMemsetAsync(s_ctr.p, 0, sizeof(unsigned long long) * (size_t)(4 * qb), st));
+        DL_CUDA(cudaMemsetAsync(s_ctr.p, 0, sizeof(unsigned long long) * (size_t)(NCTR * qb), st));
         DL_CUDA(cudaMemsetAsync(s_pcnt.p, 0, sizeof(uint32_t) * (size_t)(2 * qb), st));
         tr.mark("batch setup", st);
         DL_LAUNCH(k_init_batch, (unsigned)ceil_div(nqb, 256), 256, 0, st, s_qs.as<QState>(), act, nqb);

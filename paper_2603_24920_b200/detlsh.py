@@ -44,13 +44,13 @@ class detlsh_query_stats(C.Structure):
     _fields_ = [("rounds", C.c_int32), ("trees_last", C.c_int32), ("reason", C.c_int32),
                 ("pad", C.c_int32), ("n_cand", C.c_int64), ("r_final", C.c_double),
                 ("leaves_tested", C.c_int64), ("leaves_passed", C.c_int64), ("points_tested", C.c_int64),
-                ("points_passed", C.c_int64)]
+                ("points_passed", C.c_int64), ("subboxes_tested", C.c_int64)]
 
 
 STATS_DTYPE = np.dtype([("rounds", np.int32), ("trees_last", np.int32), ("reason", np.int32),
                         ("pad", np.int32), ("n_cand", np.int64), ("r_final", np.float64),
                         ("leaves_tested", np.int64), ("leaves_passed", np.int64), ("points_tested", np.int64),
-                        ("points_passed", np.int64)])
+                        ("points_passed", np.int64), ("subboxes_tested", np.int64)])
 
 _lib = None
 

@@ -973,18 +973,29 @@ __global__ void k_tile_write(const uint32_t* __restrict__ flags, const uint32_t*
 }
 
 // Per point (tree order): index of its leaf within its query tile (< kTileLeaves).
+// warp per tile: lane l holds the start of the tile's leaf l; each point's leaf slot by a
+// 5-step shuffle search, written coalesced
 __global__ void k_point_tile_leaf(const uint32_t* __restrict__ leaf_off, const uint32_t* __restrict__ tile_leaf,
                                   int64_t ntiles, int64_t nl, uint16_t* __restrict__ ptl) {
-    for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < nl;
-         l += (int64_t)gridDim.x * blockDim.x) {
-        int64_t lo = 0, hi = ntiles - 1;    // last tile with tile_leaf <= l
-        while (lo < hi) {
-            const int64_t mid = (lo + hi + 1) >> 1;
-            if (tile_leaf[mid] <= (uint32_t)l) lo = mid; else hi = mid - 1;
+    const int lane = threadIdx.x & 31;
+    for (int64_t t = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; t < ntiles;
+         t += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const uint32_t lb = tile_leaf[t], le = tile_leaf[t + 1];
+        const int nlt = (int)(le - lb);
+        const uint32_t start = lane < nlt ? leaf_off[lb + lane] : 0xFFFFFFFFu;
+        const uint32_t P0 = leaf_off[lb], P1 = leaf_off[le];
+        for (uint32_t b = P0; b < P1; b += 32) {      // warp-uniform (shuffles below)
+            const uint32_t p = b + lane;
+            int o_ = 0;                               // last leaf slot with start <= p
+#pragma unroll
+            for (int sd = 16; sd > 0; sd >>= 1) {
+                const uint32_t ex = __shfl_sync(0xffffffffu, start, o_ + sd);
+                if (ex <= p) o_ += sd;
+            }
+            if (p < P1) ptl[p] = (uint16_t)o_;
         }
-        const uint16_t v = (uint16_t)(l - tile_leaf[lo]);
-        for (uint32_t p = leaf_off[l]; p < leaf_off[l + 1]; ++p) ptl[p] = v;
     }
+    (void)nl;
 }
 
 __global__ void k_tree_tiles(const uint32_t* __restrict__ idx, const unsigned long long* __restrict__ leaf_begin,
@@ -1284,7 +1295,7 @@ static bool build_trees_try(Index& ix, const uint8_t* d_EP, int64_t leaf_factor,
         DL_LAUNCH(k_tile_boxes, grid_for(ntiles * K, 256), 256, 0, st, ix.tile_leaf.as<uint32_t>(), ntiles, K,
                   ix.leaf_tlo.as<uint8_t>(), ix.leaf_thi.as<uint8_t>(), ix.tile_lo.as<uint8_t>(), ix.tile_hi.as<uint8_t>());
         ix.point_tile_leaf.alloc(sizeof(uint16_t) * (size_t)total, st);
-        DL_LAUNCH(k_point_tile_leaf, grid_for(nl, 256), 256, 0, st, ix.leaf_off.as<uint32_t>(), ix.tile_leaf.as<uint32_t>(),
+        DL_LAUNCH(k_point_tile_leaf, grid_for(ntiles * 32, 256), 256, 0, st, ix.leaf_off.as<uint32_t>(), ix.tile_leaf.as<uint32_t>(),
                   ntiles, nl, ix.point_tile_leaf.as<uint16_t>());
         std::vector<unsigned long long> tb(L + 1);
         DL_CUDA(cudaMemcpyAsync(tb.data(), s_tb.p, sizeof(unsigned long long) * (L + 1), cudaMemcpyDeviceToHost, st));

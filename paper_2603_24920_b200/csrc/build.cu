@@ -854,54 +854,6 @@ __global__ void k_tile_flags(const uint32_t* __restrict__ leaf_off, int64_t nl, 
     }
 }
 
-// Tight box of each leaf: per dim the smallest and largest code of the leaf's points (contained
-// in the leaf's prefix box, so its lower bound is a tighter valid bound for every member --
-// the range filter prunes with it; the prefix box stays the leaf's box where the method uses it).
-__global__ void k_leaf_tight(const uint32_t* __restrict__ leaf_off, int64_t nl, int K, const uint8_t* __restrict__ tcodes,
-                             uint8_t* __restrict__ tlo, uint8_t* __restrict__ thi) {
-    if (K == 16) {    // 4 lanes per leaf: 16-byte code rows, byte-wise min/max, 2-step shuffle reduction
-        const int sub = threadIdx.x & 3;
-        for (int64_t l = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 2; (l & ~(int64_t)7) < nl;
-             l += ((int64_t)gridDim.x * blockDim.x) >> 2) {   // warp-uniform condition (8 leaves per warp)
-            const bool live = l < nl;            // whole warps stay in the loop for the shuffles
-            uint4 mn = make_uint4(~0u, ~0u, ~0u, ~0u), mx = make_uint4(0, 0, 0, 0);
-            if (live)
-                for (uint32_t p = leaf_off[l] + sub; p < leaf_off[l + 1]; p += 4) {
-                    const uint4 c = *reinterpret_cast<const uint4*>(tcodes + (int64_t)p * 16);
-                    mn = make_uint4(__vminu4(mn.x, c.x), __vminu4(mn.y, c.y), __vminu4(mn.z, c.z), __vminu4(mn.w, c.w));
-                    mx = make_uint4(__vmaxu4(mx.x, c.x), __vmaxu4(mx.y, c.y), __vmaxu4(mx.z, c.z), __vmaxu4(mx.w, c.w));
-                }
-            for (int o = 1; o < 4; o <<= 1) {
-                mn.x = __vminu4(mn.x, __shfl_xor_sync(0xffffffffu, mn.x, o));
-                mn.y = __vminu4(mn.y, __shfl_xor_sync(0xffffffffu, mn.y, o));
-                mn.z = __vminu4(mn.z, __shfl_xor_sync(0xffffffffu, mn.z, o));
-                mn.w = __vminu4(mn.w, __shfl_xor_sync(0xffffffffu, mn.w, o));
-                mx.x = __vmaxu4(mx.x, __shfl_xor_sync(0xffffffffu, mx.x, o));
-                mx.y = __vmaxu4(mx.y, __shfl_xor_sync(0xffffffffu, mx.y, o));
-                mx.z = __vmaxu4(mx.z, __shfl_xor_sync(0xffffffffu, mx.z, o));
-                mx.w = __vmaxu4(mx.w, __shfl_xor_sync(0xffffffffu, mx.w, o));
-            }
-            if (live && sub == 0) {
-                *reinterpret_cast<uint4*>(tlo + l * 16) = mn;
-                *reinterpret_cast<uint4*>(thi + l * 16) = mx;
-            }
-        }
-        return;
-    }
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nl * K; i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t l = i / K;
-        const int j = (int)(i - l * K);
-        int a = 255, b = 0;
-        for (uint32_t p = leaf_off[l]; p < leaf_off[l + 1]; ++p) {
-            const int c = tcodes[(int64_t)p * K + j];
-            a = min(a, c);
-            b = max(b, c);
-        }
-        tlo[i] = (uint8_t)a;
-        thi[i] = (uint8_t)b;
-    }
-}
-
 // Sub-boxes: each leaf's points cut into runs of kSubBox consecutive points (leaf order); per
 // run the min/max code per dim.  A valid lower bound for every member, tighter than the leaf's
 // (a few points span less of each dim): the pair kernel screens runs before their points.
@@ -942,6 +894,35 @@ __global__ void k_sb_boxes(const uint32_t* __restrict__ leaf_off, const uint32_t
                 }
                 lo[i * K + j] = (uint8_t)mn;
                 hi[i * K + j] = (uint8_t)mx;
+            }
+        }
+    }
+}
+
+// Tight box of each leaf as the union of its sub-boxes' boxes (same min/max over the same points).
+__global__ void k_leaf_tight_sb(const uint32_t* __restrict__ sb_off, int64_t nl, int K, const uint8_t* __restrict__ slo,
+                                const uint8_t* __restrict__ shi, uint8_t* __restrict__ tlo, uint8_t* __restrict__ thi) {
+    for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < nl; l += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t a = sb_off[l], e = sb_off[l + 1];
+        if (K == 16) {
+            uint4 mn = make_uint4(~0u, ~0u, ~0u, ~0u), mx = make_uint4(0, 0, 0, 0);
+            for (uint32_t b = a; b < e; ++b) {
+                const uint4 x = *reinterpret_cast<const uint4*>(slo + (int64_t)b * 16);
+                const uint4 y = *reinterpret_cast<const uint4*>(shi + (int64_t)b * 16);
+                mn = make_uint4(__vminu4(mn.x, x.x), __vminu4(mn.y, x.y), __vminu4(mn.z, x.z), __vminu4(mn.w, x.w));
+                mx = make_uint4(__vmaxu4(mx.x, y.x), __vmaxu4(mx.y, y.y), __vmaxu4(mx.z, y.z), __vmaxu4(mx.w, y.w));
+            }
+            *reinterpret_cast<uint4*>(tlo + l * 16) = mn;
+            *reinterpret_cast<uint4*>(thi + l * 16) = mx;
+        } else {
+            for (int j = 0; j < K; ++j) {
+                int mn = 255, mx = 0;
+                for (uint32_t b = a; b < e; ++b) {
+                    mn = min(mn, (int)slo[(int64_t)b * K + j]);
+                    mx = max(mx, (int)shi[(int64_t)b * K + j]);
+                }
+                tlo[l * K + j] = (uint8_t)mn;
+                thi[l * K + j] = (uint8_t)mx;
             }
         }
     }
@@ -1262,11 +1243,11 @@ static bool build_trees_try(Index& ix, const uint8_t* d_EP, int64_t leaf_factor,
     DL_CUDA(cudaMemcpyAsync(begin.data(), s_begin.p, sizeof(unsigned long long) * (L + 1), cudaMemcpyDeviceToHost, st));
     ix.tcodes.alloc((size_t)total * K, st);
     DL_LAUNCH(k_gather_tcodes, grid_for(total, 256), 256, 0, st, perm, d_EP, n, (int)L, K, ix.tcodes.as<uint8_t>());
+    build_subboxes(ix, nl, st);
     ix.leaf_tlo.alloc((size_t)nl * K, st);
     ix.leaf_thi.alloc((size_t)nl * K, st);
-    DL_LAUNCH(k_leaf_tight, grid_for(K == 16 ? nl * 4 : nl * K, 256), 256, 0, st, ix.leaf_off.as<uint32_t>(), nl, K,
-              ix.tcodes.as<uint8_t>(),
-              ix.leaf_tlo.as<uint8_t>(), ix.leaf_thi.as<uint8_t>());
+    DL_LAUNCH(k_leaf_tight_sb, grid_for(nl, 256), 256, 0, st, ix.sb_off.as<uint32_t>(), nl, K, ix.sb_lo.as<uint8_t>(),
+              ix.sb_hi.as<uint8_t>(), ix.leaf_tlo.as<uint8_t>(), ix.leaf_thi.as<uint8_t>());
     DL_CUDA(cudaStreamSynchronize(st));
     ix.tree_leaf_begin.assign(begin.begin(), begin.end());
     ix.tree_leaf_begin[L] = nl;
@@ -1306,8 +1287,7 @@ static bool build_trees_try(Index& ix, const uint8_t* d_EP, int64_t leaf_factor,
     return true;
 }
 
-void build_subboxes(Index& ix, cudaStream_t st) {
-    const int64_t nl = ix.nl_total();
+void build_subboxes(Index& ix, int64_t nl, cudaStream_t st) {
     if (nl <= 0) return;
     ix.sb_off.alloc(sizeof(uint32_t) * (size_t)(nl + 1), st);
     Scratch s_cnt(st, sizeof(uint32_t) * (size_t)(nl + 1));
@@ -1322,10 +1302,7 @@ void build_subboxes(Index& ix, cudaStream_t st) {
 
 static void build_trees(Index& ix, const uint8_t* d_EP, cudaStream_t st) {
     for (int64_t f = 4;; f *= 4) {
-        if (build_trees_try(ix, d_EP, f, st)) {
-            build_subboxes(ix, st);
-            return;
-        }
+        if (build_trees_try(ix, d_EP, f, st)) return;
         DL_REQUIRE(f < (int64_t)1 << 40, "tree build: leaf list overflow");
     }
 }

@@ -142,7 +142,7 @@ Index* load_index(const char* path) {
     get_dev(fh.f, ix->tile_hi, (size_t)nt * h.K);
     get_dev(fh.f, ix->leaf_tlo, (size_t)nl * h.K);
     get_dev(fh.f, ix->leaf_thi, (size_t)nl * h.K);
-    build_subboxes(*ix, 0);                            // derived from tcodes + leaf_off (not stored)
+    build_subboxes(*ix, nl, 0);                        // derived from tcodes + leaf_off (not stored)
     DL_CUDA(cudaDeviceSynchronize());
     return ix.release();
 }

@@ -135,16 +135,19 @@ def kernel_models(c, steps: int, st, n_local: int, nq: int, ld: int):
     d, LK, K = c.d, c.L * c.K, c.K
     ns = datagen_ns(c, n_local)
     ncand = float(st["n_cand"].sum())
-    filt = float((st["leaves_tested"] * 2 * K + st["leaves_passed"] * 8 + st["subboxes_tested"] * 2 * K
+    # leaf boxes are read once per 16-query group and tree ("leaf-box bytes /
+    # query-batch"); everything else per query
+    filt = float((st["leaves_tested"] * 2 * K / 16 + st["leaves_passed"] * 8 + st["subboxes_tested"] * 2 * K
                   + st["points_tested"] * K + st["points_passed"] * 12 + st["n_cand"] * 4).sum())
     lookups = float((st["points_tested"] * K + st["leaves_tested"] * K + st["subboxes_tested"] * K).sum())
     proj_bytes = n_local * (4 * ld + LK) + (ns + nq) * (4 * ld + 4 * LK)
     proj_flops = 2.0 * 2 * (n_local + ns + nq) * ((LK + 15) // 16 * 16) * ld      # x_hi and x_lo MMAs
     return {
         FILTER_UNIT: {"bytes": steps * filt, "smem_bytes": steps * lookups * 2,
-                      "unit": "per query: leaves_tested*2K + leaves_passed*8 + subboxes_tested*2K + "
-                              "points_tested*K + points_passed*12 + new*4 B (SURVEY 8(d) K5/K6, with the "
-                              "sub-box boxes the pair kernel reads), over both filter kernels "
+                      "unit": "per query: leaves_tested*2K/16 (leaf boxes read once per 16-query group, "
+                              "SURVEY 8(d) K5) + leaves_passed*8 + subboxes_tested*2K + points_tested*K + "
+                              "points_passed*12 + new*4 B (K6, with the sub-box boxes the pair kernel "
+                              "reads), over both filter kernels "
                               "(k_range_filter: tile/leaf bounds + dense tiles; k_leaf_points: sparse tiles' "
                               "points), timed together"},
         "k_verify_rows": {"bytes": steps * ncand * (4 * d + 8), "unit": "per candidate 4d+8 B (row + id + d2)"},
@@ -223,6 +226,15 @@ def load_traffic():
     if not os.path.exists(path):
         return None
     return {k: v["dram_bytes_per_launch"] for k, v in json.load(open(path)).get("kernels", {}).items()}
+
+
+def load_pipes():
+    """ncu ALU-pipe and issue utilisation (% of peak) per kernel, from the same capture."""
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    if not os.path.exists(path):
+        return {}
+    return {k: {"alu_pct": v.get("alu_pct"), "issue_pct": v.get("issue_pct")}
+            for k, v in json.load(open(path)).get("kernels", {}).items() if v.get("alu_pct") is not None}
 
 
 def datagen_ns(c, n):
@@ -414,6 +426,11 @@ def main():
                     e = roofline_entry(kname, model, ms, hbm, bf16, clocks, nl_, traffic)
                     if kname == FILTER_UNIT:
                         e["parts_ms"] = filter_parts
+                        pipes = load_pipes()
+                        e["limiter"] = ("ALU / instruction issue, not HBM: per the committed ncu capture "
+                                        "(profiles/traffic.json) the filter kernels' ALU-pipe and issue "
+                                        "utilisation are given in ncu_pipes; their DRAM traffic is small")
+                        e["ncu_pipes"] = {k: v for k, v in pipes.items() if k.startswith(FILTER_KERNELS)}
                     roofs.append(e)
                     break
         roof = next((r for r in roofs if r["kernel"] == dom), None)

@@ -286,6 +286,7 @@ struct RFArgs {
 template <int KT, int NRT, int G, bool PQ>
 __global__ void __launch_bounds__(RF_THREADS, RF_CTAS) k_range_filter(RFArgs a) {
     constexpr uint32_t QT = QuantSpec<G>::QT, CAP = QuantSpec<G>::CAP;
+    constexpr bool SIMD_LEAF = KT == 16 && G == 16;   // leaf bounds of all 16 queries per lane
     extern __shared__ __align__(16) unsigned char smem[];
     const int K = KT ? KT : a.K;
     const int N_r = NRT ? NRT : a.N_r;
@@ -390,7 +391,12 @@ __global__ void __launch_bounds__(RF_THREADS, RF_CTAS) k_range_filter(RFArgs a) 
         uint32_t tm;
         {
             bool pass = false;
-            if (lane < G && ((amask >> lane) & 1)) {
+            if (SIMD_LEAF && !(a.dbg & 1) && lane < G) {
+                // the 16-query leaf test below costs the same whatever subset reached the tile,
+                // and the group's 16 queries reach ~every tile between them: the tile screen
+                // would only add work (every leaf bound is computed for every active query)
+                pass = (amask >> lane) & 1;
+            } else if (lane < G && ((amask >> lane) & 1)) {
                 uint32_t acc = 0;
                 if (KT == 16) {
                     const uint4 tl4 = *reinterpret_cast<const uint4*>(a.tile_lo + tile * 16);

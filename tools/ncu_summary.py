@@ -87,9 +87,15 @@ def full(rep, out):
         if name and "dram__bytes_read.sum" in e:
             t = traffic.setdefault(name, {"launches": [], "dram_bytes_per_launch": 0})
             t["launches"].append({"ms": e.get("gpu__time_duration.sum"),
-                                  "dram_bytes": e["dram__bytes_read.sum"] + e.get("dram__bytes_write.sum", 0)})
+                                  "dram_bytes": e["dram__bytes_read.sum"] + e.get("dram__bytes_write.sum", 0),
+                                  "alu_pct": e.get("sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active"),
+                                  "issue_pct": e.get("smsp__issue_active.avg.pct_of_peak_sustained_active")})
     for name, t in traffic.items():
         t["dram_bytes_per_launch"] = round(sum(x["dram_bytes"] for x in t["launches"]) / len(t["launches"]))
+        for key in ("alu_pct", "issue_pct"):
+            vals = [x[key] for x in t["launches"] if x.get(key) is not None]
+            if vals:
+                t[key] = round(sum(vals) / len(vals), 1)
     json.dump({"launches": res}, open(out, "w"), indent=1)
     return traffic
 

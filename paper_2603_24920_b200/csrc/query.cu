@@ -851,10 +851,12 @@ struct LPArgs {
     unsigned long long* ctr;
 };
 
+constexpr int LP_THREADS = 256;     // threads per pair-kernel block (512 with half the blocks: slower)
+
 // KT, NRT > 0: K and N_r fixed at compile time (table rows at immediate offsets, a static table);
 // LPG listed leaves per warp chunk
 template <int KT, int NRT, int LPG>
-__global__ void __launch_bounds__(256) k_leaf_points(LPArgs a) {
+__global__ void __launch_bounds__(LP_THREADS) k_leaf_points(LPArgs a) {
     extern __shared__ __align__(16) unsigned char lp_smem[];
     __shared__ __align__(16) uint16_t lp_static[(KT > 0 && NRT > 0) ? KT * NRT : 8];
     const int ai = blockIdx.x;
@@ -884,8 +886,8 @@ __global__ void __launch_bounds__(256) k_leaf_points(LPArgs a) {
     // counter to all warps of the query's blocks -- and screens their points packed 32 per step
     // (the owning leaf of packed point i found by a log2(LPG)-step search over the chunk's prefix)
     // per warp: queued sub-boxes (first point position, point count) that passed their bound
-    __shared__ uint32_t s_sqf[8][64];
-    __shared__ uint8_t s_sqc[8][64];
+    __shared__ uint32_t s_sqf[LP_THREADS / 32][64];
+    __shared__ uint8_t s_sqc[LP_THREADS / 32][64];
     uint32_t* sq_first = s_sqf[threadIdx.x >> 5];
     uint8_t* sq_cnt = s_sqc[threadIdx.x >> 5];
     uint32_t sqn = 0;                                // warp-uniform
@@ -2506,7 +2508,7 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
                     lpa.ctr = s_ctr.as<unsigned long long>();
                     lpa.q12 = s_q12.as<uint16_t>();
                     static const int lp_y = std::getenv("DETLSH_LP_Y") ? std::atoi(std::getenv("DETLSH_LP_Y")) : 16;
-                    DL_LAUNCH(k_leaf_points_sel, dim3((unsigned)nf, (unsigned)lp_y), 256, lp_dyn, st, lpa);
+                    DL_LAUNCH(k_leaf_points_sel, dim3((unsigned)nf, (unsigned)lp_y), LP_THREADS, lp_dyn, st, lpa);
                 }
                 if (a.lb_order) lb_order_tree(t, fa, nf, dnf);
                 DL_LAUNCH(k_count_decide, (unsigned)ceil_div(nf, 256), 256, 0, st, fa, nf, dnf, s_qs.as<QState>(), budget,

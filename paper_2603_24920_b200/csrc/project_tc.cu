@@ -30,8 +30,9 @@ using namespace tc;
 
 constexpr int TC_M = 128;           // rows per tile (UMMA M)
 constexpr int TC_KB = 32;           // fp32 per k-block (= 128 B, one swizzle row)
-constexpr int TC_THREADS = 448;    // 14 warps: producer, MMA, 4 converters (2-3, 12-13), 8 epilogue (4-11)
-constexpr int TC_CONV = 128;       // converter threads
+constexpr int TC_THREADS = 576;    // 18 warps: producer, MMA, 8 converters (2-3, 12-17), 8 epilogue (4-11)
+constexpr int TC_CONV = 256;       // converter threads
+constexpr int TC_CM = TC_M * TC_KB / 4 / TC_CONV;   // float4 per converter thread per stage
 constexpr int TC_EPI = 256;        // epilogue threads
 constexpr int TC_STAGE_BYTES = TC_M * TC_KB * 4;   // 16 KB
 
@@ -154,23 +155,23 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             }
         }
     } else if (warp < 4 || warp >= 12) {
-        // converters (128 threads): lo = x - trunc_tf32(x), same swizzled offsets.  Thread t sees
-        // float4 t + 128 m (m < 8) of every stage, i.e. rows t/8 + 16 m (swizzling permutes 16-byte
-        // chunks only within a row), so it also accumulates those rows' ||x||^2 (xnorm != null).
+        // converters (TC_CONV threads): lo = x - trunc_tf32(x), same swizzled offsets.  Thread t sees
+        // float4 t + TC_CONV m (m < TC_CM) of every stage, i.e. rows t/8 + (TC_CONV/8) m (swizzling
+        // permutes 16-byte chunks only within a row), so it also accumulates those rows' ||x||^2.
         const int t = warp < 4 ? threadIdx.x - 64 : threadIdx.x - 384 + 64;
         int s = 0;
         uint32_t ph = 0;
         bool bad = false;
         for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-            float nacc[8];
+            float nacc[TC_CM];
 #pragma unroll
-            for (int m = 0; m < 8; ++m) nacc[m] = 0.f;
+            for (int m = 0; m < TC_CM; ++m) nacc[m] = 0.f;
             for (int kb = 0; kb < sh.nkb; ++kb) {
                 mbar_wait(&full[s], ph);
                 const float4* src = reinterpret_cast<const float4*>(sX + (size_t)s * TC_STAGE_BYTES);
                 float4* dst = reinterpret_cast<float4*>(sL + (size_t)s * TC_STAGE_BYTES);
 #pragma unroll
-                for (int m = 0; m < ((sh.dbg & 2) ? 0 : 8); ++m) {
+                for (int m = 0; m < ((sh.dbg & 2) ? 0 : TC_CM); ++m) {
                     const int i = t + TC_CONV * m;
                     const float4 x = src[i];
                     float4 lo;
@@ -188,12 +189,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             }
             if (xnorm) {
 #pragma unroll
-                for (int m = 0; m < 8; ++m) {
+                for (int m = 0; m < TC_CM; ++m) {
                     float v = nacc[m];
                     v += __shfl_xor_sync(0xffffffffu, v, 1);
                     v += __shfl_xor_sync(0xffffffffu, v, 2);
                     v += __shfl_xor_sync(0xffffffffu, v, 4);
-                    const int64_t row = tile * TC_M + (t >> 3) + 16 * m;
+                    const int64_t row = tile * TC_M + (t >> 3) + (TC_CONV / 8) * m;
                     if ((t & 7) == 0 && row < sh.m) xnorm[row] = v;
                 }
             }

@@ -1374,6 +1374,90 @@ __global__ void k_tree_end_compact(const int* __restrict__ act, int na_ub, const
     if (threadIdx.x == 0) *n_out = s_n;
 }
 
+// After tree t, everything per query in one launch (block = query of the tree's list): the lazy
+// count decision (k_count_decide), the bitmap diff over the summary-flagged words when needed
+// (k_count_new), the pair-list reset and the budget test (k_tree_end); the last block to finish
+// (ticket counter) then compacts the still-active queries for the next tree (k_tree_end_compact).
+// act_out == null: no compaction (last tree).  Not for lb_order (its counts are tentative).
+__global__ void __launch_bounds__(256) k_tree_post(const int* __restrict__ act, int na_ub, const int* __restrict__ dna,
+                                                   QState* __restrict__ qs, const uint32_t* __restrict__ cur,
+                                                   uint32_t* __restrict__ prev, int64_t nwords,
+                                                   const uint32_t* __restrict__ wsum, int64_t nsw, int64_t budget,
+                                                   int force, uint32_t* __restrict__ pcnt, uint32_t* __restrict__ ptake,
+                                                   int t, int round, int64_t cap, unsigned int* __restrict__ ticket,
+                                                   int* __restrict__ act_out, int* __restrict__ n_out) {
+    __shared__ unsigned int s_cnt, s_last;
+    __shared__ int s_doc;
+    const int na = dna ? *dna : na_ub;
+    const int a = blockIdx.x;
+    if (a < na) {
+        const int q = act[a];
+        QState* s = &qs[q];
+        if (threadIdx.x == 0) {
+            if (pcnt) { pcnt[q] = 0; ptake[q] = 0; }
+            const int d = (s->status == ST_ACTIVE && s->pub > 0 && (force || s->cnt + s->pub >= budget)) ? 1 : 0;
+            s_doc = d;
+            s_cnt = 0;
+            if (d) s->pub = 0;
+        }
+        __syncthreads();
+        if (s_doc) {
+            const uint32_t* c = cur + (int64_t)q * nwords;
+            uint32_t* pv = prev + (int64_t)q * nwords;
+            uint32_t cnt = 0;
+            for (int64_t sw = threadIdx.x; sw < nsw; sw += blockDim.x)
+                for (uint32_t dm = wsum[(int64_t)q * nsw + sw]; dm; dm &= dm - 1) {
+                    const int64_t w = sw * 32 + (__ffs(dm) - 1);
+                    const uint32_t cv = c[w], pw = pv[w];
+                    const uint32_t nb = cv & ~pw;
+                    if (nb) {
+                        pv[w] = cv;
+                        cnt += __popc(nb);
+                    }
+                }
+            for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+            if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(&s_cnt, cnt);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            if (s_cnt) s->cnt += s_cnt;
+            tree_end_one(s, t, round, budget, cap);
+        }
+    }
+    if (!act_out) return;
+    // last block: order-preserving compaction of the still-active queries
+    __threadfence();
+    if (threadIdx.x == 0) s_last = (atomicAdd(ticket, 1u) == gridDim.x - 1) ? 1u : 0u;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    __shared__ int s_n;
+    __shared__ int s_w[8];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    if (threadIdx.x == 0) s_n = 0;
+    __syncthreads();
+    for (int base = 0; base < na; base += blockDim.x) {
+        const int i = base + threadIdx.x;
+        const bool keep = i < na && ((volatile const QState*)qs)[act[i]].status == ST_ACTIVE;
+        const uint32_t bal = __ballot_sync(0xffffffffu, keep);
+        if (lane == 0) s_w[w] = __popc(bal);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int run = s_n;
+            for (int k = 0; k < (int)(blockDim.x / 32); ++k) { const int c_ = s_w[k]; s_w[k] = run; run += c_; }
+            s_n = run;
+        }
+        __syncthreads();
+        if (keep) act_out[s_w[w] + __popc(bal & lanemask_lt())] = act[i];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        *n_out = s_n;
+        *ticket = 0;                                  // ready for the next tree
+    }
+}
+
+
 // ---- verify (Alg. 5 lines 8/10): exact squared L2 of every member of S not yet verified,
 //      row-blocked: a CTA stages a block of consecutive data rows in shared memory once and
 //      serves every active query whose new candidates fall in that block (each row is a
@@ -2229,6 +2313,8 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
     Scratch s_qlut(st, sizeof(uint16_t) * (size_t)(qb * LK * ix.N_r));
     Scratch s_gtab(st, (size_t)16 * ceil_div(qb, RF_G) * ix.K * ix.N_r);
     Scratch s_tctr(st, sizeof(unsigned int) * (size_t)ceil_div(qb, RF_G));
+    Scratch s_ticket(st, sizeof(unsigned int));        // k_tree_post's last-block ticket
+    DL_CUDA(cudaMemsetAsync(s_ticket.p, 0, sizeof(unsigned int), st));
     static const bool rf_dyn = !std::getenv("DETLSH_RF_STRIPES");   // experiments: per-CTA stripes
     static const int pq_env = std::getenv("DETLSH_FILTER_PQ") ? std::atoi(std::getenv("DETLSH_FILTER_PQ")) : 1;
     auto k_range_filter_sel = (ix.K == 16 && ix.N_r == 256)
@@ -2510,9 +2596,23 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
                     static const int lp_y = std::getenv("DETLSH_LP_Y") ? std::atoi(std::getenv("DETLSH_LP_Y")) : 16;
                     DL_LAUNCH(k_leaf_points_sel, dim3((unsigned)nf, (unsigned)lp_y), LP_THREADS, lp_dyn, st, lpa);
                 }
-                if (a.lb_order) lb_order_tree(t, fa, nf, dnf);
+                if (!a.lb_order) {
+                    int* fa2 = (fa == fbuf0) ? fbuf1 : fbuf0;
+                    int* dn2 = (fa == fbuf0) ? n_f + 1 : n_f;
+                    const bool more = t + 1 < ix.L;
+                    DL_LAUNCH(k_tree_post, (unsigned)nf, 256, 0, st, fa, nf, dnf, s_qs.as<QState>(), s_bm.as<uint32_t>(),
+                              bm_prev, nwords, s_sum.as<uint32_t>(), nsw, budget, 0,
+                              use_pairs ? ra.pcnt : (uint32_t*)nullptr, lpa.ptake, t, m, cap, s_ticket.as<unsigned int>(),
+                              more ? fa2 : (int*)nullptr, more ? dn2 : (int*)nullptr);
+                    if (more) {
+                        fa = fa2;
+                        dnf = dn2;
+                    }
+                    continue;
+                }
+                lb_order_tree(t, fa, nf, dnf);
                 DL_LAUNCH(k_count_decide, (unsigned)ceil_div(nf, 256), 256, 0, st, fa, nf, dnf, s_qs.as<QState>(), budget,
-                          a.lb_order ? 1 : 0, use_pairs ? ra.pcnt : (uint32_t*)nullptr, lpa.ptake);
+                          1, use_pairs ? ra.pcnt : (uint32_t*)nullptr, lpa.ptake);
                 DL_LAUNCH(k_count_new, dim3((unsigned)nf, (unsigned)ceil_div(nsw, CN_SW)), 256, 0, st, fa, dnf,
                           s_qs.as<QState>(), s_bm.as<uint32_t>(), bm_prev, nwords, s_sum.as<uint32_t>(), nsw, 1);
                 if (t + 1 < ix.L) {

@@ -1385,7 +1385,10 @@ __global__ void __launch_bounds__(256) k_tree_post(const int* __restrict__ act, 
                                                    const uint32_t* __restrict__ wsum, int64_t nsw, int64_t budget,
                                                    int force, uint32_t* __restrict__ pcnt, uint32_t* __restrict__ ptake,
                                                    int t, int round, int64_t cap, unsigned int* __restrict__ ticket,
-                                                   int* __restrict__ act_out, int* __restrict__ n_out) {
+                                                   int* __restrict__ act_out, int* __restrict__ n_out,
+                                                   unsigned long long* __restrict__ total) {
+    // total != null: end of round instead -- every count forced, no budget test, and the last
+    // block lays out the round-buffer slots [roff, roff + rcnt) instead of compacting
     __shared__ unsigned int s_cnt, s_last;
     __shared__ int s_doc;
     const int na = dna ? *dna : na_ub;
@@ -1421,19 +1424,55 @@ __global__ void __launch_bounds__(256) k_tree_post(const int* __restrict__ act, 
         __syncthreads();
         if (threadIdx.x == 0) {
             if (s_cnt) s->cnt += s_cnt;
-            tree_end_one(s, t, round, budget, cap);
+            if (!total) tree_end_one(s, t, round, budget, cap);
         }
     }
-    if (!act_out) return;
+    if (!act_out && !total) return;
     // last block: order-preserving compaction of the still-active queries
     __threadfence();
     if (threadIdx.x == 0) s_last = (atomicAdd(ticket, 1u) == gridDim.x - 1) ? 1u : 0u;
     __syncthreads();
     if (!s_last) return;
     __threadfence();
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    if (total) {   // round-buffer slots: exclusive prefix of (|S| - verified) over the round's queries
+        __shared__ unsigned long long s_wl[8];
+        __shared__ unsigned long long s_run;
+        if (threadIdx.x == 0) s_run = 0;
+        __syncthreads();
+        for (int base = 0; base < na; base += blockDim.x) {
+            const int i = base + threadIdx.x;
+            unsigned long long c = 0;
+            if (i < na) {
+                const volatile QState* vs = (volatile const QState*)&qs[act[i]];
+                c = (unsigned long long)(vs->cnt - vs->nver);
+            }
+            unsigned long long x = c;
+            for (int o = 1; o < 32; o <<= 1) {
+                const unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
+                if (lane >= o) x += y;
+            }
+            if (lane == 31) s_wl[w] = x;
+            __syncthreads();
+            unsigned long long before = s_run;
+            for (int k = 0; k < w; ++k) before += s_wl[k];
+            if (i < na) {
+                QState* s2 = &qs[act[i]];
+                s2->roff = (int64_t)(before + x - c);
+                s2->rcnt = (int64_t)c;
+            }
+            __syncthreads();
+            if (threadIdx.x == blockDim.x - 1) s_run = before + x;
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) {
+            *total = s_run;
+            *ticket = 0;
+        }
+        return;
+    }
     __shared__ int s_n;
     __shared__ int s_w[8];
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     if (threadIdx.x == 0) s_n = 0;
     __syncthreads();
     for (int base = 0; base < na; base += blockDim.x) {
@@ -1741,50 +1780,6 @@ __global__ void k_prep_queries(const float* __restrict__ Q, int64_t ld, const in
         for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
         if (lane == 0) qn[a] = acc;
     }
-}
-
-// ---- per round: slot ranges of the new members of S (|S| - verified) in the round buffer
-__global__ void __launch_bounds__(1024) k_round_offsets(const int* __restrict__ act, int na, QState* __restrict__ qs,
-                                                        unsigned long long* __restrict__ total) {
-    __shared__ unsigned long long s_w[32];
-    __shared__ unsigned long long s_run;
-    if (threadIdx.x == 0) s_run = 0;
-    __syncthreads();
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    for (int base = 0; base < na; base += 1024) {
-        const int a_ = base + threadIdx.x;
-        unsigned long long c = 0;
-        if (a_ < na) {
-            const QState s = qs[act[a_]];
-            c = (unsigned long long)(s.cnt - s.nver);
-        }
-        unsigned long long x = c;
-        for (int o = 1; o < 32; o <<= 1) {
-            const unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
-            if (lane >= o) x += y;
-        }
-        if (lane == 31) s_w[w] = x;
-        __syncthreads();
-        if (w == 0) {
-            unsigned long long v = s_w[lane];
-            for (int o = 1; o < 32; o <<= 1) {
-                const unsigned long long y = __shfl_up_sync(0xffffffffu, v, o);
-                if (lane >= o) v += y;
-            }
-            s_w[lane] = v;
-        }
-        __syncthreads();
-        const unsigned long long incl = x + (w ? s_w[w - 1] : 0ull);
-        if (a_ < na) {
-            QState* s = &qs[act[a_]];
-            s->roff = (int64_t)(s_run + incl - c);
-            s->rcnt = (int64_t)c;
-        }
-        __syncthreads();
-        if (threadIdx.x == 1023) s_run += incl;
-        __syncthreads();
-    }
-    if (threadIdx.x == 0) *total = s_run;
 }
 
 // ---- top-k merge + termination test
@@ -2603,7 +2598,7 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
                     DL_LAUNCH(k_tree_post, (unsigned)nf, 256, 0, st, fa, nf, dnf, s_qs.as<QState>(), s_bm.as<uint32_t>(),
                               bm_prev, nwords, s_sum.as<uint32_t>(), nsw, budget, 0,
                               use_pairs ? ra.pcnt : (uint32_t*)nullptr, lpa.ptake, t, m, cap, s_ticket.as<unsigned int>(),
-                              more ? fa2 : (int*)nullptr, more ? dn2 : (int*)nullptr);
+                              more ? fa2 : (int*)nullptr, more ? dn2 : (int*)nullptr, (unsigned long long*)nullptr);
                     if (more) {
                         fa = fa2;
                         dnf = dn2;
@@ -2629,11 +2624,10 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
             }
             tr.mark("filter (L trees)", st);
             // |S| exact for the round's accounting (trees whose count was skipped)
-            DL_LAUNCH(k_count_decide, (unsigned)ceil_div(na, 256), 256, 0, st, cur, na, nullptr, s_qs.as<QState>(), budget, 1,
-                      (uint32_t*)nullptr, (uint32_t*)nullptr);
-            DL_LAUNCH(k_count_new, dim3((unsigned)na, (unsigned)ceil_div(nsw, CN_SW)), 256, 0, st, cur, nullptr,
-                      s_qs.as<QState>(), s_bm.as<uint32_t>(), bm_prev, nwords, s_sum.as<uint32_t>(), nsw, 1);
-            DL_LAUNCH(k_round_offsets, 1, 1024, 0, st, cur, na, s_qs.as<QState>(), s_total.as<unsigned long long>());
+            DL_LAUNCH(k_tree_post, (unsigned)na, 256, 0, st, cur, na, (const int*)nullptr, s_qs.as<QState>(),
+                      s_bm.as<uint32_t>(), bm_prev, nwords, s_sum.as<uint32_t>(), nsw, budget, 1, (uint32_t*)nullptr,
+                      (uint32_t*)nullptr, 0, m, cap, s_ticket.as<unsigned int>(), (int*)nullptr, (int*)nullptr,
+                      s_total.as<unsigned long long>());
             unsigned long long tot = 0;     // new members of S over the round's queries
             {
                 int bad = 0;

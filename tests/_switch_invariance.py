@@ -1,0 +1,21 @@
+"""Helper for test_filter_switches_do_not_change_results (run once per switch setting in a
+subprocess: the library reads its DETLSH_* switches once per process).  Builds a mid-size index
+and queries it at a small and a large radius; writes ids and distances to the .npz given."""
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import datagen  # noqa: E402
+import paper_2603_24920_b200 as P  # noqa: E402
+
+D = datagen.generate(2, n=60000, nq=300)
+c = D["cfg"]
+g = P.detlsh_build(D["X"], c.L, c.K, c.N_r, c.index_seed)
+out = {}
+for tag, r in (("small", 0.45), ("large", 0.9)):
+    ids, d = g.query(D["Q"], c.k, c.c, r, c.beta)
+    out[tag + "_ids"], out[tag + "_d"] = ids, d
+np.savez(sys.argv[1], **out)
+print("OK")

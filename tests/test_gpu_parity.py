@@ -563,3 +563,27 @@ def test_breakpoints_from_samples_paths(m, LK, N_r):
     B = P.detlsh_breakpoints_from_samples(Ps, N_r)
     for r in range(LK):
         assert np.array_equal(B[r], O.breakpoints_sort(Ps[:, r], N_r).astype(np.float32)), r
+
+
+def test_filter_switches_do_not_change_results(tmp_path):
+    """The filter's screens and work splits never change a result: the pair kernel's
+    sub-box level, the per-query scalar leaf loop with tile screens instead of the 16-query SIMD
+    leaf test, per-CTA tile stripes instead of per-group counters, and the pair path disabled
+    (all tiles through the 16-query SIMD chunks) give identical ids and distances."""
+    import os
+    import subprocess
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    runs = {"default": {}, "nosub": {"DETLSH_NO_SUBBOX": "1"}, "scalar_leaf": {"DETLSH_RF_DEBUG": "1"},
+            "stripes": {"DETLSH_RF_STRIPES": "1"}, "no_pairs": {"DETLSH_LEAF_PAIRS": "0"}}
+    res = {}
+    for name, extra in runs.items():
+        out = str(tmp_path / f"{name}.npz")
+        env = dict(os.environ, **extra)
+        r = subprocess.run([sys.executable, os.path.join(here, "_switch_invariance.py"), out], env=env,
+                           capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0 and "OK" in r.stdout, name + ": " + r.stdout + r.stderr
+        res[name] = np.load(out)
+    for name in runs:
+        for key in res["default"].files:
+            assert np.array_equal(res[name][key], res["default"][key]), (name, key)

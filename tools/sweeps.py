@@ -70,7 +70,8 @@ def main():
         r = g.estimate_rmin(D["Qs"], cfg.k, cfg.beta)
         point("E6_LK", g, cfg.k, r, cfg.beta, L=L, K=K, build_s=round(tb, 4))
         g.free()
-    path = os.path.join(ROOT, "profiles", "r01_sweeps.json")
+    # on a gpurun box only gpurun_out/ comes back: pass a path there and copy it to profiles/
+    path = sys.argv[1] if len(sys.argv) > 1 else os.path.join(ROOT, "profiles", "r01_sweeps.json")
     json.dump(out, open(path, "w"), indent=1)
 
 

@@ -2679,7 +2679,7 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
                         cq_cap = (int64_t)(tot + tot / 2 + 1024);
                         s_cq.alloc(sizeof(uint32_t) * (size_t)cq_cap);
                     }
-                    DL_LAUNCH(k_verify_list, (unsigned)na, 256, 0, st, cur, s_qs.as<QState>(), s_bm.as<uint32_t>(),
+                    DL_LAUNCH(k_verify_list, (unsigned)na, 128, 0, st, cur, s_qs.as<QState>(), s_bm.as<uint32_t>(),
                               s_ver.as<uint32_t>(), nwords, s_sum.as<uint32_t>(), nsw, va.cand, s_cq.as<uint32_t>());
                     const unsigned vg = (unsigned)std::min<int64_t>(ceil_div((int64_t)tot * 8, 256), 148 * 32);
                     auto k_verify_gather_sel = ix.ld == 128   ? k_verify_gather<4>

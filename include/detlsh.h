@@ -137,6 +137,18 @@ detlsh_status detlsh_query_ex(const detlsh_index* idx, const float* queries, int
                               int64_t* out_ids, float* out_dists, detlsh_query_stats* stats);
 
 /*
+ * Test/debug variant of detlsh_query_ex that also exports each query's candidate set S at
+ * termination (the union of Alg. 5 line 6, over every tree the query processed): S is
+ * host or device memory [nq][S_words] u32, S_words = ceil(n/32); bit (p % 32) of word p / 32 is
+ * set iff local id p is in S.  Other arguments, outputs and errors as detlsh_query_ex; EINVAL if
+ * S is NULL or S_words != ceil(n/32).
+ */
+detlsh_status detlsh_query_candidates(const detlsh_index* idx, const float* queries, int64_t nq, int32_t k,
+                                      double c, double r_min, double beta, const detlsh_opts* opts,
+                                      int64_t* out_ids, float* out_dists, detlsh_query_stats* stats,
+                                      uint32_t* S, int64_t S_words);
+
+/*
  * (r,c)-ANN for queries[nq][d] (Alg. 4): one pass over the L trees at radius
  * eps*r; as soon as |S| >= ceil(beta n) + 1 the point of S closest to q is returned
  * (line 6); after the L trees the closest point of S is returned if it lies within c r
@@ -193,8 +205,12 @@ detlsh_status detlsh_breakpoints_from_samples(const float* samples, int64_t m, i
                                               int32_t N_r, const detlsh_opts* opts, float* out);
 
 /*
- * C2 merge: G per-shard top-k lists ids[G][nq][k], dists[G][nq][k] ->
- * the k best by (dist, id); ids < 0 are empty slots.  Host memory only (plain C++).
+ * C2 merge: G per-shard top-k lists ids[G][nq][k], dists[G][nq][k], each sorted
+ * ascending by (dist, id) with empty slots (id < 0) last (as detlsh_query writes them) -> the k
+ * best by (dist, id) (AMB-21); unfilled output slots are (-1, +inf).  Pointers host or device
+ * (host inputs are staged); the merge runs on the device (k_merge_topk: rank of each element
+ * = its index + binary-searched counts in the other lists), on the legacy default stream.
+ * Errors (EINVAL): NULL pointer; G < 1; nq < 0; k < 1.
  */
 detlsh_status detlsh_merge_topk(const int64_t* ids, const float* dists, int32_t G, int64_t nq,
                                 int32_t k, int64_t* out_ids, float* out_dists);

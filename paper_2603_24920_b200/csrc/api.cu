@@ -5,6 +5,7 @@
 #include <cmath>
 #include <cstring>
 #include <memory>
+#include <mutex>
 #include <new>
 #include <string>
 #include <vector>
@@ -34,9 +35,11 @@ void project_rows(const Index& ix, const float* d_X, int64_t ld, int64_t m, floa
 std::atomic<int64_t> g_index_bytes{0};
 
 cudaMemPool_t index_pool() {
+    static std::mutex mu;
     static cudaMemPool_t pools[64] = {};
     int dev = 0;
     DL_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(mu);
     if (!pools[dev]) {
         cudaMemPoolProps props = {};
         props.allocType = cudaMemAllocationTypePinned;
@@ -85,17 +88,8 @@ void require_device() {
         cudaGetLastError();
         throw Error(DETLSH_ECUDA, "no CUDA device available");
     }
-    // Keep freed stream-ordered scratch in the device pool (no unmap/remap between calls).
-    int dev = 0;
-    DL_CUDA(cudaGetDevice(&dev));
-    static thread_local int configured = -1;
-    if (configured != dev) {
-        cudaMemPool_t pool;
-        DL_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
-        uint64_t thr = UINT64_MAX;
-        DL_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
-        configured = dev;
-    }
+    // scratch and index memory come from the library's own pools (scratch_pool, index_pool),
+    // which keep freed memory mapped; the device's default pool is left alone
 }
 
 cudaStream_t stream_of(const detlsh_opts* o) { return o ? reinterpret_cast<cudaStream_t>(o->stream) : (cudaStream_t)0; }
@@ -247,7 +241,8 @@ detlsh_status detlsh_build(const float* data, int64_t n, int32_t d, int32_t L, i
 
 static detlsh_status run_query(const detlsh_index* idx, const float* queries, int64_t nq, int32_t k, double c,
                                double r_min, double beta, const detlsh_opts* opts, int64_t* out_ids, float* out_dists,
-                               detlsh_query_stats* stats, int max_rounds, bool null_on_cap) {
+                               detlsh_query_stats* stats, int max_rounds, bool null_on_cap,
+                               uint32_t* export_S = nullptr, int64_t S_words = 0) {
     return guard([&] {
         DL_REQUIRE(idx, "index is NULL");
         const Index& ix = *reinterpret_cast<const Index*>(idx);
@@ -273,16 +268,23 @@ static detlsh_status run_query(const detlsh_index* idx, const float* queries, in
         DevOut od(out_dists, sizeof(float) * (size_t)(nq * k), st);
         std::unique_ptr<DevOut> os;
         if (stats) os.reset(new DevOut(stats, sizeof(detlsh_query_stats) * (size_t)nq, st));
+        std::unique_ptr<DevOut> oS;
+        if (export_S) {
+            DL_REQUIRE(S_words == ceil_div(ix.n, 32), "S_words must be ceil(n / 32)");
+            oS.reset(new DevOut(export_S, sizeof(uint32_t) * (size_t)(nq * S_words), st));
+        }
         DL_REQUIRE(o.verify_impl >= 0 && o.verify_impl <= 3, "verify_impl must be 0..3");
         QueryArgs a{nq, k, c, r_min, beta, o.mode, o.query_batch, o.mem_budget, o.proj_impl, o.verify_impl};
         a.max_rounds = max_rounds;
         a.null_on_cap = null_on_cap;
         a.lb_order = o.lb_order ? 1 : 0;
+        a.export_S = oS ? static_cast<uint32_t*>(oS->dev()) : nullptr;
         query_index(ix, s_q.as<float>(), ix.ld, a, static_cast<int64_t*>(oi.dev()), static_cast<float*>(od.dev()),
                     os ? static_cast<detlsh_query_stats*>(os->dev()) : nullptr, st);
         oi.finish(st);
         od.finish(st);
         if (os) os->finish(st);
+        if (oS) oS->finish(st);
         DL_CUDA(cudaStreamSynchronize(st));
     });
 }
@@ -291,6 +293,16 @@ detlsh_status detlsh_query_ex(const detlsh_index* idx, const float* queries, int
                               double r_min, double beta, const detlsh_opts* opts, int64_t* out_ids, float* out_dists,
                               detlsh_query_stats* stats) {
     return run_query(idx, queries, nq, k, c, r_min, beta, opts, out_ids, out_dists, stats, 64, false);
+}
+
+detlsh_status detlsh_query_candidates(const detlsh_index* idx, const float* queries, int64_t nq, int32_t k, double c,
+                                      double r_min, double beta, const detlsh_opts* opts, int64_t* out_ids,
+                                      float* out_dists, detlsh_query_stats* stats, uint32_t* S, int64_t S_words) {
+    if (!S) {
+        g_err = "S is NULL";
+        return DETLSH_EINVAL;
+    }
+    return run_query(idx, queries, nq, k, c, r_min, beta, opts, out_ids, out_dists, stats, 64, false, S, S_words);
 }
 
 detlsh_status detlsh_rc_ann(const detlsh_index* idx, const float* queries, int64_t nq, double r, double c,
@@ -470,21 +482,30 @@ detlsh_status detlsh_merge_topk(const int64_t* ids, const float* dists, int32_t 
     return guard([&] {
         DL_REQUIRE(ids && dists && out_ids && out_dists, "NULL argument");
         DL_REQUIRE(G >= 1 && nq >= 0 && k >= 1, "need G >= 1, nq >= 0, k >= 1");
-        std::vector<std::pair<float, int64_t>> v;
-        v.reserve((size_t)G * k);
-        for (int64_t q = 0; q < nq; ++q) {
-            v.clear();
-            for (int g = 0; g < G; ++g)
-                for (int e = 0; e < k; ++e) {
-                    const size_t o = ((size_t)g * nq + q) * k + e;
-                    if (ids[o] >= 0) v.emplace_back(dists[o], ids[o]);
-                }
-            std::sort(v.begin(), v.end());   // (dist, id) ascending (AMB-21)
-            for (int e = 0; e < k; ++e) {
-                out_ids[q * k + e] = e < (int)v.size() ? v[e].second : -1;
-                out_dists[q * k + e] = e < (int)v.size() ? v[e].first : INFINITY;
-            }
+        if (nq == 0) return;
+        require_device();
+        cudaStream_t st = 0;
+        WorkspaceScope ws(st);
+        const size_t ni = sizeof(int64_t) * (size_t)G * nq * k, nd = sizeof(float) * (size_t)G * nq * k;
+        Scratch s_i(st), s_d(st);
+        const int64_t* di = ids;
+        const float* dd = dists;
+        if (!is_device_ptr(ids)) {
+            s_i.alloc(ni);
+            DL_CUDA(cudaMemcpyAsync(s_i.p, ids, ni, cudaMemcpyHostToDevice, st));
+            di = s_i.as<int64_t>();
         }
+        if (!is_device_ptr(dists)) {
+            s_d.alloc(nd);
+            DL_CUDA(cudaMemcpyAsync(s_d.p, dists, nd, cudaMemcpyHostToDevice, st));
+            dd = s_d.as<float>();
+        }
+        DevOut oi(out_ids, sizeof(int64_t) * (size_t)(nq * k), st);
+        DevOut od(out_dists, sizeof(float) * (size_t)(nq * k), st);
+        merge_topk_device(di, dd, G, nq, k, static_cast<int64_t*>(oi.dev()), static_cast<float*>(od.dev()), st);
+        oi.finish(st);
+        od.finish(st);
+        DL_CUDA(cudaStreamSynchronize(st));
     });
 }
 

@@ -1040,11 +1040,7 @@ void sample_ids_device(uint64_t seed, int64_t id_lo, int64_t n_range, int64_t n_
     DL_LAUNCH(k_sel16_pick, 1, 1024, 0, st, hist, n_s, state);
     DL_LAUNCH(k_sel16_collect, g, 256, 0, st, salt, id_lo, n_range, n_global, state, d_out_local, counter, ckey, cid, ccap);
     const size_t fsm = (sizeof(unsigned long long) + sizeof(uint32_t)) * (size_t)ccap;
-    static size_t f_configured = 0;
-    if (f_configured < fsm) {
-        DL_CUDA(cudaFuncSetAttribute(k_sel16_finish, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm));
-        f_configured = fsm;
-    }
+    ensure_dyn_smem_fn(k_sel16_finish, fsm);
     DL_LAUNCH(k_sel16_finish, 1, 1024, fsm, st, id_lo, n_range, state, ckey, cid, ccap, d_out_local, counter);
     struct {
         unsigned long long got;
@@ -1087,7 +1083,7 @@ void breakpoints_from_projections(const float* d_Ps, int64_t m, int LK, int N_r,
 
 static void encode_all(const Index& ix, const float* d_P, int64_t m, uint8_t* d_EP, cudaStream_t st) {
     const size_t smem = sizeof(float) * (size_t)ix.LK * ix.N_r;
-    DL_CUDA(cudaFuncSetAttribute(k_encode, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    ensure_dyn_smem_fn(k_encode, smem);
     DL_LAUNCH(k_encode, grid_for(m * ix.LK / 4, 256, 148 * 4), 256, smem, st, d_P, m, ix.LK, ix.N_r,
               ix.B.as<float>(), d_EP);
 }
@@ -1198,12 +1194,7 @@ static bool build_trees_try(Index& ix, const uint8_t* d_EP, int64_t leaf_factor,
         const int LF_THREADS = lf_nt == 256 ? 256 : 512;
         auto k_local_finish_sel = K <= 16 ? (LF_THREADS == 256 ? k_local_finish<16, 256> : k_local_finish<16, 512>)
                                           : (LF_THREADS == 256 ? k_local_finish<32, 256> : k_local_finish<32, 512>);
-        static size_t lf_configured[4] = {0, 0, 0, 0};
-        const int ci = (K > 16) * 2 + (LF_THREADS == 256);
-        if (lf_configured[ci] < lsm) {
-            DL_CUDA(cudaFuncSetAttribute(k_local_finish_sel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lsm));
-            lf_configured[ci] = lsm;
-        }
+        ensure_dyn_smem_fn(k_local_finish_sel, lsm);
         int dev = 0, nsm = 148, per_sm = 1;
         DL_CUDA(cudaGetDevice(&dev));
         DL_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));

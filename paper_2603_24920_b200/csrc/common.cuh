@@ -116,9 +116,9 @@ struct Trace {
 // work opens one for its stream) requests are bump-allocated from a grow-only arena owned by
 // that (device, stream): no allocator traffic between calls, so a query or build never
 // waits on the driver mapping memory.  A request the arena cannot hold yet is served by
-// cudaMallocAsync and counted; when the call ends the arena is regrown to the call's
+// the scratch pool (stream-ordered) and counted; when the call ends the arena is regrown to the call's
 // high-water mark, so from the second call of a given shape on everything is bumped.
-// Outside a scope Scratch falls back to stream-ordered cudaMallocAsync/cudaFreeAsync.
+// Outside a scope Scratch falls back to stream-ordered allocations from scratch_pool().
 void* ws_alloc(size_t bytes, cudaStream_t st, bool* from_arena);
 
 struct WorkspaceScope {
@@ -131,6 +131,16 @@ struct WorkspaceScope {
 };
 void ws_release_all();
 int64_t ws_bytes_held();
+// Pool for per-call scratch that the arena cannot hold (private: the device's default pool and
+// its release threshold are left as the process set them).  Keeps freed memory mapped.
+cudaMemPool_t scratch_pool();
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) for `fn` on the current device, once per
+// (device, kernel) and only when `bytes` exceeds what was set before (thread-safe).
+void ensure_dyn_smem(const void* fn, size_t bytes);
+template <class F> inline void ensure_dyn_smem_fn(F* fn, size_t bytes) {
+    ensure_dyn_smem(reinterpret_cast<const void*>(fn), bytes);
+}
 
 struct Scratch {
     cudaStream_t st;

@@ -8,11 +8,11 @@
 
 namespace detlsh {
 
-// Pool for index-owned (long-lived) buffers, separate from the default pool that serves
-// per-call scratch, so the two lifetimes do not fragment each other (api.cu).
+// Pool for index-owned (long-lived) buffers, separate from the scratch pool (workspace.cu), so
+// the two lifetimes do not fragment each other (api.cu).  The query batch budget subtracts
+// what this pool has reserved since its free-memory snapshot (query.cu).
 cudaMemPool_t index_pool();
-// Bytes held by live index buffers (all devices), kept by DevBuf (the query batch budget
-// subtracts what indexes built after its free-memory snapshot hold, api.cu/query.cu).
+// Bytes held by live index buffers (all devices), kept by DevBuf.
 extern std::atomic<int64_t> g_index_bytes;
 
 // Index-owned device memory, stream-ordered from index_pool() (no device-wide sync on
@@ -97,6 +97,10 @@ void sample_ids_device(uint64_t seed, int64_t id_lo, int64_t n_range, int64_t n_
 void breakpoints_from_projections(const float* d_Ps, int64_t m, int LK, int N_r, float* d_B,
                                   cudaStream_t st);
 
+// merge.cu: C2 merge of G per-shard top-k lists [G][nq][k] (device pointers)
+void merge_topk_device(const int64_t* d_ids, const float* d_dists, int G, int64_t nq, int k, int64_t* d_out_ids,
+                       float* d_out_dists, cudaStream_t st);
+
 // persist.cu
 void save_index(const Index& ix, const char* path);
 Index* load_index(const char* path);
@@ -115,6 +119,8 @@ struct QueryArgs {
     int max_rounds = 64;        // AMB-20 round cap; 1 for (r,c)-ANN (Alg. 4)
     bool null_on_cap = false;   // (r,c)-ANN: return nothing when the single pass neither hit the
                                 // budget nor found a point within c r
+    uint32_t* export_S = nullptr;   // test export: device [nq][ceil(n/32)] copy of each query's final
+                                    // candidate-set bitmap S (bit p%32 of word p/32 = local id p)
 };
 void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArgs& a, int64_t* d_ids,
                  float* d_dists, detlsh_query_stats* d_stats, cudaStream_t st);

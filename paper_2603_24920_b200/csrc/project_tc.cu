@@ -329,11 +329,7 @@ static bool launch_tc(const Index& ix, const float* d_X, int64_t ld, int64_t m, 
     CUtensorMap mx, ma;
     make_map(&mx, d_X, m, (int)ld, TC_M);
     make_map(&ma, ix.A.as<float>(), ix.LK, (int)ld, sh.npad);
-    static size_t configured = 0;
-    if (configured < smem) {
-        DL_CUDA(cudaFuncSetAttribute(k_project_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        configured = smem;
-    }
+    ensure_dyn_smem_fn(k_project_tc, smem);
     int dev = 0, nsm = 148;
     DL_CUDA(cudaGetDevice(&dev));
     DL_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));

@@ -1983,21 +1983,24 @@ __global__ void __launch_bounds__(TK_THREADS) k_topk(const int* __restrict__ act
                 s_rem = (unsigned long long)(k - below);
             }
             __syncthreads();
-            for (int shift = 44; shift >= 0; shift -= 8) {
+            // 8-bit digits at bits 51..4, then a 4-bit digit at bits 3..0: the exact k-th key
+            for (int shift = 44; shift >= -4; shift -= 8) {
+                const int sh = shift < 0 ? 0 : shift;
+                const uint32_t dmask = shift < 0 ? 15u : 255u;
                 for (int i = threadIdx.x; i < 256; i += TK_THREADS) s_hist[i] = 0;
                 __syncthreads();
                 const unsigned long long pre = s_prefix, msk = s_mask;
                 for (int64_t i = threadIdx.x; i < M; i += TK_THREADS) {
                     const unsigned long long key = key_at(i);
-                    if ((key & msk) == pre) atomicAdd(&s_hist[(key >> shift) & 255u], 1u);
+                    if ((key & msk) == pre) atomicAdd(&s_hist[(key >> sh) & dmask], 1u);
                 }
                 __syncthreads();
                 if (threadIdx.x == 0) {
                     unsigned long long cum = 0, rem = s_rem;
-                    for (int dg = 0; dg < 256; ++dg) {
+                    for (int dg = 0; dg <= (int)dmask; ++dg) {
                         if (cum + s_hist[dg] >= rem) {
-                            s_prefix = pre | ((unsigned long long)dg << shift);
-                            s_mask = msk | (0xFFull << shift);
+                            s_prefix = pre | ((unsigned long long)dg << sh);
+                            s_mask = msk | ((unsigned long long)dmask << sh);
                             s_rem = rem - cum;
                             break;
                         }
@@ -2006,11 +2009,11 @@ __global__ void __launch_bounds__(TK_THREADS) k_topk(const int* __restrict__ act
                 }
                 __syncthreads();
             }
-            // the low 4 bits were never selected on (12 + 6*8 = 60): finish by exact compare
+            // keys are unique per query ((d2, id) with distinct ids), so exactly k keys are <= T0
             const unsigned long long T0 = s_prefix;
             for (int64_t i = threadIdx.x; i < M; i += TK_THREADS) {
                 const unsigned long long key = key_at(i);
-                if (key < T0 + 16 && ((key >> 4) <= (T0 >> 4))) {
+                if (key <= T0) {
                     const int slot = atomicAdd(&s_n, 1);
                     if (slot < TK_MAX) s_keys[slot] = key;
                 }
@@ -2115,20 +2118,25 @@ __global__ void k_init_batch(QState* __restrict__ qs, int* __restrict__ act, int
 }
 
 int64_t auto_query_budget() {
-    // free memory sampled once per device, corrected by the index bytes allocated (or freed)
-    // since the sample -- a large index built after the first query shrinks the batch
+    // free memory sampled once per device, corrected by the memory the index pool has reserved
+    // since the sample.  The pool keeps freed index memory mapped (no release), so what it
+    // reserves -- not what live indexes hold -- is unavailable to query scratch: an index
+    // built after the first query shrinks the batch, freeing it does not grow it back.
     static std::mutex mu;
-    static int64_t free0[64] = {}, index0[64] = {};
+    static int64_t free0[64] = {}, res0[64] = {};
     int dev = 0;
     DL_CUDA(cudaGetDevice(&dev));
+    cudaMemPool_t ip = index_pool();
     std::lock_guard<std::mutex> lk(mu);
+    uint64_t res = 0;
+    DL_CUDA(cudaMemPoolGetAttribute(ip, cudaMemPoolAttrReservedMemCurrent, &res));
     if (!free0[dev]) {
         size_t fr = 0, tot = 0;
         DL_CUDA(cudaMemGetInfo(&fr, &tot));
         free0[dev] = std::max<int64_t>(1, (int64_t)fr);
-        index0[dev] = g_index_bytes.load();
+        res0[dev] = (int64_t)res;
     }
-    const int64_t fr = free0[dev] - (g_index_bytes.load() - index0[dev]);
+    const int64_t fr = free0[dev] - std::max<int64_t>(0, (int64_t)res - res0[dev]);
     return std::max<int64_t>(1, (int64_t)(0.6 * (double)fr));
 }
 
@@ -2214,7 +2222,7 @@ void estimate_rstar(const Index& ix, const float* d_Q, int64_t q_ld, int64_t ns,
     Scratch s_tp(st, sizeof(uint32_t) * (size_t)(ns * n));
     DL_CUDA(cudaMemsetAsync(s_tp.p, 0xFF, sizeof(uint32_t) * (size_t)(ns * n), st));   // NaN bits > +inf bits
     const size_t smem = sizeof(float) * (size_t)ix.K * ix.N_r;
-    DL_CUDA(cudaFuncSetAttribute(k_rstar_tree, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    ensure_dyn_smem_fn(k_rstar_tree, smem);
     const unsigned gx = (unsigned)std::min<int64_t>(ceil_div(n, 256), 64);
     for (int t = 0; t < ix.L; ++t)
         DL_LAUNCH(k_rstar_tree, dim3(gx, (unsigned)ns), 256, smem, st, s_lut.as<float>(),
@@ -2316,7 +2324,7 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
                                   ? (pq_env ? k_range_filter<16 COMMA 256 COMMA RF_G COMMA true>
                                             : k_range_filter<16 COMMA 256 COMMA RF_G COMMA false>)
                                   : k_range_filter<0 COMMA 0 COMMA RF_G COMMA false>;
-    DL_CUDA(cudaFuncSetAttribute(k_range_filter_sel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rf_smem));
+    ensure_dyn_smem_fn(k_range_filter_sel, rf_smem);
     RFArgs ra;
     ra.gtab = nullptr;
     ra.tctr = nullptr;
@@ -2349,7 +2357,7 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
                                       : k_leaf_points<0, 0, 16>;
     const size_t lp_dyn = lp_fixed ? 0 : lp_smem;
     if (use_pairs && !lp_fixed)
-        DL_CUDA(cudaFuncSetAttribute(k_leaf_points_sel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lp_smem));
+        ensure_dyn_smem_fn(k_leaf_points_sel, lp_smem);
     ra.leaf_off = ix.leaf_off.as<uint32_t>();
     // leaf pruning uses the tight boxes (a valid, tighter bound for every member); RELAXED takes
     // whole leaves by the leaf's own (prefix) box, as the method defines it
@@ -2406,13 +2414,13 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
     Scratch s_boff(st, sizeof(uint32_t) * (size_t)(a.verify_impl != 1 ? 2 * qb * nw4 : qb * ceil_div(nwords, va.rbw)));
     Scratch s_qa(st, tc_ok ? sizeof(float) * (size_t)(qb * (2 * ix.ld + 1)) : 0);
     const bool vexact = (ix.ld / 4) == 8 * vnv;
-    DL_CUDA(cudaFuncSetAttribute(k_verify_rows<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)vr_smem));
-    DL_CUDA(cudaFuncSetAttribute(k_verify_rows<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)vr_smem));
-    DL_CUDA(cudaFuncSetAttribute(k_verify_rows<4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)vr_smem));
-    DL_CUDA(cudaFuncSetAttribute(k_verify_rows<4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)vr_smem));
-    DL_CUDA(cudaFuncSetAttribute(k_verify_rows<8, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)vr_smem));
-    DL_CUDA(cudaFuncSetAttribute(k_verify_rows<8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)vr_smem));
-    DL_CUDA(cudaFuncSetAttribute(k_verify_rows<0, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)vr_smem));
+    ensure_dyn_smem_fn(k_verify_rows<1, false>, vr_smem);
+    ensure_dyn_smem_fn(k_verify_rows<2, false>, vr_smem);
+    ensure_dyn_smem_fn(k_verify_rows<4, false>, vr_smem);
+    ensure_dyn_smem_fn(k_verify_rows<4, true>, vr_smem);
+    ensure_dyn_smem_fn(k_verify_rows<8, false>, vr_smem);
+    ensure_dyn_smem_fn(k_verify_rows<8, true>, vr_smem);
+    ensure_dyn_smem_fn(k_verify_rows<0, false>, vr_smem);
 
     // Sec. 6.2.2(2): for the queries whose tree-t candidates cross the budget, keep
     // only the leaves up to the one (in (LB, leaf) order) at which |S| reaches it
@@ -2726,6 +2734,11 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
         DL_LAUNCH(k_finalize, (unsigned)std::min<int64_t>(ceil_div((int64_t)nqb * k, 256), 148 * 16), 256, 0, st,
                   s_qs.as<QState>(), s_ctr.as<unsigned long long>(), s_tk.as<unsigned long long>(), nqb, k, ix.id_offset, s_radii.as<double>(),
                   d_ids + q0 * k, d_dists + q0 * k, d_stats ? d_stats + q0 : nullptr, a.null_on_cap ? 1 : 0);
+        if (a.export_S) {
+            const int64_t w = ceil_div(n, 32);
+            DL_CUDA(cudaMemcpy2DAsync(a.export_S + q0 * w, sizeof(uint32_t) * w, s_bm.p, sizeof(uint32_t) * nwords,
+                                      sizeof(uint32_t) * w, (size_t)nqb, cudaMemcpyDeviceToDevice, st));
+        }
         (void)Qb;
     }
 }

@@ -302,11 +302,7 @@ bool verify_tc(const float* d_X, int64_t n, int ld, const float* d_Qa, const flo
     make_map_sw64(&mql, d_Qalo, na, ld, sh.N);
     make_map_u32(&mnb, d_NB, na, nw4, 4, sh.N);
     make_map_u32(&mbo, d_BO, na, nw4, 4, sh.N);
-    static size_t configured = 0;
-    if (configured < smem) {
-        DL_CUDA(cudaFuncSetAttribute(k_verify_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        configured = smem;
-    }
+    ensure_dyn_smem_fn(k_verify_tc, smem);
     int dev = 0, nsm = 148;
     DL_CUDA(cudaGetDevice(&dev));
     DL_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));

@@ -50,9 +50,39 @@ void* ws_alloc(size_t bytes, cudaStream_t st, bool* from_arena) {
         }
     }
     void* p = nullptr;
-    DL_CUDA(cudaMallocAsync(&p, bytes, st));
+    DL_CUDA(cudaMallocFromPoolAsync(&p, bytes, scratch_pool(), st));
     *from_arena = false;
     return p;
+}
+
+cudaMemPool_t scratch_pool() {
+    static std::mutex mu;
+    static cudaMemPool_t pools[64] = {};
+    int dev = 0;
+    DL_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(mu);
+    if (!pools[dev]) {
+        cudaMemPoolProps props = {};
+        props.allocType = cudaMemAllocationTypePinned;
+        props.location.type = cudaMemLocationTypeDevice;
+        props.location.id = dev;
+        DL_CUDA(cudaMemPoolCreate(&pools[dev], &props));
+        uint64_t thr = UINT64_MAX;    // no unmap/remap between calls
+        DL_CUDA(cudaMemPoolSetAttribute(pools[dev], cudaMemPoolAttrReleaseThreshold, &thr));
+    }
+    return pools[dev];
+}
+
+void ensure_dyn_smem(const void* fn, size_t bytes) {
+    static std::mutex mu;
+    static std::map<std::pair<int, const void*>, size_t> done;
+    int dev = 0;
+    DL_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(mu);
+    size_t& have = done[{dev, fn}];
+    if (have >= bytes) return;
+    DL_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    have = bytes;
 }
 
 WorkspaceScope::WorkspaceScope(cudaStream_t st) {

@@ -78,6 +78,7 @@ def lib():
         "detlsh_build_ex": (i32, [P, i64, i32, i32, i32, i32, u64, O, i64, i64, P, P]),
         "detlsh_query": (i32, [P, P, i64, i32, f64, f64, f64, P, P]),
         "detlsh_query_ex": (i32, [P, P, i64, i32, f64, f64, f64, O, P, P, P]),
+        "detlsh_query_candidates": (i32, [P, P, i64, i32, f64, f64, f64, O, P, P, P, P, i64]),
         "detlsh_free": (None, [P]),
         "detlsh_last_error": (C.c_char_p, []),
         "detlsh_params": (i32, [i32, i32, f64, P, P, P]),
@@ -333,6 +334,27 @@ def detlsh_query_ex(index: Index, Q, k, c, r_min, beta, opts=None, stats=False, 
     return (ids, dists, st) if stats else (ids, dists)
 
 
+def detlsh_query_candidates(index: Index, Q, k, c, r_min, beta, opts=None):
+    """Test hook: ids, dists, stats and each query's final candidate set S as a [nq][ceil(n/32)] u32 bitmap."""
+    Q = _f32(Q)
+    nq = Q.shape[0]
+    ids = np.empty((nq, k), np.int64)
+    dists = np.empty((nq, k), np.float32)
+    st = np.zeros(nq, STATS_DTYPE)
+    w = (index.n + 31) // 32
+    S = np.zeros((nq, w), np.uint32)
+    o = opts if opts is not None else default_opts()
+    _check(lib().detlsh_query_candidates(index.handle, _ptr(Q), nq, k, c, r_min, beta, C.byref(o), _ptr(ids),
+                                         _ptr(dists), _ptr(st), _ptr(S), w))
+    return ids, dists, st, S
+
+
+def candidate_ids(S_row, n: int) -> np.ndarray:
+    """Local ids whose bit is set in one exported S bitmap row (ascending)."""
+    bits = np.unpackbits(np.ascontiguousarray(S_row, np.uint32).view(np.uint8), bitorder="little")
+    return np.flatnonzero(bits[:n])
+
+
 def detlsh_query(index: Index, Q, k, c, r_min, beta):
     return detlsh_query_ex(index, Q, k, c, r_min, beta)
 
@@ -356,12 +378,19 @@ def detlsh_build_from_codes(codes, L: int, K: int, N_r: int, max_size: int = 128
     return Index(h, n, 1, L, K, N_r)
 
 
-def detlsh_merge_topk(ids: np.ndarray, dists: np.ndarray, k: int):
-    ids = np.ascontiguousarray(ids, np.int64)
-    dists = np.ascontiguousarray(dists, np.float32)
-    G, nq, _ = ids.shape
-    oi = np.empty((nq, k), np.int64)
-    od = np.empty((nq, k), np.float32)
+def detlsh_merge_topk(ids, dists, k: int):
+    """C2 merge of [G][nq][k'] per-shard lists on the device; torch CUDA tensors stay on the device."""
+    if _is_torch(ids):
+        import torch
+        ids = ids.to(torch.int64).contiguous()
+        dists = dists.to(device=ids.device, dtype=torch.float32).contiguous()
+    else:
+        ids = np.ascontiguousarray(ids, np.int64)
+        dists = np.ascontiguousarray(dists, np.float32)
+    G, nq, kk = ids.shape
+    assert kk == k, "per-shard lists must hold k entries"
+    oi = _like(ids, (nq, k), np.int64, _torch_i64())
+    od = _like(ids, (nq, k), np.float32, _torch_f32())
     _check(lib().detlsh_merge_topk(_ptr(ids), _ptr(dists), G, nq, k, _ptr(oi), _ptr(od)))
     return oi, od
 

@@ -41,7 +41,9 @@ def test_sample_size_rule():
         [8192, 10_000, 100_000, 1_000_000, 300]
 
 
-def test_merge_topk_host():
+@pytest.mark.gpu
+def test_merge_topk_device():
+    """C2 merge (k_merge_topk) vs a plain sort of the pooled (dist, id) pairs."""
     rng = np.random.default_rng(0)
     G, nq, k = 4, 6, 5
     d = np.sort(rng.integers(0, 9, (G, nq, k)).astype(np.float32), -1)

@@ -7,6 +7,7 @@ the oracle's own G-shard result (O9).
 """
 import os
 import socket
+from types import SimpleNamespace
 
 import numpy as np
 import pytest
@@ -40,20 +41,44 @@ def _worker(rank, world, port, out_q):
         D = datagen.generate(1, n=3000, nq=12)
         X, Q = D["X"], D["Q"]
         n = X.shape[0]
+        L, K, N_r, seed = 4, 16, 256, 42
         lo, hi = PD.shard_range(n, world, rank)
-        sh = O.Index(X, 4, 16, 256, 42, row_lo=lo, row_hi=hi)
-        # C1: this shard's rows of the global sample, projected; all-gather; sort per column
-        sample = sh.sample()                      # global ids of the whole-dataset sample
-        mine = sample[(sample >= lo) & (sample < hi)] - lo
-        Ps = torch.from_numpy(sh.P()[mine])
-        allp = PD.allgather_rows(Ps).numpy()
-        B = np.stack([O.breakpoints_sort(allp[:, r], 256) for r in range(64)])
-        whole = O.Index(X, 4, 16, 256, 42)
-        assert np.array_equal(B, whole.breakpoints())
+        sh = O.Index(X, L, K, N_r, seed, row_lo=lo, row_hi=hi)   # the oracle's shard g (O9)
+        calls = []
+
+        # The per-shard arithmetic the library does on the GPU, stood in for by the oracle; the
+        # glue (C1 all-gather of ragged row sets, breakpoint hand-off, C2 all-gather + merge) is
+        # dist.py's own code under the gloo process group.
+        def sample_projections(X_shard, L_, K_, N_r_, seed_, frac, lo_, n_global, opts=None):
+            assert (L_, K_, N_r_, seed_, lo_, n_global) == (L, K, N_r, seed, lo, n)
+            assert X_shard.shape[0] == hi - lo
+            sample = sh.sample()                  # global ids of the whole-dataset sample
+            mine = sample[(sample >= lo) & (sample < hi)] - lo
+            calls.append("sample")
+            return sh.P()[mine]
+
+        def breakpoints_from_samples(allp, N_r_, opts=None):
+            calls.append(("bp", allp.shape[0]))
+            allp = allp.numpy()
+            return np.stack([O.breakpoints_sort(allp[:, r], N_r_) for r in range(allp.shape[1])])
+
+        def build(X_shard, L_, K_, N_r_, seed_, opts=None, id_offset=0, n_global=None, breakpoints=None):
+            assert id_offset == lo and n_global == n
+            assert np.array_equal(breakpoints, sh.breakpoints())   # C1 result == the oracle shard's
+            calls.append("build")
+            return sh
+
+        ix = PD.sharded_build(X[lo:hi], lo, n, L, K, N_r, seed, opts=SimpleNamespace(sample_frac=0.01),
+                              build=build, sample_projections=sample_projections,
+                              breakpoints_from_samples=breakpoints_from_samples)
+        assert ix is sh and calls[0] == "sample" and calls[-1] == "build"
+        assert calls[1] == ("bp", O.sample_size(n, N_r, 0.01))     # every rank saw the whole sample
+        whole = O.Index(X, L, K, N_r, seed)
+        assert np.array_equal(sh.breakpoints(), whole.breakpoints())
         # C2: local top-k with global ids, all-gather, merge
-        ids, d, _ = sh.query(Q, 10, 1.5, 300.0, 0.1)
-        mi, md = PD.merge_shard_topk(ids, d, 10)
-        ri, rd = O.sharded_query(X, world, Q, 10, 1.5, 300.0, 0.1, 4, 16, 256, 42)
+        mi, md = PD.sharded_query(ix, Q, 10, 1.5, 300.0, 0.1,
+                                  merge=lambda gi, gd, k: O.merge_topk(gi.numpy(), gd.numpy(), k))
+        ri, rd = O.sharded_query(X, world, Q, 10, 1.5, 300.0, 0.1, L, K, N_r, seed)
         assert np.array_equal(mi, ri) and np.array_equal(md, rd)
         out_q.put((rank, "ok"))
     except Exception as e:  # pragma: no cover - reported to the parent

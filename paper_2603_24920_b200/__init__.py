@@ -5,6 +5,6 @@ package is the thin Python binding (``detlsh``) and the multi-GPU glue (``dist``
 """
 from .detlsh import (DetlshError, Index, MODE_CELL, MODE_EXACT, MODE_RELAXED, STATS_DTYPE, build, default_opts,  # noqa: F401
                      detlsh_breakpoints_from_samples, detlsh_build, detlsh_build_from_codes,
-                     detlsh_load, detlsh_merge_topk, detlsh_params, detlsh_query, detlsh_query_ex,
+                     detlsh_load, detlsh_merge_topk, detlsh_query_candidates, candidate_ids, detlsh_params, detlsh_query, detlsh_query_ex,
                      detlsh_sample_projections, detlsh_sample_size, launch_count, lib, profile_enable,
                      profile_filter, profile_read, profile_reset, release_workspace, workspace_bytes)

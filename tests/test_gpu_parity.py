@@ -112,15 +112,49 @@ def test_trees_duplicate_heavy_codes():
                 assert np.array_equal(t[key], o[key]), (alphabet, i, key)
 
 
-def test_end_to_end_leaves(gpu_tiny, tiny_oracle):
-    """Points whose leaf differs between GPU and oracle trees (0 when codes agree)."""
-    Cg, Co = gpu_tiny.codes(), tiny_oracle.codes()
-    for i in range(4):
-        if not np.array_equal(Cg[:, i * 16:(i + 1) * 16], Co[:, i * 16:(i + 1) * 16]):
-            continue
-        t, o = gpu_tiny.tree(i), tiny_oracle.tree(i)
-        for key in ("leaf_off", "perm", "lo", "hi"):
-            assert np.array_equal(t[key], o[key])
+def _point_boxes(t, n):
+    """Per point of one exported tree: its leaf's (prefix) box, lo and hi symbols side by side."""
+    off = np.asarray(t["leaf_off"], np.int64)
+    leaf_of = np.repeat(np.arange(len(off) - 1), np.diff(off))
+    box = np.empty((n, 2 * t["lo"].shape[1]), np.uint8)
+    box[np.asarray(t["perm"], np.int64)] = np.concatenate([t["lo"], t["hi"]], 1)[leaf_of]
+    return box
+
+
+def _first_key(codes_i, nb):
+    """First-layer node of each point (Alg. 2 l.2): the top bit of every dim's symbol."""
+    top = (codes_i.astype(np.int64) >> (nb - 1)) & 1
+    return (top << np.arange(codes_i.shape[1] - 1, -1, -1)).sum(1)
+
+
+def leaf_membership_report(g, o, n, L, K, N_r):
+    """Points whose leaf (prefix box) differs between the GPU's and the oracle's tree i, and the
+    check that every one of them sits in a first-layer subtree that holds a code mismatch (on
+    either side): identical codes in a first-layer node give an identical subtree (Alg. 2 is a
+    function of the node's id-ordered codes), so a near-breakpoint code flip can only reshape the
+    subtree it belongs to.  Returns (differing memberships, mismatched points) per tree."""
+    Cg, Co = g.codes(), o.codes()
+    nb = int(np.log2(N_r))
+    out = []
+    for i in range(L):
+        sl = slice(i * K, (i + 1) * K)
+        kg, ko = _first_key(Cg[:, sl], nb), _first_key(Co[:, sl], nb)
+        bad_pts = np.flatnonzero((Cg[:, sl] != Co[:, sl]).any(1))
+        tainted = set(kg[bad_pts].tolist()) | set(ko[bad_pts].tolist())
+        diff = np.flatnonzero((_point_boxes(g.tree(i), n) != _point_boxes(o.tree(i), n)).any(1))
+        unexplained = [p for p in diff if ko[p] not in tainted and kg[p] not in tainted]
+        assert not unexplained, (i, unexplained[:10])
+        out.append((len(diff), len(bad_pts)))
+    return out
+
+
+def test_end_to_end_leaves(gpu_tiny, tiny_oracle, tiny):
+    """B5/B6 end to end (each side from its own codes): leaf memberships are identical except in
+    first-layer subtrees holding a near-breakpoint code mismatch; the differing count is reported."""
+    c = tiny["cfg"]
+    rep = leaf_membership_report(gpu_tiny, tiny_oracle, c.n, c.L, c.K, c.N_r)
+    print("differing leaf memberships / mismatched points per tree:", rep)
+    assert sum(d for d, _ in rep) <= 0.05 * c.n * c.L
 
 
 # ------------------------------------------------------------------ Q0-Q8
@@ -194,16 +228,21 @@ def test_ragged_shapes_parity(n, d, L, K, N_r, ms):
     assert np.array_equal(g.A(), o.A())
     assert np.array_equal(g.sample(), o.sample())
     Cg, Co = g.codes(), o.codes()
-    assert np.mean(Cg != Co) <= 1e-3
+    Po, Bo = o.P(), o.breakpoints()
+    norms = np.linalg.norm(X.astype(np.float64), axis=1)
+    bad = np.argwhere(Cg != Co)
+    for p, r in bad:            # north_star: every mismatch within 1e-5 of the separating breakpoint
+        tol = 1e-5 * max(abs(float(Po[p, r])), norms[p])
+        assert _code_mismatch_ok(float(Po[p, r]), int(Cg[p, r]), int(Co[p, r]), Bo[r], tol), (p, r)
+    assert len(bad) <= 1e-3 * Cg.size
+    leaf_membership_report(g, o, n, L, K, N_r)
     rmin = max(o.estimate_rmin(Q[:6], 5, 1.5, 0.1), 1e-3)   # r* can be 0 with N_r = 2
     ig, dg = g.query(Q, 5, 1.5, rmin, 0.1)
     io, do, _ = o.query(Q, 5, 1.5, rmin, 0.1)
-    assert _recall(ig, io) >= 0.95
-    if np.array_equal(Cg, Co):
-        for i in range(L):
-            t, ot = g.tree(i), o.tree(i)
-            for key in ("leaf_off", "perm", "lo", "hi", "bits"):
-                assert np.array_equal(t[key], ot[key])
+    print(f"ragged n={n} d={d} L={L} K={K} N_r={N_r}: recall vs oracle {_recall(ig, io):.4f}, "
+          f"code mismatches {len(bad)}")
+    assert _recall(ig, io) >= 0.99
+    _dist_match(ig, dg, io, do)
 
 
 def test_device_buffers_and_determinism(tiny, gpu_tiny, tiny_rmin):
@@ -587,3 +626,139 @@ def test_filter_switches_do_not_change_results(tmp_path):
     for name in runs:
         for key in res["default"].files:
             assert np.array_equal(res[name][key], res["default"][key]), (name, key)
+
+
+# ------------------------------------------------------------------ candidate set S, element by element
+def _bits_to_bool(S_row, n):
+    return np.unpackbits(np.ascontiguousarray(S_row).view(np.uint8), bitorder="little")[:n].astype(bool)
+
+
+def candidate_set_report(g, o, X, Q, k, c, r, beta, mode, L, K, N_r, rel=1e-5):
+    """S of Alg. 5 (the union of line 6) at termination, per query, element by element.
+
+    (1) GPU kernel vs its own ingredients: the exported S must equal the set the method defines
+        from the GPU's codes, breakpoints and projected query at the GPU's stop (round, tree):
+        CELL = union of per-point cell-bound tests, RELAXED = union of whole leaves whose prefix
+        box bound is <= rho (tests/_alg5_ref.py, fp64).  Only points whose bound lies within
+        `rel` (relative) of rho^2 may differ (fp32 LUT sums) -- counted.
+    (2) GPU vs oracle: where the stops agree, S against the union of the oracle's own range
+        queries (orc_range_query) over the same (tree, radius) pairs -- differences counted;
+        they come from near-breakpoint codes and the fp32 query projection.
+    Returns a dict of counts."""
+    from _alg5_ref import Space, box_lb2, radii, relaxed_range
+    n = X.shape[0]
+    ig, dg, sg, S = P.detlsh_query_candidates(g, Q, k, c, r, beta, opts=P.default_opts(mode=mode))
+    io, do, so = o.query(Q, k, c, r, beta, mode=mode)
+    eps = P.detlsh_params(K, L, c)["eps"]
+    assert abs(eps - o.eps) <= 1e-12 * o.eps
+    Bg, Cg = g.breakpoints(), g.codes()
+    spg = Space(Bg, Cg, K, N_r)
+    qpg = g.project(Q)
+    trees_g = [g.tree(i) for i in range(L)] if mode == P.MODE_RELAXED else None
+    rep = {"queries": len(Q), "kernel_flips": 0, "S_total": 0, "stop_match": 0, "oracle_diff": 0,
+           "oracle_S_total": 0}
+    for q in range(len(Q)):
+        inS = _bits_to_bool(S[q], n)
+        assert inS.sum() == sg["n_cand"][q]
+        rs = radii(r, c, int(sg["rounds"][q]))
+        pairs = [(i, rs[-1]) for i in range(int(sg["trees_last"][q]))]
+        if len(rs) >= 2:
+            pairs += [(i, rs[-2]) for i in range(int(sg["trees_last"][q]), L)]
+        model = np.zeros(n, bool)
+        border = np.zeros(n, bool)
+        for i, rr in pairs:
+            rho2 = (eps * rr) ** 2
+            sl = slice(i * K, (i + 1) * K)
+            if mode == P.MODE_RELAXED:
+                t = trees_g[i]
+                lb = box_lb2(spg.B[sl], t["lo"], t["hi"], qpg[q][sl], N_r)
+                off = np.asarray(t["leaf_off"], np.int64)
+                lbp = np.empty(n)
+                lbp[np.asarray(t["perm"], np.int64)] = np.repeat(lb, np.diff(off))
+            else:
+                lbp = spg.cell2(i, qpg[q])
+            model |= lbp <= rho2
+            border |= np.abs(lbp - rho2) <= rel * rho2
+        flips = np.flatnonzero(inS != model)
+        assert np.all(border[flips]), (q, flips[~border[flips]][:10])
+        rep["kernel_flips"] += len(flips)
+        rep["S_total"] += int(inS.sum())
+        # (2) against the oracle's own range queries at the oracle's stop, where the stops agree
+        if (sg["rounds"][q], sg["trees_last"][q], sg["reason"][q]) == (so["rounds"][q], so["trees_last"][q], so["reason"][q]):
+            rep["stop_match"] += 1
+            qpo = o.project_query(Q[q])
+            ref = np.zeros(n, bool)
+            for i, rr in pairs:
+                sl = slice(i * K, (i + 1) * K)
+                ref[o.range_query(i, qpo[sl], eps * rr, mode)] = True
+            if mode == P.MODE_RELAXED and q < 3:   # the oracle's RELAXED == the brute force (f1 pin)
+                for i, rr in pairs[:1]:
+                    sl = slice(i * K, (i + 1) * K)
+                    assert np.array_equal(o.range_query(i, qpo[sl], eps * rr, mode),
+                                          relaxed_range(o.tree(i), o.breakpoints()[sl], qpo[sl], eps * rr, N_r))
+            rep["oracle_diff"] += int((inS != ref).sum())
+            rep["oracle_S_total"] += int(ref.sum())
+    return rep
+
+
+@pytest.mark.parametrize("m", [0, 2])
+@pytest.mark.parametrize("mode", [P.MODE_CELL, P.MODE_RELAXED])
+def test_candidate_set_elementwise_tiny(gpu_tiny, tiny_oracle, tiny, tiny_rmin, mode, m):
+    """The candidate set S itself (not only |S| or the top-k): at the AMB-22 r_min and at
+    r_min c^-2 (several rounds), CELL and RELAXED."""
+    c = tiny["cfg"]
+    r = tiny_rmin * c.c ** (-m)
+    rep = candidate_set_report(gpu_tiny, tiny_oracle, tiny["X"], tiny["Q"], c.k, c.c, r, c.beta, mode, c.L, c.K, c.N_r)
+    print(f"mode {mode} m {m}: {rep}")
+    assert rep["kernel_flips"] <= 1e-4 * rep["S_total"] + 2
+    assert rep["stop_match"] >= 0.9 * rep["queries"]
+    assert rep["oracle_diff"] <= 2e-3 * rep["oracle_S_total"] + 2
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("cid,nsel", [(2, 12), (4, 6)])
+def test_candidate_set_elementwise_full_size(cid, nsel):
+    """S element by element at full size (configs[1]: 1M x 256; configs[3]: 10M x 128) on sampled
+    queries, at both bench radii (the AMB-22 r_min and r_bench), plus the stop (reason, round,
+    tree) and |S| agreement with the oracle."""
+    D = datagen.generate(cid)
+    c = D["cfg"]
+    g = P.detlsh_build(D["X"], c.L, c.K, c.N_r, c.index_seed)
+    o = O.Index(D["X"], c.L, c.K, c.N_r, c.index_seed)
+    sel = np.sort(np.random.default_rng(9).choice(c.nq, nsel, replace=False))
+    for r in _bench_radii(cid):
+        rep = candidate_set_report(g, o, D["X"], D["Q"][sel], c.k, c.c, r, c.beta, P.MODE_CELL, c.L, c.K, c.N_r)
+        print(f"cfg{cid} r={r:.4g}: {rep}")
+        assert rep["kernel_flips"] <= 1e-4 * rep["S_total"] + 2
+        assert rep["stop_match"] >= 0.8 * rep["queries"]
+        assert rep["oracle_diff"] <= 2e-3 * rep["oracle_S_total"] + 2
+
+
+@pytest.mark.parametrize("G,nq,k", [(1, 3, 4), (3, 50, 7), (8, 33, 100)])
+def test_merge_topk_device_tensors(G, nq, k):
+    """C2 merge on device tensors (the path dist.merge_shard_topk takes after the NCCL
+    all-gather): equal distances across shards (ties by id), empty tails, output stays on the GPU."""
+    import torch
+    rng = np.random.default_rng(G * 1000 + k)
+    ids = np.full((G, nq, k), -1, np.int64)
+    d = np.full((G, nq, k), np.inf, np.float32)
+    pool = rng.permutation(G * nq * k * 2)
+    t = 0
+    for g in range(G):
+        for q in range(nq):
+            m = int(rng.integers(0, k + 1))
+            dd = rng.integers(0, 6, m).astype(np.float32)          # many equal distances
+            ii = pool[t:t + m]
+            t += m
+            o = np.lexsort((ii, dd))
+            ids[g, q, :m], d[g, q, :m] = ii[o], dd[o]
+    oi, od = P.detlsh_merge_topk(torch.from_numpy(ids).cuda(), torch.from_numpy(d).cuda(), k)
+    assert oi.is_cuda and od.is_cuda
+    oi, od = oi.cpu().numpy(), od.cpu().numpy()
+    for q in range(nq):
+        pairs = sorted((float(d[g, q, e]), int(ids[g, q, e])) for g in range(G) for e in range(k) if ids[g, q, e] >= 0)[:k]
+        pairs += [(np.inf, -1)] * (k - len(pairs))
+        assert oi[q].tolist() == [p[1] for p in pairs]
+        assert od[q].tolist() == [p[0] for p in pairs]
+    ri, rd = O.merge_topk(ids, d, k)
+    assert np.array_equal(oi, ri) and np.array_equal(od, rd)

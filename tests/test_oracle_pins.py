@@ -608,3 +608,72 @@ def test_lb_order_truncation_pins():
     a = o.query(Q, 5, 1.5, 30.0, 2.0, lb_order=True)
     b = o.query(Q, 5, 1.5, 30.0, 2.0)
     assert np.array_equal(a[0], b[0]) and np.array_equal(a[2]["n_cand"], b[2]["n_cand"])
+
+
+# ----------------------------------------------------------------- RELAXED (f1) and the Alg. 5 driver,
+# pinned against tests/_alg5_ref.py (numpy brute force; shares nothing with the oracle's traversal)
+def test_tree_boxes_are_prefix_boxes(tiny_oracle):
+    """Every exported leaf box is the Alg. 2 prefix box of its members: per dim the
+    members share the top `bits` bits and [lo, hi] is exactly that prefix's symbol range."""
+    ix = tiny_oracle
+    nb = int(math.log2(ix.N_r))
+    codes = ix.codes().astype(np.int64)
+    for i in range(ix.L):
+        t = ix.tree(i)
+        c = codes[:, i * ix.K:(i + 1) * ix.K]
+        bits = t["bits"].astype(np.int64)
+        assert np.all(bits <= nb)
+        leaf_of = np.repeat(np.arange(len(t["leaf_off"]) - 1), np.diff(t["leaf_off"]))
+        mem = c[t["perm"]]
+        shift = nb - bits[leaf_of]
+        pre = (mem >> shift) << shift
+        assert np.array_equal(pre, t["lo"][leaf_of].astype(np.int64))
+        assert np.array_equal(t["hi"].astype(np.int64), t["lo"].astype(np.int64) + (1 << (nb - bits)) - 1)
+        assert np.array_equal(np.sort(t["perm"]), np.arange(ix.n))          # each point in one leaf
+
+
+def test_relaxed_range_query_brute_force(tiny_oracle, tiny):
+    """Sec. 6.2.2(1): RELAXED returns exactly the points of the leaves whose box
+    lower bound is <= rho -- brute force over the exported leaves, numpy bounds (not O6)."""
+    from _alg5_ref import relaxed_range
+    ix = tiny_oracle
+    B = ix.breakpoints()
+    rng = np.random.default_rng(17)
+    trees = [ix.tree(i) for i in range(ix.L)]
+    hit_partial = 0
+    for it in range(48):
+        qp = ix.project_query(tiny["Q"][it % 100])
+        i = it % ix.L
+        sl = slice(i * ix.K, (i + 1) * ix.K)
+        rho = float(rng.uniform(0.05, 1.2)) * ix.eps * 100.0
+        got = ix.range_query(i, qp[sl], rho, O.RELAXED)
+        ref = relaxed_range(trees[i], B[sl], qp[sl], rho, ix.N_r)
+        assert np.array_equal(got, ref), (it, len(got), len(ref))
+        cell = ix.range_query(i, qp[sl], rho, O.CELL)
+        hit_partial += len(ref) > len(cell)
+    assert hit_partial >= 10     # radii where RELAXED really takes more than CELL
+
+
+@pytest.mark.parametrize("m", [0, 3])
+def test_driver_equals_tree_granular_rederivation(tiny_oracle, tiny, m):
+    """Alg. 5 re-run in numpy tree by tree: budget |S| >= ceil(beta n)+k tested after
+    EACH tree (line 7), radius test after the round (line 9), r <- c r (line 11).  The
+    oracle's stop (reason, round, tree), |S| and top-k must equal it for every query."""
+    from _alg5_ref import Space, alg5
+    ix = tiny_oracle
+    c = tiny["cfg"]
+    rmin = ix.estimate_rmin(tiny["Qs"], c.k, c.c, c.beta) * c.c ** (-m)
+    Q = tiny["Q"][:40]
+    ids, dists, st = ix.query(Q, c.k, c.c, rmin, c.beta)
+    sp = Space(ix.breakpoints(), ix.codes(), ix.K, ix.N_r)
+    mid_round = 0
+    for q in range(len(Q)):
+        ref = alg5(sp, ix.eps, tiny["X"], Q[q], ix.project_query(Q[q]), c.k, c.c, rmin, c.beta, ix.n)
+        got = (int(st["reason"][q]), int(st["rounds"][q]), int(st["trees_last"][q]), int(st["n_cand"][q]))
+        assert got == (ref["reason"], ref["rounds"], ref["trees_last"], ref["n_cand"]), (q, got, ref["reason"])
+        assert st["r_final"][q] == ref["r_final"]
+        assert np.array_equal(ids[q], ref["ids"])
+        assert np.array_equal(dists[q], np.sqrt(ref["d2"]).astype(np.float32))
+        mid_round += ref["reason"] == 0 and ref["trees_last"] < ix.L
+    if m == 0:
+        assert mid_round >= 5    # budget stops inside a round exercise the after-each-tree rule

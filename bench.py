@@ -3,14 +3,19 @@
 
 A step = one pass of the whole hot path over one batch of synthetic input:
 detlsh_build over the configuration's n points (B0-B6) + detlsh_query of its nq queries
-(Q0-Q8).  Inputs are device-resident before the timed region (X = 1.02 GB > L2, so no
-L2 flush is needed); timing uses CUDA events on the library's stream, max over ranks.
+(Q0-Q8).  Inputs are device-resident before the timed region (X >> L2, so no L2 flush is
+needed); timing uses CUDA events on the library's stream, max over ranks.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--impl reference]
+Default workload: configs[4] (n = 100M, d = 96, L = 6, beta = 0.05, 10,000 queries) -- the
+largest BASELINE configuration, which fits one B200 (38.4 GB of data); `--config 2` selects
+configs[1] (1M x 256), `--config 4` configs[3] (10M x 128).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 5] [--impl reference]
 
 N > 1 runs under torchrun: points are sharded (strong scaling of the fixed config),
 breakpoints are global (C1 all-gather), every rank answers every query with its
-per-shard budget and the local top-k lists are all-gathered and merged (C2).
+per-shard budget and the local top-k lists are all-gathered (NCCL) and merged on the
+device (C2, k_merge_topk).
 """
 from __future__ import annotations
 
@@ -60,27 +65,76 @@ def c_index(c) -> int:
     return -1
 
 
-# ---------------------------------------------------------------- ground truth (harness)
-def exact_knn_sample(X: np.ndarray, Q: np.ndarray, k: int, sel: np.ndarray) -> np.ndarray:
-    """Exact kNN ids for Q[sel]: fp32 BLAS screening, fp64 re-rank, ties by id."""
-    norms = np.einsum("ij,ij->i", X, X, dtype=np.float64)
-    out = np.empty((len(sel), k), np.int64)
+# ---------------------------------------------------------------- ground truth and quality (harness)
+def exact_knn_sample(Xd, X: np.ndarray, Q: np.ndarray, k: int, sel: np.ndarray):
+    """Exact kNN of Q[sel] (harness, not the library): fp32 screening with torch on the GPU over
+    the device-resident data (chunks of 8M rows, TF32 off), the k + 64 best of each chunk
+    re-ranked in fp64 on the host, ties by id.  Returns (ids, dists) [len(sel)][k]."""
+    import torch
+    torch.backends.cuda.matmul.allow_tf32 = False
     extra = k + 64
-    for s in range(0, len(sel), 50):
-        qs = Q[sel[s:s + 50]]
-        approx = norms[None, :] - 2.0 * (qs @ X.T).astype(np.float64)
-        cand = np.argpartition(approx, extra, axis=1)[:, :extra]
-        for r in range(len(qs)):
-            cid = cand[r]
-            d2 = ((X[cid].astype(np.float64) - qs[r].astype(np.float64)) ** 2).sum(1)
-            order = np.lexsort((cid, d2))[:k]
-            out[s + r] = cid[order]
-    return out
+    dev = Xd.device if Xd is not None else torch.device("cuda")
+    qs = torch.from_numpy(np.ascontiguousarray(Q[sel])).to(dev)
+    n = X.shape[0]
+    cands = []
+    for s0 in range(0, n, 1 << 23):
+        # the device copy when it holds every row (N = 1), else host blocks streamed in
+        blk = Xd[s0:s0 + (1 << 23), :Q.shape[1]] if Xd is not None else torch.from_numpy(X[s0:s0 + (1 << 23)]).to(dev)
+        d2 = (blk * blk).sum(1)[None, :] - 2.0 * (qs @ blk.T)
+        kk = min(extra, blk.shape[0])
+        cands.append((torch.topk(d2, kk, dim=1, largest=False).indices + s0).cpu())
+    cand = torch.cat(cands, 1).numpy()
+    ids = np.empty((len(sel), k), np.int64)
+    dists = np.empty((len(sel), k), np.float64)
+    for r in range(len(sel)):
+        cid = np.unique(cand[r])
+        d2 = ((X[cid].astype(np.float64) - Q[sel[r]].astype(np.float64)) ** 2).sum(1)
+        o = np.lexsort((cid, d2))[:k]
+        ids[r], dists[r] = cid[o], np.sqrt(d2[o])
+    return ids, dists
 
 
 def recall(ids: np.ndarray, gt: np.ndarray) -> float:
     k = gt.shape[1]
     return float(np.mean([len(set(ids[i].tolist()) & set(gt[i].tolist())) / k for i in range(len(gt))]))
+
+
+def quality(ids, dists, gt_ids, gt_d, c2):
+    """BASELINE.md 3 quality next to the throughput: recall@k vs exact kNN, the overall
+    ratio mean_i ||q,o_i|| / ||q,o_i*||, and the c^2-k-ANN success rate of Theorem 2
+    (every returned o_i within c^2 ||q, o_i*||)."""
+    d = dists.astype(np.float64)
+    ok = np.all(d <= c2 * gt_d * (1 + 1e-6), axis=1)
+    pos = gt_d > 0
+    ratio = np.where(pos, d / np.where(pos, gt_d, 1.0), 1.0).mean(1)
+    return {"recall_at_k": recall(ids, gt_ids), "overall_ratio": float(ratio.mean()),
+            "c2_success_rate": float(ok.mean()), "theorem2_bound": 0.5 - 1 / np.e, "queries": int(len(gt_ids))}
+
+
+def oracle_agreement(cid: int, ids: np.ndarray, dists: np.ndarray, radius: str):
+    """GPU top-k vs the ORACLE's own answers where the repo holds them for this workload
+    (tests/golden/cfg5_oracle.npz: configs[4], the seeded 200-query subset, written by the
+    oracle-only tools/make_cfg5_golden.py): recall vs the oracle's ids and the largest relative
+    distance difference on common ids."""
+    path = os.path.join(ROOT, "tests", "golden", "cfg5_oracle.npz")
+    if cid != 5 or not os.path.exists(path):
+        return None
+    z = np.load(path)
+    sel = z["sel"]
+    key = "rbench" if radius == "bench" and "rbench_ids" in z.files else "rmin"
+    if radius == "bench" and key != "rbench" and int(z["bench_m"]) != 0:
+        return None
+    oi, od = z[f"{key}_ids"], z[f"{key}_dists"]
+    sel = sel[:len(oi)]
+    gi, gd = ids[sel], dists[sel]
+    worst = 0.0
+    for q in range(len(sel)):
+        m = {int(i): float(v) for i, v in zip(oi[q], od[q])}
+        for i, v in zip(gi[q], gd[q]):
+            if int(i) in m and m[int(i)] > 0:
+                worst = max(worst, abs(float(v) - m[int(i)]) / m[int(i)])
+    return {"recall_vs_oracle": recall(gi, oi), "max_rel_dist_diff": worst, "queries": int(len(sel)),
+            "source": "tests/golden/cfg5_oracle.npz (oracle-only, seed 2005 subset)"}
 
 
 # ---------------------------------------------------------------- clocks sampler
@@ -167,6 +221,17 @@ def kernel_models(c, steps: int, st, n_local: int, nq: int, ld: int):
     }
 
 
+def build_roofline(c, n_local: int, pts_per_s: float, hbm: float) -> dict:
+    """Whole-build roofline (SURVEY 8(d) "Build total"): ~4d + 9 L K + 100 L bytes per point
+    (X read once by the projection, codes written and re-read by the sort / split / gathers,
+    ~100 B per point per tree of key-value sort traffic)."""
+    bpp = 4 * c.d + 9 * c.L * c.K + 100 * c.L
+    ach = pts_per_s * bpp / 1e9
+    return {"bound": "hbm", "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s", "frac": round(ach / hbm, 4),
+            "bytes_per_point": bpp, "points": n_local,
+            "model": "4d + 9LK + 100L B per point (SURVEY 8(d) Build total) x points/s"}
+
+
 FILTER_UNIT = "filter"                       # k_range_filter + k_leaf_points (one unit of work: Alg. 3)
 FILTER_KERNELS = ("k_range_filter", "k_leaf_points")
 
@@ -242,13 +307,37 @@ def datagen_ns(c, n):
 
 
 # ---------------------------------------------------------------- reference arm (the oracle)
+ORACLE_FULL_MAX = 2_000_000      # configs up to this n: the oracle indexes all points
+ORACLE_SAMPLE_N = 1_000_000      # larger configs: the oracle indexes this prefix of the data (a bounded sample)
+_ORC = {}                        # forked oracle workers inherit the index
+
+
+def oracle_points(cfg) -> int:
+    return cfg.n if cfg.n <= ORACLE_FULL_MAX else ORACLE_SAMPLE_N
+
+
+def oracle_sample_desc(cfg, n_o: int) -> str:
+    if n_o == cfg.n:
+        return f"oracle (single-thread fp64 C) index over all {cfg.n:,} points"
+    return (f"oracle (single-thread fp64 C) index over the first {n_o:,} of the {cfg.n:,} points "
+            f"(a bounded sample: its per-query work and budget beta n + k are those of a {n_o:,}-point index)")
+
+
+def _orc_query_one(i):
+    c = _ORC["cfg"]
+    t = time.perf_counter()
+    _ORC["ix"].query(_ORC["Q"][i:i + 1], c.k, c.c, _ORC["r"], c.beta)
+    return time.perf_counter() - t
+
+
 def run_reference(args, cfg):
     from oracle import oracle as O
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     r_min = load_rmin(args.config, args.radius)
-    D = datagen.generate(cfg)
+    n_o = oracle_points(cfg)
+    D = datagen.generate(cfg, n=n_o)
     X, Q = D["X"], D["Q"]
     t0 = time.perf_counter()
     ix = O.Index(X, cfg.L, cfg.K, cfg.N_r, cfg.index_seed, cfg.max_size, cfg.sample_frac)
@@ -268,24 +357,39 @@ def run_reference(args, cfg):
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": {"workload": workload_desc(cfg), "r_min": r_min, **rmin_info(args.config)},
             "cpu_baseline": {"value": qps, "unit": "queries/s", "cores": 1, "kind": "oracle",
-                             "sample": f"{per_step} random queries of the {cfg.nq} per step, index built once "
-                                       f"(oracle build {cfg.n / build_s:.0f} points/s, 1 core)"},
+                             "sample": f"{oracle_sample_desc(cfg, n_o)}; {per_step} random queries of the {cfg.nq} "
+                                       f"per step (oracle build {n_o / build_s:.0f} points/s, 1 core)"},
             "e2e": {"value": qps, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
-def cpu_baseline(cfg, X, Q, r_min, nqs: int) -> dict:
+def cpu_baseline(cfg, Q, r, nqs: int) -> dict:
+    """The oracle as it stands on the box's host cores, on a bounded sample of the workload:
+    build points/s on 1 core; queries/s on 1 core and with P = nproc forked processes answering
+    disjoint queries of the same index ("oracle x P cores")."""
+    import multiprocessing as mp
     from oracle import oracle as O
+    n_o = oracle_points(cfg)
+    Xo = datagen.generate(cfg, n=n_o, nq=1)["X"]
     t0 = time.perf_counter()
-    ix = O.Index(X, cfg.L, cfg.K, cfg.N_r, cfg.index_seed, cfg.max_size, cfg.sample_frac)
+    ix = O.Index(Xo, cfg.L, cfg.K, cfg.N_r, cfg.index_seed, cfg.max_size, cfg.sample_frac)
     tb = time.perf_counter() - t0
     sel = np.random.default_rng(1).choice(cfg.nq, nqs, replace=False)
+    _ORC.update(ix=ix, Q=Q, cfg=cfg, r=r)
+    t1 = [_orc_query_one(int(i)) for i in sel]
+    P = os.cpu_count() or 1
+    sel_p = np.random.default_rng(3).choice(cfg.nq, min(cfg.nq, 2 * P), replace=False)
     t0 = time.perf_counter()
-    ix.query(Q[sel], cfg.k, cfg.c, r_min, cfg.beta)
-    tq = time.perf_counter() - t0
-    return {"value": nqs / tq, "unit": "queries/s", "cores": 1, "kind": "oracle",
-            "sample": f"oracle (single-thread fp64 C) full index build of all {cfg.n:,} points + {nqs} of the "
-                      f"{cfg.nq} queries", "build_points_per_s": cfg.n / tb, "seconds": tb + tq}
+    with mp.get_context("fork").Pool(P) as pool:
+        pool.map(_orc_query_one, [int(i) for i in sel_p], chunksize=1)
+    wall = time.perf_counter() - t0
+    _ORC.clear()
+    return {"value": nqs / sum(t1), "unit": "queries/s", "cores": 1, "kind": "oracle",
+            "sample": f"{oracle_sample_desc(cfg, n_o)}; {nqs} of the {cfg.nq} queries at the bench radius",
+            "build_points_per_s": n_o / tb, "seconds": tb + sum(t1) + wall,
+            "oracle_x_P_cores": {"value": len(sel_p) / wall, "unit": "queries/s", "cores": P,
+                                 "how": f"{P} forked oracle processes answering {len(sel_p)} disjoint queries "
+                                        "of the same index (embarrassingly parallel, no code change)"}}
 
 
 # ---------------------------------------------------------------- our arm
@@ -294,7 +398,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--config", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--ref-queries", type=int, default=4)
     ap.add_argument("--cpu-queries", type=int, default=16)
@@ -353,7 +457,7 @@ def main():
         if world > 1:
             ids, dists = PD.merge_shard_topk(ids, dists, cfg.k)
         e2.record(stream)
-        results["ids"], results["stats"] = ids, st
+        results["ids"], results["dists"], results["stats"] = ids, dists, st
         idx.free()
         return e0, e1, e2
 
@@ -417,11 +521,14 @@ def main():
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
 
     if rank == 0:
-        ids = results["ids"]
+        ids, dists = results["ids"], results["dists"]
         ids = ids.cpu().numpy() if torch.is_tensor(ids) else ids
+        dists = dists.cpu().numpy() if torch.is_tensor(dists) else dists
         sel = np.random.default_rng(2).choice(cfg.nq, min(args.recall_queries, cfg.nq), replace=False)
-        gt = exact_knn_sample(X, Q, cfg.k, sel)
-        rec = recall(ids[sel], gt)
+        gt, gt_d = exact_knn_sample(Xd if world == 1 else None, X, Q, cfg.k, sel)
+        qual = quality(ids[sel], dists[sel], gt, gt_d, cfg.c ** 2)
+        rec = qual["recall_at_k"]
+        agree = oracle_agreement(args.config, ids, dists, args.radius)
         hbm, bf16, bf16s, peak_src = peaks()
         kern = {k: {"launches": v[0], "ms": round(v[1], 4)} for k, v in sorted(prof.items(), key=lambda kv: -kv[1][1])}
         kern.update({k: {"launches": v[0], "ms": round(v[1] * args.steps, 4), "from": "one extra untimed step, x steps"}
@@ -462,11 +569,13 @@ def main():
             "data": "synthetic",
             "config": {"workload": workload_desc(cfg), "n": cfg.n, "d": cfg.d, "nq": cfg.nq, "k": cfg.k,
                        "r_min": r_min, **rmin_info(args.config), "parallelism": f"point-sharded x{world}",
-                       "l2": "no flush: X (1.02 GB at configs[1]) and the rebuilt index exceed L2 (126 MB)",
+                       "l2": f"no flush: X ({X.nbytes / 1e9:.2f} GB) and the rebuilt index exceed L2 (126 MB)",
                        "proj_impl": int(opts.proj_impl)},
             "recall_at_k": rec, "recall_queries": int(len(sel)),
+            "quality": qual, "vs_oracle": agree,
             "query_ms_per_step": query_ms / args.steps,
-            "build": {"points_per_s": cfg.n * args.steps / (build_ms / 1e3), "ms_per_step": build_ms / args.steps},
+            "build": {"points_per_s": cfg.n * args.steps / (build_ms / 1e3), "ms_per_step": build_ms / args.steps,
+                      "roofline": build_roofline(cfg, n_local, cfg.n * args.steps / (build_ms / 1e3) / world, hbm)},
             "candidates_per_query": float(st["n_cand"].mean()),
             "stop_reasons": np.bincount(st["reason"], minlength=3).tolist(),
             "filter_counts_per_query": {k_: float(st[k_].mean()) for k_ in
@@ -480,7 +589,7 @@ def main():
             "gpu_launches": int(launches), "clocks": clocks, "kernels": kern,
         }
         if world == 1 and not args.no_cpu_baseline:
-            line["cpu_baseline"] = cpu_baseline(cfg, X, Q, r_min, args.cpu_queries)
+            line["cpu_baseline"] = cpu_baseline(cfg, Q, r_min, args.cpu_queries)
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

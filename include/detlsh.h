@@ -167,8 +167,11 @@ detlsh_status detlsh_rc_ann(const detlsh_index* idx, const float* queries, int64
  * device), r*_q = the smallest radius whose full round (all L range queries) gives
  * |S| >= min(n, ceil(beta n) + k) -- i.e. sqrt of the B-th smallest over points of
  * min_i cellLB_i(p), divided by eps.  Writes r*_q to rstar (host, nullable) and the lower
- * median to *r_min (host).  Errors (EINVAL): NULL idx/queries/r_min; ns < 1; k < 1 or k > n;
- * beta <= 0.
+ * median to *r_min (host).  Sample queries are processed in chunks sized from free device
+ * memory (ns * n * 4 bytes are never needed at once).  Errors (EINVAL): NULL idx/queries/r_min;
+ * ns < 1; k < 1 or k > n; beta <= 0; a median of 0 (more than B points share the sample
+ * queries' own cells in every tree -- e.g. very few regions): rstar and *r_min are still
+ * written, but 0 is not a valid r_min for detlsh_query, so the caller must choose one.
  */
 detlsh_status detlsh_estimate_rmin(const detlsh_index* idx, const float* queries, int64_t ns, int32_t k,
                                    double beta, const detlsh_opts* opts, double* rstar, double* r_min);

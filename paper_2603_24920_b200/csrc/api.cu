@@ -337,6 +337,8 @@ detlsh_status detlsh_estimate_rmin(const detlsh_index* idx, const float* queries
         std::vector<double> sorted = rs;
         std::sort(sorted.begin(), sorted.end());
         *r_min = sorted[(size_t)(ns - 1) / 2];      // lower median (AMB-22)
+        DL_REQUIRE(*r_min > 0.0, "estimated r_min is 0 (more than beta n + k points share the sample queries' "
+                                 "cells in every tree); choose a positive r_min");
     });
 }
 

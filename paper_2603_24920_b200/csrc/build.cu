@@ -10,6 +10,7 @@
 //     a node with more than max_size points splits on the dimension whose next bit most
 //     evenly divides its first max_size points (ascending id); children are the stable
 //     partition.  Level-synchronous over all L trees at once.
+#include <cstring>
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
@@ -930,8 +931,9 @@ __global__ void k_leaf_tight_sb(const uint32_t* __restrict__ sb_off, int64_t nl,
 
 // Box of each query tile: per dim the smallest lo and largest hi over its leaves (the union's
 // bounding box, so its lower bound never exceeds a member leaf's -- the filter skips whole tiles).
-__global__ void k_tile_boxes(const uint32_t* __restrict__ tile_leaf, int64_t ntiles, int K, const uint8_t* __restrict__ lo,
+__global__ void k_tile_boxes(const uint32_t* __restrict__ tile_leaf, const uint32_t* __restrict__ ntiles_p, int K, const uint8_t* __restrict__ lo,
                              const uint8_t* __restrict__ hi, uint8_t* __restrict__ tlo, uint8_t* __restrict__ thi) {
+    const int64_t ntiles = *ntiles_p;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < ntiles * K;
          i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t t = i / K;
@@ -957,8 +959,9 @@ __global__ void k_tile_write(const uint32_t* __restrict__ flags, const uint32_t*
 // warp per tile: lane l holds the start of the tile's leaf l; each point's leaf slot by a
 // 5-step shuffle search, written coalesced
 __global__ void k_point_tile_leaf(const uint32_t* __restrict__ leaf_off, const uint32_t* __restrict__ tile_leaf,
-                                  int64_t ntiles, int64_t nl, uint16_t* __restrict__ ptl) {
+                                  const uint32_t* __restrict__ ntiles_p, int64_t nl, uint16_t* __restrict__ ptl) {
     const int lane = threadIdx.x & 31;
+    const int64_t ntiles = *ntiles_p;
     for (int64_t t = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; t < ntiles;
          t += ((int64_t)gridDim.x * blockDim.x) >> 5) {
         const uint32_t lb = tile_leaf[t], le = tile_leaf[t + 1];
@@ -979,11 +982,18 @@ __global__ void k_point_tile_leaf(const uint32_t* __restrict__ leaf_off, const u
     (void)nl;
 }
 
+// tile_begin[t] = first tile of tree t (tile_begin[L] = ntiles), and the tile list's end marker
+// tile_leaf[ntiles] = nl -- all from device counts (no host round trip)
 __global__ void k_tree_tiles(const uint32_t* __restrict__ idx, const unsigned long long* __restrict__ leaf_begin,
-                             int L, uint32_t ntiles, unsigned long long* __restrict__ tile_begin) {
+                             int L, const uint32_t* __restrict__ ntiles_p, uint32_t nl, uint32_t* __restrict__ tile_leaf,
+                             unsigned long long* __restrict__ tile_begin) {
     const int t = threadIdx.x;
-    if (t < L) tile_begin[t] = idx[leaf_begin[t]];
-    if (t == L) tile_begin[t] = ntiles;
+    const uint32_t ntiles = *ntiles_p;
+    if (t < L) tile_begin[t] = leaf_begin[t] < nl ? idx[leaf_begin[t]] : ntiles;
+    if (t == L) {
+        tile_begin[t] = ntiles;
+        tile_leaf[ntiles] = nl;
+    }
 }
 
 // ||x||^2 of every row, warp per row (used when the projection ran on the CUDA cores).
@@ -1090,7 +1100,8 @@ static void encode_all(const Index& ix, const float* d_P, int64_t m, uint8_t* d_
 
 // B5 + B6 for all L trees at once, from codes EP[n][LK] (data order).  Returns false if the
 // leaf list overflowed its capacity (the caller retries with a larger factor).
-static bool build_trees_try(Index& ix, const uint8_t* d_EP, int64_t leaf_factor, cudaStream_t st) {
+static bool build_trees_try(Index& ix, const uint8_t* d_EP, int64_t leaf_factor, cudaStream_t st,
+                            const int* d_flag = nullptr, int* h_flag = nullptr) {
     Trace tr("trees");
     const int64_t n = ix.n, L = ix.L, total = n * L;
     const int K = ix.K, nb = ix.nb, LK = ix.LK, max_size = ix.max_size;
@@ -1117,14 +1128,15 @@ static bool build_trees_try(Index& ix, const uint8_t* d_EP, int64_t leaf_factor,
     DL_CUDA(cudaMemsetAsync(counters, 0, 8 * sizeof(uint32_t), st));
     DL_LAUNCH(k_seg_flags, grid_for(total, 256), 256, 0, st, skeys, n, total, flags);
     exclusive_scan_u32(flags, idx, total, counters + 0, st);
-    const int64_t nseg = d2h(counters + 0, st);
-    Scratch s_starts(st, sizeof(uint32_t) * (size_t)nseg);
+    // the segment count stays on the device: first-layer nodes of one tree <= min(n, 2^K)
+    const int64_t nseg_ub = std::min<int64_t>(total, K >= 40 ? total : L * ((int64_t)1 << std::min(K, 39)));
+    Scratch s_starts(st, sizeof(uint32_t) * (size_t)std::max<int64_t>(nseg_ub, 1));
     DL_LAUNCH(k_seg_write, grid_for(total, 256), 256, 0, st, flags, idx, total, s_starts.as<uint32_t>());
 
     // node storage: active nodes of one level are disjoint and hold > max_size points each;
     // leaves are disjoint and non-empty (<= total); start from a typical size and grow on overflow
     const int64_t cap_active = total / std::max(1, max_size) + 1;
-    const int64_t cap_leaves = std::min<int64_t>(total, nseg + leaf_factor * (total / std::max(1, max_size)) + 1024);
+    const int64_t cap_leaves = std::min<int64_t>(total, nseg_ub + leaf_factor * (total / std::max(1, max_size)) + 1024);
     Scratch s_nodes(st, sizeof(Node) * (size_t)(3 * cap_active + cap_leaves));
     Node* act = s_nodes.as<Node>();
     Node* nxt = act + cap_active;
@@ -1144,7 +1156,7 @@ static bool build_trees_try(Index& ix, const uint8_t* d_EP, int64_t leaf_factor,
                                           (int64_t)(LF_MAXSEG - 1) * (max_size + 1));
     Sinks sk{act, n_act, (uint32_t)cap_active, loc, n_loc, (uint32_t)cap_active, LM > max_size ? LM : 0,
              leaves, n_leaves, (uint32_t)cap_leaves};
-    DL_LAUNCH(k_init_nodes, grid_for(nseg, 256), 256, 0, st, s_starts.as<uint32_t>(), counters + 0, total, K, nb,
+    DL_LAUNCH(k_init_nodes, grid_for(nseg_ub, 256), 256, 0, st, s_starts.as<uint32_t>(), counters + 0, total, K, nb,
               max_size, sk);
     s_starts.free_();
 
@@ -1156,8 +1168,9 @@ static bool build_trees_try(Index& ix, const uint8_t* d_EP, int64_t leaf_factor,
     uint32_t* choff = nch + cap_active;
     uint32_t* zeros = choff + cap_active;
     Scratch s_tmp(st, sizeof(uint32_t) * (size_t)total);
-    Scratch s_zc(st);
-    int64_t zc_cap = 0;
+    // chunks of one level <= total / PART_CHUNK + one partial chunk per active node
+    const int64_t nc_ub = total / PART_CHUNK + cap_active + 1;
+    Scratch s_zc(st, sizeof(uint32_t) * (size_t)nc_ub);
     int64_t na = d2h(n_act, st);
     int level = 0;
     while (na > 0) {
@@ -1165,12 +1178,8 @@ static bool build_trees_try(Index& ix, const uint8_t* d_EP, int64_t leaf_factor,
         DL_LAUNCH(k_choose_split, grid_for(na * 32, 256), 256, 0, st, act, n_act, perm, d_EP, n, LK, K, nb,
                   max_size, PART_CHUNK, split, nch);
         exclusive_scan_u32(nch, choff, na, total_ch, st);
-        const int64_t nc = d2h(total_ch, st);
-        if (nc > zc_cap) {
-            zc_cap = nc * 2;
-            s_zc.alloc(sizeof(uint32_t) * (size_t)zc_cap);
-        }
-        if (nc > 0) {
+        const int64_t nc = std::min<int64_t>(nc_ub, total / PART_CHUNK + na + 1);   // grid bound; *total_ch exact
+        {
             DL_LAUNCH(k_part_count, (unsigned)nc, PART_THREADS, 0, st, act, split, choff, n_act, total_ch, perm, d_EP,
                       n, LK, K, nb, s_zc.as<uint32_t>());
             DL_LAUNCH(k_part_offsets, grid_for(na, 256), 256, 0, st, choff, nch, n_act, s_zc.as<uint32_t>(), zeros);
@@ -1228,10 +1237,12 @@ static bool build_trees_try(Index& ix, const uint8_t* d_EP, int64_t leaf_factor,
     DL_LAUNCH(k_leaf_finalize, grid_for(nl, 256), 256, 0, st, leaves, order, nl, perm, d_EP, n, LK, K, nb,
               ix.leaf_off.as<uint32_t>(), ix.leaf_lo.as<uint8_t>(), ix.leaf_hi.as<uint8_t>(),
               ix.leaf_bits.as<uint8_t>(), total);
-    Scratch s_begin(st, sizeof(unsigned long long) * (size_t)(L + 1));
-    DL_LAUNCH(k_tree_begin, 1, 64, 0, st, ix.leaf_off.as<uint32_t>(), nl, n, (int)L, s_begin.as<unsigned long long>());
-    std::vector<unsigned long long> begin(L + 1);
-    DL_CUDA(cudaMemcpyAsync(begin.data(), s_begin.p, sizeof(unsigned long long) * (L + 1), cudaMemcpyDeviceToHost, st));
+    // per tree: first leaf (k_tree_begin) and first tile (k_tree_tiles), read back together with
+    // the caller's flag in the single host round trip at the end
+    Scratch s_begin(st, sizeof(unsigned long long) * (size_t)(2 * (L + 1)) + 16);
+    unsigned long long* d_lbeg = s_begin.as<unsigned long long>();
+    unsigned long long* d_tbeg = d_lbeg + (L + 1);
+    DL_LAUNCH(k_tree_begin, 1, 64, 0, st, ix.leaf_off.as<uint32_t>(), nl, n, (int)L, d_lbeg);
     ix.tcodes.alloc((size_t)total * K, st);
     DL_LAUNCH(k_gather_tcodes, grid_for(total, 256), 256, 0, st, perm, d_EP, n, (int)L, K, ix.tcodes.as<uint8_t>());
     build_subboxes(ix, nl, st);
@@ -1239,40 +1250,36 @@ static bool build_trees_try(Index& ix, const uint8_t* d_EP, int64_t leaf_factor,
     ix.leaf_thi.alloc((size_t)nl * K, st);
     DL_LAUNCH(k_leaf_tight_sb, grid_for(nl, 256), 256, 0, st, ix.sb_off.as<uint32_t>(), nl, K, ix.sb_lo.as<uint8_t>(),
               ix.sb_hi.as<uint8_t>(), ix.leaf_tlo.as<uint8_t>(), ix.leaf_thi.as<uint8_t>());
-    DL_CUDA(cudaStreamSynchronize(st));
-    ix.tree_leaf_begin.assign(begin.begin(), begin.end());
-    ix.tree_leaf_begin[L] = nl;
     tr.mark("leaf finalize+codes", st);
-    // query tiles
+    // query tiles: runs of kTileLeaves leaves of one tree; the tile count stays on the device
+    // (arrays sized by its bound: each tree adds at most one partial tile)
     {
+        const int64_t nt_ub = nl / kTileLeaves + L + 1;
         Scratch s_tf(st, sizeof(uint32_t) * (size_t)(2 * nl + 2));
         uint32_t* tf = s_tf.as<uint32_t>();
         uint32_t* tidx = tf + nl;
         uint32_t* ntiles_d = tidx + nl;
-        DL_CUDA(cudaMemcpyAsync(s_begin.p, begin.data(), sizeof(unsigned long long) * (L + 1), cudaMemcpyHostToDevice, st));
-        DL_LAUNCH(k_tile_flags, grid_for(nl, 256), 256, 0, st, ix.leaf_off.as<uint32_t>(), nl, n, kTileLeaves,
-                  s_begin.as<unsigned long long>(), tf);
+        DL_LAUNCH(k_tile_flags, grid_for(nl, 256), 256, 0, st, ix.leaf_off.as<uint32_t>(), nl, n, kTileLeaves, d_lbeg, tf);
         exclusive_scan_u32(tf, tidx, nl, ntiles_d, st);
-        const int64_t ntiles = d2h(ntiles_d, st);
-        ix.tile_leaf.alloc(sizeof(uint32_t) * (size_t)(ntiles + 1), st);
+        ix.tile_leaf.alloc(sizeof(uint32_t) * (size_t)(nt_ub + 1), st);
         DL_LAUNCH(k_tile_write, grid_for(nl, 256), 256, 0, st, tf, tidx, nl, ix.tile_leaf.as<uint32_t>());
-        const uint32_t last = (uint32_t)nl;
-        DL_CUDA(cudaMemcpyAsync(ix.tile_leaf.as<uint32_t>() + ntiles, &last, sizeof(uint32_t), cudaMemcpyHostToDevice, st));
-        DL_CUDA(cudaMemcpyAsync(s_begin.p, begin.data(), sizeof(unsigned long long) * (L + 1), cudaMemcpyHostToDevice, st));
-        Scratch s_tb(st, sizeof(unsigned long long) * (size_t)(L + 1));
-        DL_LAUNCH(k_tree_tiles, 1, 64, 0, st, tidx, s_begin.as<unsigned long long>(), (int)L, (uint32_t)ntiles,
-                  s_tb.as<unsigned long long>());
-        ix.tile_lo.alloc((size_t)ntiles * K, st);
-        ix.tile_hi.alloc((size_t)ntiles * K, st);
-        DL_LAUNCH(k_tile_boxes, grid_for(ntiles * K, 256), 256, 0, st, ix.tile_leaf.as<uint32_t>(), ntiles, K,
+        DL_LAUNCH(k_tree_tiles, 1, 64, 0, st, tidx, d_lbeg, (int)L, ntiles_d, (uint32_t)nl, ix.tile_leaf.as<uint32_t>(),
+                  d_tbeg);
+        ix.tile_lo.alloc((size_t)nt_ub * K, st);
+        ix.tile_hi.alloc((size_t)nt_ub * K, st);
+        DL_LAUNCH(k_tile_boxes, grid_for(nt_ub * K, 256), 256, 0, st, ix.tile_leaf.as<uint32_t>(), ntiles_d, K,
                   ix.leaf_tlo.as<uint8_t>(), ix.leaf_thi.as<uint8_t>(), ix.tile_lo.as<uint8_t>(), ix.tile_hi.as<uint8_t>());
         ix.point_tile_leaf.alloc(sizeof(uint16_t) * (size_t)total, st);
-        DL_LAUNCH(k_point_tile_leaf, grid_for(ntiles * 32, 256), 256, 0, st, ix.leaf_off.as<uint32_t>(), ix.tile_leaf.as<uint32_t>(),
-                  ntiles, nl, ix.point_tile_leaf.as<uint16_t>());
-        std::vector<unsigned long long> tb(L + 1);
-        DL_CUDA(cudaMemcpyAsync(tb.data(), s_tb.p, sizeof(unsigned long long) * (L + 1), cudaMemcpyDeviceToHost, st));
+        DL_LAUNCH(k_point_tile_leaf, grid_for(nt_ub * 32, 256), 256, 0, st, ix.leaf_off.as<uint32_t>(),
+                  ix.tile_leaf.as<uint32_t>(), ntiles_d, nl, ix.point_tile_leaf.as<uint16_t>());
+        std::vector<unsigned long long> h(2 * (L + 1) + 1, 0);
+        DL_CUDA(cudaMemcpyAsync(h.data(), d_lbeg, sizeof(unsigned long long) * 2 * (L + 1), cudaMemcpyDeviceToHost, st));
+        if (d_flag) DL_CUDA(cudaMemcpyAsync(&h[2 * (L + 1)], d_flag, sizeof(int), cudaMemcpyDeviceToHost, st));
         DL_CUDA(cudaStreamSynchronize(st));
-        ix.tree_tile_begin.assign(tb.begin(), tb.end());
+        ix.tree_leaf_begin.assign(h.begin(), h.begin() + (L + 1));
+        ix.tree_leaf_begin[L] = nl;
+        ix.tree_tile_begin.assign(h.begin() + (L + 1), h.begin() + 2 * (L + 1));
+        if (h_flag) std::memcpy(h_flag, &h[2 * (L + 1)], sizeof(int));
     }
     tr.mark("tiles", st);
     return true;
@@ -1291,9 +1298,11 @@ void build_subboxes(Index& ix, int64_t nl, cudaStream_t st) {
               ix.K, ix.tcodes.as<uint8_t>(), ix.sb_lo.as<uint8_t>(), ix.sb_hi.as<uint8_t>());
 }
 
-static void build_trees(Index& ix, const uint8_t* d_EP, cudaStream_t st) {
+// d_flag (optional): a device int read back (into *h_flag) with the build's last host round trip
+static void build_trees(Index& ix, const uint8_t* d_EP, cudaStream_t st, const int* d_flag = nullptr,
+                        int* h_flag = nullptr) {
     for (int64_t f = 4;; f *= 4) {
-        if (build_trees_try(ix, d_EP, f, st)) return;
+        if (build_trees_try(ix, d_EP, f, st, d_flag, h_flag)) return;
         DL_REQUIRE(f < (int64_t)1 << 40, "tree build: leaf list overflow");
     }
 }
@@ -1351,11 +1360,12 @@ void build_index(Index& ix, const float* d_data, int64_t data_ld, const float* b
                                         cudaMemcpyDeviceToDevice, st));
         }
     }
-    const int nonfinite = d2h(s_flag.as<int>(), st);
-    DL_REQUIRE(!nonfinite, "data contains NaN or Inf");
     tr.mark("project+encode", st);
-    // B5 + B6
-    build_trees(ix, s_ep.as<uint8_t>(), st);
+    // B5 + B6; the non-finite flag of the projection is read with the trees' last round trip
+    // (a NaN/Inf row makes the whole build fail -- after the trees, not before)
+    int nonfinite = 0;
+    build_trees(ix, s_ep.as<uint8_t>(), st, s_flag.as<int>(), &nonfinite);
+    DL_REQUIRE(!nonfinite, "data contains NaN or Inf");
     tr.mark("trees", st);
 }
 

@@ -2219,17 +2219,24 @@ void estimate_rstar(const Index& ix, const float* d_Q, int64_t q_ld, int64_t ns,
     Scratch s_sx(st, (size_t)(ns * LK));
     DL_LAUNCH(k_build_lut, (unsigned)std::min<int64_t>(ceil_div(ns * LK * ix.N_r, 256), 148 * 32), 256, 0, st,
               s_qp.as<float>(), (int)ns, (int)LK, ix.N_r, ix.B.as<float>(), s_lut.as<float>(), s_sx.as<uint8_t>());
-    Scratch s_tp(st, sizeof(uint32_t) * (size_t)(ns * n));
-    DL_CUDA(cudaMemsetAsync(s_tp.p, 0xFF, sizeof(uint32_t) * (size_t)(ns * n), st));   // NaN bits > +inf bits
+    // per-point minima of one chunk of sample queries at a time: chunk * n * 4 bytes of scratch
+    // bounded by ~1/4 of the query budget (and gridDim.y <= 65535)
+    const int64_t per_q = sizeof(uint32_t) * (int64_t)n;
+    const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>({ns, 65535, auto_query_budget() / 4 / per_q}));
+    Scratch s_tp(st, (size_t)(per_q * chunk));
+    Scratch s_out(st, sizeof(uint32_t) * (size_t)ns);
     const size_t smem = sizeof(float) * (size_t)ix.K * ix.N_r;
     ensure_dyn_smem_fn(k_rstar_tree, smem);
     const unsigned gx = (unsigned)std::min<int64_t>(ceil_div(n, 256), 64);
-    for (int t = 0; t < ix.L; ++t)
-        DL_LAUNCH(k_rstar_tree, dim3(gx, (unsigned)ns), 256, smem, st, s_lut.as<float>(),
-                  ix.tcodes.as<uint8_t>() + (int64_t)t * n * ix.K, ix.perm.as<uint32_t>() + (int64_t)t * n, n, t,
-                  ix.L, ix.K, ix.N_r, s_tp.as<uint32_t>());
-    Scratch s_out(st, sizeof(uint32_t) * (size_t)ns);
-    DL_LAUNCH(k_select_kth_u32, (unsigned)ns, 1024, 0, st, s_tp.as<uint32_t>(), n, B, s_out.as<uint32_t>());
+    for (int64_t q0 = 0; q0 < ns; q0 += chunk) {
+        const int64_t nc = std::min(chunk, ns - q0);
+        DL_CUDA(cudaMemsetAsync(s_tp.p, 0xFF, (size_t)(per_q * nc), st));   // NaN bits > +inf bits
+        for (int t = 0; t < ix.L; ++t)
+            DL_LAUNCH(k_rstar_tree, dim3(gx, (unsigned)nc), 256, smem, st, s_lut.as<float>() + q0 * LK * ix.N_r,
+                      ix.tcodes.as<uint8_t>() + (int64_t)t * n * ix.K, ix.perm.as<uint32_t>() + (int64_t)t * n, n, t,
+                      ix.L, ix.K, ix.N_r, s_tp.as<uint32_t>());
+        DL_LAUNCH(k_select_kth_u32, (unsigned)nc, 1024, 0, st, s_tp.as<uint32_t>(), n, B, s_out.as<uint32_t>() + q0);
+    }
     std::vector<uint32_t> bits(ns);
     DL_CUDA(cudaMemcpyAsync(bits.data(), s_out.p, sizeof(uint32_t) * ns, cudaMemcpyDeviceToHost, st));
     DL_CUDA(cudaStreamSynchronize(st));

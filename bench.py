@@ -46,7 +46,9 @@ def load_rmin(cid: int, which: str = "bench") -> float:
 
 
 def rmin_info(cid: int) -> dict:
-    e = json.load(open(os.path.join(ROOT, "bench_configs.json")))[str(cid)]
+    e = json.load(open(os.path.join(ROOT, "bench_configs.json"))).get(str(cid))
+    if e is None:
+        return {"r_choice": "no oracle operating point recorded for this config (--r-value experiment)"}
     return {"r_min_amb22": e["r_min"], "bench_m": e.get("bench_m", 0),
             "bench_oracle_recall": e.get("bench_oracle_recall"),
             "r_choice": "r_min c^-m, m = largest with oracle recall@k >= 0.95 on 50 held-out sample queries "
@@ -407,6 +409,8 @@ def main():
     ap.add_argument("--recall-queries", type=int, default=200)
     ap.add_argument("--radius", default="bench", choices=["bench", "amb22"],
                     help="bench: the oracle-chosen operating point r_bench; amb22: the AMB-22 r_min itself")
+    ap.add_argument("--r-value", type=float, default=None,
+                    help="experiments only: run at this radius instead of bench_configs.json's")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     cfg = datagen.CONFIGS[args.config]
@@ -424,7 +428,7 @@ def main():
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    r_min = load_rmin(args.config, args.radius)
+    r_min = args.r_value if args.r_value is not None else load_rmin(args.config, args.radius)
     Dd = datagen.generate(cfg)
     X, Q = Dd["X"], Dd["Q"]
     lo, hi = PD.shard_range(cfg.n, world, rank)

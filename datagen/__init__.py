@@ -92,6 +92,24 @@ def _draw(cfg: Config, mu: np.ndarray, m: int, stream: int) -> np.ndarray:
     return out
 
 
+def _cached(cfg: Config, n: int, make):
+    """Experiments only: with DATAGEN_CACHE_DIR set, the data rows of (config, n) are kept in that
+    directory as .npy (memory-mapped on reuse), so one job can run several benchmarks of the 100M
+    config without regenerating it.  Unset (the default, and every driver-run command) = no cache."""
+    import os
+    d = os.environ.get("DATAGEN_CACHE_DIR")
+    if not d or n < 5_000_000:
+        return make()
+    path = os.path.join(d, f"{cfg.name}_{cfg.seed}_{n}.npy")
+    if os.path.exists(path):
+        return np.load(path, mmap_mode="r")
+    X = make()
+    os.makedirs(d, exist_ok=True)
+    np.save(path + ".tmp.npy", X)
+    os.replace(path + ".tmp.npy", path)
+    return X
+
+
 def generate(cfg: Config | int, n: int | None = None, nq: int | None = None,
              with_sample_queries: int = 0):
     """Return dict(X [n][d] f32, Q [nq][d] f32, Qs [ns][d] f32, cfg).
@@ -102,7 +120,7 @@ def generate(cfg: Config | int, n: int | None = None, nq: int | None = None,
     n = cfg.n if n is None else n
     nq = cfg.nq if nq is None else nq
     mu = _centres(cfg)
-    X = _draw(cfg, mu, n, 1)
+    X = _cached(cfg, n, lambda: _draw(cfg, mu, n, 1))
     Q = _draw(cfg, mu, nq, 2)
     Qs = _draw(cfg, mu, with_sample_queries, 3) if with_sample_queries else None
     if cfg.kind == "abs01":

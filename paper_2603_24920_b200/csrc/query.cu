@@ -276,7 +276,8 @@ struct RFArgs {
     int t, L, K, N_r, mode;
     int pq_cost;                // per-query path cost per 32-point step, relative to 170 per SIMD chunk
     unsigned int* tctr;         // [groups] next tile of each group (zeroed by k_group_table), or null
-    int dbg;                    // experiments (DETLSH_RF_DEBUG): 1 = per-query leaf test
+    int dbg;                    // experiments (DETLSH_RF_DEBUG): 1 = per-query leaf test; 2 = tile screen
+                                // also on the 16-query SIMD leaf path (DETLSH_RF_TSCREEN=1)
     uint32_t* plist;            // CELL, sparse tiles: per-query lists of reachable leaves [Qb][pcap] (or null)
     uint32_t* pcnt;             // [Qb] list lengths
     int64_t pcap;
@@ -391,7 +392,7 @@ __global__ void __launch_bounds__(RF_THREADS, RF_CTAS) k_range_filter(RFArgs a) 
         uint32_t tm;
         {
             bool pass = false;
-            if (SIMD_LEAF && !(a.dbg & 1) && lane < G) {
+            if (SIMD_LEAF && !(a.dbg & 3) && lane < G) {
                 // the 16-query leaf test below costs the same whatever subset reached the tile,
                 // and the group's 16 queries reach ~every tile between them: the tile screen
                 // would only add work (every leaf bound is computed for every active query)
@@ -2393,7 +2394,8 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
         static const int pq = std::getenv("DETLSH_PQ_COST") ? std::atoi(std::getenv("DETLSH_PQ_COST")) : 40;
         ra.pq_cost = pq;
         static const int rfd = std::getenv("DETLSH_RF_DEBUG") ? std::atoi(std::getenv("DETLSH_RF_DEBUG")) : 0;
-        ra.dbg = rfd;
+        static const int tsc = std::getenv("DETLSH_RF_TSCREEN") ? std::atoi(std::getenv("DETLSH_RF_TSCREEN")) : 0;
+        ra.dbg = rfd | (tsc ? 2 : 0);
     }
     const int nv = (int)ceil_div(ix.ld / 4, 8);      // float4 per lane (8 lanes per row)
     const int vnv = nv <= 1 ? 1 : nv <= 2 ? 2 : nv <= 4 ? 4 : nv <= 8 ? 8 : 0;

@@ -508,55 +508,56 @@ def test_projection_streamed_hash_matrix(d):
 
 
 @pytest.mark.slow
-def test_config5_full_size_properties():
-    """configs[4] at full size (n = 100M, d = 96, L = 6, beta = 0.05; 38.4 GB of data).  The oracle
-    cannot build this index in a test run (fp64 single thread: hours), so the check is by
-    properties that hold at any size: the hash family bit-exact with the oracle's generator;
-    sampled projections against numpy fp64; every returned distance the exact Euclidean distance
-    of its id, ascending; the stop rules (budget: |S| >= ceil(beta n) + k; radius: k-th distance
-    <= c r, AMB-18); recall against numpy brute force reported.  r_min from the GPU estimator
-    (an input of the GPU path only; no oracle value involved)."""
-    import math
+def test_config5_vs_oracle_golden():
+    """configs[4] at full size (n = 100M, d = 96, L = 6, beta = 0.05; 38.4 GB) against the ORACLE on
+    the seeded 200-query subset (seed 2005; BASELINE.json / SURVEY 8(d)).  The oracle's answers
+    were computed once on the GPU host by the oracle-only tools/make_cfg5_golden.py (its index
+    needs ~95 GB of host RAM) and are committed as tests/golden/cfg5_oracle.npz: top-k ids and
+    distances and the stop statistics of Alg. 5 at the AMB-22 r_min, and at the bench
+    operating point r_bench for the subset's first queries.  All 10,000 queries are answered in
+    one call as bench.py runs them; the subset is compared: recall >= 0.99 vs the oracle's ids,
+    distances within 1e-4 relative, and the stop (reason, round, tree) and |S| agreement
+    reported.  Plus properties that hold at any size: the hash family bit-exact, sampled
+    projections vs numpy fp64, returned distances exact and ascending."""
+    import os
     import torch
-    D = datagen.generate(5, nq=1000, with_sample_queries=50)
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "cfg5_oracle.npz")
+    z = np.load(path)
+    D = datagen.generate(5)
     c = D["cfg"]
     X, Q = D["X"], D["Q"]
     n = X.shape[0]
+    sel = z["sel"]
+    assert np.array_equal(sel, np.sort(np.random.default_rng(2005).choice(c.nq, 200, replace=False)))
     Xd = torch.from_numpy(X).cuda()
     g = P.detlsh_build(Xd, c.L, c.K, c.N_r, c.index_seed, opts=P.default_opts(borrow_data=1))
     assert np.array_equal(g.A(), O.hash_family(c.index_seed, c.d, c.L, c.K))
-    sel = np.random.default_rng(3).choice(n, 2000, replace=False)
-    Pg = g.project(X[sel])
-    Po = X[sel].astype(np.float64) @ g.A().astype(np.float64).T
-    assert np.all(np.abs(Pg - Po) <= 1e-4 * np.maximum(np.abs(Po), np.linalg.norm(X[sel], axis=1)[:, None]))
-    r = g.estimate_rmin(D["Qs"], c.k, c.beta)
-    ig, dg, st = g.query(Q, c.k, c.c, r, c.beta, stats=True)
-    B = math.ceil(c.beta * n) + c.k
-    bud, rad = st["reason"] == 0, st["reason"] == 1
-    assert np.all(st["n_cand"][bud] >= B)
-    assert np.all(dg[rad, -1].astype(np.float64) <= c.c * st["r_final"][rad] * (1 + 1e-6))
-    qs = np.random.default_rng(4).choice(len(Q), 40, replace=False)
-    for q in qs:
-        ok = ig[q] >= 0
-        d_ex = np.sqrt(((X[ig[q][ok]].astype(np.float64) - Q[q]) ** 2).sum(1))
-        assert np.allclose(dg[q][ok], d_ex, rtol=1e-4, atol=1e-6)
-        assert np.all(np.diff(dg[q][ok]) >= 0)
-    norms = np.einsum("ij,ij->i", X, X, dtype=np.float64)
-    best = None
-    for s0 in range(0, n, 10_000_000):
-        blk = X[s0:s0 + 10_000_000]
-        d2 = norms[s0:s0 + len(blk)][None, :] - 2.0 * (Q[qs] @ blk.T).astype(np.float64)
-        part = np.argpartition(d2, c.k, axis=1)[:, :c.k] + s0
-        best = part if best is None else np.concatenate([best, part], 1)
-    gt = []
-    for i, q in enumerate(qs):
-        cand = np.unique(best[i])
-        d2 = ((X[cand].astype(np.float64) - Q[q]) ** 2).sum(1)
-        gt.append(cand[np.lexsort((cand, d2))[:c.k]])
-    rec = np.mean([len(set(ig[q]) & set(gt[i])) / c.k for i, q in enumerate(qs)])
-    print(f"cfg5 n={n}: r_min {r:.4g}, recall@{c.k} vs brute force on 40 queries {rec:.3f}, "
-          f"stops {np.bincount(st['reason'], minlength=3)}, mean |S| {st['n_cand'].mean():.0f}")
-    assert rec > 0
+    rs = np.random.default_rng(3).choice(n, 2000, replace=False)
+    Pg = g.project(X[rs])
+    Po = X[rs].astype(np.float64) @ g.A().astype(np.float64).T
+    assert np.all(np.abs(Pg - Po) <= 1e-4 * np.maximum(np.abs(Po), np.linalg.norm(X[rs], axis=1)[:, None]))
+    passes = [("rmin", float(z["r_min"]))]
+    if "rbench_ids" in z.files:
+        passes.append(("rbench", float(z["r_bench"])))
+    for tag, r in passes:
+        ig, dg, st = g.query(Q, c.k, c.c, r, c.beta, stats=True)
+        oi, od, ost = z[f"{tag}_ids"], z[f"{tag}_dists"], z[f"{tag}_stats"]
+        qs = sel[:len(oi)]
+        rec = _recall(ig[qs], oi)
+        stop = np.mean((st["reason"][qs] == ost["reason"]) & (st["rounds"][qs] == ost["rounds"]) &
+                       (st["trees_last"][qs] == ost["trees_last"]))
+        ncand = np.mean(st["n_cand"][qs] == ost["n_cand"])
+        print(f"cfg5 {tag} r={r:.4g}: recall vs oracle {rec:.4f} on {len(qs)} queries; stop agreement {stop:.3f}; "
+              f"|S| equal {ncand:.3f}; stops gpu {np.bincount(st['reason'][qs], minlength=3)} "
+              f"oracle {np.bincount(ost['reason'], minlength=3)}")
+        assert rec >= 0.99
+        _dist_match(ig[qs], dg[qs], oi, od)
+        assert stop >= 0.9
+        for q in qs[:40]:
+            ok = ig[q] >= 0
+            d_ex = np.sqrt(((X[ig[q][ok]].astype(np.float64) - Q[q]) ** 2).sum(1))
+            assert np.allclose(dg[q][ok], d_ex, rtol=1e-4, atol=1e-6)
+            assert np.all(np.diff(dg[q][ok]) >= 0)
 
 
 @pytest.mark.parametrize("local_max", ["0", "300", "1536", "8192"])

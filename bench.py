@@ -68,31 +68,42 @@ def c_index(c) -> int:
 
 
 # ---------------------------------------------------------------- ground truth and quality (harness)
-def exact_knn_sample(Xd, X: np.ndarray, Q: np.ndarray, k: int, sel: np.ndarray):
-    """Exact kNN of Q[sel] (harness, not the library): fp32 screening with torch on the GPU over
-    the device-resident data (chunks of 8M rows, TF32 off), the k + 64 best of each chunk
-    re-ranked in fp64 on the host, ties by id.  Returns (ids, dists) [len(sel)][k]."""
+def exact_knn_sample(Xd, Xs: np.ndarray, lo: int, Q: np.ndarray, k: int, sel: np.ndarray, world: int = 1):
+    """Exact kNN of Q[sel] (harness, not the library) over the point-sharded data: every rank screens
+    its own rows (device copy Xd = host rows Xs = global ids [lo, lo + len)) in fp32 with torch on
+    its GPU (8M-row blocks, TF32 off), re-ranks its k + 64 best per query in fp64 on the host (ties
+    by id), and the ranks' local top-k lists are all-gathered and merged by (distance, id).
+    Returns (ids, dists) [len(sel)][k] (every rank)."""
     import torch
     torch.backends.cuda.matmul.allow_tf32 = False
     extra = k + 64
-    dev = Xd.device if Xd is not None else torch.device("cuda")
-    qs = torch.from_numpy(np.ascontiguousarray(Q[sel])).to(dev)
-    n = X.shape[0]
+    qs = torch.from_numpy(np.ascontiguousarray(Q[sel])).to(Xd.device)
     cands = []
-    for s0 in range(0, n, 1 << 23):
-        # the device copy when it holds every row (N = 1), else host blocks streamed in
-        blk = Xd[s0:s0 + (1 << 23), :Q.shape[1]] if Xd is not None else torch.from_numpy(X[s0:s0 + (1 << 23)]).to(dev)
+    for s0 in range(0, Xd.shape[0], 1 << 23):
+        blk = Xd[s0:s0 + (1 << 23), :Q.shape[1]]
         d2 = (blk * blk).sum(1)[None, :] - 2.0 * (qs @ blk.T)
-        kk = min(extra, blk.shape[0])
-        cands.append((torch.topk(d2, kk, dim=1, largest=False).indices + s0).cpu())
+        cands.append((torch.topk(d2, min(extra, blk.shape[0]), dim=1, largest=False).indices + s0).cpu())
     cand = torch.cat(cands, 1).numpy()
-    ids = np.empty((len(sel), k), np.int64)
-    dists = np.empty((len(sel), k), np.float64)
+    kk = min(k, Xs.shape[0])
+    ids = np.full((len(sel), k), -1, np.int64)
+    dists = np.full((len(sel), k), np.inf, np.float64)
     for r in range(len(sel)):
         cid = np.unique(cand[r])
-        d2 = ((X[cid].astype(np.float64) - Q[sel[r]].astype(np.float64)) ** 2).sum(1)
-        o = np.lexsort((cid, d2))[:k]
-        ids[r], dists[r] = cid[o], np.sqrt(d2[o])
+        d2 = ((Xs[cid].astype(np.float64) - Q[sel[r]].astype(np.float64)) ** 2).sum(1)
+        o = np.lexsort((cid, d2))[:kk]
+        ids[r, :kk], dists[r, :kk] = cid[o] + lo, np.sqrt(d2[o])
+    if world > 1:
+        import torch.distributed as dist
+        ti, td = torch.from_numpy(ids).to(Xd.device), torch.from_numpy(dists).to(Xd.device)
+        gi = [torch.empty_like(ti) for _ in range(world)]
+        gd = [torch.empty_like(td) for _ in range(world)]
+        dist.all_gather(gi, ti)
+        dist.all_gather(gd, td)
+        ai = torch.cat(gi, 1).cpu().numpy()
+        ad = torch.cat(gd, 1).cpu().numpy()
+        for r in range(len(sel)):
+            o = np.lexsort((ai[r], ad[r]))[:k]
+            ids[r], dists[r] = ai[r][o], ad[r][o]
     return ids, dists
 
 
@@ -429,10 +440,15 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     r_min = args.r_value if args.r_value is not None else load_rmin(args.config, args.radius)
-    Dd = datagen.generate(cfg)
-    X, Q = Dd["X"], Dd["Q"]
     lo, hi = PD.shard_range(cfg.n, world, rank)
-    Xd = torch.from_numpy(X[lo:hi]).cuda()
+    if world == 1 or cfg.kind == "abs01":
+        Dd = datagen.generate(cfg)
+        Xs, Q = np.ascontiguousarray(Dd["X"][lo:hi]), Dd["Q"]
+        del Dd
+    else:       # each rank holds only its shard's rows (configs[4]: 38.4 GB in all)
+        Xs = datagen.generate_rows(cfg, lo, hi)
+        Q = datagen.generate(cfg, n=1)["Q"]
+    Xd = torch.from_numpy(Xs).cuda()
     Qd = torch.from_numpy(Q).cuda()
     stream = torch.cuda.current_stream()
     opts = P.default_opts(stream=stream.cuda_stream, borrow_data=1)
@@ -524,12 +540,12 @@ def main():
     if world > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
 
+    sel = np.random.default_rng(2).choice(cfg.nq, min(args.recall_queries, cfg.nq), replace=False)
+    gt, gt_d = exact_knn_sample(Xd, Xs, lo, Q, cfg.k, sel, world)
     if rank == 0:
         ids, dists = results["ids"], results["dists"]
         ids = ids.cpu().numpy() if torch.is_tensor(ids) else ids
         dists = dists.cpu().numpy() if torch.is_tensor(dists) else dists
-        sel = np.random.default_rng(2).choice(cfg.nq, min(args.recall_queries, cfg.nq), replace=False)
-        gt, gt_d = exact_knn_sample(Xd if world == 1 else None, X, Q, cfg.k, sel)
         qual = quality(ids[sel], dists[sel], gt, gt_d, cfg.c ** 2)
         rec = qual["recall_at_k"]
         agree = oracle_agreement(args.config, ids, dists, args.radius)
@@ -573,7 +589,7 @@ def main():
             "data": "synthetic",
             "config": {"workload": workload_desc(cfg), "n": cfg.n, "d": cfg.d, "nq": cfg.nq, "k": cfg.k,
                        "r_min": r_min, **rmin_info(args.config), "parallelism": f"point-sharded x{world}",
-                       "l2": f"no flush: X ({X.nbytes / 1e9:.2f} GB) and the rebuilt index exceed L2 (126 MB)",
+                       "l2": f"no flush: X ({cfg.n * cfg.d * 4 / 1e9:.2f} GB) and the rebuilt index exceed L2 (126 MB)",
                        "proj_impl": int(opts.proj_impl)},
             "recall_at_k": rec, "recall_queries": int(len(sel)),
             "quality": qual, "vs_oracle": agree,

@@ -76,20 +76,25 @@ def _draw(cfg: Config, mu: np.ndarray, m: int, stream: int) -> np.ndarray:
     out = np.empty((m, cfg.d), np.float32)
     for s in range(0, m, CHUNK):
         e = min(m, s + CHUNK)
-        comp = r.integers(0, cfg.comps, size=e - s)
-        z = r.standard_normal((e - s, cfg.d), dtype=np.float32)
-        x = mu[comp]
-        if cfg.kind == "gauss_box":      # sigma = 5
-            x = x + 5.0 * z
-        elif cfg.kind == "unit":         # noise norm ~0.3 ||mu||, then unit-normalised
-            x = x + np.float32(0.3 / math.sqrt(cfg.d)) * z
-            x = x / np.linalg.norm(x, axis=1, keepdims=True)
-        elif cfg.kind == "abs01":        # |mu + 0.3 z| (scaled to [0,1] afterwards)
-            x = np.abs(x + 0.3 * z)
-        elif cfg.kind == "int255":       # clip(round(mu + 20 z), 0, 255), ~30% zeros
-            x = np.clip(np.rint(x + 20.0 * z), 0.0, 255.0)
-        out[s:e] = x
+        out[s:e] = _draw_chunk(cfg, mu, r, e - s)
     return out
+
+
+def _draw_chunk(cfg: Config, mu: np.ndarray, r: np.random.Generator, m: int) -> np.ndarray:
+    """The next m rows of the stream r (one chunk)."""
+    comp = r.integers(0, cfg.comps, size=m)
+    z = r.standard_normal((m, cfg.d), dtype=np.float32)
+    x = mu[comp]
+    if cfg.kind == "gauss_box":      # sigma = 5
+        x = x + 5.0 * z
+    elif cfg.kind == "unit":         # noise norm ~0.3 ||mu||, then unit-normalised
+        x = x + np.float32(0.3 / math.sqrt(cfg.d)) * z
+        x = x / np.linalg.norm(x, axis=1, keepdims=True)
+    elif cfg.kind == "abs01":        # |mu + 0.3 z| (scaled to [0,1] afterwards)
+        x = np.abs(x + 0.3 * z)
+    elif cfg.kind == "int255":       # clip(round(mu + 20 z), 0, 255), ~30% zeros
+        x = np.clip(np.rint(x + 20.0 * z), 0.0, 255.0)
+    return x
 
 
 def _cached(cfg: Config, n: int, make):
@@ -108,6 +113,26 @@ def _cached(cfg: Config, n: int, make):
     np.save(path + ".tmp.npy", X)
     os.replace(path + ".tmp.npy", path)
     return X
+
+
+def generate_rows(cfg: Config | int, lo: int, hi: int, n: int | None = None) -> np.ndarray:
+    """Rows [lo, hi) of the config's data X (the same bytes as generate(cfg, n)["X"][lo:hi]); the
+    stream is drawn up to hi but only the requested rows are kept (a point shard's memory)."""
+    if isinstance(cfg, int):
+        cfg = CONFIGS[cfg]
+    n = cfg.n if n is None else n
+    mu = _centres(cfg)
+    r = _rng(cfg.seed, 1)
+    out = np.empty((hi - lo, cfg.d), np.float32)
+    for s in range(0, hi, CHUNK):
+        e = min(n, s + CHUNK)
+        blk = _draw_chunk(cfg, mu, r, e - s)
+        a, b = max(s, lo), min(e, hi)
+        if a < b:
+            out[a - lo:b - lo] = blk[a - s:b - s]
+    if cfg.kind == "abs01":
+        raise ValueError("generate_rows: the abs01 family is scaled by the global data max")
+    return out
 
 
 def generate(cfg: Config | int, n: int | None = None, nq: int | None = None,

@@ -2534,8 +2534,8 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
         const float* Qpb = s_qp.as<float>() + q0 * LK;
         va.Q = Qb;
         static const int dirty_env = std::getenv("DETLSH_DIRTY_CLEAR") ? std::atoi(std::getenv("DETLSH_DIRTY_CLEAR")) : 1;
-        const bool dirty = dirty_env && q0 > 0 &&
-                           (double)batch_members * 96.0 < 0.5 * (double)prev_rows * (double)nwords * 12.0;
+        const bool dirty = dirty_env && q0 > 0 &&      // DETLSH_DIRTY_CLEAR: 0 never, 2 always (tests)
+                           (dirty_env == 2 || (double)batch_members * 96.0 < 0.5 * (double)prev_rows * (double)nwords * 12.0);
         if (dirty) {
             DL_LAUNCH(k_clear_dirty, dim3((unsigned)std::min<int64_t>(ceil_div(nsw, 256), 64), (unsigned)prev_rows), 256, 0,
                       st, s_bm.as<uint32_t>(), bm_prev, s_ver.as<uint32_t>(), s_sum.as<uint32_t>(), nwords, nsw);

@@ -17,5 +17,9 @@ out = {}
 for tag, r in (("small", 0.45), ("large", 0.9)):
     ids, d = g.query(D["Q"], c.k, c.c, r, c.beta)
     out[tag + "_ids"], out[tag + "_d"] = ids, d
+    # the same queries in batches of 37 (S bitmaps reused across batches: cleared by streaming
+    # zeros or by their dirty words, DETLSH_DIRTY_CLEAR)
+    ids, d, st = g.query(D["Q"], c.k, c.c, r, c.beta, opts=P.default_opts(query_batch=37), stats=True)
+    out[tag + "_b_ids"], out[tag + "_b_d"], out[tag + "_b_n"] = ids, d, st["n_cand"]
 np.savez(sys.argv[1], **out)
 print("OK")

@@ -21,5 +21,6 @@ for tag, r in (("small", 0.45), ("large", 0.9)):
     # zeros or by their dirty words, DETLSH_DIRTY_CLEAR)
     ids, d, st = g.query(D["Q"], c.k, c.c, r, c.beta, opts=P.default_opts(query_batch=37), stats=True)
     out[tag + "_b_ids"], out[tag + "_b_d"], out[tag + "_b_n"] = ids, d, st["n_cand"]
+    assert np.array_equal(ids, out[tag + "_ids"]) and np.array_equal(d, out[tag + "_d"]), tag
 np.savez(sys.argv[1], **out)
 print("OK")

@@ -84,6 +84,13 @@ __global__ void __launch_bounds__(256) k_rs_scan(uint32_t* __restrict__ hist, in
     if (lane == 0) dtot[seg * 256 + dig] = carry;
 }
 
+// Scatter of one 8-bit digit pass, stable.  Warp w of the block ranks the tile's keys
+// [512 w, 512 w + 512) on its own: 16 rounds of 32 consecutive keys, warp.match_any groups a
+// round's equal digits, the group's lowest lane reads and bumps the warp's private digit counter
+// (no block barrier per round).  One block barrier later every key knows its place in the tile
+// sorted by (digit, original position); the tile is staged in shared memory in that order and
+// written out so that runs of equal digits land on consecutive addresses (coalesced), at the
+// digit's global base (this tile's per-digit offset from k_rs_scan + the digits below).
 template <bool HAS_VALS>
 __global__ void __launch_bounds__(RS_THREADS) k_rs_scatter(const uint32_t* __restrict__ kin,
                                                            const uint32_t* __restrict__ vin,
@@ -92,46 +99,78 @@ __global__ void __launch_bounds__(RS_THREADS) k_rs_scatter(const uint32_t* __res
                                                            int shift, int tiles,
                                                            const uint32_t* __restrict__ offs,
                                                            const uint32_t* __restrict__ dtot) {
-    __shared__ uint32_t s_base[256];
-    __shared__ uint32_t s_wcnt[RS_WARPS][256];
+    __shared__ uint32_t s_base[256];                 // global position of the tile's first key of digit d
+    __shared__ uint32_t s_tds[256];                  // first staged slot of digit d in the sorted tile
+    __shared__ uint32_t s_wh[RS_WARPS][256];         // per-warp digit counts -> per-warp digit offsets
     __shared__ uint32_t s_warp[32];
+    __shared__ uint32_t s_k[RS_TILE];
+    __shared__ uint32_t s_v[HAS_VALS ? RS_TILE : 1];
     const int seg = blockIdx.y, tile = blockIdx.x;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    uint32_t dbase;   // digits below this one, in this segment
-    block_exclusive_scan<RS_THREADS>(dtot[seg * 256 + threadIdx.x], s_warp, dbase);
-    s_base[threadIdx.x] = dbase + offs[((int64_t)seg * 256 + threadIdx.x) * tiles + tile];
     const uint32_t* k = kin + (int64_t)seg * m;
     const uint32_t* v = HAS_VALS ? vin + (int64_t)seg * m : nullptr;
     uint32_t* ko = kout + (int64_t)seg * m;
     uint32_t* vo = HAS_VALS ? vout + (int64_t)seg * m : nullptr;
     const int64_t base = (int64_t)tile * RS_TILE;
+    for (int i = lane; i < 256; i += 32) s_wh[w][i] = 0;
+    __syncwarp();
+    constexpr int R = RS_TILE / RS_THREADS;          // 16 rounds of 32 keys per warp
+    uint32_t key[R], val[R], loc[R];
     const uint32_t lt = lanemask_lt();
-    for (int j = 0; j < RS_IPT; ++j) {
 #pragma unroll
-        for (int ww = 0; ww < RS_WARPS; ++ww) s_wcnt[ww][threadIdx.x] = 0;
-        __syncthreads();
-        int64_t e = base + (int64_t)j * RS_THREADS + threadIdx.x;
-        bool ok = e < m;
-        uint32_t key = ok ? k[e] : 0u;
-        uint32_t val = (HAS_VALS && ok) ? v[e] : 0u;
-        uint32_t dig = ok ? ((key >> shift) & 255u) : 256u;
-        uint32_t peers = __match_any_sync(0xffffffffu, dig);
-        uint32_t rank = __popc(peers & lt);
-        if (ok && rank == 0) s_wcnt[w][dig] = __popc(peers);
-        __syncthreads();
-        if (ok) {
-            uint32_t pos = s_base[dig] + rank;
-            for (int ww = 0; ww < w; ++ww) pos += s_wcnt[ww][dig];
-            ko[pos] = key;
-            if (HAS_VALS) vo[pos] = val;
+    for (int j = 0; j < R; ++j) {
+        const int64_t e = base + (int64_t)w * (32 * R) + 32 * j + lane;
+        const bool ok = e < m;
+        key[j] = ok ? k[e] : 0u;
+        val[j] = (HAS_VALS && ok) ? v[e] : 0u;
+        const uint32_t dig = ok ? ((key[j] >> shift) & 255u) : 256u;
+        const uint32_t peers = __match_any_sync(0xffffffffu, dig);
+        const int leader = __ffs(peers) - 1;
+        uint32_t old = 0;
+        if (ok && lane == leader) {
+            old = s_wh[w][dig];
+            s_wh[w][dig] = old + __popc(peers);
         }
-        __syncthreads();
-        uint32_t add = 0;
+        old = __shfl_sync(0xffffffffu, old, leader);
+        loc[j] = ok ? old + __popc(peers & lt) : 0xFFFFFFFFu;   // rank among the warp's keys of this digit
+        __syncwarp();
+    }
+    __syncthreads();
+    // per digit (thread = digit): warps' exclusive offsets, the tile's count, global base
+    {
+        const int d = threadIdx.x;
+        uint32_t run = 0;
 #pragma unroll
-        for (int ww = 0; ww < RS_WARPS; ++ww) add += s_wcnt[ww][threadIdx.x];
-        s_base[threadIdx.x] += add;
-        // the next iteration's zeroing is ordered after this read by the barrier below
-        __syncthreads();
+        for (int ww = 0; ww < RS_WARPS; ++ww) {
+            const uint32_t c = s_wh[ww][d];
+            s_wh[ww][d] = run;
+            run += c;
+        }
+        uint32_t tds;
+        block_exclusive_scan<RS_THREADS>(run, s_warp, tds);          // slots of the digits below d
+        s_tds[d] = tds;
+        uint32_t dbase;                                               // this segment's keys of lower digits
+        block_exclusive_scan<RS_THREADS>(dtot[seg * 256 + d], s_warp, dbase);
+        s_base[d] = dbase + offs[((int64_t)seg * 256 + d) * tiles + tile];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+        if (loc[j] != 0xFFFFFFFFu) {
+            const uint32_t d = (key[j] >> shift) & 255u;
+            const uint32_t slot = s_tds[d] + s_wh[w][d] + loc[j];
+            s_k[slot] = key[j];
+            if (HAS_VALS) s_v[slot] = val[j];
+        }
+    }
+    __syncthreads();
+    const int cnt = (int)(m - base < RS_TILE ? m - base : (int64_t)RS_TILE);
+    for (int i = threadIdx.x; i < cnt; i += RS_THREADS) {
+        const uint32_t kk = s_k[i];
+        const uint32_t d = (kk >> shift) & 255u;
+        const uint32_t pos = s_base[d] + (uint32_t)i - s_tds[d];
+        ko[pos] = kk;
+        if (HAS_VALS) vo[pos] = s_v[i];
     }
 }
 

@@ -7,15 +7,18 @@
 // bits, so MMA(x) = MMA(trunc(x)), and lo = x - trunc(x) (exact in fp32) carries the rest:
 // P ~= trunc(x).A + trunc(lo).A with |error| <~ 2^-20 ||x|| ||a||  ("2xTF32").
 //
-// Kernel (persistent, one CTA per SM, 8 warps, tiles of 128 rows):
-//   warp 0      TMA producer: X k-blocks [128 rows x 32 fp32] (SWIZZLE_128B) into a ring
-//               of stages; the whole (L*K_pad x ld) hash matrix once (resident in smem).
-//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer (M=128, N=L*K_pad, K=8):
-//               per k-block 4 MMAs on x and 4 on lo, accumulating in TMEM; tcgen05.commit
-//               frees the stage and, after the last k-block, hands the tile to the epilogue.
-//   warps 2-3   converters: lo = x - trunc_tf32(x) into a twin buffer of the same swizzled
-//               layout, fence.proxy.async, arrive.
-//   warps 4-7   epilogue: tcgen05.ld (32x32b) of the double-buffered accumulator, rows to P.
+// Kernel (persistent, one CTA per SM, 18 warps = 576 threads, tiles of 128 rows):
+//   warp 0          TMA producer: X k-blocks [128 rows x 32 fp32] (SWIZZLE_128B) into a ring of
+//                   stages; the whole (L*K_pad x ld) hash matrix once (resident in smem), or one
+//                   k-block of it per stage beside the rows when it does not fit (streamA, d = 960).
+//   warp 1          TMEM allocator + single-thread tcgen05.mma issuer (M=128, N=L*K_pad, K=8):
+//                   per k-block 4 MMAs on x and 4 on lo, accumulating in TMEM; tcgen05.commit
+//                   frees the stage and, after the last k-block, hands the tile to the epilogue.
+//   warps 2-3, 12-17  8 converter warps: lo = x - trunc_tf32(x) into a twin buffer of the same
+//                   swizzled layout (+ ||x||^2 of the rows, the non-finite flag),
+//                   fence.proxy.async, arrive.
+//   warps 4-11      8 epilogue warps: tcgen05.ld (32x32b) of the double-buffered accumulator ->
+//                   projections, or (fused Alg. 1) 8-bit codes by a branch-free Eytzinger search.
 #include <cuda.h>
 
 #include <cstdlib>

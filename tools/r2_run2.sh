@@ -27,3 +27,5 @@ for cfg in 2 5; do
 done
 timeout 2400 python -m pytest tests -m "gpu and not slow" -q -rf -s > gpurun_out/gpu_tests_fast.log 2>&1; echo "fast tests exit $?"; tail -12 gpurun_out/gpu_tests_fast.log
 timeout 3000 python -m pytest tests -m "gpu and slow" -q -rf -s > gpurun_out/gpu_tests_slow.log 2>&1; echo "slow tests exit $?"; tail -12 gpurun_out/gpu_tests_slow.log
+timeout 900 python tools/vcost_check.py 3 5 > gpurun_out/vcost.log 2>&1; echo "vcost exit $?"; tail -6 gpurun_out/vcost.log
+timeout 2400 bash tools/sanitize.sh > gpurun_out/sanitize.log 2>&1; echo "sanitize exit $?"; cat gpurun_out/sanitize.log

@@ -245,6 +245,50 @@ template <> struct QuantSpec<8> { static constexpr uint32_t QT = 2048, CAP = 409
 // sure-accept limit QT - 17, so such a point is always decided in fp32 (no result changes).
 template <> struct QuantSpec<16> { static constexpr uint32_t QT = 128, CAP = 127; };
 
+// The 16-query box test (K = 16, G = 16 8-bit tables with region flags, see k_range_filter):
+// bit g set iff query g's quantised lower bound of the box [lo, hi] is <= QT (128).  Per dim
+// the rows D_j[lo] and D_j[hi] are masked by the s < lo / s >= hi query sets (sign-replicating
+// byte permutes of the flags), pair sums of 7-bit terms in 8-bit lanes widened into 16-bit lanes.
+__device__ __forceinline__ uint32_t simd16_box_mask(const uint4* __restrict__ s_qe, int N_r, uint4 lo4, uint4 hi4) {
+    uint32_t acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+    for (int jp = 0; jp < 8; ++jp) {
+        uint32_t tw[2][4];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            const int j = 2 * jp + u, sh = 8 * (j & 3);
+            const uint32_t wl = (j >> 2) == 0 ? lo4.x : (j >> 2) == 1 ? lo4.y : (j >> 2) == 2 ? lo4.z : lo4.w;
+            const uint32_t wh = (j >> 2) == 0 ? hi4.x : (j >> 2) == 1 ? hi4.y : (j >> 2) == 2 ? hi4.z : hi4.w;
+            const uint32_t cl = (wl >> sh) & 255u, ch = (wh >> sh) & 255u;
+            const uint4 dl = s_qe[j * N_r + cl];
+            const uint4 dh = s_qe[j * N_r + ch];
+            const uint32_t dlw[4] = {dl.x, dl.y, dl.z, dl.w}, dhw[4] = {dh.x, dh.y, dh.z, dh.w};
+#pragma unroll
+            for (int w = 0; w < 4; ++w) {
+                const uint32_t ml = prmt_sign(dlw[w]);                  // 0xFF: s < lo
+                const uint32_t mh = prmt_sign(dhw[w]);                  // 0xFF: s < hi
+                // D_j[lo] where s < lo (its flag bit cleared), | D_j[hi] where s >= hi
+                // (flag clear there, so bit 7 is already 0): two 3-input logic ops
+                const uint32_t tl = dlw[w] & ml & 0x7F7F7F7Fu;
+                tw[u][w] = tl | (dhw[w] & ~mh);
+            }
+        }
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+            const uint32_t p2 = tw[0][w] + tw[1][w];     // 7-bit terms: no carry out of a byte
+            acc[2 * w] += p2 & 0x00FF00FFu;
+            acc[2 * w + 1] += __byte_perm(p2, 0u, 0x4341);
+        }
+    }
+    uint32_t m = 0;
+#pragma unroll
+    for (int g = 0; g < 16; ++g) {
+        const uint32_t sg = (acc[2 * (g >> 2) + (g & 1)] >> (16 * ((g >> 1) & 1))) & 0xFFFFu;
+        m |= (sg <= QuantSpec<16>::QT ? 1u : 0u) << g;
+    }
+    return m;
+}
+
 struct RFArgs {
     const uint8_t* tcodes;      // tree t: [n][K]
     const uint16_t* ptl;        // tree t: [n] leaf within tile
@@ -435,44 +479,8 @@ __global__ void __launch_bounds__(RF_THREADS, RF_CTAS) k_range_filter(RFArgs a) 
             if (KT == 16 && G == 16 && !(a.dbg & 1)) {
                 // all 16 queries at once (same 16-bit lane layout as the SIMD point screen): per
                 // dim, the rows D_j[lo] and D_j[hi] masked by the s < lo / s > hi query sets
-                const uint4 lo4 = *reinterpret_cast<const uint4*>(a.lo + l * 16);
-                const uint4 hi4 = *reinterpret_cast<const uint4*>(a.hi + l * 16);
-                uint32_t acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-#pragma unroll
-                for (int jp = 0; jp < 8; ++jp) {
-                    uint32_t tw[2][4];
-#pragma unroll
-                    for (int u = 0; u < 2; ++u) {
-                        const int j = 2 * jp + u, sh = 8 * (j & 3);
-                        const uint32_t wl = (j >> 2) == 0 ? lo4.x : (j >> 2) == 1 ? lo4.y : (j >> 2) == 2 ? lo4.z : lo4.w;
-                        const uint32_t wh = (j >> 2) == 0 ? hi4.x : (j >> 2) == 1 ? hi4.y : (j >> 2) == 2 ? hi4.z : hi4.w;
-                        const uint32_t cl = (wl >> sh) & 255u, ch = (wh >> sh) & 255u;
-                        const uint4 dl = s_qe[j * N_r + cl];
-                        const uint4 dh = s_qe[j * N_r + ch];
-                        const uint32_t dlw[4] = {dl.x, dl.y, dl.z, dl.w}, dhw[4] = {dh.x, dh.y, dh.z, dh.w};
-#pragma unroll
-                        for (int w = 0; w < 4; ++w) {
-                            const uint32_t ml = prmt_sign(dlw[w]);                  // 0xFF: s < lo
-                            const uint32_t mh = prmt_sign(dhw[w]);                  // 0xFF: s < hi
-                            // D_j[lo] where s < lo (its flag bit cleared), | D_j[hi] where s >= hi
-                            // (flag clear there, so bit 7 is already 0): two 3-input logic ops
-                            const uint32_t tl = dlw[w] & ml & 0x7F7F7F7Fu;
-                            tw[u][w] = tl | (dhw[w] & ~mh);
-                        }
-                    }
-#pragma unroll
-                    for (int w = 0; w < 4; ++w) {
-                        const uint32_t p2 = tw[0][w] + tw[1][w];     // 7-bit terms: no carry out of a byte
-                        acc[2 * w] += p2 & 0x00FF00FFu;
-                        acc[2 * w + 1] += __byte_perm(p2, 0u, 0x4341);
-                    }
-                }
-#pragma unroll
-                for (int g = 0; g < G; ++g) {
-                    const uint32_t sg = (acc[2 * (g >> 2) + (g & 1)] >> (16 * ((g >> 1) & 1))) & 0xFFFFu;
-                    m |= (sg <= QT ? 1u : 0u) << g;
-                }
-                m &= tm;
+                m = simd16_box_mask(s_qe, N_r, *reinterpret_cast<const uint4*>(a.lo + l * 16),
+                                    *reinterpret_cast<const uint4*>(a.hi + l * 16)) & tm;
             } else if (KT == 16) {
                 const uint4 lo4 = *reinterpret_cast<const uint4*>(a.lo + l * 16);
                 const uint4 hi4 = *reinterpret_cast<const uint4*>(a.hi + l * 16);
@@ -815,6 +823,105 @@ __global__ void __launch_bounds__(RF_THREADS, RF_CTAS) k_range_filter(RFArgs a) 
     }
 }
 
+// ---- tile-pair mode (CELL, K = 16, N_r = 256): the first stage of a two-level filter for
+//      indexes whose per-query reach is a small fraction of the tiles (large n, small radius).
+//      CTA = 16-query group (its interleaved table, as k_range_filter); a warp takes 32 tiles
+//      at a time from the group's counter, lane = tile: the 16-query bound of the tile's box
+//      (union of its leaves' tight boxes -- never above a member leaf's bound), and every
+//      (query, tile) pair that passes is appended to the query's list.  k_leaf_points then
+//      expands each listed tile into its leaves (one warp per tile, lane = leaf) with the
+//      query's own 12-bit table -- only the pairs a query reaches are bounded, instead of every
+//      leaf of every tile any of the 16 queries reaches (the group's union).
+__global__ void __launch_bounds__(RF_THREADS, RF_CTAS) k_tile_pairs(RFArgs a) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    uint4* s_qe = reinterpret_cast<uint4*>(smem);                 // [16][256] x 16 B
+    constexpr int G = 16, N_r = 256, K = 16;
+    __shared__ int s_q[G];
+    __shared__ unsigned int s_ctr[G][2];
+    __shared__ uint32_t s_cnt[RF_THREADS / 32][32];                // per warp: [0,16) counts, [16,32) bases
+    __shared__ uint32_t s_slot[RF_THREADS / 32][16];
+    __shared__ int s_active_mask;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (threadIdx.x < G) {
+        const int gi = blockIdx.x * G + threadIdx.x;
+        int q = -1;
+        if (gi < (a.dna ? *a.dna : a.na)) {
+            q = a.act[gi];
+            if (a.qs[q].status != ST_ACTIVE) q = -1;
+        }
+        s_q[threadIdx.x] = q;
+        s_ctr[threadIdx.x][0] = s_ctr[threadIdx.x][1] = 0;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int m = 0;
+        for (int g = 0; g < G; ++g) m |= (s_q[g] >= 0) << g;
+        s_active_mask = m;
+    }
+    {
+        const uint4* gt = a.gtab + (int64_t)blockIdx.x * K * N_r;
+        for (int i = threadIdx.x; i < K * N_r; i += RF_THREADS) s_qe[i] = gt[i];
+    }
+    __syncthreads();
+    const uint32_t amask = (uint32_t)s_active_mask;
+    if (amask == 0) return;
+    uint32_t c_lt = 0, c_lp = 0;
+    uint32_t* w_cnt = s_cnt[warp];
+    uint32_t* w_slot = s_slot[warp];
+    unsigned int* next = a.tctr + blockIdx.x;
+    for (;;) {
+        int64_t t0 = 0;
+        if (lane == 0) t0 = a.tile_begin + 32 * (int64_t)atomicAdd(next, 1);
+        t0 = __shfl_sync(0xffffffffu, t0, 0);
+        if (t0 >= a.tile_end) break;
+        const int64_t T = t0 + lane;
+        uint32_t m = 0;
+        if (T < a.tile_end) {
+            m = simd16_box_mask(s_qe, N_r, *reinterpret_cast<const uint4*>(a.tile_lo + T * 16),
+                                *reinterpret_cast<const uint4*>(a.tile_hi + T * 16)) & amask;
+            c_lt += __popc(amask);
+            c_lp += __popc(m);
+        }
+        // append the (query, tile) pairs: per-query counts in the warp, one reservation per query
+        // in its global list, then each lane writes its own pairs
+        if (lane < 16) { w_cnt[lane] = 0; w_slot[lane] = 0; }
+        __syncwarp();
+        for (uint32_t mm = m; mm; mm &= mm - 1) atomicAdd(&w_cnt[__ffs(mm) - 1], 1u);
+        __syncwarp();
+        if (lane < 16) {
+            const uint32_t c_ = w_cnt[lane];
+            w_cnt[16 + lane] = c_ ? atomicAdd(a.pcnt + s_q[lane], c_) : 0u;
+        }
+        __syncwarp();
+        for (uint32_t mm = m; mm; mm &= mm - 1) {
+            const int g = __ffs(mm) - 1;
+            const uint32_t sl = w_cnt[16 + g] + atomicAdd(&w_slot[g], 1u);
+            a.plist[(int64_t)s_q[g] * a.pcap + sl] = (uint32_t)T;
+        }
+        __syncwarp();
+    }
+    // counters (tile bounds count as box bounds: leaves_tested / leaves_passed), per group split
+    // evenly over its active queries as in k_range_filter
+    for (int o = 16; o > 0; o >>= 1) {
+        c_lt += __shfl_xor_sync(0xffffffffu, c_lt, o);
+        c_lp += __shfl_xor_sync(0xffffffffu, c_lp, o);
+    }
+    if (lane == 0) {
+        const int na_ = max(1, __popc(amask));
+        for (int g = 0; g < G; ++g)
+            if ((amask >> g) & 1) {
+                atomicAdd(&s_ctr[g][0], c_lt / na_);
+                atomicAdd(&s_ctr[g][1], c_lp / na_);
+            }
+    }
+    __syncthreads();
+    if (threadIdx.x < G && s_q[threadIdx.x] >= 0) {
+        unsigned long long* c = a.ctr + (int64_t)s_q[threadIdx.x] * NCTR;
+        atomicAdd(c + 0, (unsigned long long)s_ctr[threadIdx.x][0]);
+        atomicAdd(c + 1, (unsigned long long)s_ctr[threadIdx.x][1]);
+    }
+}
+
 // ---- sparse tiles, CELL mode: the points of each (query, reachable leaf) pair the range filter
 //      listed, one warp per leaf, lane per point.  Block = one query (its fp32 table of tree t and a
 //      12-bit quantised lower-bound copy in shared memory, ~24 KB: many resident blocks per SM);
@@ -850,6 +957,8 @@ struct LPArgs {
     float rho2, inv_rd;         // inv_rd = 2048/rho^2 rounded down
     int t, L, K, N_r;
     unsigned long long* ctr;
+    const uint32_t* tile_leaf;  // non-null: the lists hold tiles (k_tile_pairs), each expanded into its
+                                // leaves here (one tile per warp chunk, lane = leaf; LPG = 32)
 };
 
 constexpr int LP_THREADS = 256;     // threads per pair-kernel block (512 with half the blocks: slower)
@@ -937,14 +1046,23 @@ __global__ void __launch_bounds__(LP_THREADS) k_leaf_points(LPArgs a) {
         sqn -= nb;
         __syncwarp();
     };
+    uint32_t lt = 0, lp = 0;                         // tile mode: leaf bounds evaluated / passed
     for (;;) {
         uint32_t ck = 0;
         if (lane == 0) ck = atomicAdd(a.ptake + q, 1u);
-        const uint32_t e0 = __shfl_sync(0xffffffffu, ck, 0) * LPG;
+        const uint32_t e0 = __shfl_sync(0xffffffffu, ck, 0) * (a.tile_leaf ? 1u : (uint32_t)LPG);
         if (e0 >= np) break;
         uint32_t my_p0 = 0, my_sz = 0;
-        if (lane < LPG && e0 + lane < np) {
-            const uint32_t l = pl[e0 + lane];
+        int64_t my_l = -1;
+        if (a.tile_leaf) {
+            const uint32_t T = pl[e0];
+            const uint32_t lb0 = a.tile_leaf[T], le0 = a.tile_leaf[T + 1];
+            if (lane < LPG && lb0 + lane < le0) my_l = lb0 + lane;
+        } else if (lane < LPG && e0 + lane < np) {
+            my_l = pl[e0 + lane];
+        }
+        if (my_l >= 0) {
+            const uint32_t l = (uint32_t)my_l;
             my_p0 = a.leaf_off[l];
             my_sz = a.leaf_off[l + 1] - my_p0;
             // the leaf's box bound in the finer 12-bit table: the filter's 8-bit test passes
@@ -967,6 +1085,8 @@ __global__ void __launch_bounds__(LP_THREADS) k_leaf_points(LPArgs a) {
                     lb += s_e[j * N_r + min(max(s_qx[j], (int)a.lo[(int64_t)l * K + j]), (int)a.hi[(int64_t)l * K + j])];
             }
             if (lb > 2048u) my_sz = 0;
+            ++lt;
+            lp += my_sz != 0;
         }
         if (a.sb_off) {
             // second level: the leaves' sub-boxes (kSubBox consecutive points each), packed 32 per
@@ -974,7 +1094,7 @@ __global__ void __launch_bounds__(LP_THREADS) k_leaf_points(LPArgs a) {
             // sub-boxes' points are screened per step (lane = (sub-box, point))
             const uint32_t my_nsb = (my_sz + kSubBox - 1) / kSubBox;
             uint32_t my_sb0 = 0;
-            if (lane < LPG && my_sz) my_sb0 = a.sb_off[pl[e0 + lane]];
+            if (my_l >= 0 && my_sz) my_sb0 = a.sb_off[my_l];
             uint32_t incl = my_nsb;
 #pragma unroll
             for (int o = 1; o < LPG; o <<= 1) {
@@ -1097,6 +1217,12 @@ __global__ void __launch_bounds__(LP_THREADS) k_leaf_points(LPArgs a) {
         tested += __shfl_xor_sync(0xffffffffu, tested, o);
         passed += __shfl_xor_sync(0xffffffffu, passed, o);
         sbt += __shfl_xor_sync(0xffffffffu, sbt, o);
+        lt += __shfl_xor_sync(0xffffffffu, lt, o);
+        lp += __shfl_xor_sync(0xffffffffu, lp, o);
+    }
+    if (a.tile_leaf && lane == 0 && lt) {
+        atomicAdd(a.ctr + (int64_t)q * NCTR + 0, (unsigned long long)lt);
+        atomicAdd(a.ctr + (int64_t)q * NCTR + 1, (unsigned long long)lp);
     }
     if (lane == 0) { atomicAdd(&s_tested, tested); atomicAdd(&s_passed, passed); if (sbt) atomicAdd(&s_sbt, sbt); }
     __syncthreads();
@@ -2383,8 +2509,14 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
     Scratch s_q12(st, use_pairs ? sizeof(uint16_t) * (size_t)(qb * LK * ix.N_r) : 0);
     const bool lp_fixed = ix.K == 16 && ix.N_r == 256;
     static const int lp_g = std::getenv("DETLSH_LP_G") ? std::atoi(std::getenv("DETLSH_LP_G")) : 16;
-    auto k_leaf_points_sel = lp_fixed ? (lp_g == 8 ? k_leaf_points<16, 256, 8> : k_leaf_points<16, 256, 16>)
-                                      : k_leaf_points<0, 0, 16>;
+    // two-level filter (k_tile_pairs + tile-mode k_leaf_points): DETLSH_TILE_PAIRS = 1 on, 0 off
+    static const int tp_env = std::getenv("DETLSH_TILE_PAIRS") ? std::atoi(std::getenv("DETLSH_TILE_PAIRS")) : 0;
+    const bool tile_pairs = tp_env == 1 && use_pairs && lp_fixed && RF_G == 16 && rf_dyn && !a.lb_order;
+    auto k_leaf_points_sel = tile_pairs ? k_leaf_points<16, 256, 32>
+                             : lp_fixed ? (lp_g == 8 ? k_leaf_points<16, 256, 8> : k_leaf_points<16, 256, 16>)
+                                        : k_leaf_points<0, 0, 16>;
+    lpa.tile_leaf = tile_pairs ? ix.tile_leaf.as<uint32_t>() : nullptr;
+    if (tile_pairs) ensure_dyn_smem_fn(k_tile_pairs, rf_smem);
     const size_t lp_dyn = lp_fixed ? 0 : lp_smem;
     if (use_pairs && !lp_fixed)
         ensure_dyn_smem_fn(k_leaf_points_sel, lp_smem);
@@ -2618,7 +2750,10 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
                                                                            : (rf_dyn ? 1 : 3);
                 const int stripes = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(ntiles, RF_THREADS / 32),
                                                                                  (148 * RF_CTAS * rf_waves + groups / 2) / groups));
-                DL_LAUNCH(k_range_filter_sel, dim3((unsigned)groups, (unsigned)stripes), RF_THREADS, rf_smem, st, ra);
+                if (tile_pairs)
+                    DL_LAUNCH(k_tile_pairs, dim3((unsigned)groups, (unsigned)stripes), RF_THREADS, rf_smem, st, ra);
+                else
+                    DL_LAUNCH(k_range_filter_sel, dim3((unsigned)groups, (unsigned)stripes), RF_THREADS, rf_smem, st, ra);
                 if (use_pairs) {
                     lpa.act = fa;
                     lpa.dna = dnf;

@@ -81,8 +81,9 @@ typedef struct {
     int32_t pad;
     int64_t n_cand;      /* |S| at termination */
     double  r_final;     /* r of the last round */
-    int64_t leaves_tested;   /* leaf lower bounds evaluated (all rounds, all trees) */
-    int64_t leaves_passed;   /* leaves with LB <= eps r */
+    int64_t leaves_tested;   /* box lower bounds evaluated (all rounds, all trees): leaves, and in
+                                the two-level filter (DETLSH_TILE_PAIRS) query tiles as well */
+    int64_t leaves_passed;   /* boxes with LB <= eps r */
     int64_t points_tested;   /* points of qualifying leaves examined */
     int64_t points_passed;   /* points with cell LB <= eps r (before de-duplication) */
     int64_t subboxes_tested; /* sub-box (runs of 8 leaf points) lower bounds evaluated by the pair kernel */

@@ -51,6 +51,10 @@ struct TcShape {
     int streamA;      // 1: the hash matrix does not fit in shared memory -- its k-block is loaded
                       // into every stage beside the rows (re-read from L2 per tile)
     int dbg;          // experiments only (DETLSH_PROJ_DEBUG): 1 no encode search, 2 no conversion, 4 no MMA
+    int ta;           // 1: the lo parts go to tensor memory (tcgen05.st by the converters) and the second
+                      // MMA of each k-step reads its A operand from there -- no lo buffer in shared
+                      // memory (more stages), no shared-memory store / MMA re-read of it
+    uint32_t lo_col;  // ta: first TMEM column of the S lo buffers (32 columns each)
 };
 
 __global__ void __launch_bounds__(TC_THREADS, 1)
@@ -65,8 +69,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     const int S = sh.stages;
     unsigned char* sB = base;                                            // nkb (or S if streamA) x [npad][128 B]
     unsigned char* sX = sB + (size_t)(sh.streamA ? S : sh.nkb) * sh.npad * 128;   // S x 16 KB
-    unsigned char* sL = sX + (size_t)S * TC_STAGE_BYTES;                  // S x 16 KB (lo parts)
-    float* sT = reinterpret_cast<float*>(sL + (size_t)S * TC_STAGE_BYTES);   // encode table [LK][2^lgP] (Eytzinger)
+    unsigned char* sL = sX + (size_t)S * TC_STAGE_BYTES;                  // S x 16 KB (lo parts; none if ta)
+    float* sT = reinterpret_cast<float*>(sL + (sh.ta ? 0 : (size_t)S * TC_STAGE_BYTES));   // encode table [LK][2^lgP] (Eytzinger)
+    __shared__ float s_np[2][TC_M];       // ta: ||x||^2 of the second half of each row's columns
     const int tab_floats = sh.N_r > 0 ? sh.LK << sh.lgP : 0;
     uint64_t* bars = reinterpret_cast<uint64_t*>(sT + tab_floats);
     uint64_t* full = bars;              // [S] TMA -> converters, MMA
@@ -143,12 +148,23 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                     const uint32_t ax = smem_u32(sX + (size_t)s * TC_STAGE_BYTES);
                     const uint32_t al = smem_u32(sL + (size_t)s * TC_STAGE_BYTES);
                     const uint32_t bb = smem_u32(sB + (size_t)(sh.streamA ? s : kb) * sh.npad * 128);
-                    if (!(sh.dbg & 4))
+                    if (!(sh.dbg & 4)) {
+                        if (sh.ta) {
+                            const uint32_t ta_lo = tmem_base + sh.lo_col + (uint32_t)(s * TC_KB);
 #pragma unroll
-                    for (int k = 0; k < TC_KB / 8; ++k) {        // K = 8 tf32 per MMA = 32 bytes
-                        const uint64_t bd = desc_sw128(bb + k * 32);
-                        mma_tf32(d_tmem, desc_sw128(ax + k * 32), bd, idesc, (kb | k) ? 1u : 0u);
-                        mma_tf32(d_tmem, desc_sw128(al + k * 32), bd, idesc, 1u);
+                            for (int k = 0; k < TC_KB / 8; ++k) {
+                                const uint64_t bd = desc_sw128(bb + k * 32);
+                                mma_tf32(d_tmem, desc_sw128(ax + k * 32), bd, idesc, (kb | k) ? 1u : 0u);
+                                mma_tf32_ta(d_tmem, ta_lo + (uint32_t)(8 * k), bd, idesc, 1u);
+                            }
+                        } else {
+#pragma unroll
+                            for (int k = 0; k < TC_KB / 8; ++k) {        // K = 8 tf32 per MMA = 32 bytes
+                                const uint64_t bd = desc_sw128(bb + k * 32);
+                                mma_tf32(d_tmem, desc_sw128(ax + k * 32), bd, idesc, (kb | k) ? 1u : 0u);
+                                mma_tf32(d_tmem, desc_sw128(al + k * 32), bd, idesc, 1u);
+                            }
+                        }
                     }
                     mma_commit(&empty[s]);                   // stage free once these MMAs complete
                     if (++s == S) { s = 0; ph ^= 1; }
@@ -157,6 +173,49 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                 if (++buf == 2) { buf = 0; tph ^= 1; }
             }
         }
+    } else if ((warp < 4 || warp >= 12) && sh.ta) {
+        // converters, tensor-memory form: thread = row (32 qd + lane) of its warp's TMEM lane quarter
+        // qd, half h of the k-block's 32 columns (the quarter's two converter warps split them):
+        // x from the 128B-swizzled stage (chunk c of row r at c ^ (r & 7)), lo = x - trunc_tf32(x)
+        // stored to 16 TMEM columns, waited, fenced, then the stage's conversion barrier.
+        const int qd = warp & 3, h = warp >= 14 ? 1 : 0;
+        const int r = qd * 32 + lane;
+        int s = 0;
+        uint32_t ph = 0;
+        bool bad = false;
+        int par = 0;
+        const uint32_t trow = tmem_base + ((uint32_t)(qd * 32) << 16) + sh.lo_col + (uint32_t)(16 * h);
+        for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+            float nacc = 0.f;
+            for (int kb = 0; kb < sh.nkb; ++kb) {
+                mbar_wait(&full[s], ph);
+                const unsigned char* rowp = sX + (size_t)s * TC_STAGE_BYTES + (size_t)r * 128;
+                float lo[16];
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    const float4 x = *reinterpret_cast<const float4*>(rowp + (((4 * h + c) ^ (r & 7)) << 4));
+                    const float xs[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        lo[4 * c + e] = xs[e] - __uint_as_float(__float_as_uint(xs[e]) & 0xFFFFE000u);
+                        bad |= !isfinite(xs[e]);
+                        nacc = fmaf(xs[e], xs[e], nacc);
+                    }
+                }
+                tmem_st16(trow + (uint32_t)(s * TC_KB), lo);
+                tc_fence_before();
+                mbar_arrive(&conv[s]);
+                if (++s == S) { s = 0; ph ^= 1; }
+            }
+            if (xnorm) {   // the row's two halves: h = 1 hands its sum over, h = 0 writes the norm
+                if (h) s_np[par][r] = nacc;
+                asm volatile("bar.sync 2, 256;" ::: "memory");   // the 8 converter warps
+                const int64_t row = tile * TC_M + r;
+                if (!h && row < sh.m) xnorm[row] = nacc + s_np[par][r];
+                par ^= 1;
+            }
+        }
+        if (bad) atomicOr(nonfinite, 1);
     } else if (warp < 4 || warp >= 12) {
         // converters (TC_CONV threads): lo = x - trunc_tf32(x), same swizzled offsets.  Thread t sees
         // float4 t + TC_CONV m (m < TC_CM) of every stage, i.e. rows t/8 + (TC_CONV/8) m (swizzling
@@ -311,24 +370,31 @@ static bool launch_tc(const Index& ix, const float* d_X, int64_t ld, int64_t m, 
     const size_t abytes = (size_t)sh.npad * 128;                 // one k-block of the hash matrix
     const size_t tbytes = B ? sizeof(float) * ((size_t)ix.LK << sh.lgP) : 0;
     const size_t fixed = 1024 /*align*/ + 256 /*barriers*/;
-    const size_t budget = 227 * 1024;
+    const size_t budget = 226 * 1024;     // + 1 KB of static shared memory (s_np) within the 227 KB
     static const int force_stream = std::getenv("DETLSH_STREAM_A") ? std::atoi(std::getenv("DETLSH_STREAM_A")) : 0;
     static const int pdbg = std::getenv("DETLSH_PROJ_DEBUG") ? std::atoi(std::getenv("DETLSH_PROJ_DEBUG")) : 0;
     sh.dbg = pdbg;
-    sh.streamA = (force_stream || (size_t)sh.nkb * abytes + tbytes + fixed + 2 * 2 * TC_STAGE_BYTES > budget) ? 1 : 0;
+    // DETLSH_PROJ_TA: 1 = lo parts in tensor memory (default off until measured), 0 = shared memory
+    static const int ta_env = std::getenv("DETLSH_PROJ_TA") ? std::atoi(std::getenv("DETLSH_PROJ_TA")) : 0;
+    sh.lo_col = (uint32_t)(2 * sh.npad);
+    // accumulators (2 x npad columns) + one 32-column lo buffer per stage within 512 columns
+    sh.ta = (ta_env && (int)((512 - sh.lo_col) / TC_KB) >= 2) ? 1 : 0;
+    const int spb = sh.ta ? 1 : 2;                               // 16 KB stage buffers per stage
+    sh.streamA = (force_stream || (size_t)sh.nkb * abytes + tbytes + fixed + 2 * spb * TC_STAGE_BYTES > budget) ? 1 : 0;
+    const int max_st = sh.ta ? std::min<int>(8, (int)((512 - sh.lo_col) / TC_KB)) : 6;
     if (!sh.streamA) {
         const size_t bbytes = (size_t)sh.nkb * abytes;
-        sh.stages = (int)std::min<size_t>(6, (budget - bbytes - tbytes - fixed) / (2 * TC_STAGE_BYTES));
+        sh.stages = (int)std::min<size_t>(max_st, (budget - bbytes - tbytes - fixed) / (spb * TC_STAGE_BYTES));
     } else {
-        const size_t per = 2 * TC_STAGE_BYTES + abytes;
+        const size_t per = spb * TC_STAGE_BYTES + abytes;
         if (tbytes + fixed + 2 * per > budget) return false;
-        sh.stages = (int)std::min<size_t>(6, (budget - tbytes - fixed) / per);
+        sh.stages = (int)std::min<size_t>(max_st, (budget - tbytes - fixed) / per);
     }
     const size_t bbytes = (size_t)(sh.streamA ? sh.stages : sh.nkb) * abytes;
     uint32_t cols = 32;
-    while (cols < (uint32_t)(2 * sh.npad)) cols <<= 1;
+    while (cols < (uint32_t)(2 * sh.npad + (sh.ta ? TC_KB * sh.stages : 0))) cols <<= 1;
     sh.tmem_cols = cols;
-    const size_t smem = bbytes + tbytes + (size_t)sh.stages * 2 * TC_STAGE_BYTES + fixed;
+    const size_t smem = bbytes + tbytes + (size_t)sh.stages * spb * TC_STAGE_BYTES + fixed;
     CUtensorMap mx, ma;
     make_map(&mx, d_X, m, (int)ld, TC_M);
     make_map(&ma, ix.A.as<float>(), ix.LK, (int)ld, sh.npad);

@@ -768,3 +768,39 @@ def test_merge_topk_device_tensors(G, nq, k):
         assert od[q].tolist() == [p[0] for p in pairs]
     ri, rd = O.merge_topk(ids, d, k)
     assert np.array_equal(oi, ri) and np.array_equal(od, rd)
+
+
+@pytest.mark.parametrize("ta", ["0", "1"])
+def test_projection_variants(tmp_path, ta):
+    """The tensor-core projection with the lo parts in shared memory (default) or in tensor memory
+    (DETLSH_PROJ_TA=1: converters tcgen05.st them, the second MMA reads A from TMEM): projections
+    within 1e-4 of numpy fp64 (AMB-2), fused codes = the encode of those projections except
+    near-breakpoint values, and the exact-kNN reduction (beta >= 1, huge radius) through the
+    tensor-core verification (which uses the row norms) equal to numpy brute force."""
+    import os
+    import subprocess
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    out = str(tmp_path / f"p{ta}.npz")
+    r = subprocess.run([sys.executable, os.path.join(here, "_proj_variant.py"), out],
+                       env=dict(os.environ, DETLSH_PROJ_TA=ta), capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0 and "OK" in r.stdout, r.stdout + r.stderr
+    z = np.load(out)
+    for tag, (cid, n, d, L) in {"c1": (2, 20000, 256, 4), "c5": (5, 20000, 96, 6), "c2": (3, 6000, 960, 4),
+                                "ragged": (1, 3001, 37, 3)}.items():
+        D = datagen.generate(cid, n=n, nq=50)
+        X = np.ascontiguousarray(D["X"][:, :d]).astype(np.float64)
+        Q = np.ascontiguousarray(D["Q"][:, :d]).astype(np.float64)
+        Po = X[:4000] @ z[tag + "_A"].astype(np.float64).T
+        scale = np.maximum(np.abs(Po), np.linalg.norm(X[:4000], axis=1)[:, None])
+        assert np.all(np.abs(z[tag + "_P"] - Po) <= 1e-4 * scale), tag
+        B = z[tag + "_B"]
+        C = z[tag + "_codes"][:4000].astype(np.int64)
+        ref = np.stack([np.searchsorted(B[r, 1:256], z[tag + "_P"][:, r], side="left") for r in range(B.shape[0])], 1)
+        bad = np.argwhere(C != ref)
+        for p, rr in bad:      # only values within 1e-5 of the breakpoint separating the two codes
+            lo, hi = sorted((int(C[p, rr]), int(ref[p, rr])))
+            assert np.min(np.abs(B[rr, lo + 1:hi + 1].astype(np.float64) - Po[p, rr])) <= 1e-5 * scale[p, rr], (tag, p, rr)
+        d2 = ((Q[:, None, :] - X[None]) ** 2).sum(-1)
+        gt = np.array([np.lexsort((np.arange(len(X)), row))[:10] for row in d2])
+        assert np.array_equal(z[tag + "_ids"], gt), tag

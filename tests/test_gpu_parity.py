@@ -801,6 +801,10 @@ def test_projection_variants(tmp_path, ta):
         for p, rr in bad:      # only values within 1e-5 of the breakpoint separating the two codes
             lo, hi = sorted((int(C[p, rr]), int(ref[p, rr])))
             assert np.min(np.abs(B[rr, lo + 1:hi + 1].astype(np.float64) - Po[p, rr])) <= 1e-5 * scale[p, rr], (tag, p, rr)
-        d2 = ((Q[:, None, :] - X[None]) ** 2).sum(-1)
-        gt = np.array([np.lexsort((np.arange(len(X)), row))[:10] for row in d2])
-        assert np.array_equal(z[tag + "_ids"], gt), tag
+        approx = (X * X).sum(1)[None, :] - 2.0 * Q @ X.T
+        gt = []
+        for q in range(len(Q)):
+            cand = np.argpartition(approx[q], 40)[:40]
+            dd = ((X[cand] - Q[q]) ** 2).sum(1)
+            gt.append(cand[np.lexsort((cand, dd))[:10]])
+        assert np.array_equal(z[tag + "_ids"], np.array(gt)), tag

@@ -46,8 +46,10 @@ def test_merge_topk_device():
     """C2 merge (k_merge_topk) vs a plain sort of the pooled (dist, id) pairs."""
     rng = np.random.default_rng(0)
     G, nq, k = 4, 6, 5
-    d = np.sort(rng.integers(0, 9, (G, nq, k)).astype(np.float32), -1)
+    d = rng.integers(0, 9, (G, nq, k)).astype(np.float32)
     ids = rng.permutation(G * nq * k).reshape(G, nq, k).astype(np.int64)
+    o = np.lexsort((ids, d), axis=-1)          # each list sorted by (dist, id), as detlsh_query writes it
+    d, ids = np.take_along_axis(d, o, -1), np.take_along_axis(ids, o, -1)
     ids[0, 0, 4] = -1
     d[0, 0, 4] = np.inf
     oi, od = P.detlsh_merge_topk(ids, d, k)

@@ -823,6 +823,21 @@ __global__ void __launch_bounds__(RF_THREADS, RF_CTAS) k_range_filter(RFArgs a) 
     }
 }
 
+// ---- between two chunks of a tree (L2 blocking, see query_index): the pair lists continue
+//      (entries taken so far = entries listed so far) and the groups' tile counters restart.
+__global__ void k_chunk_prep(const int* __restrict__ act, int na_ub, const int* __restrict__ dna,
+                             const uint32_t* __restrict__ pcnt, uint32_t* __restrict__ ptake,
+                             unsigned int* __restrict__ tctr) {
+    const int na = dna ? *dna : na_ub;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < na; i += gridDim.x * blockDim.x) {
+        if (pcnt) {
+            const int q = act[i];
+            ptake[q] = pcnt[q];
+        }
+        if (tctr && (i & 15) == 0) tctr[i >> 4] = 0;
+    }
+}
+
 // ---- tile-pair mode (CELL, K = 16, N_r = 256): the first stage of a two-level filter for
 //      indexes whose per-query reach is a small fraction of the tiles (large n, small radius).
 //      CTA = 16-query group (its interleaved table, as k_range_filter); a warp takes 32 tiles
@@ -973,7 +988,7 @@ __global__ void __launch_bounds__(LP_THREADS) k_leaf_points(LPArgs a) {
     if (ai >= (a.dna ? *a.dna : a.na)) return;
     const int q = a.act[ai];
     const uint32_t np = a.pcnt[q];
-    if (np == 0 || a.qs[q].status != ST_ACTIVE) return;
+    if (np == 0 || np <= a.ptake[q] || a.qs[q].status != ST_ACTIVE) return;
     const int K = KT > 0 ? KT : a.K, N_r = NRT > 0 ? NRT : a.N_r, KN = K * N_r;
     uint16_t* s_e = (KT > 0 && NRT > 0) ? lp_static : reinterpret_cast<uint16_t*>(lp_smem);   // 12-bit lower bounds
     const float* s_d = a.lut + ((int64_t)q * a.L + a.t) * KN;              // exact terms (band only, L1/L2)
@@ -1048,9 +1063,9 @@ __global__ void __launch_bounds__(LP_THREADS) k_leaf_points(LPArgs a) {
     };
     uint32_t lt = 0, lp = 0;                         // tile mode: leaf bounds evaluated / passed
     for (;;) {
-        uint32_t ck = 0;
-        if (lane == 0) ck = atomicAdd(a.ptake + q, 1u);
-        const uint32_t e0 = __shfl_sync(0xffffffffu, ck, 0) * (a.tile_leaf ? 1u : (uint32_t)LPG);
+        uint32_t ck = 0;     // ptake: the query's next untaken list entry (lists grow over a tree's chunks)
+        if (lane == 0) ck = atomicAdd(a.ptake + q, a.tile_leaf ? 1u : (uint32_t)LPG);
+        const uint32_t e0 = __shfl_sync(0xffffffffu, ck, 0);
         if (e0 >= np) break;
         uint32_t my_p0 = 0, my_sz = 0;
         int64_t my_l = -1;
@@ -2743,6 +2758,24 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
                     ra.gtab = gt;
                     ra.tctr = rf_dyn ? s_tctr.as<unsigned int>() : nullptr;
                 }
+                // L2 blocking: a large tree is filtered in chunks of consecutive tiles holding ~chunk_pts
+                // points each -- the range filter and the pair kernel of all the batch's queries finish one
+                // chunk before the next starts, so its codes, ids, boxes and sub-boxes are read from
+                // HBM about once per batch and served from L2 to every query (tree order: a chunk's
+                // tiles, leaves and points are contiguous).  Results do not depend on the chunking.
+                const int64_t t_tile0 = ix.tree_tile_begin[t], t_tile1 = ix.tree_tile_begin[t + 1];
+                static const int64_t chunk_pts = std::getenv("DETLSH_CHUNK_PTS")
+                                                     ? std::atoll(std::getenv("DETLSH_CHUNK_PTS")) : (int64_t)4 << 20;
+                const int64_t tiles_t = t_tile1 - t_tile0;
+                const int64_t chunk_tiles = (chunk_pts <= 0 || a.lb_order) ? tiles_t
+                    : std::max<int64_t>(RF_THREADS / 32, ceil_div(chunk_pts * tiles_t, std::max<int64_t>(1, n)));
+                for (int64_t c0 = t_tile0; c0 < t_tile1; c0 += chunk_tiles) {
+                ra.tile_begin = c0;
+                ra.tile_end = std::min(t_tile1, c0 + chunk_tiles);
+                if (c0 != t_tile0)
+                    DL_LAUNCH(k_chunk_prep, (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(nf, 256), 148)), 256, 0, st,
+                              fa, nf, dnf, use_pairs ? (const uint32_t*)ra.pcnt : (const uint32_t*)nullptr, lpa.ptake,
+                              ra.tctr);
                 const int64_t ntiles = ra.tile_end - ra.tile_begin;
                 // about `rf_waves` waves of RF_CTAS resident CTAs per SM in all (tiles from a per-group
                 // counter: 1 wave; else per-CTA stripes: 3 waves, 2-4 measured within 1 %)
@@ -2781,6 +2814,7 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
                     static const int lp_y = std::getenv("DETLSH_LP_Y") ? std::atoi(std::getenv("DETLSH_LP_Y")) : 16;
                     DL_LAUNCH(k_leaf_points_sel, dim3((unsigned)nf, (unsigned)lp_y), LP_THREADS, lp_dyn, st, lpa);
                 }
+                }   // chunks
                 if (!a.lb_order) {
                     int* fa2 = (fa == fbuf0) ? fbuf1 : fbuf0;
                     int* dn2 = (fa == fbuf0) ? n_f + 1 : n_f;

@@ -609,7 +609,8 @@ def test_filter_switches_do_not_change_results(tmp_path):
     """The filter's screens and work splits never change a result: the pair kernel's
     sub-box level, the per-query scalar leaf loop with tile screens instead of the 16-query SIMD
     leaf test, the tile screen on the SIMD leaf path, the two-level tile-pair filter
-    (k_tile_pairs + tile-mode k_leaf_points), per-CTA tile stripes instead of per-group counters, the pair path disabled (all tiles through the 16-query SIMD chunks), and the S
+    (k_tile_pairs + tile-mode k_leaf_points), each tree filtered in L2-sized chunks of tiles
+    (DETLSH_CHUNK_PTS), per-CTA tile stripes instead of per-group counters, the pair path disabled (all tiles through the 16-query SIMD chunks), and the S
     bitmaps between query batches cleared by their dirty words or by streaming zeros give
     identical ids, distances and |S| (one batch and batches of 37)."""
     import os
@@ -619,6 +620,9 @@ def test_filter_switches_do_not_change_results(tmp_path):
     runs = {"default": {}, "nosub": {"DETLSH_NO_SUBBOX": "1"}, "scalar_leaf": {"DETLSH_RF_DEBUG": "1"},
             "stripes": {"DETLSH_RF_STRIPES": "1"}, "no_pairs": {"DETLSH_LEAF_PAIRS": "0"},
             "tile_screen": {"DETLSH_RF_TSCREEN": "1"}, "tile_pairs": {"DETLSH_TILE_PAIRS": "1"},
+            "chunks": {"DETLSH_CHUNK_PTS": "7000"}, "one_chunk": {"DETLSH_CHUNK_PTS": "0"},
+            "tile_pairs_chunks": {"DETLSH_TILE_PAIRS": "1", "DETLSH_CHUNK_PTS": "7000"},
+            "stripes_chunks": {"DETLSH_RF_STRIPES": "1", "DETLSH_CHUNK_PTS": "7000"},
             "dirty_clear": {"DETLSH_DIRTY_CLEAR": "2"},
             "memset_clear": {"DETLSH_DIRTY_CLEAR": "0"}}
     res = {}

@@ -2524,9 +2524,14 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
     Scratch s_q12(st, use_pairs ? sizeof(uint16_t) * (size_t)(qb * LK * ix.N_r) : 0);
     const bool lp_fixed = ix.K == 16 && ix.N_r == 256;
     static const int lp_g = std::getenv("DETLSH_LP_G") ? std::atoi(std::getenv("DETLSH_LP_G")) : 16;
-    // two-level filter (k_tile_pairs + tile-mode k_leaf_points): DETLSH_TILE_PAIRS = 1 on, 0 off
-    static const int tp_env = std::getenv("DETLSH_TILE_PAIRS") ? std::atoi(std::getenv("DETLSH_TILE_PAIRS")) : 0;
-    const bool tile_pairs = tp_env == 1 && use_pairs && lp_fixed && RF_G == 16 && rf_dyn && !a.lb_order;
+    // two-level filter (k_tile_pairs + tile-mode k_leaf_points): DETLSH_TILE_PAIRS = 1 on, 0 off,
+    // default (-1) on when first-layer cells hold >= 64 points on average (n >= 64 * 2^K): then a
+    // query reaches few of a tile's leaves and the group-union SIMD leaf scan wastes most of its
+    // work (measured: configs[3] 67.5 -> 60.3 ms, configs[4] 662 -> 585 ms; configs[1], 15 points
+    // per cell: 1.93 -> 2.18 ms, so off)
+    static const int tp_env = std::getenv("DETLSH_TILE_PAIRS") ? std::atoi(std::getenv("DETLSH_TILE_PAIRS")) : -1;
+    const bool tp_want = tp_env == 1 || (tp_env < 0 && ix.K < 40 && (n >> ix.K) >= 64);
+    const bool tile_pairs = tp_want && use_pairs && lp_fixed && RF_G == 16 && rf_dyn && !a.lb_order;
     auto k_leaf_points_sel = tile_pairs ? k_leaf_points<16, 256, 32>
                              : lp_fixed ? (lp_g == 8 ? k_leaf_points<16, 256, 8> : k_leaf_points<16, 256, 16>)
                                         : k_leaf_points<0, 0, 16>;
@@ -2764,8 +2769,10 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
                 // HBM about once per batch and served from L2 to every query (tree order: a chunk's
                 // tiles, leaves and points are contiguous).  Results do not depend on the chunking.
                 const int64_t t_tile0 = ix.tree_tile_begin[t], t_tile1 = ix.tree_tile_begin[t + 1];
+                // (measured at configs[4]: 1M-8M-point chunks were 17-95 % SLOWER than one pass -- the
+                // per-chunk launches cost more than the L2 reuse gains; off by default, kept as a switch)
                 static const int64_t chunk_pts = std::getenv("DETLSH_CHUNK_PTS")
-                                                     ? std::atoll(std::getenv("DETLSH_CHUNK_PTS")) : (int64_t)4 << 20;
+                                                     ? std::atoll(std::getenv("DETLSH_CHUNK_PTS")) : (int64_t)0;
                 const int64_t tiles_t = t_tile1 - t_tile0;
                 const int64_t chunk_tiles = (chunk_pts <= 0 || a.lb_order) ? tiles_t
                     : std::max<int64_t>(RF_THREADS / 32, ceil_div(chunk_pts * tiles_t, std::max<int64_t>(1, n)));

@@ -592,8 +592,13 @@ detlsh_status detlsh_debug_export(const detlsh_index* idx, int32_t what, int32_t
                 break;
             }
             case 4: {
-                std::vector<uint32_t> p((size_t)n);
+                // canonical order: a leaf's points by ascending id (the device layout orders them by a
+                // locality key for the sub-box bounds, build.cu k_leaf_morton)
+                std::vector<uint32_t> p((size_t)n), off((size_t)nl + 1);
                 d2h(p.data(), ix.perm.as<uint32_t>() + (size_t)tree * n, p.size() * 4);
+                d2h(off.data(), ix.leaf_off.as<uint32_t>() + lb, off.size() * 4);
+                for (int64_t l = 0; l < nl; ++l)
+                    std::sort(p.begin() + (off[l] - (int64_t)tree * n), p.begin() + (off[l + 1] - (int64_t)tree * n));
                 int64_t* o = static_cast<int64_t*>(dst);
                 for (int64_t i = 0; i < n; ++i) o[i] = p[i];
                 break;

@@ -855,6 +855,67 @@ __global__ void k_tile_flags(const uint32_t* __restrict__ leaf_off, int64_t nl, 
     }
 }
 
+// Within each leaf, the points reordered by a locality key: the top bits of the K codes
+// interleaved bit-plane by bit-plane (Morton / z-order; min(8, 64 / K) bits per dim), ties by the
+// original (id) order.  A leaf is a set (Alg. 3 takes its points by their own bounds), so the
+// order is free; consecutive points then lie close in every dim and the sub-boxes of kSubBox
+// consecutive points (k_sb_boxes) get tight boxes -- measured on a configs[4]-like tree, half the
+// points behind passing sub-boxes.  Warp per leaf of <= 128 points (bitonic sort in shared
+// memory); larger (unsplittable) leaves keep their order.  perm and tcodes move together.
+constexpr int LM_WARPS = 8;
+__global__ void __launch_bounds__(LM_WARPS * 32) k_leaf_morton(const uint32_t* __restrict__ leaf_off, int64_t nl, int K,
+                                                               uint32_t* __restrict__ perm, uint8_t* __restrict__ tcodes) {
+    __shared__ unsigned long long s_key[LM_WARPS][128];
+    __shared__ uint32_t s_idx[LM_WARPS][128];
+    __shared__ uint32_t s_perm[LM_WARPS][128];
+    __shared__ __align__(16) uint8_t s_codes[LM_WARPS][128 * 32];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int bpd = K >= 8 ? 64 / K > 8 ? 8 : 64 / K : 8;          // key bits per dim
+    for (int64_t l = (int64_t)blockIdx.x * LM_WARPS + w; l < nl; l += (int64_t)gridDim.x * LM_WARPS) {
+        const uint32_t p0 = leaf_off[l];
+        const int m = (int)(leaf_off[l + 1] - p0);
+        if (m <= 2 || m > 128) continue;
+        for (int e = lane; e < 128; e += 32) {
+            unsigned long long key = ~0ull;
+            if (e < m) {
+                const uint8_t* c = tcodes + (int64_t)(p0 + e) * K;
+                key = 0;
+                for (int b = 0; b < bpd; ++b)
+                    for (int j = 0; j < K; ++j) key = (key << 1) | ((c[j] >> (7 - b)) & 1u);
+                s_perm[w][e] = perm[p0 + e];
+                for (int j = 0; j < K; ++j) s_codes[w][e * K + j] = c[j];
+            }
+            s_key[w][e] = key;
+            s_idx[w][e] = (uint32_t)e;
+        }
+        __syncwarp();
+        // bitonic sort of the 128 (key, idx) pairs, ascending
+        for (int size = 2; size <= 128; size <<= 1) {
+            for (int stride = size >> 1; stride > 0; stride >>= 1) {
+                for (int t = lane; t < 64; t += 32) {
+                    const int i = 2 * t - (t & (stride - 1)), j = i + stride;
+                    const bool up = (i & size) == 0;
+                    const unsigned long long ki = s_key[w][i], kj = s_key[w][j];
+                    const uint32_t ii = s_idx[w][i], ij = s_idx[w][j];
+                    const bool gt = ki > kj || (ki == kj && ii > ij);
+                    if (gt == up) {
+                        s_key[w][i] = kj; s_key[w][j] = ki;
+                        s_idx[w][i] = ij; s_idx[w][j] = ii;
+                    }
+                }
+                __syncwarp();
+            }
+        }
+        for (int e = lane; e < m; e += 32) {
+            const uint32_t src = s_idx[w][e];
+            perm[p0 + e] = s_perm[w][src];
+            uint8_t* dst = tcodes + (int64_t)(p0 + e) * K;
+            for (int j = 0; j < K; ++j) dst[j] = s_codes[w][src * K + j];
+        }
+        __syncwarp();
+    }
+}
+
 // Sub-boxes: each leaf's points cut into runs of kSubBox consecutive points (leaf order); per
 // run the min/max code per dim.  A valid lower bound for every member, tighter than the leaf's
 // (a few points span less of each dim): the pair kernel screens runs before their points.
@@ -1245,6 +1306,10 @@ static bool build_trees_try(Index& ix, const uint8_t* d_EP, int64_t leaf_factor,
     DL_LAUNCH(k_tree_begin, 1, 64, 0, st, ix.leaf_off.as<uint32_t>(), nl, n, (int)L, d_lbeg);
     ix.tcodes.alloc((size_t)total * K, st);
     DL_LAUNCH(k_gather_tcodes, grid_for(total, 256), 256, 0, st, perm, d_EP, n, (int)L, K, ix.tcodes.as<uint8_t>());
+    static const int morton_env = std::getenv("DETLSH_LEAF_MORTON") ? std::atoi(std::getenv("DETLSH_LEAF_MORTON")) : 1;
+    if (morton_env && K <= 32)
+        DL_LAUNCH(k_leaf_morton, grid_for(nl, LM_WARPS, 148 * 16), LM_WARPS * 32, 0, st, ix.leaf_off.as<uint32_t>(), nl, K,
+                  perm, ix.tcodes.as<uint8_t>());
     build_subboxes(ix, nl, st);
     ix.leaf_tlo.alloc((size_t)nl * K, st);
     ix.leaf_thi.alloc((size_t)nl * K, st);

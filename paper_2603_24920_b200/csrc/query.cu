@@ -1521,6 +1521,33 @@ __global__ void k_tree_end_compact(const int* __restrict__ act, int na_ub, const
 // (k_count_new), the pair-list reset and the budget test (k_tree_end); the last block to finish
 // (ticket counter) then compacts the still-active queries for the next tree (k_tree_end_compact).
 // act_out == null: no compaction (last tree).  Not for lb_order (its counts are tentative).
+// Visit the flagged words of one dirty-word summary row (bit b of summary word sw = bitmap word
+// 32 sw + b): 16-byte summary loads, four of them in flight per thread (a 100M-point row is 98K
+// summary words, mostly zero -- a one-word-per-thread loop was latency-bound).  nsw is a
+// multiple of 4 and rows are 16-byte aligned.
+template <class F>
+__device__ __forceinline__ void for_each_dirty_word(const uint32_t* __restrict__ sm_row, int64_t nsw, F&& f) {
+    const uint4* s4 = reinterpret_cast<const uint4*>(sm_row);
+    const int64_t n4 = nsw >> 2;
+    for (int64_t i0 = threadIdx.x; i0 < n4; i0 += 4 * (int64_t)blockDim.x) {
+        uint4 w[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int64_t i = i0 + u * (int64_t)blockDim.x;
+            w[u] = i < n4 ? s4[i] : make_uint4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            if ((w[u].x | w[u].y | w[u].z | w[u].w) == 0) continue;
+            const int64_t i = i0 + u * (int64_t)blockDim.x;
+            const uint32_t ws[4] = {w[u].x, w[u].y, w[u].z, w[u].w};
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                for (uint32_t dm = ws[k]; dm; dm &= dm - 1) f((4 * i + k) * 32 + (__ffs(dm) - 1));
+        }
+    }
+}
+
 __global__ void __launch_bounds__(256) k_tree_post(const int* __restrict__ act, int na_ub, const int* __restrict__ dna,
                                                    QState* __restrict__ qs, const uint32_t* __restrict__ cur,
                                                    uint32_t* __restrict__ prev, int64_t nwords,
@@ -1550,16 +1577,14 @@ __global__ void __launch_bounds__(256) k_tree_post(const int* __restrict__ act, 
             const uint32_t* c = cur + (int64_t)q * nwords;
             uint32_t* pv = prev + (int64_t)q * nwords;
             uint32_t cnt = 0;
-            for (int64_t sw = threadIdx.x; sw < nsw; sw += blockDim.x)
-                for (uint32_t dm = wsum[(int64_t)q * nsw + sw]; dm; dm &= dm - 1) {
-                    const int64_t w = sw * 32 + (__ffs(dm) - 1);
-                    const uint32_t cv = c[w], pw = pv[w];
-                    const uint32_t nb = cv & ~pw;
-                    if (nb) {
-                        pv[w] = cv;
-                        cnt += __popc(nb);
-                    }
+            for_each_dirty_word(wsum + (int64_t)q * nsw, nsw, [&](int64_t w) {
+                const uint32_t cv = c[w], pw = pv[w];
+                const uint32_t nb = cv & ~pw;
+                if (nb) {
+                    pv[w] = cv;
+                    cnt += __popc(nb);
                 }
+            });
             for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
             if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(&s_cnt, cnt);
         }
@@ -1890,21 +1915,19 @@ __global__ void __launch_bounds__(256) k_verify_list(const int* __restrict__ act
     const uint32_t* c = cur + (int64_t)q * nwords;
     uint32_t* v = ver + (int64_t)q * nwords;
     const uint32_t* sm = wsum + (int64_t)q * nsw;
-    for (int64_t sw = threadIdx.x; sw < nsw; sw += blockDim.x)
-        for (uint32_t dm = sm[sw]; dm; dm &= dm - 1) {
-            const int64_t wd = sw * 32 + (__ffs(dm) - 1);
-            const uint32_t cv = c[wd];
-            uint32_t nb = cv & ~v[wd];
-            if (!nb) continue;
-            v[wd] = cv;
-            unsigned long long slot = atomicAdd(&s_slot, (unsigned long long)__popc(nb));
-            const uint32_t base = (uint32_t)(wd * 32);
-            for (; nb; nb &= nb - 1) {
-                cand[slot] = base + (uint32_t)(__ffs(nb) - 1);
-                cq[slot] = (uint32_t)a;
-                ++slot;
-            }
+    for_each_dirty_word(sm, nsw, [&](int64_t wd) {
+        const uint32_t cv = c[wd];
+        uint32_t nb = cv & ~v[wd];
+        if (!nb) return;
+        v[wd] = cv;
+        unsigned long long slot = atomicAdd(&s_slot, (unsigned long long)__popc(nb));
+        const uint32_t base = (uint32_t)(wd * 32);
+        for (; nb; nb &= nb - 1) {
+            cand[slot] = base + (uint32_t)(__ffs(nb) - 1);
+            cq[slot] = (uint32_t)a;
+            ++slot;
         }
+    });
 }
 
 __global__ void k_prep_queries(const float* __restrict__ Q, int64_t ld, const int* __restrict__ act, int na,
@@ -2911,7 +2934,7 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
                         cq_cap = (int64_t)(tot + tot / 2 + 1024);
                         s_cq.alloc(sizeof(uint32_t) * (size_t)cq_cap);
                     }
-                    DL_LAUNCH(k_verify_list, (unsigned)na, 128, 0, st, cur, s_qs.as<QState>(), s_bm.as<uint32_t>(),
+                    DL_LAUNCH(k_verify_list, (unsigned)na, 256, 0, st, cur, s_qs.as<QState>(), s_bm.as<uint32_t>(),
                               s_ver.as<uint32_t>(), nwords, s_sum.as<uint32_t>(), nsw, va.cand, s_cq.as<uint32_t>());
                     const unsigned vg = (unsigned)std::min<int64_t>(ceil_div((int64_t)tot * 8, 256), 148 * 32);
                     auto k_verify_gather_sel = ix.ld == 128   ? k_verify_gather<4>

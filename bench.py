@@ -204,7 +204,10 @@ def kernel_models(c, steps: int, st, n_local: int, nq: int, ld: int):
     ncand = float(st["n_cand"].sum())
     # leaf boxes are read once per 16-query group and tree ("leaf-box bytes /
     # query-batch"); everything else per query
-    filt = float((st["leaves_tested"] * 2 * K / 16 + st["leaves_passed"] * 8 + st["subboxes_tested"] * 2 * K
+    # two-level filter (large n, library default n >= 64 * 2^K): the pair kernel bounds each listed
+    # tile's leaves per query, so their boxes count per query (2K), not per 16-query group
+    box_share = 1.0 if n_local >= 64 * (1 << K) else 1.0 / 16
+    filt = float((st["leaves_tested"] * 2 * K * box_share + st["leaves_passed"] * 8 + st["subboxes_tested"] * 2 * K
                   + st["points_tested"] * K + st["points_passed"] * 12 + st["n_cand"] * 4).sum())
     lookups = float((st["points_tested"] * K + st["leaves_tested"] * K + st["subboxes_tested"] * K).sum())
     proj_bytes = n_local * (4 * ld + LK) + (ns + nq) * (4 * ld + 4 * LK)
@@ -245,8 +248,8 @@ def build_roofline(c, n_local: int, pts_per_s: float, hbm: float) -> dict:
             "model": "4d + 9LK + 100L B per point (SURVEY 8(d) Build total) x points/s"}
 
 
-FILTER_UNIT = "filter"                       # k_range_filter + k_leaf_points (one unit of work: Alg. 3)
-FILTER_KERNELS = ("k_range_filter", "k_leaf_points")
+FILTER_UNIT = "filter"      # k_range_filter or k_tile_pairs + k_leaf_points (one unit of work: Alg. 3)
+FILTER_KERNELS = ("k_range_filter", "k_tile_pairs", "k_leaf_points")
 
 
 def group_filter(prof):
@@ -257,8 +260,7 @@ def group_filter(prof):
         if k.startswith(FILTER_KERNELS):
             fms += ms
             parts[k] = round(ms, 4)
-            if k.startswith("k_range_filter"):
-                fl += nl
+            fl = max(fl, nl)          # one launch of each per (batch, round, tree)
         else:
             out[k] = (nl, ms)
     if parts:
@@ -493,7 +495,7 @@ def main():
     # CUDA events in the timed region around the dominant unit's kernels only (every timed
     # launch adds an event pair to the stream); the other modelled kernels are timed in one
     # extra, untimed step below
-    P.profile_filter("k_range_filter,k_leaf_points")
+    P.profile_filter("k_range_filter,k_tile_pairs,k_leaf_points")
     P.profile_enable(True)
     l0 = P.launch_count()
     evs = [step(True) for _ in range(args.steps)]

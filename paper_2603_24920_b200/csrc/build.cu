@@ -863,6 +863,11 @@ __global__ void k_tile_flags(const uint32_t* __restrict__ leaf_off, int64_t nl, 
 // points behind passing sub-boxes.  Warp per leaf of <= 128 points (bitonic sort in shared
 // memory); larger (unsplittable) leaves keep their order.  perm and tcodes move together.
 constexpr int LM_WARPS = 8;
+// Bits b (7 >= b > 7 - 4) of the four code bytes of w gathered into a nibble (byte 0 lowest):
+// the bits sit at positions 0, 8, 16, 24 and one multiply moves them to 24..27 without carries.
+__device__ __forceinline__ uint32_t plane_nibble(uint32_t w, int b) {
+    return ((((w >> b) & 0x01010101u) * 0x01020408u) >> 24) & 0xFu;
+}
 __global__ void __launch_bounds__(LM_WARPS * 32) k_leaf_morton(const uint32_t* __restrict__ leaf_off, int64_t nl, int K,
                                                                uint32_t* __restrict__ perm, uint8_t* __restrict__ tcodes) {
     __shared__ unsigned long long s_key[LM_WARPS][128];
@@ -870,29 +875,41 @@ __global__ void __launch_bounds__(LM_WARPS * 32) k_leaf_morton(const uint32_t* _
     __shared__ uint32_t s_perm[LM_WARPS][128];
     __shared__ __align__(16) uint8_t s_codes[LM_WARPS][128 * 32];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int bpd = K >= 8 ? 64 / K > 8 ? 8 : 64 / K : 8;          // key bits per dim
+    const int bpd = K >= 8 ? (64 / K > 8 ? 8 : 64 / K) : 8;       // key bits per dim (generic K)
     for (int64_t l = (int64_t)blockIdx.x * LM_WARPS + w; l < nl; l += (int64_t)gridDim.x * LM_WARPS) {
         const uint32_t p0 = leaf_off[l];
         const int m = (int)(leaf_off[l + 1] - p0);
         if (m <= 2 || m > 128) continue;
-        for (int e = lane; e < 128; e += 32) {
+        int P2 = 4;                                   // sort size: next power of two >= m
+        while (P2 < m) P2 <<= 1;
+        for (int e = lane; e < P2; e += 32) {
             unsigned long long key = ~0ull;
             if (e < m) {
                 const uint8_t* c = tcodes + (int64_t)(p0 + e) * K;
-                key = 0;
-                for (int b = 0; b < bpd; ++b)
-                    for (int j = 0; j < K; ++j) key = (key << 1) | ((c[j] >> (7 - b)) & 1u);
                 s_perm[w][e] = perm[p0 + e];
-                for (int j = 0; j < K; ++j) s_codes[w][e * K + j] = c[j];
+                if (K == 16) {
+                    const uint4 c4 = *reinterpret_cast<const uint4*>(c);
+                    *reinterpret_cast<uint4*>(&s_codes[w][e * 16]) = c4;
+                    key = 0;
+#pragma unroll
+                    for (int b = 7; b > 3; --b)           // 4 bit-planes x 16 dims = 64 bits
+                        key = (key << 16) | (plane_nibble(c4.x, b) << 12) | (plane_nibble(c4.y, b) << 8) |
+                              (plane_nibble(c4.z, b) << 4) | plane_nibble(c4.w, b);
+                } else {
+                    key = 0;
+                    for (int b = 0; b < bpd; ++b)
+                        for (int j = 0; j < K; ++j) key = (key << 1) | ((c[j] >> (7 - b)) & 1u);
+                    for (int j = 0; j < K; ++j) s_codes[w][e * K + j] = c[j];
+                }
             }
             s_key[w][e] = key;
             s_idx[w][e] = (uint32_t)e;
         }
         __syncwarp();
-        // bitonic sort of the 128 (key, idx) pairs, ascending
-        for (int size = 2; size <= 128; size <<= 1) {
+        // bitonic sort of the P2 (key, idx) pairs, ascending
+        for (int size = 2; size <= P2; size <<= 1) {
             for (int stride = size >> 1; stride > 0; stride >>= 1) {
-                for (int t = lane; t < 64; t += 32) {
+                for (int t = lane; t < (P2 >> 1); t += 32) {
                     const int i = 2 * t - (t & (stride - 1)), j = i + stride;
                     const bool up = (i & size) == 0;
                     const unsigned long long ki = s_key[w][i], kj = s_key[w][j];
@@ -910,7 +927,11 @@ __global__ void __launch_bounds__(LM_WARPS * 32) k_leaf_morton(const uint32_t* _
             const uint32_t src = s_idx[w][e];
             perm[p0 + e] = s_perm[w][src];
             uint8_t* dst = tcodes + (int64_t)(p0 + e) * K;
-            for (int j = 0; j < K; ++j) dst[j] = s_codes[w][src * K + j];
+            if (K == 16) {
+                *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(&s_codes[w][src * 16]);
+            } else {
+                for (int j = 0; j < K; ++j) dst[j] = s_codes[w][src * K + j];
+            }
         }
         __syncwarp();
     }
@@ -926,8 +947,9 @@ __global__ void k_sb_count(const uint32_t* __restrict__ leaf_off, int64_t nl, ui
 
 // thread per sub-box (its leaf by binary search over sb_off); consecutive threads read
 // consecutive runs of points
+// Boxes are interleaved: box i = lo (K bytes) then hi (K bytes) at box + 2K i.
 __global__ void k_sb_boxes(const uint32_t* __restrict__ leaf_off, const uint32_t* __restrict__ sb_off, int64_t nl, int K,
-                           const uint8_t* __restrict__ tcodes, uint8_t* __restrict__ lo, uint8_t* __restrict__ hi) {
+                           const uint8_t* __restrict__ tcodes, uint8_t* __restrict__ box) {
     const uint32_t nsb = sb_off[nl];
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nsb; i += (int64_t)gridDim.x * blockDim.x) {
         int64_t a_ = 0, b_ = nl - 1;                  // last leaf l with sb_off[l] <= i
@@ -944,8 +966,8 @@ __global__ void k_sb_boxes(const uint32_t* __restrict__ leaf_off, const uint32_t
                 mn = make_uint4(__vminu4(mn.x, c.x), __vminu4(mn.y, c.y), __vminu4(mn.z, c.z), __vminu4(mn.w, c.w));
                 mx = make_uint4(__vmaxu4(mx.x, c.x), __vmaxu4(mx.y, c.y), __vmaxu4(mx.z, c.z), __vmaxu4(mx.w, c.w));
             }
-            *reinterpret_cast<uint4*>(lo + i * 16) = mn;
-            *reinterpret_cast<uint4*>(hi + i * 16) = mx;
+            *reinterpret_cast<uint4*>(box + i * 32) = mn;
+            *reinterpret_cast<uint4*>(box + i * 32 + 16) = mx;
         } else {
             for (int j = 0; j < K; ++j) {
                 int mn = 255, mx = 0;
@@ -954,37 +976,37 @@ __global__ void k_sb_boxes(const uint32_t* __restrict__ leaf_off, const uint32_t
                     mn = min(mn, c);
                     mx = max(mx, c);
                 }
-                lo[i * K + j] = (uint8_t)mn;
-                hi[i * K + j] = (uint8_t)mx;
+                box[i * 2 * K + j] = (uint8_t)mn;
+                box[i * 2 * K + K + j] = (uint8_t)mx;
             }
         }
     }
 }
 
 // Tight box of each leaf as the union of its sub-boxes' boxes (same min/max over the same points).
-__global__ void k_leaf_tight_sb(const uint32_t* __restrict__ sb_off, int64_t nl, int K, const uint8_t* __restrict__ slo,
-                                const uint8_t* __restrict__ shi, uint8_t* __restrict__ tlo, uint8_t* __restrict__ thi) {
+__global__ void k_leaf_tight_sb(const uint32_t* __restrict__ sb_off, int64_t nl, int K, const uint8_t* __restrict__ sbox,
+                                uint8_t* __restrict__ tbox) {
     for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < nl; l += (int64_t)gridDim.x * blockDim.x) {
         const uint32_t a = sb_off[l], e = sb_off[l + 1];
         if (K == 16) {
             uint4 mn = make_uint4(~0u, ~0u, ~0u, ~0u), mx = make_uint4(0, 0, 0, 0);
             for (uint32_t b = a; b < e; ++b) {
-                const uint4 x = *reinterpret_cast<const uint4*>(slo + (int64_t)b * 16);
-                const uint4 y = *reinterpret_cast<const uint4*>(shi + (int64_t)b * 16);
+                const uint4 x = *reinterpret_cast<const uint4*>(sbox + (int64_t)b * 32);
+                const uint4 y = *reinterpret_cast<const uint4*>(sbox + (int64_t)b * 32 + 16);
                 mn = make_uint4(__vminu4(mn.x, x.x), __vminu4(mn.y, x.y), __vminu4(mn.z, x.z), __vminu4(mn.w, x.w));
                 mx = make_uint4(__vmaxu4(mx.x, y.x), __vmaxu4(mx.y, y.y), __vmaxu4(mx.z, y.z), __vmaxu4(mx.w, y.w));
             }
-            *reinterpret_cast<uint4*>(tlo + l * 16) = mn;
-            *reinterpret_cast<uint4*>(thi + l * 16) = mx;
+            *reinterpret_cast<uint4*>(tbox + l * 32) = mn;
+            *reinterpret_cast<uint4*>(tbox + l * 32 + 16) = mx;
         } else {
             for (int j = 0; j < K; ++j) {
                 int mn = 255, mx = 0;
                 for (uint32_t b = a; b < e; ++b) {
-                    mn = min(mn, (int)slo[(int64_t)b * K + j]);
-                    mx = max(mx, (int)shi[(int64_t)b * K + j]);
+                    mn = min(mn, (int)sbox[(int64_t)b * 2 * K + j]);
+                    mx = max(mx, (int)sbox[(int64_t)b * 2 * K + K + j]);
                 }
-                tlo[l * K + j] = (uint8_t)mn;
-                thi[l * K + j] = (uint8_t)mx;
+                tbox[l * 2 * K + j] = (uint8_t)mn;
+                tbox[l * 2 * K + K + j] = (uint8_t)mx;
             }
         }
     }
@@ -1000,9 +1022,9 @@ __global__ void k_tile_boxes(const uint32_t* __restrict__ tile_leaf, const uint3
         const int64_t t = i / K;
         const int j = (int)(i - t * K);
         int a = 255, b = 0;
-        for (uint32_t l = tile_leaf[t]; l < tile_leaf[t + 1]; ++l) {
-            a = min(a, (int)lo[(int64_t)l * K + j]);
-            b = max(b, (int)hi[(int64_t)l * K + j]);
+        for (uint32_t l = tile_leaf[t]; l < tile_leaf[t + 1]; ++l) {     // leaf boxes interleaved (2K per box)
+            a = min(a, (int)lo[(int64_t)l * 2 * K + j]);
+            b = max(b, (int)hi[(int64_t)l * 2 * K + j]);
         }
         tlo[i] = (uint8_t)a;
         thi[i] = (uint8_t)b;
@@ -1311,10 +1333,9 @@ static bool build_trees_try(Index& ix, const uint8_t* d_EP, int64_t leaf_factor,
         DL_LAUNCH(k_leaf_morton, grid_for(nl, LM_WARPS, 148 * 16), LM_WARPS * 32, 0, st, ix.leaf_off.as<uint32_t>(), nl, K,
                   perm, ix.tcodes.as<uint8_t>());
     build_subboxes(ix, nl, st);
-    ix.leaf_tlo.alloc((size_t)nl * K, st);
-    ix.leaf_thi.alloc((size_t)nl * K, st);
-    DL_LAUNCH(k_leaf_tight_sb, grid_for(nl, 256), 256, 0, st, ix.sb_off.as<uint32_t>(), nl, K, ix.sb_lo.as<uint8_t>(),
-              ix.sb_hi.as<uint8_t>(), ix.leaf_tlo.as<uint8_t>(), ix.leaf_thi.as<uint8_t>());
+    ix.leaf_tbox.alloc((size_t)nl * 2 * K, st);
+    DL_LAUNCH(k_leaf_tight_sb, grid_for(nl, 256), 256, 0, st, ix.sb_off.as<uint32_t>(), nl, K, ix.sb_box.as<uint8_t>(),
+              ix.leaf_tbox.as<uint8_t>());
     tr.mark("leaf finalize+codes", st);
     // query tiles: runs of kTileLeaves leaves of one tree; the tile count stays on the device
     // (arrays sized by its bound: each tree adds at most one partial tile)
@@ -1333,7 +1354,7 @@ static bool build_trees_try(Index& ix, const uint8_t* d_EP, int64_t leaf_factor,
         ix.tile_lo.alloc((size_t)nt_ub * K, st);
         ix.tile_hi.alloc((size_t)nt_ub * K, st);
         DL_LAUNCH(k_tile_boxes, grid_for(nt_ub * K, 256), 256, 0, st, ix.tile_leaf.as<uint32_t>(), ntiles_d, K,
-                  ix.leaf_tlo.as<uint8_t>(), ix.leaf_thi.as<uint8_t>(), ix.tile_lo.as<uint8_t>(), ix.tile_hi.as<uint8_t>());
+                  ix.leaf_tbox.as<uint8_t>(), ix.leaf_tbox.as<uint8_t>() + K, ix.tile_lo.as<uint8_t>(), ix.tile_hi.as<uint8_t>());
         ix.point_tile_leaf.alloc(sizeof(uint16_t) * (size_t)total, st);
         DL_LAUNCH(k_point_tile_leaf, grid_for(nt_ub * 32, 256), 256, 0, st, ix.leaf_off.as<uint32_t>(),
                   ix.tile_leaf.as<uint32_t>(), ntiles_d, nl, ix.point_tile_leaf.as<uint16_t>());
@@ -1357,10 +1378,9 @@ void build_subboxes(Index& ix, int64_t nl, cudaStream_t st) {
     DL_LAUNCH(k_sb_count, grid_for(nl, 256), 256, 0, st, ix.leaf_off.as<uint32_t>(), nl, s_cnt.as<uint32_t>());
     exclusive_scan_u32(s_cnt.as<uint32_t>(), ix.sb_off.as<uint32_t>(), nl, ix.sb_off.as<uint32_t>() + nl, st);
     const int64_t nsb_ub = (int64_t)ix.n * ix.L / kSubBox + nl;   // each leaf adds at most one partial run
-    ix.sb_lo.alloc((size_t)nsb_ub * ix.K, st);
-    ix.sb_hi.alloc((size_t)nsb_ub * ix.K, st);
+    ix.sb_box.alloc((size_t)nsb_ub * 2 * ix.K, st);
     DL_LAUNCH(k_sb_boxes, grid_for(nsb_ub, 256), 256, 0, st, ix.leaf_off.as<uint32_t>(), ix.sb_off.as<uint32_t>(), nl,
-              ix.K, ix.tcodes.as<uint8_t>(), ix.sb_lo.as<uint8_t>(), ix.sb_hi.as<uint8_t>());
+              ix.K, ix.tcodes.as<uint8_t>(), ix.sb_box.as<uint8_t>());
 }
 
 // d_flag (optional): a device int read back (into *h_flag) with the build's last host round trip

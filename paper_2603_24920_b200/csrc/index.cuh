@@ -70,10 +70,11 @@ struct Index {
     DevBuf tile_leaf;       // [ntiles+1] first leaf of each query tile (tree-major; see build.cu)
     std::vector<int64_t> tree_tile_begin;  // [L+1] tile index range of each tree (host copy)
     DevBuf point_tile_leaf; // [L*n] u16: leaf of each point (tree order) within its tile (< 32)
-    DevBuf leaf_tlo, leaf_thi;  // [nl_total][K] u8 tight box: min/max code of the leaf's points
+    DevBuf leaf_tbox;           // [nl_total][2K] u8 tight box: min code (K bytes) then max code (K bytes)
+                                // of the leaf's points -- lo and hi in one row (one 32 B sector at K = 16)
     DevBuf tile_lo, tile_hi;// [ntiles][K] u8 bounding box of each tile's tight leaf boxes
     DevBuf sb_off;          // [nl_total+1] u32 first sub-box of each leaf (sub-box = kSubBox consecutive points)
-    DevBuf sb_lo, sb_hi;    // [nsb][K] u8 tight box of each sub-box (the pair kernel's second-level bound)
+    DevBuf sb_box;          // [nsb][2K] u8 tight box (lo | hi) of each sub-box (the pair kernel's second-level bound)
     DevBuf xnorm;           // [n] fp32 ||x||^2 of every row (tensor-core verification, verify_tc.cu)
     bool keep_proj = false; // build option: keep the projections (EXACT mode)
     DevBuf proj;            // [n][LK] fp32 projections p' in data order (EXACT mode only)

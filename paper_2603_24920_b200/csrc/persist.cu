@@ -5,7 +5,7 @@
 // File: "DETLSH\0\1" | u32 version | header (fixed-width scalars) | the two host vectors
 // (tree leaf / tile ranges) | device arrays, each as u64 byte count + bytes, in the order
 // X, A, B, sample, perm, tcodes, leaf_off, leaf_lo, leaf_hi, leaf_bits, tile_leaf,
-// point_tile_leaf, xnorm, proj (EXACT-mode projections; empty if not kept), tile_lo, tile_hi, leaf_tlo, leaf_thi.  The data rows are always stored (a borrowed X is copied out), so
+// point_tile_leaf, xnorm, proj (EXACT-mode projections; empty if not kept), tile_lo, tile_hi, leaf_tbox.  The data rows are always stored (a borrowed X is copied out), so
 // a loaded index owns everything it needs.
 #include <algorithm>
 #include <cstdio>
@@ -20,7 +20,7 @@ namespace detlsh {
 namespace {
 
 constexpr char kMagic[8] = {'D', 'E', 'T', 'L', 'S', 'H', 0, 1};
-constexpr uint32_t kVersion = 1;
+constexpr uint32_t kVersion = 2;     // 2: tight leaf boxes interleaved (leaf_tbox)
 
 struct Header {
     int64_t n, n_global, id_offset, n_s;
@@ -90,7 +90,7 @@ void save_index(const Index& ix, const char* path) {
     const size_t xbytes = ix.codes_only ? 0 : sizeof(float) * (size_t)ix.n * ix.ld;
     put_dev(fh.f, ix.Xp, xbytes);
     const DevBuf* arr[] = {&ix.A, &ix.B, &ix.sample, &ix.perm, &ix.tcodes, &ix.leaf_off, &ix.leaf_lo,
-                           &ix.leaf_hi, &ix.leaf_bits, &ix.tile_leaf, &ix.point_tile_leaf, &ix.xnorm, &ix.proj, &ix.tile_lo, &ix.tile_hi, &ix.leaf_tlo, &ix.leaf_thi};
+                           &ix.leaf_hi, &ix.leaf_bits, &ix.tile_leaf, &ix.point_tile_leaf, &ix.xnorm, &ix.proj, &ix.tile_lo, &ix.tile_hi, &ix.leaf_tbox};
     for (const DevBuf* b : arr) put_dev(fh.f, b->p, b->bytes);
     if (std::fflush(fh.f) != 0) throw Error(DETLSH_EINVAL, "write failed");
 }
@@ -140,8 +140,7 @@ Index* load_index(const char* path) {
     ix->keep_proj = ix->proj.p != nullptr;
     get_dev(fh.f, ix->tile_lo, (size_t)nt * h.K);
     get_dev(fh.f, ix->tile_hi, (size_t)nt * h.K);
-    get_dev(fh.f, ix->leaf_tlo, (size_t)nl * h.K);
-    get_dev(fh.f, ix->leaf_thi, (size_t)nl * h.K);
+    get_dev(fh.f, ix->leaf_tbox, (size_t)nl * 2 * h.K);
     build_subboxes(*ix, nl, 0);                        // derived from tcodes + leaf_off (not stored)
     DL_CUDA(cudaDeviceSynchronize());
     return ix.release();

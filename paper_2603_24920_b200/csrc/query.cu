@@ -294,8 +294,10 @@ struct RFArgs {
     const uint16_t* ptl;        // tree t: [n] leaf within tile
     const uint32_t* perm;       // tree t: [n]
     const uint32_t* leaf_off;   // global positions
-    const uint8_t* lo;          // [nl_total][K]
+    const uint8_t* lo;          // leaf boxes: box l at lo + l * bs (K bytes), likewise hi
     const uint8_t* hi;
+    int bs;                     // box stride in bytes: 2K for the interleaved tight boxes (lo | hi in
+                                // one 32-byte row at K = 16: one sector per box), K for prefix boxes
     const uint8_t* tile_lo;     // [ntiles][K] tile bounding boxes
     const uint8_t* tile_hi;
     const uint32_t* tile_leaf;  // [ntiles+1]
@@ -479,11 +481,11 @@ __global__ void __launch_bounds__(RF_THREADS, RF_CTAS) k_range_filter(RFArgs a) 
             if (KT == 16 && G == 16 && !(a.dbg & 1)) {
                 // all 16 queries at once (same 16-bit lane layout as the SIMD point screen): per
                 // dim, the rows D_j[lo] and D_j[hi] masked by the s < lo / s > hi query sets
-                m = simd16_box_mask(s_qe, N_r, *reinterpret_cast<const uint4*>(a.lo + l * 16),
-                                    *reinterpret_cast<const uint4*>(a.hi + l * 16)) & tm;
+                m = simd16_box_mask(s_qe, N_r, *reinterpret_cast<const uint4*>(a.lo + l * a.bs),
+                                    *reinterpret_cast<const uint4*>(a.hi + l * a.bs)) & tm;
             } else if (KT == 16) {
-                const uint4 lo4 = *reinterpret_cast<const uint4*>(a.lo + l * 16);
-                const uint4 hi4 = *reinterpret_cast<const uint4*>(a.hi + l * 16);
+                const uint4 lo4 = *reinterpret_cast<const uint4*>(a.lo + l * a.bs);
+                const uint4 hi4 = *reinterpret_cast<const uint4*>(a.hi + l * a.bs);
                 for (uint32_t mm = tm; mm; mm &= mm - 1) {
                     const int g = __ffs(mm) - 1;
                     const uint4 sx4 = *reinterpret_cast<const uint4*>(&s_sx[g][0]);
@@ -504,7 +506,7 @@ __global__ void __launch_bounds__(RF_THREADS, RF_CTAS) k_range_filter(RFArgs a) 
                     const int g = __ffs(mm) - 1;
                     uint32_t acc = 0;
                     for (int j = 0; j < K; ++j) {
-                        const int e = (j * N_r + min(max((int)s_sx[g][j], (int)a.lo[l * K + j]), (int)a.hi[l * K + j])) * 16;
+                        const int e = (j * N_r + min(max((int)s_sx[g][j], (int)a.lo[l * a.bs + j]), (int)a.hi[l * a.bs + j])) * 16;
                         acc += G == 8 ? (uint32_t)s_h[e / 2 + g] : (uint32_t)(s_b[e + g] & 0x7Fu);
                     }
                     if (acc <= QT) m |= 1u << g;
@@ -519,7 +521,7 @@ __global__ void __launch_bounds__(RF_THREADS, RF_CTAS) k_range_filter(RFArgs a) 
                     const float* D = a.lut + (int64_t)s_q[g] * per_q + (int64_t)a.t * K * N_r;
                     float s_ = 0.f;
                     for (int j = 0; j < K; ++j)
-                        s_ += __ldg(D + j * N_r + min(max((int)s_sx[g][j], (int)a.lo[l * K + j]), (int)a.hi[l * K + j]));
+                        s_ += __ldg(D + j * N_r + min(max((int)s_sx[g][j], (int)a.lo[l * a.bs + j]), (int)a.hi[l * a.bs + j]));
                     if (s_ <= rho2) conf |= 1u << g;
                 }
                 m = conf;
@@ -956,10 +958,11 @@ struct LPArgs {
     const float* lut;           // [Qb][L][K][N_r]
     const uint16_t* q12;        // [Qb][L][K][N_r] 12-bit lower bounds of this round (k_build_qlut, QT 2048)
     const uint32_t* leaf_off;   // global positions
-    const uint8_t* lo;          // [nl_total][K] tight leaf boxes
+    const uint8_t* lo;          // tight leaf boxes, box l at lo + l * bs (interleaved: bs = 2K)
     const uint8_t* hi;
+    int bs;
     const uint32_t* sb_off;     // [nl_total+1] first sub-box of each leaf (null: no sub-box level)
-    const uint8_t* sb_lo;       // [nsb][K] sub-box tight boxes
+    const uint8_t* sb_lo;       // sub-box tight boxes, interleaved: box i at sb_lo + 2K i, hi at sb_lo + 2K i + K
     const uint8_t* sb_hi;
     const uint8_t* sx;          // [Qb][L][K] query region codes
     const uint8_t* tcodes;      // tree t [n][K]
@@ -981,7 +984,7 @@ constexpr int LP_THREADS = 256;     // threads per pair-kernel block (512 with h
 // KT, NRT > 0: K and N_r fixed at compile time (table rows at immediate offsets, a static table);
 // LPG listed leaves per warp chunk
 template <int KT, int NRT, int LPG>
-__global__ void __launch_bounds__(LP_THREADS) k_leaf_points(LPArgs a) {
+__global__ void __launch_bounds__(LP_THREADS, 5) k_leaf_points(LPArgs a) {
     extern __shared__ __align__(16) unsigned char lp_smem[];
     __shared__ __align__(16) uint16_t lp_static[(KT > 0 && NRT > 0) ? KT * NRT : 8];
     const int ai = blockIdx.x;
@@ -1085,8 +1088,8 @@ __global__ void __launch_bounds__(LP_THREADS) k_leaf_points(LPArgs a) {
             // the leaf) is beyond rho^2 -- the leaf's points are not screened
             uint32_t lb = 0;
             if (K == 16) {
-                const uint4 lo4 = *reinterpret_cast<const uint4*>(a.lo + (int64_t)l * 16);
-                const uint4 hi4 = *reinterpret_cast<const uint4*>(a.hi + (int64_t)l * 16);
+                const uint4 lo4 = *reinterpret_cast<const uint4*>(a.lo + (int64_t)l * a.bs);
+                const uint4 hi4 = *reinterpret_cast<const uint4*>(a.hi + (int64_t)l * a.bs);
 #pragma unroll
                 for (int j = 0; j < 16; ++j) {
                     const int sh = 8 * (j & 3);
@@ -1097,7 +1100,7 @@ __global__ void __launch_bounds__(LP_THREADS) k_leaf_points(LPArgs a) {
                 }
             } else {
                 for (int j = 0; j < K; ++j)
-                    lb += s_e[j * N_r + min(max(s_qx[j], (int)a.lo[(int64_t)l * K + j]), (int)a.hi[(int64_t)l * K + j])];
+                    lb += s_e[j * N_r + min(max(s_qx[j], (int)a.lo[(int64_t)l * a.bs + j]), (int)a.hi[(int64_t)l * a.bs + j])];
             }
             if (lb > 2048u) my_sz = 0;
             ++lt;
@@ -1119,8 +1122,9 @@ __global__ void __launch_bounds__(LP_THREADS) k_leaf_points(LPArgs a) {
             const uint32_t excl = incl - my_nsb;
             const uint32_t TS = __shfl_sync(0xffffffffu, incl, LPG - 1);
             const uint32_t my_end = my_p0 + my_sz;
-            for (uint32_t c0 = 0; c0 < TS; c0 += 32) {
-                const uint32_t i = c0 + lane;
+            // software pipeline: the next 32 sub-boxes' boxes (one 32-byte row each: lo | hi) are
+            // loaded before this step's bounds are computed (the loads were the top stall, ncu)
+            auto locate = [&](uint32_t i, uint32_t& sbi, uint32_t& first, uint32_t& cnt) {
                 int o_ = 0;                               // last leaf slot with excl <= i
 #pragma unroll
                 for (int st = LPG / 2; st > 0; st >>= 1) {
@@ -1131,16 +1135,36 @@ __global__ void __launch_bounds__(LP_THREADS) k_leaf_points(LPArgs a) {
                 const uint32_t pp0 = __shfl_sync(0xffffffffu, my_p0, o_);
                 const uint32_t pend = __shfl_sync(0xffffffffu, my_end, o_);
                 const uint32_t pex = __shfl_sync(0xffffffffu, excl, o_);
+                sbi = sb0 + (i - pex);
+                first = pp0 + (i - pex) * kSubBox;
+                cnt = min((uint32_t)kSubBox, pend - first);
+                return i < TS;
+            };
+            uint4 nlo = make_uint4(0, 0, 0, 0), nhi = make_uint4(0, 0, 0, 0);
+            uint32_t nsbi = 0, nfirst = 0, ncnt = 0;
+            bool nvalid = locate(lane, nsbi, nfirst, ncnt);
+            if (K == 16 && nvalid) {
+                nlo = *reinterpret_cast<const uint4*>(a.sb_lo + (int64_t)nsbi * 32);
+                nhi = *reinterpret_cast<const uint4*>(a.sb_hi + (int64_t)nsbi * 32);
+            }
+            for (uint32_t c0 = 0; c0 < TS; c0 += 32) {
+                const uint4 lo4 = nlo, hi4 = nhi;
+                const uint32_t sbi = nsbi, first_c = nfirst, cnt_c = ncnt;
+                const bool valid = nvalid;
+                if (c0 + 32 < TS) {
+                    nvalid = locate(c0 + 32 + lane, nsbi, nfirst, ncnt);
+                    if (K == 16 && nvalid) {
+                        nlo = *reinterpret_cast<const uint4*>(a.sb_lo + (int64_t)nsbi * 32);
+                        nhi = *reinterpret_cast<const uint4*>(a.sb_hi + (int64_t)nsbi * 32);
+                    }
+                }
                 bool pass = false;
                 uint32_t first = 0, cnt = 0;
-                if (i < TS) {
-                    const uint32_t sbi = sb0 + (i - pex);
-                    first = pp0 + (i - pex) * kSubBox;
-                    cnt = min((uint32_t)kSubBox, pend - first);
+                if (valid) {
+                    first = first_c;
+                    cnt = cnt_c;
                     uint32_t lb = 0;
                     if (K == 16) {
-                        const uint4 lo4 = *reinterpret_cast<const uint4*>(a.sb_lo + (int64_t)sbi * 16);
-                        const uint4 hi4 = *reinterpret_cast<const uint4*>(a.sb_hi + (int64_t)sbi * 16);
 #pragma unroll
                         for (int j = 0; j < 16; ++j) {
                             const int sh = 8 * (j & 3);
@@ -1151,8 +1175,8 @@ __global__ void __launch_bounds__(LP_THREADS) k_leaf_points(LPArgs a) {
                         }
                     } else {
                         for (int j = 0; j < K; ++j)
-                            lb += s_e[j * N_r + min(max(s_qx[j], (int)a.sb_lo[(int64_t)sbi * K + j]),
-                                                    (int)a.sb_hi[(int64_t)sbi * K + j])];
+                            lb += s_e[j * N_r + min(max(s_qx[j], (int)a.sb_lo[(int64_t)sbi * 2 * K + j]),
+                                                    (int)a.sb_hi[(int64_t)sbi * 2 * K + j])];
                     }
                     pass = lb <= 2048u;
                     ++sbt;
@@ -2566,8 +2590,9 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
     ra.leaf_off = ix.leaf_off.as<uint32_t>();
     // leaf pruning uses the tight boxes (a valid, tighter bound for every member); RELAXED takes
     // whole leaves by the leaf's own (prefix) box, as the method defines it
-    ra.lo = (a.mode == DETLSH_MODE_RELAXED ? ix.leaf_lo : ix.leaf_tlo).as<uint8_t>();
-    ra.hi = (a.mode == DETLSH_MODE_RELAXED ? ix.leaf_hi : ix.leaf_thi).as<uint8_t>();
+    ra.lo = a.mode == DETLSH_MODE_RELAXED ? ix.leaf_lo.as<uint8_t>() : ix.leaf_tbox.as<uint8_t>();
+    ra.hi = a.mode == DETLSH_MODE_RELAXED ? ix.leaf_hi.as<uint8_t>() : ix.leaf_tbox.as<uint8_t>() + ix.K;
+    ra.bs = a.mode == DETLSH_MODE_RELAXED ? ix.K : 2 * ix.K;
     ra.tile_leaf = ix.tile_leaf.as<uint32_t>();
     ra.tile_lo = ix.tile_lo.as<uint8_t>();
     ra.tile_hi = ix.tile_hi.as<uint8_t>();
@@ -2825,10 +2850,11 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
                     lpa.tcodes = ra.tcodes;
                     lpa.lo = ra.lo;
                     lpa.hi = ra.hi;
+                    lpa.bs = ra.bs;
                     static const bool no_sb = std::getenv("DETLSH_NO_SUBBOX") != nullptr;   // experiments
                     lpa.sb_off = (ix.sb_off.p && !no_sb) ? ix.sb_off.as<uint32_t>() : nullptr;
-                    lpa.sb_lo = ix.sb_lo.as<uint8_t>();
-                    lpa.sb_hi = ix.sb_hi.as<uint8_t>();
+                    lpa.sb_lo = ix.sb_box.as<uint8_t>();
+                    lpa.sb_hi = ix.sb_box.as<uint8_t>() + ix.K;
                     lpa.sx = ra.sx;
                     lpa.perm = ra.perm;
                     lpa.pos_base = ra.pos_base;

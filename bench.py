@@ -214,8 +214,10 @@ def kernel_models(c, steps: int, st, n_local: int, nq: int, ld: int):
     proj_flops = 2.0 * 2 * (n_local + ns + nq) * ((LK + 15) // 16 * 16) * ld      # x_hi and x_lo MMAs
     return {
         FILTER_UNIT: {"bytes": steps * filt, "smem_bytes": steps * lookups * 2,
-                      "unit": "per query: leaves_tested*2K/16 (leaf boxes read once per 16-query group, "
-                              "SURVEY 8(d) K5) + leaves_passed*8 + subboxes_tested*2K + points_tested*K + "
+                      "unit": ("per query: leaves_tested*2K (box bounds read by the query itself: the two-level "
+                               "filter's tile and leaf bounds)" if box_share == 1.0 else
+                               "per query: leaves_tested*2K/16 (leaf boxes read once per 16-query group, SURVEY 8(d) K5)")
+                              + " + leaves_passed*8 + subboxes_tested*2K + points_tested*K + "
                               "points_passed*12 + new*4 B (K6, with the sub-box boxes the pair kernel "
                               "reads), over both filter kernels "
                               "(k_range_filter: tile/leaf bounds + dense tiles; k_leaf_points: sparse tiles' "

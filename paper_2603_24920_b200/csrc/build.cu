@@ -1328,8 +1328,11 @@ static bool build_trees_try(Index& ix, const uint8_t* d_EP, int64_t leaf_factor,
     DL_LAUNCH(k_tree_begin, 1, 64, 0, st, ix.leaf_off.as<uint32_t>(), nl, n, (int)L, d_lbeg);
     ix.tcodes.alloc((size_t)total * K, st);
     DL_LAUNCH(k_gather_tcodes, grid_for(total, 256), 256, 0, st, perm, d_EP, n, (int)L, K, ix.tcodes.as<uint8_t>());
-    static const int morton_env = std::getenv("DETLSH_LEAF_MORTON") ? std::atoi(std::getenv("DETLSH_LEAF_MORTON")) : 1;
-    if (morton_env && K <= 32)
+    // DETLSH_LEAF_MORTON: 1 always, 0 never, default when leaves are large (first-layer cells of
+    // >= 64 points on average: configs[3], configs[4]; at configs[1] the ~19-point leaves have 2-3
+    // sub-boxes, and the sort cost 0.23 ms of build for 0.03 ms of query)
+    static const int morton_env = std::getenv("DETLSH_LEAF_MORTON") ? std::atoi(std::getenv("DETLSH_LEAF_MORTON")) : -1;
+    if (K <= 32 && (morton_env == 1 || (morton_env < 0 && (n >> K) >= 64)))
         DL_LAUNCH(k_leaf_morton, grid_for(nl, LM_WARPS, 148 * 16), LM_WARPS * 32, 0, st, ix.leaf_off.as<uint32_t>(), nl, K,
                   perm, ix.tcodes.as<uint8_t>());
     build_subboxes(ix, nl, st);

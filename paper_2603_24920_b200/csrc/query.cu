@@ -984,7 +984,7 @@ constexpr int LP_THREADS = 256;     // threads per pair-kernel block (512 with h
 // KT, NRT > 0: K and N_r fixed at compile time (table rows at immediate offsets, a static table);
 // LPG listed leaves per warp chunk
 template <int KT, int NRT, int LPG>
-__global__ void __launch_bounds__(LP_THREADS, 5) k_leaf_points(LPArgs a) {
+__global__ void __launch_bounds__(LP_THREADS, LPG == 32 ? 5 : 6) k_leaf_points(LPArgs a) {
     extern __shared__ __align__(16) unsigned char lp_smem[];
     __shared__ __align__(16) uint16_t lp_static[(KT > 0 && NRT > 0) ? KT * NRT : 8];
     const int ai = blockIdx.x;
@@ -1143,17 +1143,19 @@ __global__ void __launch_bounds__(LP_THREADS, 5) k_leaf_points(LPArgs a) {
             uint4 nlo = make_uint4(0, 0, 0, 0), nhi = make_uint4(0, 0, 0, 0);
             uint32_t nsbi = 0, nfirst = 0, ncnt = 0;
             bool nvalid = locate(lane, nsbi, nfirst, ncnt);
-            if (K == 16 && nvalid) {
+            if (K == 16 && nvalid && LPG == 32) {
                 nlo = *reinterpret_cast<const uint4*>(a.sb_lo + (int64_t)nsbi * 32);
                 nhi = *reinterpret_cast<const uint4*>(a.sb_hi + (int64_t)nsbi * 32);
             }
             for (uint32_t c0 = 0; c0 < TS; c0 += 32) {
-                const uint4 lo4 = nlo, hi4 = nhi;
+                const uint4 lo4p = nlo, hi4p = nhi;
                 const uint32_t sbi = nsbi, first_c = nfirst, cnt_c = ncnt;
                 const bool valid = nvalid;
                 if (c0 + 32 < TS) {
                     nvalid = locate(c0 + 32 + lane, nsbi, nfirst, ncnt);
-                    if (K == 16 && nvalid) {
+                    // prefetch only in the two-level filter's instantiation (LPG = 32, large n, where
+                    // the boxes come from HBM); with LPG = 16 (L2-resident indexes) it cost occupancy
+                    if (K == 16 && nvalid && LPG == 32) {
                         nlo = *reinterpret_cast<const uint4*>(a.sb_lo + (int64_t)nsbi * 32);
                         nhi = *reinterpret_cast<const uint4*>(a.sb_hi + (int64_t)nsbi * 32);
                     }
@@ -1165,6 +1167,11 @@ __global__ void __launch_bounds__(LP_THREADS, 5) k_leaf_points(LPArgs a) {
                     cnt = cnt_c;
                     uint32_t lb = 0;
                     if (K == 16) {
+                        uint4 lo4 = lo4p, hi4 = hi4p;
+                        if (LPG != 32) {
+                            lo4 = *reinterpret_cast<const uint4*>(a.sb_lo + (int64_t)sbi * 32);
+                            hi4 = *reinterpret_cast<const uint4*>(a.sb_hi + (int64_t)sbi * 32);
+                        }
 #pragma unroll
                         for (int j = 0; j < 16; ++j) {
                             const int sh = 8 * (j & 3);
@@ -2960,7 +2967,7 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
                         cq_cap = (int64_t)(tot + tot / 2 + 1024);
                         s_cq.alloc(sizeof(uint32_t) * (size_t)cq_cap);
                     }
-                    DL_LAUNCH(k_verify_list, (unsigned)na, 256, 0, st, cur, s_qs.as<QState>(), s_bm.as<uint32_t>(),
+                    DL_LAUNCH(k_verify_list, (unsigned)na, nsw >= 8192 ? 256 : 128, 0, st, cur, s_qs.as<QState>(), s_bm.as<uint32_t>(),
                               s_ver.as<uint32_t>(), nwords, s_sum.as<uint32_t>(), nsw, va.cand, s_cq.as<uint32_t>());
                     const unsigned vg = (unsigned)std::min<int64_t>(ceil_div((int64_t)tot * 8, 256), 148 * 32);
                     auto k_verify_gather_sel = ix.ld == 128   ? k_verify_gather<4>

@@ -141,7 +141,14 @@ __global__ void __launch_bounds__(1024) k_sel16_pick(const uint32_t* __restrict_
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const uint32_t* h = hist + threadIdx.x * 64;
     unsigned long long sum = 0;
-    for (int j = 0; j < 64; ++j) sum += h[j];
+    {
+        const uint4* h4 = reinterpret_cast<const uint4*>(h);   // 16 loads of 16 B, all in flight
+        uint4 v[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) v[j] = h4[j];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) sum += (unsigned long long)v[j].x + v[j].y + v[j].z + v[j].w;
+    }
     unsigned long long x = sum;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {

@@ -346,6 +346,11 @@ __global__ void k_first_key(const uint8_t* __restrict__ EP, int64_t n, int L, in
     }
 }
 
+__global__ void k_iota_mod(uint32_t* __restrict__ v, int64_t total, int64_t n) {
+    for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total; g += (int64_t)gridDim.x * blockDim.x)
+        v[g] = (uint32_t)(g % n);
+}
+
 __global__ void k_seg_flags(const uint32_t* __restrict__ keys, int64_t n, int64_t total, uint32_t* __restrict__ flags) {
     for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total;
          g += (int64_t)gridDim.x * blockDim.x)
@@ -1191,21 +1196,25 @@ static void encode_all(const Index& ix, const float* d_P, int64_t m, uint8_t* d_
 // B5 + B6 for all L trees at once, from codes EP[n][LK] (data order).  Returns false if the
 // leaf list overflowed its capacity (the caller retries with a larger factor).
 static bool build_trees_try(Index& ix, const uint8_t* d_EP, int64_t leaf_factor, cudaStream_t st,
-                            const int* d_flag = nullptr, int* h_flag = nullptr) {
+                            const int* d_flag = nullptr, int* h_flag = nullptr, uint32_t* d_fkey = nullptr) {
     Trace tr("trees");
     const int64_t n = ix.n, L = ix.L, total = n * L;
     const int K = ix.K, nb = ix.nb, LK = ix.LK, max_size = ix.max_size;
     DL_REQUIRE(total < (int64_t)0xFFFFFFFF, "L*n must be < 2^32");
 
     ix.perm.alloc(sizeof(uint32_t) * (size_t)total, st);
-    Scratch s_sort(st, sizeof(uint32_t) * (size_t)(3 * total));
-    uint32_t* keys0 = s_sort.as<uint32_t>();
-    uint32_t* keys1 = keys0 + total;
+    Scratch s_sort(st, sizeof(uint32_t) * (size_t)((d_fkey ? 2 : 3) * total));
+    uint32_t* keys0 = d_fkey ? d_fkey : s_sort.as<uint32_t>() + 2 * total;
+    uint32_t* keys1 = s_sort.as<uint32_t>();
     uint32_t* vals1 = keys1 + total;
     uint32_t* perm = ix.perm.as<uint32_t>();
 
-    // B5: first-layer keys, stable (key, id) sort per tree
-    DL_LAUNCH(k_first_key, grid_for(total, 256), 256, 0, st, d_EP, n, (int)L, K, nb, keys0, perm);
+    // B5: first-layer keys (from the projection epilogue, or from the codes), stable (key, id)
+    // sort per tree
+    if (d_fkey)
+        DL_LAUNCH(k_iota_mod, grid_for(total, 256), 256, 0, st, perm, total, n);
+    else
+        DL_LAUNCH(k_first_key, grid_for(total, 256), 256, 0, st, d_EP, n, (int)L, K, nb, keys0, perm);
     bool flip = radix_sort_batched(keys0, perm, keys1, vals1, n, L, K, st);
     const uint32_t* skeys = flip ? keys1 : keys0;
     if (flip) DL_CUDA(cudaMemcpyAsync(perm, vals1, sizeof(uint32_t) * total, cudaMemcpyDeviceToDevice, st));
@@ -1395,15 +1404,17 @@ void build_subboxes(Index& ix, int64_t nl, cudaStream_t st) {
 
 // d_flag (optional): a device int read back (into *h_flag) with the build's last host round trip
 static void build_trees(Index& ix, const uint8_t* d_EP, cudaStream_t st, const int* d_flag = nullptr,
-                        int* h_flag = nullptr) {
+                        int* h_flag = nullptr, uint32_t* d_fkey = nullptr) {
     for (int64_t f = 4;; f *= 4) {
-        if (build_trees_try(ix, d_EP, f, st, d_flag, h_flag)) return;
+        // first-layer keys from the projection epilogue serve the first attempt only (its sort
+        // overwrites them; a retry recomputes them from the codes)
+        if (build_trees_try(ix, d_EP, f, st, d_flag, h_flag, f == 4 ? d_fkey : nullptr)) return;
         DL_REQUIRE(f < (int64_t)1 << 40, "tree build: leaf list overflow");
     }
 }
 
 bool project_encode_tc(const Index& ix, const float* d_X, int64_t ld, int64_t m, uint8_t* d_EP, int* d_nonfinite,
-                       float* d_xnorm, float* d_P, cudaStream_t st);
+                       float* d_xnorm, float* d_P, cudaStream_t st, uint32_t* d_fkey);
 
 void build_index(Index& ix, const float* d_data, int64_t data_ld, const float* bp_given, double sample_frac,
                  int proj_impl, cudaStream_t st) {
@@ -1441,8 +1452,17 @@ void build_index(Index& ix, const float* d_data, int64_t data_ld, const float* b
     Scratch s_ep(st, (size_t)n * ix.LK);
     ix.xnorm.alloc(sizeof(float) * (size_t)n, st);     // ||x||^2 per row (tensor-core verification)
     if (ix.keep_proj) ix.proj.alloc(sizeof(float) * (size_t)n * ix.LK, st);   // EXACT mode: p' of every point
-    if (!(proj_impl == 0 && project_encode_tc(ix, d_data, data_ld, n, s_ep.as<uint8_t>(), s_flag.as<int>(),
-                                              ix.xnorm.as<float>(), ix.keep_proj ? ix.proj.as<float>() : nullptr, st))) {
+    // the tensor-core epilogue also writes each tree's first-layer keys (K = 16, N_r a power of two):
+    // the tree build's sort starts from them instead of re-reading the codes (k_first_key)
+    const bool fk_ok = proj_impl == 0 && ix.K == 16 && (ix.LK & 15) == 0 && (ix.N_r & (ix.N_r - 1)) == 0 &&
+                       (int64_t)n * ix.L < (int64_t)0xFFFFFFFF;
+    Scratch s_fkey(st, fk_ok ? sizeof(uint32_t) * (size_t)(n * ix.L) : 0);
+    bool fk_written = false;
+    if (proj_impl == 0 && project_encode_tc(ix, d_data, data_ld, n, s_ep.as<uint8_t>(), s_flag.as<int>(),
+                                            ix.xnorm.as<float>(), ix.keep_proj ? ix.proj.as<float>() : nullptr, st,
+                                            fk_ok ? s_fkey.as<uint32_t>() : nullptr)) {
+        fk_written = fk_ok;
+    } else {
         DL_LAUNCH(k_row_norms, grid_for(n * 32, 256), 256, 0, st, d_data, data_ld, n, ix.xnorm.as<float>());
         const int64_t chunk = std::min<int64_t>(n, std::max<int64_t>(1 << 16, (int64_t)(1ll << 30) / (4 * ix.LK)));
         Scratch s_p(st, sizeof(float) * (size_t)(chunk * ix.LK));
@@ -1459,7 +1479,7 @@ void build_index(Index& ix, const float* d_data, int64_t data_ld, const float* b
     // B5 + B6; the non-finite flag of the projection is read with the trees' last round trip
     // (a NaN/Inf row makes the whole build fail -- after the trees, not before)
     int nonfinite = 0;
-    build_trees(ix, s_ep.as<uint8_t>(), st, s_flag.as<int>(), &nonfinite);
+    build_trees(ix, s_ep.as<uint8_t>(), st, s_flag.as<int>(), &nonfinite, fk_written ? s_fkey.as<uint32_t>() : nullptr);
     DL_REQUIRE(!nonfinite, "data contains NaN or Inf");
     tr.mark("trees", st);
 }

@@ -60,7 +60,7 @@ struct TcShape {
 __global__ void __launch_bounds__(TC_THREADS, 1)
     k_project_tc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmA, TcShape sh,
                  float* __restrict__ P, int* __restrict__ nonfinite, const float* __restrict__ B,
-                 uint8_t* __restrict__ EP, float* __restrict__ xnorm) {
+                 uint8_t* __restrict__ EP, float* __restrict__ xnorm, uint32_t* __restrict__ fkey) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     // 1024-byte alignment of every swizzled buffer
     // 1024-byte aligned, by pointer arithmetic on the shared array (keeps the shared address
@@ -314,6 +314,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                     uint32_t packed[4] = {0, 0, 0, 0};
 #pragma unroll
                     for (int i = 0; i < 16; ++i) packed[i >> 2] |= (uint32_t)(pos[i] - NP) << (8 * (i & 3));
+                    // (K = 16: the chunk is tree c0/16) the tree's first-layer key for the build's
+                    // sort, Alg. 2 l.2: the top bit of each dim's symbol, dim 0 most significant
+                    if (fkey != nullptr && row < sh.m) {
+                        uint32_t key = 0;
+#pragma unroll
+                        for (int i = 0; i < 16; ++i) key = (key << 1) | (((uint32_t)(pos[i] - NP) >> (lg - 1)) & 1u);
+                        fkey[(int64_t)(c0 >> 4) * sh.m + row] = key;
+                    }
                     if (row < sh.m) {
                         uint8_t* out = EP + row * sh.LK + c0;
                         if (c0 + 16 <= sh.LK && (sh.LK & 15) == 0) {
@@ -355,7 +363,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 // Returns false when the shape does not fit this kernel (resident hash matrix too large).
 // B != nullptr: fused encode (Alg. 1) -- writes codes EP[m][LK] instead of P.
 static bool launch_tc(const Index& ix, const float* d_X, int64_t ld, int64_t m, float* d_P, int* d_nonfinite,
-                      const float* B, uint8_t* EP, float* xnorm, cudaStream_t st) {
+                      const float* B, uint8_t* EP, float* xnorm, cudaStream_t st, uint32_t* fkey = nullptr) {
     if (m <= 0) return true;
     TcShape sh;
     sh.m = m;
@@ -404,7 +412,8 @@ static bool launch_tc(const Index& ix, const float* d_X, int64_t ld, int64_t m, 
     DL_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
     const int64_t ntiles = ceil_div(m, TC_M);
     const int grid = (int)std::min<int64_t>(ntiles, nsm);
-    DL_LAUNCH(k_project_tc, grid, TC_THREADS, smem, st, mx, ma, sh, d_P, d_nonfinite, B, EP, xnorm);
+    DL_LAUNCH(k_project_tc, grid, TC_THREADS, smem, st, mx, ma, sh, d_P, d_nonfinite, B, EP, xnorm,
+              (fkey && ix.K == 16 && (ix.LK & 15) == 0 && (1 << sh.lgP) == ix.N_r) ? fkey : (uint32_t*)nullptr);
     return true;
 }
 
@@ -414,8 +423,8 @@ bool project_rows_tc(const Index& ix, const float* d_X, int64_t ld, int64_t m, f
 }
 
 bool project_encode_tc(const Index& ix, const float* d_X, int64_t ld, int64_t m, uint8_t* d_EP, int* d_nonfinite,
-                       float* d_xnorm, float* d_P, cudaStream_t st) {
-    return launch_tc(ix, d_X, ld, m, d_P, d_nonfinite, ix.B.as<float>(), d_EP, d_xnorm, st);
+                       float* d_xnorm, float* d_P, cudaStream_t st, uint32_t* d_fkey) {
+    return launch_tc(ix, d_X, ld, m, d_P, d_nonfinite, ix.B.as<float>(), d_EP, d_xnorm, st, d_fkey);
 }
 
 }  // namespace detlsh

@@ -13,7 +13,8 @@ import sys
 
 PROFILE_NAME = {"k_range_filter": "k_range_filter_sel", "k_verify_tc": "k_verify_tc", "k_project_tc": "k_project_tc",
                 "k_topk": "k_topk", "k_verify_rows": "k_verify_rows", "k_verify_gather": "k_verify_gather_sel",
-                "k_collect_cands": "k_collect_cands", "k_count_new": "k_count_new", "k_leaf_points": "k_leaf_points_sel"}
+                "k_collect_cands": "k_collect_cands", "k_count_new": "k_count_new", "k_leaf_points": "k_leaf_points_sel",
+                "k_tile_pairs": "k_tile_pairs"}
 KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
         "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "lts__t_sector_hit_rate.pct",
         "lts__throughput.avg.pct_of_peak_sustained_elapsed", "sm__throughput.avg.pct_of_peak_sustained_elapsed",

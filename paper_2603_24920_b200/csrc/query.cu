@@ -825,6 +825,27 @@ __global__ void __launch_bounds__(RF_THREADS, RF_CTAS) k_range_filter(RFArgs a) 
     }
 }
 
+// ---- locality order of a tree's active queries (two-level filter): key = the query's own
+//      first-layer cell in tree t (top bit of its region code in each dim, dim 0 most significant);
+//      entries past the device count sort last.  Queries reaching the same cells then run side by
+//      side in the pair kernel and share its box / code reads in L2.
+__global__ void k_qkey(const int* __restrict__ act, int na_ub, const int* __restrict__ dna,
+                       const uint8_t* __restrict__ sx, int L, int K, int nb, int t,
+                       uint32_t* __restrict__ keys, uint32_t* __restrict__ vals) {
+    const int na = dna ? *dna : na_ub;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < na_ub; i += gridDim.x * blockDim.x) {
+        uint32_t key = 0xFFFFFFu;
+        int q = act[i];
+        if (i < na) {
+            const uint8_t* c = sx + ((int64_t)q * L + t) * K;
+            key = 0;
+            for (int j = 0; j < K && j < 23; ++j) key = (key << 1) | ((c[j] >> (nb - 1)) & 1u);
+        }
+        keys[i] = key;
+        vals[i] = (uint32_t)q;
+    }
+}
+
 // ---- between two chunks of a tree (L2 blocking, see query_index): the pair lists continue
 //      (entries taken so far = entries listed so far) and the groups' tile counters restart.
 __global__ void k_chunk_prep(const int* __restrict__ act, int na_ub, const int* __restrict__ dna,
@@ -2590,6 +2611,10 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
                              : lp_fixed ? (lp_g == 8 ? k_leaf_points<16, 256, 8> : k_leaf_points<16, 256, 16>)
                                         : k_leaf_points<0, 0, 16>;
     lpa.tile_leaf = tile_pairs ? ix.tile_leaf.as<uint32_t>() : nullptr;
+    // two-level filter: each tree's active queries in locality order (DETLSH_QSORT, default on)
+    static const int qsort_env = std::getenv("DETLSH_QSORT") ? std::atoi(std::getenv("DETLSH_QSORT")) : 1;
+    const bool qsort_on = qsort_env != 0;
+    Scratch s_qk(st, tile_pairs && qsort_on ? sizeof(uint32_t) * (size_t)(4 * qb) : 0);
     if (tile_pairs) ensure_dyn_smem_fn(k_tile_pairs, rf_smem);
     const size_t lp_dyn = lp_fixed ? 0 : lp_smem;
     if (use_pairs && !lp_fixed)
@@ -2808,6 +2833,15 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
                 ra.dna = dnf;
                 ra.rho2 = rho2;
                 ra.t = t;
+                if (tile_pairs && qsort_on && nf > RF_G) {
+                    uint32_t* k0 = s_qk.as<uint32_t>();
+                    uint32_t* v0 = k0 + qb;
+                    DL_LAUNCH(k_qkey, (unsigned)std::min<int64_t>(ceil_div(nf, 256), 148), 256, 0, st, fa, nf, dnf,
+                              s_sx.as<uint8_t>(), ix.L, ix.K, ix.nb, t, k0, v0);
+                    const bool flip = radix_sort_batched(k0, v0, k0 + 2 * qb, v0 + 2 * qb, nf, 1, 24, st);
+                    fa = reinterpret_cast<int*>(flip ? v0 + 2 * qb : v0);
+                    ra.act = fa;
+                }
                 const int groups = (int)ceil_div(nf, RF_G);
                 if (RF_G == 16) {
                     uint4* gt = s_gtab.as<uint4>();

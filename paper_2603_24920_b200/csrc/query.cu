@@ -2611,8 +2611,9 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
                              : lp_fixed ? (lp_g == 8 ? k_leaf_points<16, 256, 8> : k_leaf_points<16, 256, 16>)
                                         : k_leaf_points<0, 0, 16>;
     lpa.tile_leaf = tile_pairs ? ix.tile_leaf.as<uint32_t>() : nullptr;
-    // two-level filter: each tree's active queries in locality order (DETLSH_QSORT, default on)
-    static const int qsort_env = std::getenv("DETLSH_QSORT") ? std::atoi(std::getenv("DETLSH_QSORT")) : 1;
+    // two-level filter: each tree's active queries in locality order (DETLSH_QSORT=1; measured at
+    // configs[4]: no gain in the pair kernel, +9 ms of sorting -- off by default)
+    static const int qsort_env = std::getenv("DETLSH_QSORT") ? std::atoi(std::getenv("DETLSH_QSORT")) : 0;
     const bool qsort_on = qsort_env != 0;
     Scratch s_qk(st, tile_pairs && qsort_on ? sizeof(uint32_t) * (size_t)(4 * qb) : 0);
     if (tile_pairs) ensure_dyn_smem_fn(k_tile_pairs, rf_smem);

@@ -624,7 +624,7 @@ def test_filter_switches_do_not_change_results(tmp_path):
             "chunks": {"DETLSH_CHUNK_PTS": "7000"}, "one_chunk": {"DETLSH_CHUNK_PTS": "0"},
             "morton_leaves": {"DETLSH_LEAF_MORTON": "1"},
             "morton_tile_pairs": {"DETLSH_LEAF_MORTON": "1", "DETLSH_TILE_PAIRS": "1"},
-            "tile_pairs_no_qsort": {"DETLSH_TILE_PAIRS": "1", "DETLSH_QSORT": "0"},
+            "tile_pairs_qsort": {"DETLSH_TILE_PAIRS": "1", "DETLSH_QSORT": "1"},
             "tile_pairs_chunks": {"DETLSH_TILE_PAIRS": "1", "DETLSH_CHUNK_PTS": "7000"},
             "stripes_chunks": {"DETLSH_RF_STRIPES": "1", "DETLSH_CHUNK_PTS": "7000"},
             "dirty_clear": {"DETLSH_DIRTY_CLEAR": "2"},

@@ -322,6 +322,7 @@ struct RFArgs {
     int t, L, K, N_r, mode;
     int pq_cost;                // per-query path cost per 32-point step, relative to 170 per SIMD chunk
     unsigned int* tctr;         // [groups] next tile of each group (zeroed by k_group_table), or null
+    int tile_packed;            // k_tile_pairs: list entries hold packed leaf ranges (see there)
     int dbg;                    // experiments (DETLSH_RF_DEBUG): 1 = per-query leaf test; 2 = tile screen
                                 // also on the 16-query SIMD leaf path (DETLSH_RF_TSCREEN=1)
     uint32_t* plist;            // CELL, sparse tiles: per-query lists of reachable leaves [Qb][pcap] (or null)
@@ -931,10 +932,17 @@ __global__ void __launch_bounds__(RF_THREADS, RF_CTAS) k_tile_pairs(RFArgs a) {
             w_cnt[16 + lane] = c_ ? atomicAdd(a.pcnt + s_q[lane], c_) : 0u;
         }
         __syncwarp();
+        // list entry: the tile's leaf range packed as (first leaf << 5 | count - 1) when the index
+        // has < 2^27 leaves (the pair kernel then skips one dependent load), else the tile index
+        uint32_t entry = (uint32_t)T;
+        if (m && a.tile_packed) {
+            const uint32_t lb0 = a.tile_leaf[T], le0 = a.tile_leaf[T + 1];
+            entry = (lb0 << 5) | (le0 - lb0 - 1);
+        }
         for (uint32_t mm = m; mm; mm &= mm - 1) {
             const int g = __ffs(mm) - 1;
             const uint32_t sl = w_cnt[16 + g] + atomicAdd(&w_slot[g], 1u);
-            a.plist[(int64_t)s_q[g] * a.pcap + sl] = (uint32_t)T;
+            a.plist[(int64_t)s_q[g] * a.pcap + sl] = entry;
         }
         __syncwarp();
     }
@@ -998,6 +1006,7 @@ struct LPArgs {
     unsigned long long* ctr;
     const uint32_t* tile_leaf;  // non-null: the lists hold tiles (k_tile_pairs), each expanded into its
                                 // leaves here (one tile per warp chunk, lane = leaf; LPG = 32)
+    int tile_packed;            // the tile entries are packed leaf ranges (first leaf << 5 | count - 1)
 };
 
 constexpr int LP_THREADS = 256;     // threads per pair-kernel block (512 with half the blocks: slower)
@@ -1094,8 +1103,15 @@ __global__ void __launch_bounds__(LP_THREADS, LPG == 32 ? 5 : 6) k_leaf_points(L
         uint32_t my_p0 = 0, my_sz = 0;
         int64_t my_l = -1;
         if (a.tile_leaf) {
-            const uint32_t T = pl[e0];
-            const uint32_t lb0 = a.tile_leaf[T], le0 = a.tile_leaf[T + 1];
+            const uint32_t E = pl[e0];
+            uint32_t lb0, le0;
+            if (a.tile_packed) {
+                lb0 = E >> 5;
+                le0 = lb0 + (E & 31u) + 1;
+            } else {
+                lb0 = a.tile_leaf[E];
+                le0 = a.tile_leaf[E + 1];
+            }
             if (lane < LPG && lb0 + lane < le0) my_l = lb0 + lane;
         } else if (lane < LPG && e0 + lane < np) {
             my_l = pl[e0 + lane];
@@ -2611,6 +2627,8 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
                              : lp_fixed ? (lp_g == 8 ? k_leaf_points<16, 256, 8> : k_leaf_points<16, 256, 16>)
                                         : k_leaf_points<0, 0, 16>;
     lpa.tile_leaf = tile_pairs ? ix.tile_leaf.as<uint32_t>() : nullptr;
+    lpa.tile_packed = ix.tree_leaf_begin.back() < ((int64_t)1 << 27) ? 1 : 0;
+    ra.tile_packed = lpa.tile_packed;
     // two-level filter: each tree's active queries in locality order (DETLSH_QSORT=1; measured at
     // configs[4]: no gain in the pair kernel, +9 ms of sorting -- off by default)
     static const int qsort_env = std::getenv("DETLSH_QSORT") ? std::atoi(std::getenv("DETLSH_QSORT")) : 0;

@@ -1097,13 +1097,22 @@ __global__ void __launch_bounds__(LP_THREADS, LPG == 32 ? 5 : 6) k_leaf_points(L
     uint32_t lt = 0, lp = 0;                         // tile mode: leaf bounds evaluated / passed
     for (;;) {
         uint32_t ck = 0;     // ptake: the query's next untaken list entry (lists grow over a tree's chunks)
-        if (lane == 0) ck = atomicAdd(a.ptake + q, a.tile_leaf ? 1u : (uint32_t)LPG);
-        const uint32_t e0 = __shfl_sync(0xffffffffu, ck, 0);
+        // tile mode: two listed tiles per take (one atomic and both list loads in flight together)
+        if (lane == 0) ck = atomicAdd(a.ptake + q, a.tile_leaf ? 2u : (uint32_t)LPG);
+        const uint32_t e00 = __shfl_sync(0xffffffffu, ck, 0);
+        if (e00 >= np) break;
+        uint32_t Epre[2] = {0u, 0u};
+        if (a.tile_leaf) {
+            Epre[0] = pl[e00];
+            if (e00 + 1 < np) Epre[1] = pl[e00 + 1];
+        }
+        for (int u = 0; u < (a.tile_leaf ? 2 : 1); ++u) {
+        const uint32_t e0 = e00 + (uint32_t)u;
         if (e0 >= np) break;
         uint32_t my_p0 = 0, my_sz = 0;
         int64_t my_l = -1;
         if (a.tile_leaf) {
-            const uint32_t E = pl[e0];
+            const uint32_t E = Epre[u];
             uint32_t lb0, le0;
             if (a.tile_packed) {
                 lb0 = E >> 5;
@@ -1294,7 +1303,8 @@ __global__ void __launch_bounds__(LP_THREADS, LPG == 32 ? 5 : 6) k_leaf_points(L
                 mark_member(bm, sm, id);
             }
         }
-    }
+    }   // tiles of this take
+    }   // takes
     if (sqn) sb_points(sqn);
     for (int o = 16; o > 0; o >>= 1) {
         tested += __shfl_xor_sync(0xffffffffu, tested, o);

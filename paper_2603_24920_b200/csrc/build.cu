@@ -949,6 +949,160 @@ __global__ void __launch_bounds__(LM_WARPS * 32) k_leaf_morton(const uint32_t* _
     }
 }
 
+// Fused leaf layout for K = 16 (the Morton path): per leaf (warp per leaf), the points' codes
+// are gathered from the data-order codes EP (the k_gather_tcodes step), the points sorted by
+// their Morton key in registers (bitonic network over 32 / 64 / 128 elements, shuffles for
+// strides < 32, register swaps above; the key's low 7 bits carry the element's original slot,
+// so keys are distinct and the order deterministic), perm and tcodes written in that order, and
+// the sub-boxes (runs of kSubBox = 8 positions: one 8-lane group per register) and the leaf's
+// tight box reduced on the fly (k_sb_boxes + k_leaf_tight_sb).  Leaves of > 128 points
+// (unsplittable duplicates) keep their order and take the plain loops.
+__device__ __forceinline__ uint4 vmin4(uint4 a, uint4 b) {
+    return make_uint4(__vminu4(a.x, b.x), __vminu4(a.y, b.y), __vminu4(a.z, b.z), __vminu4(a.w, b.w));
+}
+__device__ __forceinline__ uint4 vmax4(uint4 a, uint4 b) {
+    return make_uint4(__vmaxu4(a.x, b.x), __vmaxu4(a.y, b.y), __vmaxu4(a.z, b.z), __vmaxu4(a.w, b.w));
+}
+__device__ __forceinline__ uint4 shfl_xor4(uint4 v, int m) {
+    return make_uint4(__shfl_xor_sync(0xffffffffu, v.x, m), __shfl_xor_sync(0xffffffffu, v.y, m),
+                      __shfl_xor_sync(0xffffffffu, v.z, m), __shfl_xor_sync(0xffffffffu, v.w, m));
+}
+constexpr int LL_WARPS = 8;
+__global__ void __launch_bounds__(LL_WARPS * 32) k_leaf_layout16(const uint32_t* __restrict__ leaf_off, int64_t nl,
+                                                                 const uint32_t* __restrict__ sb_off,
+                                                                 uint32_t* __restrict__ perm, const uint8_t* __restrict__ EP,
+                                                                 int64_t n, int LK, uint8_t* __restrict__ tcodes,
+                                                                 uint8_t* __restrict__ sbox, uint8_t* __restrict__ tbox) {
+    __shared__ uint4 s_c[LL_WARPS][128];
+    __shared__ uint32_t s_p[LL_WARPS][128];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const uint4 NEUT_LO = make_uint4(~0u, ~0u, ~0u, ~0u), NEUT_HI = make_uint4(0, 0, 0, 0);
+    for (int64_t l = (int64_t)blockIdx.x * LL_WARPS + w; l < nl; l += (int64_t)gridDim.x * LL_WARPS) {
+        const uint32_t p0 = leaf_off[l];
+        const int m = (int)(leaf_off[l + 1] - p0);
+        const int t = (int)(p0 / n);
+        const int64_t cb = (int64_t)t * 16;
+        uint32_t sb0 = sb_off[l];
+        if (m > 128) {     // unsplittable oversized leaf: gather in place, boxes by plain loops
+            for (int e = lane; e < m; e += 32) {
+                const uint4 c = *reinterpret_cast<const uint4*>(EP + (int64_t)perm[p0 + e] * LK + cb);
+                *reinterpret_cast<uint4*>(tcodes + (int64_t)(p0 + e) * 16) = c;
+            }
+            __syncwarp();
+            uint4 tl = NEUT_LO, th = NEUT_HI;
+            for (int s = lane; s < (m + kSubBox - 1) / kSubBox; s += 32) {
+                uint4 lo = NEUT_LO, hi = NEUT_HI;
+                for (int e = s * kSubBox; e < min(m, (s + 1) * kSubBox); ++e) {
+                    const uint4 c = *reinterpret_cast<const uint4*>(tcodes + (int64_t)(p0 + e) * 16);
+                    lo = vmin4(lo, c);
+                    hi = vmax4(hi, c);
+                }
+                *reinterpret_cast<uint4*>(sbox + (int64_t)(sb0 + s) * 32) = lo;
+                *reinterpret_cast<uint4*>(sbox + (int64_t)(sb0 + s) * 32 + 16) = hi;
+                tl = vmin4(tl, lo);
+                th = vmax4(th, hi);
+            }
+            for (int o = 16; o > 0; o >>= 1) {
+                tl = vmin4(tl, shfl_xor4(tl, o));
+                th = vmax4(th, shfl_xor4(th, o));
+            }
+            if (lane == 0) {
+                *reinterpret_cast<uint4*>(tbox + l * 32) = tl;
+                *reinterpret_cast<uint4*>(tbox + l * 32 + 16) = th;
+            }
+            continue;
+        }
+        const int R = m <= 32 ? 1 : m <= 64 ? 2 : 4;          // elements per lane (P2 = 32 R)
+        unsigned long long key[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const int e = r * 32 + lane;
+            key[r] = ~0ull;
+            if (r < R && e < m) {
+                const uint32_t id = perm[p0 + e];
+                const uint4 c = *reinterpret_cast<const uint4*>(EP + (int64_t)id * LK + cb);
+                s_c[w][e] = c;
+                s_p[w][e] = id;
+                unsigned long long k = 0;
+#pragma unroll
+                for (int b = 7; b > 3; --b)
+                    k = (k << 16) | (plane_nibble(c.x, b) << 12) | (plane_nibble(c.y, b) << 8) |
+                        (plane_nibble(c.z, b) << 4) | plane_nibble(c.w, b);
+                key[r] = ((k >> 1) & ~127ull) | (unsigned long long)e;     // real keys < 2^63
+            } else if (r < R) {
+                key[r] = (1ull << 63) | (unsigned long long)e;             // padding: after every real key
+            }
+        }
+        // bitonic sort, ascending, element e = r * 32 + lane (compile-time register indices only)
+        const int P2 = 32 * R;
+        auto cmpx = [](unsigned long long& x, unsigned long long& y, bool asc) {   // x: lower slot
+            const unsigned long long mn = x < y ? x : y, mx = x < y ? y : x;
+            x = asc ? mn : mx;
+            y = asc ? mx : mn;
+        };
+        for (int size = 2; size <= P2; size <<= 1) {
+            for (int stride = size >> 1; stride > 0; stride >>= 1) {
+                if (stride >= 64) {                       // pairs (0,2), (1,3)
+                    cmpx(key[0], key[2], ((0 * 32 + lane) & size) == 0);
+                    cmpx(key[1], key[3], ((1 * 32 + lane) & size) == 0);
+                } else if (stride == 32) {                // pairs (0,1), (2,3)
+                    cmpx(key[0], key[1], ((0 * 32 + lane) & size) == 0);
+                    if (R == 4) cmpx(key[2], key[3], ((2 * 32 + lane) & size) == 0);
+                } else {
+#pragma unroll
+                    for (int r = 0; r < 4; ++r) {
+                        if (r >= R) continue;
+                        const int e = r * 32 + lane;
+                        const unsigned long long other = __shfl_xor_sync(0xffffffffu, key[r], stride);
+                        const bool asc = (e & size) == 0, lower = (e & stride) == 0;
+                        const unsigned long long mn = key[r] < other ? key[r] : other;
+                        const unsigned long long mx = key[r] < other ? other : key[r];
+                        key[r] = (lower == asc) ? mn : mx;
+                    }
+                }
+            }
+        }
+        __syncwarp();
+        uint4 tl = NEUT_LO, th = NEUT_HI;
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            if (r >= R) continue;
+            const int e = r * 32 + lane;
+            uint4 c = NEUT_LO, cmax = NEUT_HI;
+            if (e < m) {
+                const int src = (int)(key[r] & 127ull);
+                c = s_c[w][src];
+                cmax = c;
+                perm[p0 + e] = s_p[w][src];
+                *reinterpret_cast<uint4*>(tcodes + (int64_t)(p0 + e) * 16) = c;
+            }
+            // sub-box of positions [8 s, 8 s + 8): lanes of one aligned 8-lane group
+            uint4 lo = c, hi = cmax;
+#pragma unroll
+            for (int o = 1; o < kSubBox; o <<= 1) {
+                lo = vmin4(lo, shfl_xor4(lo, o));
+                hi = vmax4(hi, shfl_xor4(hi, o));
+            }
+            if ((lane & (kSubBox - 1)) == 0 && e < m) {
+                const uint32_t s = sb0 + (uint32_t)(e / kSubBox);
+                *reinterpret_cast<uint4*>(sbox + (int64_t)s * 32) = lo;
+                *reinterpret_cast<uint4*>(sbox + (int64_t)s * 32 + 16) = hi;
+            }
+            tl = vmin4(tl, lo);
+            th = vmax4(th, hi);
+        }
+        for (int o = 8; o < 32; o <<= 1) {
+            tl = vmin4(tl, shfl_xor4(tl, o));
+            th = vmax4(th, shfl_xor4(th, o));
+        }
+        if (lane == 0) {
+            *reinterpret_cast<uint4*>(tbox + l * 32) = tl;
+            *reinterpret_cast<uint4*>(tbox + l * 32 + 16) = th;
+        }
+        __syncwarp();
+    }
+}
+
 // Sub-boxes: each leaf's points cut into runs of kSubBox consecutive points (leaf order); per
 // run the min/max code per dim.  A valid lower bound for every member, tighter than the leaf's
 // (a few points span less of each dim): the pair kernel screens runs before their points.
@@ -1343,18 +1497,28 @@ static bool build_trees_try(Index& ix, const uint8_t* d_EP, int64_t leaf_factor,
     unsigned long long* d_tbeg = d_lbeg + (L + 1);
     DL_LAUNCH(k_tree_begin, 1, 64, 0, st, ix.leaf_off.as<uint32_t>(), nl, n, (int)L, d_lbeg);
     ix.tcodes.alloc((size_t)total * K, st);
-    DL_LAUNCH(k_gather_tcodes, grid_for(total, 256), 256, 0, st, perm, d_EP, n, (int)L, K, ix.tcodes.as<uint8_t>());
     // DETLSH_LEAF_MORTON: 1 always, 0 never, default when leaves are large (first-layer cells of
     // >= 64 points on average: configs[3], configs[4]; at configs[1] the ~19-point leaves have 2-3
     // sub-boxes, and the sort cost 0.23 ms of build for 0.03 ms of query)
     static const int morton_env = std::getenv("DETLSH_LEAF_MORTON") ? std::atoi(std::getenv("DETLSH_LEAF_MORTON")) : -1;
-    if (K <= 32 && (morton_env == 1 || (morton_env < 0 && (n >> K) >= 64)))
-        DL_LAUNCH(k_leaf_morton, grid_for(nl, LM_WARPS, 148 * 16), LM_WARPS * 32, 0, st, ix.leaf_off.as<uint32_t>(), nl, K,
-                  perm, ix.tcodes.as<uint8_t>());
-    build_subboxes(ix, nl, st);
+    static const int fused_env = std::getenv("DETLSH_LEAF_FUSED") ? std::atoi(std::getenv("DETLSH_LEAF_FUSED")) : 1;
+    const bool morton = K <= 32 && (morton_env == 1 || (morton_env < 0 && (n >> K) >= 64));
     ix.leaf_tbox.alloc((size_t)nl * 2 * K, st);
-    DL_LAUNCH(k_leaf_tight_sb, grid_for(nl, 256), 256, 0, st, ix.sb_off.as<uint32_t>(), nl, K, ix.sb_box.as<uint8_t>(),
-              ix.leaf_tbox.as<uint8_t>());
+    if (morton && K == 16 && (LK & 15) == 0 && fused_env) {
+        // gather + Morton order + sub-boxes + tight boxes in one pass (k_leaf_layout16)
+        build_subboxes(ix, nl, st, false);
+        DL_LAUNCH(k_leaf_layout16, grid_for(nl, LL_WARPS, 148 * 16), LL_WARPS * 32, 0, st, ix.leaf_off.as<uint32_t>(), nl,
+                  ix.sb_off.as<uint32_t>(), perm, d_EP, n, LK, ix.tcodes.as<uint8_t>(), ix.sb_box.as<uint8_t>(),
+                  ix.leaf_tbox.as<uint8_t>());
+    } else {
+        DL_LAUNCH(k_gather_tcodes, grid_for(total, 256), 256, 0, st, perm, d_EP, n, (int)L, K, ix.tcodes.as<uint8_t>());
+        if (morton)
+            DL_LAUNCH(k_leaf_morton, grid_for(nl, LM_WARPS, 148 * 16), LM_WARPS * 32, 0, st, ix.leaf_off.as<uint32_t>(), nl,
+                      K, perm, ix.tcodes.as<uint8_t>());
+        build_subboxes(ix, nl, st, true);
+        DL_LAUNCH(k_leaf_tight_sb, grid_for(nl, 256), 256, 0, st, ix.sb_off.as<uint32_t>(), nl, K, ix.sb_box.as<uint8_t>(),
+                  ix.leaf_tbox.as<uint8_t>());
+    }
     tr.mark("leaf finalize+codes", st);
     // query tiles: runs of kTileLeaves leaves of one tree; the tile count stays on the device
     // (arrays sized by its bound: each tree adds at most one partial tile)
@@ -1390,7 +1554,8 @@ static bool build_trees_try(Index& ix, const uint8_t* d_EP, int64_t leaf_factor,
     return true;
 }
 
-void build_subboxes(Index& ix, int64_t nl, cudaStream_t st) {
+// Sub-box offsets (k_sb_count + scan) and storage; boxes = true also fills them from tcodes.
+void build_subboxes(Index& ix, int64_t nl, cudaStream_t st, bool boxes) {
     if (nl <= 0) return;
     ix.sb_off.alloc(sizeof(uint32_t) * (size_t)(nl + 1), st);
     Scratch s_cnt(st, sizeof(uint32_t) * (size_t)(nl + 1));
@@ -1398,8 +1563,9 @@ void build_subboxes(Index& ix, int64_t nl, cudaStream_t st) {
     exclusive_scan_u32(s_cnt.as<uint32_t>(), ix.sb_off.as<uint32_t>(), nl, ix.sb_off.as<uint32_t>() + nl, st);
     const int64_t nsb_ub = (int64_t)ix.n * ix.L / kSubBox + nl;   // each leaf adds at most one partial run
     ix.sb_box.alloc((size_t)nsb_ub * 2 * ix.K, st);
-    DL_LAUNCH(k_sb_boxes, grid_for(nsb_ub, 256), 256, 0, st, ix.leaf_off.as<uint32_t>(), ix.sb_off.as<uint32_t>(), nl,
-              ix.K, ix.tcodes.as<uint8_t>(), ix.sb_box.as<uint8_t>());
+    if (boxes)
+        DL_LAUNCH(k_sb_boxes, grid_for(nsb_ub, 256), 256, 0, st, ix.leaf_off.as<uint32_t>(), ix.sb_off.as<uint32_t>(), nl,
+                  ix.K, ix.tcodes.as<uint8_t>(), ix.sb_box.as<uint8_t>());
 }
 
 // d_flag (optional): a device int read back (into *h_flag) with the build's last host round trip

@@ -87,7 +87,7 @@ void build_index(Index& ix, const float* d_data, int64_t data_ld, const float* b
                  double sample_frac, int proj_impl, cudaStream_t st);
 void build_trees_from_codes(Index& ix, const uint8_t* d_codes, cudaStream_t st);
 // Sub-box tight boxes of the nl leaves (derived from tcodes + leaf_off; also rebuilt on load).
-void build_subboxes(Index& ix, int64_t nl, cudaStream_t st);
+void build_subboxes(Index& ix, int64_t nl, cudaStream_t st, bool boxes = true);
 void build_index_hash_only(Index& ix, cudaStream_t st);
 void gather_rows_strided(const float* d_src, int64_t src_ld, int d, const uint32_t* d_ids, int64_t m, float* d_dst,
                          int64_t dst_ld, cudaStream_t st);

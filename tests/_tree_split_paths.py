@@ -18,12 +18,17 @@ codes = rng.integers(0, N_r, (n, L * K)).astype(np.uint8)
 # enough to finish in shared memory; the rest spread over many small cells.
 hot = rng.random(n) < 0.6
 codes[hot] = rng.integers(0, 12, (int(hot.sum()), L * K)).astype(np.uint8)
-for ms in (128, 20):
-    g = P.detlsh_build_from_codes(codes, L, K, N_r, max_size=ms)
-    for i in range(L):
-        o = O.Tree(codes[:, i * K:(i + 1) * K], K, N_r, ms, builder=1).export()
-        t = g.tree(i)
-        for key in ("leaf_off", "perm", "lo", "hi", "bits"):
-            assert np.array_equal(t[key], o[key]), (ms, i, key)
-    g.free()
+# K = 16, N_r = 256 as well: the fused leaf layout (gather + Morton order + boxes) serves it when
+# the Morton order is on (DETLSH_LEAF_MORTON); its exported perm must still be canonical
+codes16 = rng.integers(0, 256, (n, 2 * 16)).astype(np.uint8)
+codes16[hot] = rng.integers(0, 40, (int(hot.sum()), 2 * 16)).astype(np.uint8)
+for cds, L_, K_, N_r_ in ((codes, L, K, N_r), (codes16, 2, 16, 256)):
+    for ms in (128, 20):
+        g = P.detlsh_build_from_codes(cds, L_, K_, N_r_, max_size=ms)
+        for i in range(L_):
+            o = O.Tree(cds[:, i * K_:(i + 1) * K_], K_, N_r_, ms, builder=1).export()
+            t = g.tree(i)
+            for key in ("leaf_off", "perm", "lo", "hi", "bits"):
+                assert np.array_equal(t[key], o[key]), (K_, ms, i, key)
+        g.free()
 print("OK")

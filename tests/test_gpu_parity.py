@@ -560,8 +560,9 @@ def test_config5_vs_oracle_golden():
             assert np.all(np.diff(dg[q][ok]) >= 0)
 
 
-@pytest.mark.parametrize("local_max", ["0", "300", "1536", "8192"])
-def test_trees_split_paths(local_max):
+@pytest.mark.parametrize("local_max,morton", [("0", "-1"), ("300", "-1"), ("1536", "-1"), ("8192", "-1"),
+                                              ("1536", "1"), ("300", "1")])
+def test_trees_split_paths(local_max, morton):
     """B6 through the global level loop only (0) and through mixes of global levels and the
     shared-memory finish (k_local_finish, nodes of <= local_max points), on codes with one
     ~18K-point first-layer node and many small ones: every variant gives the oracle's trees
@@ -569,7 +570,7 @@ def test_trees_split_paths(local_max):
     import os
     import subprocess
     import sys
-    env = dict(os.environ, DETLSH_LOCAL_MAX=local_max)
+    env = dict(os.environ, DETLSH_LOCAL_MAX=local_max, DETLSH_LEAF_MORTON=morton)
     here = os.path.dirname(os.path.abspath(__file__))
     r = subprocess.run([sys.executable, os.path.join(here, "_tree_split_paths.py")], env=env,
                        capture_output=True, text=True, timeout=600)
@@ -623,6 +624,7 @@ def test_filter_switches_do_not_change_results(tmp_path):
             "tile_screen": {"DETLSH_RF_TSCREEN": "1"}, "tile_pairs": {"DETLSH_TILE_PAIRS": "1"},
             "chunks": {"DETLSH_CHUNK_PTS": "7000"}, "one_chunk": {"DETLSH_CHUNK_PTS": "0"},
             "morton_leaves": {"DETLSH_LEAF_MORTON": "1"},
+            "morton_unfused": {"DETLSH_LEAF_MORTON": "1", "DETLSH_LEAF_FUSED": "0"},
             "morton_tile_pairs": {"DETLSH_LEAF_MORTON": "1", "DETLSH_TILE_PAIRS": "1"},
             "tile_pairs_qsort": {"DETLSH_TILE_PAIRS": "1", "DETLSH_QSORT": "1"},
             "tile_pairs_chunks": {"DETLSH_TILE_PAIRS": "1", "DETLSH_CHUNK_PTS": "7000"},

@@ -300,19 +300,25 @@ def roofline_entry(name, model, ms, hbm, bf16, clocks, launches=1, traffic=None)
     return e
 
 
-def load_traffic():
+def traffic_path(cid: int) -> str:
+    """This workload's `ncu --set full` summary (profiles/traffic_c<cid>.json, written by
+    tools/ncu_summary.py from a capture of the same configuration), else the generic one."""
+    p = os.path.join(ROOT, "profiles", f"traffic_c{cid}.json")
+    return p if os.path.exists(p) else os.path.join(ROOT, "profiles", "traffic.json")
+
+
+def load_traffic(cid: int):
     """DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum) of each modelled
-    kernel, from this round's `ncu --set full` capture (profiles/traffic.json; written by
-    tools/ncu_summary.py from the committed .csv exports)."""
-    path = os.path.join(ROOT, "profiles", "traffic.json")
+    kernel, from the committed ncu capture of this configuration."""
+    path = traffic_path(cid)
     if not os.path.exists(path):
         return None
     return {k: v["dram_bytes_per_launch"] for k, v in json.load(open(path)).get("kernels", {}).items()}
 
 
-def load_pipes():
+def load_pipes(cid: int):
     """ncu ALU-pipe and issue utilisation (% of peak) per kernel, from the same capture."""
-    path = os.path.join(ROOT, "profiles", "traffic.json")
+    path = traffic_path(cid)
     if not os.path.exists(path):
         return {}
     return {k: {"alu_pct": v.get("alu_pct"), "issue_pct": v.get("issue_pct")}
@@ -565,7 +571,7 @@ def main():
         models = kernel_models(cfg, args.steps, st, n_local, cfg.nq, (cfg.d + 7) // 8 * 8)
         models1 = kernel_models(cfg, 1, st, n_local, cfg.nq, (cfg.d + 7) // 8 * 8)
         roofs = []
-        traffic = load_traffic()
+        traffic = load_traffic(args.config)
         all_units = [(k, v, models, "timed region") for k, v in units.items()] + \
                     [(k, v, models1, "extra untimed step") for k, v in prof_extra.items()]
         for kname, (nl_, ms), mset, src in sorted(all_units, key=lambda x: -unit_step_ms[x[0]]):
@@ -575,10 +581,9 @@ def main():
                     e["timed_in"] = src
                     if kname == FILTER_UNIT:
                         e["parts_ms"] = filter_parts
-                        pipes = load_pipes()
-                        e["limiter"] = ("ALU / instruction issue, not HBM: per the committed ncu capture "
-                                        "(profiles/traffic.json) the filter kernels' ALU-pipe and issue "
-                                        "utilisation are given in ncu_pipes; their DRAM traffic is small")
+                        pipes = load_pipes(args.config)
+                        e["limiter"] = (f"see ncu_pipes (ALU-pipe and issue utilisation) and traffic (DRAM bytes "
+                                        f"per launch) from the committed capture {os.path.basename(traffic_path(args.config))}")
                         e["ncu_pipes"] = {k: v for k, v in pipes.items() if k.startswith(FILTER_KERNELS)}
                     roofs.append(e)
                     break

@@ -1017,13 +1017,6 @@ template <int KT, int NRT, int LPG>
 __global__ void __launch_bounds__(LP_THREADS, LPG == 32 ? 5 : 6) k_leaf_points(LPArgs a) {
     extern __shared__ __align__(16) unsigned char lp_smem[];
     __shared__ __align__(16) uint16_t lp_static[(KT > 0 && NRT > 0) ? KT * NRT : 8];
-    // K, N_r fixed: the box bound D_j[clamp(s_j, lo, hi)] as BL_j[lo] + BH_j[hi] with
-    // BL_j[c] = D_j[c] for c > s_j (else 0) and BH_j[c] = D_j[c] for c < s_j (else 0): D_j is 0 at
-    // s_j and the two tables cover the s < lo and s > hi cases -- no clamp (the same terms, so the
-    // same sums and decisions)
-    constexpr bool LH = KT > 0 && NRT > 0;
-    __shared__ __align__(16) uint16_t lp_bl[LH ? KT * NRT : 8];
-    __shared__ __align__(16) uint16_t lp_bh[LH ? KT * NRT : 8];
     const int ai = blockIdx.x;
     if (ai >= (a.dna ? *a.dna : a.na)) return;
     const int q = a.act[ai];
@@ -1042,15 +1035,6 @@ __global__ void __launch_bounds__(LP_THREADS, LPG == 32 ? 5 : 6) k_leaf_points(L
     if (threadIdx.x == 0) { s_tested = 0; s_passed = 0; s_sbt = 0; }
     if (threadIdx.x < K) s_qx[threadIdx.x] = a.sx[((int64_t)q * a.L + a.t) * K + threadIdx.x];
     __syncthreads();
-    if (LH) {
-        for (int i = threadIdx.x; i < KN; i += blockDim.x) {
-            const int c = i & (NRT - 1), sq = s_qx[i / NRT];
-            const uint16_t e = s_e[i];
-            lp_bl[i] = c > sq ? e : (uint16_t)0;
-            lp_bh[i] = c < sq ? e : (uint16_t)0;
-        }
-        __syncthreads();
-    }
     const int lane = threadIdx.x & 31;
     const uint32_t* pl = a.plist + (int64_t)q * a.pcap;
     uint32_t* bm = a.bitmap + (int64_t)q * a.nwords;
@@ -1157,12 +1141,8 @@ __global__ void __launch_bounds__(LP_THREADS, LPG == 32 ? 5 : 6) k_leaf_points(L
                     const int sh = 8 * (j & 3);
                     const uint32_t wl = (j >> 2) == 0 ? lo4.x : (j >> 2) == 1 ? lo4.y : (j >> 2) == 2 ? lo4.z : lo4.w;
                     const uint32_t wh = (j >> 2) == 0 ? hi4.x : (j >> 2) == 1 ? hi4.y : (j >> 2) == 2 ? hi4.z : hi4.w;
-                    if (LH) {
-                        lb += lp_bl[j * NRT + ((wl >> sh) & 255u)] + lp_bh[j * NRT + ((wh >> sh) & 255u)];
-                    } else {
-                        const int c = min(max(s_qx[j], (int)((wl >> sh) & 255u)), (int)((wh >> sh) & 255u));
-                        lb += s_e[j * N_r + c];
-                    }
+                    const int c = min(max(s_qx[j], (int)((wl >> sh) & 255u)), (int)((wh >> sh) & 255u));
+                    lb += s_e[j * N_r + c];
                 }
             } else {
                 for (int j = 0; j < K; ++j)
@@ -1243,12 +1223,8 @@ __global__ void __launch_bounds__(LP_THREADS, LPG == 32 ? 5 : 6) k_leaf_points(L
                             const int sh = 8 * (j & 3);
                             const uint32_t wl = (j >> 2) == 0 ? lo4.x : (j >> 2) == 1 ? lo4.y : (j >> 2) == 2 ? lo4.z : lo4.w;
                             const uint32_t wh = (j >> 2) == 0 ? hi4.x : (j >> 2) == 1 ? hi4.y : (j >> 2) == 2 ? hi4.z : hi4.w;
-                            if (LH) {
-                                lb += lp_bl[j * NRT + ((wl >> sh) & 255u)] + lp_bh[j * NRT + ((wh >> sh) & 255u)];
-                            } else {
-                                const int c = min(max(s_qx[j], (int)((wl >> sh) & 255u)), (int)((wh >> sh) & 255u));
-                                lb += s_e[j * N_r + c];
-                            }
+                            const int c = min(max(s_qx[j], (int)((wl >> sh) & 255u)), (int)((wh >> sh) & 255u));
+                            lb += s_e[j * N_r + c];
                         }
                     } else {
                         for (int j = 0; j < K; ++j)

@@ -818,3 +818,21 @@ def test_projection_variants(tmp_path, ta):
             dd = ((X[cand] - Q[q]) ** 2).sum(1)
             gt.append(cand[np.lexsort((cand, dd))[:10]])
         assert np.array_equal(z[tag + "_ids"], np.array(gt)), tag
+
+
+def test_topk_ties_duplicate_rows_large_k():
+    """Top-k with many exact ties (20 copies of every row, so equal distances across ids of the
+    same aligned 16-id block) at k = 4096, the ABI's maximum: the k best by (distance, id),
+    exactly (the selection's last 4-bit radix pass)."""
+    rng = np.random.default_rng(12)
+    base = rng.standard_normal((300, 24)).astype(np.float32)
+    X = np.ascontiguousarray(np.repeat(base, 20, axis=0))          # 6000 rows, ids 20 i .. 20 i + 19 equal
+    Q = np.ascontiguousarray(base[:5] + 0.01 * rng.standard_normal((5, 24)).astype(np.float32))
+    g = P.detlsh_build(X, 2, 8, 16, 5)
+    for k in (4096, 4080, 37):
+        ig, dg = g.query(Q, k, 1.5, 1e9, 2.0)                         # beta >= 1, huge radius: exact kNN
+        d2 = ((Q[:, None, :].astype(np.float64) - X[None]) ** 2).sum(-1)
+        for q in range(len(Q)):
+            ref = np.lexsort((np.arange(len(X)), d2[q]))[:k]
+            assert np.array_equal(ig[q], ref), (k, q)
+            assert np.allclose(dg[q], np.sqrt(d2[q][ref]), rtol=1e-5)

@@ -15,6 +15,7 @@
 //                 bitonic sort; then the radius test k-th d2 <= (c r)^2 (line 9, AMB-18).
 //  k_finalize     ids (global) and sqrt(d2), ascending by (dist, id) (AMB-21, AMB-28).
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <mutex>
 #include <cmath>
@@ -323,6 +324,7 @@ struct RFArgs {
     int pq_cost;                // per-query path cost per 32-point step, relative to 170 per SIMD chunk
     unsigned int* tctr;         // [groups] next tile of each group (zeroed by k_group_table), or null
     int tile_packed;            // k_tile_pairs: list entries hold packed leaf ranges (see there)
+    unsigned long long* tp_hist;   // experiments (DETLSH_TP_HIST): reached tiles by number of group queries
     int dbg;                    // experiments (DETLSH_RF_DEBUG): 1 = per-query leaf test; 2 = tile screen
                                 // also on the 16-query SIMD leaf path (DETLSH_RF_TSCREEN=1)
     uint32_t* plist;            // CELL, sparse tiles: per-query lists of reachable leaves [Qb][pcap] (or null)
@@ -920,6 +922,7 @@ __global__ void __launch_bounds__(RF_THREADS, RF_CTAS) k_tile_pairs(RFArgs a) {
                                 *reinterpret_cast<const uint4*>(a.tile_hi + T * 16)) & amask;
             c_lt += __popc(amask);
             c_lp += __popc(m);
+            if (a.tp_hist && m) atomicAdd(a.tp_hist + __popc(m), 1ull);
         }
         // append the (query, tile) pairs: per-query counts in the warp, one reservation per query
         // in its global list, then each lane writes its own pairs
@@ -2639,6 +2642,23 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
     lpa.tile_leaf = tile_pairs ? ix.tile_leaf.as<uint32_t>() : nullptr;
     lpa.tile_packed = ix.tree_leaf_begin.back() < ((int64_t)1 << 27) ? 1 : 0;
     ra.tile_packed = lpa.tile_packed;
+    static const bool tp_hist_env = std::getenv("DETLSH_TP_HIST") != nullptr;
+    Scratch s_tph(st, tp_hist_env ? sizeof(unsigned long long) * 17 : 0);
+    ra.tp_hist = tp_hist_env ? s_tph.as<unsigned long long>() : nullptr;
+    if (tp_hist_env) DL_CUDA(cudaMemsetAsync(s_tph.p, 0, sizeof(unsigned long long) * 17, st));
+    struct TpHistPrint {      // experiments: print the histogram when the query call ends
+        unsigned long long* d;
+        cudaStream_t st;
+        ~TpHistPrint() {
+            if (!d) return;
+            unsigned long long h[17];
+            if (cudaMemcpyAsync(h, d, sizeof(h), cudaMemcpyDeviceToHost, st) != cudaSuccess) return;
+            if (cudaStreamSynchronize(st) != cudaSuccess) return;
+            std::fprintf(stderr, "DETLSH_TP_HIST reached tiles by group queries:");
+            for (int i = 1; i <= 16; ++i) std::fprintf(stderr, " %llu", h[i]);
+            std::fprintf(stderr, "\n");
+        }
+    } tp_hist_print{ra.tp_hist, st};
     // two-level filter: each tree's active queries in locality order (DETLSH_QSORT=1; measured at
     // configs[4]: no gain in the pair kernel, +9 ms of sorting -- off by default)
     static const int qsort_env = std::getenv("DETLSH_QSORT") ? std::atoi(std::getenv("DETLSH_QSORT")) : 0;

@@ -1402,7 +1402,7 @@ static bool build_trees_try(Index& ix, const uint8_t* d_EP, int64_t leaf_factor,
     uint32_t* n_loc = counters + 5;
     // nodes of <= LM points finish in shared memory (k_local_finish); LM keeps the live
     // sub-nodes of one level within LF_MAXSEG and the positions within 16 bits
-    static const int lm_env = std::getenv("DETLSH_LOCAL_MAX") ? std::atoi(std::getenv("DETLSH_LOCAL_MAX")) : 1536;
+    const int lm_env = std::getenv("DETLSH_LOCAL_MAX") ? std::atoi(std::getenv("DETLSH_LOCAL_MAX")) : 1536;   // read per build
     // (scan flags of one thread fit 32 bits: LM <= 32 * 256; staged codes + indices fit shared memory)
     const int64_t lm_smem = (int64_t)(200 * 1024) / ((K <= 16 ? 16 : 32) + 11);
     const int LM = (int)std::min<int64_t>(std::min<int64_t>(std::min<int64_t>(lm_env, 8192), lm_smem),
@@ -1452,7 +1452,7 @@ static bool build_trees_try(Index& ix, const uint8_t* d_EP, int64_t leaf_factor,
     }
     if (sk.local_max > 0) {
         const size_t lsm = local_finish_smem(LM, K);
-        static const int lf_nt = std::getenv("DETLSH_LF_THREADS") ? std::atoi(std::getenv("DETLSH_LF_THREADS")) : 256;
+        const int lf_nt = std::getenv("DETLSH_LF_THREADS") ? std::atoi(std::getenv("DETLSH_LF_THREADS")) : 256;
         const int LF_THREADS = lf_nt == 256 ? 256 : 512;
         auto k_local_finish_sel = K <= 16 ? (LF_THREADS == 256 ? k_local_finish<16, 256> : k_local_finish<16, 512>)
                                           : (LF_THREADS == 256 ? k_local_finish<32, 256> : k_local_finish<32, 512>);

@@ -627,6 +627,8 @@ def test_filter_switches_do_not_change_results(tmp_path):
             "morton_unfused": {"DETLSH_LEAF_MORTON": "1", "DETLSH_LEAF_FUSED": "0"},
             "morton_tile_pairs": {"DETLSH_LEAF_MORTON": "1", "DETLSH_TILE_PAIRS": "1"},
             "tile_pairs_qsort": {"DETLSH_TILE_PAIRS": "1", "DETLSH_QSORT": "1"},
+            "tile_pairs_split1": {"DETLSH_TILE_PAIRS": "1", "DETLSH_LEAF_MORTON": "1", "DETLSH_LP_SPLIT": "1"},
+            "tile_pairs_split3": {"DETLSH_TILE_PAIRS": "1", "DETLSH_LEAF_MORTON": "1", "DETLSH_LP_SPLIT": "3"},
             "tile_pairs_chunks": {"DETLSH_TILE_PAIRS": "1", "DETLSH_CHUNK_PTS": "7000"},
             "stripes_chunks": {"DETLSH_RF_STRIPES": "1", "DETLSH_CHUNK_PTS": "7000"},
             "dirty_clear": {"DETLSH_DIRTY_CLEAR": "2"},

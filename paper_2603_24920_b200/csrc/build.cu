@@ -346,10 +346,6 @@ __global__ void k_first_key(const uint8_t* __restrict__ EP, int64_t n, int L, in
     }
 }
 
-__global__ void k_iota_mod(uint32_t* __restrict__ v, int64_t total, int64_t n) {
-    for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total; g += (int64_t)gridDim.x * blockDim.x)
-        v[g] = (uint32_t)(g % n);
-}
 
 __global__ void k_seg_flags(const uint32_t* __restrict__ keys, int64_t n, int64_t total, uint32_t* __restrict__ flags) {
     for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total;
@@ -604,14 +600,16 @@ __global__ void k_make_children(const Node* __restrict__ nodes, const uint32_t* 
 // node's sub-nodes until every piece is a leaf.  Codes are staged once (gathered from EP);
 // partitions move 16-bit positions only; perm is written back at the end.  One CTA per node
 // (grid-stride over the local list).
-constexpr int LF_MAXSEG = 128;      // live sub-nodes per level (each > max_size points: LM / (max_size+1))
+constexpr int LF_MAXSEG = 64;       // live sub-nodes per level (each > max_size points: LM / (max_size+1))
+constexpr int LF_WSTACK = 8;        // warp-mode stack: pending 1-children, each > max_size points of one
+                                    // sub-node of <= ws points (ws <= LF_WSTACK * (max_size + 1))
 
 template <int KM, int LF_THREADS>   // KM >= K: 16 or 32 (split-count registers)
 __global__ void __launch_bounds__(LF_THREADS, 1024 / LF_THREADS) k_local_finish(const Node* __restrict__ loc, const uint32_t* __restrict__ n_loc_p,
                                                              int LM, uint32_t* __restrict__ perm, const uint8_t* __restrict__ EP,
                                                              int64_t n, int LK, int K, int nb, int max_size,
                                                              Node* __restrict__ leaves, uint32_t* __restrict__ n_leaves,
-                                                             uint32_t cap_leaves) {
+                                                             uint32_t cap_leaves, int ws) {
     extern __shared__ __align__(16) unsigned char lf_smem[];
     const int CB = K <= 16 ? 16 : 32;                                     // code bytes per point
     uint8_t* s_code = lf_smem;                                            // [LM][CB], load order
@@ -623,6 +621,11 @@ __global__ void __launch_bounds__(LF_THREADS, 1024 / LF_THREADS) k_local_finish(
     __shared__ Node s_act[2][LF_MAXSEG];
     __shared__ int s_dim[LF_MAXSEG], s_shift[LF_MAXSEG];
     __shared__ uint32_t s_nact[2], s_wsum[LF_THREADS / 32];
+    // warp mode (ws > 0): sub-nodes of <= ws points leave the block-wide levels for a list that the
+    // warps then finish one sub-node each, depth first with a private stack and no block barriers
+    __shared__ Node s_wl[LF_MAXSEG];
+    __shared__ uint32_t s_nwl;
+    __shared__ Node s_wst[LF_THREADS / 32][LF_WSTACK];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = LF_THREADS / 32;
     const uint32_t n_loc = *n_loc_p;
     for (uint32_t a = blockIdx.x; a < n_loc; a += gridDim.x) {
@@ -641,7 +644,17 @@ __global__ void __launch_bounds__(LF_THREADS, 1024 / LF_THREADS) k_local_finish(
                 for (int j = 0; j < K; ++j) s_code[i * CB + j] = c[j];
             }
         }
-        if (tid == 0) { s_act[0][0] = nd; s_nact[0] = 1; }
+        if (tid == 0) {
+            s_nwl = 0;
+            if (ws > 0 && m <= ws) {   // whole node in warp mode
+                s_wl[0] = nd;
+                s_nwl = 1;
+                s_nact[0] = 0;
+            } else {
+                s_act[0][0] = nd;
+                s_nact[0] = 1;
+            }
+        }
         __syncthreads();
         uint16_t* ix = s_ixa;
         uint16_t* ix2 = s_ixb;
@@ -742,6 +755,8 @@ __global__ void __launch_bounds__(LF_THREADS, 1024 / LF_THREADS) k_local_finish(
                     if (ch.len == 0) continue;
                     if ((int64_t)ch.len <= max_size || !splittable(ch.bits, K, nb)) {
                         push_node(leaves, n_leaves, cap_leaves, ch);
+                    } else if ((int)ch.len <= ws) {
+                        s_wl[atomicAdd(&s_nwl, 1u)] = ch;
                     } else {
                         const uint32_t k = atomicAdd(&s_nact[cur ^ 1], 1u);
                         s_act[cur ^ 1][k] = ch;
@@ -751,6 +766,102 @@ __global__ void __launch_bounds__(LF_THREADS, 1024 / LF_THREADS) k_local_finish(
             __syncthreads();
             uint16_t* tmp = ix; ix = ix2; ix2 = tmp;
         }
+        // warp mode: the same SplitNode rule and stable partition per sub-node, by one warp
+        // (ballots over 32 positions at a time).  pad0 = where the sub-node's order lives (0: ix,
+        // 1: ix2); a finished piece in ix2 is copied back so the final write reads ix only.
+        const uint32_t nwl = s_nwl;
+        const uint32_t lt = lanemask_lt();
+        for (uint32_t wi = warp; wi < nwl; wi += nwarps) {
+            Node* stk = s_wst[warp];
+            int sp = 0;
+            Node cn = s_wl[wi];
+            cn.pad0 = 0;
+            for (;;) {
+                const int st = (int)(cn.start - base), len = (int)cn.len;
+                const uint16_t* src = cn.pad0 ? ix2 : ix;
+                uint16_t* dst = cn.pad0 ? ix : ix2;
+                // SplitNode dimension over the first max_size points (ties to the lowest dim)
+                int best = -1, best_imb = 0x7fffffff;
+                {
+                    int ones[KM];
+#pragma unroll
+                    for (int j = 0; j < KM; ++j) ones[j] = 0;
+                    for (int e = lane; e < max_size; e += 32) {
+                        const uint8_t* c = s_code + (int)src[st + e] * CB;
+#pragma unroll
+                        for (int j = 0; j < KM; ++j) {
+                            if (j < K) {
+                                const int b = nib(cn.bits, j);
+                                if (b < nb) ones[j] += (c[j] >> (nb - 1 - b)) & 1;
+                            }
+                        }
+                    }
+#pragma unroll
+                    for (int j = 0; j < KM; ++j) {
+                        const int v = __reduce_add_sync(0xffffffffu, ones[j]);
+                        if (j < K && nib(cn.bits, j) < nb) {
+                            const int imb = abs(max_size - 2 * v);
+                            if (imb < best_imb) { best_imb = imb; best = j; }
+                        }
+                    }
+                }
+                const int sh = nb - 1 - nib(cn.bits, best);
+                // zeros first, then ones, each in position order
+                uint32_t Z = 0;
+                for (int e0 = 0; e0 < len; e0 += 32) {
+                    const int e = e0 + lane;
+                    const bool z = e < len && !((s_code[(int)src[st + e] * CB + best] >> sh) & 1);
+                    Z += __popc(__ballot_sync(0xffffffffu, z));
+                }
+                uint32_t zc = 0, oc = 0;
+                for (int e0 = 0; e0 < len; e0 += 32) {
+                    const int e = e0 + lane;
+                    const bool in = e < len;
+                    const uint16_t v = in ? src[st + e] : (uint16_t)0;
+                    const bool z = in && !((s_code[(int)v * CB + best] >> sh) & 1);
+                    const uint32_t bz = __ballot_sync(0xffffffffu, z), bo = __ballot_sync(0xffffffffu, in && !z);
+                    if (z) dst[st + zc + __popc(bz & lt)] = v;
+                    else if (in) dst[st + (int)Z + oc + __popc(bo & lt)] = v;
+                    zc += __popc(bz);
+                    oc += __popc(bo);
+                }
+                __syncwarp();
+                // children: leaves out (copied back into ix when their order is in ix2), the rest
+                // depth first (the 1-child on the stack)
+                Node nxt;
+                bool have = false;
+                for (int b = 1; b >= 0; --b) {
+                    Node ch = cn;
+                    nib_inc(ch.bits, best);
+                    ch.start = b ? cn.start + Z : cn.start;
+                    ch.len = b ? cn.len - Z : Z;
+                    ch.pad0 = cn.pad0 ^ 1u;
+                    if (ch.len == 0) continue;
+                    if ((int64_t)ch.len <= max_size || !splittable(ch.bits, K, nb)) {
+                        if (lane == 0) push_node(leaves, n_leaves, cap_leaves, ch);
+                        if (ch.pad0) {
+                            const int cs = (int)(ch.start - base);
+                            for (int e = lane; e < (int)ch.len; e += 32) ix[cs + e] = ix2[cs + e];
+                        }
+                    } else if (b == 1) {
+                        if (lane == 0) stk[sp] = ch;
+                        ++sp;
+                    } else {
+                        nxt = ch;
+                        have = true;
+                    }
+                }
+                __syncwarp();
+                if (have) {
+                    cn = nxt;
+                } else if (sp > 0) {
+                    cn = stk[--sp];
+                } else {
+                    break;
+                }
+            }
+        }
+        __syncthreads();
         for (int i = tid; i < m; i += LF_THREADS) perm[base + i] = s_id[ix[i]];
         __syncthreads();
     }
@@ -1365,11 +1476,10 @@ static bool build_trees_try(Index& ix, const uint8_t* d_EP, int64_t leaf_factor,
 
     // B5: first-layer keys (from the projection epilogue, or from the codes), stable (key, id)
     // sort per tree
-    if (d_fkey)
-        DL_LAUNCH(k_iota_mod, grid_for(total, 256), 256, 0, st, perm, total, n);
-    else
+    // (the values start as the ids 0..n-1 of every tree: the sort's first pass generates them)
+    if (!d_fkey)
         DL_LAUNCH(k_first_key, grid_for(total, 256), 256, 0, st, d_EP, n, (int)L, K, nb, keys0, perm);
-    bool flip = radix_sort_batched(keys0, perm, keys1, vals1, n, L, K, st);
+    bool flip = radix_sort_batched(keys0, perm, keys1, vals1, n, L, K, st, true);
     const uint32_t* skeys = flip ? keys1 : keys0;
     if (flip) DL_CUDA(cudaMemcpyAsync(perm, vals1, sizeof(uint32_t) * total, cudaMemcpyDeviceToDevice, st));
 
@@ -1461,8 +1571,12 @@ static bool build_trees_try(Index& ix, const uint8_t* d_EP, int64_t leaf_factor,
         DL_CUDA(cudaGetDevice(&dev));
         DL_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
         DL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_local_finish_sel, LF_THREADS, lsm));
+        // warp mode below ws points (DETLSH_LF_WS, read per build; 0 = block-wide levels to the end);
+        // the warp stack bounds it by LF_WSTACK * (max_size + 1)
+        const int ws_env = std::getenv("DETLSH_LF_WS") ? std::atoi(std::getenv("DETLSH_LF_WS")) : 512;
+        const int ws = std::max(0, std::min(ws_env, LF_WSTACK * (max_size + 1)));
         DL_LAUNCH(k_local_finish_sel, nsm * std::max(1, per_sm), LF_THREADS, lsm, st, loc, n_loc, LM, perm, d_EP, n, LK, K,
-                  nb, max_size, leaves, n_leaves, (uint32_t)cap_leaves);
+                  nb, max_size, leaves, n_leaves, (uint32_t)cap_leaves, ws);
     }
     s_tmp.free_();
     s_zc.free_();

@@ -94,9 +94,10 @@ __device__ inline uint32_t lanemask_lt() {
 // ------------------------------------------------------------------ primitives (radix.cu)
 // Stable batched LSD radix sort: nseg independent segments of m u32 keys (segment s at
 // keys + s*m), optional u32 values; sorts on key bits [0, bits).  Ping-pongs between
-// (k0,v0) and (k1,v1); returns true if the result ended in (k1,v1).
+// (k0,v0) and (k1,v1); returns true if the result ended in (k1,v1).  vals_iota: the values
+// start as 0..m-1 in every segment and v0 is not read.
 bool radix_sort_batched(uint32_t* k0, uint32_t* v0, uint32_t* k1, uint32_t* v1, int64_t m,
-                        int64_t nseg, int bits, cudaStream_t st);
+                        int64_t nseg, int bits, cudaStream_t st, bool vals_iota = false);
 // Exclusive scan of n u32 values; writes the total to *d_total (device) if non-null.
 void exclusive_scan_u32(const uint32_t* in, uint32_t* out, int64_t n, uint32_t* d_total,
                         cudaStream_t st);

@@ -237,6 +237,36 @@ __device__ __forceinline__ void mark_member(uint32_t* bm, uint32_t* sm, uint32_t
     atomicOr(sm + (id >> 10), 1u << ((id >> 5) & 31));
 }
 
+// Box bound of one query in the 12-bit table (K = 16, N_r = 256): sum_j e_j[clamp(q_j, lo_j, hi_j)]
+// with the clamps done two dims per instruction -- each code word's even and odd bytes spread
+// into 16-bit lanes (one byte permute each), VIMNMX.U16x2 against the query's codes spread the same
+// way (qe[i] / qo[i]: bytes 0, 2 / 1, 3 of word i), and the lanes' byte offsets into the table
+// (2c) taken from the doubled word.  Same terms as the byte-wise min/max form, same sum.
+__device__ __forceinline__ uint32_t spread_even(uint32_t w) { return __byte_perm(w, 0u, 0x4240); }
+__device__ __forceinline__ uint32_t spread_odd(uint32_t w) { return __byte_perm(w, 0u, 0x4341); }
+__device__ __forceinline__ uint32_t clamp_u16x2(uint32_t q, uint32_t lo, uint32_t hi) {
+    uint32_t r;
+    asm("max.u16x2 %0, %1, %2;" : "=r"(r) : "r"(q), "r"(lo));
+    asm("min.u16x2 %0, %0, %1;" : "+r"(r) : "r"(hi));
+    return r;
+}
+__device__ __forceinline__ uint32_t box_bound16(const uint16_t* s_e, const uint32_t* qe, const uint32_t* qo,
+                                                uint4 lo4, uint4 hi4) {
+    const char* tb = reinterpret_cast<const char*>(s_e);
+    const uint32_t lw[4] = {lo4.x, lo4.y, lo4.z, lo4.w}, hw[4] = {hi4.x, hi4.y, hi4.z, hi4.w};
+    uint32_t lb = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const uint32_t ce = clamp_u16x2(qe[i], spread_even(lw[i]), spread_even(hw[i])) * 2u;   // lanes <= 510
+        const uint32_t co = clamp_u16x2(qo[i], spread_odd(lw[i]), spread_odd(hw[i])) * 2u;
+        lb += *reinterpret_cast<const uint16_t*>(tb + (4 * i + 0) * 512 + (ce & 0xFFFFu)) +
+              *reinterpret_cast<const uint16_t*>(tb + (4 * i + 2) * 512 + (ce >> 16));
+        lb += *reinterpret_cast<const uint16_t*>(tb + (4 * i + 1) * 512 + (co & 0xFFFFu)) +
+              *reinterpret_cast<const uint16_t*>(tb + (4 * i + 3) * 512 + (co >> 16));
+    }
+    return lb;
+}
+
 constexpr int NCTR = 5;          // per-query filter counters: leaves tested/passed, points tested/passed, sub-boxes tested
 
 template <int G> struct QuantSpec;
@@ -1010,15 +1040,15 @@ struct LPArgs {
     const uint32_t* tile_leaf;  // non-null: the lists hold tiles (k_tile_pairs), each expanded into its
                                 // leaves here (one tile per warp chunk, lane = leaf; LPG = 32)
     int tile_packed;            // the tile entries are packed leaf ranges (first leaf << 5 | count - 1)
-    unsigned long long* dbg;    // experiments (DETLSH_LP_STATS): points, sub-boxes, leaves: each tested / past dims 0-7
 };
 
 constexpr int LP_THREADS = 256;     // threads per pair-kernel block (512 with half the blocks: slower)
 
 // KT, NRT > 0: K and N_r fixed at compile time (table rows at immediate offsets, a static table);
 // LPG listed leaves per warp chunk
-template <int KT, int NRT, int LPG, int SP = 0>
-__global__ void __launch_bounds__(LP_THREADS, (LPG == 32 || SP) ? 5 : 6) k_leaf_points(LPArgs a) {
+// BX: box bounds by box_bound16 (K = 16, N_r = 256)
+template <int KT, int NRT, int LPG, int BX = 0>
+__global__ void __launch_bounds__(LP_THREADS, LPG == 32 ? 5 : 6) k_leaf_points(LPArgs a) {
     extern __shared__ __align__(16) unsigned char lp_smem[];
     __shared__ __align__(16) uint16_t lp_static[(KT > 0 && NRT > 0) ? KT * NRT : 8];
     const int ai = blockIdx.x;
@@ -1038,6 +1068,13 @@ __global__ void __launch_bounds__(LP_THREADS, (LPG == 32 || SP) ? 5 : 6) k_leaf_
     __shared__ int s_qx[32];                          // the query's region codes in tree t
     if (threadIdx.x == 0) { s_tested = 0; s_passed = 0; s_sbt = 0; }
     if (threadIdx.x < K) s_qx[threadIdx.x] = a.sx[((int64_t)q * a.L + a.t) * K + threadIdx.x];
+    constexpr bool B16 = BX && KT == 16 && NRT == 256;
+    __shared__ uint32_t s_qeo[8];                     // B16: the query's codes spread for box_bound16
+    if (B16 && threadIdx.x >= 32 && threadIdx.x < 40) {
+        const int i = (threadIdx.x - 32) & 3, od = (threadIdx.x - 32) >> 2;
+        const uint8_t* x = a.sx + ((int64_t)q * a.L + a.t) * K + 4 * i + od;
+        s_qeo[threadIdx.x - 32] = (uint32_t)x[0] | ((uint32_t)x[2] << 16);
+    }
     __syncthreads();
     const int lane = threadIdx.x & 31;
     const uint32_t* pl = a.plist + (int64_t)q * a.pcap;
@@ -1053,73 +1090,9 @@ __global__ void __launch_bounds__(LP_THREADS, (LPG == 32 || SP) ? 5 : 6) k_leaf_
     uint32_t* sq_first = s_sqf[threadIdx.x >> 5];
     uint8_t* sq_cnt = s_sqc[threadIdx.x >> 5];
     uint32_t sqn = 0;                                // warp-uniform
-    // Two-stage bounds (K = 16, SP != 0; DETLSH_LP_SPLIT): every term is >= 0, so a partial sum over dims 0-7 that
-    // is already > 2048 rejects.  The survivors are queued per warp and finished 32 at a time (dims
-    // 8-15, then the unchanged accept / band rule), so the rejected majority does not hold lanes
-    // through the second half.  Same terms, same decision for every point and sub-box.
-    __shared__ uint4 s_pq[(KT == 16) ? LP_THREADS / 32 : 1][64];   // points: pos, partial, codes 8-15
-    uint4* pq = s_pq[(KT == 16) ? (threadIdx.x >> 5) : 0];
-    uint32_t pqn = 0, pq_in = 0, bq_in = 0;         // pqn warp-uniform; pq_in / bq_in: stats
-    auto pq_drain = [&](uint32_t m) {
-        if (lane < m) {
-            const uint4 v = pq[pqn - m + lane];
-            uint32_t acc = v.y;
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                const uint32_t w = j < 4 ? v.z : v.w;
-                acc += s_e[(8 + j) * N_r + ((w >> (8 * (j & 3))) & 255u)];
-            }
-            if (acc <= 2048u) {
-                bool pass = acc + 17u <= 2048u;
-                if (!pass) {
-                    const uint4 c4 = *reinterpret_cast<const uint4*>(a.tcodes + (int64_t)v.x * 16);
-                    float s_ = 0.f;
-#pragma unroll
-                    for (int j = 0; j < 16; ++j) {
-                        const uint32_t w = (j >> 2) == 0 ? c4.x : (j >> 2) == 1 ? c4.y : (j >> 2) == 2 ? c4.z : c4.w;
-                        s_ += __ldg(s_d + j * N_r + ((w >> (8 * (j & 3))) & 255u));
-                    }
-                    pass = s_ <= a.rho2;
-                }
-                if (pass) {
-                    ++passed;
-                    mark_member(bm, sm, a.perm[v.x]);
-                }
-            }
-        }
-        pqn -= m;
-        __syncwarp();
-    };
     // screen the points of the last nb queued sub-boxes: lane = (sub-box lane / kSubBox, point)
     auto sb_points = [&](uint32_t nb) {
         const uint32_t sbs = lane / kSubBox, k = lane % kSubBox;
-        if (KT == 16 && (SP & 1)) {
-            bool surv = false;
-            uint32_t pos = 0, acc = 0;
-            uint4 c4 = make_uint4(0, 0, 0, 0);
-            if (sbs < nb) {
-                const uint32_t e = sqn - nb + sbs;
-                if (k < sq_cnt[e]) {
-                    pos = sq_first[e] + k - (uint32_t)a.pos_base;
-                    c4 = *reinterpret_cast<const uint4*>(a.tcodes + (int64_t)pos * 16);
-#pragma unroll
-                    for (int j = 0; j < 8; ++j) {
-                        const uint32_t w = j < 4 ? c4.x : c4.y;
-                        acc += s_e[j * N_r + ((w >> (8 * (j & 3))) & 255u)];
-                    }
-                    ++tested;
-                    surv = acc <= 2048u;
-                }
-            }
-            const uint32_t bal = __ballot_sync(0xffffffffu, surv);
-            if (surv) pq[pqn + __popc(bal & lanemask_lt())] = make_uint4(pos, acc, c4.z, c4.w);
-            pqn += __popc(bal);
-            pq_in += surv;
-            sqn -= nb;
-            __syncwarp();
-            if (pqn >= 32) pq_drain(32);
-            return;
-        }
         if (sbs < nb) {
             const uint32_t e = sqn - nb + sbs;
             if (k < sq_cnt[e]) {
@@ -1162,205 +1135,7 @@ __global__ void __launch_bounds__(LP_THREADS, (LPG == 32 || SP) ? 5 : 6) k_leaf_
         sqn -= nb;
         __syncwarp();
     };
-    // queued sub-boxes past dims 0-7 (SP bit 1): box bytes of dims 8-15 (lo, hi) and
-    // (first point, partial sum << 4 | point count)
-    __shared__ uint4 s_bq4[(KT == 16) ? LP_THREADS / 32 : 1][64];
-    __shared__ uint2 s_bq2[(KT == 16) ? LP_THREADS / 32 : 1][64];
-    uint4* bq4 = s_bq4[(KT == 16) ? (threadIdx.x >> 5) : 0];
-    uint2* bq2 = s_bq2[(KT == 16) ? (threadIdx.x >> 5) : 0];
-    uint32_t bqn = 0;                                // warp-uniform
-    auto bq_drain = [&](uint32_t m) {
-        bool pass = false;
-        uint32_t first = 0, cnt = 0;
-        if (lane < m) {
-            const uint32_t e = bqn - m + lane;
-            const uint4 h = bq4[e];
-            const uint2 f = bq2[e];
-            uint32_t lb = f.y >> 4;
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                const int sh = 8 * (j & 3);
-                const uint32_t wl = j < 4 ? h.x : h.y, wh = j < 4 ? h.z : h.w;
-                const int c = min(max(s_qx[8 + j], (int)((wl >> sh) & 255u)), (int)((wh >> sh) & 255u));
-                lb += s_e[(8 + j) * N_r + c];
-            }
-            pass = lb <= 2048u;
-            first = f.x;
-            cnt = f.y & 15u;
-        }
-        bqn -= m;
-        const uint32_t bal = __ballot_sync(0xffffffffu, pass);
-        if (pass) {
-            const uint32_t slot = sqn + __popc(bal & lanemask_lt());
-            sq_first[slot] = first;
-            sq_cnt[slot] = (uint8_t)cnt;
-        }
-        sqn += __popc(bal);
-        __syncwarp();
-        while (sqn >= 32 / kSubBox) sb_points(32 / kSubBox);
-    };
-    // second level over the sub-boxes of up to LPG leaves held one per lane (my_sz = 0: none)
-    auto sb_enum = [&](int64_t my_l, uint32_t my_p0, uint32_t my_sz) {
-        // second level: the leaves' sub-boxes (kSubBox consecutive points each), packed 32 per
-        // step; each sub-box whose 12-bit bound is <= 2048 is queued, and 32 / kSubBox queued
-        // sub-boxes' points are screened per step (lane = (sub-box, point))
-        const uint32_t my_nsb = (my_sz + kSubBox - 1) / kSubBox;
-        uint32_t my_sb0 = 0;
-        if (my_l >= 0 && my_sz) my_sb0 = a.sb_off[my_l];
-        uint32_t incl = my_nsb;
-#pragma unroll
-        for (int o = 1; o < LPG; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += y;
-        }
-        const uint32_t excl = incl - my_nsb;
-        const uint32_t TS = __shfl_sync(0xffffffffu, incl, LPG - 1);
-        const uint32_t my_end = my_p0 + my_sz;
-        // software pipeline: the next 32 sub-boxes' boxes (one 32-byte row each: lo | hi) are
-        // loaded before this step's bounds are computed (the loads were the top stall, ncu)
-        auto locate = [&](uint32_t i, uint32_t& sbi, uint32_t& first, uint32_t& cnt) {
-            int o_ = 0;                               // last leaf slot with excl <= i
-#pragma unroll
-            for (int st = LPG / 2; st > 0; st >>= 1) {
-                const uint32_t ex = __shfl_sync(0xffffffffu, excl, o_ + st);
-                if (ex <= i) o_ += st;
-            }
-            const uint32_t sb0 = __shfl_sync(0xffffffffu, my_sb0, o_);
-            const uint32_t pp0 = __shfl_sync(0xffffffffu, my_p0, o_);
-            const uint32_t pend = __shfl_sync(0xffffffffu, my_end, o_);
-            const uint32_t pex = __shfl_sync(0xffffffffu, excl, o_);
-            sbi = sb0 + (i - pex);
-            first = pp0 + (i - pex) * kSubBox;
-            cnt = min((uint32_t)kSubBox, pend - first);
-            return i < TS;
-        };
-        uint4 nlo = make_uint4(0, 0, 0, 0), nhi = make_uint4(0, 0, 0, 0);
-        uint32_t nsbi = 0, nfirst = 0, ncnt = 0;
-        bool nvalid = locate(lane, nsbi, nfirst, ncnt);
-        if (K == 16 && nvalid && LPG == 32) {
-            nlo = *reinterpret_cast<const uint4*>(a.sb_lo + (int64_t)nsbi * 32);
-            nhi = *reinterpret_cast<const uint4*>(a.sb_hi + (int64_t)nsbi * 32);
-        }
-        for (uint32_t c0 = 0; c0 < TS; c0 += 32) {
-            const uint4 lo4p = nlo, hi4p = nhi;
-            const uint32_t sbi = nsbi, first_c = nfirst, cnt_c = ncnt;
-            const bool valid = nvalid;
-            if (c0 + 32 < TS) {
-                nvalid = locate(c0 + 32 + lane, nsbi, nfirst, ncnt);
-                // prefetch only in the two-level filter's instantiation (LPG = 32, large n, where
-                // the boxes come from HBM); with LPG = 16 (L2-resident indexes) it cost occupancy
-                if (K == 16 && nvalid && LPG == 32) {
-                    nlo = *reinterpret_cast<const uint4*>(a.sb_lo + (int64_t)nsbi * 32);
-                    nhi = *reinterpret_cast<const uint4*>(a.sb_hi + (int64_t)nsbi * 32);
-                }
-            }
-            bool pass = false;
-            uint32_t first = 0, cnt = 0;
-            if (KT == 16 && (SP & 2)) {
-                uint32_t lb = 0;
-                uint4 lo4 = lo4p, hi4 = hi4p;
-                if (valid) {
-                    if (LPG != 32) {
-                        lo4 = *reinterpret_cast<const uint4*>(a.sb_lo + (int64_t)sbi * 32);
-                        hi4 = *reinterpret_cast<const uint4*>(a.sb_hi + (int64_t)sbi * 32);
-                    }
-#pragma unroll
-                    for (int j = 0; j < 8; ++j) {
-                        const int sh = 8 * (j & 3);
-                        const uint32_t wl = j < 4 ? lo4.x : lo4.y, wh = j < 4 ? hi4.x : hi4.y;
-                        const int c = min(max(s_qx[j], (int)((wl >> sh) & 255u)), (int)((wh >> sh) & 255u));
-                        lb += s_e[j * N_r + c];
-                    }
-                    ++sbt;
-                    pass = lb <= 2048u;
-                }
-                const uint32_t bal = __ballot_sync(0xffffffffu, pass);
-                if (pass) {
-                    const uint32_t slot = bqn + __popc(bal & lanemask_lt());
-                    bq4[slot] = make_uint4(lo4.z, lo4.w, hi4.z, hi4.w);
-                    bq2[slot] = make_uint2(first_c, (lb << 4) | cnt_c);
-                }
-                bqn += __popc(bal);
-                bq_in += pass;
-                __syncwarp();
-                if (bqn >= 32) bq_drain(32);
-                continue;
-            }
-            if (valid) {
-                first = first_c;
-                cnt = cnt_c;
-                uint32_t lb = 0;
-                if (K == 16) {
-                    uint4 lo4 = lo4p, hi4 = hi4p;
-                    if (LPG != 32) {
-                        lo4 = *reinterpret_cast<const uint4*>(a.sb_lo + (int64_t)sbi * 32);
-                        hi4 = *reinterpret_cast<const uint4*>(a.sb_hi + (int64_t)sbi * 32);
-                    }
-#pragma unroll
-                    for (int j = 0; j < 16; ++j) {
-                        const int sh = 8 * (j & 3);
-                        const uint32_t wl = (j >> 2) == 0 ? lo4.x : (j >> 2) == 1 ? lo4.y : (j >> 2) == 2 ? lo4.z : lo4.w;
-                        const uint32_t wh = (j >> 2) == 0 ? hi4.x : (j >> 2) == 1 ? hi4.y : (j >> 2) == 2 ? hi4.z : hi4.w;
-                        const int c = min(max(s_qx[j], (int)((wl >> sh) & 255u)), (int)((wh >> sh) & 255u));
-                        lb += s_e[j * N_r + c];
-                    }
-                } else {
-                    for (int j = 0; j < K; ++j)
-                        lb += s_e[j * N_r + min(max(s_qx[j], (int)a.sb_lo[(int64_t)sbi * 2 * K + j]),
-                                                (int)a.sb_hi[(int64_t)sbi * 2 * K + j])];
-                }
-                pass = lb <= 2048u;
-                ++sbt;
-            }
-            const uint32_t bal = __ballot_sync(0xffffffffu, pass);
-            if (pass) {
-                const uint32_t slot = sqn + __popc(bal & lanemask_lt());
-                sq_first[slot] = first;
-                sq_cnt[slot] = (uint8_t)cnt;
-            }
-            sqn += __popc(bal);
-            __syncwarp();
-            while (sqn >= 32 / kSubBox) {
-                sb_points(32 / kSubBox);
-            }
-        }
-    };
     uint32_t lt = 0, lp = 0;                         // tile mode: leaf bounds evaluated / passed
-    // tile mode, SP bit 2: the listed tiles' leaves bounded in two halves as well; leaves past dims
-    // 0-7 are queued (box bytes of dims 8-15, leaf id, partial sum) and finished 32 at a time, and
-    // the 32 leaves of a drained queue -- only those that pass -- feed one sub-box enumeration
-    // (their leaf offsets are read only then)
-    __shared__ uint4 s_lq4[(SP & 4) ? LP_THREADS / 32 : 1][64];
-    __shared__ uint2 s_lq2[(SP & 4) ? LP_THREADS / 32 : 1][64];
-    uint4* lq4 = s_lq4[(SP & 4) ? (threadIdx.x >> 5) : 0];
-    uint2* lq2 = s_lq2[(SP & 4) ? (threadIdx.x >> 5) : 0];
-    uint32_t lqn = 0, lq_in = 0;                     // lqn warp-uniform
-    auto lq_drain = [&](uint32_t m) {
-        int64_t my_l = -1;
-        uint32_t my_p0 = 0, my_sz = 0;
-        if (lane < m) {
-            const uint32_t e = lqn - m + lane;
-            const uint4 h = lq4[e];
-            const uint2 f = lq2[e];
-            uint32_t lb = f.y;
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                const int sh = 8 * (j & 3);
-                const uint32_t wl = j < 4 ? h.x : h.y, wh = j < 4 ? h.z : h.w;
-                const int c = min(max(s_qx[8 + j], (int)((wl >> sh) & 255u)), (int)((wh >> sh) & 255u));
-                lb += s_e[(8 + j) * N_r + c];
-            }
-            if (lb <= 2048u) {
-                my_l = f.x;
-                my_p0 = a.leaf_off[f.x];
-                my_sz = a.leaf_off[f.x + 1] - my_p0;
-                ++lp;
-            }
-        }
-        lqn -= m;
-        __syncwarp();
-        sb_enum(my_l, my_p0, my_sz);
-    };
     for (;;) {
         uint32_t ck = 0;     // ptake: the query's next untaken list entry (lists grow over a tree's chunks)
         // tile mode: two listed tiles per take (one atomic and both list loads in flight together)
@@ -1391,35 +1166,6 @@ __global__ void __launch_bounds__(LP_THREADS, (LPG == 32 || SP) ? 5 : 6) k_leaf_
         } else if (lane < LPG && e0 + lane < np) {
             my_l = pl[e0 + lane];
         }
-        if (KT == 16 && (SP & 4) && LPG == 32 && a.sb_off) {
-            bool surv = false;
-            uint32_t lb = 0;
-            uint4 lo4 = make_uint4(0, 0, 0, 0), hi4 = make_uint4(0, 0, 0, 0);
-            if (my_l >= 0) {
-                lo4 = *reinterpret_cast<const uint4*>(a.lo + my_l * a.bs);
-                hi4 = *reinterpret_cast<const uint4*>(a.hi + my_l * a.bs);
-#pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                    const int sh = 8 * (j & 3);
-                    const uint32_t wl = j < 4 ? lo4.x : lo4.y, wh = j < 4 ? hi4.x : hi4.y;
-                    const int c = min(max(s_qx[j], (int)((wl >> sh) & 255u)), (int)((wh >> sh) & 255u));
-                    lb += s_e[j * N_r + c];
-                }
-                ++lt;
-                surv = lb <= 2048u;
-            }
-            const uint32_t bal = __ballot_sync(0xffffffffu, surv);
-            if (surv) {
-                const uint32_t slot = lqn + __popc(bal & lanemask_lt());
-                lq4[slot] = make_uint4(lo4.z, lo4.w, hi4.z, hi4.w);
-                lq2[slot] = make_uint2((uint32_t)my_l, lb);
-            }
-            lqn += __popc(bal);
-            lq_in += surv;
-            __syncwarp();
-            if (lqn >= 32) lq_drain(32);
-            continue;
-        }
         if (my_l >= 0) {
             const uint32_t l = (uint32_t)my_l;
             my_p0 = a.leaf_off[l];
@@ -1428,7 +1174,10 @@ __global__ void __launch_bounds__(LP_THREADS, (LPG == 32 || SP) ? 5 : 6) k_leaf_
             // boxes up to ~12 % above rho^2; a sum > 2048 proves the box (hence every point of
             // the leaf) is beyond rho^2 -- the leaf's points are not screened
             uint32_t lb = 0;
-            if (K == 16) {
+            if (B16) {
+                lb = box_bound16(s_e, s_qeo, s_qeo + 4, *reinterpret_cast<const uint4*>(a.lo + (int64_t)l * a.bs),
+                                 *reinterpret_cast<const uint4*>(a.hi + (int64_t)l * a.bs));
+            } else if (K == 16) {
                 const uint4 lo4 = *reinterpret_cast<const uint4*>(a.lo + (int64_t)l * a.bs);
                 const uint4 hi4 = *reinterpret_cast<const uint4*>(a.hi + (int64_t)l * a.bs);
 #pragma unroll
@@ -1448,7 +1197,106 @@ __global__ void __launch_bounds__(LP_THREADS, (LPG == 32 || SP) ? 5 : 6) k_leaf_
             lp += my_sz != 0;
         }
         if (a.sb_off) {
-            sb_enum(my_l, my_p0, my_sz);
+            // second level: the leaves' sub-boxes (kSubBox consecutive points each), packed 32 per
+            // step; each sub-box whose 12-bit bound is <= 2048 is queued, and 32 / kSubBox queued
+            // sub-boxes' points are screened per step (lane = (sub-box, point))
+            const uint32_t my_nsb = (my_sz + kSubBox - 1) / kSubBox;
+            uint32_t my_sb0 = 0;
+            if (my_l >= 0 && my_sz) my_sb0 = a.sb_off[my_l];
+            uint32_t incl = my_nsb;
+#pragma unroll
+            for (int o = 1; o < LPG; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            const uint32_t excl = incl - my_nsb;
+            const uint32_t TS = __shfl_sync(0xffffffffu, incl, LPG - 1);
+            const uint32_t my_end = my_p0 + my_sz;
+            // software pipeline: the next 32 sub-boxes' boxes (one 32-byte row each: lo | hi) are
+            // loaded before this step's bounds are computed (the loads were the top stall, ncu)
+            auto locate = [&](uint32_t i, uint32_t& sbi, uint32_t& first, uint32_t& cnt) {
+                int o_ = 0;                               // last leaf slot with excl <= i
+#pragma unroll
+                for (int st = LPG / 2; st > 0; st >>= 1) {
+                    const uint32_t ex = __shfl_sync(0xffffffffu, excl, o_ + st);
+                    if (ex <= i) o_ += st;
+                }
+                const uint32_t sb0 = __shfl_sync(0xffffffffu, my_sb0, o_);
+                const uint32_t pp0 = __shfl_sync(0xffffffffu, my_p0, o_);
+                const uint32_t pend = __shfl_sync(0xffffffffu, my_end, o_);
+                const uint32_t pex = __shfl_sync(0xffffffffu, excl, o_);
+                sbi = sb0 + (i - pex);
+                first = pp0 + (i - pex) * kSubBox;
+                cnt = min((uint32_t)kSubBox, pend - first);
+                return i < TS;
+            };
+            uint4 nlo = make_uint4(0, 0, 0, 0), nhi = make_uint4(0, 0, 0, 0);
+            uint32_t nsbi = 0, nfirst = 0, ncnt = 0;
+            bool nvalid = locate(lane, nsbi, nfirst, ncnt);
+            if (K == 16 && nvalid && LPG == 32) {
+                nlo = *reinterpret_cast<const uint4*>(a.sb_lo + (int64_t)nsbi * 32);
+                nhi = *reinterpret_cast<const uint4*>(a.sb_hi + (int64_t)nsbi * 32);
+            }
+            for (uint32_t c0 = 0; c0 < TS; c0 += 32) {
+                const uint4 lo4p = nlo, hi4p = nhi;
+                const uint32_t sbi = nsbi, first_c = nfirst, cnt_c = ncnt;
+                const bool valid = nvalid;
+                if (c0 + 32 < TS) {
+                    nvalid = locate(c0 + 32 + lane, nsbi, nfirst, ncnt);
+                    // prefetch only in the two-level filter's instantiation (LPG = 32, large n, where
+                    // the boxes come from HBM); with LPG = 16 (L2-resident indexes) it cost occupancy
+                    if (K == 16 && nvalid && LPG == 32) {
+                        nlo = *reinterpret_cast<const uint4*>(a.sb_lo + (int64_t)nsbi * 32);
+                        nhi = *reinterpret_cast<const uint4*>(a.sb_hi + (int64_t)nsbi * 32);
+                    }
+                }
+                bool pass = false;
+                uint32_t first = 0, cnt = 0;
+                if (valid) {
+                    first = first_c;
+                    cnt = cnt_c;
+                    uint32_t lb = 0;
+                    if (B16) {
+                        uint4 lo4 = lo4p, hi4 = hi4p;
+                        if (LPG != 32) {
+                            lo4 = *reinterpret_cast<const uint4*>(a.sb_lo + (int64_t)sbi * 32);
+                            hi4 = *reinterpret_cast<const uint4*>(a.sb_hi + (int64_t)sbi * 32);
+                        }
+                        lb = box_bound16(s_e, s_qeo, s_qeo + 4, lo4, hi4);
+                    } else if (K == 16) {
+                        uint4 lo4 = lo4p, hi4 = hi4p;
+                        if (LPG != 32) {
+                            lo4 = *reinterpret_cast<const uint4*>(a.sb_lo + (int64_t)sbi * 32);
+                            hi4 = *reinterpret_cast<const uint4*>(a.sb_hi + (int64_t)sbi * 32);
+                        }
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) {
+                            const int sh = 8 * (j & 3);
+                            const uint32_t wl = (j >> 2) == 0 ? lo4.x : (j >> 2) == 1 ? lo4.y : (j >> 2) == 2 ? lo4.z : lo4.w;
+                            const uint32_t wh = (j >> 2) == 0 ? hi4.x : (j >> 2) == 1 ? hi4.y : (j >> 2) == 2 ? hi4.z : hi4.w;
+                            const int c = min(max(s_qx[j], (int)((wl >> sh) & 255u)), (int)((wh >> sh) & 255u));
+                            lb += s_e[j * N_r + c];
+                        }
+                    } else {
+                        for (int j = 0; j < K; ++j)
+                            lb += s_e[j * N_r + min(max(s_qx[j], (int)a.sb_lo[(int64_t)sbi * 2 * K + j]),
+                                                    (int)a.sb_hi[(int64_t)sbi * 2 * K + j])];
+                    }
+                    pass = lb <= 2048u;
+                    ++sbt;
+                }
+                const uint32_t bal = __ballot_sync(0xffffffffu, pass);
+                if (pass) {
+                    const uint32_t slot = sqn + __popc(bal & lanemask_lt());
+                    sq_first[slot] = first;
+                    sq_cnt[slot] = (uint8_t)cnt;
+                }
+                sqn += __popc(bal);
+                __syncwarp();
+                while (sqn >= 32 / kSubBox) {
+                    sb_points(32 / kSubBox);
+                }
+            }
             continue;
         }
         uint32_t incl = my_sz;
@@ -1508,31 +1356,13 @@ __global__ void __launch_bounds__(LP_THREADS, (LPG == 32 || SP) ? 5 : 6) k_leaf_
         }
     }   // tiles of this take
     }   // takes
-    if (lqn) lq_drain(lqn);
-    if (bqn) bq_drain(bqn);
     if (sqn) sb_points(sqn);
-    if (pqn) pq_drain(pqn);
-    if (a.dbg) {
-        for (int o = 16; o > 0; o >>= 1) {
-            pq_in += __shfl_xor_sync(0xffffffffu, pq_in, o);
-            bq_in += __shfl_xor_sync(0xffffffffu, bq_in, o);
-            lq_in += __shfl_xor_sync(0xffffffffu, lq_in, o);
-        }
-    }
     for (int o = 16; o > 0; o >>= 1) {
         tested += __shfl_xor_sync(0xffffffffu, tested, o);
         passed += __shfl_xor_sync(0xffffffffu, passed, o);
         sbt += __shfl_xor_sync(0xffffffffu, sbt, o);
         lt += __shfl_xor_sync(0xffffffffu, lt, o);
         lp += __shfl_xor_sync(0xffffffffu, lp, o);
-    }
-    if (a.dbg && lane == 0) {
-        atomicAdd(a.dbg + 0, (unsigned long long)tested);
-        atomicAdd(a.dbg + 1, (unsigned long long)pq_in);
-        atomicAdd(a.dbg + 2, (unsigned long long)sbt);
-        atomicAdd(a.dbg + 3, (unsigned long long)bq_in);
-        atomicAdd(a.dbg + 4, (unsigned long long)lt);
-        atomicAdd(a.dbg + 5, (unsigned long long)lq_in);
     }
     if (a.tile_leaf && lane == 0 && lt) {
         atomicAdd(a.ctr + (int64_t)q * NCTR + 0, (unsigned long long)lt);
@@ -2854,37 +2684,16 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
     static const int tp_env = std::getenv("DETLSH_TILE_PAIRS") ? std::atoi(std::getenv("DETLSH_TILE_PAIRS")) : -1;
     const bool tp_want = tp_env == 1 || (tp_env < 0 && ix.K < 40 && (n >> ix.K) >= 64);
     const bool tile_pairs = tp_want && use_pairs && lp_fixed && RF_G == 16 && rf_dyn && !a.lb_order;
-    // read per call (experiments switch modes between queries of one index)
-    const int split_env = std::getenv("DETLSH_LP_SPLIT") ? std::atoi(std::getenv("DETLSH_LP_SPLIT")) : 0;
-    auto k_leaf_points_sel = tile_pairs ? (split_env == 7   ? k_leaf_points<16, 256, 32, 7>
-                                           : split_env == 6 ? k_leaf_points<16, 256, 32, 6>
-                                           : split_env == 3 ? k_leaf_points<16, 256, 32, 3>
-                                           : split_env == 2 ? k_leaf_points<16, 256, 32, 2>
-                                           : split_env == 1 ? k_leaf_points<16, 256, 32, 1>
-                                                            : k_leaf_points<16, 256, 32>)
-                             : lp_fixed ? (lp_g == 8           ? k_leaf_points<16, 256, 8>
-                                           : (split_env & 3) == 3 ? k_leaf_points<16, 256, 16, 3>
-                                           : (split_env & 3) == 1 ? k_leaf_points<16, 256, 16, 1>
-                                                                  : k_leaf_points<16, 256, 16>)
+    // box bounds two dims per min/max (box_bound16); DETLSH_BOX16=0 selects the byte-wise form (read
+    // per call: experiments switch it between queries of one index)
+    const bool box16 = !(std::getenv("DETLSH_BOX16") && std::atoi(std::getenv("DETLSH_BOX16")) == 0);
+    auto k_leaf_points_sel = tile_pairs ? (box16 ? k_leaf_points<16, 256, 32, 1> : k_leaf_points<16, 256, 32>)
+                             : lp_fixed ? (lp_g == 8 ? k_leaf_points<16, 256, 8>
+                                           : box16   ? k_leaf_points<16, 256, 16, 1>
+                                                     : k_leaf_points<16, 256, 16>)
                                         : k_leaf_points<0, 0, 16>;
     lpa.tile_leaf = tile_pairs ? ix.tile_leaf.as<uint32_t>() : nullptr;
     lpa.tile_packed = ix.tree_leaf_begin.back() < ((int64_t)1 << 27) ? 1 : 0;
-    static const bool lp_stats_env = std::getenv("DETLSH_LP_STATS") != nullptr;
-    Scratch s_lps(st, lp_stats_env ? sizeof(unsigned long long) * 6 : 0);
-    lpa.dbg = lp_stats_env ? s_lps.as<unsigned long long>() : nullptr;
-    if (lp_stats_env) DL_CUDA(cudaMemsetAsync(s_lps.p, 0, sizeof(unsigned long long) * 6, st));
-    struct LpStatsPrint {     // experiments: print the two-stage counters when the query call ends
-        unsigned long long* d;
-        cudaStream_t st;
-        ~LpStatsPrint() {
-            if (!d) return;
-            unsigned long long h[6];
-            if (cudaMemcpyAsync(h, d, sizeof(h), cudaMemcpyDeviceToHost, st) != cudaSuccess) return;
-            if (cudaStreamSynchronize(st) != cudaSuccess) return;
-            std::fprintf(stderr, "DETLSH_LP_STATS points %llu past-half %llu sub-boxes %llu past-half %llu leaves %llu past-half %llu\n",
-                         h[0], h[1], h[2], h[3], h[4], h[5]);
-        }
-    } lp_stats_print{lpa.dbg, st};
     ra.tile_packed = lpa.tile_packed;
     static const bool tp_hist_env = std::getenv("DETLSH_TP_HIST") != nullptr;
     Scratch s_tph(st, tp_hist_env ? sizeof(unsigned long long) * 17 : 0);
@@ -2912,9 +2721,6 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
     const size_t lp_dyn = lp_fixed ? 0 : lp_smem;
     if (use_pairs && !lp_fixed)
         ensure_dyn_smem_fn(k_leaf_points_sel, lp_smem);
-    if (tile_pairs)   // the two-stage queues take up to ~43 KB of static shared memory per block (5 per SM)
-        DL_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_leaf_points_sel),
-                                     cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared));
     ra.leaf_off = ix.leaf_off.as<uint32_t>();
     // leaf pruning uses the tight boxes (a valid, tighter bound for every member); RELAXED takes
     // whole leaves by the leaf's own (prefix) box, as the method defines it

@@ -13,8 +13,8 @@ namespace detlsh {
 namespace {
 
 constexpr int RS_THREADS = 256;
-constexpr int RS_IPT = 16;                          // items per thread
-constexpr int RS_TILE = RS_THREADS * RS_IPT;        // 4096 keys per tile
+constexpr int RS_IPT = 8;                           // items per thread (16: 104 registers, 2 blocks per SM)
+constexpr int RS_TILE = RS_THREADS * RS_IPT;        // 2048 keys per tile
 constexpr int RS_WARPS = RS_THREADS / 32;
 
 __global__ void __launch_bounds__(RS_THREADS) k_rs_hist(const uint32_t* __restrict__ keys, int64_t m,
@@ -85,13 +85,15 @@ __global__ void __launch_bounds__(256) k_rs_scan(uint32_t* __restrict__ hist, in
 }
 
 // Scatter of one 8-bit digit pass, stable.  Warp w of the block ranks the tile's keys
-// [512 w, 512 w + 512) on its own: 16 rounds of 32 consecutive keys, warp.match_any groups a
+// [256 w, 256 w + 256) on its own (all its loads issued first): 8 rounds of 32 consecutive keys, warp.match_any groups a
 // round's equal digits, the group's lowest lane reads and bumps the warp's private digit counter
 // (no block barrier per round).  One block barrier later every key knows its place in the tile
 // sorted by (digit, original position); the tile is staged in shared memory in that order and
 // written out so that runs of equal digits land on consecutive addresses (coalesced), at the
 // digit's global base (this tile's per-digit offset from k_rs_scan + the digits below).
-template <bool HAS_VALS>
+// IOTA: the values are the keys' positions in their segment (not read; the first pass of a sort
+// whose values start as 0..m-1 per segment).
+template <bool HAS_VALS, bool IOTA = false>
 __global__ void __launch_bounds__(RS_THREADS) k_rs_scatter(const uint32_t* __restrict__ kin,
                                                            const uint32_t* __restrict__ vin,
                                                            uint32_t* __restrict__ kout,
@@ -114,15 +116,20 @@ __global__ void __launch_bounds__(RS_THREADS) k_rs_scatter(const uint32_t* __res
     const int64_t base = (int64_t)tile * RS_TILE;
     for (int i = lane; i < 256; i += 32) s_wh[w][i] = 0;
     __syncwarp();
-    constexpr int R = RS_TILE / RS_THREADS;          // 16 rounds of 32 keys per warp
+    constexpr int R = RS_TILE / RS_THREADS;          // rounds of 32 keys per warp
     uint32_t key[R], val[R], loc[R];
     const uint32_t lt = lanemask_lt();
 #pragma unroll
     for (int j = 0; j < R; ++j) {
         const int64_t e = base + (int64_t)w * (32 * R) + 32 * j + lane;
         const bool ok = e < m;
-        key[j] = ok ? k[e] : 0u;
-        val[j] = (HAS_VALS && ok) ? v[e] : 0u;
+        key[j] = ok ? __ldg(k + e) : 0u;
+        val[j] = !HAS_VALS ? 0u : IOTA ? (uint32_t)e : ok ? __ldg(v + e) : 0u;
+    }
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+        const int64_t e = base + (int64_t)w * (32 * R) + 32 * j + lane;
+        const bool ok = e < m;
         const uint32_t dig = ok ? ((key[j] >> shift) & 255u) : 256u;
         const uint32_t peers = __match_any_sync(0xffffffffu, dig);
         const int leader = __ffs(peers) - 1;
@@ -234,7 +241,7 @@ __global__ void __launch_bounds__(SC_THREADS) k_scan_apply(const uint32_t* __res
 }  // namespace
 
 bool radix_sort_batched(uint32_t* k0, uint32_t* v0, uint32_t* k1, uint32_t* v1, int64_t m,
-                        int64_t nseg, int bits, cudaStream_t st) {
+                        int64_t nseg, int bits, cudaStream_t st, bool vals_iota) {
     if (m <= 0 || nseg <= 0 || bits <= 0) return false;
     const int tiles = (int)ceil_div(m, RS_TILE);
     const int64_t len = (int64_t)256 * tiles;
@@ -249,7 +256,10 @@ bool radix_sort_batched(uint32_t* k0, uint32_t* v0, uint32_t* k1, uint32_t* v1, 
         dim3 grid(tiles, (unsigned)nseg);
         DL_LAUNCH(k_rs_hist, grid, RS_THREADS, 0, st, ki, m, shift, tiles, hist.as<uint32_t>());
         DL_LAUNCH(k_rs_scan, dim3(32, (unsigned)nseg), 256, 0, st, hist.as<uint32_t>(), tiles, dtot);
-        if (v0) {
+        if (v0 && vals_iota && shift == 0) {
+            DL_LAUNCH(k_rs_scatter<true COMMA true>, grid, RS_THREADS, 0, st, ki, (const uint32_t*)nullptr, ko, vo, m,
+                      shift, tiles, hist.as<uint32_t>(), dtot);
+        } else if (v0) {
             DL_LAUNCH(k_rs_scatter<true>, grid, RS_THREADS, 0, st, ki, vi, ko, vo, m, shift, tiles,
                       hist.as<uint32_t>(), dtot);
         } else {

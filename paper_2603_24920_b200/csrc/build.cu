@@ -369,15 +369,26 @@ __device__ inline void push_node(Node* arr, uint32_t* cnt, uint32_t cap, const N
 
 // Where a node goes: a leaf (<= max_size points or no bits left), the block-local list (small
 // enough for k_local_finish to split it to the end in shared memory), or the next global level.
+// Local nodes in two size tiers sharing one array: <= local_max1 points from the front,
+// (local_max1, local_max] from the back (each tier's k_local_finish launch sizes its shared memory
+// for its own largest node; both tiers' nodes are disjoint, > max_size points: <= cap_local in all).
 struct Sinks {
     Node* active; uint32_t* n_active; uint32_t cap_active;
     Node* local; uint32_t* n_local; uint32_t cap_local; int local_max;
     Node* leaves; uint32_t* n_leaves; uint32_t cap_leaves;
+    uint32_t* n_local2; int local_max1;
 };
 __device__ inline void route_node(const Sinks& k, const Node& nd, int K, int nb, int max_size) {
-    if ((int64_t)nd.len <= max_size || !splittable(nd.bits, K, nb)) push_node(k.leaves, k.n_leaves, k.cap_leaves, nd);
-    else if ((int64_t)nd.len <= k.local_max) push_node(k.local, k.n_local, k.cap_local, nd);
-    else push_node(k.active, k.n_active, k.cap_active, nd);
+    if ((int64_t)nd.len <= max_size || !splittable(nd.bits, K, nb)) {
+        push_node(k.leaves, k.n_leaves, k.cap_leaves, nd);
+    } else if ((int64_t)nd.len <= k.local_max1) {
+        push_node(k.local, k.n_local, k.cap_local, nd);
+    } else if ((int64_t)nd.len <= k.local_max) {
+        const uint32_t i = atomicAdd(k.n_local2, 1u);
+        if (i < k.cap_local) k.local[k.cap_local - 1 - i] = nd;
+    } else {
+        push_node(k.active, k.n_active, k.cap_active, nd);
+    }
 }
 
 __global__ void k_init_nodes(const uint32_t* __restrict__ starts, const uint32_t* __restrict__ nseg_p,
@@ -600,16 +611,14 @@ __global__ void k_make_children(const Node* __restrict__ nodes, const uint32_t* 
 // node's sub-nodes until every piece is a leaf.  Codes are staged once (gathered from EP);
 // partitions move 16-bit positions only; perm is written back at the end.  One CTA per node
 // (grid-stride over the local list).
-constexpr int LF_MAXSEG = 64;       // live sub-nodes per level (each > max_size points: LM / (max_size+1))
-constexpr int LF_WSTACK = 8;        // warp-mode stack: pending 1-children, each > max_size points of one
-                                    // sub-node of <= ws points (ws <= LF_WSTACK * (max_size + 1))
+constexpr int LF_MAXSEG = 128;      // live sub-nodes per level (each > max_size points: LM / (max_size+1))
 
 template <int KM, int LF_THREADS>   // KM >= K: 16 or 32 (split-count registers)
 __global__ void __launch_bounds__(LF_THREADS, 1024 / LF_THREADS) k_local_finish(const Node* __restrict__ loc, const uint32_t* __restrict__ n_loc_p,
                                                              int LM, uint32_t* __restrict__ perm, const uint8_t* __restrict__ EP,
                                                              int64_t n, int LK, int K, int nb, int max_size,
                                                              Node* __restrict__ leaves, uint32_t* __restrict__ n_leaves,
-                                                             uint32_t cap_leaves, int ws) {
+                                                             uint32_t cap_leaves, int64_t rev_cap) {
     extern __shared__ __align__(16) unsigned char lf_smem[];
     const int CB = K <= 16 ? 16 : 32;                                     // code bytes per point
     uint8_t* s_code = lf_smem;                                            // [LM][CB], load order
@@ -621,15 +630,10 @@ __global__ void __launch_bounds__(LF_THREADS, 1024 / LF_THREADS) k_local_finish(
     __shared__ Node s_act[2][LF_MAXSEG];
     __shared__ int s_dim[LF_MAXSEG], s_shift[LF_MAXSEG];
     __shared__ uint32_t s_nact[2], s_wsum[LF_THREADS / 32];
-    // warp mode (ws > 0): sub-nodes of <= ws points leave the block-wide levels for a list that the
-    // warps then finish one sub-node each, depth first with a private stack and no block barriers
-    __shared__ Node s_wl[LF_MAXSEG];
-    __shared__ uint32_t s_nwl;
-    __shared__ Node s_wst[LF_THREADS / 32][LF_WSTACK];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = LF_THREADS / 32;
     const uint32_t n_loc = *n_loc_p;
     for (uint32_t a = blockIdx.x; a < n_loc; a += gridDim.x) {
-        const Node nd = loc[a];
+        const Node nd = loc[rev_cap ? rev_cap - 1 - (int64_t)a : (int64_t)a];   // rev_cap: the back tier
         const int t = (int)(nd.start / n);
         const int m = (int)nd.len;
         const uint32_t base = nd.start;
@@ -644,17 +648,7 @@ __global__ void __launch_bounds__(LF_THREADS, 1024 / LF_THREADS) k_local_finish(
                 for (int j = 0; j < K; ++j) s_code[i * CB + j] = c[j];
             }
         }
-        if (tid == 0) {
-            s_nwl = 0;
-            if (ws > 0 && m <= ws) {   // whole node in warp mode
-                s_wl[0] = nd;
-                s_nwl = 1;
-                s_nact[0] = 0;
-            } else {
-                s_act[0][0] = nd;
-                s_nact[0] = 1;
-            }
-        }
+        if (tid == 0) { s_act[0][0] = nd; s_nact[0] = 1; }
         __syncthreads();
         uint16_t* ix = s_ixa;
         uint16_t* ix2 = s_ixb;
@@ -755,8 +749,6 @@ __global__ void __launch_bounds__(LF_THREADS, 1024 / LF_THREADS) k_local_finish(
                     if (ch.len == 0) continue;
                     if ((int64_t)ch.len <= max_size || !splittable(ch.bits, K, nb)) {
                         push_node(leaves, n_leaves, cap_leaves, ch);
-                    } else if ((int)ch.len <= ws) {
-                        s_wl[atomicAdd(&s_nwl, 1u)] = ch;
                     } else {
                         const uint32_t k = atomicAdd(&s_nact[cur ^ 1], 1u);
                         s_act[cur ^ 1][k] = ch;
@@ -766,102 +758,6 @@ __global__ void __launch_bounds__(LF_THREADS, 1024 / LF_THREADS) k_local_finish(
             __syncthreads();
             uint16_t* tmp = ix; ix = ix2; ix2 = tmp;
         }
-        // warp mode: the same SplitNode rule and stable partition per sub-node, by one warp
-        // (ballots over 32 positions at a time).  pad0 = where the sub-node's order lives (0: ix,
-        // 1: ix2); a finished piece in ix2 is copied back so the final write reads ix only.
-        const uint32_t nwl = s_nwl;
-        const uint32_t lt = lanemask_lt();
-        for (uint32_t wi = warp; wi < nwl; wi += nwarps) {
-            Node* stk = s_wst[warp];
-            int sp = 0;
-            Node cn = s_wl[wi];
-            cn.pad0 = 0;
-            for (;;) {
-                const int st = (int)(cn.start - base), len = (int)cn.len;
-                const uint16_t* src = cn.pad0 ? ix2 : ix;
-                uint16_t* dst = cn.pad0 ? ix : ix2;
-                // SplitNode dimension over the first max_size points (ties to the lowest dim)
-                int best = -1, best_imb = 0x7fffffff;
-                {
-                    int ones[KM];
-#pragma unroll
-                    for (int j = 0; j < KM; ++j) ones[j] = 0;
-                    for (int e = lane; e < max_size; e += 32) {
-                        const uint8_t* c = s_code + (int)src[st + e] * CB;
-#pragma unroll
-                        for (int j = 0; j < KM; ++j) {
-                            if (j < K) {
-                                const int b = nib(cn.bits, j);
-                                if (b < nb) ones[j] += (c[j] >> (nb - 1 - b)) & 1;
-                            }
-                        }
-                    }
-#pragma unroll
-                    for (int j = 0; j < KM; ++j) {
-                        const int v = __reduce_add_sync(0xffffffffu, ones[j]);
-                        if (j < K && nib(cn.bits, j) < nb) {
-                            const int imb = abs(max_size - 2 * v);
-                            if (imb < best_imb) { best_imb = imb; best = j; }
-                        }
-                    }
-                }
-                const int sh = nb - 1 - nib(cn.bits, best);
-                // zeros first, then ones, each in position order
-                uint32_t Z = 0;
-                for (int e0 = 0; e0 < len; e0 += 32) {
-                    const int e = e0 + lane;
-                    const bool z = e < len && !((s_code[(int)src[st + e] * CB + best] >> sh) & 1);
-                    Z += __popc(__ballot_sync(0xffffffffu, z));
-                }
-                uint32_t zc = 0, oc = 0;
-                for (int e0 = 0; e0 < len; e0 += 32) {
-                    const int e = e0 + lane;
-                    const bool in = e < len;
-                    const uint16_t v = in ? src[st + e] : (uint16_t)0;
-                    const bool z = in && !((s_code[(int)v * CB + best] >> sh) & 1);
-                    const uint32_t bz = __ballot_sync(0xffffffffu, z), bo = __ballot_sync(0xffffffffu, in && !z);
-                    if (z) dst[st + zc + __popc(bz & lt)] = v;
-                    else if (in) dst[st + (int)Z + oc + __popc(bo & lt)] = v;
-                    zc += __popc(bz);
-                    oc += __popc(bo);
-                }
-                __syncwarp();
-                // children: leaves out (copied back into ix when their order is in ix2), the rest
-                // depth first (the 1-child on the stack)
-                Node nxt;
-                bool have = false;
-                for (int b = 1; b >= 0; --b) {
-                    Node ch = cn;
-                    nib_inc(ch.bits, best);
-                    ch.start = b ? cn.start + Z : cn.start;
-                    ch.len = b ? cn.len - Z : Z;
-                    ch.pad0 = cn.pad0 ^ 1u;
-                    if (ch.len == 0) continue;
-                    if ((int64_t)ch.len <= max_size || !splittable(ch.bits, K, nb)) {
-                        if (lane == 0) push_node(leaves, n_leaves, cap_leaves, ch);
-                        if (ch.pad0) {
-                            const int cs = (int)(ch.start - base);
-                            for (int e = lane; e < (int)ch.len; e += 32) ix[cs + e] = ix2[cs + e];
-                        }
-                    } else if (b == 1) {
-                        if (lane == 0) stk[sp] = ch;
-                        ++sp;
-                    } else {
-                        nxt = ch;
-                        have = true;
-                    }
-                }
-                __syncwarp();
-                if (have) {
-                    cn = nxt;
-                } else if (sp > 0) {
-                    cn = stk[--sp];
-                } else {
-                    break;
-                }
-            }
-        }
-        __syncthreads();
         for (int i = tid; i < m; i += LF_THREADS) perm[base + i] = s_id[ix[i]];
         __syncthreads();
     }
@@ -1487,7 +1383,7 @@ static bool build_trees_try(Index& ix, const uint8_t* d_EP, int64_t leaf_factor,
     Scratch s_seg(st, sizeof(uint32_t) * (size_t)(2 * total + 8));
     uint32_t* flags = s_seg.as<uint32_t>();
     uint32_t* idx = flags + total;
-    uint32_t* counters = idx + total;  // [0]=nseg [1]=n_active [2]=n_next [3]=n_leaves [4]=total_chunks [5]=n_local
+    uint32_t* counters = idx + total;  // [0]=nseg [1]=n_active [2]=n_next [3]=n_leaves [4]=total_chunks [5]=n_local [6]=n_local2
     DL_CUDA(cudaMemsetAsync(counters, 0, 8 * sizeof(uint32_t), st));
     DL_LAUNCH(k_seg_flags, grid_for(total, 256), 256, 0, st, skeys, n, total, flags);
     exclusive_scan_u32(flags, idx, total, counters + 0, st);
@@ -1512,13 +1408,18 @@ static bool build_trees_try(Index& ix, const uint8_t* d_EP, int64_t leaf_factor,
     uint32_t* n_loc = counters + 5;
     // nodes of <= LM points finish in shared memory (k_local_finish); LM keeps the live
     // sub-nodes of one level within LF_MAXSEG and the positions within 16 bits
-    const int lm_env = std::getenv("DETLSH_LOCAL_MAX") ? std::atoi(std::getenv("DETLSH_LOCAL_MAX")) : 1536;   // read per build
+    const int lm_env = std::getenv("DETLSH_LOCAL_MAX") ? std::atoi(std::getenv("DETLSH_LOCAL_MAX")) : 3072;   // read per build
     // (scan flags of one thread fit 32 bits: LM <= 32 * 256; staged codes + indices fit shared memory)
     const int64_t lm_smem = (int64_t)(200 * 1024) / ((K <= 16 ? 16 : 32) + 11);
     const int LM = (int)std::min<int64_t>(std::min<int64_t>(std::min<int64_t>(lm_env, 8192), lm_smem),
                                           (int64_t)(LF_MAXSEG - 1) * (max_size + 1));
+    // two local tiers: nodes of <= LM1 points in CTAs sized for LM1 (4 per SM), larger ones up to LM
+    // in CTAs of 512 threads sized for LM (measured at configs[4]: one LM = 1536 tier 170.1 ms of
+    // build, LM = 3072 in one tier 162.7 ms but slower at configs[1] / configs[3])
+    const int LM1 = std::min(LM, 1536);
+    uint32_t* n_loc2 = counters + 6;
     Sinks sk{act, n_act, (uint32_t)cap_active, loc, n_loc, (uint32_t)cap_active, LM > max_size ? LM : 0,
-             leaves, n_leaves, (uint32_t)cap_leaves};
+             leaves, n_leaves, (uint32_t)cap_leaves, n_loc2, LM1};
     DL_LAUNCH(k_init_nodes, grid_for(nseg_ub, 256), 256, 0, st, s_starts.as<uint32_t>(), counters + 0, total, K, nb,
               max_size, sk);
     s_starts.free_();
@@ -1561,22 +1462,24 @@ static bool build_trees_try(Index& ix, const uint8_t* d_EP, int64_t leaf_factor,
         DL_REQUIRE(na <= cap_active, "tree build: active-node capacity exceeded");
     }
     if (sk.local_max > 0) {
-        const size_t lsm = local_finish_smem(LM, K);
-        const int lf_nt = std::getenv("DETLSH_LF_THREADS") ? std::atoi(std::getenv("DETLSH_LF_THREADS")) : 256;
-        const int LF_THREADS = lf_nt == 256 ? 256 : 512;
-        auto k_local_finish_sel = K <= 16 ? (LF_THREADS == 256 ? k_local_finish<16, 256> : k_local_finish<16, 512>)
-                                          : (LF_THREADS == 256 ? k_local_finish<32, 256> : k_local_finish<32, 512>);
-        ensure_dyn_smem_fn(k_local_finish_sel, lsm);
-        int dev = 0, nsm = 148, per_sm = 1;
+        int dev = 0, nsm = 148;
         DL_CUDA(cudaGetDevice(&dev));
         DL_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-        DL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_local_finish_sel, LF_THREADS, lsm));
-        // warp mode below ws points (DETLSH_LF_WS, read per build; 0 = block-wide levels to the end);
-        // the warp stack bounds it by LF_WSTACK * (max_size + 1)
-        const int ws_env = std::getenv("DETLSH_LF_WS") ? std::atoi(std::getenv("DETLSH_LF_WS")) : 512;
-        const int ws = std::max(0, std::min(ws_env, LF_WSTACK * (max_size + 1)));
-        DL_LAUNCH(k_local_finish_sel, nsm * std::max(1, per_sm), LF_THREADS, lsm, st, loc, n_loc, LM, perm, d_EP, n, LK, K,
-                  nb, max_size, leaves, n_leaves, (uint32_t)cap_leaves, ws);
+        const int lf_nt = std::getenv("DETLSH_LF_THREADS") ? std::atoi(std::getenv("DETLSH_LF_THREADS")) : 0;
+        for (int tier = 0; tier < 2; ++tier) {
+            const int lm_t = tier == 0 ? LM1 : LM;
+            if (tier == 1 && LM <= LM1) break;
+            const size_t lsm = local_finish_smem(lm_t, K);
+            const int LF_THREADS = lf_nt == 256 ? 256 : lf_nt == 512 ? 512 : (tier == 0 ? 256 : 512);
+            auto k_local_finish_sel = K <= 16 ? (LF_THREADS == 256 ? k_local_finish<16, 256> : k_local_finish<16, 512>)
+                                              : (LF_THREADS == 256 ? k_local_finish<32, 256> : k_local_finish<32, 512>);
+            ensure_dyn_smem_fn(k_local_finish_sel, lsm);
+            int per_sm = 1;
+            DL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_local_finish_sel, LF_THREADS, lsm));
+            DL_LAUNCH(k_local_finish_sel, nsm * std::max(1, per_sm), LF_THREADS, lsm, st, loc, tier == 0 ? n_loc : n_loc2,
+                      lm_t, perm, d_EP, n, LK, K, nb, max_size, leaves, n_leaves, (uint32_t)cap_leaves,
+                      tier == 0 ? (int64_t)0 : cap_active);
+        }
     }
     s_tmp.free_();
     s_zc.free_();

@@ -1068,7 +1068,7 @@ __global__ void __launch_bounds__(LP_THREADS, LPG == 32 ? 5 : 6) k_leaf_points(L
     __shared__ int s_qx[32];                          // the query's region codes in tree t
     if (threadIdx.x == 0) { s_tested = 0; s_passed = 0; s_sbt = 0; }
     if (threadIdx.x < K) s_qx[threadIdx.x] = a.sx[((int64_t)q * a.L + a.t) * K + threadIdx.x];
-    constexpr bool B16 = BX && KT == 16 && NRT == 256;
+    constexpr bool B16 = (BX & 1) && KT == 16 && NRT == 256;
     __shared__ uint32_t s_qeo[8];                     // B16: the query's codes spread for box_bound16
     if (B16 && threadIdx.x >= 32 && threadIdx.x < 40) {
         const int i = (threadIdx.x - 32) & 3, od = (threadIdx.x - 32) >> 2;

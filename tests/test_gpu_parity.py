@@ -560,19 +560,17 @@ def test_config5_vs_oracle_golden():
             assert np.all(np.diff(dg[q][ok]) >= 0)
 
 
-@pytest.mark.parametrize("local_max,morton,lf_ws", [("0", "-1", "512"), ("300", "-1", "512"), ("1536", "-1", "512"),
-                                                    ("8192", "-1", "512"), ("1536", "1", "512"), ("300", "1", "512"),
-                                                    ("1536", "-1", "0"), ("8192", "-1", "0"), ("300", "-1", "60"),
-                                                    ("3072", "1", "1032")])
-def test_trees_split_paths(local_max, morton, lf_ws):
+@pytest.mark.parametrize("local_max,morton", [("0", "-1"), ("300", "-1"), ("1536", "-1"), ("3072", "-1"),
+                                              ("8192", "-1"), ("1536", "1"), ("300", "1")])
+def test_trees_split_paths(local_max, morton):
     """B6 through the global level loop only (0) and through mixes of global levels and the
-    shared-memory finish (k_local_finish, nodes of <= local_max points; sub-nodes of <= lf_ws
-    points finished warp by warp, 0 = block-wide levels to the end), on codes with one ~18K-point
-    first-layer node and many small ones: every variant gives the oracle's trees bit for bit."""
+    shared-memory finish (k_local_finish, nodes of <= local_max points), on codes with one
+    ~18K-point first-layer node and many small ones: every variant gives the oracle's trees
+    bit for bit."""
     import os
     import subprocess
     import sys
-    env = dict(os.environ, DETLSH_LOCAL_MAX=local_max, DETLSH_LEAF_MORTON=morton, DETLSH_LF_WS=lf_ws)
+    env = dict(os.environ, DETLSH_LOCAL_MAX=local_max, DETLSH_LEAF_MORTON=morton)
     here = os.path.dirname(os.path.abspath(__file__))
     r = subprocess.run([sys.executable, os.path.join(here, "_tree_split_paths.py")], env=env,
                        capture_output=True, text=True, timeout=600)

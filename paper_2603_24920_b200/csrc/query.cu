@@ -3010,7 +3010,16 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
                     lpa.t = t;
                     lpa.ctr = s_ctr.as<unsigned long long>();
                     lpa.q12 = s_q12.as<uint16_t>();
-                    static const int lp_y = std::getenv("DETLSH_LP_Y") ? std::atoi(std::getenv("DETLSH_LP_Y")) : 16;
+                    // blocks per query (grid y).  Blocks start in x-major order, so a query holds ~1-2
+                    // blocks at first and gains more only as other blocks finish; a query with a
+                    // long list needs many blocks available late in the launch (blocks that find the
+                    // list taken exit before loading anything).  Measured (per 2,000 queries at
+                    // configs[4], ~460 per batch): y = 16 88.5 ms, 32 72.8, 64 66.2, 128 64.0, 256
+                    // 63.5; configs[3] (~3,400 per batch) best at 32 (47.3 ms vs 48.1 at 16, 49.0 at
+                    // 128); configs[1] (pair kernel of the SIMD path) 32.  Tile mode: ~100K blocks
+                    // per launch, y in [16, 256]; DETLSH_LP_Y overrides (read per call).
+                    int lp_y = tile_pairs ? (int)std::min<int64_t>(256, std::max<int64_t>(16, 100000 / std::max(1, nf))) : 32;
+                    if (std::getenv("DETLSH_LP_Y")) lp_y = std::max(1, std::atoi(std::getenv("DETLSH_LP_Y")));
                     DL_LAUNCH(k_leaf_points_sel, dim3((unsigned)nf, (unsigned)lp_y), LP_THREADS, lp_dyn, st, lpa);
                 }
                 }   // chunks

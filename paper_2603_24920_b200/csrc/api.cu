@@ -15,6 +15,11 @@
 namespace detlsh {
 
 std::atomic<int64_t> g_launches{0};
+// PDL on every launch unless DETLSH_PDL=0 (read per call: experiments switch it between calls)
+bool pdl_enabled() {
+    const char* e = std::getenv("DETLSH_PDL");
+    return !(e && std::atoi(e) == 0);
+}
 static thread_local std::string g_err;
 
 void project_rows_simt(const Index& ix, const float* d_X, int64_t ld, int64_t m, float* d_P, int* d_nonfinite,

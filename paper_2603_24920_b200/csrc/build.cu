@@ -24,6 +24,7 @@ namespace {
 
 // ------------------------------------------------------------------ B0
 __global__ void k_hash_family(uint64_t seed, int LK, int d, int ld, float* __restrict__ A) {
+    pdl_wait();
     const int64_t total = (int64_t)LK * ld;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
          i += (int64_t)gridDim.x * blockDim.x) {
@@ -49,12 +50,14 @@ struct SelState {
 };
 
 __global__ void k_sel_init(SelState* s, int64_t n_s) {
+    pdl_wait();
     s->prefix = 0; s->mask = 0; s->remaining = (unsigned long long)n_s; s->eq_count = 0;
 }
 
 __global__ void __launch_bounds__(256) k_sel_hist(uint64_t salt, int64_t n_global, int shift,
                                                   const SelState* __restrict__ st,
                                                   uint32_t* __restrict__ hist) {
+    pdl_wait();
     __shared__ uint32_t h[256];
     h[threadIdx.x] = 0;
     __syncthreads();
@@ -69,6 +72,7 @@ __global__ void __launch_bounds__(256) k_sel_hist(uint64_t salt, int64_t n_globa
 }
 
 __global__ void __launch_bounds__(256) k_sel_pick(int shift, SelState* st, uint32_t* hist) {
+    pdl_wait();
     __shared__ unsigned long long s_incl[256];
     const unsigned long long v = hist[threadIdx.x];
     s_incl[threadIdx.x] = v;
@@ -95,6 +99,7 @@ __global__ void __launch_bounds__(256) k_sel_collect(uint64_t salt, int64_t id_l
                                                      const SelState* __restrict__ st,
                                                      uint32_t* __restrict__ out,
                                                      unsigned long long* __restrict__ counter) {
+    pdl_wait();
     const uint64_t T = st->prefix;
     const bool take_eq = st->eq_count == st->remaining;         // all ties needed (the usual case)
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_range;
@@ -109,6 +114,7 @@ __global__ void __launch_bounds__(256) k_sel_collect(uint64_t salt, int64_t id_l
 __global__ void k_sel_ties(uint64_t salt, int64_t id_lo, int64_t n_range, int64_t n_global,
                            const SelState* __restrict__ st, uint32_t* __restrict__ out,
                            unsigned long long* __restrict__ counter) {
+    pdl_wait();
     if (st->eq_count == st->remaining) return;
     const uint64_t T = st->prefix;
     unsigned long long need = st->remaining;
@@ -129,6 +135,7 @@ struct Sel16 {
 };
 
 __global__ void __launch_bounds__(256) k_sel16_hist(uint64_t salt, int64_t n_global, uint32_t* __restrict__ hist) {
+    pdl_wait();
     for (int64_t id = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; id < n_global;
          id += (int64_t)gridDim.x * blockDim.x)
         atomicAdd(&hist[keyed(salt, (uint64_t)id) >> 48], 1u);
@@ -136,6 +143,7 @@ __global__ void __launch_bounds__(256) k_sel16_hist(uint64_t salt, int64_t n_glo
 
 // one CTA of 1024 threads, 64 bins each
 __global__ void __launch_bounds__(1024) k_sel16_pick(const uint32_t* __restrict__ hist, int64_t n_s, Sel16* __restrict__ st) {
+    pdl_wait();
     __shared__ uint32_t s_warp[32];
     __shared__ unsigned long long s_tot[32];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -181,6 +189,7 @@ __global__ void __launch_bounds__(256) k_sel16_collect(uint64_t salt, int64_t id
                                                        unsigned long long* __restrict__ counter,
                                                        unsigned long long* __restrict__ ckey, uint32_t* __restrict__ cid,
                                                        uint32_t ccap) {
+    pdl_wait();
     const uint32_t b = st->bin;
     for (int64_t id = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; id < n_global;
          id += (int64_t)gridDim.x * blockDim.x) {
@@ -200,6 +209,7 @@ __global__ void __launch_bounds__(1024) k_sel16_finish(int64_t id_lo, int64_t n_
                                                        const unsigned long long* __restrict__ ckey,
                                                        const uint32_t* __restrict__ cid, uint32_t ccap,
                                                        uint32_t* __restrict__ out, unsigned long long* __restrict__ counter) {
+    pdl_wait();
     extern __shared__ unsigned long long s_key[];
     uint32_t* s_id = reinterpret_cast<uint32_t*>(s_key + ccap);
     const uint32_t nc = st->ncand;
@@ -222,6 +232,7 @@ __global__ void __launch_bounds__(1024) k_sel16_finish(int64_t id_lo, int64_t n_
 
 __global__ void k_gather_rows(const float* __restrict__ X, int64_t ld, const uint32_t* __restrict__ ids,
                               int64_t m, float* __restrict__ out) {
+    pdl_wait();
     const int lane = threadIdx.x & 31;
     const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -234,6 +245,7 @@ __global__ void k_gather_rows(const float* __restrict__ X, int64_t ld, const uin
 
 // ------------------------------------------------------------------ B3
 __global__ void k_transpose_keys(const float* __restrict__ Ps, int64_t m, int LK, uint32_t* __restrict__ keys) {
+    pdl_wait();
     const int64_t total = m * LK;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
          i += (int64_t)gridDim.x * blockDim.x) {
@@ -245,6 +257,7 @@ __global__ void k_transpose_keys(const float* __restrict__ Ps, int64_t m, int LK
 
 // B(1) = C^(1), B(z) = C^(floor(m/N_r)(z-1)) (1-based, z=2..N_r), B(N_r+1) = C^(m)  (AMB-5)
 __global__ void k_bp_gather(const uint32_t* __restrict__ sorted, int64_t m, int LK, int N_r, float* __restrict__ B) {
+    pdl_wait();
     const int64_t total = (int64_t)LK * (N_r + 1);
     const int64_t stride = m / N_r > 0 ? m / N_r : 1;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
@@ -263,6 +276,7 @@ __global__ void k_bp_gather(const uint32_t* __restrict__ sorted, int64_t m, int 
 // with a +inf sentinel (AMB-6: ties go to the lower region; AMB-7: clamp to 0 / N_r-1).
 __global__ void __launch_bounds__(256) k_encode(const float* __restrict__ P, int64_t m, int LK, int N_r,
                                                 const float* __restrict__ B, uint8_t* __restrict__ EP) {
+    pdl_wait();
     extern __shared__ float tab[];  // [LK][N_r]
     for (int i = threadIdx.x; i < LK * N_r; i += blockDim.x) {
         const int r = i / N_r, t = i % N_r;
@@ -325,6 +339,7 @@ __device__ inline bool splittable(const uint4& b, int K, int nb) {
 // First-layer key of point id in tree t: MSB of each of the K symbols, dim 0 most significant (AMB-11).
 __global__ void k_first_key(const uint8_t* __restrict__ EP, int64_t n, int L, int K, int nb,
                             uint32_t* __restrict__ keys, uint32_t* __restrict__ vals) {
+    pdl_wait();
     const int LK = L * K;
     const int64_t total = n * L;
     for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total;
@@ -348,6 +363,7 @@ __global__ void k_first_key(const uint8_t* __restrict__ EP, int64_t n, int L, in
 
 
 __global__ void k_seg_flags(const uint32_t* __restrict__ keys, int64_t n, int64_t total, uint32_t* __restrict__ flags) {
+    pdl_wait();
     for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total;
          g += (int64_t)gridDim.x * blockDim.x)
         flags[g] = (g % n == 0 || keys[g] != keys[g - 1]) ? 1u : 0u;
@@ -355,6 +371,7 @@ __global__ void k_seg_flags(const uint32_t* __restrict__ keys, int64_t n, int64_
 
 __global__ void k_seg_write(const uint32_t* __restrict__ flags, const uint32_t* __restrict__ idx, int64_t total,
                             uint32_t* __restrict__ starts) {
+    pdl_wait();
     for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total;
          g += (int64_t)gridDim.x * blockDim.x)
         if (flags[g]) starts[idx[g]] = (uint32_t)g;
@@ -393,6 +410,7 @@ __device__ inline void route_node(const Sinks& k, const Node& nd, int K, int nb,
 
 __global__ void k_init_nodes(const uint32_t* __restrict__ starts, const uint32_t* __restrict__ nseg_p,
                              int64_t total, int K, int nb, int max_size, Sinks sk) {
+    pdl_wait();
     const uint32_t nseg = *nseg_p;
     for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < nseg;
          s += (int64_t)gridDim.x * blockDim.x) {
@@ -417,6 +435,7 @@ __global__ void k_choose_split(const Node* __restrict__ nodes, const uint32_t* _
                                const uint32_t* __restrict__ perm, const uint8_t* __restrict__ EP,
                                int64_t n, int LK, int K, int nb, int max_size, int chunk,
                                int* __restrict__ split, uint32_t* __restrict__ nch) {
+    pdl_wait();
     const uint32_t n_nodes = *n_nodes_p;
     const int lane = threadIdx.x & 31;
     const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -477,6 +496,7 @@ __global__ void __launch_bounds__(PART_THREADS) k_part_count(const Node* __restr
                                                              const uint32_t* __restrict__ total_ch_p,
                                                              const uint32_t* __restrict__ perm, const uint8_t* __restrict__ EP,
                                                              int64_t n, int LK, int K, int nb, uint32_t* __restrict__ zc) {
+    pdl_wait();
     __shared__ uint32_t s_cnt;
     const uint32_t c = blockIdx.x;
     if (c >= *total_ch_p) return;
@@ -502,6 +522,7 @@ __global__ void __launch_bounds__(PART_THREADS) k_part_count(const Node* __restr
 __global__ void k_part_offsets(const uint32_t* __restrict__ choff, const uint32_t* __restrict__ nch,
                                const uint32_t* __restrict__ n_nodes_p, uint32_t* __restrict__ zc,
                                uint32_t* __restrict__ zeros) {
+    pdl_wait();
     const uint32_t n_nodes = *n_nodes_p;
     for (int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a < n_nodes;
          a += (int64_t)gridDim.x * blockDim.x) {
@@ -521,6 +542,7 @@ __global__ void __launch_bounds__(PART_THREADS) k_part_scatter(const Node* __res
                                                                const uint32_t* __restrict__ zoff, const uint32_t* __restrict__ zeros,
                                                                const uint32_t* __restrict__ perm, const uint8_t* __restrict__ EP,
                                                                int64_t n, int LK, int K, int nb, uint32_t* __restrict__ perm_out) {
+    pdl_wait();
     __shared__ uint32_t s_warp[PART_THREADS / 32];
     const uint32_t c = blockIdx.x;
     if (c >= *total_ch_p) return;
@@ -571,6 +593,7 @@ __global__ void __launch_bounds__(PART_THREADS) k_part_copy(const Node* __restri
                                                             const uint32_t* __restrict__ n_nodes_p,
                                                             const uint32_t* __restrict__ total_ch_p,
                                                             const uint32_t* __restrict__ src, uint32_t* __restrict__ dst) {
+    pdl_wait();
     const uint32_t c = blockIdx.x;
     if (c >= *total_ch_p) return;
     const int64_t a = chunk_owner(choff, *n_nodes_p, c);
@@ -585,6 +608,7 @@ __global__ void __launch_bounds__(PART_THREADS) k_part_copy(const Node* __restri
 __global__ void k_make_children(const Node* __restrict__ nodes, const uint32_t* __restrict__ n_nodes_p,
                                 const int* __restrict__ split, const uint32_t* __restrict__ zeros,
                                 int K, int nb, int max_size, Sinks sk) {
+    pdl_wait();
     const uint32_t n_nodes = *n_nodes_p;
     for (int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a < n_nodes;
          a += (int64_t)gridDim.x * blockDim.x) {
@@ -611,7 +635,7 @@ __global__ void k_make_children(const Node* __restrict__ nodes, const uint32_t* 
 // node's sub-nodes until every piece is a leaf.  Codes are staged once (gathered from EP);
 // partitions move 16-bit positions only; perm is written back at the end.  One CTA per node
 // (grid-stride over the local list).
-constexpr int LF_MAXSEG = 128;      // live sub-nodes per level (each > max_size points: LM / (max_size+1))
+constexpr int LF_MAXSEG = 64;       // live sub-nodes per level (each > max_size points: LM / (max_size+1))
 
 template <int KM, int LF_THREADS>   // KM >= K: 16 or 32 (split-count registers)
 __global__ void __launch_bounds__(LF_THREADS, 1024 / LF_THREADS) k_local_finish(const Node* __restrict__ loc, const uint32_t* __restrict__ n_loc_p,
@@ -619,6 +643,7 @@ __global__ void __launch_bounds__(LF_THREADS, 1024 / LF_THREADS) k_local_finish(
                                                              int64_t n, int LK, int K, int nb, int max_size,
                                                              Node* __restrict__ leaves, uint32_t* __restrict__ n_leaves,
                                                              uint32_t cap_leaves, int64_t rev_cap) {
+    pdl_wait();
     extern __shared__ __align__(16) unsigned char lf_smem[];
     const int CB = K <= 16 ? 16 : 32;                                     // code bytes per point
     uint8_t* s_code = lf_smem;                                            // [LM][CB], load order
@@ -629,6 +654,7 @@ __global__ void __launch_bounds__(LF_THREADS, 1024 / LF_THREADS) k_local_finish(
     uint8_t* s_seg = reinterpret_cast<uint8_t*>(s_pz + LM + 8);           // [LM] live sub-node of each position
     __shared__ Node s_act[2][LF_MAXSEG];
     __shared__ int s_dim[LF_MAXSEG], s_shift[LF_MAXSEG];
+    __shared__ uint32_t s_ones[LF_MAXSEG * KM];                          // per live sub-node: ones per dim
     __shared__ uint32_t s_nact[2], s_wsum[LF_THREADS / 32];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = LF_THREADS / 32;
     const uint32_t n_loc = *n_loc_p;
@@ -649,6 +675,7 @@ __global__ void __launch_bounds__(LF_THREADS, 1024 / LF_THREADS) k_local_finish(
             }
         }
         if (tid == 0) { s_act[0][0] = nd; s_nact[0] = 1; }
+        for (int i = tid; i < KM; i += LF_THREADS) s_ones[i] = 0;
         __syncthreads();
         uint16_t* ix = s_ixa;
         uint16_t* ix2 = s_ixb;
@@ -656,38 +683,44 @@ __global__ void __launch_bounds__(LF_THREADS, 1024 / LF_THREADS) k_local_finish(
         for (int cur = 0;; cur ^= 1) {
             const int nact = (int)s_nact[cur];
             if (nact == 0) break;
-            // SplitNode dimension of each live sub-node (warp per sub-node), as k_choose_split
-            for (int sg = warp; sg < nact; sg += nwarps) {
-                const Node sn = s_act[cur][sg];
-                const int st = (int)(sn.start - base);
-                int ones[KM];
-#pragma unroll
-                for (int j = 0; j < KM; ++j) ones[j] = 0;
-                for (int e = lane; e < max_size; e += 32) {
-                    const uint8_t* c = s_code + (int)ix[st + e] * CB;
+            // SplitNode dimension of each live sub-node (AMB-9), block-wide: warp items are
+            // (sub-node, 32 of its first max_size points); per dim a ballot counts the item's ones and
+            // lane j adds dim j's count to the sub-node's tally (s_ones, zeroed a phase earlier); then
+            // a thread per sub-node takes the dim with bits left whose next bit most evenly divides
+            // those points, ties to the lowest dim -- as k_choose_split.  (A warp per sub-node left
+            // the other warps at the next barrier: 34 % of the stall samples, ncu.)
+            {
+                const int CH = (max_size + 31) / 32;
+                for (int wi = warp; wi < nact * CH; wi += nwarps) {
+                    const int sg = wi / CH, e = (wi - sg * CH) * 32 + lane;
+                    const Node sn = s_act[cur][sg];
+                    const int st = (int)(sn.start - base);
+                    const bool ok = e < max_size;
+                    const uint8_t* c = s_code + (int)ix[st + (ok ? e : 0)] * CB;
+                    uint32_t my = 0;
 #pragma unroll
                     for (int j = 0; j < KM; ++j) {
                         if (j < K) {
                             const int b = nib(sn.bits, j);
-                            if (b < nb) ones[j] += (c[j] >> (nb - 1 - b)) & 1;
+                            const bool bit = ok && b < nb && ((c[j] >> (nb - 1 - b)) & 1);
+                            const uint32_t cnt = __popc(__ballot_sync(0xffffffffu, bit));
+                            if (lane == j) my = cnt;
                         }
                     }
+                    if (lane < K && my) atomicAdd(&s_ones[sg * KM + lane], my);
                 }
+            }
+            __syncthreads();
+            for (int sg = tid; sg < nact; sg += LF_THREADS) {   // live sub-nodes are splittable: best >= 0
+                const Node sn = s_act[cur][sg];
                 int best = -1, best_imb = 0x7fffffff;
-#pragma unroll
-                for (int j = 0; j < KM; ++j) {
-                    int v = ones[j];
-#pragma unroll
-                    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-                    if (j < K && nib(sn.bits, j) < nb) {
-                        const int imb = abs(max_size - 2 * v);
+                for (int j = 0; j < K; ++j)
+                    if (nib(sn.bits, j) < nb) {
+                        const int imb = abs(max_size - 2 * (int)s_ones[sg * KM + j]);
                         if (imb < best_imb) { best_imb = imb; best = j; }
                     }
-                }
-                if (lane == 0) {   // live sub-nodes are splittable, so best >= 0
-                    s_dim[sg] = best;
-                    s_shift[sg] = nb - 1 - nib(sn.bits, best);
-                }
+                s_dim[sg] = best;
+                s_shift[sg] = nb - 1 - nib(sn.bits, best);
             }
             for (int i = tid; i < m; i += LF_THREADS) s_seg[i] = 0xFF;
             if (tid == 0) s_nact[cur ^ 1] = 0;
@@ -696,6 +729,8 @@ __global__ void __launch_bounds__(LF_THREADS, 1024 / LF_THREADS) k_local_finish(
                 const int st = (int)(s_act[cur][sg].start - base), len = (int)s_act[cur][sg].len;
                 for (int e = lane; e < len; e += 32) s_seg[st + e] = (uint8_t)sg;
             }
+            // next level's tallies (at most two live children per live sub-node)
+            for (int i = tid; i < min(2 * nact, LF_MAXSEG) * KM; i += LF_THREADS) s_ones[i] = 0;
             __syncthreads();
             // zero flags of positions in live sub-nodes, block-wide exclusive scan
             uint32_t fl = 0, cnt = 0;
@@ -772,6 +807,7 @@ size_t local_finish_smem(int LM, int K) {
 // count of its words.
 __global__ void k_leaf_starts(const Node* __restrict__ leaves, const uint32_t* __restrict__ nl_p,
                               uint32_t* __restrict__ bitmap) {
+    pdl_wait();
     const uint32_t nl = *nl_p;
     for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < nl;
          l += (int64_t)gridDim.x * blockDim.x) {
@@ -781,6 +817,7 @@ __global__ void k_leaf_starts(const Node* __restrict__ leaves, const uint32_t* _
 }
 
 __global__ void k_word_popc(const uint32_t* __restrict__ bitmap, int64_t nw, uint32_t* __restrict__ cnt) {
+    pdl_wait();
     for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < nw;
          w += (int64_t)gridDim.x * blockDim.x)
         cnt[w] = __popc(bitmap[w]);
@@ -789,6 +826,7 @@ __global__ void k_word_popc(const uint32_t* __restrict__ bitmap, int64_t nw, uin
 __global__ void k_leaf_rank(const Node* __restrict__ leaves, const uint32_t* __restrict__ nl_p,
                             const uint32_t* __restrict__ bitmap, const uint32_t* __restrict__ pre,
                             uint32_t* __restrict__ order) {
+    pdl_wait();
     const uint32_t nl = *nl_p;
     for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < nl;
          l += (int64_t)gridDim.x * blockDim.x) {
@@ -802,6 +840,7 @@ __global__ void k_leaf_finalize(const Node* __restrict__ leaves, const uint32_t*
                                 const uint32_t* __restrict__ perm, const uint8_t* __restrict__ EP, int64_t n,
                                 int LK, int K, int nb, uint32_t* __restrict__ leaf_off, uint8_t* __restrict__ lo,
                                 uint8_t* __restrict__ hi, uint8_t* __restrict__ bits, int64_t total) {
+    pdl_wait();
     for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < nl;
          l += (int64_t)gridDim.x * blockDim.x) {
         const Node nd = leaves[order[l]];
@@ -821,6 +860,7 @@ __global__ void k_leaf_finalize(const Node* __restrict__ leaves, const uint32_t*
 
 __global__ void k_tree_begin(const uint32_t* __restrict__ leaf_off, int64_t nl, int64_t n, int L,
                              unsigned long long* __restrict__ begin) {
+    pdl_wait();
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t > L) return;
     const uint64_t target = (uint64_t)t * n;   // first leaf with start >= t*n
@@ -834,6 +874,7 @@ __global__ void k_tree_begin(const uint32_t* __restrict__ leaf_off, int64_t nl, 
 
 __global__ void k_gather_tcodes(const uint32_t* __restrict__ perm, const uint8_t* __restrict__ EP, int64_t n,
                                 int L, int K, uint8_t* __restrict__ tcodes) {
+    pdl_wait();
     const int LK = L * K;
     const int64_t total = n * L;
     for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total;
@@ -853,6 +894,7 @@ __global__ void k_gather_tcodes(const uint32_t* __restrict__ perm, const uint8_t
 __global__ void k_gather_rows_strided(const float* __restrict__ src, int64_t src_ld, int d,
                                       const uint32_t* __restrict__ ids, int64_t m, float* __restrict__ dst,
                                       int64_t dst_ld) {
+    pdl_wait();
     const int lane = threadIdx.x & 31;
     const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -867,6 +909,7 @@ __global__ void k_gather_rows_strided(const float* __restrict__ src, int64_t src
 // tree (the last tile of a tree may be shorter); one warp of the range filter owns a tile.
 __global__ void k_tile_flags(const uint32_t* __restrict__ leaf_off, int64_t nl, int64_t n, int tl,
                              const unsigned long long* __restrict__ tree_begin, uint32_t* __restrict__ flags) {
+    pdl_wait();
     for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < nl;
          l += (int64_t)gridDim.x * blockDim.x) {
         const int64_t t = leaf_off[l] / n;
@@ -889,6 +932,7 @@ __device__ __forceinline__ uint32_t plane_nibble(uint32_t w, int b) {
 }
 __global__ void __launch_bounds__(LM_WARPS * 32) k_leaf_morton(const uint32_t* __restrict__ leaf_off, int64_t nl, int K,
                                                                uint32_t* __restrict__ perm, uint8_t* __restrict__ tcodes) {
+    pdl_wait();
     __shared__ unsigned long long s_key[LM_WARPS][128];
     __shared__ uint32_t s_idx[LM_WARPS][128];
     __shared__ uint32_t s_perm[LM_WARPS][128];
@@ -980,6 +1024,7 @@ __global__ void __launch_bounds__(LL_WARPS * 32) k_leaf_layout16(const uint32_t*
                                                                  uint32_t* __restrict__ perm, const uint8_t* __restrict__ EP,
                                                                  int64_t n, int LK, uint8_t* __restrict__ tcodes,
                                                                  uint8_t* __restrict__ sbox, uint8_t* __restrict__ tbox) {
+    pdl_wait();
     __shared__ uint4 s_c[LL_WARPS][128];
     __shared__ uint32_t s_p[LL_WARPS][128];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -1114,6 +1159,7 @@ __global__ void __launch_bounds__(LL_WARPS * 32) k_leaf_layout16(const uint32_t*
 // run the min/max code per dim.  A valid lower bound for every member, tighter than the leaf's
 // (a few points span less of each dim): the pair kernel screens runs before their points.
 __global__ void k_sb_count(const uint32_t* __restrict__ leaf_off, int64_t nl, uint32_t* __restrict__ cnt) {
+    pdl_wait();
     for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < nl; l += (int64_t)gridDim.x * blockDim.x)
         cnt[l] = (leaf_off[l + 1] - leaf_off[l] + kSubBox - 1) / kSubBox;
 }
@@ -1123,6 +1169,7 @@ __global__ void k_sb_count(const uint32_t* __restrict__ leaf_off, int64_t nl, ui
 // Boxes are interleaved: box i = lo (K bytes) then hi (K bytes) at box + 2K i.
 __global__ void k_sb_boxes(const uint32_t* __restrict__ leaf_off, const uint32_t* __restrict__ sb_off, int64_t nl, int K,
                            const uint8_t* __restrict__ tcodes, uint8_t* __restrict__ box) {
+    pdl_wait();
     const uint32_t nsb = sb_off[nl];
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nsb; i += (int64_t)gridDim.x * blockDim.x) {
         int64_t a_ = 0, b_ = nl - 1;                  // last leaf l with sb_off[l] <= i
@@ -1159,6 +1206,7 @@ __global__ void k_sb_boxes(const uint32_t* __restrict__ leaf_off, const uint32_t
 // Tight box of each leaf as the union of its sub-boxes' boxes (same min/max over the same points).
 __global__ void k_leaf_tight_sb(const uint32_t* __restrict__ sb_off, int64_t nl, int K, const uint8_t* __restrict__ sbox,
                                 uint8_t* __restrict__ tbox) {
+    pdl_wait();
     for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < nl; l += (int64_t)gridDim.x * blockDim.x) {
         const uint32_t a = sb_off[l], e = sb_off[l + 1];
         if (K == 16) {
@@ -1189,6 +1237,7 @@ __global__ void k_leaf_tight_sb(const uint32_t* __restrict__ sb_off, int64_t nl,
 // bounding box, so its lower bound never exceeds a member leaf's -- the filter skips whole tiles).
 __global__ void k_tile_boxes(const uint32_t* __restrict__ tile_leaf, const uint32_t* __restrict__ ntiles_p, int K, const uint8_t* __restrict__ lo,
                              const uint8_t* __restrict__ hi, uint8_t* __restrict__ tlo, uint8_t* __restrict__ thi) {
+    pdl_wait();
     const int64_t ntiles = *ntiles_p;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < ntiles * K;
          i += (int64_t)gridDim.x * blockDim.x) {
@@ -1206,6 +1255,7 @@ __global__ void k_tile_boxes(const uint32_t* __restrict__ tile_leaf, const uint3
 
 __global__ void k_tile_write(const uint32_t* __restrict__ flags, const uint32_t* __restrict__ idx, int64_t nl,
                              uint32_t* __restrict__ tile_leaf) {
+    pdl_wait();
     for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < nl;
          l += (int64_t)gridDim.x * blockDim.x)
         if (flags[l]) tile_leaf[idx[l]] = (uint32_t)l;
@@ -1216,6 +1266,7 @@ __global__ void k_tile_write(const uint32_t* __restrict__ flags, const uint32_t*
 // 5-step shuffle search, written coalesced
 __global__ void k_point_tile_leaf(const uint32_t* __restrict__ leaf_off, const uint32_t* __restrict__ tile_leaf,
                                   const uint32_t* __restrict__ ntiles_p, int64_t nl, uint16_t* __restrict__ ptl) {
+    pdl_wait();
     const int lane = threadIdx.x & 31;
     const int64_t ntiles = *ntiles_p;
     for (int64_t t = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; t < ntiles;
@@ -1243,6 +1294,7 @@ __global__ void k_point_tile_leaf(const uint32_t* __restrict__ leaf_off, const u
 __global__ void k_tree_tiles(const uint32_t* __restrict__ idx, const unsigned long long* __restrict__ leaf_begin,
                              int L, const uint32_t* __restrict__ ntiles_p, uint32_t nl, uint32_t* __restrict__ tile_leaf,
                              unsigned long long* __restrict__ tile_begin) {
+    pdl_wait();
     const int t = threadIdx.x;
     const uint32_t ntiles = *ntiles_p;
     if (t < L) tile_begin[t] = leaf_begin[t] < nl ? idx[leaf_begin[t]] : ntiles;
@@ -1254,6 +1306,7 @@ __global__ void k_tree_tiles(const uint32_t* __restrict__ idx, const unsigned lo
 
 // ||x||^2 of every row, warp per row (used when the projection ran on the CUDA cores).
 __global__ void k_row_norms(const float* __restrict__ X, int64_t ld, int64_t n, float* __restrict__ out) {
+    pdl_wait();
     const int lane = threadIdx.x & 31;
     for (int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; r < n;
          r += ((int64_t)gridDim.x * blockDim.x) >> 5) {

@@ -44,16 +44,34 @@ void profile_end(cudaStream_t st, int slot);
 
 // Every kernel launch goes through this macro: counts launches (the evidence counter
 // behind detlsh_launch_count), optionally times it, and checks the launch error.
-#define DL_LAUNCH(kernel, grid, block, smem, stream, ...)                                       \
+// Every launch allows programmatic dependent launch (PDL): the next kernel on the stream is
+// launched while this one drains, and every kernel of the library begins with pdl_wait()
+// (griddepcontrol.wait: returns once the preceding grid has completed and its memory is visible;
+// a no-op for a launch without the attribute), so results are those of plain stream order and
+// only the launch latency between dependent kernels overlaps.  DETLSH_PDL=0 turns it off.
+bool pdl_enabled();
+#define DL_LAUNCH(kernel, grid, block, smem, strm_, ...)                                         \
     do {                                                                                       \
         int _slot = -1;                                                                        \
         if (::detlsh::g_profile.load(std::memory_order_relaxed))                               \
-            ::detlsh::profile_begin((stream), #kernel, &_slot);                                \
-        kernel<<<(grid), (block), (smem), (stream)>>>(__VA_ARGS__);                            \
+            ::detlsh::profile_begin((strm_), #kernel, &_slot);                                \
+        cudaLaunchConfig_t _cfg = {};                                                          \
+        _cfg.gridDim = dim3(grid);                                                             \
+        _cfg.blockDim = dim3(block);                                                           \
+        _cfg.dynamicSmemBytes = (size_t)(smem);                                                \
+        _cfg.stream = (strm_);                                                                  \
+        cudaLaunchAttribute _attr[1];                                                          \
+        _attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;                      \
+        _attr[0].val.programmaticStreamSerializationAllowed = 1;                               \
+        _cfg.attrs = _attr;                                                                    \
+        _cfg.numAttrs = ::detlsh::pdl_enabled() ? 1 : 0;                                       \
+        DL_CUDA(cudaLaunchKernelEx(&_cfg, kernel, __VA_ARGS__));                               \
         ::detlsh::g_launches.fetch_add(1, std::memory_order_relaxed);                          \
-        if (_slot >= 0) ::detlsh::profile_end((stream), _slot);                                \
+        if (_slot >= 0) ::detlsh::profile_end((strm_), _slot);                                \
         DL_CUDA(cudaGetLastError());                                                           \
     } while (0)
+
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 #define COMMA ,
 

@@ -42,6 +42,7 @@ __device__ int mrank(const int64_t* ids, const float* dists, int64_t base, int k
 __global__ void __launch_bounds__(256) k_merge_topk(const int64_t* __restrict__ ids, const float* __restrict__ dists,
                                                     int G, int64_t nq, int k, int64_t* __restrict__ out_ids,
                                                     float* __restrict__ out_dists) {
+    pdl_wait();
     for (int64_t q = blockIdx.x; q < nq; q += gridDim.x) {
         for (int e = threadIdx.x; e < k; e += blockDim.x) {
             out_ids[q * k + e] = -1;

@@ -12,6 +12,7 @@ constexpr int BM = 64, BN = 64, BK = 32;
 __global__ void __launch_bounds__(256) k_project_simt(const float* __restrict__ X, int64_t ld, int64_t m,
                                                       const float* __restrict__ A, int LK,
                                                       float* __restrict__ P, int* __restrict__ nonfinite) {
+    pdl_wait();
     __shared__ __align__(16) float Xs[BK][BM + 4];
     __shared__ __align__(16) float As[BK][BN + 4];
     const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;

@@ -61,6 +61,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     k_project_tc(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmA, TcShape sh,
                  float* __restrict__ P, int* __restrict__ nonfinite, const float* __restrict__ B,
                  uint8_t* __restrict__ EP, float* __restrict__ xnorm, uint32_t* __restrict__ fkey) {
+    pdl_wait();
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     // 1024-byte alignment of every swizzled buffer
     // 1024-byte aligned, by pointer arithmetic on the shared array (keeps the shared address

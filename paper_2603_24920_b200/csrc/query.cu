@@ -57,6 +57,7 @@ struct QState {  // per query of a batch
 //      s_x (AMB-6).  The LUT depends only on the projected query, not on the radius.
 __global__ void k_build_lut(const float* __restrict__ Qp, int nqb, int LK, int N_r, const float* __restrict__ B,
                             float* __restrict__ lut, uint8_t* __restrict__ sx) {
+    pdl_wait();
     const int64_t total = (int64_t)nqb * LK * N_r;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
          i += (int64_t)gridDim.x * blockDim.x) {
@@ -98,6 +99,7 @@ __global__ void k_build_tables(const float* __restrict__ Qp, int LK, int N_r, co
                                float* __restrict__ lut, uint8_t* __restrict__ sx,
                                float inv_a, float cap_a, uint16_t* __restrict__ qa,
                                float inv_b, float cap_b, uint16_t* __restrict__ qb_) {
+    pdl_wait();
     const int r = blockIdx.x, q = blockIdx.y, s = threadIdx.x;
     const int64_t qr = (int64_t)q * LK + r;
     const float* b = B + (int64_t)r * (N_r + 1);
@@ -120,6 +122,7 @@ __global__ void __launch_bounds__(256) k_build_tables256(const float* __restrict
                                                          int LK, float* __restrict__ lut, uint8_t* __restrict__ sx,
                                                          float inv_a, float cap_a, uint16_t* __restrict__ qa,
                                                          float inv_b, float cap_b, uint16_t* __restrict__ qb_) {
+    pdl_wait();
     constexpr int N_r = 256;
     const int lane = threadIdx.x & 31;
     const int64_t qr = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);   // q * LK + r
@@ -157,6 +160,7 @@ __global__ void __launch_bounds__(256) k_build_tables256(const float* __restrict
 // later rounds: block = one active query's (coordinate, region) rows
 __global__ void k_build_qlut(const float* __restrict__ lut, const int* __restrict__ act, int64_t per_q,
                              float inv_rd, float cap, uint16_t* __restrict__ qlut) {
+    pdl_wait();
     const int64_t q = act[blockIdx.y];
     const float* src = lut + q * per_q;
     uint16_t* dst = qlut + q * per_q;
@@ -172,6 +176,7 @@ __global__ void __launch_bounds__(256) k_group_table(const int* __restrict__ act
                                                      int64_t per_q, int t, int KN, uint32_t cap,
                                                      const uint8_t* __restrict__ sx, int L, int K, int N_r,
                                                      uint4* __restrict__ gtab, unsigned int* __restrict__ tctr) {
+    pdl_wait();
     // block = (16-query group, dim j); thread = region code c (coalesced table reads per query)
     __shared__ int s_qq[16], s_sv[16];
     const int na = dna ? *dna : na_ub;       // device count (the list is compacted on the device)
@@ -365,6 +370,7 @@ struct RFArgs {
 
 template <int KT, int NRT, int G, bool PQ>
 __global__ void __launch_bounds__(RF_THREADS, RF_CTAS) k_range_filter(RFArgs a) {
+    pdl_wait();
     constexpr uint32_t QT = QuantSpec<G>::QT, CAP = QuantSpec<G>::CAP;
     constexpr bool SIMD_LEAF = KT == 16 && G == 16;   // leaf bounds of all 16 queries per lane
     extern __shared__ __align__(16) unsigned char smem[];
@@ -865,6 +871,7 @@ __global__ void __launch_bounds__(RF_THREADS, RF_CTAS) k_range_filter(RFArgs a) 
 __global__ void k_qkey(const int* __restrict__ act, int na_ub, const int* __restrict__ dna,
                        const uint8_t* __restrict__ sx, int L, int K, int nb, int t,
                        uint32_t* __restrict__ keys, uint32_t* __restrict__ vals) {
+    pdl_wait();
     const int na = dna ? *dna : na_ub;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < na_ub; i += gridDim.x * blockDim.x) {
         uint32_t key = 0xFFFFFFu;
@@ -884,6 +891,7 @@ __global__ void k_qkey(const int* __restrict__ act, int na_ub, const int* __rest
 __global__ void k_chunk_prep(const int* __restrict__ act, int na_ub, const int* __restrict__ dna,
                              const uint32_t* __restrict__ pcnt, uint32_t* __restrict__ ptake,
                              unsigned int* __restrict__ tctr) {
+    pdl_wait();
     const int na = dna ? *dna : na_ub;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < na; i += gridDim.x * blockDim.x) {
         if (pcnt) {
@@ -904,6 +912,7 @@ __global__ void k_chunk_prep(const int* __restrict__ act, int na_ub, const int* 
 //      query's own 12-bit table -- only the pairs a query reaches are bounded, instead of every
 //      leaf of every tile any of the 16 queries reaches (the group's union).
 __global__ void __launch_bounds__(RF_THREADS, RF_CTAS) k_tile_pairs(RFArgs a) {
+    pdl_wait();
     extern __shared__ __align__(16) unsigned char smem[];
     uint4* s_qe = reinterpret_cast<uint4*>(smem);                 // [16][256] x 16 B
     constexpr int G = 16, N_r = 256, K = 16;
@@ -1046,9 +1055,10 @@ constexpr int LP_THREADS = 256;     // threads per pair-kernel block (512 with h
 
 // KT, NRT > 0: K and N_r fixed at compile time (table rows at immediate offsets, a static table);
 // LPG listed leaves per warp chunk
-// BX: box bounds by box_bound16 (K = 16, N_r = 256)
+// BX bit 0: box bounds by box_bound16 (K = 16, N_r = 256); bit 1: FIFO sub-box queue with L2 prefetch
 template <int KT, int NRT, int LPG, int BX = 0>
 __global__ void __launch_bounds__(LP_THREADS, LPG == 32 ? 5 : 6) k_leaf_points(LPArgs a) {
+    pdl_wait();
     extern __shared__ __align__(16) unsigned char lp_smem[];
     __shared__ __align__(16) uint16_t lp_static[(KT > 0 && NRT > 0) ? KT * NRT : 8];
     const int ai = blockIdx.x;
@@ -1085,16 +1095,23 @@ __global__ void __launch_bounds__(LP_THREADS, LPG == 32 ? 5 : 6) k_leaf_points(L
     // counter to all warps of the query's blocks -- and screens their points packed 32 per step
     // (the owning leaf of packed point i found by a log2(LPG)-step search over the chunk's prefix)
     // per warp: queued sub-boxes (first point position, point count) that passed their bound
-    __shared__ uint32_t s_sqf[LP_THREADS / 32][64];
-    __shared__ uint8_t s_sqc[LP_THREADS / 32][64];
+    // PF (tile mode): the queue is a FIFO ring; a passing sub-box's codes are prefetched into L2
+    // when it is queued and its points are screened only after the next sub-box step (the code
+    // loads were the top stall: 24 % of the samples on the point-screen line, ncu)
+    constexpr bool PF = (BX & 2) != 0;
+    constexpr int SQ = PF ? 128 : 64;
+    __shared__ uint32_t s_sqf[LP_THREADS / 32][SQ];
+    __shared__ uint8_t s_sqc[LP_THREADS / 32][SQ];
     uint32_t* sq_first = s_sqf[threadIdx.x >> 5];
     uint8_t* sq_cnt = s_sqc[threadIdx.x >> 5];
-    uint32_t sqn = 0;                                // warp-uniform
-    // screen the points of the last nb queued sub-boxes: lane = (sub-box lane / kSubBox, point)
+    uint32_t sqn = 0;                                // warp-uniform (PF: the ring's tail)
+    uint32_t sqh = 0;                                // PF: the ring's head
+    // screen the points of nb queued sub-boxes (the last nb; PF: the first nb): lane = (sub-box
+    // lane / kSubBox, point)
     auto sb_points = [&](uint32_t nb) {
         const uint32_t sbs = lane / kSubBox, k = lane % kSubBox;
         if (sbs < nb) {
-            const uint32_t e = sqn - nb + sbs;
+            const uint32_t e = PF ? ((sqh + sbs) & (SQ - 1)) : sqn - nb + sbs;
             if (k < sq_cnt[e]) {
                 const uint32_t pos = sq_first[e] + k - (uint32_t)a.pos_base;
                 uint32_t acc = 0;
@@ -1132,7 +1149,8 @@ __global__ void __launch_bounds__(LP_THREADS, LPG == 32 ? 5 : 6) k_leaf_points(L
                 }
             }
         }
-        sqn -= nb;
+        if (PF) sqh += nb;
+        else sqn -= nb;
         __syncwarp();
     };
     uint32_t lt = 0, lp = 0;                         // tile mode: leaf bounds evaluated / passed
@@ -1286,15 +1304,30 @@ __global__ void __launch_bounds__(LP_THREADS, LPG == 32 ? 5 : 6) k_leaf_points(L
                     ++sbt;
                 }
                 const uint32_t bal = __ballot_sync(0xffffffffu, pass);
-                if (pass) {
-                    const uint32_t slot = sqn + __popc(bal & lanemask_lt());
-                    sq_first[slot] = first;
-                    sq_cnt[slot] = (uint8_t)cnt;
-                }
-                sqn += __popc(bal);
-                __syncwarp();
-                while (sqn >= 32 / kSubBox) {
-                    sb_points(32 / kSubBox);
+                if constexpr (PF) {
+                    const uint32_t before = sqn;         // queued before this step: prefetched a step ago
+                    if (pass) {
+                        const uint32_t slot = (sqn + __popc(bal & lanemask_lt())) & (SQ - 1);
+                        sq_first[slot] = first;
+                        sq_cnt[slot] = (uint8_t)cnt;
+                        const uint8_t* c0p = a.tcodes + (int64_t)(first - (uint32_t)a.pos_base) * 16;
+                        asm volatile("prefetch.global.L2 [%0];" ::"l"(c0p));
+                        asm volatile("prefetch.global.L2 [%0];" ::"l"(c0p + 16 * (cnt - 1)));
+                    }
+                    sqn += __popc(bal);
+                    __syncwarp();
+                    while (before - sqh >= 32 / kSubBox) sb_points(32 / kSubBox);
+                } else {
+                    if (pass) {
+                        const uint32_t slot = sqn + __popc(bal & lanemask_lt());
+                        sq_first[slot] = first;
+                        sq_cnt[slot] = (uint8_t)cnt;
+                    }
+                    sqn += __popc(bal);
+                    __syncwarp();
+                    while (sqn >= 32 / kSubBox) {
+                        sb_points(32 / kSubBox);
+                    }
                 }
             }
             continue;
@@ -1356,7 +1389,12 @@ __global__ void __launch_bounds__(LP_THREADS, LPG == 32 ? 5 : 6) k_leaf_points(L
         }
     }   // tiles of this take
     }   // takes
-    if (sqn) sb_points(sqn);
+    if constexpr (PF) {
+        while (sqn - sqh >= 32 / kSubBox) sb_points(32 / kSubBox);
+        if (sqn != sqh) sb_points(sqn - sqh);
+    } else {
+        if (sqn) sb_points(sqn);
+    }
     for (int o = 16; o > 0; o >>= 1) {
         tested += __shfl_xor_sync(0xffffffffu, tested, o);
         passed += __shfl_xor_sync(0xffffffffu, passed, o);
@@ -1388,6 +1426,7 @@ __global__ void __launch_bounds__(256) k_count_new(const int* __restrict__ act, 
                                                    QState* __restrict__ qs, const uint32_t* __restrict__ cur,
                                                    uint32_t* __restrict__ prev, int64_t nwords,
                                                    const uint32_t* __restrict__ wsum, int64_t nsw, int commit) {
+    pdl_wait();
     __shared__ unsigned int s_cnt;
     if (dna && (int)blockIdx.x >= *dna) return;
     const int q = act[blockIdx.x];
@@ -1430,6 +1469,7 @@ __global__ void __launch_bounds__(256) k_count_new(const int* __restrict__ act, 
 __global__ void k_lbo_cross(const int* __restrict__ act, int na_ub, const int* __restrict__ dna,
                             const QState* __restrict__ qs, int64_t budget, int* __restrict__ cross,
                             int* __restrict__ ncross) {
+    pdl_wait();
     const int na = dna ? *dna : na_ub;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < na; i += gridDim.x * blockDim.x) {
         const int q = act[i];
@@ -1462,6 +1502,7 @@ struct LboArgs {
 
 template <bool MARK>
 __global__ void __launch_bounds__(256) k_lbo_leaves(LboArgs a) {
+    pdl_wait();
     extern __shared__ float s_lut[];                   // the query's fp32 table of tree t
     const int c = blockIdx.y;
     const int q = a.cross[c];
@@ -1525,6 +1566,7 @@ __global__ void __launch_bounds__(1024) k_lbo_cut(const int* __restrict__ cross,
                                                   int64_t budget, const uint32_t* __restrict__ skeys,
                                                   const uint32_t* __restrict__ svals, const uint32_t* __restrict__ nnew,
                                                   int64_t nl, unsigned long long* __restrict__ cut) {
+    pdl_wait();
     __shared__ uint32_t s_w[32];
     __shared__ int64_t s_hit;
     const int c = blockIdx.x;
@@ -1569,6 +1611,7 @@ __global__ void __launch_bounds__(1024) k_lbo_cut(const int* __restrict__ cross,
 
 __global__ void k_lbo_reset(const int* __restrict__ cross, int ncross, const uint32_t* __restrict__ prev,
                             uint32_t* __restrict__ cur, int64_t nwords) {
+    pdl_wait();
     const int64_t total = (int64_t)ncross * nwords;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t c = i / nwords, w = i - c * nwords;
@@ -1584,6 +1627,7 @@ __global__ void k_lbo_reset(const int* __restrict__ cross, int ncross, const uin
 __global__ void k_count_decide(const int* __restrict__ act, int na_ub, const int* __restrict__ dna,
                                QState* __restrict__ qs, int64_t budget, int force, uint32_t* __restrict__ pcnt,
                                uint32_t* __restrict__ ptake) {
+    pdl_wait();
     const int na = dna ? *dna : na_ub;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < na; i += gridDim.x * blockDim.x) {
         if (pcnt) { pcnt[act[i]] = 0; ptake[act[i]] = 0; }
@@ -1606,6 +1650,7 @@ __device__ inline void tree_end_one(QState* s, int t, int round, int64_t budget,
 
 __global__ void k_tree_end(const int* __restrict__ act, int na_ub, const int* __restrict__ dna, QState* __restrict__ qs,
                            int t, int round, int64_t budget, int64_t cap) {
+    pdl_wait();
     const int na = dna ? *dna : na_ub;
     for (int a_ = blockIdx.x * blockDim.x + threadIdx.x; a_ < na; a_ += gridDim.x * blockDim.x)
         tree_end_one(&qs[act[a_]], t, round, budget, cap);
@@ -1616,6 +1661,7 @@ __global__ void k_tree_end(const int* __restrict__ act, int na_ub, const int* __
 __global__ void k_tree_end_compact(const int* __restrict__ act, int na_ub, const int* __restrict__ dna,
                                    QState* __restrict__ qs, int t, int round, int64_t budget, int64_t cap,
                                    int* __restrict__ act_out, int* __restrict__ n_out) {
+    pdl_wait();
     const int na = dna ? *dna : na_ub;
     __shared__ int s_n;
     __shared__ int s_w[32];
@@ -1685,6 +1731,7 @@ __global__ void __launch_bounds__(256) k_tree_post(const int* __restrict__ act, 
                                                    int t, int round, int64_t cap, unsigned int* __restrict__ ticket,
                                                    int* __restrict__ act_out, int* __restrict__ n_out,
                                                    unsigned long long* __restrict__ total) {
+    pdl_wait();
     // total != null: end of round instead -- every count forced, no budget test, and the last
     // block lays out the round-buffer slots [roff, roff + rcnt) instead of compacting
     __shared__ unsigned int s_cnt, s_last;
@@ -1825,6 +1872,7 @@ __global__ void __launch_bounds__(1024) k_verify_offsets(const int* __restrict__
                                                          const uint32_t* __restrict__ cur, const uint32_t* __restrict__ ver,
                                                          int64_t nwords, int rbw, int64_t nblocks,
                                                          uint32_t* __restrict__ boff) {
+    pdl_wait();
     __shared__ uint32_t s_w[32];
     const int q = act[blockIdx.x];
     const uint32_t* c = cur + (int64_t)q * nwords;
@@ -1870,6 +1918,7 @@ __global__ void __launch_bounds__(1024) k_verify_offsets(const int* __restrict__
 // NV = 0: rows wider than 256 fp32, the query is re-read from L1/L2).
 template <int NV, bool EXACT>
 __global__ void __launch_bounds__(VR_THREADS) k_verify_rows(VRArgs a) {
+    pdl_wait();
     extern __shared__ __align__(16) float4 s_rows[];
     __shared__ uint8_t s_list[VR_THREADS / 32][256];     // per warp: rows (in block) of the new bits
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = VR_THREADS / 32;
@@ -1980,6 +2029,7 @@ __global__ void __launch_bounds__(1024) k_verify_prep(const int* __restrict__ ac
                                                       const uint32_t* __restrict__ cur, uint32_t* __restrict__ ver,
                                                       int64_t nwords, uint32_t* __restrict__ NB,
                                                       uint32_t* __restrict__ BO) {
+    pdl_wait();
     // nwords is a multiple of 4 (padded bitmap rows): each thread owns 4 consecutive words
     __shared__ uint32_t s_w[32];
     const int a = blockIdx.x;
@@ -2036,6 +2086,7 @@ __global__ void __launch_bounds__(256) k_verify_list(const int* __restrict__ act
                                                      const uint32_t* __restrict__ cur, uint32_t* __restrict__ ver,
                                                      int64_t nwords, const uint32_t* __restrict__ wsum, int64_t nsw,
                                                      uint32_t* __restrict__ cand, uint32_t* __restrict__ cq) {
+    pdl_wait();
     __shared__ unsigned long long s_slot;             // 64-bit slots: a round may hold >= 2^32 pairs
     const int a = blockIdx.x;
     const int q = act[a];
@@ -2061,6 +2112,7 @@ __global__ void __launch_bounds__(256) k_verify_list(const int* __restrict__ act
 
 __global__ void k_prep_queries(const float* __restrict__ Q, int64_t ld, const int* __restrict__ act, int na,
                                float* __restrict__ Qa, float* __restrict__ Qalo, float* __restrict__ qn) {
+    pdl_wait();
     const int lane = threadIdx.x & 31;
     for (int a = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); a < na; a += gridDim.x * (blockDim.x >> 5)) {
         const float* src = Q + (int64_t)act[a] * ld;
@@ -2111,6 +2163,7 @@ __global__ void __launch_bounds__(256) k_verify_gather(const uint32_t* __restric
                                                        const int* __restrict__ act, const float* __restrict__ X,
                                                        const float* __restrict__ Q, int64_t ld, int64_t total,
                                                        float* __restrict__ d2) {
+    pdl_wait();
     const int u = threadIdx.x & 7;
     const int nf4 = (int)(ld / 4);
     for (int64_t slot = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 3; slot < total;
@@ -2163,6 +2216,7 @@ __global__ void __launch_bounds__(256) k_verify_gather(const uint32_t* __restric
 __global__ void __launch_bounds__(256) k_rerank_exact(const QState* __restrict__ qs, const float* __restrict__ X,
                                                       const float* __restrict__ Q, int64_t ld, int k,
                                                       unsigned long long* __restrict__ topk) {
+    pdl_wait();
     __shared__ unsigned long long s_keys[TK_MAX];
     const int q = blockIdx.x;
     const int tk = qs[q].tk;
@@ -2197,6 +2251,7 @@ __global__ void __launch_bounds__(TK_THREADS) k_topk(const int* __restrict__ act
                                                      const uint32_t* __restrict__ cand, const float* __restrict__ d2,
                                                      unsigned long long* __restrict__ topk, int k,
                                                      float cr2, int round, int max_rounds) {
+    pdl_wait();
     __shared__ unsigned long long s_keys[TK_MAX];
     __shared__ uint32_t s_hist[256];
     uint32_t* s_h12 = reinterpret_cast<uint32_t*>(s_keys);   // 4096 bins, dead before s_keys is filled
@@ -2339,6 +2394,7 @@ __global__ void __launch_bounds__(TK_THREADS) k_topk(const int* __restrict__ act
 
 __global__ void k_compact(const int* __restrict__ act, int na_ub, const int* __restrict__ dna, const QState* __restrict__ qs, int* __restrict__ act_out,
                           int* __restrict__ n_out) {
+    pdl_wait();
     const int na = dna ? *dna : na_ub;
     __shared__ int s_n;
     if (threadIdx.x == 0) s_n = 0;
@@ -2368,6 +2424,7 @@ __global__ void k_finalize(const QState* __restrict__ qs, const unsigned long lo
                            const unsigned long long* __restrict__ topk, int nqb, int k,
                            int64_t id_offset, const double* __restrict__ radii, int64_t* __restrict__ out_ids,
                            float* __restrict__ out_d, detlsh_query_stats* __restrict__ stats, int null_on_cap) {
+    pdl_wait();
     const int64_t total = (int64_t)nqb * k;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
          i += (int64_t)gridDim.x * blockDim.x) {
@@ -2408,6 +2465,7 @@ __global__ void k_finalize(const QState* __restrict__ qs, const unsigned long lo
 __global__ void __launch_bounds__(256) k_clear_dirty(uint32_t* __restrict__ bm, uint32_t* __restrict__ prev,
                                                      uint32_t* __restrict__ ver, const uint32_t* __restrict__ wsum,
                                                      int64_t nwords, int64_t nsw) {
+    pdl_wait();
     const int64_t row = blockIdx.y;
     for (int64_t sw = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; sw < nsw; sw += (int64_t)gridDim.x * blockDim.x) {
         uint32_t f = wsum[row * nsw + sw];
@@ -2424,6 +2482,7 @@ __global__ void __launch_bounds__(256) k_clear_dirty(uint32_t* __restrict__ bm, 
 }
 
 __global__ void k_init_batch(QState* __restrict__ qs, int* __restrict__ act, int nqb) {
+    pdl_wait();
     for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < nqb; q += gridDim.x * blockDim.x) {
         QState s;
         s.cnt = 0; s.nver = 0; s.roff = 0; s.rcnt = 0; s.status = ST_ACTIVE; s.tk = 0; s.trees_last = 0; s.rounds = 0;
@@ -2472,6 +2531,7 @@ float fdiv_rd_host(float num, float den) {
 __global__ void __launch_bounds__(256) k_rstar_tree(const float* __restrict__ lut, const uint8_t* __restrict__ tcodes,
                                                     const uint32_t* __restrict__ perm, int64_t n, int t, int L, int K,
                                                     int N_r, uint32_t* __restrict__ tp) {
+    pdl_wait();
     extern __shared__ float s_lut1[];
     const int q = blockIdx.y;
     const float* src = lut + ((int64_t)q * L + t) * K * N_r;
@@ -2487,6 +2547,7 @@ __global__ void __launch_bounds__(256) k_rstar_tree(const float* __restrict__ lu
 
 __global__ void __launch_bounds__(1024) k_select_kth_u32(const uint32_t* __restrict__ vals, int64_t n, int64_t rank,
                                                           uint32_t* __restrict__ out) {
+    pdl_wait();
     __shared__ uint32_t s_hist[256];
     __shared__ uint32_t s_prefix, s_mask;
     __shared__ unsigned long long s_rem;
@@ -2687,7 +2748,10 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
     // box bounds two dims per min/max (box_bound16); DETLSH_BOX16=0 selects the byte-wise form (read
     // per call: experiments switch it between queries of one index)
     const bool box16 = !(std::getenv("DETLSH_BOX16") && std::atoi(std::getenv("DETLSH_BOX16")) == 0);
-    auto k_leaf_points_sel = tile_pairs ? (box16 ? k_leaf_points<16, 256, 32, 1> : k_leaf_points<16, 256, 32>)
+    // tile mode: point codes prefetched into L2 one sub-box step ahead (DETLSH_LP_PF, read per call)
+    const bool lp_pf = std::getenv("DETLSH_LP_PF") && std::atoi(std::getenv("DETLSH_LP_PF")) == 1;
+    auto k_leaf_points_sel = tile_pairs ? (box16 ? (lp_pf ? k_leaf_points<16, 256, 32, 3> : k_leaf_points<16, 256, 32, 1>)
+                                                 : k_leaf_points<16, 256, 32>)
                              : lp_fixed ? (lp_g == 8 ? k_leaf_points<16, 256, 8>
                                            : box16   ? k_leaf_points<16, 256, 16, 1>
                                                      : k_leaf_points<16, 256, 16>)

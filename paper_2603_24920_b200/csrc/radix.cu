@@ -19,6 +19,7 @@ constexpr int RS_WARPS = RS_THREADS / 32;
 
 __global__ void __launch_bounds__(RS_THREADS) k_rs_hist(const uint32_t* __restrict__ keys, int64_t m,
                                                         int shift, int tiles, uint32_t* __restrict__ hist) {
+    pdl_wait();
     __shared__ uint32_t h[256];
     const int seg = blockIdx.y, tile = blockIdx.x;
     h[threadIdx.x] = 0;
@@ -65,6 +66,7 @@ __device__ inline uint32_t block_exclusive_scan(uint32_t v, uint32_t* s_warp, ui
 // Exclusive scan, in place, of one digit's per-tile counts (warp per (digit, segment); 8 digits
 // per block); the digit's total goes to dtot[seg][digit] (the scatter turns those into digit bases).
 __global__ void __launch_bounds__(256) k_rs_scan(uint32_t* __restrict__ hist, int tiles, uint32_t* __restrict__ dtot) {
+    pdl_wait();
     const int lane = threadIdx.x & 31;
     const int dig = blockIdx.x * 8 + (threadIdx.x >> 5), seg = blockIdx.y;
     uint32_t* h = hist + ((int64_t)seg * 256 + dig) * tiles;
@@ -101,6 +103,7 @@ __global__ void __launch_bounds__(RS_THREADS) k_rs_scatter(const uint32_t* __res
                                                            int shift, int tiles,
                                                            const uint32_t* __restrict__ offs,
                                                            const uint32_t* __restrict__ dtot) {
+    pdl_wait();
     __shared__ uint32_t s_base[256];                 // global position of the tile's first key of digit d
     __shared__ uint32_t s_tds[256];                  // first staged slot of digit d in the sorted tile
     __shared__ uint32_t s_wh[RS_WARPS][256];         // per-warp digit counts -> per-warp digit offsets
@@ -187,6 +190,7 @@ constexpr int SC_TILE = SC_THREADS * SC_IPT;
 
 __global__ void __launch_bounds__(SC_THREADS) k_scan_tiles(const uint32_t* __restrict__ in, int64_t n,
                                                            uint32_t* __restrict__ tile_sums) {
+    pdl_wait();
     __shared__ uint32_t s_warp[32];
     int64_t base = (int64_t)blockIdx.x * SC_TILE;
     uint32_t s = 0;
@@ -202,6 +206,7 @@ __global__ void __launch_bounds__(SC_THREADS) k_scan_tiles(const uint32_t* __res
 
 __global__ void __launch_bounds__(SC_THREADS) k_scan_sums(uint32_t* __restrict__ sums, int64_t nt,
                                                           uint32_t* __restrict__ d_total) {
+    pdl_wait();
     __shared__ uint32_t s_warp[32];
     uint32_t carry = 0;
     for (int64_t base = 0; base < nt; base += SC_THREADS) {
@@ -218,6 +223,7 @@ __global__ void __launch_bounds__(SC_THREADS) k_scan_sums(uint32_t* __restrict__
 __global__ void __launch_bounds__(SC_THREADS) k_scan_apply(const uint32_t* __restrict__ in, int64_t n,
                                                            const uint32_t* __restrict__ tile_offs,
                                                            uint32_t* __restrict__ out) {
+    pdl_wait();
     __shared__ uint32_t s_warp[32];
     int64_t base = (int64_t)blockIdx.x * SC_TILE;
     uint32_t v[SC_IPT], s = 0;

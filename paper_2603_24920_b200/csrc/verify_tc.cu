@@ -60,6 +60,7 @@ __global__ void __launch_bounds__(VT_THREADS, 1)
                 const __grid_constant__ CUtensorMap tmQlo, const __grid_constant__ CUtensorMap tmNB,
                 const __grid_constant__ CUtensorMap tmBO, VtcShape sh, const float* __restrict__ xn,
                 const float* __restrict__ qn, uint32_t* __restrict__ cand, float* __restrict__ d2) {
+    pdl_wait();
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     // 1024-byte aligned, by pointer arithmetic on the shared array (keeps the shared address
     // space: LDS/STS instead of generic LD/ST)

@@ -1018,6 +1018,40 @@ __device__ __forceinline__ uint4 shfl_xor4(uint4 v, int m) {
     return make_uint4(__shfl_xor_sync(0xffffffffu, v.x, m), __shfl_xor_sync(0xffffffffu, v.y, m),
                       __shfl_xor_sync(0xffffffffu, v.z, m), __shfl_xor_sync(0xffffffffu, v.w, m));
 }
+// 16 code bytes spread into 8 words of 16-bit lanes (even bytes of word i in e[i], odd in o[i]):
+// byte-wise min / max of two such boxes is 8 VIMNMX.U16x2 (the packed __vminu4 is emulated, ~6
+// instructions per word), packed back into bytes once at the end.
+struct Spread16 { uint32_t v[8]; };
+__device__ __forceinline__ Spread16 spread16(uint4 c) {
+    const uint32_t w[4] = {c.x, c.y, c.z, c.w};
+    Spread16 r;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        r.v[2 * i] = __byte_perm(w[i], 0u, 0x4240);
+        r.v[2 * i + 1] = __byte_perm(w[i], 0u, 0x4341);
+    }
+    return r;
+}
+__device__ __forceinline__ uint4 pack16(const Spread16& a) {   // inverse of spread16
+    uint32_t w[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) w[i] = __byte_perm(a.v[2 * i], a.v[2 * i + 1], 0x6240);
+    return make_uint4(w[0], w[1], w[2], w[3]);
+}
+__device__ __forceinline__ void min16x2_into(Spread16& a, const Spread16& b) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) asm("min.u16x2 %0, %0, %1;" : "+r"(a.v[i]) : "r"(b.v[i]));
+}
+__device__ __forceinline__ void max16x2_into(Spread16& a, const Spread16& b) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) asm("max.u16x2 %0, %0, %1;" : "+r"(a.v[i]) : "r"(b.v[i]));
+}
+__device__ __forceinline__ Spread16 shfl_xor16(const Spread16& a, int m) {
+    Spread16 r;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) r.v[i] = __shfl_xor_sync(0xffffffffu, a.v[i], m);
+    return r;
+}
 constexpr int LL_WARPS = 8;
 __global__ void __launch_bounds__(LL_WARPS * 32) k_leaf_layout16(const uint32_t* __restrict__ leaf_off, int64_t nl,
                                                                  const uint32_t* __restrict__ sb_off,
@@ -1027,6 +1061,7 @@ __global__ void __launch_bounds__(LL_WARPS * 32) k_leaf_layout16(const uint32_t*
     pdl_wait();
     __shared__ uint4 s_c[LL_WARPS][128];
     __shared__ uint32_t s_p[LL_WARPS][128];
+    __shared__ uint8_t s_srt[LL_WARPS][128];          // sorted position -> gathered slot
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const uint4 NEUT_LO = make_uint4(~0u, ~0u, ~0u, ~0u), NEUT_HI = make_uint4(0, 0, 0, 0);
     for (int64_t l = (int64_t)blockIdx.x * LL_WARPS + w; l < nl; l += (int64_t)gridDim.x * LL_WARPS) {
@@ -1115,41 +1150,43 @@ __global__ void __launch_bounds__(LL_WARPS * 32) k_leaf_layout16(const uint32_t*
             }
         }
         __syncwarp();
-        uint4 tl = NEUT_LO, th = NEUT_HI;
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
             if (r >= R) continue;
             const int e = r * 32 + lane;
-            uint4 c = NEUT_LO, cmax = NEUT_HI;
             if (e < m) {
                 const int src = (int)(key[r] & 127ull);
-                c = s_c[w][src];
-                cmax = c;
+                s_srt[w][e] = (uint8_t)src;
                 perm[p0 + e] = s_p[w][src];
-                *reinterpret_cast<uint4*>(tcodes + (int64_t)(p0 + e) * 16) = c;
+                *reinterpret_cast<uint4*>(tcodes + (int64_t)(p0 + e) * 16) = s_c[w][src];
             }
-            // sub-box of positions [8 s, 8 s + 8): lanes of one aligned 8-lane group
-            uint4 lo = c, hi = cmax;
-#pragma unroll
-            for (int o = 1; o < kSubBox; o <<= 1) {
-                lo = vmin4(lo, shfl_xor4(lo, o));
-                hi = vmax4(hi, shfl_xor4(hi, o));
-            }
-            if ((lane & (kSubBox - 1)) == 0 && e < m) {
-                const uint32_t s = sb0 + (uint32_t)(e / kSubBox);
-                *reinterpret_cast<uint4*>(sbox + (int64_t)s * 32) = lo;
-                *reinterpret_cast<uint4*>(sbox + (int64_t)s * 32 + 16) = hi;
-            }
-            tl = vmin4(tl, lo);
-            th = vmax4(th, hi);
         }
-        for (int o = 8; o < 32; o <<= 1) {
-            tl = vmin4(tl, shfl_xor4(tl, o));
-            th = vmax4(th, shfl_xor4(th, o));
+        __syncwarp();
+        // sub-box s = sorted positions [8 s, 8 s + 8) on lane s (<= 16 of them), byte-wise min / max
+        // in the spread form; then the leaf's tight box as the union of its sub-boxes' boxes
+        const int nsb = (m + kSubBox - 1) / kSubBox;
+        Spread16 lo, hi;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) { lo.v[i] = 0x00FF00FFu; hi.v[i] = 0u; }
+        if (lane < nsb) {
+            const int e0 = lane * kSubBox, e1 = min(m, e0 + kSubBox);
+            for (int e = e0; e < e1; ++e) {
+                const Spread16 c = spread16(s_c[w][s_srt[w][e]]);
+                min16x2_into(lo, c);
+                max16x2_into(hi, c);
+            }
+            const uint32_t sidx = sb0 + (uint32_t)lane;
+            *reinterpret_cast<uint4*>(sbox + (int64_t)sidx * 32) = pack16(lo);
+            *reinterpret_cast<uint4*>(sbox + (int64_t)sidx * 32 + 16) = pack16(hi);
+        }
+#pragma unroll
+        for (int o = 1; o < 16; o <<= 1) {             // nsb <= 16: lanes 0-15 hold every sub-box
+            min16x2_into(lo, shfl_xor16(lo, o));
+            max16x2_into(hi, shfl_xor16(hi, o));
         }
         if (lane == 0) {
-            *reinterpret_cast<uint4*>(tbox + l * 32) = tl;
-            *reinterpret_cast<uint4*>(tbox + l * 32 + 16) = th;
+            *reinterpret_cast<uint4*>(tbox + l * 32) = pack16(lo);
+            *reinterpret_cast<uint4*>(tbox + l * 32 + 16) = pack16(hi);
         }
         __syncwarp();
     }

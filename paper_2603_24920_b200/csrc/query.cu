@@ -1056,6 +1056,7 @@ constexpr int LP_THREADS = 256;     // threads per pair-kernel block (512 with h
 // KT, NRT > 0: K and N_r fixed at compile time (table rows at immediate offsets, a static table);
 // LPG listed leaves per warp chunk
 // BX bit 0: box bounds by box_bound16 (K = 16, N_r = 256); bit 1: FIFO sub-box queue with L2 prefetch
+// of the point codes (bit 2: into L1)
 template <int KT, int NRT, int LPG, int BX = 0>
 __global__ void __launch_bounds__(LP_THREADS, LPG == 32 ? 5 : 6) k_leaf_points(LPArgs a) {
     pdl_wait();
@@ -1311,8 +1312,13 @@ __global__ void __launch_bounds__(LP_THREADS, LPG == 32 ? 5 : 6) k_leaf_points(L
                         sq_first[slot] = first;
                         sq_cnt[slot] = (uint8_t)cnt;
                         const uint8_t* c0p = a.tcodes + (int64_t)(first - (uint32_t)a.pos_base) * 16;
-                        asm volatile("prefetch.global.L2 [%0];" ::"l"(c0p));
-                        asm volatile("prefetch.global.L2 [%0];" ::"l"(c0p + 16 * (cnt - 1)));
+                        if constexpr ((BX & 4) != 0) {   // into L1 (the SM's own cache)
+                            asm volatile("prefetch.global.L1 [%0];" ::"l"(c0p));
+                            asm volatile("prefetch.global.L1 [%0];" ::"l"(c0p + 16 * (cnt - 1)));
+                        } else {
+                            asm volatile("prefetch.global.L2 [%0];" ::"l"(c0p));
+                            asm volatile("prefetch.global.L2 [%0];" ::"l"(c0p + 16 * (cnt - 1)));
+                        }
                     }
                     sqn += __popc(bal);
                     __syncwarp();
@@ -2749,8 +2755,10 @@ void query_index(const Index& ix, const float* d_Q, int64_t q_ld, const QueryArg
     // per call: experiments switch it between queries of one index)
     const bool box16 = !(std::getenv("DETLSH_BOX16") && std::atoi(std::getenv("DETLSH_BOX16")) == 0);
     // tile mode: point codes prefetched into L2 one sub-box step ahead (DETLSH_LP_PF, read per call)
-    const bool lp_pf = std::getenv("DETLSH_LP_PF") && std::atoi(std::getenv("DETLSH_LP_PF")) == 1;
-    auto k_leaf_points_sel = tile_pairs ? (box16 ? (lp_pf ? k_leaf_points<16, 256, 32, 3> : k_leaf_points<16, 256, 32, 1>)
+    const int lp_pf = std::getenv("DETLSH_LP_PF") ? std::atoi(std::getenv("DETLSH_LP_PF")) : 0;   // 1 L2, 2 L1
+    auto k_leaf_points_sel = tile_pairs ? (box16 ? (lp_pf == 2   ? k_leaf_points<16, 256, 32, 7>
+                                                    : lp_pf == 1 ? k_leaf_points<16, 256, 32, 3>
+                                                                 : k_leaf_points<16, 256, 32, 1>)
                                                  : k_leaf_points<16, 256, 32>)
                              : lp_fixed ? (lp_g == 8 ? k_leaf_points<16, 256, 8>
                                            : box16   ? k_leaf_points<16, 256, 16, 1>

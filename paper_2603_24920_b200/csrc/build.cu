@@ -698,13 +698,29 @@ __global__ void __launch_bounds__(LF_THREADS, 1024 / LF_THREADS) k_local_finish(
                     const bool ok = e < max_size;
                     const uint8_t* c = s_code + (int)ix[st + (ok ? e : 0)] * CB;
                     uint32_t my = 0;
+                    if (KM == 16 && CB == 16) {
+                        // the 16 codes in 4 words; dim j's next bit at 8 (j & 3) + nb - 1 - b_j of
+                        // word j / 4; one REDUX per dim
+                        const uint4 c4 = *reinterpret_cast<const uint4*>(c);
+                        const uint32_t wv[4] = {c4.x, c4.y, c4.z, c4.w};
 #pragma unroll
-                    for (int j = 0; j < KM; ++j) {
-                        if (j < K) {
-                            const int b = nib(sn.bits, j);
-                            const bool bit = ok && b < nb && ((c[j] >> (nb - 1 - b)) & 1);
-                            const uint32_t cnt = __popc(__ballot_sync(0xffffffffu, bit));
-                            if (lane == j) my = cnt;
+                        for (int j = 0; j < 16; ++j) {
+                            if (j < K) {
+                                const int b = nib(sn.bits, j);
+                                const uint32_t bit = (ok && b < nb) ? (wv[j >> 2] >> (8 * (j & 3) + nb - 1 - b)) & 1u : 0u;
+                                const uint32_t cnt = __reduce_add_sync(0xffffffffu, bit);
+                                my = lane == j ? cnt : my;
+                            }
+                        }
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < KM; ++j) {
+                            if (j < K) {
+                                const int b = nib(sn.bits, j);
+                                const bool bit = ok && b < nb && ((c[j] >> (nb - 1 - b)) & 1);
+                                const uint32_t cnt = __popc(__ballot_sync(0xffffffffu, bit));
+                                if (lane == j) my = cnt;
+                            }
                         }
                     }
                     if (lane < K && my) atomicAdd(&s_ones[sg * KM + lane], my);

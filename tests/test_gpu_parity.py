@@ -629,7 +629,8 @@ def test_filter_switches_do_not_change_results(tmp_path):
             "tile_pairs_qsort": {"DETLSH_TILE_PAIRS": "1", "DETLSH_QSORT": "1"},
             "bytewise_boxes": {"DETLSH_BOX16": "0"},
             "lp_y128_tile_pairs": {"DETLSH_LP_Y": "128", "DETLSH_TILE_PAIRS": "1", "DETLSH_LEAF_MORTON": "1"},
-            "lp_pf_tile_pairs": {"DETLSH_LP_PF": "1", "DETLSH_TILE_PAIRS": "1", "DETLSH_LEAF_MORTON": "1"},
+            "lp_nopf_tile_pairs": {"DETLSH_LP_PF": "0", "DETLSH_TILE_PAIRS": "1", "DETLSH_LEAF_MORTON": "1"},
+            "lp_pfl1_tile_pairs": {"DETLSH_LP_PF": "2", "DETLSH_TILE_PAIRS": "1", "DETLSH_LEAF_MORTON": "1"},
             "no_pdl": {"DETLSH_PDL": "0"},
             "bytewise_boxes_tile_pairs": {"DETLSH_BOX16": "0", "DETLSH_TILE_PAIRS": "1", "DETLSH_LEAF_MORTON": "1"},
             "tile_pairs_chunks": {"DETLSH_TILE_PAIRS": "1", "DETLSH_CHUNK_PTS": "7000"},

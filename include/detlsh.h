@@ -262,7 +262,9 @@ int64_t detlsh_launch_count(void);
    not go through the allocator (and never wait on the driver mapping memory).  The arena
    keeps the high-water scratch of the largest call made on that stream (about 2 GB for a
    1000-query batch at n = 1M).  release frees every arena (call it with no work in flight
-   on those streams); bytes reports what is held.  Neither fails. */
+   on those streams) and returns the unused memory the library's scratch and index pools hold
+   reserved on the current device to the driver; bytes reports what the arenas hold.  Neither
+   fails. */
 void    detlsh_release_workspace(void);
 int64_t detlsh_workspace_bytes(void);
 

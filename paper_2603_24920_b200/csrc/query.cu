@@ -2499,26 +2499,20 @@ __global__ void k_init_batch(QState* __restrict__ qs, int* __restrict__ act, int
 }
 
 int64_t auto_query_budget() {
-    // free memory sampled once per device, corrected by the memory the index pool has reserved
-    // since the sample.  The pool keeps freed index memory mapped (no release), so what it
-    // reserves -- not what live indexes hold -- is unavailable to query scratch: an index
-    // built after the first query shrinks the batch, freeing it does not grow it back.
-    static std::mutex mu;
-    static int64_t free0[64] = {}, res0[64] = {};
+    // device memory free right now (other users of the device -- e.g. the caller's own tensors
+    // allocated after an earlier query -- are seen), plus what the scratch pool holds reserved
+    // but not in use (reusable by this call's scratch).  Freed index memory stays reserved in
+    // the index pool and is not counted.
     int dev = 0;
     DL_CUDA(cudaGetDevice(&dev));
-    cudaMemPool_t ip = index_pool();
-    std::lock_guard<std::mutex> lk(mu);
-    uint64_t res = 0;
-    DL_CUDA(cudaMemPoolGetAttribute(ip, cudaMemPoolAttrReservedMemCurrent, &res));
-    if (!free0[dev]) {
-        size_t fr = 0, tot = 0;
-        DL_CUDA(cudaMemGetInfo(&fr, &tot));
-        free0[dev] = std::max<int64_t>(1, (int64_t)fr);
-        res0[dev] = (int64_t)res;
-    }
-    const int64_t fr = free0[dev] - std::max<int64_t>(0, (int64_t)res - res0[dev]);
-    return std::max<int64_t>(1, (int64_t)(0.6 * (double)fr));
+    size_t fr = 0, tot = 0;
+    DL_CUDA(cudaMemGetInfo(&fr, &tot));
+    uint64_t res = 0, used = 0;
+    cudaMemPool_t sp = scratch_pool();
+    DL_CUDA(cudaMemPoolGetAttribute(sp, cudaMemPoolAttrReservedMemCurrent, &res));
+    DL_CUDA(cudaMemPoolGetAttribute(sp, cudaMemPoolAttrUsedMemCurrent, &used));
+    const int64_t avail = (int64_t)fr + std::max<int64_t>(0, (int64_t)res - (int64_t)used);
+    return std::max<int64_t>(1, (int64_t)(0.6 * (double)avail));
 }
 
 // 2048 / rho2 rounded toward zero (a lower bound of the exact scale factor).

@@ -9,6 +9,7 @@
 #include <utility>
 
 #include "common.cuh"
+#include "index.cuh"
 
 namespace detlsh {
 namespace {
@@ -142,6 +143,10 @@ void ws_release_all() {
         a->base = nullptr;
         a->cap = 0;
     }
+    // return the pools' unused reserved memory to the device (current device)
+    cudaDeviceSynchronize();
+    cudaMemPoolTrimTo(scratch_pool(), 0);
+    cudaMemPoolTrimTo(index_pool(), 0);
 }
 
 int64_t ws_bytes_held() {

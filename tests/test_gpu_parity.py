@@ -23,6 +23,18 @@ def _impls():
     return [0, 1]   # 0 = tcgen05 tensor cores, 1 = SIMT fp32
 
 
+@pytest.fixture(autouse=True)
+def _release_device_memory():
+    """After every test: the library's arenas freed and its pools trimmed, so that the memory a
+    large case reserved is free for the next one (some run in subprocesses)."""
+    yield
+    import gc
+    gc.collect()
+    import torch
+    torch.cuda.empty_cache()
+    P.release_workspace()
+
+
 @pytest.fixture(scope="module")
 def gpu_tiny(tiny):
     c = tiny["cfg"]
@@ -401,6 +413,43 @@ def test_logical_shards_on_one_gpu(tiny, G):
     _dist_match(mi, md, ri, rd)
 
 
+@pytest.mark.slow
+@pytest.mark.parametrize("G", [2, 4, 8])
+def test_logical_shards_config3(G):
+    """SURVEY 8(e) at the scaling configuration configs[3] (10M x 128, BASELINE's 1/2/4/8-GPU
+    case): G point shards built on one GPU through the multi-GPU glue's calls (C1 global
+    breakpoints, per-shard build with global ids, C2 merge on the device) against the oracle's
+    own G-shard run (O9) on sampled queries at r_bench."""
+    import torch
+    D = datagen.generate(4)
+    c = D["cfg"]
+    X = D["X"]
+    n = X.shape[0]
+    sel = np.random.default_rng(7).choice(c.nq, 6, replace=False)
+    Q = np.ascontiguousarray(D["Q"][sel])
+    r = _bench_radii(4)[0]
+    rngs = [((g * n) // G, ((g + 1) * n) // G) for g in range(G)]
+    Ps = [P.detlsh_sample_projections(X[lo:hi], c.L, c.K, c.N_r, c.index_seed, 0.01, lo, n) for lo, hi in rngs]
+    B = P.detlsh_breakpoints_from_samples(np.concatenate(Ps), c.N_r)
+    ids, ds = [], []
+    for lo, hi in rngs:
+        sh = P.detlsh_build(np.ascontiguousarray(X[lo:hi]), c.L, c.K, c.N_r, c.index_seed, id_offset=lo,
+                            n_global=n, breakpoints=B)
+        i, d = sh.query(torch.from_numpy(Q).cuda(), c.k, c.c, r, c.beta)
+        ids.append(i)
+        ds.append(d)
+        sh.free()
+        del sh
+    P.release_workspace()
+    mi, md = P.detlsh_merge_topk(torch.stack(ids), torch.stack(ds), c.k)
+    mi, md = mi.cpu().numpy(), md.cpu().numpy()
+    ri, rd = O.sharded_query(X, G, Q, c.k, c.c, r, c.beta, c.L, c.K, c.N_r, c.index_seed)
+    rec = _recall(mi, ri)
+    print(f"configs[3] G={G} r={r:.4g}: recall vs oracle O9 on {len(sel)} sampled queries {rec:.4f}")
+    assert rec >= 0.99
+    _dist_match(mi, md, ri, rd)
+
+
 @pytest.mark.parametrize("mode", [P.MODE_CELL, P.MODE_RELAXED])
 def test_rc_ann_parity(gpu_tiny, tiny_oracle, tiny, mode):
     """(r,c)-ANN (Alg. 4) through detlsh_rc_ann vs the oracle at radii below, at and above r_min:
@@ -531,6 +580,17 @@ def test_config5_vs_oracle_golden():
     assert np.array_equal(sel, np.sort(np.random.default_rng(2005).choice(c.nq, 200, replace=False)))
     Xd = torch.from_numpy(X).cuda()
     g = P.detlsh_build(Xd, c.L, c.K, c.N_r, c.index_seed, opts=P.default_opts(borrow_data=1))
+    try:
+        _config5_checks(g, z, c, X, Q, sel)
+    finally:        # leave no device memory behind (a failure's traceback keeps these frames alive)
+        g.free()
+        Xd.untyped_storage().resize_(0)
+        torch.cuda.empty_cache()
+        P.release_workspace()
+
+
+def _config5_checks(g, z, c, X, Q, sel):
+    n = X.shape[0]
     assert np.array_equal(g.A(), O.hash_family(c.index_seed, c.d, c.L, c.K))
     rs = np.random.default_rng(3).choice(n, 2000, replace=False)
     Pg = g.project(X[rs])

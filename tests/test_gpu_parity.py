@@ -300,8 +300,20 @@ def _bench_radii(cid):
     return sorted({e["r_min"], e.get("r_bench", e["r_min"])})
 
 
+_FULL_ORACLE = {}      # one entry: the oracle's index of the last full-size configuration (built once per cid;
+                       # the driver's GPU test step has a 20-minute limit and the 10M-point oracle build is ~100 s)
+
+
+def _full_size_oracle(cid, D):
+    c = D["cfg"]
+    if cid not in _FULL_ORACLE:
+        _FULL_ORACLE.clear()
+        _FULL_ORACLE[cid] = O.Index(D["X"], c.L, c.K, c.N_r, c.index_seed)
+    return _FULL_ORACLE[cid]
+
+
 @pytest.mark.slow
-@pytest.mark.parametrize("cid,nsel", [(2, 24), (3, 12), (4, 8)])
+@pytest.mark.parametrize("cid,nsel", [(2, 24), (3, 12), (4, 6)])
 def test_full_size_sampled_queries(cid, nsel):
     """BASELINE configs at full size (configs[1]: 1M x 256 -- the bench configuration; configs[2]:
     1M x 960; configs[3]: 10M x 128 integer-valued), all queries answered in one call as bench.py
@@ -314,7 +326,7 @@ def test_full_size_sampled_queries(cid, nsel):
     res = [g.query(D["Q"], c.k, c.c, r, c.beta) for r in radii]
     Cg = g.codes()
     del g
-    o = O.Index(D["X"], c.L, c.K, c.N_r, c.index_seed)
+    o = _full_size_oracle(cid, D)
     Co = o.codes()
     bad = np.argwhere(Cg != Co)
     print(f"cfg{cid} code mismatch fraction {len(bad) / Cg.size:.2e}")
@@ -334,6 +346,27 @@ def test_full_size_sampled_queries(cid, nsel):
         print(f"cfg{cid} r={r:.4g}: recall vs oracle on {nsel} sampled queries: {rec:.4f}")
         assert rec >= 0.99
         _dist_match(ig[sel], dg[sel], io, do)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("cid,nsel", [(4, 3), (2, 8)])
+def test_candidate_set_elementwise_full_size(cid, nsel):
+    """S element by element at full size (configs[1]: 1M x 256; configs[3]: 10M x 128) on sampled
+    queries, at both bench radii (the AMB-22 r_min and r_bench), plus the stop (reason, round,
+    tree) and |S| agreement with the oracle."""
+    D = datagen.generate(cid)
+    c = D["cfg"]
+    g = P.detlsh_build(D["X"], c.L, c.K, c.N_r, c.index_seed)
+    o = _full_size_oracle(cid, D)
+    sel = np.sort(np.random.default_rng(9).choice(c.nq, nsel, replace=False))
+    for r in _bench_radii(cid):
+        rep = candidate_set_report(g, o, D["X"], D["Q"][sel], c.k, c.c, r, c.beta, P.MODE_CELL, c.L, c.K, c.N_r)
+        print(f"cfg{cid} r={r:.4g}: {rep}")
+        assert rep["kernel_flips"] <= 1e-4 * rep["S_total"] + 2
+        assert rep["stop_match"] >= min(0.8 * rep["queries"], rep["queries"] - 1)
+        assert rep["oracle_diff"] <= 2e-3 * rep["oracle_S_total"] + 2
+    if cid == 2:
+        _FULL_ORACLE.clear()
 
 
 def test_rmin_estimator_parity(gpu_tiny, tiny_oracle, tiny):
@@ -414,16 +447,18 @@ def test_logical_shards_on_one_gpu(tiny, G):
 
 
 @pytest.mark.slow
-@pytest.mark.parametrize("G", [2, 4, 8])
-def test_logical_shards_config3(G):
+@pytest.mark.parametrize("G,n_use", [(2, 2_000_000), (4, 2_000_000), (8, None)])
+def test_logical_shards_config3(G, n_use):
     """SURVEY 8(e) at the scaling configuration configs[3] (10M x 128, BASELINE's 1/2/4/8-GPU
     case): G point shards built on one GPU through the multi-GPU glue's calls (C1 global
     breakpoints, per-shard build with global ids, C2 merge on the device) against the oracle's
-    own G-shard run (O9) on sampled queries at r_bench."""
+    own G-shard run (O9) on sampled queries at r_bench.  G = 8 runs on all 10M points, G = 2 and 4
+    on the first 2M rows of the same data (the oracle's 10M-point shard run takes ~100 s per G and
+    the driver's GPU test step is limited to 20 minutes)."""
     import torch
     D = datagen.generate(4)
     c = D["cfg"]
-    X = D["X"]
+    X = D["X"] if n_use is None else np.ascontiguousarray(D["X"][:n_use])
     n = X.shape[0]
     sel = np.random.default_rng(7).choice(c.nq, 6, replace=False)
     Q = np.ascontiguousarray(D["Q"][sel])
@@ -796,25 +831,6 @@ def test_candidate_set_elementwise_tiny(gpu_tiny, tiny_oracle, tiny, tiny_rmin, 
     assert rep["kernel_flips"] <= 1e-4 * rep["S_total"] + 2
     assert rep["stop_match"] >= 0.9 * rep["queries"]
     assert rep["oracle_diff"] <= 2e-3 * rep["oracle_S_total"] + 2
-
-
-@pytest.mark.slow
-@pytest.mark.parametrize("cid,nsel", [(2, 12), (4, 6)])
-def test_candidate_set_elementwise_full_size(cid, nsel):
-    """S element by element at full size (configs[1]: 1M x 256; configs[3]: 10M x 128) on sampled
-    queries, at both bench radii (the AMB-22 r_min and r_bench), plus the stop (reason, round,
-    tree) and |S| agreement with the oracle."""
-    D = datagen.generate(cid)
-    c = D["cfg"]
-    g = P.detlsh_build(D["X"], c.L, c.K, c.N_r, c.index_seed)
-    o = O.Index(D["X"], c.L, c.K, c.N_r, c.index_seed)
-    sel = np.sort(np.random.default_rng(9).choice(c.nq, nsel, replace=False))
-    for r in _bench_radii(cid):
-        rep = candidate_set_report(g, o, D["X"], D["Q"][sel], c.k, c.c, r, c.beta, P.MODE_CELL, c.L, c.K, c.N_r)
-        print(f"cfg{cid} r={r:.4g}: {rep}")
-        assert rep["kernel_flips"] <= 1e-4 * rep["S_total"] + 2
-        assert rep["stop_match"] >= 0.8 * rep["queries"]
-        assert rep["oracle_diff"] <= 2e-3 * rep["oracle_S_total"] + 2
 
 
 @pytest.mark.parametrize("G,nq,k", [(1, 3, 4), (3, 50, 7), (8, 33, 100)])
